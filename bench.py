@@ -1,0 +1,398 @@
+#!/usr/bin/env python3
+"""bench.py — driver contract for the gbx-b200 hot path.
+
+Workload (BASELINE.json configs[1], the single-GPU config the metric is quoted
+on): a synthetic 1M-tuple experience log (44 fp32 features + fp64 Boltzmann
+target pair per record), default 44->64->32->2 policy MLP. One STEP = one
+epoch of `fit` (device Fisher-Yates replay + fused fp64-parity train-step
+kernel + SGD) over the whole log at global batch B. The secondary numbers
+(`inference`, `aggregation`) time the full-suite greedy inference over the
+same 1M states and a C5-style aggregation sweep.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--n N]
+  python bench.py --impl reference ...   # the reference's own CPU fit
+
+Multi-GPU (torchrun): weak scaling — every rank holds an N*1M-record log (the
+global permutation needs the whole log), the global batch is N*B, and each
+step's gradient is all-reduced once over NCCL inside libgbxcu.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "experience samples/sec trained; shader decisions/sec inferred, at 1/2/4/8 GPU"
+HBM_PEAK_FALLBACK = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1_000_000, help="records per GPU (weak scaling)")
+    ap.add_argument("--batch", type=int, default=4096, help="minibatch per GPU")
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--c5-apps", type=int, default=10_000)
+    ap.add_argument("--c5-shaders-per-app", type=int, default=1_000)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ inputs
+def synthetic_log(n: int, seed: int = 42):
+    """G1-shaped synthetic records: stage one-hot + 36 counter features in
+    [0, 7), target p ~ U[0.02, 0.98) -> (p, 1-p) (proj/tests/test_policy.cpp:15-28)."""
+    rng = np.random.default_rng(seed)
+    feat = np.zeros((n, 44), np.float32)
+    feat[np.arange(n), rng.integers(0, 8, n)] = 1.0
+    feat[:, 8:] = rng.random((n, 36), dtype=np.float32) * np.float32(7.0)
+    p = rng.uniform(0.02, 0.98, n)
+    tgt = np.stack([p, 1.0 - p], 1)
+    return feat, tgt
+
+
+def synthetic_suite(n_apps: int, per_app: int, seed: int = 5, cap: float = np.inf):
+    """C5-style suite: per_app distinct shaders per app, 2-4 pipelines,
+    exec_fraction U[0.03,0.09) scaled to a 0.85 cap per pipeline."""
+    rng = np.random.default_rng(seed)
+    n_sh = n_apps * per_app
+    lat = np.stack([rng.random(n_sh), rng.random(n_sh) * 1.6, rng.random(n_sh) * 0.6], 1)
+    pipes = rng.integers(2, 5, n_apps)
+    app_pipe_off = np.concatenate([[0], np.cumsum(pipes)]).astype(np.uint64)
+    sizes = []
+    for a in range(n_apps):
+        k = int(pipes[a])
+        base, extra = divmod(per_app, k)
+        sizes.extend([base + (1 if i < extra else 0) for i in range(k)])
+    pipe_slot_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint64)
+    frac = rng.uniform(0.03, 0.09, n_sh)
+    tot = np.add.reduceat(frac, pipe_slot_off[:-1].astype(np.int64))
+    scale = np.where(tot > 0.85, 0.85 / tot, 1.0)
+    frac = frac * np.repeat(scale, np.diff(pipe_slot_off).astype(np.int64))
+    npipe = len(sizes)
+    wt = np.stack([rng.uniform(0.5, 2.0, npipe), rng.uniform(2.0, 8.0, npipe) * 1e-3], 1)
+    app = np.stack([np.ones(n_apps), np.full(n_apps, cap), np.full(n_apps, 0.005),
+                    np.ones(n_apps)], 1)
+    s = dict(app_pipe_off=app_pipe_off, pipe_slot_off=pipe_slot_off,
+             slot_shader=np.arange(n_sh, dtype=np.uint32), slot_frac=frac, pipe_wt=wt,
+             shader_lat=lat, app_f64=app)
+    feat, _ = synthetic_log(n_sh, seed + 1)
+    return s, feat
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def pipe_peaks(device: int):
+    import ctypes as C
+
+    path = os.path.join(ROOT, "tools", "libpeaks.so")
+    if not os.path.exists(path):
+        return None, None
+    L = C.CDLL(path)
+    L.peak_fp64_tflops.restype = C.c_double
+    L.peak_fp32_tflops.restype = C.c_double
+    return L.peak_fp64_tflops(device), L.peak_fp32_tflops(device)
+
+
+# ------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+
+    if not oracle.ref_available():
+        kind, impl = "port", oracle.Restatement()
+    else:
+        kind, impl = "reference", oracle.Reference()
+    sample = min(args.n, 100_000)
+    feat, tgt = synthetic_log(sample)
+    p0 = impl.policy_init(7)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        rc = impl.fit(p0, feat, tgt, args.lr, 1, args.batch * world, 99)[0]
+        dt = time.perf_counter() - t0
+        assert rc == 0
+        if it >= args.warmup:
+            times.append(dt)
+    v = sample / statistics.mean(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 fit epoch (reference CPU, bounded sample)",
+                   "records": sample, "batch": args.batch * world, "lr": args.lr},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": kind,
+                         "sample": f"{sample} records, 1 epoch, batch {args.batch * world}; "
+                                   "fit is single-threaded by contract (SPEC.md:301)"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args):
+    import oracle
+
+    kind, impl = ("reference", oracle.Reference()) if oracle.ref_available() else (
+        "port", oracle.Restatement())
+    sample = min(args.n, 200_000)
+    feat, tgt = synthetic_log(sample)
+    t0 = time.perf_counter()
+    rc = impl.fit(impl.policy_init(7), feat, tgt, args.lr, 1, args.batch, 99)[0]
+    dt = time.perf_counter() - t0
+    assert rc == 0
+    return {"value": sample / dt, "unit": "samples/s", "cores": 1, "kind": kind,
+            "sample": f"fit of {sample} synthetic records, 1 epoch, batch {args.batch}, "
+                      f"{dt:.1f} s on 1 host core (fit is single-threaded, SPEC.md:301)"}
+
+
+# ----------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2111_12055_b200 as gbx
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = gbx.Device(local)
+    if world > 1:
+        uid = [gbx.Device.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        dev.comm_init(uid[0], world, rank)
+    stream = torch.cuda.ExternalStream(dev.stream)
+
+    n_total = args.n * world
+    batch = args.batch * world
+    feat_h, tgt_h = synthetic_log(n_total)
+    feat_h = np.ascontiguousarray(feat_h)
+    params0 = dev.policy_init(7)
+    feat_d = torch.from_numpy(feat_h).cuda()
+    tgt_d = torch.from_numpy(tgt_h).cuda()
+    params_d = torch.from_numpy(params0).cuda()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        dev.fit_dev(params_d.data_ptr(), feat_d.data_ptr(), tgt_d.data_ptr(), n_total, args.lr, 1,
+                    batch, 99, stream=dev.stream)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    l0 = dev.launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = dev.launches - l0
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = n_total * args.steps / (ms_max * 1e-3)
+
+    # ---- e2e: public host API, host buffers, H2D + D2H inside the region
+    pinned_feat = torch.from_numpy(feat_h).pin_memory().numpy()
+    pinned_tgt = torch.from_numpy(tgt_h).pin_memory().numpy()
+    dev.fit(params0, pinned_feat, pinned_tgt, args.lr, 1, batch, 99)  # warm
+    barrier()
+    e2e_times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        dev.fit(params0, pinned_feat, pinned_tgt, args.lr, 1, batch, 99)
+        e2e_times.append(time.perf_counter() - t0)
+    tt = torch.tensor([statistics.mean(e2e_times)], device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e = {"value": n_total / float(tt.item()), "unit": "samples/s",
+           "h2d_bytes_per_step": int(feat_h.nbytes + tgt_h.nbytes + 4 * 5026),
+           "d2h_bytes_per_step": int(4 * 5026 + 8)}
+
+    # ---- roofline of the dominant kernel (train_epoch_kernel)
+    peaks = measured_peaks()
+    fp64_peak, fp32_peak = (None, None)
+    secondary = {}
+    if rank == 0:
+        fp64_peak, fp32_peak = pipe_peaks(local)
+    # the train kernel's share: time one epoch split by kernel with events
+    flop_per_record = 23936
+    train_tflops = n_total * flop_per_record / (ms_step * 1e-3) / 1e12 / world
+    hbm_bytes = n_total * 196 / world
+    roofline = {
+        "bound": "fp64",
+        "achieved": train_tflops,
+        "peak": fp64_peak,
+        "unit": "TFLOP/s",
+        "frac": (train_tflops / fp64_peak) if fp64_peak else None,
+        "traffic": None,
+        "kernel": "train_epoch_kernel (fp64 parity mode, whole-step time)",
+        "work_per_unit": "23,936 FLOP/record (fwd 9,856 + bwd 14,080), 196 B/record",
+        "peak_source": "measured DFMA throughput, tools/peaks.cu (MEASURED_PEAKS.json has no fp64)",
+        "hbm_view": {"achieved_gbs": hbm_bytes / (ms_step * 1e-3) / 1e9,
+                     "peak_gbs": peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)},
+    }
+
+    if rank == 0 and not args.no_secondary:
+        secondary = run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak,
+                                  peaks, local)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "C2: 1M-tuple experience log per GPU, default MLP 44-64-32-2, "
+                               "1 fit epoch per step (fp64 parity mode)",
+                   "records": n_total, "global_batch": batch, "lr": args.lr,
+                   "parallelism": f"dp{world}", "l2": "inputs (196 MB/GPU) larger than L2"},
+        "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
+    }
+    line.update(secondary)
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, peaks, local):
+    """Full-suite greedy inference over the 1M states + a C5-style aggregation sweep."""
+    out = {}
+    n = args.n
+    act_d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    for mode, name in ((gbx.FWD_FAST, "fast"), (gbx.FWD_EXACT, "exact")):
+        for _ in range(3):
+            dev.forward_dev(params_d.data_ptr(), feat_d.data_ptr(), n, None, act_d.data_ptr(),
+                            mode, dev.stream)
+        torch.cuda.synchronize()
+        reps = 10
+        ev0.record(stream)
+        for _ in range(reps):
+            dev.forward_dev(params_d.data_ptr(), feat_d.data_ptr(), n, None, act_d.data_ptr(),
+                            mode, dev.stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / reps
+        rate = n / (ms * 1e-3)
+        out.setdefault("inference", {})[name] = {
+            "value": rate, "unit": "decisions/s", "ms": ms, "states": n,
+            "fp32_tflops": rate * 9856 / 1e12,
+            "hbm_gbs": rate * 177 / 1e9}
+    out["inference"]["fp32_peak_tflops_measured"] = fp32_peak
+    out["inference"]["hbm_peak_gbs"] = peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)
+
+    # C5-style sweep: inference + aggregation over n_apps x per_app shaders
+    s, feat = synthetic_suite(args.c5_apps, args.c5_shaders_per_app)
+    ds = dev.suite_upload(s, feat)
+    params = params_d.cpu().numpy()
+    pd = torch.from_numpy(params).cuda()
+    nsh = feat.shape[0]
+    a_d = torch.empty(nsh, dtype=torch.uint8, device="cuda")
+    rows_d = torch.empty((args.c5_apps, 5), dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        ds.evaluate_dev(pd.data_ptr(), 10, 77, a_d.data_ptr(), rows_d.data_ptr(), dev.stream)
+    torch.cuda.synchronize()
+    reps = 5
+    ev0.record(stream)
+    for _ in range(reps):
+        ds.evaluate_dev(pd.data_ptr(), 10, 77, a_d.data_ptr(), rows_d.data_ptr(), dev.stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / reps
+    out["aggregation"] = {"value": nsh / (ms * 1e-3), "unit": "shader decisions/s (infer+agg)",
+                          "ms": ms, "apps": args.c5_apps, "shaders": nsh,
+                          "bytes_per_shader": 204}
+    ds.close()
+    return out
+
+
+if __name__ == "__main__":
+    main()

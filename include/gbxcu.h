@@ -1,0 +1,204 @@
+/*
+ * gbxcu.h — C ABI of the B200 (sm_100a) implementation of the gbxtune hot path.
+ *
+ * The reference (arXiv 2111.12055 analog, /root/reference/proj) exposes the
+ * path only as C++ functions of the static library `gbx`; it has no FFI or
+ * plugin registry. Each entry point below replaces one of those functions
+ * (cited per declaration) with a batched, device-executed equivalent. The C++
+ * drop-in mirror (paper_2111_12055_b200/include/gbx/*.hpp) and the Python
+ * binding (paper_2111_12055_b200/__init__.py, ctypes) both bind exactly this
+ * surface; INTEGRATION.md shows the binding a maintainer adds.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no C++ or torch types cross the ABI.
+ *   - Functions without a `_dev` suffix take caller-owned HOST buffers and are
+ *     synchronous. `_dev` variants take DEVICE pointers plus a cudaStream_t
+ *     (passed as void*, NULL = the context's stream) and are asynchronous
+ *     unless noted.
+ *   - Parameters are the 5,026 fp32 values of the 44->64->32->2 policy in the
+ *     reference's flat serialization order (proj/src/policy.cpp:152-182):
+ *     w0[64][44] b0[64] w1[32][64] b1[32] w2[2][32] b2[2].
+ *   - Features: [n][44] fp32 rows (176 B). Targets: [n][2] fp64.
+ *   - Actions: uint8, 0 = Wave32, 1 = Wave64 (proj/include/gbx/core.hpp:19).
+ *   - Every call returns a gbxcu_status. On failure gbxcu_last_error() holds
+ *     a message. There is no CPU fallback: without a usable sm_100 device every
+ *     compute entry point fails with GBXCU_ECUDA.
+ */
+#ifndef GBXCU_H
+#define GBXCU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GBXCU_ABI_VERSION 1
+
+#define GBXCU_N_FEATURES 44
+#define GBXCU_N_PARAMS 5026
+
+typedef enum {
+    GBXCU_OK = 0,
+    GBXCU_EINVAL = 1,      /* ValidationError (bad config, empty dataset, ...) */
+    GBXCU_EDIVERGED = 2,   /* TrainingDivergedError; epoch reported separately */
+    GBXCU_ECUDA = 3,       /* CUDA runtime / launch failure, or no device */
+    GBXCU_ENCCL = 4,       /* NCCL failure in the data-parallel path */
+    GBXCU_ENONFINITE = 5,  /* ValidationError: non-finite feature in forward */
+    GBXCU_ETEMPERATURE = 6 /* InvalidTemperatureError (rho <= 0) */
+} gbxcu_status;
+
+/* Inference precision.
+ *   EXACT: fp64 forward in the reference's summation order (bias first,
+ *          ascending index, no FMA contraction where products round); probs
+ *          match PolicyNet::forward to the last ulp of exp().
+ *   FAST : fp32 forward + a rigorous per-state error bound; every state whose
+ *          logit margin is inside the bound is re-run in EXACT mode, so the
+ *          ACTIONS are identical to EXACT; probabilities are fp32-accurate
+ *          (relative error <= 1e-5). */
+typedef enum { GBXCU_FWD_EXACT = 0, GBXCU_FWD_FAST = 1 } gbxcu_fwd_mode;
+
+typedef struct gbxcu_ctx gbxcu_ctx;
+
+/* ----------------------------------------------------------------- context */
+int gbxcu_abi_version(void);
+const char* gbxcu_last_error(void); /* thread-local message of the last failure */
+int gbxcu_create(int device, gbxcu_ctx** out);
+void gbxcu_destroy(gbxcu_ctx* ctx);
+/* cudaStream_t the context enqueues on when a _dev call passes NULL. */
+void* gbxcu_stream(gbxcu_ctx* ctx);
+/* Number of kernels this context launched since creation (for bench.py's
+ * gpu_launches claim; counts our kernels only, not memcpys or NCCL). */
+uint64_t gbxcu_launch_count(const gbxcu_ctx* ctx);
+
+/* ------------------------------------------------------------------- init */
+/* PolicyNet::init (proj/src/policy.cpp:128-139) computed on the device:
+ * fan-scaled uniform weights from derive_seed({seed,0x1A17,l}), zero biases. */
+int gbxcu_policy_init(gbxcu_ctx* ctx, uint64_t seed, float* params_out);
+
+/* -------------------------------------------------------------- inference */
+/* PolicyNet::forward + select_greedy, batched (proj/src/policy.cpp:141-148,
+ * 339-342). probs [n][2] and actions [n] are each nullable. Non-finite
+ * features -> GBXCU_ENONFINITE (the whole call fails, like the first throwing
+ * forward() in a reference loop). */
+int gbxcu_forward(gbxcu_ctx* ctx, const float* params, const float* feat, size_t n,
+                  double* probs, uint8_t* actions, int mode);
+int gbxcu_forward_dev(gbxcu_ctx* ctx, const float* d_params, const float* d_feat, size_t n,
+                      double* d_probs, uint8_t* d_actions, int mode, void* stream);
+
+/* Sampled (collection) decisions, proj/src/tuner.cpp:183-196 with
+ * select_sample semantics (proj/src/policy.cpp:344-347): states are grouped
+ * in segments (one per benchmark, seg_off[nseg+1]); segment b draws from
+ * SplitMix64(seg_seed[b]) two uniforms per state (u_explore, u_action) in
+ * state order; u_explore < eps -> Wave32 iff u_action < 0.5, else Wave32 iff
+ * u_action < p0. Decisions are exact (fp64 re-check inside the margin). */
+int gbxcu_collect(gbxcu_ctx* ctx, const float* params, const float* feat,
+                  const uint64_t* seg_off, size_t nseg, const uint64_t* seg_seed, double eps,
+                  uint8_t* actions);
+int gbxcu_collect_dev(gbxcu_ctx* ctx, const float* d_params, const float* d_feat,
+                      const uint64_t* d_seg_off, size_t nseg, const uint64_t* d_seg_seed,
+                      size_t n_states, double eps, uint8_t* d_actions, void* stream);
+
+/* ------------------------------------------------------- loss / gradient */
+/* batch_kl_loss (proj/src/policy.cpp:194-201). */
+int gbxcu_batch_kl_loss(gbxcu_ctx* ctx, const float* params, const float* feat,
+                        const double* tgt, size_t n, double* loss_out);
+/* batch_kl_gradient (proj/src/policy.cpp:270-279): grad_out[5026] fp64, flat
+ * order; record contributions summed in batch order (bit-exact up to log()). */
+int gbxcu_batch_kl_gradient(gbxcu_ctx* ctx, const float* params, const float* feat,
+                            const double* tgt, size_t n, double* grad_out);
+
+/* -------------------------------------------------------------------- fit */
+typedef struct {
+    double learning_rate; /* TrainConfig::learning_rate (> 0) */
+    int epochs;           /* >= 1 */
+    int batch_size;       /* >= 1; global batch across all ranks */
+    uint64_t seed;        /* TrainConfig::seed (epoch shuffle stream) */
+    int max_ctas;         /* 0 = auto (1 CTA per 64 records of the per-rank batch, <= #SMs) */
+    int reserved;
+} gbxcu_train_cfg;
+
+/* fit (proj/src/policy.cpp:297-337): seeded in-place Fisher-Yates per epoch
+ * (reproduced on the device), minibatch KL loss, analytic gradient, SGD
+ * w = float(double(w) - lr*g). params_inout is updated in place; on
+ * GBXCU_EDIVERGED it holds the last successful update and *diverged_epoch is
+ * set (TrainingDivergedError semantics). epoch_loss_out[epochs] nullable.
+ * With a communicator attached (gbxcu_comm_init) every global batch is split
+ * into equal contiguous slices per rank and the flat fp64 gradient (+ loss)
+ * is all-reduced once per step; all ranks must pass identical arguments. */
+int gbxcu_fit(gbxcu_ctx* ctx, float* params_inout, const float* feat, const double* tgt, size_t n,
+              const gbxcu_train_cfg* cfg, double* epoch_loss_out, int* diverged_epoch);
+/* Device-resident form: d_params updated in place on the device; the epoch
+ * losses are copied to the host buffer at the end (synchronous). */
+int gbxcu_fit_dev(gbxcu_ctx* ctx, float* d_params, const float* d_feat, const double* d_tgt,
+                  size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out,
+                  int* diverged_epoch, void* stream);
+
+/* Permutation `order` after `epochs` Fisher-Yates passes of fit (device
+ * deterministic-reservations replay of proj/src/policy.cpp:303-314). */
+int gbxcu_fit_order(gbxcu_ctx* ctx, size_t n, uint64_t seed, int epochs, uint32_t* order_out);
+
+/* -------------------------------------------------- data-parallel plumbing */
+#define GBXCU_COMM_ID_BYTES 128
+int gbxcu_comm_unique_id(uint8_t id_out[GBXCU_COMM_ID_BYTES]);
+int gbxcu_comm_init(gbxcu_ctx* ctx, const uint8_t id[GBXCU_COMM_ID_BYTES], int nranks, int rank);
+int gbxcu_comm_destroy(gbxcu_ctx* ctx);
+
+/* ------------------------------------------------------------ aggregation */
+/* Application suite in CSR form (the per-benchmark data SimSuite::frame_time
+ * reads, proj/src/simenv.cpp:439-474; proj/include/gbx/simenv.hpp:55-100).
+ * App (benchmark) ids are their indices. */
+typedef struct {
+    size_t n_apps, n_pipes, n_slots, n_shaders;
+    const uint64_t* app_pipe_off;  /* [n_apps+1]  pipelines of app a          */
+    const uint64_t* pipe_slot_off; /* [n_pipes+1] slots of pipeline p          */
+    const uint32_t* slot_shader;   /* [n_slots]   shader id                    */
+    const double* slot_frac;       /* [n_slots]   exec_fraction                */
+    const double* pipe_wt;         /* [n_pipes][2] weight, base_time (s)       */
+    const double* shader_lat;      /* [n_shaders][3] divergence, bandwidth_demand, parallelism */
+    const double* app_f64;         /* [n_apps][4] baseline_fps, bandwidth_capacity (+inf =
+                                       unconstrained), noise_sigma, memory_bound_threshold */
+} gbxcu_suite;
+
+/* Per-app frame time + noisy samples + reward/uplift for a per-shader action
+ * vector: run_benchmark (proj/src/simenv.cpp:481-510), attribute_rewards /
+ * reward_from_framerate (proj/src/tuner.cpp:131-147, core.cpp:125-133) and
+ * evaluate's uplift (proj/src/tuner.cpp:282-289). run_seed[a] is the seed the
+ * caller hands run_benchmark for app a. rows_out [n_apps][5] =
+ * frame_time, true_fps, mean sample fps, uplift_pct, reward. samples_out
+ * [n_apps][n_samples] nullable. Bit-exact vs the reference. */
+int gbxcu_aggregate(gbxcu_ctx* ctx, const gbxcu_suite* suite, const uint8_t* shader_actions,
+                    const uint64_t* run_seed, int n_samples, double* rows_out,
+                    double* samples_out);
+
+/* evaluate's 1%-bin histogram (proj/src/tuner.cpp:293-313). Writes up to
+ * cap bins; *n_bins = the true bin count. */
+int gbxcu_histogram(gbxcu_ctx* ctx, const double* uplift, size_t n, double* lower_out,
+                    uint64_t* count_out, size_t cap, size_t* n_bins);
+
+/* Device-resident suite handle (uploaded once, reused per sweep). */
+typedef struct gbxcu_dsuite gbxcu_dsuite;
+int gbxcu_suite_upload(gbxcu_ctx* ctx, const gbxcu_suite* host, const float* shader_features,
+                       gbxcu_dsuite** out);
+void gbxcu_suite_free(gbxcu_dsuite* s);
+/* Raw device pointers of an uploaded suite (features [n_shaders][44] fp32). */
+const float* gbxcu_suite_features(const gbxcu_dsuite* s);
+
+/* Greedy evaluation sweep = evaluate() (proj/src/tuner.cpp:266-315):
+ * inference over every shader, per-app aggregation with
+ * run_seed = derive_seed({seed, 0x45564C, app}), uplift rows + histogram.
+ * Host outputs: rows_out [n_apps][5] (as gbxcu_aggregate), histogram as
+ * gbxcu_histogram (nullable). shader_actions_out [n_shaders] nullable. */
+int gbxcu_evaluate(gbxcu_ctx* ctx, const gbxcu_dsuite* s, const float* params, int n_samples,
+                   uint64_t seed, double* rows_out, uint8_t* shader_actions_out,
+                   double* hist_lower, uint64_t* hist_count, size_t hist_cap, size_t* n_bins);
+/* Device form: params, actions and rows are device buffers; no host sync. */
+int gbxcu_evaluate_dev(gbxcu_ctx* ctx, const gbxcu_dsuite* s, const float* d_params,
+                       int n_samples, uint64_t seed, uint8_t* d_actions, double* d_rows,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GBXCU_H */

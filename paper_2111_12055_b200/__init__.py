@@ -1,0 +1,380 @@
+"""gbx-b200: B200-native (sm_100a) implementation of the gbxtune hot path.
+
+Python binding of the C ABI in ``include/gbxcu.h`` (ctypes). The compute
+lives in ``libgbxcu.so`` (CUDA kernels for sm_100a, built in-tree by
+``build()``); this module only marshals buffers and maps status codes to the
+reference's exception types (proj/include/gbx/core.hpp:14-16,
+policy.hpp:16-31, qtable.hpp:15-25). There is no CPU fallback: if the library
+or a B200 is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgbxcu.so")
+N_PARAMS = 5026
+N_FEATURES = 44
+DIMS = (44, 64, 32, 2)
+WAVE32, WAVE64 = 0, 1
+FWD_EXACT, FWD_FAST = 0, 1
+
+OK, EINVAL, EDIVERGED, ECUDA, ENCCL, ENONFINITE, ETEMPERATURE = range(7)
+
+
+# ----------------------------------------------------------------- errors
+class ValidationError(ValueError):
+    """gbx::ValidationError (proj/include/gbx/core.hpp:14-16)."""
+
+
+class TrainingDivergedError(RuntimeError):
+    """gbx::TrainingDivergedError{epoch} (proj/include/gbx/policy.hpp:25-30)."""
+
+    def __init__(self, epoch: int, what: str):
+        super().__init__(what)
+        self.epoch = epoch
+
+
+class InvalidTemperatureError(ValueError):
+    """gbx::InvalidTemperatureError (proj/include/gbx/qtable.hpp:23-25)."""
+
+
+class CudaError(RuntimeError):
+    """CUDA / device failure (no reference analogue: the reference is CPU-only)."""
+
+
+class NcclError(RuntimeError):
+    pass
+
+
+def build(force: bool = False) -> str:
+    """Compile libgbxcu.so for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-C", os.path.join(HERE, "csrc")], check=True)
+    return LIB_PATH
+
+
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_vp = C.c_void_p
+_sz = C.c_size_t
+_u64 = C.c_uint64
+
+
+class TrainCfg(C.Structure):
+    _fields_ = [("learning_rate", C.c_double), ("epochs", C.c_int), ("batch_size", C.c_int),
+                ("seed", C.c_uint64), ("max_ctas", C.c_int), ("reserved", C.c_int)]
+
+
+class SuiteC(C.Structure):
+    _fields_ = [("n_apps", _sz), ("n_pipes", _sz), ("n_slots", _sz), ("n_shaders", _sz),
+                ("app_pipe_off", _vp), ("pipe_slot_off", _vp), ("slot_shader", _vp),
+                ("slot_frac", _vp), ("pipe_wt", _vp), ("shader_lat", _vp), ("app_f64", _vp)]
+
+
+# Every symbol include/gbxcu.h declares (tests check the library exports them).
+EXPORTS = (
+    "gbxcu_abi_version", "gbxcu_last_error", "gbxcu_create", "gbxcu_destroy", "gbxcu_stream",
+    "gbxcu_launch_count", "gbxcu_policy_init", "gbxcu_forward", "gbxcu_forward_dev",
+    "gbxcu_collect", "gbxcu_collect_dev", "gbxcu_batch_kl_loss", "gbxcu_batch_kl_gradient",
+    "gbxcu_fit", "gbxcu_fit_dev", "gbxcu_fit_order", "gbxcu_comm_unique_id", "gbxcu_comm_init",
+    "gbxcu_comm_destroy", "gbxcu_aggregate", "gbxcu_histogram", "gbxcu_suite_upload",
+    "gbxcu_suite_free", "gbxcu_suite_features", "gbxcu_evaluate", "gbxcu_evaluate_dev",
+)
+
+_LIB = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Load libgbxcu.so (raises if absent — there is no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise CudaError(f"{path} is missing: run paper_2111_12055_b200.build() (no CPU fallback)")
+    L = C.CDLL(path)
+    L.gbxcu_abi_version.restype = C.c_int
+    L.gbxcu_last_error.restype = C.c_char_p
+    L.gbxcu_create.argtypes = [C.c_int, C.POINTER(_vp)]
+    L.gbxcu_destroy.argtypes = [_vp]
+    L.gbxcu_destroy.restype = None
+    L.gbxcu_stream.argtypes = [_vp]
+    L.gbxcu_stream.restype = _vp
+    L.gbxcu_launch_count.argtypes = [_vp]
+    L.gbxcu_launch_count.restype = _u64
+    L.gbxcu_policy_init.argtypes = [_vp, _u64, _f32p]
+    L.gbxcu_forward.argtypes = [_vp, _f32p, _f32p, _sz, _vp, _vp, C.c_int]
+    L.gbxcu_forward_dev.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp, C.c_int, _vp]
+    L.gbxcu_collect.argtypes = [_vp, _f32p, _f32p, _u64p, _sz, _u64p, C.c_double, _u8p]
+    L.gbxcu_collect_dev.argtypes = [_vp, _vp, _vp, _vp, _sz, _vp, _sz, C.c_double, _vp, _vp]
+    L.gbxcu_batch_kl_loss.argtypes = [_vp, _f32p, _f32p, _f64p, _sz, C.POINTER(C.c_double)]
+    L.gbxcu_batch_kl_gradient.argtypes = [_vp, _f32p, _f32p, _f64p, _sz, _f64p]
+    L.gbxcu_fit.argtypes = [_vp, _f32p, _f32p, _f64p, _sz, C.POINTER(TrainCfg), _vp,
+                            C.POINTER(C.c_int)]
+    L.gbxcu_fit_dev.argtypes = [_vp, _vp, _vp, _vp, _sz, C.POINTER(TrainCfg), _vp,
+                                C.POINTER(C.c_int), _vp]
+    L.gbxcu_fit_order.argtypes = [_vp, _sz, _u64, C.c_int, _u32p]
+    L.gbxcu_comm_unique_id.argtypes = [C.c_char_p]
+    L.gbxcu_comm_init.argtypes = [_vp, C.c_char_p, C.c_int, C.c_int]
+    L.gbxcu_comm_destroy.argtypes = [_vp]
+    L.gbxcu_aggregate.argtypes = [_vp, C.POINTER(SuiteC), _u8p, _u64p, C.c_int, _f64p, _vp]
+    L.gbxcu_histogram.argtypes = [_vp, _f64p, _sz, _f64p, _u64p, _sz, C.POINTER(_sz)]
+    L.gbxcu_suite_upload.argtypes = [_vp, C.POINTER(SuiteC), _f32p, C.POINTER(_vp)]
+    L.gbxcu_suite_free.argtypes = [_vp]
+    L.gbxcu_suite_free.restype = None
+    L.gbxcu_suite_features.argtypes = [_vp]
+    L.gbxcu_suite_features.restype = _vp
+    L.gbxcu_evaluate.argtypes = [_vp, _vp, _f32p, C.c_int, _u64, _f64p, _vp, _vp, _vp, _sz,
+                                 C.POINTER(_sz)]
+    L.gbxcu_evaluate_dev.argtypes = [_vp, _vp, _vp, C.c_int, _u64, _vp, _vp, _vp]
+    _LIB = L
+    return L
+
+
+def _raise(L, rc: int, diverged_epoch: int = -1):
+    msg = (L.gbxcu_last_error() or b"").decode()
+    if rc == EINVAL:
+        raise ValidationError(msg)
+    if rc == ENONFINITE:
+        raise ValidationError(msg)
+    if rc == EDIVERGED:
+        raise TrainingDivergedError(diverged_epoch, msg)
+    if rc == ETEMPERATURE:
+        raise InvalidTemperatureError(msg)
+    if rc == ENCCL:
+        raise NcclError(msg)
+    raise CudaError(msg)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def suite_struct(s: dict) -> tuple[SuiteC, list]:
+    """Build the C view of a CSR suite dict (keys as in oracle export); returns (struct, keepalive)."""
+    keep = [np.ascontiguousarray(s["app_pipe_off"], np.uint64),
+            np.ascontiguousarray(s["pipe_slot_off"], np.uint64),
+            np.ascontiguousarray(s["slot_shader"], np.uint32),
+            np.ascontiguousarray(s["slot_frac"], np.float64),
+            np.ascontiguousarray(s["pipe_wt"], np.float64),
+            np.ascontiguousarray(s["shader_lat"], np.float64),
+            np.ascontiguousarray(s["app_f64"], np.float64)]
+    st = SuiteC(len(keep[0]) - 1, len(keep[1]) - 1, len(keep[2]), keep[5].shape[0],
+                *(k.ctypes.data for k in keep))
+    return st, keep
+
+
+class Device:
+    """One gbxcu context (device buffers + stream) on one B200."""
+
+    def __init__(self, device: int = 0):
+        self.L = load_library()
+        h = _vp()
+        rc = self.L.gbxcu_create(device, C.byref(h))
+        if rc:
+            _raise(self.L, rc)
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.gbxcu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, rc, diverged_epoch=-1):
+        if rc:
+            _raise(self.L, rc, diverged_epoch)
+
+    @property
+    def stream(self) -> int:
+        return int(self.L.gbxcu_stream(self.h) or 0)
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.gbxcu_launch_count(self.h))
+
+    # ------------------------------------------------------------ policy
+    def policy_init(self, seed: int) -> np.ndarray:
+        p = np.empty(N_PARAMS, np.float32)
+        self._ck(self.L.gbxcu_policy_init(self.h, seed, p))
+        return p
+
+    def forward(self, params, feat, mode=FWD_EXACT, want_probs=True, want_actions=True):
+        feat = _f32(feat).reshape(-1, N_FEATURES)
+        n = feat.shape[0]
+        probs = np.empty((n, 2), np.float64) if want_probs else None
+        act = np.empty(n, np.uint8) if want_actions else None
+        self._ck(self.L.gbxcu_forward(self.h, _f32(params), feat, n,
+                                      None if probs is None else probs.ctypes.data,
+                                      None if act is None else act.ctypes.data, mode))
+        return probs, act
+
+    def select_greedy(self, params, feat, mode=FWD_FAST):
+        return self.forward(params, feat, mode, want_probs=False)[1]
+
+    def collect(self, params, feat, seg_off, seg_seed, eps):
+        feat = _f32(feat).reshape(-1, N_FEATURES)
+        seg_off = np.ascontiguousarray(seg_off, np.uint64)
+        act = np.empty(feat.shape[0], np.uint8)
+        self._ck(self.L.gbxcu_collect(self.h, _f32(params), feat, seg_off, len(seg_off) - 1,
+                                      np.ascontiguousarray(seg_seed, np.uint64), eps, act))
+        return act
+
+    def batch_kl_loss(self, params, feat, tgt) -> float:
+        out = C.c_double()
+        feat = _f32(feat).reshape(-1, N_FEATURES)
+        self._ck(self.L.gbxcu_batch_kl_loss(self.h, _f32(params), feat, _f64(tgt), feat.shape[0],
+                                            C.byref(out)))
+        return out.value
+
+    def batch_kl_gradient(self, params, feat, tgt) -> np.ndarray:
+        g = np.empty(N_PARAMS, np.float64)
+        feat = _f32(feat).reshape(-1, N_FEATURES)
+        self._ck(self.L.gbxcu_batch_kl_gradient(self.h, _f32(params), feat, _f64(tgt),
+                                                feat.shape[0], g))
+        return g
+
+    def fit(self, params, feat, tgt, lr=0.01, epochs=50, batch=32, seed=0, max_ctas=0,
+            raise_on_diverge=True):
+        """fit(): returns (params, epoch_loss). Raises TrainingDivergedError like the reference
+        (the partially trained params are attached as .params)."""
+        p = np.array(params, np.float32, copy=True)
+        feat = _f32(feat).reshape(-1, N_FEATURES)
+        el = np.full(max(epochs, 1), np.nan, np.float64)
+        de = C.c_int(-1)
+        cfg = TrainCfg(lr, epochs, batch, seed, max_ctas, 0)
+        rc = self.L.gbxcu_fit(self.h, p, feat, _f64(tgt), feat.shape[0], C.byref(cfg),
+                              el.ctypes.data, C.byref(de))
+        if rc == EDIVERGED and not raise_on_diverge:
+            return p, el, de.value
+        if rc:
+            try:
+                _raise(self.L, rc, de.value)
+            except TrainingDivergedError as e:
+                e.params = p
+                raise
+        return (p, el, -1) if not raise_on_diverge else (p, el)
+
+    def fit_order(self, n: int, seed: int, epochs: int) -> np.ndarray:
+        o = np.empty(n, np.uint32)
+        self._ck(self.L.gbxcu_fit_order(self.h, n, seed, epochs, o))
+        return o
+
+    # ------------------------------------------------- device-resident forms
+    def forward_dev(self, d_params: int, d_feat: int, n: int, d_probs: int | None,
+                    d_actions: int | None, mode=FWD_FAST, stream: int | None = None):
+        self._ck(self.L.gbxcu_forward_dev(self.h, d_params, d_feat, n, d_probs, d_actions, mode,
+                                          stream))
+
+    def fit_dev(self, d_params: int, d_feat: int, d_tgt: int, n: int, lr=0.01, epochs=1,
+                batch=32, seed=0, max_ctas=0, stream: int | None = None):
+        el = np.full(max(epochs, 1), np.nan, np.float64)
+        de = C.c_int(-1)
+        cfg = TrainCfg(lr, epochs, batch, seed, max_ctas, 0)
+        rc = self.L.gbxcu_fit_dev(self.h, d_params, d_feat, d_tgt, n, C.byref(cfg),
+                                  el.ctypes.data, C.byref(de), stream)
+        self._ck(rc, de.value)
+        return el
+
+    # ----------------------------------------------------------- data parallel
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        L = load_library()
+        buf = C.create_string_buffer(128)
+        rc = L.gbxcu_comm_unique_id(buf)
+        if rc:
+            _raise(L, rc)
+        return buf.raw
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int):
+        self._ck(self.L.gbxcu_comm_init(self.h, uid, nranks, rank))
+
+    def comm_destroy(self):
+        self._ck(self.L.gbxcu_comm_destroy(self.h))
+
+    # ------------------------------------------------------------ aggregation
+    def aggregate(self, suite: dict, shader_actions, run_seed, n_samples, want_samples=False):
+        st, keep = suite_struct(suite)
+        rows = np.empty((st.n_apps, 5), np.float64)
+        samples = np.empty((st.n_apps, n_samples), np.float64) if want_samples else None
+        self._ck(self.L.gbxcu_aggregate(self.h, C.byref(st),
+                                        np.ascontiguousarray(shader_actions, np.uint8),
+                                        np.ascontiguousarray(run_seed, np.uint64), n_samples, rows,
+                                        None if samples is None else samples.ctypes.data))
+        return (rows, samples) if want_samples else rows
+
+    def histogram(self, uplift):
+        u = _f64(uplift)
+        cap = 1 << 16
+        lo = np.empty(cap, np.float64)
+        cnt = np.empty(cap, np.uint64)
+        nb = _sz()
+        self._ck(self.L.gbxcu_histogram(self.h, u, len(u), lo, cnt, cap, C.byref(nb)))
+        return lo[:nb.value].copy(), cnt[:nb.value].copy()
+
+    def suite_upload(self, suite: dict, features) -> "DeviceSuite":
+        return DeviceSuite(self, suite, features)
+
+
+class DeviceSuite:
+    """A suite resident in HBM (gbxcu_suite_upload)."""
+
+    def __init__(self, dev: Device, suite: dict, features):
+        self.dev = dev
+        st, keep = suite_struct(suite)
+        self.n_apps, self.n_shaders = st.n_apps, st.n_shaders
+        h = _vp()
+        dev._ck(dev.L.gbxcu_suite_upload(dev.h, C.byref(st), _f32(features), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.dev.L.gbxcu_suite_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def features_ptr(self) -> int:
+        return int(self.dev.L.gbxcu_suite_features(self.h))
+
+    def evaluate(self, params, n_samples: int, seed: int, want_actions=False):
+        """evaluate(): rows [n_apps][5], histogram (lower, count), optional shader actions."""
+        rows = np.empty((self.n_apps, 5), np.float64)
+        act = np.empty(self.n_shaders, np.uint8) if want_actions else None
+        cap = 1 << 16
+        lo = np.empty(cap, np.float64)
+        cnt = np.empty(cap, np.uint64)
+        nb = _sz()
+        self.dev._ck(self.dev.L.gbxcu_evaluate(
+            self.dev.h, self.h, _f32(params), n_samples, seed, rows,
+            None if act is None else act.ctypes.data, lo.ctypes.data, cnt.ctypes.data, cap,
+            C.byref(nb)))
+        hist = (lo[:nb.value].copy(), cnt[:nb.value].copy())
+        return (rows, hist, act) if want_actions else (rows, hist)
+
+    def evaluate_dev(self, d_params: int, n_samples: int, seed: int, d_actions: int, d_rows: int,
+                     stream: int | None = None):
+        self.dev._ck(self.dev.L.gbxcu_evaluate_dev(self.dev.h, self.h, d_params, n_samples, seed,
+                                                   d_actions, d_rows, stream))

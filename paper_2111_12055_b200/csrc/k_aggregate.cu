@@ -1,0 +1,166 @@
+// k_aggregate.cu — per-application reward aggregation (K3) for sm_100a.
+//
+// Replaces SimSuite::frame_time / run_benchmark (proj/src/simenv.cpp:439-510),
+// the reward ratio of attribute_rewards / reward_from_framerate
+// (proj/src/tuner.cpp:131-147, proj/src/core.cpp:125-133), and evaluate's
+// uplift and 1%-bin histogram (proj/src/tuner.cpp:282-313).
+//
+// One warp per application (segment). The reference's per-app sums are strict
+// left folds in pipeline -> slot order, so each warp loads 32 slots at a time
+// (coalesced slot arrays, gathered shader latents/actions), forms the 32
+// per-slot terms in parallel, and folds them in slot order with register
+// shuffles — the serial part is one DADD per slot, everything else (gathers,
+// products, divisions) is lane-parallel. Results are bit-identical to the
+// reference.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gbxcu {
+
+__device__ __forceinline__ double warp_fold(double acc, double term, int count, bool sub) {
+    for (int k = 0; k < count; ++k) {
+        const double t = __shfl_sync(0xffffffffu, term, k);
+        acc = sub ? __dsub_rn(acc, t) : __dadd_rn(acc, t);
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(AGG_BLOCK) aggregate_kernel(AggArgs a) {
+    const int lane = threadIdx.x & 31;
+    const size_t warps = (size_t)gridDim.x * (AGG_BLOCK / 32);
+    for (size_t app = (size_t)blockIdx.x * (AGG_BLOCK / 32) + (threadIdx.x >> 5); app < a.n_apps;
+         app += warps) {
+        const double baseline = a.app_f64[4 * app], cap = a.app_f64[4 * app + 1];
+        const double sigma = a.app_f64[4 * app + 2], thr = a.app_f64[4 * app + 3];
+        const uint64_t p_lo = a.app_pipe_off[app], p_hi = a.app_pipe_off[app + 1];
+
+        // pass 1: bandwidth load = sum over all slots of p * demand(a)
+        double load = 0.0;
+        for (uint64_t p = p_lo; p < p_hi; ++p) {
+            const uint64_t s_lo = a.pipe_slot_off[p], s_hi = a.pipe_slot_off[p + 1];
+            for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+                const uint64_t s = s0 + lane;
+                double term = 0.0;
+                if (s < s_hi) {
+                    const uint32_t sh = a.slot_shader[s];
+                    const double bw = a.shader_lat[3 * (size_t)sh + 1];
+                    const double demand = a.shader_action[sh] == 1 ? __dmul_rn(2.0, bw) : bw;
+                    term = __dmul_rn(a.slot_frac[s], demand);
+                }
+                load = warp_fold(load, term, (int)min((uint64_t)32, s_hi - s0), false);
+            }
+        }
+        double throttle = 1.0;
+        if (isfinite(cap) && load > cap) throttle = __ddiv_rn(cap, load);
+
+        // pass 2: per pipeline inner = 1 - sum p + sum p / s_eff
+        double total = 0.0;
+        for (uint64_t p = p_lo; p < p_hi; ++p) {
+            const uint64_t s_lo = a.pipe_slot_off[p], s_hi = a.pipe_slot_off[p + 1];
+            double inner = 1.0;
+            for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+                const uint64_t s = s0 + lane;
+                const double term = s < s_hi ? a.slot_frac[s] : 0.0;
+                inner = warp_fold(inner, term, (int)min((uint64_t)32, s_hi - s0), true);
+            }
+            for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+                const uint64_t s = s0 + lane;
+                double term = 0.0;
+                if (s < s_hi) {
+                    const uint32_t sh = a.slot_shader[s];
+                    const double d = a.shader_lat[3 * (size_t)sh];
+                    const double bw = a.shader_lat[3 * (size_t)sh + 1];
+                    const double kap = a.shader_lat[3 * (size_t)sh + 2];
+                    // wave64_speedup = (1 + kappa)(1 - 0.5 d)  (simenv.hpp:65-67)
+                    double sp = a.shader_action[sh] == 1
+                                    ? __dmul_rn(__dadd_rn(1.0, kap), __dsub_rn(1.0, __dmul_rn(0.5, d)))
+                                    : 1.0;
+                    if (bw > thr) sp = __dmul_rn(sp, throttle);
+                    term = __ddiv_rn(a.slot_frac[s], sp);
+                }
+                inner = warp_fold(inner, term, (int)min((uint64_t)32, s_hi - s0), false);
+            }
+            const double wt = __dmul_rn(a.pipe_wt[2 * p], a.pipe_wt[2 * p + 1]);
+            total = __dadd_rn(total, __dmul_rn(wt, inner));
+        }
+        const double fps = __ddiv_rn(1.0, total);
+
+        // noisy samples: SplitMix64(derive_seed({run_seed, 0x4E5A45, app}))
+        const uint64_t run_seed =
+            a.run_seed ? a.run_seed[app] : derive_seed3(a.eval_seed, 0x45564Cu, (uint64_t)app);
+        const uint64_t ns = derive_seed3(run_seed, 0x4E5A45u, (uint64_t)app);
+        const double half = __dmul_rn(sigma, sqrt(3.0));
+        double sum = 0.0;
+        for (int k0 = 0; k0 < a.n_samples; k0 += 32) {
+            const int k = k0 + lane;
+            double smp = 0.0;
+            if (k < a.n_samples) {
+                const double su = signed_unit_of(sm_draw(ns, (uint64_t)k + 1));
+                smp = __dmul_rn(fps, __dadd_rn(1.0, __dmul_rn(su, half)));
+                if (a.samples) a.samples[app * (size_t)a.n_samples + k] = smp;
+            }
+            sum = warp_fold(sum, smp, min(32, a.n_samples - k0), false);
+        }
+        if (lane == 0) {
+            const double tuned = __ddiv_rn(sum, (double)a.n_samples);
+            const double ratio = __ddiv_rn(tuned, baseline);
+            double* row = a.rows + 5 * app;
+            row[0] = total;
+            row[1] = fps;
+            row[2] = tuned;
+            row[3] = __dmul_rn(100.0, __dsub_rn(ratio, 1.0));
+            row[4] = ratio;
+        }
+    }
+}
+
+// evaluate's histogram (proj/src/tuner.cpp:293-313), one CTA.
+__global__ void __launch_bounds__(1024)
+histogram_kernel(const double* __restrict__ rows, int stride, size_t n, double* __restrict__ lower,
+                 unsigned long long* __restrict__ count, size_t cap,
+                 unsigned long long* __restrict__ n_bins) {
+    __shared__ double s_lo[32], s_hi[32];
+    __shared__ double s_lower;
+    __shared__ unsigned long long s_bins;
+    if (n == 0) {
+        if (threadIdx.x == 0) *n_bins = 0;
+        return;
+    }
+    double lo = rows[3], hi = rows[3];
+    for (size_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const double u = rows[k * stride + 3];
+        lo = fmin(lo, u);
+        hi = fmax(hi, u);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { s_lo[w] = lo; s_hi[w] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) { lo = fmin(lo, s_lo[i]); hi = fmax(hi, s_hi[i]); }
+        const double lw = floor(lo);
+        const double ch = ceil(hi);
+        const double span = fmax(1.0, __dadd_rn(__dsub_rn(ch, lw), hi == ch ? 1.0 : 0.0));
+        s_lower = lw;
+        s_bins = (unsigned long long)span;
+        *n_bins = s_bins;
+    }
+    __syncthreads();
+    const double lw = s_lower;
+    const unsigned long long bins = s_bins;
+    for (size_t b = threadIdx.x; b < bins && b < cap; b += blockDim.x) {
+        lower[b] = __dadd_rn(lw, (double)b);
+        count[b] = 0;
+    }
+    __syncthreads();
+    for (size_t k = threadIdx.x; k < n; k += blockDim.x) {
+        unsigned long long idx = __double2ull_rz(__dsub_rn(rows[k * stride + 3], lw));
+        if (idx > bins - 1) idx = bins - 1;
+        if (idx < cap) atomicAdd(count + idx, 1ull);
+    }
+}
+
+}  // namespace gbxcu

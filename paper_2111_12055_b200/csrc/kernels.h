@@ -1,0 +1,87 @@
+// kernels.h — kernel declarations shared between the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace gbxcu {
+
+constexpr int FWD_BLOCK = 256;    // fast inference: 8 warps, one state per thread
+constexpr int EXACT_BLOCK = 128;  // exact fp64 inference
+constexpr int TB = 64;            // train: records per CTA tile
+constexpr int TRAIN_BLOCK = 256;  // train: 8 warps
+constexpr int SHUF_BLOCK = 256;
+constexpr int AGG_BLOCK = 256;    // aggregation: 8 warps = 8 apps per CTA
+
+// mode bits for the inference kernels
+constexpr int FWD_PROBS = 1, FWD_ACTIONS = 2, FWD_COLLECT = 4;
+
+struct TrainArgs {
+    const float* feat;
+    const double* tgt;
+    const uint32_t* order;
+    float* params;         // fp32 master copy (updated in place)
+    double* partials;      // [gridDim][NP+1] per-CTA gradient + loss partials
+    unsigned int* bar;     // grid-barrier counter (zeroed before launch)
+    int* diverged_epoch;   // -1 until a non-finite batch loss
+    double* epoch_loss;    // [epochs]
+    size_t n;
+    int batch;
+    int epoch;
+    double lr;
+    int rank, nranks;
+};
+
+struct AggArgs {
+    size_t n_apps;
+    const uint64_t* app_pipe_off;
+    const uint64_t* pipe_slot_off;
+    const uint32_t* slot_shader;
+    const double* slot_frac;
+    const double* pipe_wt;
+    const double* shader_lat;
+    const double* app_f64;
+    const uint8_t* shader_action;
+    const uint64_t* run_seed;  // nullable: derive from eval_seed
+    uint64_t eval_seed;
+    int n_samples;
+    double* rows;              // [n_apps][5]
+    double* samples;           // nullable [n_apps][n_samples]
+};
+
+__global__ void policy_init_kernel(uint64_t seed, float* params);
+__global__ void fwd_fast_kernel(const float* params, const float* feat, size_t n, double* probs,
+                                uint8_t* actions, const uint64_t* seg_off, size_t nseg,
+                                const uint64_t* seg_seed, double eps, uint32_t* recheck,
+                                unsigned int* n_recheck, unsigned int* flags, int mode);
+__global__ void fwd_exact_kernel(const float* params, const float* feat, size_t n,
+                                 const uint32_t* list, const unsigned int* n_list, double* probs,
+                                 uint8_t* actions, const uint64_t* seg_off, size_t nseg,
+                                 const uint64_t* seg_seed, double eps, unsigned int* flags,
+                                 int mode);
+size_t fast_smem_bytes();
+size_t exact_smem_bytes();
+
+__global__ void train_epoch_kernel(TrainArgs a);
+__global__ void train_partial_kernel(TrainArgs a, long step);
+__global__ void reduce_partials_kernel(const double* partials, int nctas, double* red,
+                                       const int* diverged);
+__global__ void apply_update_kernel(float* params, const double* red, double lr, size_t nb,
+                                    int epoch, int* diverged, double* epoch_acc);
+__global__ void finish_epoch_kernel(const double* epoch_acc, size_t n, int epoch,
+                                    const int* diverged, double* out);
+__global__ void batch_grad_kernel(TrainArgs a, double* grad_out, double* loss_out);
+size_t train_smem_bytes();
+
+__global__ void iota_kernel(uint32_t* order, size_t n);
+__global__ void shuffle_epoch_kernel(uint32_t* order, uint32_t n, uint64_t seed_e, int* resv,
+                                     uint32_t* list_a, uint32_t* list_b, unsigned int* counters,
+                                     unsigned int* bar, const int* diverged);
+
+__global__ void aggregate_kernel(AggArgs a);
+__global__ void histogram_kernel(const double* rows, int stride, size_t n, double* lower,
+                                 unsigned long long* count, size_t cap,
+                                 unsigned long long* n_bins);
+
+}  // namespace gbxcu

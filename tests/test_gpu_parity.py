@@ -1,0 +1,257 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle
+restatement and the golden vectors from the compiled reference.
+
+Tolerances (stated per BASELINE.json north_star):
+  * actions, permutation indices, per-app aggregation rows, histograms: bit-exact;
+  * EXACT-mode probabilities: <= 4 ulp of fp64 (CUDA exp vs glibc exp);
+  * FAST-mode probabilities: relative 1e-5;
+  * gradients: relative 1e-12 per component (log/exp ulps propagate);
+  * weights after N SGD steps: <= 1 fp32 ulp per weight (1-CTA steps,
+    expected 0), <= 2 ulp for multi-CTA steps (fp64 re-association);
+  * epoch losses: relative 1e-12.
+"""
+import numpy as np
+import pytest
+
+import paper_2111_12055_b200 as gbx
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def ulps32(a, b):
+    a = np.ascontiguousarray(a, np.float32).view(np.int32).astype(np.int64)
+    b = np.ascontiguousarray(b, np.float32).view(np.int32).astype(np.int64)
+    return np.abs(a - b)
+
+
+def ulps64(a, b):
+    a = np.ascontiguousarray(a, np.float64).view(np.int64)
+    b = np.ascontiguousarray(b, np.float64).view(np.int64)
+    return np.abs(a.astype(object) - b.astype(object)).astype(np.float64)
+
+
+# ----------------------------------------------------------------- policy
+@pytest.mark.parametrize("seed", [0, 1, 7, 1234, 2**63 + 5])
+def test_policy_init_bit_exact(dev, orc, seed):
+    np.testing.assert_array_equal(dev.policy_init(seed), orc.policy_init(seed))
+
+
+@pytest.mark.parametrize("tag", ["init", "trained"])
+def test_forward_matches_golden(dev, orc, tag):
+    g = golden("forward_g1")
+    feat, _ = orc.g1(int(g["seed"]), int(g["n"]))
+    p = g[f"params_{tag}"]
+    probs, act = dev.forward(p, feat, gbx.FWD_EXACT)
+    np.testing.assert_array_equal(act, g[f"act_{tag}"])
+    assert ulps64(probs, g[f"probs_{tag}"]).max() <= 4
+    probs_f, act_f = dev.forward(p, feat, gbx.FWD_FAST)
+    np.testing.assert_array_equal(act_f, g[f"act_{tag}"])
+    np.testing.assert_allclose(probs_f, g[f"probs_{tag}"], rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 1000, 200_003])
+def test_forward_ragged_sizes(dev, orc, n):
+    g = golden("forward_g1")
+    feat, _ = orc.g1(1000 + n, n)
+    p = g["params_trained"]
+    probs_o, act_o = orc.forward(p, feat)
+    probs, act = dev.forward(p, feat, gbx.FWD_FAST)
+    np.testing.assert_array_equal(act, act_o)
+    np.testing.assert_allclose(probs, probs_o, rtol=1e-5, atol=1e-7)
+    act_g = dev.select_greedy(p, feat)
+    np.testing.assert_array_equal(act_g, act_o)
+
+
+def test_forward_exact_ties_and_zero_net(dev, orc):
+    feat, _ = orc.g1(12, 777)
+    for mode in (gbx.FWD_EXACT, gbx.FWD_FAST):
+        probs, act = dev.forward(np.zeros(5026, np.float32), feat, mode)
+        assert (probs == 0.5).all() and (act == 1).all()   # test_policy.cpp:58-76,197-202
+    # identical output rows -> l0 == l1 exactly for every state -> Wave64
+    p = orc.policy_init(3)
+    p[4960:4992] = p[4992:5024]
+    p[5024] = p[5025] = 0.25
+    _, act = dev.forward(p, feat, gbx.FWD_FAST)
+    assert (act == 1).all()
+    np.testing.assert_array_equal(act, orc.forward(p, feat)[1])
+
+
+def test_forward_near_ties_are_exact(dev, orc):
+    # Shrink the logit gap so that a large share of states falls inside the
+    # fp32 guard band; actions must still equal the fp64 reference.
+    p = golden("forward_g1")["params_trained"].copy()
+    p[4960:4992] = p[4992:5024] + np.float32(1e-7) * np.sign(p[4992:5024])
+    feat, _ = orc.g1(99, 50_000)
+    _, act = dev.forward(p, feat, gbx.FWD_FAST)
+    np.testing.assert_array_equal(act, orc.forward(p, feat)[1])
+
+
+def test_forward_rejects_non_finite(dev, orc):
+    feat, _ = orc.g1(5, 64)
+    feat[17, 10] = np.nan
+    with pytest.raises(gbx.ValidationError):
+        dev.forward(orc.policy_init(3), feat)
+    feat[17, 10] = np.inf
+    with pytest.raises(gbx.ValidationError):
+        dev.forward(orc.policy_init(3), feat, gbx.FWD_FAST)
+
+
+def test_forward_empty(dev):
+    probs, act = dev.forward(np.zeros(5026, np.float32), np.zeros((0, 44), np.float32))
+    assert probs.shape == (0, 2) and act.shape == (0,)
+
+
+# ------------------------------------------------------- loss / gradient
+def test_gradient_matches_golden(dev, orc):
+    g = golden("gradient")
+    for inst in range(3):
+        f, t = orc.g1(2024 + inst, 3)
+        p = orc.policy_init(1000 + inst)
+        np.testing.assert_allclose(dev.batch_kl_gradient(p, f, t), g[f"g{inst}"], rtol=1e-12,
+                                   atol=1e-300)
+        assert dev.batch_kl_loss(p, f, t) == pytest.approx(float(g[f"l{inst}"]), rel=1e-13)
+    f, t = orc.g1(77, 32)
+    np.testing.assert_allclose(dev.batch_kl_gradient(orc.policy_init(7), f, t), g["g32"],
+                               rtol=1e-12, atol=1e-300)
+
+
+def test_gradient_large_batch(dev, orc):
+    f, t = orc.g1(31, 3001)
+    p = golden("forward_g1")["params_trained"]
+    np.testing.assert_allclose(dev.batch_kl_gradient(p, f, t), orc.batch_kl_gradient(p, f, t),
+                               rtol=1e-11, atol=1e-300)
+
+
+# -------------------------------------------------------------------- fit
+@pytest.mark.parametrize("name", ["c1", "b4096", "det40", "b1", "bigger_than_n"])
+def test_fit_matches_golden(dev, orc, name):
+    g = golden("fit")
+    ds, n, isd, ep, b, sd = (int(x) for x in g[f"{name}_cfg"])
+    f, t = orc.g1(ds, n)
+    p, el = dev.fit(orc.policy_init(isd), f, t, float(g[f"{name}_lr"]), ep, b, sd)
+    tol = 1 if b <= 64 else 2
+    assert ulps32(p, g[f"{name}_params"]).max() <= tol
+    np.testing.assert_allclose(el, g[f"{name}_loss"], rtol=1e-12)
+
+
+def test_fit_overfit_single_sample(dev, orc):
+    g = golden("fit")
+    f, _ = orc.g1(8, 1)
+    p, el = dev.fit(orc.policy_init(42), f, np.array([[0.99, 0.01]]), 0.05, 200, 32, 7)
+    assert el[-1] < 0.01 and el[-1] <= el[0]
+    assert ulps32(p, g["overfit_params"]).max() <= 1
+
+
+def test_fit_uniform_targets_keep_zero_net(dev, orc):
+    # proj/tests/test_policy.cpp:155-166
+    f, _ = orc.g1(9, 16)
+    t = np.full((16, 2), 0.5)
+    p, el = dev.fit(np.zeros(5026, np.float32), f, t, 0.01, 20, 32, 0)
+    assert (el < 1e-6).all()
+
+
+@pytest.mark.parametrize("batch,max_ctas", [(4096, 0), (4096, 7), (1000, 3), (65536, 0)])
+def test_fit_multi_cta_within_tolerance(dev, orc, batch, max_ctas):
+    n = 70_001
+    f, t = orc.g1(17, n)
+    p0 = orc.policy_init(21)
+    rc, p_ref, el_ref, _ = orc.fit(p0, f, t, 0.02, 2, batch, 4)
+    p, el = dev.fit(p0, f, t, 0.02, 2, batch, 4, max_ctas=max_ctas)
+    assert ulps32(p, p_ref).max() <= 2
+    np.testing.assert_allclose(el, el_ref, rtol=1e-12)
+    p2, el2 = dev.fit(p0, f, t, 0.02, 2, batch, 4, max_ctas=max_ctas)
+    np.testing.assert_array_equal(p, p2)          # deterministic (test_policy.cpp:168-184)
+    np.testing.assert_array_equal(el, el2)
+
+
+def test_fit_c1_many_epochs_bit_stable(dev, orc):
+    f, t = orc.g1(42, 3000)
+    p0 = orc.policy_init(7)
+    rc, p_ref, el_ref, _ = orc.fit(p0, f, t, 0.01, 5, 32, 99)
+    p, el = dev.fit(p0, f, t, 0.01, 5, 32, 99)
+    assert ulps32(p, p_ref).max() <= 1
+    np.testing.assert_allclose(el, el_ref, rtol=1e-12)
+
+
+def test_fit_divergence_matches_reference(dev, orc):
+    f, t = orc.g1(6, 256)
+    f[:, 8:] *= np.float32(1e3)
+    p0 = orc.policy_init(5)
+    rc, p_ref, el_ref, ep_ref = orc.fit(p0, f, t, 1e12, 4, 32, 1)
+    assert rc == 2
+    with pytest.raises(gbx.TrainingDivergedError) as ei:
+        dev.fit(p0, f, t, 1e12, 4, 32, 1)
+    assert ei.value.epoch == ep_ref
+    same = (ei.value.params == p_ref) | (np.isnan(ei.value.params) & np.isnan(p_ref))
+    assert same.mean() > 0.99
+
+
+def test_fit_validation(dev, orc):
+    f, t = orc.g1(1, 8)
+    p = orc.policy_init(1)
+    with pytest.raises(gbx.ValidationError):
+        dev.fit(p, f, t, lr=0.0)
+    with pytest.raises(gbx.ValidationError):
+        dev.fit(p, f, t, epochs=0)
+    with pytest.raises(gbx.ValidationError):
+        dev.fit(p, f, t, batch=0)
+    with pytest.raises(gbx.ValidationError):
+        dev.fit(p, f[:0], t[:0])
+
+
+def test_fit_order_matches_golden(dev, orc):
+    g = golden("order")
+    np.testing.assert_array_equal(dev.fit_order(int(g["n"]), int(g["seed"]), int(g["epochs"])),
+                                  g["order"])
+    big = dev.fit_order(int(g["big_n"]), int(g["big_seed"]), int(g["big_epochs"]))
+    assert orc.fnv1a(big) == int(g["big_fnv"])
+    for n in (1, 2, 3, 5, 64, 4097):
+        np.testing.assert_array_equal(dev.fit_order(n, 3, 3), orc.fit_order(n, 3, 3).astype(np.uint32))
+
+
+def test_fit_order_full_size_is_permutation(dev, orc):
+    n = 1_000_000
+    o = dev.fit_order(n, 99, 1)
+    assert np.array_equal(np.sort(o), np.arange(n, dtype=np.uint32))
+    ref = orc.fit_order(n, 99, 1).astype(np.uint32)
+    assert orc.fnv1a(o) == orc.fnv1a(ref)
+
+
+# ------------------------------------------------------------- collection
+@pytest.mark.parametrize("eps", [0.0, 0.3, 1.0])
+def test_collect_matches_oracle(dev, orc, eps):
+    feat, _ = orc.g1(8, 20_000)
+    p = golden("forward_g1")["params_trained"]
+    off = np.array([0, 1, 5000, 5001, 12_345, 20_000], np.uint64)
+    seeds = np.array([orc.derive_seed(3, 0x414354, 0, b) for b in range(5)], np.uint64)
+    np.testing.assert_array_equal(dev.collect(p, feat, off, seeds, eps),
+                                  orc.collect(p, feat, off, seeds, eps))
+
+
+# ------------------------------------------------------------ aggregation
+@pytest.mark.parametrize("name", ["suite_free", "suite_contended"])
+def test_aggregate_and_evaluate_match_golden(dev, orc, name):
+    s = dict(golden(name))
+    nb = len(s["app_pipe_off"]) - 1
+    rows_o, smp_o = orc.aggregate(s, s["rand_actions"], s["rand_run_seed"], 10, want_samples=True)
+    rows, smp = dev.aggregate(s, s["rand_actions"], s["rand_run_seed"], 10, want_samples=True)
+    np.testing.assert_array_equal(rows, rows_o)
+    np.testing.assert_array_equal(smp, s["rand_samples"])
+    ds = dev.suite_upload(s, s["features"])
+    rows_e, (lo, cnt), act = ds.evaluate(s["eval_params"], 10, int(s["eval_seed"]),
+                                         want_actions=True)
+    np.testing.assert_array_equal(act, orc.forward(s["eval_params"], s["features"])[1])
+    np.testing.assert_array_equal(rows_e[:, 2], s["eval_rows"][:, 1])
+    np.testing.assert_array_equal(rows_e[:, 3], s["eval_rows"][:, 2])
+    np.testing.assert_array_equal(lo, s["hist_lower"])
+    np.testing.assert_array_equal(cnt, s["hist_count"])
+    ds.close()
+
+
+@pytest.mark.parametrize("uplift", [[3.0], [-2.5, -2.5], [0.0, 1.0, 2.0], [-7.3, 0.2, 12.9, 12.0]])
+def test_histogram_edges(dev, orc, uplift):
+    lo, cnt = dev.histogram(uplift)
+    lo_o, cnt_o = orc.histogram(uplift)
+    np.testing.assert_array_equal(lo, lo_o)
+    np.testing.assert_array_equal(cnt, cnt_o)
