@@ -14,6 +14,8 @@
 //     summation order (bias first, ascending index; layer-1 products are exact
 //     in fp64 so DFMA is used there, layers 2-3 use mul-then-add rounding).
 //     Runs either over all states (EXACT mode) or over the re-check list.
+#include <cstddef>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -40,6 +42,7 @@ __global__ void policy_init_kernel(uint64_t seed, float* __restrict__ params) {
 
 // --------------------------------------------------------------- fast path
 struct FastSmem {
+    __align__(16) float xs[FWD_BLOCK / 32][32 * F];  // per-warp staging of 32 rows
     float w0[H1 * F];   // [j][i]
     float w1t[H1 * H2]; // [j][k] = w1[k][j]
     float w2[A * H2];   // [a][k]
@@ -47,8 +50,8 @@ struct FastSmem {
     float b1[H2];
     float b2[A];
     float stats[8];     // R0,B0,R1,B1,R2,B2
-    float xs[FWD_BLOCK / 32][32 * F];  // per-warp staging of 32 rows
 };
+static_assert(offsetof(FastSmem, w0) % 16 == 0 && offsetof(FastSmem, w1t) % 16 == 0, "align");
 
 // Per-net constants of the guard: R_l = max_row ||w_row||_1, B_l = max |b|.
 // Computed in fp64 and rounded up so the fp32 bound stays an upper bound.

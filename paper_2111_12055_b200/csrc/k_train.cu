@@ -24,6 +24,8 @@
 //   PARTIAL: one launch = one step's per-CTA partial gradients (data-parallel
 //            path; reduction, NCCL all-reduce and update run in follow-up
 //            kernels, see gbxcu_api.cu).
+#include <cstddef>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -47,6 +49,10 @@ struct TrainSmem {
     double kl[TB];
     double scal[4];      // [0] step loss total, [1] loss, [2] diverged flag
 };
+
+static_assert(offsetof(TrainSmem, x) % 16 == 0 && offsetof(TrainSmem, h1) % 16 == 0 &&
+                  offsetof(TrainSmem, d2) % 16 == 0 && offsetof(TrainSmem, d1) % 16 == 0,
+              "double2 loads need 16-byte alignment");
 
 size_t train_smem_bytes() { return sizeof(TrainSmem); }
 
