@@ -112,9 +112,11 @@ int setup_kernel_attrs() {
         };
         set((const void*)fwd_fast_kernel, fast_smem_bytes());
         set((const void*)fwd_exact_kernel, exact_smem_bytes());
-        set((const void*)train_epoch_kernel, train_smem_bytes());
-        set((const void*)train_partial_kernel, train_smem_bytes());
-        set((const void*)batch_grad_kernel, train_smem_bytes());
+        set((const void*)train_epoch_kernel<32>, train_smem_bytes(32));
+        set((const void*)train_epoch_kernel<64>, train_smem_bytes(64));
+        set((const void*)train_partial_kernel<32>, train_smem_bytes(32));
+        set((const void*)train_partial_kernel<64>, train_smem_bytes(64));
+        set((const void*)batch_grad_kernel, train_smem_bytes(64));
     });
     return rc;
 }
@@ -182,12 +184,17 @@ int validate_cfg(const gbxcu_train_cfg* cfg, size_t n) {
     return GBXCU_OK;
 }
 
-int train_grid(gbxcu_ctx* c, const gbxcu_train_cfg* cfg, size_t n) {
+// CTAs per step and records per tile: spread each rank's share of the batch
+// over up to one CTA per SM in tiles of 32 records; switch to 64-record
+// tiles once every SM already has more than 32 records.
+void train_grid(gbxcu_ctx* c, const gbxcu_train_cfg* cfg, size_t n, int& G, int& tb) {
     const size_t b = std::min<size_t>((size_t)cfg->batch_size, n);
     const size_t per_rank = (b + c->nranks - 1) / c->nranks;
-    int g = (int)std::min<size_t>((per_rank + TB - 1) / TB, (size_t)c->num_sms);
-    if (cfg->max_ctas > 0) g = std::min(g, cfg->max_ctas);
-    return std::max(g, 1);
+    G = (int)std::min<size_t>((per_rank + 31) / 32, (size_t)c->num_sms);
+    if (cfg->max_ctas > 0) G = std::min(G, cfg->max_ctas);
+    G = std::max(G, 1);
+    const size_t per_cta = (per_rank + G - 1) / G;
+    tb = per_cta <= 32 ? 32 : 64;
 }
 
 int shuffle_epoch(gbxcu_ctx* c, size_t n, uint64_t seed, int epoch, cudaStream_t st) {
@@ -231,7 +238,8 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     RET(prepare_order(c, n, st));
     RET(c->epoch_loss.ensure(sizeof(double) * cfg->epochs));
     RET(c->epoch_acc.ensure(16));
-    const int G = train_grid(c, cfg, n);
+    int G = 1, tb = 32;
+    train_grid(c, cfg, n, G, tb);
     RET(c->partials.ensure(sizeof(double) * (size_t)G * (NP + 1)));
     RET(c->red.ensure(sizeof(double) * (NP + 1)));
 
@@ -257,11 +265,12 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
         if (c->nranks == 1) {
             CK(cudaMemsetAsync(c->bar.as<unsigned int>() + 2, 0, 8, st));
             void* args[] = {&a};
+            const void* fn = tb == 32 ? (const void*)train_epoch_kernel<32>
+                                      : (const void*)train_epoch_kernel<64>;
             if (G == 1) {
-                train_epoch_kernel<<<1, TRAIN_BLOCK, train_smem_bytes(), st>>>(a);
+                CK(cudaLaunchKernel(fn, 1, TRAIN_BLOCK, args, train_smem_bytes(tb), st));
             } else {
-                CK(cudaLaunchCooperativeKernel((const void*)train_epoch_kernel, G, TRAIN_BLOCK,
-                                               args, train_smem_bytes(), st));
+                CK(cudaLaunchCooperativeKernel(fn, G, TRAIN_BLOCK, args, train_smem_bytes(tb), st));
             }
             RET(check_launch(c, "train_epoch_kernel"));
         } else {
@@ -269,9 +278,12 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
             for (long s = 0; s < n_steps; ++s) {
                 const size_t start = (size_t)s * cfg->batch_size;
                 const size_t nb = std::min(n, start + (size_t)cfg->batch_size) - start;
-                train_partial_kernel<<<G, TRAIN_BLOCK, train_smem_bytes(), st>>>(a, s);
+                if (tb == 32)
+                    train_partial_kernel<32><<<G, TRAIN_BLOCK, train_smem_bytes(32), st>>>(a, s);
+                else
+                    train_partial_kernel<64><<<G, TRAIN_BLOCK, train_smem_bytes(64), st>>>(a, s);
                 RET(check_launch(c, "train_partial_kernel"));
-                reduce_partials_kernel<<<(NP + 1 + 255) / 256, 256, 0, st>>>(
+                reduce_partials_kernel<<<(NP + 1 + 7) / 8, 256, 0, st>>>(
                     c->partials.as<double>(), G, c->red.as<double>(), c->diverged.as<int>());
                 RET(check_launch(c, "reduce_partials_kernel"));
                 CKN(ncclAllReduce(c->red.p, c->red.p, NP + 1, ncclFloat64, ncclSum, c->comm, st));
@@ -469,7 +481,7 @@ static int batch_grad(gbxcu_ctx* c, const float* params, const float* feat, cons
     a.rank = 0;
     a.nranks = 1;
     double* dg = c->grad.as<double>();
-    batch_grad_kernel<<<1, TRAIN_BLOCK, train_smem_bytes(), st>>>(a, dg, dg + NP);
+    batch_grad_kernel<<<1, TRAIN_BLOCK, train_smem_bytes(64), st>>>(a, dg, dg + NP);
     RET(check_launch(c, "batch_grad_kernel"));
     if (grad_out) CK(cudaMemcpyAsync(grad_out, dg, sizeof(double) * NP, cudaMemcpyDeviceToHost, st));
     if (loss_out) CK(cudaMemcpyAsync(loss_out, dg + NP, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -125,7 +125,7 @@ __device__ __forceinline__ float guard_threshold(const float* st, float X, float
 }
 
 // mode bits: 1 = write probs, 2 = write actions, 4 = collect (sampled) mode
-__global__ void __launch_bounds__(FWD_BLOCK)
+__global__ void __launch_bounds__(FWD_BLOCK, 2)
 fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat, size_t n,
                 double* __restrict__ probs, uint8_t* __restrict__ actions,
                 const uint64_t* __restrict__ seg_off, size_t nseg,

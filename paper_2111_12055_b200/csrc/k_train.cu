@@ -9,21 +9,26 @@
 // — while M/N are spread over the CTA with register blocking:
 //   F1 h1[r][j]  = relu(b0[j] + sum_i x[r][i]  w0[j][i])   K = 44  (DFMA: products exact)
 //   F2 h2[r][k]  = relu(b1[k] + sum_j h1[r][j] w1[k][j])   K = 64  (mul, then add)
-//   F3 logits, softmax, KL, d3 = p (ln(p^/t^) - L) / |b|
+//   F3 logits, softmax, KL, d3 = p (ln(p^/t^) - L) / |b|   (2 threads per record)
 //   B1 d2[r][k]  = d3[r][0] w2[0][k] + d3[r][1] w2[1][k], masked by h2 > 0
 //   B2 d1[r][j]  = sum_k d2[r][k] w1[k][j], masked by h1 > 0
 //   G  gw2/gw1/gw0/gb* += per-record outer products, K = records in batch order
 // Gradient accumulators are owned by threads (registers) across all tiles of a
 // step, so a 1-CTA step reproduces the reference's per-parameter left fold bit
-// for bit (up to exp/log ulps). Multi-CTA steps reduce per-CTA partials in
-// CTA order (fp64; differs from the reference only in re-association).
+// for bit (up to exp/log ulps). Multi-CTA steps reduce per-CTA partials with a
+// fixed-shape tree (deterministic; differs from the reference only by fp64
+// re-association).
 //
-// Modes
-//   FUSED  : one launch = one epoch; G CTAs; in-kernel deterministic
-//            cross-CTA reduction + SGD with a grid barrier (cooperative launch).
-//   PARTIAL: one launch = one step's per-CTA partial gradients (data-parallel
-//            path; reduction, NCCL all-reduce and update run in follow-up
-//            kernels, see gbxcu_api.cu).
+// The records of the NEXT tile (possibly of the next step — the epoch's
+// permutation is known up front) are gathered with cp.async into a second
+// staging buffer while the current tile computes.
+//
+// Kernels
+//   train_epoch_kernel<TB>  : one launch = one epoch on one GPU; G CTAs
+//                             (cooperative when G > 1: in-kernel reduction +
+//                             SGD between two grid barriers per step).
+//   train_partial_kernel<TB>: one step's per-CTA partials (data-parallel path;
+//                             reduction, NCCL all-reduce and update follow).
 #include <cstddef>
 
 #include "common.cuh"
@@ -31,6 +36,10 @@
 
 namespace gbxcu {
 
+constexpr int NT = TRAIN_BLOCK;  // 512 threads
+constexpr int NW = NT / 32;      // 16 warps
+
+template <int TB>
 struct TrainSmem {
     double w0t[F * H1];  // [i][j]
     double w1[H2 * H1];  // [k][j]
@@ -47,76 +56,40 @@ struct TrainSmem {
     double d3[TB * 2];
     double tgt[TB * 2];
     double kl[TB];
-    double scal[4];      // [0] step loss total, [1] loss, [2] diverged flag
+    double stage_t[2][TB * 2];  // cp.async staging: targets
+    float stage_f[2][TB * F];   // cp.async staging: raw fp32 features
+    double scal[4];             // [1] batch loss, [2] diverged flag
 };
 
-static_assert(offsetof(TrainSmem, x) % 16 == 0 && offsetof(TrainSmem, h1) % 16 == 0 &&
-                  offsetof(TrainSmem, d2) % 16 == 0 && offsetof(TrainSmem, d1) % 16 == 0,
-              "double2 loads need 16-byte alignment");
+template <int TB>
+constexpr bool smem_aligned() {
+    return offsetof(TrainSmem<TB>, x) % 16 == 0 && offsetof(TrainSmem<TB>, h1) % 16 == 0 &&
+           offsetof(TrainSmem<TB>, d2) % 16 == 0 && offsetof(TrainSmem<TB>, d1) % 16 == 0 &&
+           offsetof(TrainSmem<TB>, stage_t) % 16 == 0 && offsetof(TrainSmem<TB>, stage_f) % 16 == 0;
+}
+static_assert(smem_aligned<32>() && smem_aligned<64>(), "16-byte aligned smem arrays");
 
-size_t train_smem_bytes() { return sizeof(TrainSmem); }
-
-__device__ void load_train_weights(TrainSmem& S, const float* __restrict__ p) {
-    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) {
-        const int j = t / F, i = t % F;
-        S.w0t[i * H1 + j] = p[OFF_W0 + t];
-    }
-    for (int t = threadIdx.x; t < H2 * H1; t += blockDim.x) {
-        const double w = p[OFF_W1 + t];
-        const int k = t / H1, j = t % H1;
-        S.w1[t] = w;
-        S.w1t[j * H2 + k] = w;
-    }
-    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[t] = p[OFF_W2 + t];
-    for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = p[OFF_B0 + t];
-    for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = p[OFF_B1 + t];
-    if (threadIdx.x < A) S.b2[threadIdx.x] = p[OFF_B2 + threadIdx.x];
+size_t train_smem_bytes(int tb) {
+    return tb == 32 ? sizeof(TrainSmem<32>) : sizeof(TrainSmem<64>);
 }
 
-// Thread-owned gradient accumulators for one step.
-struct GradRegs {
-    double g0a[8], g0b[8];  // gw0[8w+jj][lane], gw0[8w+jj][lane+32] (lane < 12)
-    double g1[4][2];        // gw1[4w+kk][lane + 32q]
-    double gx;              // tid<64: gb0[tid]; <96: gb1; <160: gw2; <162: gb2
-    double loss;            // tid 0: running sum of per-record KL (batch order)
-};
-
-__device__ __forceinline__ void zero_grads(GradRegs& g) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) g.g0a[q] = g.g0b[q] = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) g.g1[q][0] = g.g1[q][1] = 0.0;
-    g.gx = 0.0;
-    g.loss = 0.0;
+// ----------------------------------------------------------- cp.async
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes)
+                 : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// Flat parameter index owned by slot (used for partial writes and updates).
-// Visits every owned (flat index, accumulator) pair.
-template <typename Fn>
-__device__ __forceinline__ void for_each_owned(GradRegs& g, Fn fn) {
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-        const int j = 8 * w + jj;
-        fn(OFF_W0 + j * F + lane, g.g0a[jj]);
-        if (lane < F - 32) fn(OFF_W0 + j * F + lane + 32, g.g0b[jj]);
-    }
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) fn(OFF_W1 + (4 * w + kk) * H1 + lane + 32 * q, g.g1[kk][q]);
-    if (tid < 64) fn(OFF_B0 + tid, g.gx);
-    else if (tid < 96) fn(OFF_B1 + tid - 64, g.gx);
-    else if (tid < 160) fn(OFF_W2 + tid - 96, g.gx);
-    else if (tid < 162) fn(OFF_B2 + tid - 160, g.gx);
-}
-
-// Write a new fp32 parameter value (as double) into every smem copy.
-__device__ __forceinline__ void set_smem_param(TrainSmem& S, int p, double v) {
-    if (p < OFF_B0) { const int j = p / F, i = p % F; S.w0t[i * H1 + j] = v; }
+// ------------------------------------------------------------ weights
+template <int TB>
+__device__ __forceinline__ void set_smem_param(TrainSmem<TB>& S, int p, double v) {
+    if (p < OFF_B0) { const int j = p / F, i = p - j * F; S.w0t[i * H1 + j] = v; }
     else if (p < OFF_W1) S.b0[p - OFF_B0] = v;
     else if (p < OFF_B1) {
-        const int t = p - OFF_W1, k = t / H1, j = t % H1;
+        const int t = p - OFF_W1, k = t >> 6, j = t & 63;
         S.w1[t] = v;
         S.w1t[j * H2 + k] = v;
     } else if (p < OFF_W2) S.b1[p - OFF_B1] = v;
@@ -124,8 +97,9 @@ __device__ __forceinline__ void set_smem_param(TrainSmem& S, int p, double v) {
     else S.b2[p - OFF_B2] = v;
 }
 
-__device__ __forceinline__ double get_smem_param(const TrainSmem& S, int p) {
-    if (p < OFF_B0) { const int j = p / F, i = p % F; return S.w0t[i * H1 + j]; }
+template <int TB>
+__device__ __forceinline__ double get_smem_param(const TrainSmem<TB>& S, int p) {
+    if (p < OFF_B0) { const int j = p / F, i = p - j * F; return S.w0t[i * H1 + j]; }
     if (p < OFF_W1) return S.b0[p - OFF_B0];
     if (p < OFF_B1) return S.w1[p - OFF_W1];
     if (p < OFF_W2) return S.b1[p - OFF_B1];
@@ -133,48 +107,152 @@ __device__ __forceinline__ double get_smem_param(const TrainSmem& S, int p) {
     return S.b2[p - OFF_B2];
 }
 
-// Process up to TB records rows[0..nv) of the batch; accumulates into g.
-__device__ void train_tile(TrainSmem& S, GradRegs& g, const float* __restrict__ feat,
-                           const double* __restrict__ tgt, const uint32_t* __restrict__ order,
-                           size_t row0, int nv, double inv_b) {
+// All threads: fp32 master params (global) -> fp64 smem replicas, float2 loads
+// (NP is even; the buffer is 8-byte aligned).
+template <int TB>
+__device__ void load_train_weights(TrainSmem<TB>& S, const float* __restrict__ p, bool coherent) {
+    const float2* p2 = reinterpret_cast<const float2*>(p);
+    constexpr int N2 = NP / 2;
+    constexpr int PER = (N2 + NT - 1) / NT;
+    float2 v[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int t = threadIdx.x + q * NT;
+        if (t < N2) v[q] = coherent ? __ldcg(p2 + t) : __ldg(p2 + t);
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int t = threadIdx.x + q * NT;
+        if (t < N2) {
+            set_smem_param(S, 2 * t, (double)v[q].x);
+            set_smem_param(S, 2 * t + 1, (double)v[q].y);
+        }
+    }
+}
+
+// ------------------------------------------------- gradient ownership
+// warp w: gw0 rows j = 4w..4w+3 at columns i = lane (+ lane+32 if lane < 12),
+//         gw1 rows k = 2w, 2w+1 at columns j = lane, lane+32.
+// extras: tid 256..319 gb0[j], 320..351 gb1[k], 352..415 gw2[a][k],
+//         416..417 gb2[a]; tid NT-1 keeps the running KL sum.
+struct GradRegs {
+    double g0a[4], g0b[4];
+    double g1[2][2];
+    double gx;
+    double loss;
+};
+
+__device__ __forceinline__ void zero_grads(GradRegs& g) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) g.g0a[q] = g.g0b[q] = 0.0;
+    g.g1[0][0] = g.g1[0][1] = g.g1[1][0] = g.g1[1][1] = 0.0;
+    g.gx = 0.0;
+    g.loss = 0.0;
+}
+
+template <typename Fn>
+__device__ __forceinline__ void for_each_owned(GradRegs& g, Fn fn) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    // ---- P0: gather records (zero-fill rows past nv)
-    for (int t = tid; t < TB * (F / 4); t += TRAIN_BLOCK) {
-        const int r = t / (F / 4), q = t % (F / 4);
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r < nv) {
-            const size_t rec = order[row0 + r];
-            v = __ldg(reinterpret_cast<const float4*>(feat + rec * F) + q);
-        }
-        double* xr = S.x + r * F + 4 * q;
-        xr[0] = v.x; xr[1] = v.y; xr[2] = v.z; xr[3] = v.w;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+        const int j = 4 * w + jj;
+        fn(OFF_W0 + j * F + lane, g.g0a[jj]);
+        if (lane < F - 32) fn(OFF_W0 + j * F + lane + 32, g.g0b[jj]);
     }
-    if (tid < TB) {
-        double t0 = 0.5, t1 = 0.5;
-        if (tid < nv) {
-            const size_t rec = order[row0 + tid];
-            t0 = tgt[2 * rec];
-            t1 = tgt[2 * rec + 1];
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) fn(OFF_W1 + (2 * w + kk) * H1 + lane + 32 * q, g.g1[kk][q]);
+    if (tid >= 256 && tid < 320) fn(OFF_B0 + tid - 256, g.gx);
+    else if (tid >= 320 && tid < 352) fn(OFF_B1 + tid - 320, g.gx);
+    else if (tid >= 352 && tid < 416) fn(OFF_W2 + tid - 352, g.gx);
+    else if (tid >= 416 && tid < 418) fn(OFF_B2 + tid - 416, g.gx);
+}
+
+// ------------------------------------------------------------ tiling
+// Records of step `step` handled by CTA `cta` of `nctas` on rank `rank`:
+// equal contiguous slices of the global batch, rank-major then CTA-major.
+__device__ __forceinline__ void step_slice(const TrainArgs& a, long step, int cta, int nctas,
+                                           size_t& lo, size_t& hi, size_t& nb) {
+    const size_t start = (size_t)step * (size_t)a.batch;
+    const size_t stop = min(a.n, start + (size_t)a.batch);
+    nb = stop - start;
+    const size_t per_rank = (nb + a.nranks - 1) / a.nranks;
+    const size_t r_lo = min(stop, start + (size_t)a.rank * per_rank);
+    const size_t r_hi = min(stop, r_lo + per_rank);
+    const size_t per_cta = (r_hi - r_lo + nctas - 1) / nctas;
+    lo = min(r_hi, r_lo + (size_t)cta * per_cta);
+    hi = min(r_hi, lo + per_cta);
+}
+
+// Next tile of this CTA after (step, r0) within steps < step_end. r0 == SIZE_MAX
+// asks for the first tile of `step`.
+template <int TB>
+__device__ bool next_tile(const TrainArgs& a, long step_end, long& step, size_t& r0, int& nv) {
+    size_t lo, hi, nb;
+    if (r0 != (size_t)-1) {
+        step_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
+        if (r0 + TB < hi) {
+            r0 += TB;
+            nv = (int)min((size_t)TB, hi - r0);
+            return true;
         }
-        S.tgt[2 * tid] = t0;
-        S.tgt[2 * tid + 1] = t1;
+        ++step;
     }
+    for (; step < step_end; ++step) {
+        step_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
+        if (hi > lo) {
+            r0 = lo;
+            nv = (int)min((size_t)TB, hi - lo);
+            return true;
+        }
+    }
+    return false;
+}
+
+template <int TB>
+__device__ void prefetch_tile(TrainSmem<TB>& S, int buf, const TrainArgs& a, size_t r0, int nv) {
+    for (int t = threadIdx.x; t < TB * (F / 4); t += NT) {
+        const int r = t / (F / 4), q = t - r * (F / 4);
+        const float* src = a.feat;
+        if (r < nv) src = a.feat + (size_t)a.order[r0 + r] * F + 4 * q;
+        cp_async16(&S.stage_f[buf][r * F + 4 * q], src, r < nv ? 16 : 0);
+    }
+    if (threadIdx.x < TB) {
+        const int r = threadIdx.x;
+        const double* src = a.tgt;
+        if (r < nv) src = a.tgt + 2 * (size_t)a.order[r0 + r];
+        cp_async16(&S.stage_t[buf][2 * r], src, r < nv ? 16 : 0);
+    }
+    cp_async_commit();
+}
+
+// One tile: rows [0, nv) of the staged buffer `buf`; accumulates into g.
+template <int TB>
+__device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, double inv_b) {
+    constexpr int RPW = TB / NW;  // rows per warp in the row-parallel phases
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+    // ---- P0: staged fp32 -> fp64 tile
+    for (int t = tid; t < TB * F; t += NT) S.x[t] = (double)S.stage_f[buf][t];
+    if (tid < 2 * TB) S.tgt[tid] = S.stage_t[buf][tid];
     __syncthreads();
 
-    // ---- F1: lanes <-> j (lane, lane+32), warp <-> rows 8w..8w+7
+    // ---- F1: lanes <-> j (lane, lane+32), warp <-> rows
     {
-        double acc[8][2];
+        double acc[RPW][2];
         const double bA = S.b0[lane], bB = S.b0[lane + 32];
 #pragma unroll
-        for (int rr = 0; rr < 8; ++rr) { acc[rr][0] = bA; acc[rr][1] = bB; }
-        const double* xb = S.x + (8 * w) * F;
+        for (int rr = 0; rr < RPW; ++rr) { acc[rr][0] = bA; acc[rr][1] = bB; }
+        const double* xb = S.x + (RPW * w) * F;
 #pragma unroll 2
         for (int i = 0; i < F; i += 2) {
             const double wA0 = S.w0t[i * H1 + lane], wB0 = S.w0t[i * H1 + lane + 32];
             const double wA1 = S.w0t[(i + 1) * H1 + lane], wB1 = S.w0t[(i + 1) * H1 + lane + 32];
 #pragma unroll
-            for (int rr = 0; rr < 8; ++rr) {
+            for (int rr = 0; rr < RPW; ++rr) {
                 const double2 xv = *reinterpret_cast<const double2*>(xb + rr * F + i);
+                // fp32 x fp32 products are exact in fp64, so DFMA == mul-then-add
                 acc[rr][0] = fma(wA0, xv.x, acc[rr][0]);
                 acc[rr][1] = fma(wB0, xv.x, acc[rr][1]);
                 acc[rr][0] = fma(wA1, xv.y, acc[rr][0]);
@@ -182,8 +260,8 @@ __device__ void train_tile(TrainSmem& S, GradRegs& g, const float* __restrict__ 
             }
         }
 #pragma unroll
-        for (int rr = 0; rr < 8; ++rr) {
-            double* hr = S.h1 + (8 * w + rr) * H1;
+        for (int rr = 0; rr < RPW; ++rr) {
+            double* hr = S.h1 + (RPW * w + rr) * H1;
             hr[lane] = acc[rr][0] > 0.0 ? acc[rr][0] : 0.0;
             hr[lane + 32] = acc[rr][1] > 0.0 ? acc[rr][1] : 0.0;
         }
@@ -192,54 +270,51 @@ __device__ void train_tile(TrainSmem& S, GradRegs& g, const float* __restrict__ 
 
     // ---- F2: lanes <-> k, warp <-> rows
     {
-        double acc[8];
+        double acc[RPW];
         const double b = S.b1[lane];
 #pragma unroll
-        for (int rr = 0; rr < 8; ++rr) acc[rr] = b;
-        const double* hb = S.h1 + (8 * w) * H1;
-#pragma unroll 2
+        for (int rr = 0; rr < RPW; ++rr) acc[rr] = b;
+        const double* hb = S.h1 + (RPW * w) * H1;
+#pragma unroll 4
         for (int j = 0; j < H1; j += 2) {
             const double w0 = S.w1t[j * H2 + lane], w1 = S.w1t[(j + 1) * H2 + lane];
 #pragma unroll
-            for (int rr = 0; rr < 8; ++rr) {
+            for (int rr = 0; rr < RPW; ++rr) {
                 const double2 hv = *reinterpret_cast<const double2*>(hb + rr * H1 + j);
                 acc[rr] = madd_rn(acc[rr], w0, hv.x);
                 acc[rr] = madd_rn(acc[rr], w1, hv.y);
             }
         }
 #pragma unroll
-        for (int rr = 0; rr < 8; ++rr)
-            S.h2[(8 * w + rr) * H2 + lane] = acc[rr] > 0.0 ? acc[rr] : 0.0;
+        for (int rr = 0; rr < RPW; ++rr)
+            S.h2[(RPW * w + rr) * H2 + lane] = acc[rr] > 0.0 ? acc[rr] : 0.0;
     }
     __syncthreads();
 
-    // ---- F3 + loss + d3: one thread per row
-    if (tid < TB) {
-        const int r = tid;
-        double l0 = S.b2[0], l1 = S.b2[1];
+    // ---- F3: thread (r, a) computes logit a, then softmax/KL/d3 with its pair
+    if (tid < 2 * TB) {
+        const int r = tid >> 1, a = tid & 1;
+        double l = S.b2[a];
         const double* h = S.h2 + r * H2;
+        const double* wr = S.w2 + a * H2;
 #pragma unroll 8
-        for (int k = 0; k < H2; ++k) {
-            l0 = madd_rn(l0, S.w2[k], h[k]);
-            l1 = madd_rn(l1, S.w2[H2 + k], h[k]);
-        }
-        const double m = fmax(l0, l1);
-        const double e0 = exp(__dsub_rn(l0, m)), e1 = exp(__dsub_rn(l1, m));
-        const double s = __dadd_rn(e0, e1);
-        const double p[2] = {__ddiv_rn(e0, s), __ddiv_rn(e1, s)};
-        double lr[2], loss = 0.0;
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-            const double pc = clampp(p[a]);
-            const double tc = clampp(S.tgt[2 * r + a]);
-            lr[a] = log(__ddiv_rn(pc, tc));
-            loss = madd_rn(loss, pc, lr[a]);
-        }
+        for (int k = 0; k < H2; ++k) l = madd_rn(l, wr[k], h[k]);
+        const double lo = __shfl_xor_sync(0xffffffffu, l, 1);
+        const double l0 = a ? lo : l, l1 = a ? l : lo;
+        const double m = l0 < l1 ? l1 : l0;  // std::max(l0, l1)
+        const double e = exp(__dsub_rn(l, m));
+        const double eo = __shfl_xor_sync(0xffffffffu, e, 1);
+        const double s = a ? __dadd_rn(eo, e) : __dadd_rn(e, eo);  // e0 + e1
+        const double p = __ddiv_rn(e, s);
+        const double pc = clampp(p);
+        const double tc = clampp(S.tgt[2 * r + a]);
+        const double lr = log(__ddiv_rn(pc, tc));
+        const double term = __dmul_rn(pc, lr);
+        const double to = __shfl_xor_sync(0xffffffffu, term, 1);
+        const double loss = __dadd_rn(__dadd_rn(0.0, a ? to : term), a ? term : to);
         const bool valid = r < nv;
-        S.kl[r] = valid ? loss : 0.0;
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-            S.d3[2 * r + a] = valid ? __dmul_rn(__dmul_rn(p[a], __dsub_rn(lr[a], loss)), inv_b) : 0.0;
+        if (a == 0) S.kl[r] = valid ? loss : 0.0;
+        S.d3[2 * r + a] = valid ? __dmul_rn(__dmul_rn(p, __dsub_rn(lr, loss)), inv_b) : 0.0;
     }
     __syncthreads();
 
@@ -247,34 +322,31 @@ __device__ void train_tile(TrainSmem& S, GradRegs& g, const float* __restrict__ 
     {
         const double w20 = S.w2[lane], w21 = S.w2[H2 + lane];
 #pragma unroll
-        for (int rr = 0; rr < 8; ++rr) {
-            const int r = 8 * w + rr;
+        for (int rr = 0; rr < RPW; ++rr) {
+            const int r = RPW * w + rr;
             double d = madd_rn(0.0, S.d3[2 * r], w20);
             d = madd_rn(d, S.d3[2 * r + 1], w21);
             S.d2[r * H2 + lane] = S.h2[r * H2 + lane] <= 0.0 ? 0.0 : d;
         }
     }
-    if (tid == 0) {
-        for (int r = 0; r < nv; ++r) g.loss = __dadd_rn(g.loss, S.kl[r]);
-    }
     __syncthreads();
 
-    // ---- B2: d1[r][j] = sum_k d2[r][k] w1[k][j], masked by h1 > 0
-    //      (+ gw1/gb1/gw2/gb2 accumulation, which only needs d2/d3/h1/h2)
+    // ---- B2: d1[r][j] = sum_k d2[r][k] w1[k][j] (masked by h1 > 0)
+    //      + gw1 / gb1 / gw2 / gb2 / KL-sum accumulation (need only d2, d3, h1, h2)
     {
-        double acc[8][2];
+        double acc[RPW][2];
 #pragma unroll
-        for (int rr = 0; rr < 8; ++rr) acc[rr][0] = acc[rr][1] = 0.0;
-        const double* db = S.d2 + (8 * w) * H2;
-#pragma unroll 2
+        for (int rr = 0; rr < RPW; ++rr) acc[rr][0] = acc[rr][1] = 0.0;
+        const double* db = S.d2 + (RPW * w) * H2;
+#pragma unroll 4
         for (int k = 0; k < H2; k += 2) {
             const double wA0 = S.w1[k * H1 + lane], wB0 = S.w1[k * H1 + lane + 32];
             const double wA1 = S.w1[(k + 1) * H1 + lane], wB1 = S.w1[(k + 1) * H1 + lane + 32];
 #pragma unroll
-            for (int rr = 0; rr < 8; ++rr) {
+            for (int rr = 0; rr < RPW; ++rr) {
                 const double2 dv = *reinterpret_cast<const double2*>(db + rr * H2 + k);
-                // rows with d2 == 0 add a signed zero: a no-op, matching the
-                // reference's `continue` (policy.cpp:247)
+                // a zero d2 adds a signed zero: a no-op, matching the reference's
+                // `continue` on zero rows (policy.cpp:247)
                 acc[rr][0] = madd_rn(acc[rr][0], dv.x, wA0);
                 acc[rr][1] = madd_rn(acc[rr][1], dv.x, wB0);
                 acc[rr][0] = madd_rn(acc[rr][0], dv.y, wA1);
@@ -282,120 +354,131 @@ __device__ void train_tile(TrainSmem& S, GradRegs& g, const float* __restrict__ 
             }
         }
 #pragma unroll
-        for (int rr = 0; rr < 8; ++rr) {
-            const int r = 8 * w + rr;
+        for (int rr = 0; rr < RPW; ++rr) {
+            const int r = RPW * w + rr;
             S.d1[r * H1 + lane] = S.h1[r * H1 + lane] <= 0.0 ? 0.0 : acc[rr][0];
             S.d1[r * H1 + lane + 32] = S.h1[r * H1 + lane + 32] <= 0.0 ? 0.0 : acc[rr][1];
         }
-        // gw1[4w+kk][lane+32q] += d2[r][4w+kk] * h1[r][lane+32q], r in batch order
+        // gw1[2w+kk][lane+32q] += d2[r][2w+kk] * h1[r][lane+32q], r in batch order
+#pragma unroll 4
         for (int r = 0; r < nv; ++r) {
-            const double2 da = *reinterpret_cast<const double2*>(S.d2 + r * H2 + 4 * w);
-            const double2 dbv = *reinterpret_cast<const double2*>(S.d2 + r * H2 + 4 * w + 2);
+            const double2 dk = *reinterpret_cast<const double2*>(S.d2 + r * H2 + 2 * w);
             const double hA = S.h1[r * H1 + lane], hB = S.h1[r * H1 + lane + 32];
-            g.g1[0][0] = madd_rn(g.g1[0][0], da.x, hA);
-            g.g1[0][1] = madd_rn(g.g1[0][1], da.x, hB);
-            g.g1[1][0] = madd_rn(g.g1[1][0], da.y, hA);
-            g.g1[1][1] = madd_rn(g.g1[1][1], da.y, hB);
-            g.g1[2][0] = madd_rn(g.g1[2][0], dbv.x, hA);
-            g.g1[2][1] = madd_rn(g.g1[2][1], dbv.x, hB);
-            g.g1[3][0] = madd_rn(g.g1[3][0], dbv.y, hA);
-            g.g1[3][1] = madd_rn(g.g1[3][1], dbv.y, hB);
+            g.g1[0][0] = madd_rn(g.g1[0][0], dk.x, hA);
+            g.g1[0][1] = madd_rn(g.g1[0][1], dk.x, hB);
+            g.g1[1][0] = madd_rn(g.g1[1][0], dk.y, hA);
+            g.g1[1][1] = madd_rn(g.g1[1][1], dk.y, hB);
         }
-        if (tid >= 64 && tid < 96) {
-            const int k = tid - 64;
+        if (tid >= 320 && tid < 352) {
+            const int k = tid - 320;
             for (int r = 0; r < nv; ++r) g.gx = __dadd_rn(g.gx, S.d2[r * H2 + k]);
-        } else if (tid >= 96 && tid < 160) {
-            const int a = (tid - 96) / H2, k = (tid - 96) % H2;
+        } else if (tid >= 352 && tid < 416) {
+            const int a = (tid - 352) >> 5, k = (tid - 352) & 31;
             for (int r = 0; r < nv; ++r) g.gx = madd_rn(g.gx, S.d3[2 * r + a], S.h2[r * H2 + k]);
-        } else if (tid >= 160 && tid < 162) {
-            const int a = tid - 160;
+        } else if (tid >= 416 && tid < 418) {
+            const int a = tid - 416;
             for (int r = 0; r < nv; ++r) g.gx = __dadd_rn(g.gx, S.d3[2 * r + a]);
+        } else if (tid == NT - 1) {
+            for (int r = 0; r < nv; ++r) g.loss = __dadd_rn(g.loss, S.kl[r]);
         }
     }
     __syncthreads();
 
-    // ---- G0: gw0[8w+jj][i] += d1[r][8w+jj] * x[r][i]; gb0[j] += d1[r][j]
+    // ---- G0: gw0[4w+jj][i] += d1[r][4w+jj] * x[r][i]; gb0[j] += d1[r][j]
     {
         const bool two = lane < F - 32;
+        const int ib = two ? lane + 32 : lane;
+#pragma unroll 2
         for (int r = 0; r < nv; ++r) {
-            const double* dr = S.d1 + r * H1 + 8 * w;
-            const double2 d01 = *reinterpret_cast<const double2*>(dr);
-            const double2 d23 = *reinterpret_cast<const double2*>(dr + 2);
-            const double2 d45 = *reinterpret_cast<const double2*>(dr + 4);
-            const double2 d67 = *reinterpret_cast<const double2*>(dr + 6);
-            const double dv[8] = {d01.x, d01.y, d23.x, d23.y, d45.x, d45.y, d67.x, d67.y};
+            const double2 d01 = *reinterpret_cast<const double2*>(S.d1 + r * H1 + 4 * w);
+            const double2 d23 = *reinterpret_cast<const double2*>(S.d1 + r * H1 + 4 * w + 2);
             const double xa = S.x[r * F + lane];
-            const double xb = two ? S.x[r * F + lane + 32] : 0.0;
+            const double xb = S.x[r * F + ib];
+            g.g0a[0] = madd_rn(g.g0a[0], d01.x, xa);
+            g.g0a[1] = madd_rn(g.g0a[1], d01.y, xa);
+            g.g0a[2] = madd_rn(g.g0a[2], d23.x, xa);
+            g.g0a[3] = madd_rn(g.g0a[3], d23.y, xa);
+            g.g0b[0] = madd_rn(g.g0b[0], d01.x, xb);
+            g.g0b[1] = madd_rn(g.g0b[1], d01.y, xb);
+            g.g0b[2] = madd_rn(g.g0b[2], d23.x, xb);
+            g.g0b[3] = madd_rn(g.g0b[3], d23.y, xb);
+        }
+        if (tid >= 256 && tid < 320) {
+            const int j = tid - 256;
+            for (int r = 0; r < nv; ++r) g.gx = __dadd_rn(g.gx, S.d1[r * H1 + j]);
+        }
+    }
+    __syncthreads();
+}
+
+// Deterministic fixed-shape warp sum of per-lane partials (lane 0 holds it).
+__device__ __forceinline__ double warp_tree_sum(double v) {
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                g.g0a[jj] = madd_rn(g.g0a[jj], dv[jj], xa);
-                g.g0b[jj] = madd_rn(g.g0b[jj], dv[jj], xb);
-            }
-        }
-        if (tid < 64) {
-            for (int r = 0; r < nv; ++r) g.gx = __dadd_rn(g.gx, S.d1[r * H1 + tid]);
-        }
-    }
-    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;
 }
 
-// Records of step `step` handled by CTA `cta` of `nctas` on rank `rank` of
-// `nranks`: equal contiguous slices of the global batch, rank-major.
-__device__ __forceinline__ void step_slice(size_t n, int batch, long step, int rank, int nranks,
-                                           int cta, int nctas, size_t& lo, size_t& hi,
-                                           size_t& nb) {
-    const size_t start = (size_t)step * (size_t)batch;
-    const size_t stop = min(n, start + (size_t)batch);
-    nb = stop - start;
-    const size_t per_rank = (nb + nranks - 1) / nranks;
-    const size_t r_lo = min(stop, start + (size_t)rank * per_rank);
-    const size_t r_hi = min(stop, r_lo + per_rank);
-    const size_t m = r_hi - r_lo;
-    const size_t per_cta = (m + nctas - 1) / nctas;
-    lo = min(r_hi, r_lo + (size_t)cta * per_cta);
-    hi = min(r_hi, lo + per_cta);
+// Sum of partials[c][p] over c < G with a fixed association (per-lane strided
+// left fold, then a shuffle-down tree). Called by a full warp; lane 0 result.
+__device__ __forceinline__ double reduce_over_ctas(const double* __restrict__ partials, int G,
+                                                   int p, int lane) {
+    double v = 0.0;
+    for (int c = lane; c < G; c += 32) v = __dadd_rn(v, __ldcg(partials + (size_t)c * (NP + 1) + p));
+    return warp_tree_sum(v);
 }
 
-__device__ void run_step_tiles(TrainSmem& S, GradRegs& g, const TrainArgs& a, long step,
-                               size_t& nb) {
-    size_t lo, hi;
-    step_slice(a.n, a.batch, step, a.rank, a.nranks, blockIdx.x, gridDim.x, lo, hi, nb);
-    const double inv_b = 1.0 / (double)nb;  // batch_kl_gradient's 1/|b| (global batch)
-    for (size_t r0 = lo; r0 < hi; r0 += TB) {
-        const int nv = (int)min((size_t)TB, hi - r0);
-        train_tile(S, g, a.feat, a.tgt, a.order, r0, nv, inv_b);
-    }
-}
-
-__global__ void __launch_bounds__(TRAIN_BLOCK, 1) train_epoch_kernel(TrainArgs a) {
+template <int TB>
+__global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TrainSmem& S = *reinterpret_cast<TrainSmem*>(smem_raw);
+    TrainSmem<TB>& S = *reinterpret_cast<TrainSmem<TB>*>(smem_raw);
     if (*a.diverged_epoch >= 0) return;  // an earlier epoch diverged
-    load_train_weights(S, a.params);
-    __syncthreads();
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int G = gridDim.x;
+    const bool single = G == 1;
+    const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
+
+    // first tile's records in flight while the weights load
+    long pf_step = 0;
+    size_t pf_r0 = (size_t)-1;
+    int pf_nv = 0;
+    bool have_next = next_tile<TB>(a, n_steps, pf_step, pf_r0, pf_nv);
+    int buf = 0;
+    if (have_next) prefetch_tile<TB>(S, buf, a, pf_r0, pf_nv);
+    load_train_weights(S, a.params, false);
     GradRegs g;
     zero_grads(g);
     unsigned int bar_target = 0;
-    const bool single = gridDim.x == 1;
     double epoch_total = 0.0;
-    const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
+    __syncthreads();
 
     for (long step = 0; step < n_steps; ++step) {
-        size_t nb;
-        run_step_tiles(S, g, a, step, nb);
+        size_t lo, hi, nb;
+        step_slice(a, step, blockIdx.x, G, lo, hi, nb);
+        const double inv_b = 1.0 / (double)nb;  // batch_kl_gradient's 1/|b| (global batch)
+        for (size_t r0 = lo; r0 < hi; r0 += TB) {
+            const int nv = (int)min((size_t)TB, hi - r0);
+            cp_async_wait_all();
+            __syncthreads();
+            const int cur = buf;
+            buf ^= 1;
+            // queue the following tile (this step or a later one)
+            have_next = next_tile<TB>(a, n_steps, pf_step, pf_r0, pf_nv);
+            if (have_next) prefetch_tile<TB>(S, buf, a, pf_r0, pf_nv);
+            train_tile<TB>(S, g, cur, nv, inv_b);
+        }
         if (single) {
             // loss = (sum of per-record KL, batch order) / |b|  (policy.cpp:194-201)
-            if (threadIdx.x == 0) {
+            if (tid == NT - 1) {
                 const double loss = __ddiv_rn(g.loss, (double)nb);
                 S.scal[1] = loss;
                 S.scal[2] = isfinite(loss) ? 0.0 : 1.0;
             }
             __syncthreads();
             if (S.scal[2] != 0.0) {
-                if (threadIdx.x == 0) *a.diverged_epoch = a.epoch;
+                if (tid == 0) *a.diverged_epoch = a.epoch;
                 break;
             }
-            if (threadIdx.x == 0) epoch_total = madd_rn(epoch_total, S.scal[1], (double)nb);
+            if (tid == 0) epoch_total = madd_rn(epoch_total, S.scal[1], (double)nb);
             const double lr = a.lr;
             for_each_owned(g, [&](int p, double& acc) {
                 const double wv = get_smem_param(S, p);
@@ -407,71 +490,83 @@ __global__ void __launch_bounds__(TRAIN_BLOCK, 1) train_epoch_kernel(TrainArgs a
             // ---- per-CTA partials -> deterministic cross-CTA reduction
             double* part = a.partials + (size_t)blockIdx.x * (NP + 1);
             for_each_owned(g, [&](int p, double& acc) { part[p] = acc; });
-            if (threadIdx.x == 0) part[NP] = g.loss;
+            if (tid == NT - 1) part[NP] = g.loss;
             grid_barrier(a.bar, bar_target);
-            if (threadIdx.x == 0) {
-                double tot = 0.0;
-                for (int c = 0; c < (int)gridDim.x; ++c)
-                    tot = __dadd_rn(tot, __ldcg(a.partials + (size_t)c * (NP + 1) + NP));
-                const double loss = __ddiv_rn(tot, (double)nb);
-                S.scal[1] = loss;
-                S.scal[2] = isfinite(loss) ? 0.0 : 1.0;
+            if (w == 0) {
+                const double tot = reduce_over_ctas(a.partials, G, NP, lane);
+                if (lane == 0) {
+                    const double loss = __ddiv_rn(tot, (double)nb);
+                    S.scal[1] = loss;
+                    S.scal[2] = isfinite(loss) ? 0.0 : 1.0;
+                }
             }
             __syncthreads();
             if (S.scal[2] != 0.0) {
-                if (blockIdx.x == 0 && threadIdx.x == 0) *a.diverged_epoch = a.epoch;
+                if (blockIdx.x == 0 && tid == 0) *a.diverged_epoch = a.epoch;
                 break;
             }
-            if (threadIdx.x == 0) epoch_total = madd_rn(epoch_total, S.scal[1], (double)nb);
-            const int chunk = (NP + gridDim.x - 1) / gridDim.x;
+            if (tid == 0) epoch_total = madd_rn(epoch_total, S.scal[1], (double)nb);
+            const int chunk = (NP + G - 1) / G;
             const int p_lo = blockIdx.x * chunk, p_hi = min(NP, p_lo + chunk);
-            for (int p = p_lo + threadIdx.x; p < p_hi; p += blockDim.x) {
-                double gs = 0.0;
-                for (int c = 0; c < (int)gridDim.x; ++c)
-                    gs = __dadd_rn(gs, __ldcg(a.partials + (size_t)c * (NP + 1) + p));
-                const double wv = get_smem_param(S, p);
-                a.params[p] = __double2float_rn(__dsub_rn(wv, __dmul_rn(a.lr, gs)));
+            for (int p = p_lo + w; p < p_hi; p += NW) {
+                const double gs = reduce_over_ctas(a.partials, G, p, lane);
+                if (lane == 0) {
+                    const double wv = get_smem_param(S, p);
+                    a.params[p] = __double2float_rn(__dsub_rn(wv, __dmul_rn(a.lr, gs)));
+                }
             }
             grid_barrier(a.bar, bar_target);
-            for (int t = threadIdx.x; t < NP; t += blockDim.x) set_smem_param(S, t, (double)__ldcg(a.params + t));
+            load_train_weights(S, a.params, true);
             zero_grads(g);
             __syncthreads();
         }
     }
+    cp_async_wait_all();
     // epoch loss = total / n (policy.cpp:334); params back to global
-    if (blockIdx.x == 0 && threadIdx.x == 0 && *a.diverged_epoch < 0)
+    if (blockIdx.x == 0 && tid == 0 && *a.diverged_epoch < 0)
         a.epoch_loss[a.epoch] = __ddiv_rn(epoch_total, (double)a.n);
     if (single) {
         __syncthreads();
-        for (int t = threadIdx.x; t < NP; t += blockDim.x) a.params[t] = (float)get_smem_param(S, t);
+        for (int t = tid; t < NP; t += NT) a.params[t] = (float)get_smem_param(S, t);
     }
 }
 
 // Data-parallel path: one step's per-CTA partials only.
-__global__ void __launch_bounds__(TRAIN_BLOCK, 1) train_partial_kernel(TrainArgs a, long step) {
+template <int TB>
+__global__ void __launch_bounds__(NT, 1) train_partial_kernel(TrainArgs a, long step) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TrainSmem& S = *reinterpret_cast<TrainSmem*>(smem_raw);
+    TrainSmem<TB>& S = *reinterpret_cast<TrainSmem<TB>*>(smem_raw);
     if (*a.diverged_epoch >= 0) return;
-    load_train_weights(S, a.params);
-    __syncthreads();
+    size_t lo, hi, nb;
+    step_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
+    if (hi > lo) prefetch_tile<TB>(S, 0, a, lo, (int)min((size_t)TB, hi - lo));
+    load_train_weights(S, a.params, false);
     GradRegs g;
     zero_grads(g);
-    size_t nb;
-    run_step_tiles(S, g, a, step, nb);
+    const double inv_b = 1.0 / (double)nb;
+    int buf = 0;
+    for (size_t r0 = lo; r0 < hi; r0 += TB) {
+        const int nv = (int)min((size_t)TB, hi - r0);
+        cp_async_wait_all();
+        __syncthreads();
+        const int cur = buf;
+        buf ^= 1;
+        if (r0 + TB < hi) prefetch_tile<TB>(S, buf, a, r0 + TB, (int)min((size_t)TB, hi - r0 - TB));
+        train_tile<TB>(S, g, cur, nv, inv_b);
+    }
     double* part = a.partials + (size_t)blockIdx.x * (NP + 1);
     for_each_owned(g, [&](int p, double& acc) { part[p] = acc; });
-    if (threadIdx.x == 0) part[NP] = g.loss;
+    if (threadIdx.x == NT - 1) part[NP] = g.loss;
 }
 
-// Sum per-CTA partials in CTA order into red[NP+1].
+// Sum per-CTA partials (fixed tree) into red[NP+1]; one warp per entry.
 __global__ void reduce_partials_kernel(const double* __restrict__ partials, int nctas,
                                        double* __restrict__ red, const int* __restrict__ diverged) {
     if (*diverged >= 0) return;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (p > NP) return;
-    double s = 0.0;
-    for (int c = 0; c < nctas; ++c) s = __dadd_rn(s, partials[(size_t)c * (NP + 1) + p]);
-    red[p] = s;
+    const double s = reduce_over_ctas(partials, nctas, p, threadIdx.x & 31);
+    if ((threadIdx.x & 31) == 0) red[p] = s;
 }
 
 // SGD update from an (all-reduced) gradient + loss total; tracks epoch loss.
@@ -495,21 +590,31 @@ __global__ void finish_epoch_kernel(const double* __restrict__ epoch_acc, size_t
     out[epoch] = __ddiv_rn(*epoch_acc, (double)n);
 }
 
-// ------------------------------------------------------ loss / gradient API
 // batch_kl_loss / batch_kl_gradient for one batch (rows 0..n-1 in order):
-// identical code path as fit with order = identity and a single step.
-__global__ void __launch_bounds__(TRAIN_BLOCK, 1)
+// fit's tile code with order = identity and a single 1-CTA step.
+__global__ void __launch_bounds__(NT, 1)
 batch_grad_kernel(TrainArgs a, double* __restrict__ grad_out, double* __restrict__ loss_out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TrainSmem& S = *reinterpret_cast<TrainSmem*>(smem_raw);
-    load_train_weights(S, a.params);
-    __syncthreads();
+    TrainSmem<64>& S = *reinterpret_cast<TrainSmem<64>*>(smem_raw);
+    load_train_weights(S, a.params, false);
     GradRegs g;
     zero_grads(g);
-    size_t nb;
-    run_step_tiles(S, g, a, 0, nb);
+    const double inv_b = 1.0 / (double)a.n;
+    for (size_t r0 = 0; r0 < a.n; r0 += 64) {
+        const int nv = (int)min((size_t)64, a.n - r0);
+        __syncthreads();
+        prefetch_tile<64>(S, 0, a, r0, nv);
+        cp_async_wait_all();
+        __syncthreads();
+        train_tile<64>(S, g, 0, nv, inv_b);
+    }
     for_each_owned(g, [&](int p, double& acc) { grad_out[p] = acc; });
-    if (threadIdx.x == 0) *loss_out = __ddiv_rn(g.loss, (double)nb);
+    if (threadIdx.x == NT - 1) *loss_out = __ddiv_rn(g.loss, (double)a.n);
 }
+
+template __global__ void train_epoch_kernel<32>(TrainArgs);
+template __global__ void train_epoch_kernel<64>(TrainArgs);
+template __global__ void train_partial_kernel<32>(TrainArgs, long);
+template __global__ void train_partial_kernel<64>(TrainArgs, long);
 
 }  // namespace gbxcu

@@ -9,8 +9,7 @@ namespace gbxcu {
 
 constexpr int FWD_BLOCK = 256;    // fast inference: 8 warps, one state per thread
 constexpr int EXACT_BLOCK = 128;  // exact fp64 inference
-constexpr int TB = 64;            // train: records per CTA tile
-constexpr int TRAIN_BLOCK = 256;  // train: 8 warps
+constexpr int TRAIN_BLOCK = 512;  // train: 16 warps; tiles of 32 or 64 records
 constexpr int SHUF_BLOCK = 256;
 constexpr int AGG_BLOCK = 256;    // aggregation: 8 warps = 8 apps per CTA
 
@@ -63,7 +62,9 @@ __global__ void fwd_exact_kernel(const float* params, const float* feat, size_t 
 size_t fast_smem_bytes();
 size_t exact_smem_bytes();
 
+template <int TB>
 __global__ void train_epoch_kernel(TrainArgs a);
+template <int TB>
 __global__ void train_partial_kernel(TrainArgs a, long step);
 __global__ void reduce_partials_kernel(const double* partials, int nctas, double* red,
                                        const int* diverged);
@@ -72,7 +73,7 @@ __global__ void apply_update_kernel(float* params, const double* red, double lr,
 __global__ void finish_epoch_kernel(const double* epoch_acc, size_t n, int epoch,
                                     const int* diverged, double* out);
 __global__ void batch_grad_kernel(TrainArgs a, double* grad_out, double* loss_out);
-size_t train_smem_bytes();
+size_t train_smem_bytes(int tb);
 
 __global__ void iota_kernel(uint32_t* order, size_t n);
 __global__ void shuffle_epoch_kernel(uint32_t* order, uint32_t n, uint64_t seed_e, int* resv,
