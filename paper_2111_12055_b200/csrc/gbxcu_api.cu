@@ -79,7 +79,8 @@ struct gbxcu_ctx {
     std::mutex mu;
     // scratch
     DevBuf params, feat, tgt, probs, actions, recheck, counters, flags;
-    DevBuf order, resv, list_a, list_b, partials, red, bar, diverged, epoch_loss, epoch_acc;
+    DevBuf order, order2, partials, red, bar, diverged, epoch_loss, epoch_acc;
+    DevBuf sh_jp, sh_head, sh_nxt, sh_succ, sh_root, sh_root2, sh_flags;
     DevBuf seg_off, seg_seed, grad, scalar;
     DevBuf s_app_pipe, s_pipe_slot, s_slot_shader, s_slot_frac, s_pipe_wt, s_shader_lat, s_app_f64;
     DevBuf s_actions, s_run_seed, s_rows, s_samples, h_lower, h_count, h_nbins;
@@ -197,33 +198,40 @@ void train_grid(gbxcu_ctx* c, const gbxcu_train_cfg* cfg, size_t n, int& G, int&
     tb = per_cta <= 32 ? 32 : 64;
 }
 
+// One epoch's Fisher-Yates pass: order -> order2, then the two are swapped.
 int shuffle_epoch(gbxcu_ctx* c, size_t n, uint64_t seed, int epoch, cudaStream_t st) {
     if (n < 2) return GBXCU_OK;
-    const uint64_t seed_e = derive_seed3(seed, 0x5F17u, (uint64_t)epoch);
-    uint32_t* order = c->order.as<uint32_t>();
-    uint32_t nn = (uint32_t)n;
-    int* resv = c->resv.as<int>();
-    uint32_t* la = c->list_a.as<uint32_t>();
-    uint32_t* lb = c->list_b.as<uint32_t>();
-    unsigned int* cnt = c->counters.as<unsigned int>();
-    unsigned int* bar = c->bar.as<unsigned int>();
-    const int* div = c->diverged.as<int>();
-    CK(cudaMemsetAsync(c->bar.p, 0, 16, st));
-    void* args[] = {&order, &nn, (void*)&seed_e, &resv, &la, &lb, &cnt, &bar, (void*)&div};
+    ShuffleArgs s{};
+    s.in = c->order.as<uint32_t>();
+    s.out = c->order2.as<uint32_t>();
+    s.n = (uint32_t)n;
+    s.seed_e = derive_seed3(seed, 0x5F17u, (uint64_t)epoch);
+    s.jp = c->sh_jp.as<uint32_t>();
+    s.head = c->sh_head.as<uint32_t>();
+    s.nxt = c->sh_nxt.as<uint32_t>();
+    s.succ = c->sh_succ.as<uint32_t>();
+    s.root = c->sh_root.as<uint32_t>();
+    s.root2 = c->sh_root2.as<uint32_t>();
+    s.flags = c->sh_flags.as<unsigned int>();
+    s.fg0 = c->sh_flags.as<uint32_t>() + 64;
+    s.bar = c->sh_flags.as<unsigned int>() + 72;
+    s.diverged = c->diverged.as<int>();
+    CK(cudaMemsetAsync(c->sh_flags.p, 0, 80 * sizeof(uint32_t), st));
+    void* args[] = {&s};
     CK(cudaLaunchCooperativeKernel((const void*)shuffle_epoch_kernel, c->shuffle_grid, SHUF_BLOCK,
                                    args, 0, st));
+    std::swap(c->order.p, c->order2.p);
+    std::swap(c->order.cap, c->order2.cap);
     return check_launch(c, "shuffle_epoch_kernel");
 }
 
 int prepare_order(gbxcu_ctx* c, size_t n, cudaStream_t st) {
-    RET(c->order.ensure(n * 4));
-    RET(c->resv.ensure(n * 4));
-    RET(c->list_a.ensure(n * 4));
-    RET(c->list_b.ensure(n * 4));
-    RET(c->counters.ensure(16));
+    for (DevBuf* b : {&c->order, &c->order2, &c->sh_jp, &c->sh_head, &c->sh_nxt, &c->sh_succ,
+                      &c->sh_root, &c->sh_root2})
+        RET(b->ensure(n * 4));
+    RET(c->sh_flags.ensure(80 * sizeof(uint32_t)));
     RET(c->bar.ensure(16));
     RET(c->diverged.ensure(16));
-    CK(cudaMemsetAsync(c->resv.p, 0xFF, n * 4, st));
     CK(cudaMemsetAsync(c->diverged.p, 0xFF, 16, st));
     iota_kernel<<<std::max(1, std::min<int>((int)((n + 255) / 256), c->num_sms * 8)), 256, 0, st>>>(
         c->order.as<uint32_t>(), n);
@@ -261,6 +269,7 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
 
     for (int e = 0; e < cfg->epochs; ++e) {
         RET(shuffle_epoch(c, n, cfg->seed, e, st));
+        a.order = c->order.as<uint32_t>();  // the pass output (buffers ping-pong)
         a.epoch = e;
         if (c->nranks == 1) {
             CK(cudaMemsetAsync(c->bar.as<unsigned int>() + 2, 0, 8, st));

@@ -1,23 +1,30 @@
 // k_shuffle.cu — device replay of fit's per-epoch in-place Fisher-Yates
-// shuffle (proj/src/policy.cpp:303-314).
+// shuffle (proj/src/policy.cpp:303-314), in closed form.
 //
 // The sequential loop `for i = n..2: j = next_below(i); swap(order[i-1],
-// order[j])` is a fixed sequence of swaps S_p = (p, j_p), p = n-1..1, whose
-// partners depend only on the stream: j_p = umulhi(draw_{n-p}, p+1) with
-// draw_k = fin(seed + k*gamma) (SplitMix64 skip-ahead). Swaps on disjoint
-// positions commute, so S can be applied out of order as long as, per
-// position, swaps land in sequence order. Deterministic reservations
-// (Shun, Blelloch, Fineman, Gibbons, SODA'15): every pending swap
-// atomicMax-reserves its two positions with priority p (earlier swap = larger
-// p); a swap commits when it holds both reservations. The earliest pending
-// swap always commits, the committed set touches disjoint positions, and the
-// result equals the sequential shuffle exactly. Dependence depth is O(log n)
-// w.h.p., so an epoch's permutation takes a few dozen rounds of one
-// persistent cooperative kernel instead of n serial host steps.
+// order[j])` is the swap sequence S_p = (p, j_p), p = n-1 down to 1, whose
+// partners depend only on the SplitMix64 stream: j_p = umulhi(draw_{n-p}, p+1)
+// with draw_k = fin(seed + k*gamma) (skip-ahead). Group swaps by target:
+// list(x) = {q : j_q = x} sorted ascending. Position p >= 1 is never touched
+// after S_p, and S_p moves into p whatever sat at j_p just before it; the last
+// swap to write j_p before S_p is succ(p), the next-larger element of
+// list(j_p). What S_q writes into j_q is V(q) = the value at q just before S_q,
+// which in turn was written by fg(q) = min{q' > q : j_q' = q}. Hence
+//   V(q)     = A[root(q)],  root = end of the chain q -> fg(q) -> fg(fg(q)) ...
+//   final[p] = succ(p) ? V(succ(p)) : A[j_p]            (p >= 1)
+//   final[0] = fg(0)   ? V(fg(0))   : A[0]
+// Chains are O(log n) long, so pointer jumping needs ~6 rounds (measured:
+// 6 at n = 1e6 and 1e7; buckets hold <= ~21 swaps), instead of the O(log n)
+// *dependence depth* of ~50 rounds a reservation-based replay needs. The
+// result equals the sequential shuffle exactly (tests/test_gpu_parity.py
+// compares against the reference at 1e5 and 1e6).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace gbxcu {
+
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr int LOCAL_BUCKET = 32;
 
 __global__ void iota_kernel(uint32_t* __restrict__ order, size_t n) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -29,82 +36,93 @@ __device__ __forceinline__ uint32_t partner(uint64_t seed_e, uint32_t n, uint32_
     return (uint32_t)below_of(sm_draw(seed_e, (uint64_t)(n - p)), (uint64_t)p + 1);
 }
 
-// resv[] must be all -1 on entry and is left all -1 on exit.
-// counters[0..1]: list lengths (counters[0] = 0 on entry), counters[2] scratch.
 __global__ void __launch_bounds__(SHUF_BLOCK)
-shuffle_epoch_kernel(uint32_t* __restrict__ order, uint32_t n, uint64_t seed_e,
-                     int* __restrict__ resv, uint32_t* __restrict__ list_a,
-                     uint32_t* __restrict__ list_b, unsigned int* __restrict__ counters,
-                     unsigned int* __restrict__ bar, const int* __restrict__ diverged) {
-    if (*diverged >= 0 || n < 2) return;
+shuffle_epoch_kernel(ShuffleArgs s) {
+    if (*s.diverged >= 0) return;
     unsigned int target = 0;
+    const uint32_t n = s.n;
     const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t nthr = (size_t)gridDim.x * blockDim.x;
-    const int lane = threadIdx.x & 31;
 
-    // pending list: every swap position p = 1..n-1
-    for (size_t t = tid; t < (size_t)n - 1; t += nthr) list_a[t] = (uint32_t)(t + 1);
-    if (tid == 0) {
-        counters[0] = n - 1;
-        counters[1] = 0;
+    // 1: empty buckets
+    for (size_t x = tid; x < n; x += nthr) __stcg(s.head + x, NONE);
+    grid_barrier(s.bar, target);
+
+    // 2: partners + bucket lists (arbitrary order inside a bucket)
+    for (size_t p = tid + 1; p < n; p += nthr) {
+        const uint32_t j = partner(s.seed_e, n, (uint32_t)p);
+        __stcg(s.jp + p, j);
+        __stcg(s.nxt + p, atomicExch(s.head + j, (uint32_t)p));
     }
-    grid_barrier(bar, target);
+    grid_barrier(s.bar, target);
 
-    uint32_t* cur = list_a;
-    uint32_t* nxt = list_b;
-    int ci = 0;
-    for (;;) {
-        const unsigned int cnt = __ldcg(counters + ci);
-        if (cnt == 0) break;
-        // reserve
-        for (size_t t = tid; t < cnt; t += nthr) {
-            const uint32_t p = __ldcg(cur + t);
-            const uint32_t j = partner(seed_e, n, p);
-            atomicMax(resv + p, (int)p);
-            if (j != p) atomicMax(resv + j, (int)p);
+    // 3: sort each bucket -> succ() of its members, fg(x), chain start
+    for (size_t x = tid; x < n; x += nthr) {
+        uint32_t loc[LOCAL_BUCKET];
+        int m = 0;
+        bool overflow = false;
+        for (uint32_t e = __ldcg(s.head + x); e != NONE; e = __ldcg(s.nxt + e)) {
+            if (m < LOCAL_BUCKET) loc[m] = e;
+            else overflow = true;
+            ++m;
         }
-        grid_barrier(bar, target);
-        // commit or carry over
-        const size_t cnt_round = ((cnt + nthr - 1) / nthr) * nthr;  // warp-uniform trip count
-        for (size_t t = tid; t < cnt_round; t += nthr) {
-            bool carry = false;
-            uint32_t p = 0;
-            if (t < cnt) {
-                p = __ldcg(cur + t);
-                const uint32_t j = partner(seed_e, n, p);
-                const bool win = __ldcg(resv + p) == (int)p && __ldcg(resv + j) == (int)p;
-                if (win) {
-                    if (j != p) {
-                        const uint32_t a = __ldcg(order + p), b = __ldcg(order + j);
-                        __stcg(order + p, b);
-                        __stcg(order + j, a);
-                    }
-                } else {
-                    carry = true;
-                }
+        uint32_t fg = NONE;
+        if (!overflow) {
+            for (int a = 1; a < m; ++a) {  // insertion sort, ascending
+                const uint32_t v = loc[a];
+                int b = a - 1;
+                while (b >= 0 && loc[b] > v) { loc[b + 1] = loc[b]; --b; }
+                loc[b + 1] = v;
             }
-            const unsigned int m = __ballot_sync(0xffffffffu, carry);
-            if (m) {
-                unsigned int base = 0;
-                if (lane == 0) base = atomicAdd(counters + (ci ^ 1), __popc(m));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (carry) __stcg(nxt + base + __popc(m & ((1u << lane) - 1)), p);
+            for (int k = 0; k < m; ++k) {
+                __stcg(s.succ + loc[k], k + 1 < m ? loc[k + 1] : NONE);
+                if (fg == NONE && loc[k] > x) fg = loc[k];
+            }
+        } else {
+            // rare (> 32 swaps aimed at one slot): quadratic walk of the list
+            for (uint32_t e = __ldcg(s.head + x); e != NONE; e = __ldcg(s.nxt + e)) {
+                uint32_t nx = NONE;
+                for (uint32_t f = __ldcg(s.head + x); f != NONE; f = __ldcg(s.nxt + f))
+                    if (f > e && f < nx) nx = f;
+                __stcg(s.succ + e, nx);
+                if (e > x && e < fg) fg = e;
             }
         }
-        grid_barrier(bar, target);
-        // release reservations of this round
-        for (size_t t = tid; t < cnt; t += nthr) {
-            const uint32_t p = __ldcg(cur + t);
-            const uint32_t j = partner(seed_e, n, p);
-            __stcg(resv + p, -1);
-            __stcg(resv + j, -1);
+        __stcg(s.root + x, fg != NONE ? fg : (uint32_t)x);
+        if (x == 0) __stcg(s.fg0, fg);
+    }
+    grid_barrier(s.bar, target);
+
+    // 4: pointer jumping root(q) <- root(root(q)) until no change
+    uint32_t* cur = s.root;
+    uint32_t* nxt = s.root2;
+    for (int round = 0; round < 64; ++round) {
+        bool changed = false;
+        for (size_t q = tid; q < n; q += nthr) {
+            const uint32_t r = __ldcg(cur + q);
+            const uint32_t r2 = __ldcg(cur + r);
+            __stcg(nxt + q, r2);
+            changed |= r2 != r;
         }
-        if (tid == 0) counters[ci] = 0;
-        grid_barrier(bar, target);
-        uint32_t* tmp = cur;
+        if (__syncthreads_or(changed) && threadIdx.x == 0) atomicOr(s.flags + round, 1u);
+        grid_barrier(s.bar, target);
+        uint32_t* t = cur;
         cur = nxt;
-        nxt = tmp;
-        ci ^= 1;
+        nxt = t;
+        if (__ldcg(s.flags + round) == 0) break;
+    }
+
+    // 5: final permutation
+    const uint32_t fg0 = __ldcg(s.fg0);
+    for (size_t p = tid; p < n; p += nthr) {
+        uint32_t src;
+        if (p == 0) {
+            src = fg0 != NONE ? __ldcg(cur + fg0) : 0u;
+        } else {
+            const uint32_t sc = __ldcg(s.succ + p);
+            src = sc != NONE ? __ldcg(cur + sc) : __ldcg(s.jp + p);
+        }
+        s.out[p] = __ldg(s.in + src);
     }
 }
 

@@ -39,12 +39,18 @@ namespace gbxcu {
 constexpr int NT = TRAIN_BLOCK;  // 512 threads
 constexpr int NW = NT / 32;      // 16 warps
 
+// Weight replicas are row-major with odd row strides (in 8-byte words), so a
+// warp reading one column across 32 rows, or one row across 32 columns, hits
+// 32 distinct banks: no transposed copies are needed and the owner-computes
+// SGD update writes conflict-free.
+constexpr int W0S = F + 1;   // 45
+constexpr int W1S = H1 + 1;  // 65
+
 template <int TB>
 struct TrainSmem {
-    double w0t[F * H1];  // [i][j]
-    double w1[H2 * H1];  // [k][j]
-    double w1t[H1 * H2]; // [j][k]
-    double w2[A * H2];   // [a][k]
+    double w0[H1 * W0S];  // [j][i], stride 45
+    double w1[H2 * W1S];  // [k][j], stride 65
+    double w2[A * H2];    // [a][k]
     double b0[H1];
     double b1[H2];
     double b2[A];
@@ -86,12 +92,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ------------------------------------------------------------ weights
 template <int TB>
 __device__ __forceinline__ void set_smem_param(TrainSmem<TB>& S, int p, double v) {
-    if (p < OFF_B0) { const int j = p / F, i = p - j * F; S.w0t[i * H1 + j] = v; }
+    if (p < OFF_B0) { const int j = p / F, i = p - j * F; S.w0[j * W0S + i] = v; }
     else if (p < OFF_W1) S.b0[p - OFF_B0] = v;
     else if (p < OFF_B1) {
         const int t = p - OFF_W1, k = t >> 6, j = t & 63;
-        S.w1[t] = v;
-        S.w1t[j * H2 + k] = v;
+        S.w1[k * W1S + j] = v;
     } else if (p < OFF_W2) S.b1[p - OFF_B1] = v;
     else if (p < OFF_B2) S.w2[p - OFF_W2] = v;
     else S.b2[p - OFF_B2] = v;
@@ -99,9 +104,9 @@ __device__ __forceinline__ void set_smem_param(TrainSmem<TB>& S, int p, double v
 
 template <int TB>
 __device__ __forceinline__ double get_smem_param(const TrainSmem<TB>& S, int p) {
-    if (p < OFF_B0) { const int j = p / F, i = p - j * F; return S.w0t[i * H1 + j]; }
+    if (p < OFF_B0) { const int j = p / F, i = p - j * F; return S.w0[j * W0S + i]; }
     if (p < OFF_W1) return S.b0[p - OFF_B0];
-    if (p < OFF_B1) return S.w1[p - OFF_W1];
+    if (p < OFF_B1) { const int t = p - OFF_W1; return S.w1[(t >> 6) * W1S + (t & 63)]; }
     if (p < OFF_W2) return S.b1[p - OFF_B1];
     if (p < OFF_B2) return S.w2[p - OFF_W2];
     return S.b2[p - OFF_B2];
@@ -169,20 +174,51 @@ __device__ __forceinline__ void for_each_owned(GradRegs& g, Fn fn) {
     else if (tid >= 416 && tid < 418) fn(OFF_B2 + tid - 416, g.gx);
 }
 
+// w = float(double(w) - lr * g) (policy.cpp:329-331), kept as fp64 in smem.
+__device__ __forceinline__ double sgd(double w, double lr, double g) {
+    return (double)__double2float_rn(__dsub_rn(w, __dmul_rn(lr, g)));
+}
+
+// 1-CTA step: every owner updates its parameters in the smem replica directly.
+template <int TB>
+__device__ __forceinline__ void sgd_update_owned(TrainSmem<TB>& S, const GradRegs& g, double lr) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+        double* row = S.w0 + (4 * w + jj) * W0S;
+        row[lane] = sgd(row[lane], lr, g.g0a[jj]);
+        if (lane < F - 32) row[lane + 32] = sgd(row[lane + 32], lr, g.g0b[jj]);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+        double* row = S.w1 + (2 * w + kk) * W1S;
+        row[lane] = sgd(row[lane], lr, g.g1[kk][0]);
+        row[lane + 32] = sgd(row[lane + 32], lr, g.g1[kk][1]);
+    }
+    if (tid >= 256 && tid < 320) S.b0[tid - 256] = sgd(S.b0[tid - 256], lr, g.gx);
+    else if (tid >= 320 && tid < 352) S.b1[tid - 320] = sgd(S.b1[tid - 320], lr, g.gx);
+    else if (tid >= 352 && tid < 416) S.w2[tid - 352] = sgd(S.w2[tid - 352], lr, g.gx);
+    else if (tid >= 416 && tid < 418) S.b2[tid - 416] = sgd(S.b2[tid - 416], lr, g.gx);
+}
+
 // ------------------------------------------------------------ tiling
 // Records of step `step` handled by CTA `cta` of `nctas` on rank `rank`:
 // equal contiguous slices of the global batch, rank-major then CTA-major.
+// n < 2^31 and batch < 2^31 are validated on the host, so 32-bit math suffices.
 __device__ __forceinline__ void step_slice(const TrainArgs& a, long step, int cta, int nctas,
                                            size_t& lo, size_t& hi, size_t& nb) {
-    const size_t start = (size_t)step * (size_t)a.batch;
-    const size_t stop = min(a.n, start + (size_t)a.batch);
-    nb = stop - start;
-    const size_t per_rank = (nb + a.nranks - 1) / a.nranks;
-    const size_t r_lo = min(stop, start + (size_t)a.rank * per_rank);
-    const size_t r_hi = min(stop, r_lo + per_rank);
-    const size_t per_cta = (r_hi - r_lo + nctas - 1) / nctas;
-    lo = min(r_hi, r_lo + (size_t)cta * per_cta);
-    hi = min(r_hi, lo + per_cta);
+    const uint32_t n = (uint32_t)a.n, batch = (uint32_t)a.batch;
+    const uint32_t start = (uint32_t)step * batch;
+    const uint32_t stop = min(n, start + batch);
+    const uint32_t nbu = stop - start;
+    const uint32_t per_rank = (nbu + a.nranks - 1) / (uint32_t)a.nranks;
+    const uint32_t r_lo = min(stop, start + (uint32_t)a.rank * per_rank);
+    const uint32_t r_hi = min(stop, r_lo + per_rank);
+    const uint32_t per_cta = (r_hi - r_lo + nctas - 1) / (uint32_t)nctas;
+    const uint32_t l = min(r_hi, r_lo + (uint32_t)cta * per_cta);
+    lo = l;
+    hi = min(r_hi, l + per_cta);
+    nb = nbu;
 }
 
 // Next tile of this CTA after (step, r0) within steps < step_end. r0 == SIZE_MAX
@@ -247,8 +283,9 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
         const double* xb = S.x + (RPW * w) * F;
 #pragma unroll 2
         for (int i = 0; i < F; i += 2) {
-            const double wA0 = S.w0t[i * H1 + lane], wB0 = S.w0t[i * H1 + lane + 32];
-            const double wA1 = S.w0t[(i + 1) * H1 + lane], wB1 = S.w0t[(i + 1) * H1 + lane + 32];
+            const double* wa = S.w0 + lane * W0S + i;
+            const double* wb = S.w0 + (lane + 32) * W0S + i;
+            const double wA0 = wa[0], wB0 = wb[0], wA1 = wa[1], wB1 = wb[1];
 #pragma unroll
             for (int rr = 0; rr < RPW; ++rr) {
                 const double2 xv = *reinterpret_cast<const double2*>(xb + rr * F + i);
@@ -277,7 +314,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
         const double* hb = S.h1 + (RPW * w) * H1;
 #pragma unroll 4
         for (int j = 0; j < H1; j += 2) {
-            const double w0 = S.w1t[j * H2 + lane], w1 = S.w1t[(j + 1) * H2 + lane];
+            const double w0 = S.w1[lane * W1S + j], w1 = S.w1[lane * W1S + j + 1];
 #pragma unroll
             for (int rr = 0; rr < RPW; ++rr) {
                 const double2 hv = *reinterpret_cast<const double2*>(hb + rr * H1 + j);
@@ -314,19 +351,18 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
         const double loss = __dadd_rn(__dadd_rn(0.0, a ? to : term), a ? term : to);
         const bool valid = r < nv;
         if (a == 0) S.kl[r] = valid ? loss : 0.0;
-        S.d3[2 * r + a] = valid ? __dmul_rn(__dmul_rn(p, __dsub_rn(lr, loss)), inv_b) : 0.0;
-    }
-    __syncthreads();
-
-    // ---- B1: d2 = (0 + d3_0 w2_0k) + d3_1 w2_1k, masked by h2 > 0
-    {
-        const double w20 = S.w2[lane], w21 = S.w2[H2 + lane];
+        const double d3 = valid ? __dmul_rn(__dmul_rn(p, __dsub_rn(lr, loss)), inv_b) : 0.0;
+        S.d3[2 * r + a] = d3;
+        // ---- B1 (same pair): d2[r][k] = (0 + d3_0 w2_0k) + d3_1 w2_1k, masked by
+        //      h2 > 0; thread a covers k in [16a, 16a+16)
+        const double d3o = __shfl_xor_sync(0xffffffffu, d3, 1);
+        const double d30 = a ? d3o : d3, d31 = a ? d3 : d3o;
 #pragma unroll
-        for (int rr = 0; rr < RPW; ++rr) {
-            const int r = RPW * w + rr;
-            double d = madd_rn(0.0, S.d3[2 * r], w20);
-            d = madd_rn(d, S.d3[2 * r + 1], w21);
-            S.d2[r * H2 + lane] = S.h2[r * H2 + lane] <= 0.0 ? 0.0 : d;
+        for (int kk = 0; kk < H2 / 2; ++kk) {
+            const int k = (H2 / 2) * a + kk;
+            double d = madd_rn(0.0, d30, S.w2[k]);
+            d = madd_rn(d, d31, S.w2[H2 + k]);
+            S.d2[r * H2 + k] = h[k] <= 0.0 ? 0.0 : d;
         }
     }
     __syncthreads();
@@ -340,8 +376,9 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
         const double* db = S.d2 + (RPW * w) * H2;
 #pragma unroll 4
         for (int k = 0; k < H2; k += 2) {
-            const double wA0 = S.w1[k * H1 + lane], wB0 = S.w1[k * H1 + lane + 32];
-            const double wA1 = S.w1[(k + 1) * H1 + lane], wB1 = S.w1[(k + 1) * H1 + lane + 32];
+            const double* wk = S.w1 + k * W1S;
+            const double wA0 = wk[lane], wB0 = wk[lane + 32];
+            const double wA1 = wk[W1S + lane], wB1 = wk[W1S + lane + 32];
 #pragma unroll
             for (int rr = 0; rr < RPW; ++rr) {
                 const double2 dv = *reinterpret_cast<const double2*>(db + rr * H2 + k);
@@ -479,11 +516,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
                 break;
             }
             if (tid == 0) epoch_total = madd_rn(epoch_total, S.scal[1], (double)nb);
-            const double lr = a.lr;
-            for_each_owned(g, [&](int p, double& acc) {
-                const double wv = get_smem_param(S, p);
-                set_smem_param(S, p, (double)__double2float_rn(__dsub_rn(wv, __dmul_rn(lr, acc))));
-            });
+            sgd_update_owned(S, g, a.lr);
             zero_grads(g);
             __syncthreads();
         } else {

@@ -76,9 +76,18 @@ __global__ void batch_grad_kernel(TrainArgs a, double* grad_out, double* loss_ou
 size_t train_smem_bytes(int tb);
 
 __global__ void iota_kernel(uint32_t* order, size_t n);
-__global__ void shuffle_epoch_kernel(uint32_t* order, uint32_t n, uint64_t seed_e, int* resv,
-                                     uint32_t* list_a, uint32_t* list_b, unsigned int* counters,
-                                     unsigned int* bar, const int* diverged);
+struct ShuffleArgs {
+    const uint32_t* in;   // order before this epoch's pass
+    uint32_t* out;        // order after it
+    uint32_t n;
+    uint64_t seed_e;      // derive_seed({seed, 0x5F17, epoch})
+    uint32_t *jp, *head, *nxt, *succ, *root, *root2;  // [n] scratch each
+    uint32_t* fg0;
+    unsigned int* flags;  // [64] zeroed: "pointer jumping changed something in round r"
+    unsigned int* bar;    // grid-barrier counter, zeroed
+    const int* diverged;
+};
+__global__ void shuffle_epoch_kernel(ShuffleArgs s);
 
 __global__ void aggregate_kernel(AggArgs a);
 __global__ void histogram_kernel(const double* rows, int stride, size_t n, double* lower,
