@@ -5,7 +5,7 @@
  * path only as C++ functions of the static library `gbx`; it has no FFI or
  * plugin registry. Each entry point below replaces one of those functions
  * (cited per declaration) with a batched, device-executed equivalent. The C++
- * drop-in mirror (paper_2111_12055_b200/include/gbx/*.hpp) and the Python
+ * drop-in mirror (headers under paper_2111_12055_b200/include/gbx/) and the Python
  * binding (paper_2111_12055_b200/__init__.py, ctypes) both bind exactly this
  * surface; INTEGRATION.md shows the binding a maintainer adds.
  *

@@ -1,0 +1,368 @@
+// gbx_policy.cpp — the policy API of the drop-in, executed on the B200.
+//
+// fit, batch_kl_loss, batch_kl_gradient, PolicyNet::init/forward and the
+// select_* functions marshal into one flat fp32 parameter vector plus
+// [n][44] fp32 features / [n][2] fp64 targets and call libgbxcu (C ABI,
+// include/gbxcu.h). Status codes map back onto the reference's exception
+// types (proj/include/gbx/policy.hpp:16-31). Only the GBXP byte format and the
+// scalar kl_loss stay on the host (no batched work behind them).
+#include <zlib.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <string>
+
+#include "gbx/policy.hpp"
+#include "gbxcu.h"
+
+namespace gbx {
+
+namespace {
+
+// ------------------------------------------------------------ device context
+std::mutex g_mu;
+gbxcu_ctx* g_ctx = nullptr;
+int g_device = -1;
+
+gbxcu_ctx* ctx() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_ctx) {
+        int dev = g_device;
+        if (dev < 0) {
+            const char* env = std::getenv("GBX_DEVICE");
+            dev = env ? std::atoi(env) : 0;
+        }
+        if (gbxcu_create(dev, &g_ctx) != GBXCU_OK) {
+            g_ctx = nullptr;
+            throw std::runtime_error(std::string("gbx: no usable B200 (no CPU fallback): ") +
+                                     gbxcu_last_error());
+        }
+    }
+    return g_ctx;
+}
+
+void check(int rc, int diverged_epoch = -1) {
+    if (rc == GBXCU_OK) return;
+    const std::string msg = gbxcu_last_error();
+    switch (rc) {
+        case GBXCU_EINVAL:
+        case GBXCU_ENONFINITE: throw ValidationError(msg);
+        case GBXCU_EDIVERGED: throw TrainingDivergedError(diverged_epoch, msg);
+        case GBXCU_ETEMPERATURE: throw InvalidTemperatureError(msg);
+        default: throw std::runtime_error("gbxcu: " + msg);
+    }
+}
+
+constexpr double kProbClamp = 1e-7;
+
+double clamp_prob(double p) { return std::min(std::max(p, kProbClamp), 1.0 - kProbClamp); }
+
+void flatten_states(std::span<const ShaderState> s, std::vector<float>& out) {
+    out.resize(s.size() * kFeatureCount);
+    for (std::size_t r = 0; r < s.size(); ++r)
+        std::memcpy(out.data() + r * kFeatureCount, s[r].features.data(), sizeof(float) * kFeatureCount);
+}
+
+void flatten_records(std::span<const std::pair<ShaderState, EmpiricalPolicy>> d,
+                     std::vector<float>& feat, std::vector<double>& tgt) {
+    feat.resize(d.size() * kFeatureCount);
+    tgt.resize(d.size() * 2);
+    for (std::size_t r = 0; r < d.size(); ++r) {
+        std::memcpy(feat.data() + r * kFeatureCount, d[r].first.features.data(),
+                    sizeof(float) * kFeatureCount);
+        tgt[2 * r] = d[r].second.prob[0];
+        tgt[2 * r + 1] = d[r].second.prob[1];
+    }
+}
+
+}  // namespace
+
+void set_device(int device) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_ctx) {
+        gbxcu_destroy(g_ctx);
+        g_ctx = nullptr;
+    }
+    g_device = device;
+}
+
+// --------------------------------------------------------------- PolicyNet
+PolicyNet PolicyNet::zeros() {
+    PolicyNet net;
+    for (int l = 0; l < kPolicyLayers; ++l) {
+        net.weights[l].assign(static_cast<std::size_t>(kPolicyDims[l]) * kPolicyDims[l + 1], 0.0f);
+        net.biases[l].assign(static_cast<std::size_t>(kPolicyDims[l + 1]), 0.0f);
+    }
+    return net;
+}
+
+std::vector<float> PolicyNet::flat() const {
+    std::vector<float> p;
+    p.reserve(kPolicyParamCount);
+    for (int l = 0; l < kPolicyLayers; ++l) {
+        p.insert(p.end(), weights[l].begin(), weights[l].end());
+        p.insert(p.end(), biases[l].begin(), biases[l].end());
+    }
+    return p;
+}
+
+PolicyNet PolicyNet::from_flat(std::span<const float> p) {
+    if (p.size() != kPolicyParamCount) throw ValidationError("flat parameter vector has wrong size");
+    PolicyNet net = zeros();
+    std::size_t o = 0;
+    for (int l = 0; l < kPolicyLayers; ++l) {
+        for (auto& w : net.weights[l]) w = p[o++];
+        for (auto& b : net.biases[l]) b = p[o++];
+    }
+    return net;
+}
+
+PolicyNet PolicyNet::init(std::uint64_t seed) {
+    std::vector<float> p(kPolicyParamCount);
+    check(gbxcu_policy_init(ctx(), seed, p.data()));
+    return from_flat(p);
+}
+
+std::array<double, 2> PolicyNet::forward(const ShaderState& s) const {
+    for (float f : s.features)
+        if (!std::isfinite(f)) throw ValidationError("non-finite feature in shader state");
+    const auto p = flat();
+    std::array<double, 2> probs{};
+    check(gbxcu_forward(ctx(), p.data(), s.features.data(), 1, probs.data(), nullptr,
+                        GBXCU_FWD_EXACT));
+    return probs;
+}
+
+std::size_t PolicyNet::param_count() const {
+    std::size_t n = 0;
+    for (int l = 0; l < kPolicyLayers; ++l) n += weights[l].size() + biases[l].size();
+    return n;
+}
+
+float PolicyNet::param(std::size_t i) const {
+    for (int l = 0; l < kPolicyLayers; ++l) {
+        if (i < weights[l].size()) return weights[l][i];
+        i -= weights[l].size();
+        if (i < biases[l].size()) return biases[l][i];
+        i -= biases[l].size();
+    }
+    throw ValidationError("parameter index out of range");
+}
+
+void PolicyNet::set_param(std::size_t i, float v) {
+    for (int l = 0; l < kPolicyLayers; ++l) {
+        if (i < weights[l].size()) { weights[l][i] = v; return; }
+        i -= weights[l].size();
+        if (i < biases[l].size()) { biases[l][i] = v; return; }
+        i -= biases[l].size();
+    }
+    throw ValidationError("parameter index out of range");
+}
+
+// -------------------------------------------------------------- loss / grad
+double kl_loss(const std::array<double, 2>& predicted, const EmpiricalPolicy& target) {
+    double loss = 0.0;
+    for (int a = 0; a < 2; ++a) {
+        const double p = clamp_prob(predicted[a]);
+        loss += p * std::log(p / clamp_prob(target.prob[a]));
+    }
+    return loss;
+}
+
+double batch_kl_loss(const PolicyNet& net,
+                     std::span<const std::pair<ShaderState, EmpiricalPolicy>> batch) {
+    if (batch.empty()) return 0.0 / static_cast<double>(batch.size());  // reference: 0/0
+    std::vector<float> feat;
+    std::vector<double> tgt;
+    flatten_records(batch, feat, tgt);
+    const auto p = net.flat();
+    double loss = 0.0;
+    check(gbxcu_batch_kl_loss(ctx(), p.data(), feat.data(), tgt.data(), batch.size(), &loss));
+    return loss;
+}
+
+std::vector<double> batch_kl_gradient(const PolicyNet& net,
+                                      std::span<const std::pair<ShaderState, EmpiricalPolicy>> batch) {
+    std::vector<double> g(net.param_count(), 0.0);
+    if (batch.empty()) return g;
+    std::vector<float> feat;
+    std::vector<double> tgt;
+    flatten_records(batch, feat, tgt);
+    const auto p = net.flat();
+    check(gbxcu_batch_kl_gradient(ctx(), p.data(), feat.data(), tgt.data(), batch.size(), g.data()));
+    return g;
+}
+
+// ---------------------------------------------------------------------- fit
+void TrainConfig::validate() const {
+    if (!(learning_rate > 0.0)) throw ValidationError("learning rate must be positive");
+    if (epochs < 1) throw ValidationError("epochs must be >= 1");
+    if (batch_size < 1) throw ValidationError("batch size must be >= 1");
+    if (!(rho_min > 0.0) || !(rho0 >= rho_min))
+        throw ValidationError("temperature schedule requires rho0 >= rho_min > 0");
+    if (!(rho_decay > 0.0 && rho_decay <= 1.0)) throw ValidationError("rho decay must be in (0, 1]");
+}
+
+double TrainConfig::rho_at(int iteration) const {
+    return std::max(rho_min, rho0 * std::pow(rho_decay, iteration));
+}
+
+FitResult fit(PolicyNet& net, const PolicyDataset& dataset, const TrainConfig& cfg) {
+    cfg.validate();
+    if (dataset.empty()) throw ValidationError("fit requires a non-empty dataset");
+    std::vector<float> feat;
+    std::vector<double> tgt;
+    flatten_records(dataset, feat, tgt);
+    auto p = net.flat();
+    gbxcu_train_cfg c{cfg.learning_rate, cfg.epochs, cfg.batch_size, cfg.seed, 0, 0};
+    FitResult res;
+    res.epoch_loss.assign(cfg.epochs, 0.0);
+    int diverged = -1;
+    const int rc = gbxcu_fit(ctx(), p.data(), feat.data(), tgt.data(), dataset.size(), &c,
+                             res.epoch_loss.data(), &diverged);
+    if (rc == GBXCU_OK || rc == GBXCU_EDIVERGED) net = PolicyNet::from_flat(p);
+    if (rc == GBXCU_EDIVERGED)
+        throw TrainingDivergedError(diverged, "training loss became non-finite at epoch " +
+                                                  std::to_string(diverged));
+    check(rc);
+    return res;
+}
+
+// ---------------------------------------------------------------- actions
+Action select_greedy(const BehaviorPolicy& beh, const ShaderState& s) {
+    const auto probs = beh.forward(s);
+    return probs[1] >= probs[0] ? Action::Wave64 : Action::Wave32;
+}
+
+Action select_sample(const BehaviorPolicy& beh, const ShaderState& s, SplitMix64& rng) {
+    const auto probs = beh.forward(s);
+    return rng.next_unit() < probs[0] ? Action::Wave32 : Action::Wave64;
+}
+
+std::vector<std::array<double, 2>> forward_batch(const PolicyNet& net,
+                                                 std::span<const ShaderState> states) {
+    std::vector<std::array<double, 2>> out(states.size());
+    if (states.empty()) return out;
+    std::vector<float> feat;
+    flatten_states(states, feat);
+    const auto p = net.flat();
+    check(gbxcu_forward(ctx(), p.data(), feat.data(), states.size(), out.data()->data(), nullptr,
+                        GBXCU_FWD_EXACT));
+    return out;
+}
+
+std::vector<Action> select_greedy_batch(const BehaviorPolicy& beh,
+                                        std::span<const ShaderState> states) {
+    std::vector<Action> out(states.size());
+    if (states.empty()) return out;
+    std::vector<float> feat;
+    flatten_states(states, feat);
+    std::vector<std::uint8_t> act(states.size());
+    const auto p = beh.net.flat();
+    check(gbxcu_forward(ctx(), p.data(), feat.data(), states.size(), nullptr, act.data(),
+                        GBXCU_FWD_FAST));
+    for (std::size_t i = 0; i < act.size(); ++i) out[i] = act[i] ? Action::Wave64 : Action::Wave32;
+    return out;
+}
+
+// ------------------------------------------------------------------- GBXP
+namespace {
+
+constexpr char kMagic[4] = {'G', 'B', 'X', 'P'};
+constexpr std::uint16_t kFormat = 1;
+
+template <typename T>
+void put_le(std::vector<std::uint8_t>& o, T v) {
+    for (std::size_t b = 0; b < sizeof(T); ++b) o.push_back(static_cast<std::uint8_t>(v >> (8 * b)));
+}
+
+struct ByteReader {
+    std::span<const std::uint8_t> b;
+    std::size_t pos = 0;
+    std::span<const std::uint8_t> take(std::size_t n) {
+        if (pos + n > b.size()) throw PolicyFormatError("truncated policy file");
+        auto s = b.subspan(pos, n);
+        pos += n;
+        return s;
+    }
+    template <typename T>
+    T le() {
+        const auto s = take(sizeof(T));
+        T v = 0;
+        for (std::size_t i = 0; i < sizeof(T); ++i) v |= static_cast<T>(static_cast<T>(s[i]) << (8 * i));
+        return v;
+    }
+};
+
+}  // namespace
+
+std::vector<std::uint8_t> serialize_policy(const BehaviorPolicy& beh) {
+    std::vector<std::uint8_t> out(kMagic, kMagic + 4);
+    put_le<std::uint16_t>(out, kFormat);
+    out.push_back(static_cast<std::uint8_t>(kPolicyLayers));
+    for (int l = 0; l < kPolicyLayers; ++l) {
+        put_le<std::uint16_t>(out, static_cast<std::uint16_t>(kPolicyDims[l]));
+        put_le<std::uint16_t>(out, static_cast<std::uint16_t>(kPolicyDims[l + 1]));
+    }
+    const std::size_t start = out.size();
+    for (float v : beh.net.flat()) {
+        std::uint32_t u;
+        std::memcpy(&u, &v, 4);
+        put_le<std::uint32_t>(out, u);
+    }
+    put_le<std::uint32_t>(out, static_cast<std::uint32_t>(
+                                   crc32(0, out.data() + start, static_cast<uInt>(out.size() - start))));
+    put_le<std::uint32_t>(out, beh.version_tag);
+    put_le<std::uint64_t>(out, beh.source_checkin);
+    return out;
+}
+
+BehaviorPolicy deserialize_policy(std::span<const std::uint8_t> bytes) {
+    ByteReader r{bytes};
+    if (std::memcmp(r.take(4).data(), kMagic, 4) != 0) throw PolicyFormatError("not a GBXP policy file");
+    if (r.le<std::uint16_t>() != kFormat) throw PolicyFormatError("unsupported policy format version");
+    const int layers = r.le<std::uint8_t>();
+    if (layers != kPolicyLayers)
+        throw PolicySchemaError("expected 3 layers, found " + std::to_string(layers));
+    for (int l = 0; l < kPolicyLayers; ++l) {
+        const int in = r.le<std::uint16_t>(), out = r.le<std::uint16_t>();
+        if (in != kPolicyDims[l] || out != kPolicyDims[l + 1])
+            throw PolicySchemaError("layer " + std::to_string(l) + " has shape " + std::to_string(in) +
+                                    "x" + std::to_string(out));
+    }
+    const std::size_t start = r.pos;
+    std::vector<float> p(kPolicyParamCount);
+    for (auto& v : p) {
+        const std::uint32_t u = r.le<std::uint32_t>();
+        std::memcpy(&v, &u, 4);
+    }
+    const std::size_t end = r.pos;
+    const std::uint32_t stored = r.le<std::uint32_t>();
+    if (stored != static_cast<std::uint32_t>(crc32(0, bytes.data() + start, static_cast<uInt>(end - start))))
+        throw PolicyFormatError("policy payload checksum mismatch");
+    BehaviorPolicy beh;
+    beh.net = PolicyNet::from_flat(p);
+    beh.version_tag = r.le<std::uint32_t>();
+    beh.source_checkin = r.le<std::uint64_t>();
+    return beh;
+}
+
+void save_policy(const BehaviorPolicy& beh, const std::filesystem::path& path) {
+    const auto bytes = serialize_policy(beh);
+    std::ofstream os(path, std::ios::binary | std::ios::trunc);
+    if (!os) throw ValidationError("cannot open policy file for writing: " + path.string());
+    os.write(reinterpret_cast<const char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
+    if (!os) throw ValidationError("failed writing policy file: " + path.string());
+}
+
+BehaviorPolicy load_policy(const std::filesystem::path& path) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw ValidationError("cannot open policy file: " + path.string());
+    std::vector<std::uint8_t> bytes((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    return deserialize_policy(bytes);
+}
+
+}  // namespace gbx
