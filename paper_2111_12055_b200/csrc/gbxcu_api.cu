@@ -271,7 +271,7 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
         RET(shuffle_epoch(c, n, cfg->seed, e, st));
         a.order = c->order.as<uint32_t>();  // the pass output (buffers ping-pong)
         a.epoch = e;
-        if (c->nranks == 1) {
+        if (!c->comm) {
             CK(cudaMemsetAsync(c->bar.as<unsigned int>() + 2, 0, 8, st));
             void* args[] = {&a};
             const void* fn = tb == 32 ? (const void*)train_epoch_kernel<32>
@@ -570,11 +570,9 @@ int gbxcu_comm_init(gbxcu_ctx* c, const uint8_t id[GBXCU_COMM_ID_BYTES], int nra
         ncclCommDestroy(c->comm);
         c->comm = nullptr;
     }
-    if (nranks == 1) {
-        c->nranks = 1;
-        c->rank = 0;
-        return GBXCU_OK;
-    }
+    // nranks == 1 still builds a (trivial) communicator: fit then runs the
+    // data-parallel step sequence (partials -> reduce -> all-reduce -> update),
+    // which is how that path is exercised on a single-GPU box.
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     CKN(ncclCommInitRank(&c->comm, nranks, uid, rank));

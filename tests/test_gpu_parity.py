@@ -255,3 +255,20 @@ def test_histogram_edges(dev, orc, uplift):
     lo_o, cnt_o = orc.histogram(uplift)
     np.testing.assert_array_equal(lo, lo_o)
     np.testing.assert_array_equal(cnt, cnt_o)
+
+
+# ------------------------------------------------------- data-parallel path
+@pytest.mark.parametrize("batch", [64, 4096])
+def test_fit_data_parallel_step_path(orc, batch):
+    """One-rank NCCL communicator: fit runs the DP step sequence (per-CTA
+    partials -> fixed-tree reduce -> ncclAllReduce -> SGD update kernel)."""
+    d = gbx.Device(0)
+    d.comm_init(gbx.Device.comm_unique_id(), 1, 0)
+    f, t = orc.g1(23, 20_000)
+    p0 = orc.policy_init(4)
+    rc, p_ref, el_ref, _ = orc.fit(p0, f, t, 0.01, 2, batch, 8)
+    p, el = d.fit(p0, f, t, 0.01, 2, batch, 8)
+    assert ulps32(p, p_ref).max() <= 2
+    np.testing.assert_allclose(el, el_ref, rtol=1e-12)
+    d.comm_destroy()
+    d.close()
