@@ -136,21 +136,28 @@ __device__ void load_train_weights(TrainSmem<TB>& S, const float* __restrict__ p
 }
 
 // ------------------------------------------------- gradient ownership
-// warp w: gw0 rows j = 4w..4w+3 at columns i = lane (+ lane+32 if lane < 12),
-//         gw1 rows k = 2w, 2w+1 at columns j = lane, lane+32.
-// extras: tid 256..319 gb0[j], 320..351 gb1[k], 352..415 gw2[a][k],
-//         416..417 gb2[a]; tid NT-1 keeps the running KL sum.
+// gw0: lane owns columns j = lane, lane+32; warp w owns inputs i = 2w, 2w+1 and,
+//      for w < 12, i = 32 + w (44 = 2*16 + 12): 4 or 6 accumulators.
+// gw1: warp w owns rows k = 2w, 2w+1 at columns j = lane, lane+32.
+// gb0: warp 12 (one of the lighter warps) owns j = lane, lane+32.
+// extras (gx): tid 320..351 gb1[k], 352..415 gw2[a][k], 416..417 gb2[a];
+// tid NT-1 keeps the running KL sum.
 struct GradRegs {
-    double g0a[4], g0b[4];
+    double g0[3][2];  // [i-slot][j-slot]
     double g1[2][2];
+    double gb0[2];
     double gx;
     double loss;
 };
 
+__device__ __forceinline__ int g0_col(int w, int m) { return m < 2 ? 2 * w + m : 32 + w; }
+__device__ __forceinline__ int g0_slots(int w) { return w < F - 32 ? 3 : 2; }
+
 __device__ __forceinline__ void zero_grads(GradRegs& g) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) g.g0a[q] = g.g0b[q] = 0.0;
+    for (int m = 0; m < 3; ++m) g.g0[m][0] = g.g0[m][1] = 0.0;
     g.g1[0][0] = g.g1[0][1] = g.g1[1][0] = g.g1[1][1] = 0.0;
+    g.gb0[0] = g.gb0[1] = 0.0;
     g.gx = 0.0;
     g.loss = 0.0;
 }
@@ -159,17 +166,22 @@ template <typename Fn>
 __device__ __forceinline__ void for_each_owned(GradRegs& g, Fn fn) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-        const int j = 4 * w + jj;
-        fn(OFF_W0 + j * F + lane, g.g0a[jj]);
-        if (lane < F - 32) fn(OFF_W0 + j * F + lane + 32, g.g0b[jj]);
+    for (int m = 0; m < 3; ++m) {
+        if (m < g0_slots(w)) {
+            const int i = g0_col(w, m);
+            fn(OFF_W0 + lane * F + i, g.g0[m][0]);
+            fn(OFF_W0 + (lane + 32) * F + i, g.g0[m][1]);
+        }
     }
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk)
 #pragma unroll
         for (int q = 0; q < 2; ++q) fn(OFF_W1 + (2 * w + kk) * H1 + lane + 32 * q, g.g1[kk][q]);
-    if (tid >= 256 && tid < 320) fn(OFF_B0 + tid - 256, g.gx);
-    else if (tid >= 320 && tid < 352) fn(OFF_B1 + tid - 320, g.gx);
+    if (w == 12) {
+        fn(OFF_B0 + lane, g.gb0[0]);
+        fn(OFF_B0 + lane + 32, g.gb0[1]);
+    }
+    if (tid >= 320 && tid < 352) fn(OFF_B1 + tid - 320, g.gx);
     else if (tid >= 352 && tid < 416) fn(OFF_W2 + tid - 352, g.gx);
     else if (tid >= 416 && tid < 418) fn(OFF_B2 + tid - 416, g.gx);
 }
@@ -179,15 +191,20 @@ __device__ __forceinline__ double sgd(double w, double lr, double g) {
     return (double)__double2float_rn(__dsub_rn(w, __dmul_rn(lr, g)));
 }
 
-// 1-CTA step: every owner updates its parameters in the smem replica directly.
+// 1-CTA step: every owner updates its parameters in the smem replica directly
+// (w0 rows have odd stride 45, so the column-parallel writes are conflict-free).
 template <int TB>
 __device__ __forceinline__ void sgd_update_owned(TrainSmem<TB>& S, const GradRegs& g, double lr) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-        double* row = S.w0 + (4 * w + jj) * W0S;
-        row[lane] = sgd(row[lane], lr, g.g0a[jj]);
-        if (lane < F - 32) row[lane + 32] = sgd(row[lane + 32], lr, g.g0b[jj]);
+    for (int m = 0; m < 3; ++m) {
+        if (m < g0_slots(w)) {
+            const int i = g0_col(w, m);
+            double* a = S.w0 + lane * W0S + i;
+            double* b = S.w0 + (lane + 32) * W0S + i;
+            *a = sgd(*a, lr, g.g0[m][0]);
+            *b = sgd(*b, lr, g.g0[m][1]);
+        }
     }
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk) {
@@ -195,8 +212,11 @@ __device__ __forceinline__ void sgd_update_owned(TrainSmem<TB>& S, const GradReg
         row[lane] = sgd(row[lane], lr, g.g1[kk][0]);
         row[lane + 32] = sgd(row[lane + 32], lr, g.g1[kk][1]);
     }
-    if (tid >= 256 && tid < 320) S.b0[tid - 256] = sgd(S.b0[tid - 256], lr, g.gx);
-    else if (tid >= 320 && tid < 352) S.b1[tid - 320] = sgd(S.b1[tid - 320], lr, g.gx);
+    if (w == 12) {
+        S.b0[lane] = sgd(S.b0[lane], lr, g.gb0[0]);
+        S.b0[lane + 32] = sgd(S.b0[lane + 32], lr, g.gb0[1]);
+    }
+    if (tid >= 320 && tid < 352) S.b1[tid - 320] = sgd(S.b1[tid - 320], lr, g.gx);
     else if (tid >= 352 && tid < 416) S.w2[tid - 352] = sgd(S.w2[tid - 352], lr, g.gx);
     else if (tid >= 416 && tid < 418) S.b2[tid - 416] = sgd(S.b2[tid - 416], lr, g.gx);
 }
@@ -421,28 +441,28 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
     }
     __syncthreads();
 
-    // ---- G0: gw0[4w+jj][i] += d1[r][4w+jj] * x[r][i]; gb0[j] += d1[r][j]
+    // ---- G0: gw0[j][i] += d1[r][j] * x[r][i] (j = lane, lane+32; i = warp's
+    //      columns), gb0[j] += d1[r][j] on warp 12; records in batch order
     {
-        const bool two = lane < F - 32;
-        const int ib = two ? lane + 32 : lane;
+        const int i0 = 2 * w, i2 = 32 + w;
+        const bool three = w < F - 32;
 #pragma unroll 2
         for (int r = 0; r < nv; ++r) {
-            const double2 d01 = *reinterpret_cast<const double2*>(S.d1 + r * H1 + 4 * w);
-            const double2 d23 = *reinterpret_cast<const double2*>(S.d1 + r * H1 + 4 * w + 2);
-            const double xa = S.x[r * F + lane];
-            const double xb = S.x[r * F + ib];
-            g.g0a[0] = madd_rn(g.g0a[0], d01.x, xa);
-            g.g0a[1] = madd_rn(g.g0a[1], d01.y, xa);
-            g.g0a[2] = madd_rn(g.g0a[2], d23.x, xa);
-            g.g0a[3] = madd_rn(g.g0a[3], d23.y, xa);
-            g.g0b[0] = madd_rn(g.g0b[0], d01.x, xb);
-            g.g0b[1] = madd_rn(g.g0b[1], d01.y, xb);
-            g.g0b[2] = madd_rn(g.g0b[2], d23.x, xb);
-            g.g0b[3] = madd_rn(g.g0b[3], d23.y, xb);
-        }
-        if (tid >= 256 && tid < 320) {
-            const int j = tid - 256;
-            for (int r = 0; r < nv; ++r) g.gx = __dadd_rn(g.gx, S.d1[r * H1 + j]);
+            const double2 xp = *reinterpret_cast<const double2*>(S.x + r * F + i0);
+            const double da = S.d1[r * H1 + lane], db = S.d1[r * H1 + lane + 32];
+            g.g0[0][0] = madd_rn(g.g0[0][0], da, xp.x);
+            g.g0[0][1] = madd_rn(g.g0[0][1], db, xp.x);
+            g.g0[1][0] = madd_rn(g.g0[1][0], da, xp.y);
+            g.g0[1][1] = madd_rn(g.g0[1][1], db, xp.y);
+            if (three) {
+                const double x2 = S.x[r * F + i2];
+                g.g0[2][0] = madd_rn(g.g0[2][0], da, x2);
+                g.g0[2][1] = madd_rn(g.g0[2][1], db, x2);
+            }
+            if (w == 12) {
+                g.gb0[0] = __dadd_rn(g.gb0[0], da);
+                g.gb0[1] = __dadd_rn(g.gb0[1], db);
+            }
         }
     }
     __syncthreads();
