@@ -85,6 +85,7 @@ struct gbxcu_ctx {
     DevBuf s_app_pipe, s_pipe_slot, s_slot_shader, s_slot_frac, s_pipe_wt, s_shader_lat, s_app_f64;
     DevBuf s_actions, s_run_seed, s_rows, s_samples, h_lower, h_count, h_nbins;
     int shuffle_grid = 0;
+    int fast_per_sm = 1;
     // data parallel
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
@@ -146,7 +147,7 @@ int run_forward(gbxcu_ctx* c, const float* d_params, const float* d_feat, size_t
         RET(recheck.ensure(n * sizeof(uint32_t)));
         const size_t warps = (n + 31) / 32;
         const size_t blocks_needed = (warps + FWD_BLOCK / 32 - 1) / (FWD_BLOCK / 32);
-        const int grid = (int)std::min<size_t>(blocks_needed, (size_t)c->num_sms * 3);
+        const int grid = (int)std::min<size_t>(blocks_needed, (size_t)c->num_sms * c->fast_per_sm);
         fwd_fast_kernel<<<grid, FWD_BLOCK, fast_smem_bytes(), st>>>(
             d_params, d_feat, n, d_probs, d_actions, d_seg_off, nseg, d_seg_seed, eps,
             recheck.as<uint32_t>(), counters.as<unsigned int>(), flags.as<unsigned int>(), bits);
@@ -370,6 +371,9 @@ int gbxcu_create(int device, gbxcu_ctx** out) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, shuffle_epoch_kernel, SHUF_BLOCK, 0);
     c->shuffle_grid = std::max(1, std::min(per_sm, 4)) * c->num_sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_fast_kernel, FWD_BLOCK,
+                                                  fast_smem_bytes());
+    c->fast_per_sm = std::max(1, per_sm);
     *out = c;
     return GBXCU_OK;
 }

@@ -6,7 +6,7 @@ for b in ${BATCHES:-32 4096 65536}; do
   n=1000000; [ $b -le 64 ] && n=200000
   timeout 300 python bench.py --steps 3 --warmup 2 --batch $b --n $n --no-secondary --no-cpu-baseline > gpurun_out/bench_b$b.log 2>&1
 done
-${EXTRA:-true}
+eval "${EXTRA:-true}"
 tail -2 gpurun_out/pytest_quick.log
 for b in ${BATCHES:-32 4096 65536}; do grep -E '^\{' gpurun_out/bench_b$b.log | python -c "
 import json,sys
