@@ -198,6 +198,28 @@ int gbxcu_evaluate_dev(gbxcu_ctx* ctx, const gbxcu_dsuite* s, const float* d_par
                        int n_samples, uint64_t seed, uint8_t* d_actions, double* d_rows,
                        void* stream);
 
+/* ------------------------------------------------ wide MLP variant (C4) */
+/* 44 -> H -> H -> 2 policy (H multiple of 32, <= 1024) trained on the
+ * tcgen05 tensor cores in TF32 with fp32 accumulation (BASELINE.json config
+ * C4). Same algorithm as fit (shuffle, KL loss, analytic gradient, SGD),
+ * generalised over widths; the reference hard-codes 44-64-32-2
+ * (proj/include/gbx/policy.hpp:32-35), so parity is tolerance-based against
+ * the generic oracle. Parameters use the same flat serialization order:
+ * w0[H][44] b0[H] w1[H][H] b1[H] w2[2][H] b2[2]. */
+size_t gbxcu_wide_param_count(int hidden);
+int gbxcu_wide_init(gbxcu_ctx* ctx, int hidden, uint64_t seed, float* params_out);
+int gbxcu_wide_forward(gbxcu_ctx* ctx, int hidden, const float* params, const float* feat, size_t n,
+                       double* probs_out);
+int gbxcu_wide_fit(gbxcu_ctx* ctx, int hidden, float* params_inout, const float* feat,
+                   const double* tgt, size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out,
+                   int* diverged_epoch);
+int gbxcu_wide_fit_dev(gbxcu_ctx* ctx, int hidden, float* d_params, const float* d_feat,
+                       const double* d_tgt, size_t n, const gbxcu_train_cfg* cfg,
+                       double* epoch_loss_out, int* diverged_epoch, void* stream);
+/* D[M][N] = A[M][K] . B[N][K]^T through the same tcgen05 TF32 GEMM kernel
+ * (host buffers; K multiple of 4) — exposed for testing. */
+int gbxcu_tf32_gemm(gbxcu_ctx* ctx, int M, int N, int K, const float* A, const float* B, float* D);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,8 @@ EXPORTS = (
     "gbxcu_fit", "gbxcu_fit_dev", "gbxcu_fit_order", "gbxcu_comm_unique_id", "gbxcu_comm_init",
     "gbxcu_comm_destroy", "gbxcu_aggregate", "gbxcu_histogram", "gbxcu_suite_upload",
     "gbxcu_suite_free", "gbxcu_suite_features", "gbxcu_evaluate", "gbxcu_evaluate_dev",
+    "gbxcu_wide_param_count", "gbxcu_wide_init", "gbxcu_wide_forward", "gbxcu_wide_fit",
+    "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm",
 )
 
 _LIB = None
@@ -134,6 +136,15 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_evaluate.argtypes = [_vp, _vp, _f32p, C.c_int, _u64, _f64p, _vp, _vp, _vp, _sz,
                                  C.POINTER(_sz)]
     L.gbxcu_evaluate_dev.argtypes = [_vp, _vp, _vp, C.c_int, _u64, _vp, _vp, _vp]
+    L.gbxcu_wide_param_count.argtypes = [C.c_int]
+    L.gbxcu_wide_param_count.restype = _sz
+    L.gbxcu_wide_init.argtypes = [_vp, C.c_int, _u64, _f32p]
+    L.gbxcu_wide_forward.argtypes = [_vp, C.c_int, _f32p, _f32p, _sz, _f64p]
+    L.gbxcu_wide_fit.argtypes = [_vp, C.c_int, _f32p, _f32p, _f64p, _sz, C.POINTER(TrainCfg), _vp,
+                                 C.POINTER(C.c_int)]
+    L.gbxcu_wide_fit_dev.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _sz, C.POINTER(TrainCfg), _vp,
+                                     C.POINTER(C.c_int), _vp]
+    L.gbxcu_tf32_gemm.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _f32p, _f32p, _f32p]
     _LIB = L
     return L
 
@@ -292,6 +303,49 @@ class Device:
                                   el.ctypes.data, C.byref(de), stream)
         self._ck(rc, de.value)
         return el
+
+    # ------------------------------------------------------ wide MLP (C4)
+    def wide_param_count(self, hidden: int) -> int:
+        return int(self.L.gbxcu_wide_param_count(hidden))
+
+    def wide_init(self, hidden: int, seed: int) -> np.ndarray:
+        p = np.empty(self.wide_param_count(hidden), np.float32)
+        self._ck(self.L.gbxcu_wide_init(self.h, hidden, seed, p))
+        return p
+
+    def wide_forward(self, hidden: int, params, feat) -> np.ndarray:
+        feat = _f32(feat).reshape(-1, N_FEATURES)
+        probs = np.empty((feat.shape[0], 2), np.float64)
+        self._ck(self.L.gbxcu_wide_forward(self.h, hidden, _f32(params), feat, feat.shape[0], probs))
+        return probs
+
+    def wide_fit(self, hidden: int, params, feat, tgt, lr=0.01, epochs=1, batch=32, seed=0):
+        p = np.array(params, np.float32, copy=True)
+        feat = _f32(feat).reshape(-1, N_FEATURES)
+        el = np.full(max(epochs, 1), np.nan, np.float64)
+        de = C.c_int(-1)
+        cfg = TrainCfg(lr, epochs, batch, seed, 0, 0)
+        rc = self.L.gbxcu_wide_fit(self.h, hidden, p, feat, _f64(tgt), feat.shape[0], C.byref(cfg),
+                                   el.ctypes.data, C.byref(de))
+        self._ck(rc, de.value)
+        return p, el
+
+    def wide_fit_dev(self, hidden, d_params, d_feat, d_tgt, n, lr=0.01, epochs=1, batch=32, seed=0,
+                     stream=None):
+        el = np.full(max(epochs, 1), np.nan, np.float64)
+        de = C.c_int(-1)
+        cfg = TrainCfg(lr, epochs, batch, seed, 0, 0)
+        self._ck(self.L.gbxcu_wide_fit_dev(self.h, hidden, d_params, d_feat, d_tgt, n, C.byref(cfg),
+                                           el.ctypes.data, C.byref(de), stream), de.value)
+        return el
+
+    def tf32_gemm(self, A, B) -> np.ndarray:
+        A, B = _f32(A), _f32(B)
+        M, K = A.shape
+        N = B.shape[0]
+        D = np.empty((M, N), np.float32)
+        self._ck(self.L.gbxcu_tf32_gemm(self.h, M, N, K, A, B, D))
+        return D
 
     # ----------------------------------------------------------- data parallel
     @staticmethod

@@ -86,6 +86,9 @@ struct gbxcu_ctx {
     DevBuf s_actions, s_run_seed, s_rows, s_samples, h_lower, h_count, h_nbins;
     int shuffle_grid = 0;
     int fast_per_sm = 1;
+    // wide MLP (C4) working set
+    DevBuf w_params, w_grad, w_w1t, w_h1, w_h1t, w_h2, w_d2, w_d2t, w_d1t, w_xt, w_d3, w_kl;
+    DevBuf w_part, w_g4, w_g5, w_loss, w_feat, w_tgt, w_probs;
     // data parallel
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
@@ -119,6 +122,7 @@ int setup_kernel_attrs() {
         set((const void*)train_partial_kernel<32>, train_smem_bytes(32));
         set((const void*)train_partial_kernel<64>, train_smem_bytes(64));
         set((const void*)batch_grad_kernel, train_smem_bytes(64));
+        set((const void*)tc_gemm_kernel, gemm_smem_bytes());
     });
     return rc;
 }
@@ -783,6 +787,316 @@ int gbxcu_evaluate_dev(gbxcu_ctx* c, const gbxcu_dsuite* s, const float* d_param
     gbxcu_dsuite* sm = const_cast<gbxcu_dsuite*>(s);
     return evaluate_dev(c, s, d_params, n_samples, seed, d_actions, d_rows, pick(c, stream),
                         sm->recheck, sm->counters, sm->flags);
+}
+
+}  // extern "C"
+
+// =========================================================================
+// Wide MLP (C4): 44 -> H -> H -> 2 on tcgen05 TF32 GEMMs (k_wide.cu).
+namespace {
+
+constexpr int kGemmTile = 128;  // GM == GN in k_wide.cu
+
+size_t wide_param_count(int H) { return (size_t)H * F + H + (size_t)H * H + H + 2 * (size_t)H + 2; }
+
+int launch_gemm(gbxcu_ctx* c, const GemmArgs& g, int splits, cudaStream_t st) {
+    dim3 grid((g.N + kGemmTile - 1) / kGemmTile, (g.M + kGemmTile - 1) / kGemmTile, splits);
+    tc_gemm_kernel<<<grid, 128, gemm_smem_bytes(), st>>>(g);
+    return check_launch(c, "tc_gemm_kernel");
+}
+
+int check_hidden(int H) {
+    if (H < 32 || H > 1024 || H % 32 != 0)
+        return fail(GBXCU_EINVAL, "wide MLP hidden width must be a multiple of 32 in [32, 1024]");
+    return GBXCU_OK;
+}
+
+// Working set for batches of up to bmax rows per rank.
+int wide_alloc(gbxcu_ctx* c, int H, size_t bmax, int splits4, int splits5, int rsplit) {
+    const size_t ldt = (bmax + 3) & ~(size_t)3;
+    RET(c->w_grad.ensure(sizeof(float) * wide_param_count(H)));
+    RET(c->w_w1t.ensure(sizeof(float) * H * H));
+    RET(c->w_h1.ensure(sizeof(float) * bmax * H));
+    RET(c->w_h2.ensure(sizeof(float) * bmax * H));
+    RET(c->w_d2.ensure(sizeof(float) * bmax * H));
+    for (DevBuf* b : {&c->w_h1t, &c->w_d2t, &c->w_d1t}) RET(b->ensure(sizeof(float) * H * ldt));
+    RET(c->w_xt.ensure(sizeof(float) * 48 * ldt));
+    RET(c->w_d3.ensure(sizeof(float) * 2 * bmax));
+    RET(c->w_kl.ensure(sizeof(double) * bmax));
+    RET(c->w_part.ensure(sizeof(double) * rsplit * (2 * H + 3)));
+    RET(c->w_g4.ensure(sizeof(float) * (size_t)splits4 * H * H));
+    RET(c->w_g5.ensure(sizeof(float) * (size_t)splits5 * H * 48));
+    RET(c->w_loss.ensure(64));
+    return GBXCU_OK;
+}
+
+int blocks(size_t n, int t = 256) { return (int)std::max<size_t>(1, (n + t - 1) / t); }
+
+// One SGD step on rows[0, nbr) (this rank's slice of a global batch of nb).
+int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tgt,
+              const uint32_t* rows, int nbr, size_t nb, size_t ldt, double lr, int epoch,
+              int splits4, int splits5, int rsplit, cudaStream_t st) {
+    const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H,
+                 o_w2 = o_b1 + H;
+    float* G = c->w_grad.as<float>();
+    if (nbr > 0) {
+        // K tails of the transposed operands read as zeros
+        const int c_hi = (int)std::min<size_t>(ldt, ((size_t)nbr + 3) & ~(size_t)3);
+        for (DevBuf* b : {&c->w_h1t, &c->w_d2t, &c->w_d1t}) {
+            zero_cols_kernel<<<blocks((size_t)H * 4), 256, 0, st>>>(b->as<float>(), H, (int)ldt, nbr, c_hi);
+            RET(check_launch(c, "zero_cols_kernel"));
+        }
+        wide_gather_xt_kernel<<<blocks(nbr), 256, 0, st>>>(feat, rows, nbr, c->w_xt.as<float>(), (int)ldt);
+        RET(check_launch(c, "wide_gather_xt_kernel"));
+        zero_cols_kernel<<<blocks(48 * 4), 256, 0, st>>>(c->w_xt.as<float>(), 48, (int)ldt, nbr, c_hi);
+        RET(check_launch(c, "zero_cols_kernel"));
+
+        GemmArgs g1{};  // H1 = relu(X W0^T + b0), also H1^T
+        g1.M = nbr; g1.N = H; g1.K = F;
+        g1.A = feat; g1.lda = F; g1.a_rows = rows;
+        g1.B = P; g1.ldb = F;
+        g1.epi = EPI_BIAS_RELU; g1.bias = P + o_b0;
+        g1.out = c->w_h1.as<float>(); g1.ldo = H;
+        g1.out_t = c->w_h1t.as<float>(); g1.ldt = (int)ldt;
+        RET(launch_gemm(c, g1, 1, st));
+
+        GemmArgs g2{};  // H2 = relu(H1 W1^T + b1)
+        g2.M = nbr; g2.N = H; g2.K = H;
+        g2.A = c->w_h1.as<float>(); g2.lda = H;
+        g2.B = P + o_w1; g2.ldb = H;
+        g2.epi = EPI_BIAS_RELU; g2.bias = P + o_b1;
+        g2.out = c->w_h2.as<float>(); g2.ldo = H;
+        RET(launch_gemm(c, g2, 1, st));
+
+        WideHeadArgs h{};
+        h.h2 = c->w_h2.as<float>(); h.w2 = P + o_w2; h.b2 = P + o_w2 + 2 * H;
+        h.tgt = tgt; h.rows = rows; h.nb = nbr; h.hidden = H; h.ldt = (int)ldt;
+        h.inv_b = 1.0 / (double)nb;
+        h.kl = c->w_kl.as<double>(); h.d3 = c->w_d3.as<float>();
+        h.d2 = c->w_d2.as<float>(); h.d2t = c->w_d2t.as<float>();
+        wide_head_kernel<<<blocks((size_t)nbr * 32), 256, 0, st>>>(h);
+        RET(check_launch(c, "wide_head_kernel"));
+
+        GemmArgs g3{};  // D1^T = ((D2 W1) . [H1 > 0])^T
+        g3.M = nbr; g3.N = H; g3.K = H;
+        g3.A = c->w_d2.as<float>(); g3.lda = H;
+        g3.B = c->w_w1t.as<float>(); g3.ldb = H;
+        g3.epi = EPI_MASK_T; g3.mask = c->w_h1.as<float>(); g3.ldm = H;
+        g3.out_t = c->w_d1t.as<float>(); g3.ldt = (int)ldt;
+        RET(launch_gemm(c, g3, 1, st));
+
+        GemmArgs g4{};  // gW1 = D2^T H1 (split-K partials)
+        g4.M = H; g4.N = H; g4.K = nbr;
+        g4.A = c->w_d2t.as<float>(); g4.lda = (int)ldt;
+        g4.B = c->w_h1t.as<float>(); g4.ldb = (int)ldt;
+        g4.epi = EPI_STORE; g4.out = c->w_g4.as<float>(); g4.ldo = H;
+        g4.split_stride = (size_t)H * H;
+        RET(launch_gemm(c, g4, splits4, st));
+
+        GemmArgs g5{};  // gW0 = D1^T X (split-K partials, 48 padded columns)
+        g5.M = H; g5.N = 48; g5.K = nbr;
+        g5.A = c->w_d1t.as<float>(); g5.lda = (int)ldt;
+        g5.B = c->w_xt.as<float>(); g5.ldb = (int)ldt;
+        g5.epi = EPI_STORE; g5.out = c->w_g5.as<float>(); g5.ldo = 48;
+        g5.split_stride = (size_t)H * 48;
+        RET(launch_gemm(c, g5, splits5, st));
+
+        split_reduce_f32_kernel<<<blocks((size_t)H * H), 256, 0, st>>>(
+            c->w_g4.as<float>(), splits4, (size_t)H * H, H, H, H, G + o_w1, H);
+        RET(check_launch(c, "split_reduce_f32_kernel"));
+        wide_gw0_kernel<<<blocks((size_t)H * F), 256, 0, st>>>(c->w_g5.as<float>(), splits5,
+                                                               (size_t)H * 48, H, G);
+        RET(check_launch(c, "wide_gw0_kernel"));
+        row_sum_kernel<<<H, 256, 0, st>>>(c->w_d1t.as<float>(), (int)ldt, nbr, G + o_b0);
+        RET(check_launch(c, "row_sum_kernel"));
+        row_sum_kernel<<<H, 256, 0, st>>>(c->w_d2t.as<float>(), (int)ldt, nbr, G + o_b1);
+        RET(check_launch(c, "row_sum_kernel"));
+        wide_w2_partial_kernel<<<dim3((H + 127) / 128, rsplit), 128, 0, st>>>(
+            c->w_h2.as<float>(), c->w_d3.as<float>(), c->w_kl.as<double>(), nbr, H,
+            c->w_part.as<double>());
+        RET(check_launch(c, "wide_w2_partial_kernel"));
+        split_reduce_f64_kernel<<<blocks(2 * H + 3), 256, 0, st>>>(
+            c->w_part.as<double>(), rsplit, 2 * H + 3, G + o_w2, c->w_loss.as<double>());
+        RET(check_launch(c, "split_reduce_f64_kernel"));
+    } else {
+        CK(cudaMemsetAsync(G, 0, sizeof(float) * wide_param_count(H), st));
+        CK(cudaMemsetAsync(c->w_loss.p, 0, sizeof(double), st));
+    }
+    if (c->comm) {
+        CKN(ncclAllReduce(G, G, wide_param_count(H), ncclFloat32, ncclSum, c->comm, st));
+        CKN(ncclAllReduce(c->w_loss.p, c->w_loss.p, 1, ncclFloat64, ncclSum, c->comm, st));
+    }
+    wide_update_kernel<<<blocks(wide_param_count(H)), 256, 0, st>>>(
+        P, G, c->w_loss.as<double>(), nb, lr, H, c->w_w1t.as<float>(), epoch,
+        c->diverged.as<int>(), c->epoch_acc.as<double>(), wide_param_count(H));
+    return check_launch(c, "wide_update_kernel");
+}
+
+int wide_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, const double* d_tgt,
+                    size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out,
+                    int* diverged_epoch, cudaStream_t st) {
+    RET(check_hidden(H));
+    RET(validate_cfg(cfg, n));
+    RET(setup_kernel_attrs());
+    RET(prepare_order(c, n, st));
+    const size_t b = std::min<size_t>((size_t)cfg->batch_size, n);
+    const size_t bmax = (b + c->nranks - 1) / c->nranks;
+    const size_t ldt = (bmax + 3) & ~(size_t)3;
+    // split-K so the two K = batch GEMMs fill the machine
+    const int tiles4 = ((H + 127) / 128) * ((H + 127) / 128), tiles5 = (H + 127) / 128;
+    const int kblocks = (int)((bmax + 31) / 32);
+    const int splits4 = std::max(1, std::min(kblocks, c->num_sms / tiles4));
+    const int splits5 = std::max(1, std::min(kblocks, c->num_sms / tiles5));
+    const int rsplit = (int)std::max<size_t>(1, std::min<size_t>(64, bmax / 64));
+    RET(wide_alloc(c, H, bmax, splits4, splits5, rsplit));
+    RET(c->epoch_loss.ensure(sizeof(double) * cfg->epochs));
+    RET(c->epoch_acc.ensure(16));
+    wide_w1t_kernel<<<blocks((size_t)H * H), 256, 0, st>>>(d_params, H, c->w_w1t.as<float>());
+    RET(check_launch(c, "wide_w1t_kernel"));
+    const long n_steps = (long)((n + cfg->batch_size - 1) / cfg->batch_size);
+    for (int e = 0; e < cfg->epochs; ++e) {
+        RET(shuffle_epoch(c, n, cfg->seed, e, st));
+        CK(cudaMemsetAsync(c->epoch_acc.p, 0, sizeof(double), st));
+        const uint32_t* order = c->order.as<uint32_t>();
+        for (long s = 0; s < n_steps; ++s) {
+            const size_t start = (size_t)s * cfg->batch_size;
+            const size_t nb = std::min(n, start + (size_t)cfg->batch_size) - start;
+            const size_t per = (nb + c->nranks - 1) / c->nranks;
+            const size_t lo = std::min(nb, (size_t)c->rank * per), hi = std::min(nb, lo + per);
+            RET(wide_step(c, H, d_params, d_feat, d_tgt, order + start + lo, (int)(hi - lo), nb, ldt,
+                          cfg->learning_rate, e, splits4, splits5, rsplit, st));
+        }
+        finish_epoch_kernel<<<1, 1, 0, st>>>(c->epoch_acc.as<double>(), n, e, c->diverged.as<int>(),
+                                              c->epoch_loss.as<double>());
+        RET(check_launch(c, "finish_epoch_kernel"));
+    }
+    int dv = -1;
+    CK(cudaMemcpyAsync(&dv, c->diverged.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (epoch_loss_out)
+        CK(cudaMemcpyAsync(epoch_loss_out, c->epoch_loss.p, sizeof(double) * cfg->epochs,
+                           cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (diverged_epoch) *diverged_epoch = dv;
+    if (dv >= 0)
+        return fail(GBXCU_EDIVERGED, "training loss became non-finite at epoch " + std::to_string(dv));
+    return GBXCU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t gbxcu_wide_param_count(int hidden) { return wide_param_count(hidden); }
+
+int gbxcu_wide_init(gbxcu_ctx* c, int hidden, uint64_t seed, float* params_out) {
+    if (!c || !params_out) return fail(GBXCU_EINVAL, "null argument");
+    RET(check_hidden(hidden));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    const size_t np = wide_param_count(hidden);
+    RET(c->w_params.ensure(sizeof(float) * np));
+    wide_init_kernel<<<blocks(np), 256, 0, c->stream>>>(seed, hidden, c->w_params.as<float>(), np);
+    RET(check_launch(c, "wide_init_kernel"));
+    CK(cudaMemcpyAsync(params_out, c->w_params.p, sizeof(float) * np, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return GBXCU_OK;
+}
+
+int gbxcu_wide_forward(gbxcu_ctx* c, int hidden, const float* params, const float* feat, size_t n,
+                       double* probs) {
+    if (!c || !params || !probs || (n && !feat)) return fail(GBXCU_EINVAL, "null argument");
+    RET(check_hidden(hidden));
+    if (n == 0) return GBXCU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    RET(setup_kernel_attrs());
+    cudaStream_t st = c->stream;
+    const int H = hidden;
+    const size_t np = wide_param_count(H), chunk = std::min<size_t>(n, 65536);
+    RET(upload(c->w_params, params, np, st));
+    RET(upload(c->w_feat, feat, n * F, st));
+    RET(c->w_probs.ensure(sizeof(double) * 2 * n));
+    RET(c->w_h1.ensure(sizeof(float) * chunk * H));
+    RET(c->w_h2.ensure(sizeof(float) * chunk * H));
+    const float* P = c->w_params.as<float>();
+    for (size_t r0 = 0; r0 < n; r0 += chunk) {
+        const int m = (int)std::min(chunk, n - r0);
+        GemmArgs g1{};
+        g1.M = m; g1.N = H; g1.K = F;
+        g1.A = c->w_feat.as<float>() + r0 * F; g1.lda = F;
+        g1.B = P; g1.ldb = F;
+        g1.epi = EPI_BIAS_RELU; g1.bias = P + (size_t)H * F;
+        g1.out = c->w_h1.as<float>(); g1.ldo = H;
+        RET(launch_gemm(c, g1, 1, st));
+        GemmArgs g2{};
+        g2.M = m; g2.N = H; g2.K = H;
+        g2.A = c->w_h1.as<float>(); g2.lda = H;
+        g2.B = P + (size_t)H * F + H; g2.ldb = H;
+        g2.epi = EPI_BIAS_RELU; g2.bias = P + (size_t)H * F + H + (size_t)H * H;
+        g2.out = c->w_h2.as<float>(); g2.ldo = H;
+        RET(launch_gemm(c, g2, 1, st));
+        const float* w2 = P + (size_t)H * F + H + (size_t)H * H + H;
+        wide_probs_kernel<<<blocks((size_t)m * 32), 256, 0, st>>>(c->w_h2.as<float>(), w2, w2 + 2 * H, m,
+                                                                  H, c->w_probs.as<double>() + 2 * r0);
+        RET(check_launch(c, "wide_probs_kernel"));
+    }
+    CK(cudaMemcpyAsync(probs, c->w_probs.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return GBXCU_OK;
+}
+
+int gbxcu_wide_fit(gbxcu_ctx* c, int hidden, float* params_inout, const float* feat, const double* tgt,
+                   size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out, int* diverged_epoch) {
+    if (!c || !params_inout || !feat || !tgt) return fail(GBXCU_EINVAL, "null argument");
+    RET(check_hidden(hidden));
+    RET(validate_cfg(cfg, n));
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    const size_t np = wide_param_count(hidden);
+    RET(upload(c->w_params, params_inout, np, st));
+    RET(upload(c->w_feat, feat, n * F, st));
+    RET(upload(c->w_tgt, tgt, n * 2, st));
+    int rc = wide_fit_device(c, hidden, c->w_params.as<float>(), c->w_feat.as<float>(),
+                             c->w_tgt.as<double>(), n, cfg, epoch_loss_out, diverged_epoch, st);
+    if (rc != GBXCU_OK && rc != GBXCU_EDIVERGED) return rc;
+    const std::string msg = g_err;
+    CK(cudaMemcpyAsync(params_inout, c->w_params.p, sizeof(float) * np, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    g_err = msg;
+    return rc;
+}
+
+int gbxcu_wide_fit_dev(gbxcu_ctx* c, int hidden, float* d_params, const float* d_feat,
+                       const double* d_tgt, size_t n, const gbxcu_train_cfg* cfg,
+                       double* epoch_loss_out, int* diverged_epoch, void* stream) {
+    if (!c || !d_params || !d_feat || !d_tgt) return fail(GBXCU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    return wide_fit_device(c, hidden, d_params, d_feat, d_tgt, n, cfg, epoch_loss_out,
+                           diverged_epoch, pick(c, stream));
+}
+
+// Plain D[M][N] = A[M][K] . B[N][K]^T on the tcgen05 TF32 path (host buffers).
+int gbxcu_tf32_gemm(gbxcu_ctx* c, int M, int N, int K, const float* A, const float* B, float* D) {
+    if (!c || !A || !B || !D || M < 1 || N < 1 || K < 1) return fail(GBXCU_EINVAL, "bad gemm arguments");
+    if (K % 4) return fail(GBXCU_EINVAL, "K must be a multiple of 4");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    RET(setup_kernel_attrs());
+    cudaStream_t st = c->stream;
+    RET(upload(c->w_h1, A, (size_t)M * K, st));
+    RET(upload(c->w_h2, B, (size_t)N * K, st));
+    RET(c->w_d2.ensure(sizeof(float) * (size_t)M * N));
+    GemmArgs g{};
+    g.M = M; g.N = N; g.K = K;
+    g.A = c->w_h1.as<float>(); g.lda = K;
+    g.B = c->w_h2.as<float>(); g.ldb = K;
+    g.epi = EPI_STORE; g.out = c->w_d2.as<float>(); g.ldo = N;
+    RET(launch_gemm(c, g, 1, st));
+    CK(cudaMemcpyAsync(D, c->w_d2.p, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return GBXCU_OK;
 }
 
 }  // extern "C"

@@ -89,6 +89,63 @@ struct ShuffleArgs {
 };
 __global__ void shuffle_epoch_kernel(ShuffleArgs s);
 
+// ---------------------------------------------------------- wide MLP (C4)
+enum GemmEpi { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_MASK_T = 2 };
+
+struct GemmArgs {
+    int M, N, K;
+    const float* A;          // [M][lda], K-major (rows optionally gathered)
+    int lda;
+    const uint32_t* a_rows;  // nullable row indirection for A
+    const float* B;          // [N][ldb], K-major
+    int ldb;
+    int epi;
+    const float* bias;       // EPI_BIAS_RELU
+    float* out;              // row-major [M][ldo] (EPI_STORE: + blockIdx.z * split_stride)
+    int ldo;
+    float* out_t;            // transposed [N][ldt]
+    int ldt;
+    const float* mask;       // EPI_MASK_T: [M][ldm]
+    int ldm;
+    size_t split_stride;
+};
+
+struct WideHeadArgs {
+    const float* h2;        // [nb][hidden]
+    const float* w2;        // [2][hidden]
+    const float* b2;        // [2]
+    const double* tgt;      // targets, indexed through rows
+    const uint32_t* rows;   // nullable
+    int nb, hidden, ldt;
+    double inv_b;
+    double* kl;             // [nb]
+    float* d3;              // [nb][2]
+    float* d2;              // [nb][hidden]
+    float* d2t;             // [hidden][ldt]
+};
+
+__global__ void tc_gemm_kernel(GemmArgs g);
+size_t gemm_smem_bytes();
+__global__ void wide_gather_xt_kernel(const float* feat, const uint32_t* rows, int nb, float* xt,
+                                      int ldt);
+__global__ void wide_head_kernel(WideHeadArgs a);
+__global__ void row_sum_kernel(const float* in, int ld, int ncols, float* out);
+__global__ void wide_w2_partial_kernel(const float* h2, const float* d3, const double* kl, int nb,
+                                       int hidden, double* part);
+__global__ void split_reduce_f32_kernel(const float* src, int splits, size_t stride, int rows,
+                                        int cols, int ld_src, float* dst, int ld_dst);
+__global__ void split_reduce_f64_kernel(const double* src, int splits, int n, float* dst,
+                                        double* loss_out);
+__global__ void wide_update_kernel(float* params, const float* grad, const double* loss_sum,
+                                   size_t nb, double lr, int hidden, float* w1t, int epoch,
+                                   int* diverged, double* epoch_acc, size_t np);
+__global__ void wide_w1t_kernel(const float* params, int hidden, float* w1t);
+__global__ void wide_gw0_kernel(const float* src, int splits, size_t stride, int hidden, float* dst);
+__global__ void wide_init_kernel(uint64_t seed, int hidden, float* params, size_t np);
+__global__ void wide_probs_kernel(const float* h2, const float* w2, const float* b2, int nb,
+                                  int hidden, double* probs);
+__global__ void zero_cols_kernel(float* m, int rows, int ld, int c_lo, int c_hi);
+
 __global__ void aggregate_kernel(AggArgs a);
 __global__ void histogram_kernel(const double* rows, int stride, size_t n, double* lower,
                                  unsigned long long* count, size_t cap,

@@ -112,6 +112,20 @@ __device__ __forceinline__ void tmem_ld_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+// cp.async 16-byte copy global -> shared (zero-fill when src_bytes == 0).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_group() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // Byte offset of element (r, k) in the canonical layout of an R-row operand.
 __host__ __device__ __forceinline__ uint32_t canon_off(int r, int k, int R) {
     return (uint32_t)((k >> 2) * R * 16 + r * 16 + (k & 3) * 4);

@@ -20,7 +20,7 @@ def lib():
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "gbxcu.h")).read()
-    return sorted(set(re.findall(r"\b(gbxcu_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(gbxcu_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_exports_every_declared_symbol(lib):
