@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1_000_000, help="records per GPU (weak scaling)")
-    ap.add_argument("--batch", type=int, default=4096, help="minibatch per GPU")
+    ap.add_argument("--batch", type=int, default=8192,
+                    help="minibatch per GPU (global = N x this; 65,536 at 8 GPUs, SURVEY C3)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -391,6 +392,31 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
                           "ms": ms, "apps": args.c5_apps, "shaders": nsh,
                           "bytes_per_shader": 204}
     ds.close()
+
+    # C4: wide MLP (44-512-512-2) fit epoch on the tcgen05 TF32 path
+    H = 512
+    n_w = min(n, 262_144)
+    pw = torch.from_numpy(dev.wide_init(H, 7)).cuda()
+    tw = torch.empty((n_w, 2), dtype=torch.float64, device="cuda")
+    tw[:, 0] = 0.5
+    tw[:, 1] = 0.5
+    dev.wide_fit_dev(H, pw.data_ptr(), feat_d.data_ptr(), tw.data_ptr(), n_w, 0.01, 1, args.batch, 1,
+                     stream=dev.stream)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    reps = 3
+    for _ in range(reps):
+        dev.wide_fit_dev(H, pw.data_ptr(), feat_d.data_ptr(), tw.data_ptr(), n_w, 0.01, 1, args.batch,
+                         1, stream=dev.stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / reps
+    tf = n_w * 1_669_120 / (ms * 1e-3) / 1e12
+    out["wide_mlp"] = {"value": n_w / (ms * 1e-3), "unit": "samples/s", "ms_per_epoch": ms,
+                       "records": n_w, "hidden": H, "batch": args.batch, "dtype": "tf32",
+                       "tflops": tf, "flop_per_record": 1_669_120,
+                       "tf32_peak_tflops": peaks.get("bf16_tflops", 1590.0) / 2,
+                       "peak_note": "dense TF32 = half the measured bf16 cuBLAS peak"}
     return out
 
 
