@@ -45,6 +45,10 @@ constexpr int NW = NT / 32;      // 16 warps
 // SGD update writes conflict-free.
 constexpr int W0S = F + 1;   // 45
 constexpr int W1S = H1 + 1;  // 65
+// h2/d2 rows are also read/written record-parallel (F3: lanes = records), so
+// their stride is padded off the 32-word period; 34 keeps 16-byte alignment
+// for the double2 row reads of B2.
+constexpr int H2S = H2 + 2;  // 34
 
 template <int TB>
 struct TrainSmem {
@@ -56,8 +60,8 @@ struct TrainSmem {
     double b2[A];
     double x[TB * F];    // [r][i]
     double h1[TB * H1];  // [r][j]
-    double h2[TB * H2];  // [r][k]
-    double d2[TB * H2];  // [r][k]
+    double h2[TB * H2S]; // [r][k], stride 34
+    double d2[TB * H2S]; // [r][k], stride 34
     double d1[TB * H1];  // [r][j]
     double d3[TB * 2];
     double tgt[TB * 2];
@@ -344,7 +348,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
         }
 #pragma unroll
         for (int rr = 0; rr < RPW; ++rr)
-            S.h2[(RPW * w + rr) * H2 + lane] = acc[rr] > 0.0 ? acc[rr] : 0.0;
+            S.h2[(RPW * w + rr) * H2S + lane] = acc[rr] > 0.0 ? acc[rr] : 0.0;
     }
     __syncthreads();
 
@@ -352,7 +356,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
     if (tid < 2 * TB) {
         const int r = tid >> 1, a = tid & 1;
         double l = S.b2[a];
-        const double* h = S.h2 + r * H2;
+        const double* h = S.h2 + r * H2S;
         const double* wr = S.w2 + a * H2;
 #pragma unroll 8
         for (int k = 0; k < H2; ++k) l = madd_rn(l, wr[k], h[k]);
@@ -382,7 +386,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
             const int k = (H2 / 2) * a + kk;
             double d = madd_rn(0.0, d30, S.w2[k]);
             d = madd_rn(d, d31, S.w2[H2 + k]);
-            S.d2[r * H2 + k] = h[k] <= 0.0 ? 0.0 : d;
+            S.d2[r * H2S + k] = h[k] <= 0.0 ? 0.0 : d;
         }
     }
     __syncthreads();
@@ -393,7 +397,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
         double acc[RPW][2];
 #pragma unroll
         for (int rr = 0; rr < RPW; ++rr) acc[rr][0] = acc[rr][1] = 0.0;
-        const double* db = S.d2 + (RPW * w) * H2;
+        const double* db = S.d2 + (RPW * w) * H2S;
 #pragma unroll 4
         for (int k = 0; k < H2; k += 2) {
             const double* wk = S.w1 + k * W1S;
@@ -401,7 +405,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
             const double wA1 = wk[W1S + lane], wB1 = wk[W1S + lane + 32];
 #pragma unroll
             for (int rr = 0; rr < RPW; ++rr) {
-                const double2 dv = *reinterpret_cast<const double2*>(db + rr * H2 + k);
+                const double2 dv = *reinterpret_cast<const double2*>(db + rr * H2S + k);
                 // a zero d2 adds a signed zero: a no-op, matching the reference's
                 // `continue` on zero rows (policy.cpp:247)
                 acc[rr][0] = madd_rn(acc[rr][0], dv.x, wA0);
@@ -419,7 +423,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
         // gw1[2w+kk][lane+32q] += d2[r][2w+kk] * h1[r][lane+32q], r in batch order
 #pragma unroll 4
         for (int r = 0; r < nv; ++r) {
-            const double2 dk = *reinterpret_cast<const double2*>(S.d2 + r * H2 + 2 * w);
+            const double2 dk = *reinterpret_cast<const double2*>(S.d2 + r * H2S + 2 * w);
             const double hA = S.h1[r * H1 + lane], hB = S.h1[r * H1 + lane + 32];
             g.g1[0][0] = madd_rn(g.g1[0][0], dk.x, hA);
             g.g1[0][1] = madd_rn(g.g1[0][1], dk.x, hB);
@@ -428,10 +432,10 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
         }
         if (tid >= 320 && tid < 352) {
             const int k = tid - 320;
-            for (int r = 0; r < nv; ++r) g.gx = __dadd_rn(g.gx, S.d2[r * H2 + k]);
+            for (int r = 0; r < nv; ++r) g.gx = __dadd_rn(g.gx, S.d2[r * H2S + k]);
         } else if (tid >= 352 && tid < 416) {
             const int a = (tid - 352) >> 5, k = (tid - 352) & 31;
-            for (int r = 0; r < nv; ++r) g.gx = madd_rn(g.gx, S.d3[2 * r + a], S.h2[r * H2 + k]);
+            for (int r = 0; r < nv; ++r) g.gx = madd_rn(g.gx, S.d3[2 * r + a], S.h2[r * H2S + k]);
         } else if (tid >= 416 && tid < 418) {
             const int a = tid - 416;
             for (int r = 0; r < nv; ++r) g.gx = __dadd_rn(g.gx, S.d3[2 * r + a]);
