@@ -252,13 +252,19 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    kernel_ms = {"shuffle": 0.0, "train": 0.0}
+
     def step():
         dev.fit_dev(params_d.data_ptr(), feat_d.data_ptr(), tgt_d.data_ptr(), n_total, args.lr, 1,
                     batch, 99, stream=dev.stream)
+        sh, tr = dev.last_fit_timing()  # CUDA events around the launches (fit syncs at its end)
+        kernel_ms["shuffle"] += sh
+        kernel_ms["train"] += tr
 
     for _ in range(args.warmup):
         step()
     barrier()
+    kernel_ms = {"shuffle": 0.0, "train": 0.0}
     l0 = dev.launches
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -300,21 +306,36 @@ def main():
     secondary = {}
     if rank == 0:
         fp64_peak, fp32_peak = pipe_peaks(local)
-    # the train kernel's share: time one epoch split by kernel with events
-    flop_per_record = 23936
-    train_tflops = n_total * flop_per_record / (ms_step * 1e-3) / 1e12 / world
-    hbm_bytes = n_total * 196 / world
+    # dominant kernel: train_epoch_kernel, timed with CUDA events on its stream
+    flop_per_record = 23936          # fwd 9,856 + bwd 14,080
+    fp64_instr_per_record = 21120    # reference rounding: DFMA only where products are exact
+    records_per_gpu = n_total / world
+    k_ms = kernel_ms["train"] / args.steps if kernel_ms["train"] > 0 else ms_step
+    train_tflops = records_per_gpu * flop_per_record / (k_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get("train_epoch_kernel")
+            if tr and tr.get("records") == records_per_gpu and tr.get("batch") == batch:
+                traffic = tr["dram_bytes"]
+    except (OSError, ValueError):
+        pass
     roofline = {
         "bound": "fp64",
         "achieved": train_tflops,
         "peak": fp64_peak,
         "unit": "TFLOP/s",
         "frac": (train_tflops / fp64_peak) if fp64_peak else None,
-        "traffic": None,
-        "kernel": "train_epoch_kernel (fp64 parity mode, whole-step time)",
+        "traffic": traffic,
+        "kernel": "train_epoch_kernel (fp64 parity mode)",
+        "kernel_ms_per_step": k_ms,
+        "shuffle_ms_per_step": kernel_ms["shuffle"] / args.steps,
         "work_per_unit": "23,936 FLOP/record (fwd 9,856 + bwd 14,080), 196 B/record",
+        "algorithmic_bytes": records_per_gpu * 196,
         "peak_source": "measured DFMA throughput, tools/peaks.cu (MEASURED_PEAKS.json has no fp64)",
-        "hbm_view": {"achieved_gbs": hbm_bytes / (ms_step * 1e-3) / 1e9,
+        "fp64_issue_frac": (records_per_gpu * fp64_instr_per_record / (k_ms * 1e-3)) / (fp64_peak * 1e12 / 2)
+        if fp64_peak else None,
+        "hbm_view": {"achieved_gbs": records_per_gpu * 196 / (k_ms * 1e-3) / 1e9,
                      "peak_gbs": peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)},
     }
 

@@ -71,6 +71,10 @@ void* gbxcu_stream(gbxcu_ctx* ctx);
 /* Number of kernels this context launched since creation (for bench.py's
  * gpu_launches claim; counts our kernels only, not memcpys or NCCL). */
 uint64_t gbxcu_launch_count(const gbxcu_ctx* ctx);
+/* Device time (CUDA events on the launching stream) of the last single-GPU
+ * fit with <= 8 epochs: epoch-permutation replay and train_epoch kernel,
+ * summed over epochs (0 for the data-parallel path). */
+int gbxcu_last_fit_timing(const gbxcu_ctx* ctx, double* shuffle_ms, double* train_kernel_ms);
 
 /* ------------------------------------------------------------------- init */
 /* PolicyNet::init (proj/src/policy.cpp:128-139) computed on the device:

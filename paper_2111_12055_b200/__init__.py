@@ -88,7 +88,7 @@ EXPORTS = (
     "gbxcu_comm_destroy", "gbxcu_aggregate", "gbxcu_histogram", "gbxcu_suite_upload",
     "gbxcu_suite_free", "gbxcu_suite_features", "gbxcu_evaluate", "gbxcu_evaluate_dev",
     "gbxcu_wide_param_count", "gbxcu_wide_init", "gbxcu_wide_forward", "gbxcu_wide_fit",
-    "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm",
+    "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing",
 )
 
 _LIB = None
@@ -145,6 +145,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_wide_fit_dev.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _sz, C.POINTER(TrainCfg), _vp,
                                      C.POINTER(C.c_int), _vp]
     L.gbxcu_tf32_gemm.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _f32p, _f32p, _f32p]
+    L.gbxcu_last_fit_timing.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     _LIB = L
     return L
 
@@ -220,6 +221,12 @@ class Device:
     @property
     def launches(self) -> int:
         return int(self.L.gbxcu_launch_count(self.h))
+
+    def last_fit_timing(self):
+        """(shuffle_ms, train_kernel_ms) of the last single-GPU fit (CUDA events)."""
+        a, b = C.c_double(), C.c_double()
+        self._ck(self.L.gbxcu_last_fit_timing(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     # ------------------------------------------------------------ policy
     def policy_init(self, seed: int) -> np.ndarray:

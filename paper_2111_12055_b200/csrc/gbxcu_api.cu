@@ -76,6 +76,8 @@ struct gbxcu_ctx {
     int num_sms = 0;
     cudaStream_t stream = nullptr;
     uint64_t launches = 0;
+    cudaEvent_t ev[24] = {};                 // fit's per-kernel timing events
+    double last_shuffle_ms = 0, last_train_ms = 0;
     std::mutex mu;
     // scratch
     DevBuf params, feat, tgt, probs, actions, recheck, counters, flags;
@@ -272,7 +274,9 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     a.nranks = c->nranks;
     const long n_steps = (long)((n + cfg->batch_size - 1) / cfg->batch_size);
 
+    const bool timed = cfg->epochs <= 8;  // per-kernel event timing (bench / profiling)
     for (int e = 0; e < cfg->epochs; ++e) {
+        if (timed) CK(cudaEventRecord(c->ev[2 * e % 16], st));
         RET(shuffle_epoch(c, n, cfg->seed, e, st));
         a.order = c->order.as<uint32_t>();  // the pass output (buffers ping-pong)
         a.epoch = e;
@@ -281,12 +285,14 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
             void* args[] = {&a};
             const void* fn = tb == 32 ? (const void*)train_epoch_kernel<32>
                                       : (const void*)train_epoch_kernel<64>;
+            if (timed) CK(cudaEventRecord(c->ev[(2 * e + 1) % 16], st));
             if (G == 1) {
                 CK(cudaLaunchKernel(fn, 1, TRAIN_BLOCK, args, train_smem_bytes(tb), st));
             } else {
                 CK(cudaLaunchCooperativeKernel(fn, G, TRAIN_BLOCK, args, train_smem_bytes(tb), st));
             }
             RET(check_launch(c, "train_epoch_kernel"));
+            if (timed) CK(cudaEventRecord(c->ev[16 + e % 8], st));
         } else {
             CK(cudaMemsetAsync(c->epoch_acc.p, 0, sizeof(double), st));
             for (long s = 0; s < n_steps; ++s) {
@@ -317,6 +323,16 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
         CK(cudaMemcpyAsync(epoch_loss_out, c->epoch_loss.p, sizeof(double) * cfg->epochs,
                            cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    c->last_shuffle_ms = c->last_train_ms = 0.0;
+    if (timed && !c->comm) {
+        for (int e = 0; e < cfg->epochs; ++e) {
+            float a_ms = 0.f, b_ms = 0.f;
+            cudaEventElapsedTime(&a_ms, c->ev[2 * e % 16], c->ev[(2 * e + 1) % 16]);
+            cudaEventElapsedTime(&b_ms, c->ev[(2 * e + 1) % 16], c->ev[16 + e % 8]);
+            c->last_shuffle_ms += a_ms;
+            c->last_train_ms += b_ms;
+        }
+    }
     if (diverged_epoch) *diverged_epoch = dv;
     if (dv >= 0)
         return fail(GBXCU_EDIVERGED,
@@ -378,6 +394,7 @@ int gbxcu_create(int device, gbxcu_ctx** out) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fwd_fast_kernel, FWD_BLOCK,
                                                   fast_smem_bytes());
     c->fast_per_sm = std::max(1, per_sm);
+    for (auto& e : c->ev) cudaEventCreate(&e);
     *out = c;
     return GBXCU_OK;
 }
@@ -385,12 +402,21 @@ int gbxcu_create(int device, gbxcu_ctx** out) {
 void gbxcu_destroy(gbxcu_ctx* c) {
     if (!c) return;
     if (c->comm) ncclCommDestroy(c->comm);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
 
 void* gbxcu_stream(gbxcu_ctx* c) { return c ? (void*)c->stream : nullptr; }
 uint64_t gbxcu_launch_count(const gbxcu_ctx* c) { return c ? c->launches : 0; }
+
+int gbxcu_last_fit_timing(const gbxcu_ctx* c, double* shuffle_ms, double* train_kernel_ms) {
+    if (!c) return fail(GBXCU_EINVAL, "null context");
+    if (shuffle_ms) *shuffle_ms = c->last_shuffle_ms;
+    if (train_kernel_ms) *train_kernel_ms = c->last_train_ms;
+    return GBXCU_OK;
+}
 
 int gbxcu_policy_init(gbxcu_ctx* c, uint64_t seed, float* params_out) {
     if (!c || !params_out) return fail(GBXCU_EINVAL, "null argument");
