@@ -36,6 +36,22 @@
 
 namespace gbxcu {
 
+#ifdef GBX_PHASE_TIMING
+// Debug build only (tools/phase_timing.sh): per-phase cycle totals of CTA 0.
+__device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_phase_t;
+#define PHASE_MARK(i)                                                          \
+    do {                                                                       \
+        if (threadIdx.x == 0 && blockIdx.x == 0) {                             \
+            const unsigned long long t_ = clock64();                           \
+            g_phase_cycles[i] += t_ - g_phase_t;                               \
+            g_phase_t = t_;                                                    \
+        }                                                                      \
+    } while (0)
+#else
+#define PHASE_MARK(i) ((void)0)
+#endif
+
 constexpr int NT = TRAIN_BLOCK;  // 512 threads
 constexpr int NW = NT / 32;      // 16 warps
 
@@ -298,6 +314,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
     if (tid < 2 * TB) S.tgt[tid] = S.stage_t[buf][tid];
     __syncthreads();
 
+    PHASE_MARK(0);
     // ---- F1: lanes <-> j (lane, lane+32), warp <-> rows
     {
         double acc[RPW][2];
@@ -329,6 +346,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
     }
     __syncthreads();
 
+    PHASE_MARK(1);
     // ---- F2: lanes <-> k, warp <-> rows
     {
         double acc[RPW];
@@ -352,6 +370,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
     }
     __syncthreads();
 
+    PHASE_MARK(2);
     // ---- F3: thread (r, a) computes logit a, then softmax/KL/d3 with its pair
     if (tid < 2 * TB) {
         const int r = tid >> 1, a = tid & 1;
@@ -391,6 +410,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
     }
     __syncthreads();
 
+    PHASE_MARK(3);
     // ---- B2: d1[r][j] = sum_k d2[r][k] w1[k][j] (masked by h1 > 0)
     //      + gw1 / gb1 / gw2 / gb2 / KL-sum accumulation (need only d2, d3, h1, h2)
     {
@@ -445,6 +465,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
     }
     __syncthreads();
 
+    PHASE_MARK(4);
     // ---- G0: gw0[j][i] += d1[r][j] * x[r][i] (j = lane, lane+32; i = warp's
     //      columns), gb0[j] += d1[r][j] on warp 12; records in batch order
     {
@@ -470,6 +491,7 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
         }
     }
     __syncthreads();
+    PHASE_MARK(5);
 }
 
 // Deterministic fixed-shape warp sum of per-lane partials (lane 0 holds it).
@@ -518,6 +540,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
         const double inv_b = 1.0 / (double)nb;  // batch_kl_gradient's 1/|b| (global batch)
         for (size_t r0 = lo; r0 < hi; r0 += TB) {
             const int nv = (int)min((size_t)TB, hi - r0);
+            PHASE_MARK(6);
             cp_async_wait_all();
             __syncthreads();
             const int cur = buf;
@@ -525,6 +548,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
             // queue the following tile (this step or a later one)
             have_next = next_tile<TB>(a, n_steps, pf_step, pf_r0, pf_nv);
             if (have_next) prefetch_tile<TB>(S, buf, a, pf_r0, pf_nv);
+            PHASE_MARK(7);
             train_tile<TB>(S, g, cur, nv, inv_b);
         }
         if (single) {
@@ -548,7 +572,9 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
             double* part = a.partials + (size_t)blockIdx.x * (NP + 1);
             for_each_owned(g, [&](int p, double& acc) { part[p] = acc; });
             if (tid == NT - 1) part[NP] = g.loss;
+            PHASE_MARK(8);
             grid_barrier(a.bar, bar_target);
+            PHASE_MARK(9);
             if (w == 0) {
                 const double tot = reduce_over_ctas(a.partials, G, NP, lane);
                 if (lane == 0) {
@@ -572,10 +598,13 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
                     a.params[p] = __double2float_rn(__dsub_rn(wv, __dmul_rn(a.lr, gs)));
                 }
             }
+            PHASE_MARK(10);
             grid_barrier(a.bar, bar_target);
+            PHASE_MARK(11);
             load_train_weights(S, a.params, true);
             zero_grads(g);
             __syncthreads();
+            PHASE_MARK(12);
         }
     }
     cp_async_wait_all();
@@ -675,3 +704,15 @@ template __global__ void train_partial_kernel<32>(TrainArgs, long);
 template __global__ void train_partial_kernel<64>(TrainArgs, long);
 
 }  // namespace gbxcu
+
+#ifdef GBX_PHASE_TIMING
+extern "C" int gbxcu_debug_phase_cycles(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, gbxcu::g_phase_cycles, sizeof(unsigned long long) * 16) != cudaSuccess)
+        return 3;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(gbxcu::g_phase_cycles, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
