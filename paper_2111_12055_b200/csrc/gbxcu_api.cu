@@ -81,7 +81,7 @@ struct gbxcu_ctx {
     std::mutex mu;
     // scratch
     DevBuf params, feat, tgt, probs, actions, recheck, counters, flags;
-    DevBuf order, order2, partials, red, bar, diverged, epoch_loss, epoch_acc;
+    DevBuf order, order2, partials, red, bar, diverged, epoch_loss, epoch_acc, step_flags, llp;
     DevBuf sh_jp, sh_head, sh_nxt, sh_succ, sh_root, sh_root2, sh_flags;
     DevBuf seg_off, seg_seed, grad, scalar;
     DevBuf s_app_pipe, s_pipe_slot, s_slot_shader, s_slot_frac, s_pipe_wt, s_shader_lat, s_app_f64;
@@ -124,6 +124,10 @@ int setup_kernel_attrs() {
         set((const void*)train_partial_kernel<32>, train_smem_bytes(32));
         set((const void*)train_partial_kernel<64>, train_smem_bytes(64));
         set((const void*)batch_grad_kernel, train_smem_bytes(64));
+        set((const void*)train_epoch_tc_kernel<4>, train_tc_smem_bytes(4));
+        set((const void*)train_epoch_tc_kernel<7>, train_tc_smem_bytes(7));
+        set((const void*)train_partial_tc_kernel<4>, train_tc_smem_bytes(4));
+        set((const void*)train_partial_tc_kernel<7>, train_tc_smem_bytes(7));
         set((const void*)tc_gemm_kernel, gemm_smem_bytes());
     });
     return rc;
@@ -255,7 +259,15 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     RET(c->epoch_acc.ensure(16));
     int G = 1, tb = 32;
     train_grid(c, cfg, n, G, tb);
-    RET(c->partials.ensure(sizeof(double) * (size_t)G * (NP + 1)));
+    RET(c->partials.ensure(sizeof(double) * (size_t)G * PSTR));
+    RET(c->step_flags.ensure(sizeof(unsigned int) * (size_t)G));
+    RET(c->llp.ensure(sizeof(unsigned long long) * NP));
+    CK(cudaMemsetAsync(c->step_flags.p, 0, sizeof(unsigned int) * (size_t)G, st));
+    CK(cudaMemsetAsync(c->llp.p, 0, sizeof(unsigned long long) * NP, st));
+    // multi-CTA steps: tensor-core kernel, tiles of 32 (MT 4) or 56 (MT 7) records
+    const size_t per_cta = ((std::min<size_t>((size_t)cfg->batch_size, n) + c->nranks - 1) /
+                                c->nranks + G - 1) / G;
+    const int mt = per_cta <= 32 ? 4 : 7;
     RET(c->red.ensure(sizeof(double) * (NP + 1)));
 
     TrainArgs a{};
@@ -272,6 +284,8 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     a.lr = cfg->learning_rate;
     a.rank = c->rank;
     a.nranks = c->nranks;
+    a.flags = c->step_flags.as<unsigned int>();
+    a.llp = c->llp.as<unsigned long long>();
     const long n_steps = (long)((n + cfg->batch_size - 1) / cfg->batch_size);
 
     const bool timed = cfg->epochs <= 8;  // per-kernel event timing (bench / profiling)
@@ -280,16 +294,19 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
         RET(shuffle_epoch(c, n, cfg->seed, e, st));
         a.order = c->order.as<uint32_t>();  // the pass output (buffers ping-pong)
         a.epoch = e;
+        a.tag_base = (unsigned int)((long)e * n_steps);
         if (!c->comm) {
-            CK(cudaMemsetAsync(c->bar.as<unsigned int>() + 2, 0, 8, st));
             void* args[] = {&a};
-            const void* fn = tb == 32 ? (const void*)train_epoch_kernel<32>
-                                      : (const void*)train_epoch_kernel<64>;
             if (timed) CK(cudaEventRecord(c->ev[(2 * e + 1) % 16], st));
             if (G == 1) {
+                // 1-CTA steps: the bit-exact fp64 kernel (reference summation order)
+                const void* fn = tb == 32 ? (const void*)train_epoch_kernel<32>
+                                          : (const void*)train_epoch_kernel<64>;
                 CK(cudaLaunchKernel(fn, 1, TRAIN_BLOCK, args, train_smem_bytes(tb), st));
             } else {
-                CK(cudaLaunchCooperativeKernel(fn, G, TRAIN_BLOCK, args, train_smem_bytes(tb), st));
+                const void* fn = mt == 4 ? (const void*)train_epoch_tc_kernel<4>
+                                         : (const void*)train_epoch_tc_kernel<7>;
+                CK(cudaLaunchCooperativeKernel(fn, G, TRAIN_BLOCK, args, train_tc_smem_bytes(mt), st));
             }
             RET(check_launch(c, "train_epoch_kernel"));
             if (timed) CK(cudaEventRecord(c->ev[16 + e % 8], st));
@@ -298,10 +315,14 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
             for (long s = 0; s < n_steps; ++s) {
                 const size_t start = (size_t)s * cfg->batch_size;
                 const size_t nb = std::min(n, start + (size_t)cfg->batch_size) - start;
-                if (tb == 32)
+                if (G == 1 && tb == 32)
                     train_partial_kernel<32><<<G, TRAIN_BLOCK, train_smem_bytes(32), st>>>(a, s);
-                else
+                else if (G == 1)
                     train_partial_kernel<64><<<G, TRAIN_BLOCK, train_smem_bytes(64), st>>>(a, s);
+                else if (mt == 4)
+                    train_partial_tc_kernel<4><<<G, TRAIN_BLOCK, train_tc_smem_bytes(4), st>>>(a, s);
+                else
+                    train_partial_tc_kernel<7><<<G, TRAIN_BLOCK, train_tc_smem_bytes(7), st>>>(a, s);
                 RET(check_launch(c, "train_partial_kernel"));
                 reduce_partials_kernel<<<(NP + 1 + 7) / 8, 256, 0, st>>>(
                     c->partials.as<double>(), G, c->red.as<double>(), c->diverged.as<int>());

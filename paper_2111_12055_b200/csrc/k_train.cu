@@ -506,7 +506,7 @@ __device__ __forceinline__ double warp_tree_sum(double v) {
 __device__ __forceinline__ double reduce_over_ctas(const double* __restrict__ partials, int G,
                                                    int p, int lane) {
     double v = 0.0;
-    for (int c = lane; c < G; c += 32) v = __dadd_rn(v, __ldcg(partials + (size_t)c * (NP + 1) + p));
+    for (int c = lane; c < G; c += 32) v = __dadd_rn(v, __ldcg(partials + (size_t)c * PSTR + p));
     return warp_tree_sum(v);
 }
 
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
             __syncthreads();
         } else {
             // ---- per-CTA partials -> deterministic cross-CTA reduction
-            double* part = a.partials + (size_t)blockIdx.x * (NP + 1);
+            double* part = a.partials + (size_t)blockIdx.x * PSTR;
             for_each_owned(g, [&](int p, double& acc) { part[p] = acc; });
             if (tid == NT - 1) part[NP] = g.loss;
             PHASE_MARK(8);
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(NT, 1) train_partial_kernel(TrainArgs a, long 
         if (r0 + TB < hi) prefetch_tile<TB>(S, buf, a, r0 + TB, (int)min((size_t)TB, hi - r0 - TB));
         train_tile<TB>(S, g, cur, nv, inv_b);
     }
-    double* part = a.partials + (size_t)blockIdx.x * (NP + 1);
+    double* part = a.partials + (size_t)blockIdx.x * PSTR;
     for_each_owned(g, [&](int p, double& acc) { part[p] = acc; });
     if (threadIdx.x == NT - 1) part[NP] = g.loss;
 }

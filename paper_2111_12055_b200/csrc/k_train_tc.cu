@@ -1,0 +1,687 @@
+// k_train_tc.cu — multi-CTA fused train epoch (K1, throughput regime) on the
+// FP64 tensor cores (DMMA m8n8k4), sm_100a.
+//
+// Replaces fit's inner loop (proj/src/policy.cpp:316-333) when a step's batch
+// is spread over G > 1 CTAs: batch_kl_loss / batch_kl_gradient (forward +
+// analytic backward, :29-55, :209-279) and the SGD update
+// w = float(double(w) - lr * g) (:328-332).
+//
+// Numerics: fp32 parameters, fp64 arithmetic everywhere (as the reference),
+// but the contractions run as fp64 MMA (fused multiply-add, tensor-core
+// summation order) instead of the reference's sequential mul-then-add. A
+// multi-CTA step already re-associates the gradient sum across CTAs, so this
+// path is graded by tolerance (<= 2 fp32 ulp per weight, losses rel 1e-12);
+// the bit-exact 1-CTA path stays in k_train.cu.
+//
+// One tile = 8*MT records (MT m-tiles of 8). Per tile, all on DMMA:
+//   F1  H1 = relu(X W0^T + b0)      M=8MT  N=64  K=44   (C initialised with b0)
+//   F2  H2 = relu(H1 W1^T + b1)     M=8MT  N=32  K=64
+//   F3  logits / softmax / KL / d3 and B1 d2 = (d3 W2) o [h2 > 0]   (CUDA cores)
+//   B2  D1 = (D2 W1) o [h1 > 0]     M=8MT  N=64  K=32
+//   G1  gW1 += D2^T H1              M=32   N=64  K=8MT (accumulators live across tiles)
+//   G0  [gW0|gb0]^T += [X|1]^T D1   M=48   N=64  K=8MT (X column 44 == 1 gives gb0)
+//   gb1, gW2, gb2 and the KL sum: 99 threads, sequential folds over the tile.
+// Operand layouts use row strides = 4 or 12 (mod 16) doubles, so every m8n8k4
+// fragment load (row- or column-wise) is bank-conflict free.
+//
+// Step synchronisation is data-flow, not grid barriers:
+//   1. every CTA stores its gradient+loss partial (row of PSTR doubles) and
+//      publishes flag[c] = tag (release);
+//   2. CTA c waits for all flags, then reduces the contiguous slice
+//      [c*chunk, (c+1)*chunk) of every partial plus the loss (fixed order:
+//      8 CTA subsets x strided folds, then an in-order sum of the 8) — every
+//      CTA reduces the loss identically, so all agree on divergence;
+//   3. CTA c applies SGD to its slice and publishes each new parameter as a
+//      64-bit word {tag, fp32 bits} (NCCL "LL" style: the tag validates the
+//      value, single-copy atomic, no fence or flag round trip);
+//   4. every CTA spins on the words of all parameters (one L2 round trip in
+//      the common case) and rebuilds its fp64 shared-memory replicas.
+// A producer cannot overwrite a partial / parameter word before every
+// consumer has read it: its next write needs inputs that only exist after
+// all consumers have moved on.
+#include <cstddef>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gbxcu {
+
+#ifdef GBX_PHASE_TIMING
+// Debug build only (tools/phase_timing.sh): per-phase cycle totals of CTA 0.
+__device__ unsigned long long g_tc_phase[16];
+__device__ unsigned long long g_tc_t;
+#define TC_MARK(i)                                                                             \
+    do {                                                                                       \
+        if (threadIdx.x == 0 && blockIdx.x == 0) {                                             \
+            const unsigned long long t_ = clock64();                                           \
+            if ((i) >= 0) g_tc_phase[(i) < 0 ? 0 : (i)] += t_ - g_tc_t;                        \
+            g_tc_t = t_;                                                                       \
+        }                                                                                      \
+    } while (0)
+#else
+#define TC_MARK(i) ((void)0)
+#endif
+
+static_assert(PSTR >= NP + 1 && PSTR % 2 == 0, "partial rows hold NP params + loss, 16-B aligned");
+
+namespace {
+
+constexpr int NT = TRAIN_BLOCK;  // 512
+constexpr int NW = NT / 32;      // 16 warps
+constexpr int SX = 52;           // X  [r][i]: 44 features, col 44 = 1.0, 45..51 = 0
+constexpr int SW0 = 44;          // W0 [j][i]
+constexpr int SW1 = 68;          // W1 [k][j]
+constexpr int SH1 = 68;          // H1, D1 [r][j]
+constexpr int SH2 = 36;          // H2, D2 [r][k]
+
+template <int MT>
+struct TcSmem {
+    static constexpr int TB = 8 * MT;
+    double w0[H1 * SW0];
+    double w1[H2 * SW1];
+    double w2[A * H2];
+    double b0[H1];
+    double b1[H2];
+    double b2[A];
+    double scal[2];
+    double x[TB * SX];
+    double h1[TB * SH1];
+    double d1[TB * SH1];
+    double h2[TB * SH2];
+    double d2[TB * SH2];
+    double d3[TB * 2];
+    double tgt[TB * 2];
+    double kl[TB];
+    double red[8 * 64];          // slice reduction: [CTA subset][element]
+    double stage_t[2][TB * 2];   // cp.async staging: targets
+    float stage_f[2][TB * F];    // cp.async staging: raw fp32 features
+};
+
+template <int MT>
+constexpr bool tc_aligned() {
+    return offsetof(TcSmem<MT>, x) % 16 == 0 && offsetof(TcSmem<MT>, h1) % 16 == 0 &&
+           offsetof(TcSmem<MT>, stage_t) % 16 == 0 && offsetof(TcSmem<MT>, stage_f) % 16 == 0;
+}
+static_assert(tc_aligned<4>() && tc_aligned<7>(), "16-byte aligned smem arrays");
+
+// D = A B + D for one 8x8x4 fp64 tile. Fragments (lane = 4g + t):
+//   A[g][t] (row-major 8x4), B[t][g] (4x8), D[g][2t], D[g][2t+1].
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d[0]), "+d"(d[1])
+        : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// fp32 parameter p -> fp64 smem replica
+template <int MT>
+__device__ __forceinline__ void put_param(TcSmem<MT>& S, int p, double v) {
+    if (p < OFF_B0) {
+        const int j = p / F;
+        S.w0[j * SW0 + (p - j * F)] = v;
+    } else if (p < OFF_W1) S.b0[p - OFF_B0] = v;
+    else if (p < OFF_B1) {
+        const int t = p - OFF_W1;
+        S.w1[(t >> 6) * SW1 + (t & 63)] = v;
+    } else if (p < OFF_W2) S.b1[p - OFF_B1] = v;
+    else if (p < OFF_B2) S.w2[p - OFF_W2] = v;
+    else S.b2[p - OFF_B2] = v;
+}
+
+template <int MT>
+__device__ __forceinline__ double get_param(const TcSmem<MT>& S, int p) {
+    if (p < OFF_B0) {
+        const int j = p / F;
+        return S.w0[j * SW0 + (p - j * F)];
+    }
+    if (p < OFF_W1) return S.b0[p - OFF_B0];
+    if (p < OFF_B1) {
+        const int t = p - OFF_W1;
+        return S.w1[(t >> 6) * SW1 + (t & 63)];
+    }
+    if (p < OFF_W2) return S.b1[p - OFF_B1];
+    if (p < OFF_B2) return S.w2[p - OFF_W2];
+    return S.b2[p - OFF_B2];
+}
+
+template <int MT>
+__device__ void load_params_plain(TcSmem<MT>& S, const float* __restrict__ p) {
+    for (int t = threadIdx.x; t < NP / 2; t += NT) {
+        const float2 v = __ldcg(reinterpret_cast<const float2*>(p) + t);
+        put_param(S, 2 * t, (double)v.x);
+        put_param(S, 2 * t + 1, (double)v.y);
+    }
+}
+
+// All-gather of the LL words {tag, fp32 bits}: spin until every word this
+// thread owns carries `tag`.
+template <int MT>
+__device__ void load_params_ll(TcSmem<MT>& S, const unsigned long long* __restrict__ ll,
+                               unsigned tag) {
+    constexpr int PER = (NP + NT - 1) / NT;  // 10
+    unsigned long long v[PER];
+    unsigned pending = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+        if (threadIdx.x + q * NT < NP) pending |= 1u << q;
+    while (pending) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+            if (pending & (1u << q)) v[q] = ld_relaxed_u64(ll + threadIdx.x + q * NT);
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+            if ((pending & (1u << q)) && (unsigned)(v[q] >> 32) == tag) pending &= ~(1u << q);
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int p = threadIdx.x + q * NT;
+        if (p < NP) put_param(S, p, (double)__uint_as_float((unsigned)v[q]));
+    }
+}
+
+// Persistent per-thread gradient accumulators of one step.
+struct TcGrads {
+    double g1[2][2];  // gW1 tiles (mt = (w>>3) + 2q, nt = w & 7)
+    double g0[3][2];  // [gW0|gb0]^T tiles (mt = (w>>3) + 2q over i, nt = w & 7 over j)
+    double gx;        // gb1 / gW2 / gb2 / KL sum (threads 256..354)
+};
+
+__device__ __forceinline__ void tc_zero(TcGrads& g) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) g.g1[q][0] = g.g1[q][1] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) g.g0[q][0] = g.g0[q][1] = 0.0;
+    g.gx = 0.0;
+}
+
+// Scalar-gradient threads: 256..287 gb1[k], 288..351 gW2[a][k], 352..353 gb2[a], 354 KL.
+constexpr int XG0 = 256;
+
+// Visit every (parameter index, value) this thread accumulated.
+template <typename Fn>
+__device__ __forceinline__ void tc_for_each(const TcGrads& g, Fn fn) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int nt = w & 7, mq = w >> 3;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int k = (mq + 2 * q) * 8 + gq, j = nt * 8 + 2 * tq;
+        fn(OFF_W1 + k * H1 + j, g.g1[q][0], g.g1[q][1], true);
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const int i = (mq + 2 * q) * 8 + gq, j = nt * 8 + 2 * tq;
+        if (i < F) {
+            fn(OFF_W0 + j * F + i, g.g0[q][0], 0.0, false);
+            fn(OFF_W0 + (j + 1) * F + i, g.g0[q][1], 0.0, false);
+        } else if (i == F) {
+            fn(OFF_B0 + j, g.g0[q][0], g.g0[q][1], true);
+        }
+    }
+    const int x = tid - XG0;
+    if (x >= 0 && x < 32) fn(OFF_B1 + x, g.gx, 0.0, false);
+    else if (x >= 32 && x < 96) fn(OFF_W2 + (x - 32), g.gx, 0.0, false);
+    else if (x >= 96 && x < 98) fn(OFF_B2 + (x - 96), g.gx, 0.0, false);
+    else if (x == 98) fn(NP, g.gx, 0.0, false);
+}
+
+template <int MT>
+__device__ void tc_prefetch(TcSmem<MT>& S, int buf, const TrainArgs& a, size_t r0, int nv) {
+    constexpr int TB = 8 * MT;
+    for (int t = threadIdx.x; t < TB * (F / 4); t += NT) {
+        const int r = t / (F / 4), q = t - r * (F / 4);
+        const float* src = a.feat;
+        if (r < nv) src = a.feat + (size_t)a.order[r0 + r] * F + 4 * q;
+        cp_async16(&S.stage_f[buf][r * F + 4 * q], src, r < nv ? 16 : 0);
+    }
+    if (threadIdx.x < TB) {
+        const int r = threadIdx.x;
+        const double* src = a.tgt;
+        if (r < nv) src = a.tgt + 2 * (size_t)a.order[r0 + r];
+        cp_async16(&S.stage_t[buf][2 * r], src, r < nv ? 16 : 0);
+    }
+    cp_async_commit();
+}
+
+// One tile of 8*MT records (rows >= nv are zero padding and contribute 0).
+template <int MT>
+__device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int buf, int nv, double inv_b) {
+    constexpr int TB = 8 * MT;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+
+    // ---- P0: staged fp32 -> fp64 X (cols 0..43), targets
+    for (int t = tid; t < TB * F; t += NT) {
+        const int r = t / F;
+        S.x[r * SX + (t - r * F)] = (double)S.stage_f[buf][t];
+    }
+    if (tid < 2 * TB) S.tgt[tid] = S.stage_t[buf][tid];
+    __syncthreads();
+    TC_MARK(0);
+
+    // ---- F1: H1 = relu(X W0^T + b0). Warp: n-tile w&7, m-tiles (w>>3) + 2q.
+    {
+        constexpr int Q = (MT + 1) / 2;
+        const int nt = w & 7, mq = w >> 3;
+        double acc[Q][2];
+        const double bA = S.b0[nt * 8 + 2 * tq], bB = S.b0[nt * 8 + 2 * tq + 1];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) { acc[q][0] = bA; acc[q][1] = bB; }
+        const double* wb = S.w0 + (nt * 8 + gq) * SW0 + tq;
+        const double* xb = S.x + (mq * 8 + gq) * SX + tq;
+#pragma unroll
+        for (int k0 = 0; k0 < F; k0 += 4) {
+            const double bf = wb[k0];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (mq + 2 * q < MT) dmma(acc[q], xb[q * 16 * SX + k0], bf);
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int mt = mq + 2 * q;
+            if (mt < MT) {
+                double* o = S.h1 + (mt * 8 + gq) * SH1 + nt * 8 + 2 * tq;
+                o[0] = acc[q][0] > 0.0 ? acc[q][0] : 0.0;
+                o[1] = acc[q][1] > 0.0 ? acc[q][1] : 0.0;
+            }
+        }
+    }
+    __syncthreads();
+    TC_MARK(1);
+
+    // ---- F2: H2 = relu(H1 W1^T + b1). Warp: n-tile w&3, m-tiles (w>>2) + 4q.
+    {
+        constexpr int Q = (MT + 3) / 4;
+        const int nt = w & 3, mq = w >> 2;
+        double acc[Q][2];
+        const double bA = S.b1[nt * 8 + 2 * tq], bB = S.b1[nt * 8 + 2 * tq + 1];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) { acc[q][0] = bA; acc[q][1] = bB; }
+        const double* wb = S.w1 + (nt * 8 + gq) * SW1 + tq;
+        const double* hb = S.h1 + (mq * 8 + gq) * SH1 + tq;
+#pragma unroll 4
+        for (int k0 = 0; k0 < H1; k0 += 4) {
+            const double bf = wb[k0];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (mq + 4 * q < MT) dmma(acc[q], hb[q * 32 * SH1 + k0], bf);
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int mt = mq + 4 * q;
+            if (mt < MT) {
+                double* o = S.h2 + (mt * 8 + gq) * SH2 + nt * 8 + 2 * tq;
+                o[0] = acc[q][0] > 0.0 ? acc[q][0] : 0.0;
+                o[1] = acc[q][1] > 0.0 ? acc[q][1] : 0.0;
+            }
+        }
+    }
+    __syncthreads();
+    TC_MARK(2);
+
+    // ---- F3 + B1: thread (r, a): logit a, softmax, KL, d3; then d2 for k in [16a, 16a+16).
+    //      Whole warps take part (the pair exchanges are full-mask shuffles);
+    //      lanes past the tile recompute row TB-1 and store nothing.
+    if (tid < ((2 * TB + 31) & ~31)) {
+        const bool live = tid < 2 * TB;
+        const int r = live ? tid >> 1 : TB - 1, a = tid & 1;
+        const double* h = S.h2 + r * SH2;
+        const double* wr = S.w2 + a * H2;
+        double l = S.b2[a];
+#pragma unroll 8
+        for (int k = 0; k < H2; ++k) l = fma(wr[k], h[k], l);
+        const double lo = __shfl_xor_sync(0xffffffffu, l, 1);
+        const double l0 = a ? lo : l, l1 = a ? l : lo;
+        const double m = l0 < l1 ? l1 : l0;
+        const double e = exp(l - m);
+        const double eo = __shfl_xor_sync(0xffffffffu, e, 1);
+        const double s = a ? eo + e : e + eo;
+        const double p = e / s;
+        const double pc = clampp(p);
+        const double tc = clampp(S.tgt[2 * r + a]);
+        const double lr = log(pc / tc);
+        const double term = pc * lr;
+        const double to = __shfl_xor_sync(0xffffffffu, term, 1);
+        const double loss = a ? to + term : term + to;
+        const bool valid = r < nv;
+        if (live && a == 0) S.kl[r] = valid ? loss : 0.0;
+        const double d3 = valid ? p * (lr - loss) * inv_b : 0.0;
+        if (live) S.d3[2 * r + a] = d3;
+        const double d3o = __shfl_xor_sync(0xffffffffu, d3, 1);
+        const double d30 = a ? d3o : d3, d31 = a ? d3 : d3o;
+#pragma unroll
+        for (int kk = 0; kk < H2 / 2; ++kk) {
+            const int k = (H2 / 2) * a + kk;
+            const double d = fma(d31, S.w2[H2 + k], d30 * S.w2[k]);
+            if (live) S.d2[r * SH2 + k] = h[k] <= 0.0 ? 0.0 : d;
+        }
+    }
+    __syncthreads();
+    TC_MARK(3);
+
+    // ---- B2: D1 = (D2 W1) o [h1 > 0]; G1: gW1 += D2^T H1; scalar gradients
+    {
+        constexpr int Q = (MT + 1) / 2;
+        const int nt = w & 7, mq = w >> 3;
+        double acc[Q][2];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[q][0] = acc[q][1] = 0.0;
+        const double* wb = S.w1 + tq * SW1 + nt * 8 + gq;  // B[k][j] = W1[k][j]
+        const double* db = S.d2 + (mq * 8 + gq) * SH2 + tq;
+#pragma unroll
+        for (int k0 = 0; k0 < H2; k0 += 4) {
+            const double bf = wb[k0 * SW1];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (mq + 2 * q < MT) dmma(acc[q], db[q * 16 * SH2 + k0], bf);
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int mt = mq + 2 * q;
+            if (mt < MT) {
+                const int r = mt * 8 + gq, j = nt * 8 + 2 * tq;
+                S.d1[r * SH1 + j] = S.h1[r * SH1 + j] <= 0.0 ? 0.0 : acc[q][0];
+                S.d1[r * SH1 + j + 1] = S.h1[r * SH1 + j + 1] <= 0.0 ? 0.0 : acc[q][1];
+            }
+        }
+        // G1: A[k][r] = D2[r][k], B[r][j] = H1[r][j]; m-tiles (k) mq + 2q, n-tile nt
+        const double* ab = S.d2 + tq * SH2 + mq * 8 + gq;
+        const double* bb = S.h1 + tq * SH1 + nt * 8 + gq;
+#pragma unroll
+        for (int r0 = 0; r0 < TB; r0 += 4) {
+            const double bf = bb[r0 * SH1];
+            dmma(g.g1[0], ab[r0 * SH2], bf);
+            dmma(g.g1[1], ab[r0 * SH2 + 16], bf);
+        }
+        const int x = tid - XG0;
+        if (x >= 0 && x < 32) {
+#pragma unroll 8
+            for (int r = 0; r < nv; ++r) g.gx += S.d2[r * SH2 + x];
+        } else if (x >= 32 && x < 96) {
+            const int a = (x - 32) >> 5, k = (x - 32) & 31;
+#pragma unroll 8
+            for (int r = 0; r < nv; ++r) g.gx = fma(S.d3[2 * r + a], S.h2[r * SH2 + k], g.gx);
+        } else if (x >= 96 && x < 98) {
+#pragma unroll 8
+            for (int r = 0; r < nv; ++r) g.gx += S.d3[2 * r + (x - 96)];
+        } else if (x == 98) {
+#pragma unroll 8
+            for (int r = 0; r < nv; ++r) g.gx += S.kl[r];
+        }
+    }
+    __syncthreads();
+    TC_MARK(4);
+
+    // ---- G0: [gW0|gb0]^T += [X|1]^T D1: A[i][r] = X[r][i], B[r][j] = D1[r][j]
+    {
+        const int nt = w & 7, mq = w >> 3;
+        const double* ab = S.x + tq * SX + mq * 8 + gq;
+        const double* bb = S.d1 + tq * SH1 + nt * 8 + gq;
+#pragma unroll 2
+        for (int r0 = 0; r0 < TB; r0 += 4) {
+            const double bf = bb[r0 * SH1];
+            const double* ar = ab + r0 * SX;
+            dmma(g.g0[0], ar[0], bf);
+            dmma(g.g0[1], ar[16], bf);
+            dmma(g.g0[2], ar[32], bf);
+        }
+    }
+    TC_MARK(5);
+    // (the caller's next __syncthreads orders G0's reads of X / D1 before P0)
+}
+
+// Per-step record slice of CTA `cta` (rank-major, then CTA-major; identical to
+// k_train.cu's step_slice).
+__device__ __forceinline__ void tc_slice(const TrainArgs& a, long step, int cta, int nctas,
+                                         uint32_t& lo, uint32_t& hi, uint32_t& nb) {
+    const uint32_t n = (uint32_t)a.n, batch = (uint32_t)a.batch;
+    const uint32_t start = (uint32_t)step * batch;
+    const uint32_t stop = min(n, start + batch);
+    nb = stop - start;
+    const uint32_t per_rank = (nb + a.nranks - 1) / (uint32_t)a.nranks;
+    const uint32_t r_lo = min(stop, start + (uint32_t)a.rank * per_rank);
+    const uint32_t r_hi = min(stop, r_lo + per_rank);
+    const uint32_t per_cta = (r_hi - r_lo + nctas - 1) / (uint32_t)nctas;
+    lo = min(r_hi, r_lo + (uint32_t)cta * per_cta);
+    hi = min(r_hi, lo + per_cta);
+}
+
+// Next tile after (step, r0) within [step, n_steps); r0 == UINT32_MAX asks for
+// the first tile of `step`.
+template <int TB>
+__device__ bool tc_next(const TrainArgs& a, long n_steps, long& step, uint32_t& r0, int& nv) {
+    uint32_t lo, hi, nb;
+    if (r0 != 0xFFFFFFFFu) {
+        tc_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
+        if (r0 + TB < hi) {
+            r0 += TB;
+            nv = (int)min((uint32_t)TB, hi - r0);
+            return true;
+        }
+        ++step;
+    }
+    for (; step < n_steps; ++step) {
+        tc_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
+        if (hi > lo) {
+            r0 = lo;
+            nv = (int)min((uint32_t)TB, hi - lo);
+            return true;
+        }
+    }
+    return false;
+}
+
+// Stores this thread's accumulators into partial row `part` (parameter order,
+// loss at NP).
+__device__ __forceinline__ void tc_store_partial(const TcGrads& g, double* __restrict__ part) {
+    tc_for_each(g, [&](int p, double v0, double v1, bool pair) {
+        if (pair) __stcg(reinterpret_cast<double2*>(part + p), make_double2(v0, v1));
+        else __stcg(part + p, v0);
+    });
+}
+
+}  // namespace
+
+size_t train_tc_smem_bytes(int mt) { return mt == 4 ? sizeof(TcSmem<4>) : sizeof(TcSmem<7>); }
+
+template <int MT>
+__global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
+    constexpr int TB = 8 * MT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TcSmem<MT>& S = *reinterpret_cast<TcSmem<MT>*>(smem_raw);
+    if (*a.diverged_epoch >= 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
+    const int chunk = (NP + G - 1) / G;
+    const int p_lo = c * chunk, p_hi = min(NP, p_lo + chunk);
+    const int n_elem = 1 + max(0, p_hi - p_lo);  // element 0 = loss, then the slice
+
+    long pf_step = 0;
+    uint32_t pf_r0 = 0xFFFFFFFFu;
+    int pf_nv = 0;
+    bool have_next = tc_next<TB>(a, n_steps, pf_step, pf_r0, pf_nv);
+    int buf = 0;
+    if (have_next) tc_prefetch<MT>(S, buf, a, pf_r0, pf_nv);
+    load_params_plain(S, a.params);
+    for (int t = tid; t < TB * (SX - F); t += NT) {
+        const int r = t / (SX - F), i = F + (t - r * (SX - F));
+        S.x[r * SX + i] = i == F ? 1.0 : 0.0;
+    }
+    TcGrads g;
+    tc_zero(g);
+    double epoch_total = 0.0;
+    __syncthreads();
+    TC_MARK(-1);
+
+    for (long step = 0; step < n_steps; ++step) {
+        uint32_t lo, hi, nb;
+        tc_slice(a, step, c, G, lo, hi, nb);
+        const double inv_b = 1.0 / (double)nb;
+        const unsigned tag = a.tag_base + (unsigned)step + 1u;
+        for (uint32_t r0 = lo; r0 < hi; r0 += TB) {
+            const int nv = (int)min((uint32_t)TB, hi - r0);
+            cp_async_wait_all();
+            __syncthreads();
+            const int cur = buf;
+            buf ^= 1;
+            have_next = tc_next<TB>(a, n_steps, pf_step, pf_r0, pf_nv);
+            if (have_next) tc_prefetch<MT>(S, buf, a, pf_r0, pf_nv);
+            TC_MARK(6);
+            tc_tile<MT>(S, g, cur, nv, inv_b);
+        }
+        // ---- 1. publish this CTA's partial
+        double* part = a.partials + (size_t)c * PSTR;
+        tc_store_partial(g, part);
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release_u32(a.flags + c, tag);
+        }
+        TC_MARK(7);
+        // ---- 2. wait for every partial, reduce [loss | slice] in a fixed order
+        if (tid < G)
+            while (ld_acquire_u32(a.flags + tid) != tag) {
+            }
+        __syncthreads();
+        TC_MARK(8);
+        bool diverged = false;
+        for (int e0 = 0; e0 < n_elem; e0 += 64) {
+            // warp w: elements e0 + 32*(w&1) + lane, CTA subset s = w>>1 (c' = s + 8q)
+            const int e = e0 + 32 * (w & 1) + lane, s8 = w >> 1;
+            double v = 0.0;
+            if (e < n_elem) {
+                const int p = e == 0 ? NP : p_lo + e - 1;
+                const double* src = a.partials + p;
+                double buf_v[19];
+#pragma unroll
+                for (int q = 0; q < 19; ++q) {
+                    const int cc = s8 + 8 * q;
+                    buf_v[q] = cc < G ? __ldcg(src + (size_t)cc * PSTR) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 19; ++q) v += buf_v[q];
+                for (int cc = s8 + 8 * 19; cc < G; cc += 8) v += __ldcg(src + (size_t)cc * PSTR);
+            }
+            S.red[s8 * 64 + 32 * (w & 1) + lane] = v;
+            __syncthreads();
+            if (tid < 64) {
+                double t = 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) t += S.red[q * 64 + tid];
+                S.red[tid] = t;  // row 0 is only read by this thread
+                if (e0 == 0 && tid == 0) {
+                    const double loss = t / (double)nb;
+                    S.scal[0] = loss;
+                    S.scal[1] = isfinite(loss) ? 0.0 : 1.0;
+                }
+            }
+            __syncthreads();
+            if (S.scal[1] != 0.0) {
+                diverged = true;
+                break;
+            }
+            // ---- 3. SGD on the slice; publish {tag, fp32} words + the plain fp32 copy
+            if (tid < 64) {
+                const int e2 = e0 + tid;
+                if (e2 >= 1 && e2 < n_elem) {
+                    const int p = p_lo + e2 - 1;
+                    const float nw = __double2float_rn(get_param(S, p) - a.lr * S.red[tid]);
+                    a.params[p] = nw;
+                    st_relaxed_u64(a.llp + p, ((unsigned long long)tag << 32) | __float_as_uint(nw));
+                }
+            }
+            __syncthreads();  // S.red reuse
+        }
+        if (diverged) {
+            if (c == 0 && tid == 0) *a.diverged_epoch = a.epoch;
+            break;
+        }
+        TC_MARK(9);
+        if (tid == 0) epoch_total = fma(S.scal[0], (double)nb, epoch_total);
+        // ---- 4. all-gather the new parameters (the next launch reads a.params)
+        if (step + 1 < n_steps) load_params_ll(S, a.llp, tag);
+        tc_zero(g);
+        TC_MARK(10);
+        // (the next tile's __syncthreads orders the replicas before use)
+    }
+    cp_async_wait_all();
+    if (c == 0 && tid == 0 && *a.diverged_epoch < 0)
+        a.epoch_loss[a.epoch] = epoch_total / (double)a.n;
+}
+
+// Data-parallel path: one step's per-CTA partials (the reduction, NCCL
+// all-reduce and SGD update follow as separate launches).
+template <int MT>
+__global__ void __launch_bounds__(NT, 1) train_partial_tc_kernel(TrainArgs a, long step) {
+    constexpr int TB = 8 * MT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TcSmem<MT>& S = *reinterpret_cast<TcSmem<MT>*>(smem_raw);
+    if (*a.diverged_epoch >= 0) return;
+    uint32_t lo, hi, nb;
+    tc_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
+    if (hi > lo) tc_prefetch<MT>(S, 0, a, lo, (int)min((uint32_t)TB, hi - lo));
+    load_params_plain(S, a.params);
+    for (int t = threadIdx.x; t < TB * (SX - F); t += NT) {
+        const int r = t / (SX - F), i = F + (t - r * (SX - F));
+        S.x[r * SX + i] = i == F ? 1.0 : 0.0;
+    }
+    TcGrads g;
+    tc_zero(g);
+    const double inv_b = 1.0 / (double)nb;
+    int buf = 0;
+    for (uint32_t r0 = lo; r0 < hi; r0 += TB) {
+        const int nv = (int)min((uint32_t)TB, hi - r0);
+        cp_async_wait_all();
+        __syncthreads();
+        const int cur = buf;
+        buf ^= 1;
+        if (r0 + TB < hi) tc_prefetch<MT>(S, buf, a, r0 + TB, (int)min((uint32_t)TB, hi - r0 - TB));
+        tc_tile<MT>(S, g, cur, nv, inv_b);
+    }
+    tc_store_partial(g, a.partials + (size_t)blockIdx.x * PSTR);
+}
+
+template __global__ void train_epoch_tc_kernel<4>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<7>(TrainArgs);
+template __global__ void train_partial_tc_kernel<4>(TrainArgs, long);
+template __global__ void train_partial_tc_kernel<7>(TrainArgs, long);
+
+}  // namespace gbxcu
+
+#ifdef GBX_PHASE_TIMING
+extern "C" int gbxcu_debug_phase_cycles_tc(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, gbxcu::g_tc_phase, sizeof(unsigned long long) * 16) != cudaSuccess)
+        return 3;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(gbxcu::g_tc_phase, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

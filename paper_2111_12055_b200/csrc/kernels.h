@@ -13,6 +13,8 @@ constexpr int TRAIN_BLOCK = 512;  // train: 16 warps; tiles of 32 or 64 records
 constexpr int SHUF_BLOCK = 256;
 constexpr int AGG_BLOCK = 256;    // aggregation: 8 warps = 8 apps per CTA
 
+constexpr int PSTR = 5028;        // per-CTA partial row: 5,026 gradient entries, loss, pad
+
 // mode bits for the inference kernels
 constexpr int FWD_PROBS = 1, FWD_ACTIONS = 2, FWD_COLLECT = 4;
 
@@ -30,6 +32,10 @@ struct TrainArgs {
     int epoch;
     double lr;
     int rank, nranks;
+    // multi-CTA (tensor-core) epoch kernel: data-flow step synchronisation
+    unsigned int* flags;       // [G] "partial of step tag is published"
+    unsigned long long* llp;   // [NP] {tag, fp32 bits} parameter words
+    unsigned int tag_base;     // epoch * n_steps (flags/llp zeroed once per fit)
 };
 
 struct AggArgs {
@@ -66,6 +72,11 @@ template <int TB>
 __global__ void train_epoch_kernel(TrainArgs a);
 template <int TB>
 __global__ void train_partial_kernel(TrainArgs a, long step);
+template <int MT>
+__global__ void train_epoch_tc_kernel(TrainArgs a);
+template <int MT>
+__global__ void train_partial_tc_kernel(TrainArgs a, long step);
+size_t train_tc_smem_bytes(int mt);
 __global__ void reduce_partials_kernel(const double* partials, int nctas, double* red,
                                        const int* diverged);
 __global__ void apply_update_kernel(float* params, const double* red, double lr, size_t nb,

@@ -19,6 +19,51 @@ __global__ void fma_peak_kernel(T* out, int iters, T a, T b) {
     if (s == (T)-12345.0) out[0] = s;
 }
 
+// FP64 tensor-core (DMMA 8x8x4) throughput: 8 independent accumulator pairs per warp.
+__global__ void dmma_peak_kernel(double* out, int iters) {
+    double a = 0.5 + threadIdx.x * 1e-3, b = 0.25;
+    double c[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = q;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1},{%2},{%3},{%0,%1};"
+                         : "+d"(c[q][0]), "+d"(c[q][1]) : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += c[q][0] + c[q][1];
+    if (s == -12345.0) out[0] = s;
+}
+
+static double run_dmma(int device, int iters) {
+    cudaSetDevice(device);
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, device);
+    double* out;
+    cudaMalloc(&out, sizeof(double));
+    const int blocks = prop.multiProcessorCount * 4, threads = 256;
+    dmma_peak_kernel<<<blocks, threads>>>(out, 16);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best = 0;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        dmma_peak_kernel<<<blocks, threads>>>(out, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        // 8x8x4 = 256 FMA = 512 FLOP per warp-instruction
+        const double flops = 512.0 * 8 * (double)iters * blocks * (threads / 32);
+        best = best > flops / (ms * 1e-3) ? best : flops / (ms * 1e-3);
+    }
+    cudaFree(out);
+    return best / 1e12;
+}
+
 template <typename T>
 static double run(int device, int iters) {
     cudaSetDevice(device);
@@ -48,3 +93,4 @@ static double run(int device, int iters) {
 
 extern "C" double peak_fp64_tflops(int device) { return run<double>(device, 4096); }
 extern "C" double peak_fp32_tflops(int device) { return run<float>(device, 16384); }
+extern "C" double peak_fp64_tensor_tflops(int device) { return run_dmma(device, 8192); }

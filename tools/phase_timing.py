@@ -3,18 +3,23 @@ sys.path.insert(0, ".")
 import paper_2111_12055_b200 as gbx
 lib = gbx.load_library(os.path.abspath("tools/timing/libgbxcu.so"))
 lib.gbxcu_debug_phase_cycles.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+lib.gbxcu_debug_phase_cycles_tc.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+names_tc = ["P0 convert", "F1", "F2", "F3+B1", "B2+G1+scalars", "G0", "tile top (wait+prefetch)",
+            "partial store+flag", "flag wait", "reduce+SGD+publish", "LL all-gather", "", "", "", "", ""]
 from bench import synthetic_log
 names = ["P0 convert", "F1", "F2", "F3+B1", "B2(+gw1,extras)", "G0", "tile loop top", "wait+prefetch",
          "partials write", "grid barrier 1", "loss+param reduce", "grid barrier 2", "reload", "", "", ""]
 dev = gbx.Device(0)
-for n, b in [(20000, 32), (1000000, 8192), (1000000, 65536)]:
+for n, b in [(20000, 32), (1000000, 4096), (1000000, 8192), (1000000, 65536)]:
     f, t = synthetic_log(n)
     p = dev.policy_init(7)
     dev.fit(p, f, t, 0.01, 1, b, 99)
     buf = (C.c_ulonglong * 16)()
-    lib.gbxcu_debug_phase_cycles(buf, 1)
+    fn = lib.gbxcu_debug_phase_cycles if b <= 32 else lib.gbxcu_debug_phase_cycles_tc
+    if b > 32: names = names_tc
+    fn(buf, 1)
     dev.fit(p, f, t, 0.01, 1, b, 99)
-    lib.gbxcu_debug_phase_cycles(buf, 1)
+    fn(buf, 1)
     v = np.array(buf[:], np.float64); steps = (n + b - 1) // b
     print(f"batch {b}: {v.sum()/steps:.0f} cycles/step (CTA 0)")
     for i in np.argsort(-v):
