@@ -16,11 +16,14 @@
 // One tile = 8*MT records (MT m-tiles of 8). Per tile, all on DMMA:
 //   F1  H1 = relu(X W0^T + b0)      M=8MT  N=64  K=44   (C initialised with b0)
 //   F2  H2 = relu(H1 W1^T + b1)     M=8MT  N=32  K=64
-//   F3  logits / softmax / KL / d3 and B1 d2 = (d3 W2) o [h2 > 0]   (CUDA cores)
+//   F3  logits = H2 W2^T + b2       M=8MT  N=8(2) K=32  (warp w < MT owns m-tile w)
+//       softmax / KL / d3 in the lanes holding each record's logits, then
+//   B1  D2 = ([d3|0] [W2;0]) o [h2 > 0]   K=4 from the same lanes' registers
 //   B2  D1 = (D2 W1) o [h1 > 0]     M=8MT  N=64  K=32
-//   G1  gW1 += D2^T H1              M=32   N=64  K=8MT (accumulators live across tiles)
+//   G1  [gW1|gb1] += D2^T [H1|1]    M=32   N=72  K=8MT (H1 column 64 == 1 gives gb1)
+//   E   [gW2|gb2; .|KL] += U^T [H2|1]  M=8 N=40 K=8MT (U = [d3_0 d3_1 kl 0..])
 //   G0  [gW0|gb0]^T += [X|1]^T D1   M=48   N=64  K=8MT (X column 44 == 1 gives gb0)
-//   gb1, gW2, gb2 and the KL sum: 99 threads, sequential folds over the tile.
+// Gradient accumulators (G1, E, G0) stay in registers across the tiles of a step.
 // Operand layouts use row strides = 4 or 12 (mod 16) doubles, so every m8n8k4
 // fragment load (row- or column-wise) is bank-conflict free.
 //
@@ -50,6 +53,17 @@ namespace gbxcu {
 // Debug build only (tools/phase_timing.sh): per-phase cycle totals of CTA 0.
 __device__ unsigned long long g_tc_phase[16];
 __device__ unsigned long long g_tc_t;
+__device__ unsigned long long g_tc_trace[8][160][6];  // steps 8..15: per-CTA globaltimer marks
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TC_TRACE(step, k)                                                                      \
+    do {                                                                                       \
+        if (threadIdx.x == 0 && (step) >= 8 && (step) < 16 && blockIdx.x < 160)               \
+            g_tc_trace[(step) - 8][blockIdx.x][k] = gtimer();                                  \
+    } while (0)
 #define TC_MARK(i)                                                                             \
     do {                                                                                       \
         if (threadIdx.x == 0 && blockIdx.x == 0) {                                             \
@@ -60,6 +74,7 @@ __device__ unsigned long long g_tc_t;
     } while (0)
 #else
 #define TC_MARK(i) ((void)0)
+#define TC_TRACE(step, k) ((void)0)
 #endif
 
 static_assert(PSTR >= NP + 1 && PSTR % 2 == 0, "partial rows hold NP params + loss, 16-B aligned");
@@ -72,7 +87,8 @@ constexpr int SX = 52;           // X  [r][i]: 44 features, col 44 = 1.0, 45..51
 constexpr int SW0 = 44;          // W0 [j][i]
 constexpr int SW1 = 68;          // W1 [k][j]
 constexpr int SH1 = 68;          // H1, D1 [r][j]
-constexpr int SH2 = 36;          // H2, D2 [r][k]
+constexpr int SH2 = 36;          // H2, D2 [r][k]: H2 col 32 = 1.0
+constexpr int SU = 12;           // U [r][m]: d3_0, d3_1, kl, then zeros
 
 template <int MT>
 struct TcSmem {
@@ -89,10 +105,10 @@ struct TcSmem {
     double d1[TB * SH1];
     double h2[TB * SH2];
     double d2[TB * SH2];
-    double d3[TB * 2];
+    double u[TB * SU];
     double tgt[TB * 2];
-    double kl[TB];
     double red[8 * 64];          // slice reduction: [CTA subset][element]
+    uint32_t ord[2][TB];         // record indices of the next two tiles (cp.async ring)
     double stage_t[2][TB * 2];   // cp.async staging: targets
     float stage_f[2][TB * F];    // cp.async staging: raw fp32 features
 };
@@ -208,7 +224,7 @@ __device__ void load_params_ll(TcSmem<MT>& S, const unsigned long long* __restri
 struct TcGrads {
     double g1[2][2];  // gW1 tiles (mt = (w>>3) + 2q, nt = w & 7)
     double g0[3][2];  // [gW0|gb0]^T tiles (mt = (w>>3) + 2q over i, nt = w & 7 over j)
-    double gx;        // gb1 / gW2 / gb2 / KL sum (threads 256..354)
+    double gx[2];     // warps 7..15: one extra tile (see tc_extra)
 };
 
 __device__ __forceinline__ void tc_zero(TcGrads& g) {
@@ -216,11 +232,12 @@ __device__ __forceinline__ void tc_zero(TcGrads& g) {
     for (int q = 0; q < 2; ++q) g.g1[q][0] = g.g1[q][1] = 0.0;
 #pragma unroll
     for (int q = 0; q < 3; ++q) g.g0[q][0] = g.g0[q][1] = 0.0;
-    g.gx = 0.0;
+    g.gx[0] = g.gx[1] = 0.0;
 }
 
-// Scalar-gradient threads: 256..287 gb1[k], 288..351 gW2[a][k], 352..353 gb2[a], 354 KL.
-constexpr int XG0 = 256;
+// Extra K=TB tiles, one per warp 7..15: x = w - 7 in 0..3 is the G1 tile of
+// m-tile x at n-tile 8 (column 64 of [H1|1] -> gb1); x in 4..8 is E n-tile x - 4.
+constexpr int XW0 = 7;
 
 // Visit every (parameter index, value) this thread accumulated.
 template <typename Fn>
@@ -243,11 +260,18 @@ __device__ __forceinline__ void tc_for_each(const TcGrads& g, Fn fn) {
             fn(OFF_B0 + j, g.g0[q][0], g.g0[q][1], true);
         }
     }
-    const int x = tid - XG0;
-    if (x >= 0 && x < 32) fn(OFF_B1 + x, g.gx, 0.0, false);
-    else if (x >= 32 && x < 96) fn(OFF_W2 + (x - 32), g.gx, 0.0, false);
-    else if (x >= 96 && x < 98) fn(OFF_B2 + (x - 96), g.gx, 0.0, false);
-    else if (x == 98) fn(NP, g.gx, 0.0, false);
+    const int x = w - XW0;
+    if (x >= 0 && x < 4) {
+        if (tq == 0) fn(OFF_B1 + x * 8 + gq, g.gx[0], 0.0, false);  // column 64
+    } else if (x >= 4) {
+        const int n = (x - 4) * 8 + 2 * tq;  // E column; row gq
+        if (n < H2) {
+            if (gq < A) fn(OFF_W2 + gq * H2 + n, g.gx[0], g.gx[1], true);
+        } else if (n == H2) {
+            if (gq < A) fn(OFF_B2 + gq, g.gx[0], 0.0, false);
+            else if (gq == 2) fn(NP, g.gx[0], 0.0, false);
+        }
+    }
 }
 
 template <int MT>
@@ -266,6 +290,48 @@ __device__ void tc_prefetch(TcSmem<MT>& S, int buf, const TrainArgs& a, size_t r
         cp_async16(&S.stage_t[buf][2 * r], src, r < nv ? 16 : 0);
     }
     cp_async_commit();
+}
+
+// Ring prefetch (epoch kernel): record indices two tiles ahead, features and
+// targets one tile ahead, gathered through the indices already in smem.
+template <int MT>
+__device__ __forceinline__ void tc_fetch_idx(TcSmem<MT>& S, int slot, const TrainArgs& a,
+                                             uint32_t r0, int nv) {
+    if ((int)threadIdx.x < nv) {
+        const unsigned s = (unsigned)__cvta_generic_to_shared(&S.ord[slot][threadIdx.x]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s),
+                     "l"(a.order + r0 + threadIdx.x)
+                     : "memory");
+    }
+}
+template <int MT>
+__device__ __forceinline__ void tc_fetch_rows(TcSmem<MT>& S, int slot, const TrainArgs& a, int nv) {
+    constexpr int TB = 8 * MT;
+    for (int t = threadIdx.x; t < TB * (F / 4); t += NT) {
+        const int r = t / (F / 4), q = t - r * (F / 4);
+        const float* src = a.feat;
+        if (r < nv) src = a.feat + (size_t)S.ord[slot][r] * F + 4 * q;
+        cp_async16(&S.stage_f[slot][r * F + 4 * q], src, r < nv ? 16 : 0);
+    }
+    if (threadIdx.x < TB) {
+        const int r = threadIdx.x;
+        const double* src = a.tgt;
+        if (r < nv) src = a.tgt + 2 * (size_t)S.ord[slot][r];
+        cp_async16(&S.stage_t[slot][2 * r], src, r < nv ? 16 : 0);
+    }
+}
+
+// Constant columns: X col 44 = 1 (gb0), H1 col 64 = 1 (gb1), H2 col 32 = 1
+// (gb2, KL), U cols 3.. = 0. Tiles never overwrite them.
+template <int MT>
+__device__ void tc_init_consts(TcSmem<MT>& S) {
+    constexpr int TB = 8 * MT;
+    for (int t = threadIdx.x; t < TB; t += NT) {
+        for (int i = F; i < SX; ++i) S.x[t * SX + i] = i == F ? 1.0 : 0.0;
+        for (int j = H1; j < SH1; ++j) S.h1[t * SH1 + j] = j == H1 ? 1.0 : 0.0;
+        for (int k = H2; k < SH2; ++k) S.h2[t * SH2 + k] = k == H2 ? 1.0 : 0.0;
+        for (int m = 0; m < SU; ++m) S.u[t * SU + m] = 0.0;
+    }
 }
 
 // One tile of 8*MT records (rows >= nv are zero padding and contribute 0).
@@ -344,19 +410,23 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int buf, int nv, double inv_b
     __syncthreads();
     TC_MARK(2);
 
-    // ---- F3 + B1: thread (r, a): logit a, softmax, KL, d3; then d2 for k in [16a, 16a+16).
-    //      Whole warps take part (the pair exchanges are full-mask shuffles);
-    //      lanes past the tile recompute row TB-1 and store nothing.
-    if (tid < ((2 * TB + 31) & ~31)) {
-        const bool live = tid < 2 * TB;
-        const int r = live ? tid >> 1 : TB - 1, a = tid & 1;
-        const double* h = S.h2 + r * SH2;
-        const double* wr = S.w2 + a * H2;
-        double l = S.b2[a];
-#pragma unroll 8
-        for (int k = 0; k < H2; ++k) l = fma(wr[k], h[k], l);
-        const double lo = __shfl_xor_sync(0xffffffffu, l, 1);
-        const double l0 = a ? lo : l, l1 = a ? l : lo;
+    // ---- F3 + B1 on warps w < MT (m-tile w): logits by DMMA (B = W2^T padded
+    //      to 8 columns), softmax / KL / d3 in lanes t < 2 of each row group
+    //      (record r = 8w + g, action a = t), then D2 by a K=4 DMMA whose A
+    //      fragment is exactly those lanes' d3 values.
+    if (w < MT) {
+        const int r = w * 8 + gq;
+        double lg[2];
+        lg[0] = tq == 0 ? S.b2[0] : 0.0;
+        lg[1] = tq == 0 ? S.b2[1] : 0.0;
+        const double* hb = S.h2 + r * SH2 + tq;
+#pragma unroll
+        for (int k0 = 0; k0 < H2; k0 += 4)
+            dmma(lg, hb[k0], gq < A ? S.w2[gq * H2 + k0 + tq] : 0.0);
+        const double l0 = __shfl_sync(0xffffffffu, lg[0], lane & ~3);
+        const double l1 = __shfl_sync(0xffffffffu, lg[1], lane & ~3);
+        const int a = tq & 1;
+        const double l = a ? l1 : l0;
         const double m = l0 < l1 ? l1 : l0;
         const double e = exp(l - m);
         const double eo = __shfl_xor_sync(0xffffffffu, e, 1);
@@ -369,22 +439,23 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int buf, int nv, double inv_b
         const double to = __shfl_xor_sync(0xffffffffu, term, 1);
         const double loss = a ? to + term : term + to;
         const bool valid = r < nv;
-        if (live && a == 0) S.kl[r] = valid ? loss : 0.0;
-        const double d3 = valid ? p * (lr - loss) * inv_b : 0.0;
-        if (live) S.d3[2 * r + a] = d3;
-        const double d3o = __shfl_xor_sync(0xffffffffu, d3, 1);
-        const double d30 = a ? d3o : d3, d31 = a ? d3 : d3o;
+        const double d3 = (valid && tq < 2) ? p * (lr - loss) * inv_b : 0.0;
+        if (tq < 2) S.u[r * SU + tq] = d3;
+        if (tq == 0) S.u[r * SU + 2] = valid ? loss : 0.0;
 #pragma unroll
-        for (int kk = 0; kk < H2 / 2; ++kk) {
-            const int k = (H2 / 2) * a + kk;
-            const double d = fma(d31, S.w2[H2 + k], d30 * S.w2[k]);
-            if (live) S.d2[r * SH2 + k] = h[k] <= 0.0 ? 0.0 : d;
+        for (int nt = 0; nt < H2 / 8; ++nt) {
+            double dd[2] = {0.0, 0.0};
+            dmma(dd, d3, tq < A ? S.w2[tq * H2 + nt * 8 + gq] : 0.0);
+            const int k = nt * 8 + 2 * tq;
+            const double* h = S.h2 + r * SH2 + k;
+            S.d2[r * SH2 + k] = h[0] <= 0.0 ? 0.0 : dd[0];
+            S.d2[r * SH2 + k + 1] = h[1] <= 0.0 ? 0.0 : dd[1];
         }
     }
     __syncthreads();
     TC_MARK(3);
 
-    // ---- B2: D1 = (D2 W1) o [h1 > 0]; G1: gW1 += D2^T H1; scalar gradients
+    // ---- B2: D1 = (D2 W1) o [h1 > 0]; G1: gW1 += D2^T H1; extra tiles (gb1, E)
     {
         constexpr int Q = (MT + 1) / 2;
         const int nt = w & 7, mq = w >> 3;
@@ -418,20 +489,15 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int buf, int nv, double inv_b
             dmma(g.g1[0], ab[r0 * SH2], bf);
             dmma(g.g1[1], ab[r0 * SH2 + 16], bf);
         }
-        const int x = tid - XG0;
-        if (x >= 0 && x < 32) {
-#pragma unroll 8
-            for (int r = 0; r < nv; ++r) g.gx += S.d2[r * SH2 + x];
-        } else if (x >= 32 && x < 96) {
-            const int a = (x - 32) >> 5, k = (x - 32) & 31;
-#pragma unroll 8
-            for (int r = 0; r < nv; ++r) g.gx = fma(S.d3[2 * r + a], S.h2[r * SH2 + k], g.gx);
-        } else if (x >= 96 && x < 98) {
-#pragma unroll 8
-            for (int r = 0; r < nv; ++r) g.gx += S.d3[2 * r + (x - 96)];
-        } else if (x == 98) {
-#pragma unroll 8
-            for (int r = 0; r < nv; ++r) g.gx += S.kl[r];
+        const int x = w - XW0;
+        if (x >= 0) {
+            // x < 4: A = D2^T (m-tile x), B = H1 cols 64..71; x >= 4: A = U^T, B = H2 cols 8(x-4)..
+            const double* xa = x < 4 ? S.d2 + tq * SH2 + x * 8 + gq : S.u + tq * SU + gq;
+            const int sa = x < 4 ? SH2 : SU;
+            const double* xb = x < 4 ? S.h1 + tq * SH1 + H1 + gq : S.h2 + tq * SH2 + (x - 4) * 8 + gq;
+            const int sb = x < 4 ? SH1 : SH2;
+#pragma unroll 7
+            for (int r0 = 0; r0 < TB; r0 += 4) dmma(g.gx, xa[r0 * sa], xb[r0 * sb]);
         }
     }
     __syncthreads();
@@ -522,21 +588,30 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     const int p_lo = c * chunk, p_hi = min(NP, p_lo + chunk);
     const int n_elem = 1 + max(0, p_hi - p_lo);  // element 0 = loss, then the slice
 
-    long pf_step = 0;
-    uint32_t pf_r0 = 0xFFFFFFFFu;
-    int pf_nv = 0;
-    bool have_next = tc_next<TB>(a, n_steps, pf_step, pf_r0, pf_nv);
-    int buf = 0;
-    if (have_next) tc_prefetch<MT>(S, buf, a, pf_r0, pf_nv);
+    // prefetch cursors: c1 = tile k+1 (rows in flight), c2 = tile k+2 (indices in flight)
+    long s1 = 0, s2 = 0;
+    uint32_t r1 = 0xFFFFFFFFu, r2;
+    int n1 = 0, n2 = 0;
+    bool h1 = tc_next<TB>(a, n_steps, s1, r1, n1);  // tile 0
+    if (h1) tc_fetch_idx(S, 0, a, r1, n1);
+    s2 = s1; r2 = r1;
+    bool h2 = h1 && tc_next<TB>(a, n_steps, s2, r2, n2);  // tile 1
+    if (h2) tc_fetch_idx(S, 1, a, r2, n2);
+    cp_async_commit();
     load_params_plain(S, a.params);
-    for (int t = tid; t < TB * (SX - F); t += NT) {
-        const int r = t / (SX - F), i = F + (t - r * (SX - F));
-        S.x[r * SX + i] = i == F ? 1.0 : 0.0;
-    }
+    tc_init_consts(S);
+    cp_async_wait_all();
+    __syncthreads();
+    if (h1) tc_fetch_rows(S, 0, a, n1);  // tile 0 rows
+    cp_async_commit();
+    // shift: c1 <- tile 1, c2 <- tile 2
+    h1 = h2; s1 = s2; r1 = r2; n1 = n2;
+    s2 = s1; r2 = r1;
+    h2 = h1 && tc_next<TB>(a, n_steps, s2, r2, n2);
     TcGrads g;
     tc_zero(g);
     double epoch_total = 0.0;
-    __syncthreads();
+    int k = 0;  // tile counter: tile k's rows in stage[k & 1], its indices were in ord[k & 1]
     TC_MARK(-1);
 
     for (long step = 0; step < n_steps; ++step) {
@@ -544,16 +619,18 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         tc_slice(a, step, c, G, lo, hi, nb);
         const double inv_b = 1.0 / (double)nb;
         const unsigned tag = a.tag_base + (unsigned)step + 1u;
-        for (uint32_t r0 = lo; r0 < hi; r0 += TB) {
+        TC_TRACE(step, 0);
+        for (uint32_t r0 = lo; r0 < hi; r0 += TB, ++k) {
             const int nv = (int)min((uint32_t)TB, hi - r0);
             cp_async_wait_all();
             __syncthreads();
-            const int cur = buf;
-            buf ^= 1;
-            have_next = tc_next<TB>(a, n_steps, pf_step, pf_r0, pf_nv);
-            if (have_next) tc_prefetch<MT>(S, buf, a, pf_r0, pf_nv);
+            if (h1) tc_fetch_rows(S, (k + 1) & 1, a, n1);     // rows of tile k+1
+            if (h2) tc_fetch_idx(S, k & 1, a, r2, n2);        // indices of tile k+2
+            cp_async_commit();
+            h1 = h2; s1 = s2; r1 = r2; n1 = n2;
+            if (h2) h2 = tc_next<TB>(a, n_steps, s2, r2, n2);
             TC_MARK(6);
-            tc_tile<MT>(S, g, cur, nv, inv_b);
+            tc_tile<MT>(S, g, k & 1, nv, inv_b);
         }
         // ---- 1. publish this CTA's partial
         double* part = a.partials + (size_t)c * PSTR;
@@ -564,12 +641,14 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
             st_release_u32(a.flags + c, tag);
         }
         TC_MARK(7);
+        TC_TRACE(step, 1);
         // ---- 2. wait for every partial, reduce [loss | slice] in a fixed order
         if (tid < G)
             while (ld_acquire_u32(a.flags + tid) != tag) {
             }
         __syncthreads();
         TC_MARK(8);
+        TC_TRACE(step, 2);
         bool diverged = false;
         for (int e0 = 0; e0 < n_elem; e0 += 64) {
             // warp w: elements e0 + 32*(w&1) + lane, CTA subset s = w>>1 (c' = s + 8q)
@@ -623,11 +702,13 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
             break;
         }
         TC_MARK(9);
+        TC_TRACE(step, 3);
         if (tid == 0) epoch_total = fma(S.scal[0], (double)nb, epoch_total);
         // ---- 4. all-gather the new parameters (the next launch reads a.params)
         if (step + 1 < n_steps) load_params_ll(S, a.llp, tag);
         tc_zero(g);
         TC_MARK(10);
+        TC_TRACE(step, 4);
         // (the next tile's __syncthreads orders the replicas before use)
     }
     cp_async_wait_all();
@@ -647,10 +728,7 @@ __global__ void __launch_bounds__(NT, 1) train_partial_tc_kernel(TrainArgs a, lo
     tc_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
     if (hi > lo) tc_prefetch<MT>(S, 0, a, lo, (int)min((uint32_t)TB, hi - lo));
     load_params_plain(S, a.params);
-    for (int t = threadIdx.x; t < TB * (SX - F); t += NT) {
-        const int r = t / (SX - F), i = F + (t - r * (SX - F));
-        S.x[r * SX + i] = i == F ? 1.0 : 0.0;
-    }
+    tc_init_consts(S);
     TcGrads g;
     tc_zero(g);
     const double inv_b = 1.0 / (double)nb;
@@ -683,5 +761,9 @@ extern "C" int gbxcu_debug_phase_cycles_tc(unsigned long long* out, int reset) {
         cudaMemcpyToSymbol(gbxcu::g_tc_phase, z, sizeof(z));
     }
     return 0;
+}
+extern "C" int gbxcu_debug_trace_tc(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, gbxcu::g_tc_trace, sizeof(unsigned long long) * 8 * 160 * 6) ==
+                   cudaSuccess ? 0 : 3;
 }
 #endif

@@ -94,3 +94,30 @@ static double run(int device, int iters) {
 extern "C" double peak_fp64_tflops(int device) { return run<double>(device, 4096); }
 extern "C" double peak_fp32_tflops(int device) { return run<float>(device, 16384); }
 extern "C" double peak_fp64_tensor_tflops(int device) { return run_dmma(device, 8192); }
+
+// DMMA dependent-chain latency: one warp, one accumulator chain.
+__global__ void dmma_latency_kernel(double* out, int iters, long long* cycles) {
+    double a = 0.5 + threadIdx.x * 1e-3, b = 0.25, c0 = 0, c1 = 0;
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1},{%2},{%3},{%0,%1};"
+                     : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) *cycles = t1 - t0;
+    if (c0 + c1 == -12345.0) out[0] = c0;
+}
+
+extern "C" double dmma_latency_cycles(int device) {
+    cudaSetDevice(device);
+    double* out;
+    long long* cyc;
+    cudaMalloc(&out, sizeof(double));
+    cudaMalloc(&cyc, sizeof(long long));
+    dmma_latency_kernel<<<1, 32>>>(out, 1000, cyc);
+    dmma_latency_kernel<<<1, 32>>>(out, 1000, cyc);
+    long long h = 0;
+    cudaMemcpy(&h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(out);
+    cudaFree(cyc);
+    return h / 1000.0;
+}

@@ -24,3 +24,19 @@ for n, b in [(20000, 32), (1000000, 4096), (1000000, 8192), (1000000, 65536)]:
     print(f"batch {b}: {v.sum()/steps:.0f} cycles/step (CTA 0)")
     for i in np.argsort(-v):
         if v[i] > 0: print(f"   {names[i]:22s} {v[i]/steps:9.0f} cyc/step {v[i]/v.sum():6.1%}")
+
+# per-CTA globaltimer trace (steps 8..15) of the last fit (batch 65536 above -> rerun 8192)
+f, t = synthetic_log(1000000)
+p = dev.policy_init(7)
+dev.fit(p, f, t, 0.01, 1, 8192, 99)
+tr = (C.c_ulonglong * (8 * 160 * 6))()
+lib.gbxcu_debug_trace_tc(tr)
+T = np.array(tr[:], np.float64).reshape(8, 160, 6)[:, :148, :5]
+for s in range(8):
+    base = T[s, :, 0].min()
+    rel = (T[s] - base)
+    print(f"step {8+s}: start spread {np.ptp(T[s,:,0]):.0f} ns | publish min/med/max "
+          f"{rel[:,1].min():.0f}/{np.median(rel[:,1]):.0f}/{rel[:,1].max():.0f} | waitdone "
+          f"{rel[:,2].min():.0f}/{rel[:,2].max():.0f} | slice pub {rel[:,3].min():.0f}/{rel[:,3].max():.0f}"
+          f" | gathered {rel[:,4].min():.0f}/{rel[:,4].max():.0f} ns; slowest publisher CTA {int(rel[:,1].argmax())}")
+np.save("gpurun_out/tc_trace.npy", T)
