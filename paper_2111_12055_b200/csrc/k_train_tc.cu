@@ -89,6 +89,8 @@ constexpr int SW1 = 68;          // W1 [k][j]
 constexpr int SH1 = 68;          // H1, D1 [r][j]
 constexpr int SH2 = 36;          // H2, D2 [r][k]: H2 col 32 = 1.0
 constexpr int SU = 12;           // U [r][m]: d3_0, d3_1, kl, then zeros
+constexpr double LN_PMIN = -16.11809565095832;        // ln(1e-7)
+constexpr double LN_PMAX = -1.0000000494736474e-07;   // ln(double(1 - 1e-7))
 
 template <int MT>
 struct TcSmem {
@@ -106,7 +108,7 @@ struct TcSmem {
     double h2[TB * SH2];
     double d2[TB * SH2];
     double u[TB * SU];
-    double tgt[TB * 2];
+    double ltgt[TB * 2];         // ln(clamp(target)) per (record, action)
     double red[8 * 64];          // slice reduction: [CTA subset][element]
     uint32_t ord[2][TB];         // record indices of the next two tiles (cp.async ring)
     double stage_t[2][TB * 2];   // cp.async staging: targets
@@ -149,6 +151,9 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 }
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -334,21 +339,31 @@ __device__ void tc_init_consts(TcSmem<MT>& S) {
     }
 }
 
-// One tile of 8*MT records (rows >= nv are zero padding and contribute 0).
+// P0 of a tile, run ahead of it (overlapping the previous step's
+// synchronisation): staged fp32 rows -> fp64 X (cols 0..43) and the clamped
+// log-targets ln(t^_a) the KL term needs. Caller: cp.async complete + barrier
+// before, barrier after.
 template <int MT>
-__device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int buf, int nv, double inv_b) {
+__device__ void tc_stage_in(TcSmem<MT>& S, int slot) {
+    constexpr int TB = 8 * MT;
+    const int tid = threadIdx.x;
+    for (int t = tid; t < TB * F; t += NT) {
+        const int r = t / F;
+        S.x[r * SX + (t - r * F)] = (double)S.stage_f[slot][t];
+    }
+    if (tid >= NT - 2 * TB) {
+        const int q = tid - (NT - 2 * TB);
+        S.ltgt[q] = log(clampp(S.stage_t[slot][q]));
+    }
+}
+
+// One tile of 8*MT records (rows >= nv are zero padding and contribute 0);
+// X and ltgt already staged by tc_stage_in.
+template <int MT>
+__device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
     constexpr int TB = 8 * MT;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int gq = lane >> 2, tq = lane & 3;
-
-    // ---- P0: staged fp32 -> fp64 X (cols 0..43), targets
-    for (int t = tid; t < TB * F; t += NT) {
-        const int r = t / F;
-        S.x[r * SX + (t - r * F)] = (double)S.stage_f[buf][t];
-    }
-    if (tid < 2 * TB) S.tgt[tid] = S.stage_t[buf][tid];
-    __syncthreads();
-    TC_MARK(0);
 
     // ---- F1: H1 = relu(X W0^T + b0). Warp: n-tile w&7, m-tiles (w>>3) + 2q.
     {
@@ -426,15 +441,16 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int buf, int nv, double inv_b
         const double l0 = __shfl_sync(0xffffffffu, lg[0], lane & ~3);
         const double l1 = __shfl_sync(0xffffffffu, lg[1], lane & ~3);
         const int a = tq & 1;
-        const double l = a ? l1 : l0;
-        const double m = l0 < l1 ? l1 : l0;
-        const double e = exp(l - m);
-        const double eo = __shfl_xor_sync(0xffffffffu, e, 1);
-        const double s = a ? eo + e : e + eo;
-        const double p = e / s;
+        // log-softmax form: with d = l_a - l_other, z = exp(-|d|),
+        //   p_a = (d >= 0 ? 1 : z) / (1 + z),  ln p_a = min(d, 0) - log1p(z)
+        // (equal to the reference's exp / sum / log(p/t) up to fp64 rounding)
+        const double d = a ? l1 - l0 : l0 - l1;
+        const double z = exp(-fabs(d));
+        const double lse = log1p(z);
+        const double p = (d >= 0.0 ? 1.0 : z) / (1.0 + z);
+        const double lpc = p < 1e-7 ? LN_PMIN : (p > 1.0 - 1e-7 ? LN_PMAX : fmin(d, 0.0) - lse);
         const double pc = clampp(p);
-        const double tc = clampp(S.tgt[2 * r + a]);
-        const double lr = log(pc / tc);
+        const double lr = lpc - S.ltgt[2 * r + a];
         const double term = pc * lr;
         const double to = __shfl_xor_sync(0xffffffffu, term, 1);
         const double loss = a ? to + term : term + to;
@@ -588,7 +604,10 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     const int p_lo = c * chunk, p_hi = min(NP, p_lo + chunk);
     const int n_elem = 1 + max(0, p_hi - p_lo);  // element 0 = loss, then the slice
 
-    // prefetch cursors: c1 = tile k+1 (rows in flight), c2 = tile k+2 (indices in flight)
+    // Pipeline (tile k): rows of tile k+1 and indices of tile k+2 are fetched
+    // (cp.async) at the top of tile k; tile k+1 is staged into X (P0) right
+    // after tile k, overlapping the step synchronisation.
+    // Cursors: c1 = tile k+1, c2 = tile k+2.
     long s1 = 0, s2 = 0;
     uint32_t r1 = 0xFFFFFFFFu, r2;
     int n1 = 0, n2 = 0;
@@ -604,6 +623,9 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     __syncthreads();
     if (h1) tc_fetch_rows(S, 0, a, n1);  // tile 0 rows
     cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    if (h1) tc_stage_in(S, 0);
     // shift: c1 <- tile 1, c2 <- tile 2
     h1 = h2; s1 = s2; r1 = r2; n1 = n2;
     s2 = s1; r2 = r1;
@@ -612,6 +634,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     tc_zero(g);
     double epoch_total = 0.0;
     int k = 0;  // tile counter: tile k's rows in stage[k & 1], its indices were in ord[k & 1]
+    bool stage_due = false;  // tile k (next to compute) fetched but not yet staged into X
     TC_MARK(-1);
 
     for (long step = 0; step < n_steps; ++step) {
@@ -622,30 +645,57 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         TC_TRACE(step, 0);
         for (uint32_t r0 = lo; r0 < hi; r0 += TB, ++k) {
             const int nv = (int)min((uint32_t)TB, hi - r0);
-            cp_async_wait_all();
-            __syncthreads();
+            __syncthreads();  // tile k staged; replicas (re)loaded
+            const bool more = h1;
             if (h1) tc_fetch_rows(S, (k + 1) & 1, a, n1);     // rows of tile k+1
             if (h2) tc_fetch_idx(S, k & 1, a, r2, n2);        // indices of tile k+2
             cp_async_commit();
             h1 = h2; s1 = s2; r1 = r2; n1 = n2;
             if (h2) h2 = tc_next<TB>(a, n_steps, s2, r2, n2);
             TC_MARK(6);
-            tc_tile<MT>(S, g, k & 1, nv, inv_b);
+            tc_tile<MT>(S, g, nv, inv_b);
+            if (more && r0 + TB < hi) {
+                // the next tile belongs to this step: stage it now
+                cp_async_wait_all();
+                __syncthreads();
+                tc_stage_in(S, (k + 1) & 1);
+                TC_MARK(0);
+            } else {
+                stage_due = more;  // staged after this step's partial is published
+            }
         }
-        // ---- 1. publish this CTA's partial
+        // ---- 1. publish this CTA's partial; stage the next tile meanwhile
         double* part = a.partials + (size_t)c * PSTR;
         tc_store_partial(g, part);
         __syncthreads();
+#ifdef GBX_TC_FLAGS
         if (tid == 0) {
             __threadfence();
             st_release_u32(a.flags + c, tag);
         }
+#else
+        if (tid == 0) red_release_add_u32(a.flags, 1u);
+#endif
+        if (stage_due) {
+            cp_async_wait_all();
+            __syncthreads();
+            tc_stage_in(S, k & 1);
+            stage_due = false;
+        }
         TC_MARK(7);
         TC_TRACE(step, 1);
         // ---- 2. wait for every partial, reduce [loss | slice] in a fixed order
+#ifdef GBX_TC_FLAGS
         if (tid < G)
             while (ld_acquire_u32(a.flags + tid) != tag) {
             }
+#else
+        if (tid == 0) {
+            const unsigned target = tag * (unsigned)G;
+            while ((int)(ld_acquire_u32(a.flags) - target) < 0) {
+            }
+        }
+#endif
         __syncthreads();
         TC_MARK(8);
         TC_TRACE(step, 2);
@@ -737,10 +787,11 @@ __global__ void __launch_bounds__(NT, 1) train_partial_tc_kernel(TrainArgs a, lo
         const int nv = (int)min((uint32_t)TB, hi - r0);
         cp_async_wait_all();
         __syncthreads();
-        const int cur = buf;
+        tc_stage_in(S, buf);
+        __syncthreads();
         buf ^= 1;
         if (r0 + TB < hi) tc_prefetch<MT>(S, buf, a, r0 + TB, (int)min((uint32_t)TB, hi - r0 - TB));
-        tc_tile<MT>(S, g, cur, nv, inv_b);
+        tc_tile<MT>(S, g, nv, inv_b);
     }
     tc_store_partial(g, a.partials + (size_t)blockIdx.x * PSTR);
 }
