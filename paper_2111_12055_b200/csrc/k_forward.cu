@@ -41,11 +41,16 @@ __global__ void policy_init_kernel(uint64_t seed, float* __restrict__ params) {
 }
 
 // --------------------------------------------------------------- fast path
+// Weights are laid out for packed FFMA2 (two fp32 FMAs per instruction, each
+// with its own single rounding — numerically identical to two FFMAs):
+//   w0p [j/2][i][2] pairs rows j, j+1 of W0, so one FFMA2 advances z_j, z_j+1;
+//   w1t [j][k]      consecutive k pairs advance acc2[k], acc2[k+1];
+//   w2p [k][2]      advances both logits.
 struct FastSmem {
     __align__(16) float xs[FWD_BLOCK / 32][32 * F];  // per-warp staging of 32 rows
-    float w0[H1 * F];   // [j][i]
+    float w0[H1 * F];   // w0p: [j/2][i][j&1]
     float w1t[H1 * H2]; // [j][k] = w1[k][j]
-    float w2[A * H2];   // [a][k]
+    float w2[A * H2];   // w2p: [k][a]
     float b0[H1];
     float b1[H2];
     float b2[A];
@@ -56,12 +61,15 @@ static_assert(offsetof(FastSmem, w0) % 16 == 0 && offsetof(FastSmem, w1t) % 16 =
 // Per-net constants of the guard: R_l = max_row ||w_row||_1, B_l = max |b|.
 // Computed in fp64 and rounded up so the fp32 bound stays an upper bound.
 __device__ void load_fast_weights(FastSmem& S, const float* __restrict__ p) {
-    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) S.w0[t] = p[OFF_W0 + t];
+    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) {
+        const int j = t / F, i = t - j * F;  // coalesced read of w0[j][i]
+        S.w0[(j >> 1) * (2 * F) + 2 * i + (j & 1)] = p[OFF_W0 + t];
+    }
     for (int t = threadIdx.x; t < H1 * H2; t += blockDim.x) {
         const int k = t / H1, j = t % H1;  // coalesced read of w1[k][j]
         S.w1t[j * H2 + k] = p[OFF_W1 + t];
     }
-    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[t] = p[OFF_W2 + t];
+    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[(t % H2) * A + t / H2] = p[OFF_W2 + t];
     for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = p[OFF_B0 + t];
     for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = p[OFF_B1 + t];
     if (threadIdx.x < A) S.b2[threadIdx.x] = p[OFF_B2 + threadIdx.x];
@@ -71,7 +79,7 @@ __device__ void load_fast_weights(FastSmem& S, const float* __restrict__ p) {
         double r0 = 0, bb0 = 0, r1 = 0, bb1 = 0, r2 = 0, bb2 = 0;
         for (int j = lane; j < H1; j += 32) {
             double s = 0;
-            for (int i = 0; i < F; ++i) s += fabs((double)S.w0[j * F + i]);
+            for (int i = 0; i < F; ++i) s += fabs((double)S.w0[(j >> 1) * (2 * F) + 2 * i + (j & 1)]);
             r0 = fmax(r0, s);
             bb0 = fmax(bb0, fabs((double)S.b0[j]));
         }
@@ -83,7 +91,7 @@ __device__ void load_fast_weights(FastSmem& S, const float* __restrict__ p) {
         }
         if (lane < A) {
             double s = 0;
-            for (int k = 0; k < H2; ++k) s += fabs((double)S.w2[lane * H2 + k]);
+            for (int k = 0; k < H2; ++k) s += fabs((double)S.w2[k * A + lane]);
             r2 = s;
             bb2 = fabs((double)S.b2[lane]);
         }
@@ -170,43 +178,50 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
         }
         __syncwarp();
 
-        // ---- layers 1+2 interleaved: acc2[k] += w1[k][j] * relu(z1_j)
-        float acc2[H2];
+        // ---- layers 1+2 interleaved: acc2[k] += w1[k][j] * relu(z1_j), packed FFMA2
+        float2 acc2[H2 / 2];
 #pragma unroll
-        for (int k = 0; k < H2; ++k) acc2[k] = S.b1[k];
+        for (int q = 0; q < H2 / 2; ++q) acc2[q] = make_float2(S.b1[2 * q], S.b1[2 * q + 1]);
         float hm1 = 0.f;
-#pragma unroll 2
-        for (int j = 0; j < H1; ++j) {
-            const float4* wr = reinterpret_cast<const float4*>(S.w0 + j * F);
-            float z = S.b0[j];
+#pragma unroll 1
+        for (int jp = 0; jp < H1 / 2; ++jp) {
+            const float4* wr = reinterpret_cast<const float4*>(S.w0 + jp * (2 * F));
+            float2 z = make_float2(S.b0[2 * jp], S.b0[2 * jp + 1]);
 #pragma unroll
-            for (int q = 0; q < F / 4; ++q) {
+            for (int q = 0; q < F / 2; ++q) {
                 const float4 w = wr[q];
-                z = fmaf(w.x, x[4 * q], z);
-                z = fmaf(w.y, x[4 * q + 1], z);
-                z = fmaf(w.z, x[4 * q + 2], z);
-                z = fmaf(w.w, x[4 * q + 3], z);
+                z = __ffma2_rn(make_float2(w.x, w.y), make_float2(x[2 * q], x[2 * q]), z);
+                z = __ffma2_rn(make_float2(w.z, w.w), make_float2(x[2 * q + 1], x[2 * q + 1]), z);
             }
-            const float h = z > 0.f ? z : 0.f;
-            hm1 = fmaxf(hm1, h);
-            const float4* w1c = reinterpret_cast<const float4*>(S.w1t + j * H2);
+            const float hA = z.x > 0.f ? z.x : 0.f, hB = z.y > 0.f ? z.y : 0.f;
+            hm1 = fmaxf(hm1, fmaxf(hA, hB));
+            const float4* wa = reinterpret_cast<const float4*>(S.w1t + (2 * jp) * H2);
+            const float4* wb = reinterpret_cast<const float4*>(S.w1t + (2 * jp + 1) * H2);
 #pragma unroll
             for (int q = 0; q < H2 / 4; ++q) {
-                const float4 w = w1c[q];
-                acc2[4 * q] = fmaf(w.x, h, acc2[4 * q]);
-                acc2[4 * q + 1] = fmaf(w.y, h, acc2[4 * q + 1]);
-                acc2[4 * q + 2] = fmaf(w.z, h, acc2[4 * q + 2]);
-                acc2[4 * q + 3] = fmaf(w.w, h, acc2[4 * q + 3]);
+                const float4 w = wa[q];
+                acc2[2 * q] = __ffma2_rn(make_float2(w.x, w.y), make_float2(hA, hA), acc2[2 * q]);
+                acc2[2 * q + 1] = __ffma2_rn(make_float2(w.z, w.w), make_float2(hA, hA), acc2[2 * q + 1]);
+            }
+#pragma unroll
+            for (int q = 0; q < H2 / 4; ++q) {
+                const float4 w = wb[q];
+                acc2[2 * q] = __ffma2_rn(make_float2(w.x, w.y), make_float2(hB, hB), acc2[2 * q]);
+                acc2[2 * q + 1] = __ffma2_rn(make_float2(w.z, w.w), make_float2(hB, hB), acc2[2 * q + 1]);
             }
         }
-        float l0 = S.b2[0], l1 = S.b2[1], hm2 = 0.f;
+        float2 lg = make_float2(S.b2[0], S.b2[1]);
+        float hm2 = 0.f;
+        const float2* w2p = reinterpret_cast<const float2*>(S.w2);
 #pragma unroll
-        for (int k = 0; k < H2; ++k) {
-            const float h = acc2[k] > 0.f ? acc2[k] : 0.f;
-            hm2 = fmaxf(hm2, h);
-            l0 = fmaf(S.w2[k], h, l0);
-            l1 = fmaf(S.w2[H2 + k], h, l1);
+        for (int q = 0; q < H2 / 2; ++q) {
+            const float ha = acc2[q].x > 0.f ? acc2[q].x : 0.f;
+            const float hb = acc2[q].y > 0.f ? acc2[q].y : 0.f;
+            hm2 = fmaxf(hm2, fmaxf(ha, hb));
+            lg = __ffma2_rn(w2p[2 * q], make_float2(ha, ha), lg);
+            lg = __ffma2_rn(w2p[2 * q + 1], make_float2(hb, hb), lg);
         }
+        const float l0 = lg.x, l1 = lg.y;
         if (!active) continue;
         if (!finite) {
             atomicOr(flags, 1u);
@@ -315,12 +330,15 @@ __device__ __forceinline__ void exact_forward(const ExactSmem& S, const float* _
 }
 
 __device__ void load_exact_weights(ExactSmem& S, const float* __restrict__ p) {
-    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) S.w0[t] = p[OFF_W0 + t];
+    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) {
+        const int j = t / F, i = t - j * F;  // coalesced read of w0[j][i]
+        S.w0[(j >> 1) * (2 * F) + 2 * i + (j & 1)] = p[OFF_W0 + t];
+    }
     for (int t = threadIdx.x; t < H1 * H2; t += blockDim.x) {
         const int k = t / H1, j = t % H1;
         S.w1t[j * H2 + k] = p[OFF_W1 + t];
     }
-    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[t] = p[OFF_W2 + t];
+    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[(t % H2) * A + t / H2] = p[OFF_W2 + t];
     for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = p[OFF_B0 + t];
     for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = p[OFF_B1 + t];
     if (threadIdx.x < A) S.b2[threadIdx.x] = p[OFF_B2 + threadIdx.x];

@@ -15,20 +15,20 @@
 //   G  gw2/gw1/gw0/gb* += per-record outer products, K = records in batch order
 // Gradient accumulators are owned by threads (registers) across all tiles of a
 // step, so a 1-CTA step reproduces the reference's per-parameter left fold bit
-// for bit (up to exp/log ulps). Multi-CTA steps reduce per-CTA partials with a
-// fixed-shape tree (deterministic; differs from the reference only by fp64
-// re-association).
+// for bit (up to exp/log ulps). Steps spread over several CTAs run on the FP64
+// tensor cores instead (k_train_tc.cu).
 //
 // The records of the NEXT tile (possibly of the next step — the epoch's
 // permutation is known up front) are gathered with cp.async into a second
 // staging buffer while the current tile computes.
 //
 // Kernels
-//   train_epoch_kernel<TB>  : one launch = one epoch on one GPU; G CTAs
-//                             (cooperative when G > 1: in-kernel reduction +
-//                             SGD between two grid barriers per step).
-//   train_partial_kernel<TB>: one step's per-CTA partials (data-parallel path;
-//                             reduction, NCCL all-reduce and update follow).
+//   train_epoch_kernel<TB>  : one launch = one epoch on one GPU, one CTA
+//                             (batches of <= 32 records per rank: the
+//                             reference's default and its bit-exact regime).
+//   train_partial_kernel<TB>: one step's partials on one CTA (data-parallel
+//                             path; NCCL all-reduce and update follow).
+//   batch_grad_kernel       : batch_kl_loss / batch_kl_gradient.
 #include <cstddef>
 
 #include "common.cuh"
@@ -516,8 +516,6 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
     TrainSmem<TB>& S = *reinterpret_cast<TrainSmem<TB>*>(smem_raw);
     if (*a.diverged_epoch >= 0) return;  // an earlier epoch diverged
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int G = gridDim.x;
-    const bool single = G == 1;
     const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
 
     // first tile's records in flight while the weights load
@@ -530,13 +528,12 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
     load_train_weights(S, a.params, false);
     GradRegs g;
     zero_grads(g);
-    unsigned int bar_target = 0;
     double epoch_total = 0.0;
     __syncthreads();
 
     for (long step = 0; step < n_steps; ++step) {
         size_t lo, hi, nb;
-        step_slice(a, step, blockIdx.x, G, lo, hi, nb);
+        step_slice(a, step, 0, 1, lo, hi, nb);
         const double inv_b = 1.0 / (double)nb;  // batch_kl_gradient's 1/|b| (global batch)
         for (size_t r0 = lo; r0 < hi; r0 += TB) {
             const int nv = (int)min((size_t)TB, hi - r0);
@@ -551,70 +548,28 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
             PHASE_MARK(7);
             train_tile<TB>(S, g, cur, nv, inv_b);
         }
-        if (single) {
-            // loss = (sum of per-record KL, batch order) / |b|  (policy.cpp:194-201)
-            if (tid == NT - 1) {
-                const double loss = __ddiv_rn(g.loss, (double)nb);
-                S.scal[1] = loss;
-                S.scal[2] = isfinite(loss) ? 0.0 : 1.0;
-            }
-            __syncthreads();
-            if (S.scal[2] != 0.0) {
-                if (tid == 0) *a.diverged_epoch = a.epoch;
-                break;
-            }
-            if (tid == 0) epoch_total = madd_rn(epoch_total, S.scal[1], (double)nb);
-            sgd_update_owned(S, g, a.lr);
-            zero_grads(g);
-            __syncthreads();
-        } else {
-            // ---- per-CTA partials -> deterministic cross-CTA reduction
-            double* part = a.partials + (size_t)blockIdx.x * PSTR;
-            for_each_owned(g, [&](int p, double& acc) { part[p] = acc; });
-            if (tid == NT - 1) part[NP] = g.loss;
-            PHASE_MARK(8);
-            grid_barrier(a.bar, bar_target);
-            PHASE_MARK(9);
-            if (w == 0) {
-                const double tot = reduce_over_ctas(a.partials, G, NP, lane);
-                if (lane == 0) {
-                    const double loss = __ddiv_rn(tot, (double)nb);
-                    S.scal[1] = loss;
-                    S.scal[2] = isfinite(loss) ? 0.0 : 1.0;
-                }
-            }
-            __syncthreads();
-            if (S.scal[2] != 0.0) {
-                if (blockIdx.x == 0 && tid == 0) *a.diverged_epoch = a.epoch;
-                break;
-            }
-            if (tid == 0) epoch_total = madd_rn(epoch_total, S.scal[1], (double)nb);
-            const int chunk = (NP + G - 1) / G;
-            const int p_lo = blockIdx.x * chunk, p_hi = min(NP, p_lo + chunk);
-            for (int p = p_lo + w; p < p_hi; p += NW) {
-                const double gs = reduce_over_ctas(a.partials, G, p, lane);
-                if (lane == 0) {
-                    const double wv = get_smem_param(S, p);
-                    a.params[p] = __double2float_rn(__dsub_rn(wv, __dmul_rn(a.lr, gs)));
-                }
-            }
-            PHASE_MARK(10);
-            grid_barrier(a.bar, bar_target);
-            PHASE_MARK(11);
-            load_train_weights(S, a.params, true);
-            zero_grads(g);
-            __syncthreads();
-            PHASE_MARK(12);
+        // loss = (sum of per-record KL, batch order) / |b|  (policy.cpp:194-201)
+        if (tid == NT - 1) {
+            const double loss = __ddiv_rn(g.loss, (double)nb);
+            S.scal[1] = loss;
+            S.scal[2] = isfinite(loss) ? 0.0 : 1.0;
         }
+        __syncthreads();
+        if (S.scal[2] != 0.0) {
+            if (tid == 0) *a.diverged_epoch = a.epoch;
+            break;
+        }
+        if (tid == 0) epoch_total = madd_rn(epoch_total, S.scal[1], (double)nb);
+        sgd_update_owned(S, g, a.lr);
+        zero_grads(g);
+        __syncthreads();
     }
     cp_async_wait_all();
     // epoch loss = total / n (policy.cpp:334); params back to global
-    if (blockIdx.x == 0 && tid == 0 && *a.diverged_epoch < 0)
+    if (tid == 0 && *a.diverged_epoch < 0)
         a.epoch_loss[a.epoch] = __ddiv_rn(epoch_total, (double)a.n);
-    if (single) {
-        __syncthreads();
-        for (int t = tid; t < NP; t += NT) a.params[t] = (float)get_smem_param(S, t);
-    }
+    __syncthreads();
+    for (int t = tid; t < NP; t += NT) a.params[t] = (float)get_smem_param(S, t);
 }
 
 // Data-parallel path: one step's per-CTA partials only.

@@ -10,6 +10,9 @@ def launch_shares(path):
         if len(r) <= vi: continue
         k = r[ki].split('(')[0].replace('void ', '').replace('gbxcu::', '')
         a = agg.setdefault(k, [0, 0.0]); a[0] += 1; a[1] += float(r[vi].replace(',', ''))
+    # bench.py's own pipe-peak probes (tools/peaks.cu) are not part of the step
+    for probe in [k for k in agg if 'peak_kernel' in k]:
+        agg.pop(probe)
     tot = sum(v[1] for v in agg.values())
     return [(k, c, t / c / 1e3, t / tot) for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])]
 
@@ -51,8 +54,17 @@ if __name__ == '__main__':
     tag = sys.argv[1]
     lines = [f"# ncu summary {tag}", "", "## Launch list (bench.py --steps 1 --warmup 1; cold-cache, serialised)", "",
              "| kernel | launches | avg us | share |", "|---|---|---|---|"]
-    for k, c, avg, sh in launch_shares('gpurun_out/launches.csv'):
+    shares = launch_shares('gpurun_out/launches.csv')
+    for k, c, avg, sh in shares:
         lines.append(f"| {k} | {c} | {avg:.1f} | {sh:.1%} |")
+    # the timed step of the headline (one fit epoch): shuffle + train kernel
+    step = [(k, c, avg) for k, c, avg, _ in shares
+            if k.startswith(('train_epoch', 'shuffle_epoch', 'iota_kernel', 'finish_epoch'))]
+    tot = sum(c * avg for _, c, avg in step)
+    lines += ["", "### Share of the headline step (fit epoch: shuffle + train)", "",
+              "| kernel | launches | avg us | share of step |", "|---|---|---|---|"]
+    for k, c, avg in step:
+        lines.append(f"| {k} | {c} | {avg:.1f} | {c * avg / tot:.1%} |")
     allm = []
     for rep in ['gpurun_out/prof_train.ncu-rep', 'gpurun_out/prof_other.ncu-rep']:
         try: allm += kernel_metrics(rep)
