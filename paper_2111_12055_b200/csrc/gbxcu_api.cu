@@ -155,7 +155,7 @@ int run_forward(gbxcu_ctx* c, const float* d_params, const float* d_feat, size_t
     CK(cudaMemsetAsync(flags.p, 0, 16, st));
     if (mode == GBXCU_FWD_FAST) {
         RET(recheck.ensure(n * sizeof(uint32_t)));
-        const size_t warps = (n + 31) / 32;
+        const size_t warps = (n + 63) / 64;  // 64 states per warp pass
         const size_t blocks_needed = (warps + FWD_BLOCK / 32 - 1) / (FWD_BLOCK / 32);
         const int grid = (int)std::min<size_t>(blocks_needed, (size_t)c->num_sms * c->fast_per_sm);
         fwd_fast_kernel<<<grid, FWD_BLOCK, fast_smem_bytes(), st>>>(

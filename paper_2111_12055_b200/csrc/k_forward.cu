@@ -41,13 +41,14 @@ __global__ void policy_init_kernel(uint64_t seed, float* __restrict__ params) {
 }
 
 // --------------------------------------------------------------- fast path
+constexpr int FAST_ROWS = 64;  // states per warp per iteration (two per lane)
 // Weights are laid out for packed FFMA2 (two fp32 FMAs per instruction, each
 // with its own single rounding — numerically identical to two FFMAs):
 //   w0p [j/2][i][2] pairs rows j, j+1 of W0, so one FFMA2 advances z_j, z_j+1;
 //   w1t [j][k]      consecutive k pairs advance acc2[k], acc2[k+1];
 //   w2p [k][2]      advances both logits.
 struct FastSmem {
-    __align__(16) float xs[FWD_BLOCK / 32][32 * F];  // per-warp staging of 32 rows
+    __align__(16) float xs[FWD_BLOCK / 32][2][FAST_ROWS * F];  // per-warp double-buffered staging
     float w0[H1 * F];   // w0p: [j/2][i][j&1]
     float w1t[H1 * H2]; // [j][k] = w1[k][j]
     float w2[A * H2];   // w2p: [k][a]
@@ -132,8 +133,86 @@ __device__ __forceinline__ float guard_threshold(const float* st, float X, float
     return 2.02f * D3 + 1e-30f;
 }
 
-// mode bits: 1 = write probs, 2 = write actions, 4 = collect (sampled) mode
-__global__ void __launch_bounds__(FWD_BLOCK, 2)
+// Per-state tail of the fast path: guard, fp32 softmax, action (greedy or
+// collection draw), re-check list, outputs.
+__device__ __forceinline__ void fast_finish(const FastSmem& S, size_t s, float l0, float l1,
+                                            float X, float hm1, float hm2, bool finite,
+                                            double* __restrict__ probs, uint8_t* __restrict__ actions,
+                                            const uint64_t* __restrict__ seg_off, size_t nseg,
+                                            const uint64_t* __restrict__ seg_seed, double eps,
+                                            uint32_t* __restrict__ recheck,
+                                            unsigned int* __restrict__ n_recheck,
+                                            unsigned int* __restrict__ flags, int mode) {
+    if (!finite) {
+        atomicOr(flags, 1u);
+        return;
+    }
+    const float T = guard_threshold(S.stats, X, hm1, hm2);
+    const float d = l1 - l0;
+    // fp32 softmax (max-subtracted like the reference)
+    const float m = fmaxf(l0, l1);
+    const float e0 = expf(l0 - m), e1 = expf(l1 - m);
+    const float p0 = e0 / (e0 + e1);
+    bool ambiguous;
+    uint8_t act;
+    if (mode & 4) {
+        // collection: find this state's segment and its two draws
+        size_t lo = 0, hi = nseg;  // seg_off[lo] <= s < seg_off[hi]
+        while (hi - lo > 1) {
+            const size_t mid = (lo + hi) >> 1;
+            if (seg_off[mid] <= s) lo = mid; else hi = mid;
+        }
+        const uint64_t j = s - seg_off[lo];
+        const uint64_t seed = seg_seed[lo];
+        const double ue = unit_of(sm_draw(seed, 2 * j + 1));
+        const double ua = unit_of(sm_draw(seed, 2 * j + 2));
+        if (ue < eps) {
+            act = ua < 0.5 ? 0 : 1;
+            ambiguous = false;
+        } else {
+            // |p0_fp32 - p0_exact| <= |dp0/dd| * 2D3 + fp32 rounding of exp/div
+            //                     <= 0.25 * T + 16 u
+            const double tol = 0.25 * (double)T + 16.0 * 5.9604645e-8;
+            ambiguous = fabs(ua - (double)p0) <= tol;
+            act = ua < (double)p0 ? 0 : 1;
+        }
+    } else {
+        ambiguous = !(fabsf(d) > T);
+        act = d > 0.f ? 1 : 0;
+    }
+    if (ambiguous) {
+        const unsigned int slot = atomicAdd(n_recheck, 1u);
+        recheck[slot] = (uint32_t)s;
+    }
+    if (mode & 2) actions[s] = act;
+    if (mode & 1) {
+        probs[2 * s] = (double)p0;
+        probs[2 * s + 1] = (double)(e1 / (e0 + e1));
+    }
+}
+
+// Loads one staged row into registers; returns max |x| and finiteness.
+__device__ __forceinline__ void fast_row(const float* xs, int r, float (&x)[F], float& X, bool& finite) {
+    const float4* row = reinterpret_cast<const float4*>(xs + r * F);
+#pragma unroll
+    for (int q = 0; q < F / 4; ++q) {
+        const float4 v = row[q];
+        x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+    }
+    X = 0.f;
+    finite = true;
+#pragma unroll
+    for (int i = 0; i < F; ++i) {
+        finite &= isfinite(x[i]);
+        X = fmaxf(X, fabsf(x[i]));
+    }
+}
+
+// mode bits: 1 = write probs, 2 = write actions, 4 = collect (sampled) mode.
+// Each lane evaluates two states (rows lane and lane + 32 of the warp's
+// 64-row tile): every weight read from shared memory feeds two packed FFMA2s,
+// which keeps the shared-memory instruction rate below the FMA pipe's.
+__global__ void __launch_bounds__(FWD_BLOCK, 1)
 fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat, size_t n,
                 double* __restrict__ probs, uint8_t* __restrict__ actions,
                 const uint64_t* __restrict__ seg_off, size_t nseg,
@@ -145,130 +224,101 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
     load_fast_weights(S, params);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float* xs = S.xs[warp];
     const size_t n_warps_total = (size_t)gridDim.x * (FWD_BLOCK / 32);
-
-    for (size_t base = ((size_t)blockIdx.x * (FWD_BLOCK / 32) + warp) * 32; base < n;
-         base += n_warps_total * 32) {
-        // ---- stage 32 rows (32*176 B) through shared memory, float4 coalesced
-        const size_t rows = min((size_t)32, n - base);
-        const float4* src = reinterpret_cast<const float4*>(feat + base * F);
-        float4* dst = reinterpret_cast<float4*>(xs);
-        const int nvec = (int)rows * (F / 4);
-        for (int v = lane; v < nvec; v += 32) dst[v] = __ldg(src + v);
-        __syncwarp();
-        const size_t s = base + lane;
-        const bool active = lane < (int)rows;
-
-        float x[F];
-        float X = 0.f;
-        bool finite = true;
-        {
-            const float4* row = reinterpret_cast<const float4*>(xs + (active ? lane : 0) * F);
-#pragma unroll
-            for (int q = 0; q < F / 4; ++q) {
-                const float4 v = row[q];
-                x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
-            }
-#pragma unroll
-            for (int i = 0; i < F; ++i) {
-                finite &= isfinite(x[i]);
-                X = fmaxf(X, fabsf(x[i]));
+    // rows of this warp's next pass stream in (cp.async) while the current one computes
+    auto stage = [&](size_t b, int buf) {
+        if (b < n) {
+            const int nvec = (int)min((size_t)FAST_ROWS, n - b) * (F / 4);
+            const float4* src = reinterpret_cast<const float4*>(feat + b * F);
+            float4* dst = reinterpret_cast<float4*>(S.xs[warp][buf]);
+            for (int v = lane; v < nvec; v += 32) {
+                const unsigned d = (unsigned)__cvta_generic_to_shared(dst + v);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + v) : "memory");
             }
         }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    size_t base = ((size_t)blockIdx.x * (FWD_BLOCK / 32) + warp) * FAST_ROWS;
+    int buf = 0;
+    stage(base, 0);
+    for (; base < n; base += n_warps_total * FAST_ROWS, buf ^= 1) {
+        stage(base + n_warps_total * FAST_ROWS, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         __syncwarp();
+        const float* xs = S.xs[warp][buf];
+        const size_t rows = min((size_t)FAST_ROWS, n - base);
+        const bool act0 = lane < (int)rows, act1 = lane + 32 < (int)rows;
+
+        float xa[F], xb[F];
+        float Xa, Xb;
+        bool fa, fb;
+        fast_row(xs, act0 ? lane : 0, xa, Xa, fa);
+        fast_row(xs, act1 ? lane + 32 : 0, xb, Xb, fb);
+        __syncwarp();  // the buffer is refilled two passes later
 
         // ---- layers 1+2 interleaved: acc2[k] += w1[k][j] * relu(z1_j), packed FFMA2
-        float2 acc2[H2 / 2];
+        float2 ca[H2 / 2], cb[H2 / 2];
 #pragma unroll
-        for (int q = 0; q < H2 / 2; ++q) acc2[q] = make_float2(S.b1[2 * q], S.b1[2 * q + 1]);
-        float hm1 = 0.f;
-#pragma unroll 1
+        for (int q = 0; q < H2 / 2; ++q) ca[q] = cb[q] = make_float2(S.b1[2 * q], S.b1[2 * q + 1]);
+        float hma = 0.f, hmb = 0.f;
+#pragma unroll 2
         for (int jp = 0; jp < H1 / 2; ++jp) {
             const float4* wr = reinterpret_cast<const float4*>(S.w0 + jp * (2 * F));
-            float2 z = make_float2(S.b0[2 * jp], S.b0[2 * jp + 1]);
+            float2 za = make_float2(S.b0[2 * jp], S.b0[2 * jp + 1]), zb = za;
 #pragma unroll
             for (int q = 0; q < F / 2; ++q) {
                 const float4 w = wr[q];
-                z = __ffma2_rn(make_float2(w.x, w.y), make_float2(x[2 * q], x[2 * q]), z);
-                z = __ffma2_rn(make_float2(w.z, w.w), make_float2(x[2 * q + 1], x[2 * q + 1]), z);
+                const float2 w01 = make_float2(w.x, w.y), w23 = make_float2(w.z, w.w);
+                za = __ffma2_rn(w01, make_float2(xa[2 * q], xa[2 * q]), za);
+                zb = __ffma2_rn(w01, make_float2(xb[2 * q], xb[2 * q]), zb);
+                za = __ffma2_rn(w23, make_float2(xa[2 * q + 1], xa[2 * q + 1]), za);
+                zb = __ffma2_rn(w23, make_float2(xb[2 * q + 1], xb[2 * q + 1]), zb);
             }
-            const float hA = z.x > 0.f ? z.x : 0.f, hB = z.y > 0.f ? z.y : 0.f;
-            hm1 = fmaxf(hm1, fmaxf(hA, hB));
-            const float4* wa = reinterpret_cast<const float4*>(S.w1t + (2 * jp) * H2);
-            const float4* wb = reinterpret_cast<const float4*>(S.w1t + (2 * jp + 1) * H2);
+            const float hA0 = za.x > 0.f ? za.x : 0.f, hA1 = za.y > 0.f ? za.y : 0.f;
+            const float hB0 = zb.x > 0.f ? zb.x : 0.f, hB1 = zb.y > 0.f ? zb.y : 0.f;
+            hma = fmaxf(hma, fmaxf(hA0, hA1));
+            hmb = fmaxf(hmb, fmaxf(hB0, hB1));
+            const float4* w1a = reinterpret_cast<const float4*>(S.w1t + (2 * jp) * H2);
+            const float4* w1b = reinterpret_cast<const float4*>(S.w1t + (2 * jp + 1) * H2);
 #pragma unroll
             for (int q = 0; q < H2 / 4; ++q) {
-                const float4 w = wa[q];
-                acc2[2 * q] = __ffma2_rn(make_float2(w.x, w.y), make_float2(hA, hA), acc2[2 * q]);
-                acc2[2 * q + 1] = __ffma2_rn(make_float2(w.z, w.w), make_float2(hA, hA), acc2[2 * q + 1]);
+                const float4 w = w1a[q];
+                const float2 w01 = make_float2(w.x, w.y), w23 = make_float2(w.z, w.w);
+                ca[2 * q] = __ffma2_rn(w01, make_float2(hA0, hA0), ca[2 * q]);
+                cb[2 * q] = __ffma2_rn(w01, make_float2(hB0, hB0), cb[2 * q]);
+                ca[2 * q + 1] = __ffma2_rn(w23, make_float2(hA0, hA0), ca[2 * q + 1]);
+                cb[2 * q + 1] = __ffma2_rn(w23, make_float2(hB0, hB0), cb[2 * q + 1]);
             }
 #pragma unroll
             for (int q = 0; q < H2 / 4; ++q) {
-                const float4 w = wb[q];
-                acc2[2 * q] = __ffma2_rn(make_float2(w.x, w.y), make_float2(hB, hB), acc2[2 * q]);
-                acc2[2 * q + 1] = __ffma2_rn(make_float2(w.z, w.w), make_float2(hB, hB), acc2[2 * q + 1]);
+                const float4 w = w1b[q];
+                const float2 w01 = make_float2(w.x, w.y), w23 = make_float2(w.z, w.w);
+                ca[2 * q] = __ffma2_rn(w01, make_float2(hA1, hA1), ca[2 * q]);
+                cb[2 * q] = __ffma2_rn(w01, make_float2(hB1, hB1), cb[2 * q]);
+                ca[2 * q + 1] = __ffma2_rn(w23, make_float2(hA1, hA1), ca[2 * q + 1]);
+                cb[2 * q + 1] = __ffma2_rn(w23, make_float2(hB1, hB1), cb[2 * q + 1]);
             }
         }
-        float2 lg = make_float2(S.b2[0], S.b2[1]);
-        float hm2 = 0.f;
+        float2 la = make_float2(S.b2[0], S.b2[1]), lb = la;
+        float h2a = 0.f, h2b = 0.f;
         const float2* w2p = reinterpret_cast<const float2*>(S.w2);
 #pragma unroll
         for (int q = 0; q < H2 / 2; ++q) {
-            const float ha = acc2[q].x > 0.f ? acc2[q].x : 0.f;
-            const float hb = acc2[q].y > 0.f ? acc2[q].y : 0.f;
-            hm2 = fmaxf(hm2, fmaxf(ha, hb));
-            lg = __ffma2_rn(w2p[2 * q], make_float2(ha, ha), lg);
-            lg = __ffma2_rn(w2p[2 * q + 1], make_float2(hb, hb), lg);
+            const float a0 = ca[q].x > 0.f ? ca[q].x : 0.f, a1 = ca[q].y > 0.f ? ca[q].y : 0.f;
+            const float b0 = cb[q].x > 0.f ? cb[q].x : 0.f, b1 = cb[q].y > 0.f ? cb[q].y : 0.f;
+            h2a = fmaxf(h2a, fmaxf(a0, a1));
+            h2b = fmaxf(h2b, fmaxf(b0, b1));
+            la = __ffma2_rn(w2p[2 * q], make_float2(a0, a0), la);
+            lb = __ffma2_rn(w2p[2 * q], make_float2(b0, b0), lb);
+            la = __ffma2_rn(w2p[2 * q + 1], make_float2(a1, a1), la);
+            lb = __ffma2_rn(w2p[2 * q + 1], make_float2(b1, b1), lb);
         }
-        const float l0 = lg.x, l1 = lg.y;
-        if (!active) continue;
-        if (!finite) {
-            atomicOr(flags, 1u);
-            continue;
-        }
-        const float T = guard_threshold(S.stats, X, hm1, hm2);
-        const float d = l1 - l0;
-        // fp32 softmax (max-subtracted like the reference)
-        const float m = fmaxf(l0, l1);
-        const float e0 = expf(l0 - m), e1 = expf(l1 - m);
-        const float p0 = e0 / (e0 + e1);
-        bool ambiguous;
-        uint8_t act;
-        if (mode & 4) {
-            // collection: find this state's segment and its two draws
-            size_t lo = 0, hi = nseg;  // seg_off[lo] <= s < seg_off[hi]
-            while (hi - lo > 1) {
-                const size_t mid = (lo + hi) >> 1;
-                if (seg_off[mid] <= s) lo = mid; else hi = mid;
-            }
-            const uint64_t j = s - seg_off[lo];
-            const uint64_t seed = seg_seed[lo];
-            const double ue = unit_of(sm_draw(seed, 2 * j + 1));
-            const double ua = unit_of(sm_draw(seed, 2 * j + 2));
-            if (ue < eps) {
-                act = ua < 0.5 ? 0 : 1;
-                ambiguous = false;
-            } else {
-                // |p0_fp32 - p0_exact| <= |dp0/dd| * 2D3 + fp32 rounding of exp/div
-                //                     <= 0.25 * T + 16 u
-                const double tol = 0.25 * (double)T + 16.0 * 5.9604645e-8;
-                ambiguous = fabs(ua - (double)p0) <= tol;
-                act = ua < (double)p0 ? 0 : 1;
-            }
-        } else {
-            ambiguous = !(fabsf(d) > T);
-            act = d > 0.f ? 1 : 0;
-        }
-        if (ambiguous) {
-            const unsigned int slot = atomicAdd(n_recheck, 1u);
-            recheck[slot] = (uint32_t)s;
-        }
-        if (mode & 2) actions[s] = act;
-        if (mode & 1) {
-            probs[2 * s] = (double)p0;
-            probs[2 * s + 1] = (double)(e1 / (e0 + e1));
-        }
+        if (act0)
+            fast_finish(S, base + lane, la.x, la.y, Xa, hma, h2a, fa, probs, actions, seg_off, nseg,
+                        seg_seed, eps, recheck, n_recheck, flags, mode);
+        if (act1)
+            fast_finish(S, base + 32 + lane, lb.x, lb.y, Xb, hmb, h2b, fb, probs, actions, seg_off,
+                        nseg, seg_seed, eps, recheck, n_recheck, flags, mode);
     }
 }
 
@@ -330,15 +380,12 @@ __device__ __forceinline__ void exact_forward(const ExactSmem& S, const float* _
 }
 
 __device__ void load_exact_weights(ExactSmem& S, const float* __restrict__ p) {
-    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) {
-        const int j = t / F, i = t - j * F;  // coalesced read of w0[j][i]
-        S.w0[(j >> 1) * (2 * F) + 2 * i + (j & 1)] = p[OFF_W0 + t];
-    }
+    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) S.w0[t] = p[OFF_W0 + t];
     for (int t = threadIdx.x; t < H1 * H2; t += blockDim.x) {
         const int k = t / H1, j = t % H1;
         S.w1t[j * H2 + k] = p[OFF_W1 + t];
     }
-    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[(t % H2) * A + t / H2] = p[OFF_W2 + t];
+    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[t] = p[OFF_W2 + t];
     for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = p[OFF_B0 + t];
     for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = p[OFF_B1 + t];
     if (threadIdx.x < A) S.b2[threadIdx.x] = p[OFF_B2 + threadIdx.x];

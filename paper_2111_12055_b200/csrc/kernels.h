@@ -7,7 +7,7 @@
 
 namespace gbxcu {
 
-constexpr int FWD_BLOCK = 256;    // fast inference: 8 warps, one state per thread
+constexpr int FWD_BLOCK = 256;    // fast inference: 8 warps, two states per thread
 constexpr int EXACT_BLOCK = 128;  // exact fp64 inference
 constexpr int TRAIN_BLOCK = 512;  // train: 16 warps; tiles of 32 or 64 records
 constexpr int SHUF_BLOCK = 256;
