@@ -27,10 +27,11 @@
 // Operand layouts use row strides = 4 or 12 (mod 16) doubles, so every m8n8k4
 // fragment load (row- or column-wise) is bank-conflict free.
 //
-// Step synchronisation is data-flow, not grid barriers:
+// Step synchronisation (one arrival counter + data-flow words):
 //   1. every CTA stores its gradient+loss partial (row of PSTR doubles) and
-//      publishes flag[c] = tag (release);
-//   2. CTA c waits for all flags, then reduces the contiguous slice
+//      arrives on a monotonic counter (red.release); one thread per CTA polls
+//      it (ld.acquire) while the other warps stage the next tile;
+//   2. CTA c then reduces the contiguous slice
 //      [c*chunk, (c+1)*chunk) of every partial plus the loss (fixed order:
 //      8 CTA subsets x strided folds, then an in-order sum of the 8) — every
 //      CTA reduces the loss identically, so all agree on divergence;
@@ -154,9 +155,6 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
 }
 __device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // fp32 parameter p -> fp64 smem replica
@@ -344,10 +342,10 @@ __device__ void tc_init_consts(TcSmem<MT>& S) {
 // log-targets ln(t^_a) the KL term needs. Caller: cp.async complete + barrier
 // before, barrier after.
 template <int MT>
-__device__ void tc_stage_in(TcSmem<MT>& S, int slot) {
+__device__ void tc_stage_in(TcSmem<MT>& S, int slot, int t0 = 0) {
     constexpr int TB = 8 * MT;
     const int tid = threadIdx.x;
-    for (int t = tid; t < TB * F; t += NT) {
+    for (int t = tid - t0; t < TB * F; t += NT - t0) {
         const int r = t / F;
         S.x[r * SX + (t - r * F)] = (double)S.stage_f[slot][t];
     }
@@ -357,153 +355,162 @@ __device__ void tc_stage_in(TcSmem<MT>& S, int slot) {
     }
 }
 
+__device__ __forceinline__ void pair_sync(int id) {
+    asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+
 // One tile of 8*MT records (rows >= nv are zero padding and contribute 0);
 // X and ltgt already staged by tc_stage_in.
+//
+// Record chain, per m-tile, on a warp pair (warps 2p, 2p+1 own m-tile p; they
+// synchronise with a 64-thread named barrier only, so pairs drift freely and
+// one pair's softmax overlaps the others' tensor work):
+//   F1 (n-tiles 4h..4h+3) | F2 (n-tiles 2h, 2h+1) | F3 + B1 | B2 (n-tiles 4h..4h+3)
+// then one CTA barrier and the gradient phase over all records (all warps):
+//   G1 (+ gb1 via H1's ones column), E, G0 (+ gb0 via X's ones column).
 template <int MT>
 __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
     constexpr int TB = 8 * MT;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int gq = lane >> 2, tq = lane & 3;
 
-    // ---- F1: H1 = relu(X W0^T + b0). Warp: n-tile w&7, m-tiles (w>>3) + 2q.
+    if (w < 2 * MT) {
+        const int p = w >> 1, h = w & 1, bar = 1 + p;
+        const int r = p * 8 + gq;  // this lane's record row in A fragments / C rows
+        // ---- F1: H1[p-tile][n-tiles 4h..4h+3] = relu(X W0^T + b0), K = 44
+        {
+            double acc[4][2];
+#pragma unroll
+            for (int nn = 0; nn < 4; ++nn) {
+                const int c = (4 * h + nn) * 8 + 2 * tq;
+                acc[nn][0] = S.b0[c];
+                acc[nn][1] = S.b0[c + 1];
+            }
+            const double* xa = S.x + r * SX + tq;
+            const double* wb = S.w0 + ((4 * h) * 8 + gq) * SW0 + tq;
+#pragma unroll
+            for (int k0 = 0; k0 < F; k0 += 4) {
+                const double af = xa[k0];
+#pragma unroll
+                for (int nn = 0; nn < 4; ++nn) dmma(acc[nn], af, wb[nn * 8 * SW0 + k0]);
+            }
+#pragma unroll
+            for (int nn = 0; nn < 4; ++nn) {
+                double* o = S.h1 + r * SH1 + (4 * h + nn) * 8 + 2 * tq;
+                o[0] = acc[nn][0] > 0.0 ? acc[nn][0] : 0.0;
+                o[1] = acc[nn][1] > 0.0 ? acc[nn][1] : 0.0;
+            }
+        }
+        pair_sync(bar);
+        TC_MARK(1);
+        // ---- F2: H2[p-tile][n-tiles 2h, 2h+1] = relu(H1 W1^T + b1), K = 64
+        {
+            double acc[2][2];
+#pragma unroll
+            for (int nn = 0; nn < 2; ++nn) {
+                const int c = (2 * h + nn) * 8 + 2 * tq;
+                acc[nn][0] = S.b1[c];
+                acc[nn][1] = S.b1[c + 1];
+            }
+            const double* ha = S.h1 + r * SH1 + tq;
+            const double* wb = S.w1 + ((2 * h) * 8 + gq) * SW1 + tq;
+#pragma unroll
+            for (int k0 = 0; k0 < H1; k0 += 4) {
+                const double af = ha[k0];
+#pragma unroll
+                for (int nn = 0; nn < 2; ++nn) dmma(acc[nn], af, wb[nn * 8 * SW1 + k0]);
+            }
+#pragma unroll
+            for (int nn = 0; nn < 2; ++nn) {
+                double* o = S.h2 + r * SH2 + (2 * h + nn) * 8 + 2 * tq;
+                o[0] = acc[nn][0] > 0.0 ? acc[nn][0] : 0.0;
+                o[1] = acc[nn][1] > 0.0 ? acc[nn][1] : 0.0;
+            }
+        }
+        pair_sync(bar);
+        TC_MARK(2);
+        // ---- F3 + B1 (both warps of the pair compute the logits / softmax;
+        //      warp h writes D2 n-tiles 2h, 2h+1, warp 0 writes U)
+        {
+            double lg[2];
+            lg[0] = tq == 0 ? S.b2[0] : 0.0;
+            lg[1] = tq == 0 ? S.b2[1] : 0.0;
+            const double* hb = S.h2 + r * SH2 + tq;
+#pragma unroll
+            for (int k0 = 0; k0 < H2; k0 += 4)
+                dmma(lg, hb[k0], gq < A ? S.w2[gq * H2 + k0 + tq] : 0.0);
+            const double l0 = __shfl_sync(0xffffffffu, lg[0], lane & ~3);
+            const double l1 = __shfl_sync(0xffffffffu, lg[1], lane & ~3);
+            const int a = tq & 1;
+            // log-softmax form: with d = l_a - l_other, z = exp(-|d|),
+            //   p_a = (d >= 0 ? 1 : z) / (1 + z),  ln p_a = min(d, 0) - log1p(z)
+            // (equal to the reference's exp / sum / log(p/t) up to fp64 rounding)
+            const double d = a ? l1 - l0 : l0 - l1;
+            const double z = exp(-fabs(d));
+            const double lse = log1p(z);
+            const double pa = (d >= 0.0 ? 1.0 : z) / (1.0 + z);
+            const double lpc = pa < 1e-7 ? LN_PMIN : (pa > 1.0 - 1e-7 ? LN_PMAX : fmin(d, 0.0) - lse);
+            const double pc = clampp(pa);
+            const double lr = lpc - S.ltgt[2 * r + a];
+            const double term = pc * lr;
+            const double to = __shfl_xor_sync(0xffffffffu, term, 1);
+            const double loss = a ? to + term : term + to;
+            const bool valid = r < nv;
+            const double d3 = (valid && tq < 2) ? pa * (lr - loss) * inv_b : 0.0;
+            if (h == 0) {
+                if (tq < 2) S.u[r * SU + tq] = d3;
+                if (tq == 0) S.u[r * SU + 2] = valid ? loss : 0.0;
+            }
+#pragma unroll
+            for (int nn = 0; nn < 2; ++nn) {
+                const int nt = 2 * h + nn;
+                double dd[2] = {0.0, 0.0};
+                dmma(dd, d3, tq < A ? S.w2[tq * H2 + nt * 8 + gq] : 0.0);
+                const int k = nt * 8 + 2 * tq;
+                const double* hh = S.h2 + r * SH2 + k;
+                S.d2[r * SH2 + k] = hh[0] <= 0.0 ? 0.0 : dd[0];
+                S.d2[r * SH2 + k + 1] = hh[1] <= 0.0 ? 0.0 : dd[1];
+            }
+        }
+        pair_sync(bar);
+        TC_MARK(3);
+        // ---- B2: D1[p-tile][n-tiles 4h..4h+3] = (D2 W1) o [h1 > 0], K = 32
+        {
+            double acc[4][2];
+#pragma unroll
+            for (int nn = 0; nn < 4; ++nn) acc[nn][0] = acc[nn][1] = 0.0;
+            const double* da = S.d2 + r * SH2 + tq;
+            const double* wb = S.w1 + tq * SW1 + (4 * h) * 8 + gq;  // B[k][j] = W1[k][j]
+#pragma unroll
+            for (int k0 = 0; k0 < H2; k0 += 4) {
+                const double af = da[k0];
+#pragma unroll
+                for (int nn = 0; nn < 4; ++nn) dmma(acc[nn], af, wb[k0 * SW1 + nn * 8]);
+            }
+#pragma unroll
+            for (int nn = 0; nn < 4; ++nn) {
+                const int j = (4 * h + nn) * 8 + 2 * tq;
+                S.d1[r * SH1 + j] = S.h1[r * SH1 + j] <= 0.0 ? 0.0 : acc[nn][0];
+                S.d1[r * SH1 + j + 1] = S.h1[r * SH1 + j + 1] <= 0.0 ? 0.0 : acc[nn][1];
+            }
+        }
+    }
+    __syncthreads();
+    TC_MARK(4);
+
+    // ---- gradient phase, K = records of the tile (accumulators persist over the step)
     {
-        constexpr int Q = (MT + 1) / 2;
         const int nt = w & 7, mq = w >> 3;
-        double acc[Q][2];
-        const double bA = S.b0[nt * 8 + 2 * tq], bB = S.b0[nt * 8 + 2 * tq + 1];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) { acc[q][0] = bA; acc[q][1] = bB; }
-        const double* wb = S.w0 + (nt * 8 + gq) * SW0 + tq;
-        const double* xb = S.x + (mq * 8 + gq) * SX + tq;
-#pragma unroll
-        for (int k0 = 0; k0 < F; k0 += 4) {
-            const double bf = wb[k0];
-#pragma unroll
-            for (int q = 0; q < Q; ++q)
-                if (mq + 2 * q < MT) dmma(acc[q], xb[q * 16 * SX + k0], bf);
-        }
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            const int mt = mq + 2 * q;
-            if (mt < MT) {
-                double* o = S.h1 + (mt * 8 + gq) * SH1 + nt * 8 + 2 * tq;
-                o[0] = acc[q][0] > 0.0 ? acc[q][0] : 0.0;
-                o[1] = acc[q][1] > 0.0 ? acc[q][1] : 0.0;
-            }
-        }
-    }
-    __syncthreads();
-    TC_MARK(1);
-
-    // ---- F2: H2 = relu(H1 W1^T + b1). Warp: n-tile w&3, m-tiles (w>>2) + 4q.
-    {
-        constexpr int Q = (MT + 3) / 4;
-        const int nt = w & 3, mq = w >> 2;
-        double acc[Q][2];
-        const double bA = S.b1[nt * 8 + 2 * tq], bB = S.b1[nt * 8 + 2 * tq + 1];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) { acc[q][0] = bA; acc[q][1] = bB; }
-        const double* wb = S.w1 + (nt * 8 + gq) * SW1 + tq;
-        const double* hb = S.h1 + (mq * 8 + gq) * SH1 + tq;
-#pragma unroll 4
-        for (int k0 = 0; k0 < H1; k0 += 4) {
-            const double bf = wb[k0];
-#pragma unroll
-            for (int q = 0; q < Q; ++q)
-                if (mq + 4 * q < MT) dmma(acc[q], hb[q * 32 * SH1 + k0], bf);
-        }
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            const int mt = mq + 4 * q;
-            if (mt < MT) {
-                double* o = S.h2 + (mt * 8 + gq) * SH2 + nt * 8 + 2 * tq;
-                o[0] = acc[q][0] > 0.0 ? acc[q][0] : 0.0;
-                o[1] = acc[q][1] > 0.0 ? acc[q][1] : 0.0;
-            }
-        }
-    }
-    __syncthreads();
-    TC_MARK(2);
-
-    // ---- F3 + B1 on warps w < MT (m-tile w): logits by DMMA (B = W2^T padded
-    //      to 8 columns), softmax / KL / d3 in lanes t < 2 of each row group
-    //      (record r = 8w + g, action a = t), then D2 by a K=4 DMMA whose A
-    //      fragment is exactly those lanes' d3 values.
-    if (w < MT) {
-        const int r = w * 8 + gq;
-        double lg[2];
-        lg[0] = tq == 0 ? S.b2[0] : 0.0;
-        lg[1] = tq == 0 ? S.b2[1] : 0.0;
-        const double* hb = S.h2 + r * SH2 + tq;
-#pragma unroll
-        for (int k0 = 0; k0 < H2; k0 += 4)
-            dmma(lg, hb[k0], gq < A ? S.w2[gq * H2 + k0 + tq] : 0.0);
-        const double l0 = __shfl_sync(0xffffffffu, lg[0], lane & ~3);
-        const double l1 = __shfl_sync(0xffffffffu, lg[1], lane & ~3);
-        const int a = tq & 1;
-        // log-softmax form: with d = l_a - l_other, z = exp(-|d|),
-        //   p_a = (d >= 0 ? 1 : z) / (1 + z),  ln p_a = min(d, 0) - log1p(z)
-        // (equal to the reference's exp / sum / log(p/t) up to fp64 rounding)
-        const double d = a ? l1 - l0 : l0 - l1;
-        const double z = exp(-fabs(d));
-        const double lse = log1p(z);
-        const double p = (d >= 0.0 ? 1.0 : z) / (1.0 + z);
-        const double lpc = p < 1e-7 ? LN_PMIN : (p > 1.0 - 1e-7 ? LN_PMAX : fmin(d, 0.0) - lse);
-        const double pc = clampp(p);
-        const double lr = lpc - S.ltgt[2 * r + a];
-        const double term = pc * lr;
-        const double to = __shfl_xor_sync(0xffffffffu, term, 1);
-        const double loss = a ? to + term : term + to;
-        const bool valid = r < nv;
-        const double d3 = (valid && tq < 2) ? p * (lr - loss) * inv_b : 0.0;
-        if (tq < 2) S.u[r * SU + tq] = d3;
-        if (tq == 0) S.u[r * SU + 2] = valid ? loss : 0.0;
-#pragma unroll
-        for (int nt = 0; nt < H2 / 8; ++nt) {
-            double dd[2] = {0.0, 0.0};
-            dmma(dd, d3, tq < A ? S.w2[tq * H2 + nt * 8 + gq] : 0.0);
-            const int k = nt * 8 + 2 * tq;
-            const double* h = S.h2 + r * SH2 + k;
-            S.d2[r * SH2 + k] = h[0] <= 0.0 ? 0.0 : dd[0];
-            S.d2[r * SH2 + k + 1] = h[1] <= 0.0 ? 0.0 : dd[1];
-        }
-    }
-    __syncthreads();
-    TC_MARK(3);
-
-    // ---- B2: D1 = (D2 W1) o [h1 > 0]; G1: gW1 += D2^T H1; extra tiles (gb1, E)
-    {
-        constexpr int Q = (MT + 1) / 2;
-        const int nt = w & 7, mq = w >> 3;
-        double acc[Q][2];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) acc[q][0] = acc[q][1] = 0.0;
-        const double* wb = S.w1 + tq * SW1 + nt * 8 + gq;  // B[k][j] = W1[k][j]
-        const double* db = S.d2 + (mq * 8 + gq) * SH2 + tq;
-#pragma unroll
-        for (int k0 = 0; k0 < H2; k0 += 4) {
-            const double bf = wb[k0 * SW1];
-#pragma unroll
-            for (int q = 0; q < Q; ++q)
-                if (mq + 2 * q < MT) dmma(acc[q], db[q * 16 * SH2 + k0], bf);
-        }
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            const int mt = mq + 2 * q;
-            if (mt < MT) {
-                const int r = mt * 8 + gq, j = nt * 8 + 2 * tq;
-                S.d1[r * SH1 + j] = S.h1[r * SH1 + j] <= 0.0 ? 0.0 : acc[q][0];
-                S.d1[r * SH1 + j + 1] = S.h1[r * SH1 + j + 1] <= 0.0 ? 0.0 : acc[q][1];
-            }
-        }
         // G1: A[k][r] = D2[r][k], B[r][j] = H1[r][j]; m-tiles (k) mq + 2q, n-tile nt
-        const double* ab = S.d2 + tq * SH2 + mq * 8 + gq;
-        const double* bb = S.h1 + tq * SH1 + nt * 8 + gq;
+        {
+            const double* ab = S.d2 + tq * SH2 + mq * 8 + gq;
+            const double* bb = S.h1 + tq * SH1 + nt * 8 + gq;
 #pragma unroll
-        for (int r0 = 0; r0 < TB; r0 += 4) {
-            const double bf = bb[r0 * SH1];
-            dmma(g.g1[0], ab[r0 * SH2], bf);
-            dmma(g.g1[1], ab[r0 * SH2 + 16], bf);
+            for (int r0 = 0; r0 < TB; r0 += 4) {
+                const double bf = bb[r0 * SH1];
+                dmma(g.g1[0], ab[r0 * SH2], bf);
+                dmma(g.g1[1], ab[r0 * SH2 + 16], bf);
+            }
         }
         const int x = w - XW0;
         if (x >= 0) {
@@ -515,26 +522,23 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
 #pragma unroll 7
             for (int r0 = 0; r0 < TB; r0 += 4) dmma(g.gx, xa[r0 * sa], xb[r0 * sb]);
         }
-    }
-    __syncthreads();
-    TC_MARK(4);
-
-    // ---- G0: [gW0|gb0]^T += [X|1]^T D1: A[i][r] = X[r][i], B[r][j] = D1[r][j]
-    {
-        const int nt = w & 7, mq = w >> 3;
-        const double* ab = S.x + tq * SX + mq * 8 + gq;
-        const double* bb = S.d1 + tq * SH1 + nt * 8 + gq;
+        // G0: [gW0|gb0]^T += [X|1]^T D1: A[i][r] = X[r][i], B[r][j] = D1[r][j]
+        {
+            const double* ab = S.x + tq * SX + mq * 8 + gq;
+            const double* bb = S.d1 + tq * SH1 + nt * 8 + gq;
 #pragma unroll 2
-        for (int r0 = 0; r0 < TB; r0 += 4) {
-            const double bf = bb[r0 * SH1];
-            const double* ar = ab + r0 * SX;
-            dmma(g.g0[0], ar[0], bf);
-            dmma(g.g0[1], ar[16], bf);
-            dmma(g.g0[2], ar[32], bf);
+            for (int r0 = 0; r0 < TB; r0 += 4) {
+                const double bf = bb[r0 * SH1];
+                const double* ar = ab + r0 * SX;
+                dmma(g.g0[0], ar[0], bf);
+                dmma(g.g0[1], ar[16], bf);
+                dmma(g.g0[2], ar[32], bf);
+            }
         }
     }
     TC_MARK(5);
-    // (the caller's next __syncthreads orders G0's reads of X / D1 before P0)
+    // (the caller's next __syncthreads orders the gradient reads of X / D1 / H1
+    //  before the next tile overwrites them)
 }
 
 // Per-step record slice of CTA `cta` (rank-major, then CTA-major; identical to
@@ -667,35 +671,21 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         // ---- 1. publish this CTA's partial; stage the next tile meanwhile
         double* part = a.partials + (size_t)c * PSTR;
         tc_store_partial(g, part);
-        __syncthreads();
-#ifdef GBX_TC_FLAGS
+        if (stage_due) cp_async_wait_all();  // this thread's copies of the next tile
+        __syncthreads();                      // partial issued, gradient phase done, rows landed
+        // ---- 2. arrive, and wait for every partial (warp 0) while warps 1..15
+        //      stage the next tile
         if (tid == 0) {
-            __threadfence();
-            st_release_u32(a.flags + c, tag);
-        }
-#else
-        if (tid == 0) red_release_add_u32(a.flags, 1u);
-#endif
-        if (stage_due) {
-            cp_async_wait_all();
-            __syncthreads();
-            tc_stage_in(S, k & 1);
-            stage_due = false;
-        }
-        TC_MARK(7);
-        TC_TRACE(step, 1);
-        // ---- 2. wait for every partial, reduce [loss | slice] in a fixed order
-#ifdef GBX_TC_FLAGS
-        if (tid < G)
-            while (ld_acquire_u32(a.flags + tid) != tag) {
-            }
-#else
-        if (tid == 0) {
+            red_release_add_u32(a.flags, 1u);
+            TC_MARK(7);
+            TC_TRACE(step, 1);
             const unsigned target = tag * (unsigned)G;
             while ((int)(ld_acquire_u32(a.flags) - target) < 0) {
             }
+        } else if (stage_due && tid >= 32) {
+            tc_stage_in(S, k & 1, 32);
         }
-#endif
+        stage_due = false;
         __syncthreads();
         TC_MARK(8);
         TC_TRACE(step, 2);
