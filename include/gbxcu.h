@@ -119,8 +119,9 @@ typedef struct {
     int epochs;           /* >= 1 */
     int batch_size;       /* >= 1; global batch across all ranks */
     uint64_t seed;        /* TrainConfig::seed (epoch shuffle stream) */
-    int max_ctas;         /* 0 = auto (1 CTA per 64 records of the per-rank batch, <= #SMs) */
-    int reserved;
+    int max_ctas;         /* 0 = auto (1 CTA per 32 records of the per-rank batch, <= #SMs) */
+    int virtual_ranks;    /* 0/1 = off. V in 2..8: run the fused peer-set path with V ranks
+                             inside one launch on this GPU (tests of the multi-GPU kernel) */
 } gbxcu_train_cfg;
 
 /* fit (proj/src/policy.cpp:297-337): seeded in-place Fisher-Yates per epoch
@@ -148,6 +149,22 @@ int gbxcu_fit_order(gbxcu_ctx* ctx, size_t n, uint64_t seed, int epochs, uint32_
 int gbxcu_comm_unique_id(uint8_t id_out[GBXCU_COMM_ID_BYTES]);
 int gbxcu_comm_init(gbxcu_ctx* ctx, const uint8_t id[GBXCU_COMM_ID_BYTES], int nranks, int rank);
 int gbxcu_comm_destroy(gbxcu_ctx* ctx);
+
+/* Fused data-parallel path over NVLink peer memory (one process per GPU).
+ * Instead of a per-step NCCL all-reduce, the multi-CTA train kernel of every
+ * rank exchanges gradient partials, arrival counts and the updated
+ * parameters directly in the peers' memory (reduce-scatter over all ranks'
+ * CTAs, then an LL-word all-gather) — one launch per epoch on every GPU.
+ * Protocol: every rank calls gbxcu_peer_export, the 64-byte handles are
+ * all-gathered by the caller (e.g. torch.distributed), every rank calls
+ * gbxcu_peer_attach with all of them, then the caller barriers before the
+ * first fit. All ranks must then make identical fit calls (as with NCCL).
+ * Replaces the all-reduce of the gradient in fit (proj/src/policy.cpp:327-332
+ * run data-parallel; the reference itself is single-threaded). */
+#define GBXCU_PEER_HANDLE_BYTES 64
+int gbxcu_peer_export(gbxcu_ctx* ctx, uint8_t handle_out[GBXCU_PEER_HANDLE_BYTES]);
+int gbxcu_peer_attach(gbxcu_ctx* ctx, int nranks, int rank, const uint8_t* handles);
+int gbxcu_peer_detach(gbxcu_ctx* ctx);
 
 /* ------------------------------------------------------------ aggregation */
 /* Application suite in CSR form (the per-benchmark data SimSuite::frame_time

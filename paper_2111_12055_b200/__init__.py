@@ -70,7 +70,7 @@ _u64 = C.c_uint64
 
 class TrainCfg(C.Structure):
     _fields_ = [("learning_rate", C.c_double), ("epochs", C.c_int), ("batch_size", C.c_int),
-                ("seed", C.c_uint64), ("max_ctas", C.c_int), ("reserved", C.c_int)]
+                ("seed", C.c_uint64), ("max_ctas", C.c_int), ("virtual_ranks", C.c_int)]
 
 
 class SuiteC(C.Structure):
@@ -88,8 +88,10 @@ EXPORTS = (
     "gbxcu_comm_destroy", "gbxcu_aggregate", "gbxcu_histogram", "gbxcu_suite_upload",
     "gbxcu_suite_free", "gbxcu_suite_features", "gbxcu_evaluate", "gbxcu_evaluate_dev",
     "gbxcu_wide_param_count", "gbxcu_wide_init", "gbxcu_wide_forward", "gbxcu_wide_fit",
-    "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing",
+    "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_peer_export",
+    "gbxcu_peer_attach", "gbxcu_peer_detach",
 )
+PEER_HANDLE_BYTES = 64
 
 _LIB = None
 
@@ -126,6 +128,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_comm_unique_id.argtypes = [C.c_char_p]
     L.gbxcu_comm_init.argtypes = [_vp, C.c_char_p, C.c_int, C.c_int]
     L.gbxcu_comm_destroy.argtypes = [_vp]
+    L.gbxcu_peer_export.argtypes = [_vp, C.c_char_p]
+    L.gbxcu_peer_attach.argtypes = [_vp, C.c_int, C.c_int, C.c_char_p]
+    L.gbxcu_peer_detach.argtypes = [_vp]
     L.gbxcu_aggregate.argtypes = [_vp, C.POINTER(SuiteC), _u8p, _u64p, C.c_int, _f64p, _vp]
     L.gbxcu_histogram.argtypes = [_vp, _f64p, _sz, _f64p, _u64p, _sz, C.POINTER(_sz)]
     L.gbxcu_suite_upload.argtypes = [_vp, C.POINTER(SuiteC), _f32p, C.POINTER(_vp)]
@@ -270,14 +275,15 @@ class Device:
         return g
 
     def fit(self, params, feat, tgt, lr=0.01, epochs=50, batch=32, seed=0, max_ctas=0,
-            raise_on_diverge=True):
+            raise_on_diverge=True, virtual_ranks=0):
         """fit(): returns (params, epoch_loss). Raises TrainingDivergedError like the reference
-        (the partially trained params are attached as .params)."""
+        (the partially trained params are attached as .params). virtual_ranks > 1 runs the
+        multi-GPU peer-set kernel path with that many ranks inside one launch."""
         p = np.array(params, np.float32, copy=True)
         feat = _f32(feat).reshape(-1, N_FEATURES)
         el = np.full(max(epochs, 1), np.nan, np.float64)
         de = C.c_int(-1)
-        cfg = TrainCfg(lr, epochs, batch, seed, max_ctas, 0)
+        cfg = TrainCfg(lr, epochs, batch, seed, max_ctas, virtual_ranks)
         rc = self.L.gbxcu_fit(self.h, p, feat, _f64(tgt), feat.shape[0], C.byref(cfg),
                               el.ctypes.data, C.byref(de))
         if rc == EDIVERGED and not raise_on_diverge:
@@ -302,10 +308,10 @@ class Device:
                                           stream))
 
     def fit_dev(self, d_params: int, d_feat: int, d_tgt: int, n: int, lr=0.01, epochs=1,
-                batch=32, seed=0, max_ctas=0, stream: int | None = None):
+                batch=32, seed=0, max_ctas=0, stream: int | None = None, virtual_ranks=0):
         el = np.full(max(epochs, 1), np.nan, np.float64)
         de = C.c_int(-1)
-        cfg = TrainCfg(lr, epochs, batch, seed, max_ctas, 0)
+        cfg = TrainCfg(lr, epochs, batch, seed, max_ctas, virtual_ranks)
         rc = self.L.gbxcu_fit_dev(self.h, d_params, d_feat, d_tgt, n, C.byref(cfg),
                                   el.ctypes.data, C.byref(de), stream)
         self._ck(rc, de.value)
@@ -369,6 +375,20 @@ class Device:
 
     def comm_destroy(self):
         self._ck(self.L.gbxcu_comm_destroy(self.h))
+
+    # fused data-parallel path over NVLink peer memory (see include/gbxcu.h)
+    def peer_export(self) -> bytes:
+        buf = C.create_string_buffer(PEER_HANDLE_BYTES)
+        self._ck(self.L.gbxcu_peer_export(self.h, buf))
+        return buf.raw
+
+    def peer_attach(self, handles: list, rank: int):
+        blob = b"".join(bytes(h) for h in handles)
+        assert len(blob) == PEER_HANDLE_BYTES * len(handles)
+        self._ck(self.L.gbxcu_peer_attach(self.h, len(handles), rank, blob))
+
+    def peer_detach(self):
+        self._ck(self.L.gbxcu_peer_detach(self.h))
 
     # ------------------------------------------------------------ aggregation
     def aggregate(self, suite: dict, shader_actions, run_seed, n_samples, want_samples=False):

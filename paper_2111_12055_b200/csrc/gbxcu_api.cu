@@ -81,7 +81,16 @@ struct gbxcu_ctx {
     std::mutex mu;
     // scratch
     DevBuf params, feat, tgt, probs, actions, recheck, counters, flags;
-    DevBuf order, order2, partials, red, bar, diverged, epoch_loss, epoch_acc, step_flags, llp;
+    DevBuf order, order2, partials, red, bar, diverged, epoch_loss, epoch_acc, status;
+    // multi-CTA epoch kernel: exchange regions (counter | LL words | partials)
+    // of the peer set. Real peer set: xchg[0] is this rank's (exported),
+    // peer_ptr[r] the opened regions of the others. Virtual ranks (single-GPU
+    // tests of the peer path): xchg[0..V) all local.
+    DevBuf xchg[MAX_PEERS];
+    void* peer_ptr[MAX_PEERS] = {};
+    int peers = 1, prank = 0;
+    uint32_t tag_next = 0;                 // LL tags used so far on the peer set
+    unsigned long long ctr_base[MAX_PEERS] = {};  // counter values (identical across a real set)
     DevBuf sh_jp, sh_head, sh_nxt, sh_succ, sh_root, sh_root2, sh_flags;
     DevBuf seg_off, seg_seed, grad, scalar;
     DevBuf s_app_pipe, s_pipe_slot, s_slot_shader, s_slot_frac, s_pipe_wt, s_shader_lat, s_app_f64;
@@ -124,8 +133,10 @@ int setup_kernel_attrs() {
         set((const void*)train_partial_kernel<32>, train_smem_bytes(32));
         set((const void*)train_partial_kernel<64>, train_smem_bytes(64));
         set((const void*)batch_grad_kernel, train_smem_bytes(64));
-        set((const void*)train_epoch_tc_kernel<4>, train_tc_smem_bytes(4));
-        set((const void*)train_epoch_tc_kernel<7>, train_tc_smem_bytes(7));
+        set((const void*)train_epoch_tc_kernel<4, false>, train_tc_smem_bytes(4));
+        set((const void*)train_epoch_tc_kernel<7, false>, train_tc_smem_bytes(7));
+        set((const void*)train_epoch_tc_kernel<4, true>, train_tc_smem_bytes(4));
+        set((const void*)train_epoch_tc_kernel<7, true>, train_tc_smem_bytes(7));
         set((const void*)train_partial_tc_kernel<4>, train_tc_smem_bytes(4));
         set((const void*)train_partial_tc_kernel<7>, train_tc_smem_bytes(7));
         set((const void*)tc_gemm_kernel, gemm_smem_bytes());
@@ -199,10 +210,11 @@ int validate_cfg(const gbxcu_train_cfg* cfg, size_t n) {
 // CTAs per step and records per tile: spread each rank's share of the batch
 // over up to one CTA per SM in tiles of 32 records; switch to 64-record
 // tiles once every SM already has more than 32 records.
-void train_grid(gbxcu_ctx* c, const gbxcu_train_cfg* cfg, size_t n, int& G, int& tb) {
+void train_grid(gbxcu_ctx* c, const gbxcu_train_cfg* cfg, size_t n, int nranks, int& G, int& tb,
+                int sm_share = 1) {
     const size_t b = std::min<size_t>((size_t)cfg->batch_size, n);
-    const size_t per_rank = (b + c->nranks - 1) / c->nranks;
-    G = (int)std::min<size_t>((per_rank + 31) / 32, (size_t)c->num_sms);
+    const size_t per_rank = (b + nranks - 1) / nranks;
+    G = (int)std::min<size_t>((per_rank + 31) / 32, (size_t)(c->num_sms / sm_share));
     if (cfg->max_ctas > 0) G = std::min(G, cfg->max_ctas);
     G = std::max(G, 1);
     const size_t per_cta = (per_rank + G - 1) / G;
@@ -249,6 +261,27 @@ int prepare_order(gbxcu_ctx* c, size_t n, cudaStream_t st) {
     return check_launch(c, "iota_kernel");
 }
 
+// Exchange region layout: [u64 counter | pad to 256 B][NP u64 LL words | pad][G x PSTR f64 partials]
+constexpr size_t XCHG_LL_OFF = 256;
+constexpr size_t XCHG_PART_OFF = XCHG_LL_OFF + ((NP * 8 + 255) / 256) * 256;
+size_t xchg_bytes(int g) { return XCHG_PART_OFF + (size_t)g * PSTR * sizeof(double); }
+
+int ensure_xchg(gbxcu_ctx* c, int slot, int g, cudaStream_t st) {
+    if (c->xchg[slot].cap >= xchg_bytes(g)) return GBXCU_OK;
+    CK(cudaStreamSynchronize(st));
+    RET(c->xchg[slot].ensure(xchg_bytes(g)));
+    CK(cudaMemsetAsync(c->xchg[slot].p, 0, xchg_bytes(g), st));
+    c->ctr_base[slot] = 0;
+    return GBXCU_OK;
+}
+
+void bind_region(TrainArgs& a, int r, void* base) {
+    auto* b = static_cast<unsigned char*>(base);
+    a.ctr[r] = reinterpret_cast<unsigned long long*>(b);
+    a.llp[r] = reinterpret_cast<unsigned long long*>(b + XCHG_LL_OFF);
+    a.part[r] = reinterpret_cast<double*>(b + XCHG_PART_OFF);
+}
+
 int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double* d_tgt, size_t n,
                const gbxcu_train_cfg* cfg, double* epoch_loss_out, int* diverged_epoch,
                cudaStream_t st) {
@@ -257,19 +290,41 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     RET(prepare_order(c, n, st));
     RET(c->epoch_loss.ensure(sizeof(double) * cfg->epochs));
     RET(c->epoch_acc.ensure(16));
+    if (c->peers < 0) return fail(GBXCU_EINVAL, "peer set timed out earlier; re-attach it");
+    // Peer set of the fused multi-CTA path: a real one (gbxcu_peer_attach: one
+    // process per GPU), or cfg->virtual_ranks virtual ranks inside one launch
+    // (single-GPU tests of the same kernel path).
+    if (cfg->virtual_ranks > 1 && (c->peers > 1 || c->comm))
+        return fail(GBXCU_EINVAL, "virtual ranks need a context without peers or communicator");
+    const int vranks = c->peers > 1 ? 1 : std::max(1, cfg->virtual_ranks);
+    const int eff_ranks = vranks > 1 ? vranks : c->nranks;
     int G = 1, tb = 32;
-    train_grid(c, cfg, n, G, tb);
+    train_grid(c, cfg, n, eff_ranks, G, tb, vranks);
     RET(c->partials.ensure(sizeof(double) * (size_t)G * PSTR));
-    RET(c->step_flags.ensure(sizeof(unsigned int) * (size_t)G));
-    RET(c->llp.ensure(sizeof(unsigned long long) * NP));
-    CK(cudaMemsetAsync(c->step_flags.p, 0, sizeof(unsigned int) * (size_t)G, st));
-    CK(cudaMemsetAsync(c->llp.p, 0, sizeof(unsigned long long) * NP, st));
-    // multi-CTA steps: tensor-core kernel, tiles of 32 (MT 4) or 56 (MT 7) records
-    const size_t per_cta = ((std::min<size_t>((size_t)cfg->batch_size, n) + c->nranks - 1) /
-                                c->nranks + G - 1) / G;
-    const int mt = per_cta <= 32 ? 4 : 7;
     RET(c->red.ensure(sizeof(double) * (NP + 1)));
-
+    RET(c->status.ensure(16));
+    CK(cudaMemsetAsync(c->status.p, 0, 16, st));
+    // multi-CTA steps: tensor-core kernel, tiles of 32 (MT 4) or 56 (MT 7) records
+    const size_t per_cta = ((std::min<size_t>((size_t)cfg->batch_size, n) + eff_ranks - 1) /
+                                eff_ranks + G - 1) / G;
+    const int mt = per_cta <= 32 ? 4 : 7;
+    if (vranks > MAX_PEERS || vranks * G > c->num_sms)
+        return fail(GBXCU_EINVAL, "virtual ranks x CTAs exceed the GPU");
+    if (vranks > 1 && G == 1) return fail(GBXCU_EINVAL, "virtual ranks need multi-CTA steps");
+    if (c->peers > 1 && c->comm) return fail(GBXCU_EINVAL, "peer set and NCCL communicator both attached");
+    if (c->peers > 1 && G == 1) return fail(GBXCU_EINVAL, "peer set needs multi-CTA steps (batch > 32 per rank)");
+    if (c->peers > 1 && c->xchg[0].cap < xchg_bytes(G))
+        return fail(GBXCU_EINVAL, "peer exchange region too small for this grid");
+    if (c->peers == 1) {
+        // local peer set (this GPU alone, or virtual ranks): this process owns
+        // every region, so the arrival counters restart at 0 each fit. LL tags
+        // stay monotonic over the context's life (stale words never match).
+        for (int r = 0; r < vranks; ++r) {
+            RET(ensure_xchg(c, r, G, st));
+            CK(cudaMemsetAsync(c->xchg[r].p, 0, sizeof(unsigned long long), st));
+            c->ctr_base[r] = 0;
+        }
+    }
     TrainArgs a{};
     a.feat = d_feat;
     a.tgt = d_tgt;
@@ -284,8 +339,18 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     a.lr = cfg->learning_rate;
     a.rank = c->rank;
     a.nranks = c->nranks;
-    a.flags = c->step_flags.as<unsigned int>();
-    a.llp = c->llp.as<unsigned long long>();
+    a.status = c->status.as<int>();
+    const int R = c->peers > 1 ? c->peers : vranks;
+    a.peers = R;
+    a.prank = c->peers > 1 ? c->prank : 0;
+    a.pvirt = c->peers > 1 ? 0 : (vranks > 1 ? 1 : 0);
+    for (int r = 0; r < R; ++r)
+        bind_region(a, r, c->peers > 1 ? (r == c->prank ? c->xchg[0].p : c->peer_ptr[r]) : c->xchg[r].p);
+    if (a.pvirt) {  // each virtual rank trains its slice of every global batch
+        a.nranks = R;
+        a.rank = 0;
+    }
+    const int GG = R * G;
     const long n_steps = (long)((n + cfg->batch_size - 1) / cfg->batch_size);
 
     const bool timed = cfg->epochs <= 8;  // per-kernel event timing (bench / profiling)
@@ -294,7 +359,8 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
         RET(shuffle_epoch(c, n, cfg->seed, e, st));
         a.order = c->order.as<uint32_t>();  // the pass output (buffers ping-pong)
         a.epoch = e;
-        a.tag_base = (unsigned int)((long)e * n_steps);
+        a.tag_base = c->tag_next + (unsigned int)((long)e * n_steps);
+        a.ctr_base = c->ctr_base[0] + (unsigned long long)e * n_steps * GG;
         if (!c->comm) {
             void* args[] = {&a};
             if (timed) CK(cudaEventRecord(c->ev[(2 * e + 1) % 16], st));
@@ -304,9 +370,14 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
                                           : (const void*)train_epoch_kernel<64>;
                 CK(cudaLaunchKernel(fn, 1, TRAIN_BLOCK, args, train_smem_bytes(tb), st));
             } else {
-                const void* fn = mt == 4 ? (const void*)train_epoch_tc_kernel<4>
-                                         : (const void*)train_epoch_tc_kernel<7>;
-                CK(cudaLaunchCooperativeKernel(fn, G, TRAIN_BLOCK, args, train_tc_smem_bytes(mt), st));
+                // system-scope exchange only across GPUs (a real peer set)
+                const bool sys = c->peers > 1;
+                const void* fn = mt == 4 ? (sys ? (const void*)train_epoch_tc_kernel<4, true>
+                                                : (const void*)train_epoch_tc_kernel<4, false>)
+                                         : (sys ? (const void*)train_epoch_tc_kernel<7, true>
+                                                : (const void*)train_epoch_tc_kernel<7, false>);
+                CK(cudaLaunchCooperativeKernel(fn, a.pvirt ? GG : G, TRAIN_BLOCK, args,
+                                               train_tc_smem_bytes(mt), st));
             }
             RET(check_launch(c, "train_epoch_kernel"));
             if (timed) CK(cudaEventRecord(c->ev[16 + e % 8], st));
@@ -338,8 +409,15 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
             RET(check_launch(c, "finish_epoch_kernel"));
         }
     }
-    int dv = -1;
+    int dv = -1, wd = 0;
     CK(cudaMemcpyAsync(&dv, c->diverged.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&wd, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    const bool used_tc = !c->comm && G > 1;
+    if (used_tc) {  // resynchronise the monotonic counters (divergence stops early)
+        for (int r = 0; r < (c->peers > 1 ? 1 : vranks); ++r)
+            CK(cudaMemcpyAsync(&c->ctr_base[r], c->xchg[r].p, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, st));
+    }
     if (epoch_loss_out)
         CK(cudaMemcpyAsync(epoch_loss_out, c->epoch_loss.p, sizeof(double) * cfg->epochs,
                            cudaMemcpyDeviceToHost, st));
@@ -353,6 +431,11 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
             c->last_shuffle_ms += a_ms;
             c->last_train_ms += b_ms;
         }
+    }
+    if (used_tc) c->tag_next += (uint32_t)((long)cfg->epochs * n_steps);
+    if (wd != 0) {
+        c->peers = c->peers > 1 ? -c->peers : c->peers;  // the set is unusable until re-attached
+        return fail(GBXCU_ECUDA, "peer synchronisation timed out (a rank stopped responding)");
     }
     if (diverged_epoch) *diverged_epoch = dv;
     if (dv >= 0)
@@ -423,6 +506,8 @@ int gbxcu_create(int device, gbxcu_ctx** out) {
 void gbxcu_destroy(gbxcu_ctx* c) {
     if (!c) return;
     if (c->comm) ncclCommDestroy(c->comm);
+    for (auto& p : c->peer_ptr)
+        if (p) cudaIpcCloseMemHandle(p);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -633,6 +718,63 @@ int gbxcu_comm_init(gbxcu_ctx* c, const uint8_t id[GBXCU_COMM_ID_BYTES], int nra
     CKN(ncclCommInitRank(&c->comm, nranks, uid, rank));
     c->nranks = nranks;
     c->rank = rank;
+    return GBXCU_OK;
+}
+
+int gbxcu_peer_export(gbxcu_ctx* c, uint8_t handle_out[GBXCU_PEER_HANDLE_BYTES]) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == GBXCU_PEER_HANDLE_BYTES, "IPC handle size");
+    if (!c || !handle_out) return fail(GBXCU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    // sized for the largest grid (one CTA per SM); zeroed: counters start at 0
+    if (c->xchg[0].cap < xchg_bytes(c->num_sms)) {
+        if (c->xchg[0].p) CK(cudaFree(c->xchg[0].p));
+        c->xchg[0].p = nullptr;
+        c->xchg[0].cap = 0;
+        RET(c->xchg[0].ensure(xchg_bytes(c->num_sms)));
+    }
+    CK(cudaMemset(c->xchg[0].p, 0, xchg_bytes(c->num_sms)));
+    CK(cudaDeviceSynchronize());
+    c->ctr_base[0] = 0;
+    c->tag_next = 0;
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->xchg[0].p));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return GBXCU_OK;
+}
+
+int gbxcu_peer_attach(gbxcu_ctx* c, int nranks, int rank, const uint8_t* handles) {
+    if (!c || !handles || nranks < 2 || nranks > MAX_PEERS || rank < 0 || rank >= nranks)
+        return fail(GBXCU_EINVAL, "bad peer-set arguments (2..8 ranks)");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    if (c->comm) return fail(GBXCU_EINVAL, "detach the NCCL communicator first");
+    if (c->xchg[0].cap < xchg_bytes(c->num_sms)) return fail(GBXCU_EINVAL, "call gbxcu_peer_export first");
+    for (int r = 0; r < nranks; ++r) {
+        if (r == rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + (size_t)r * GBXCU_PEER_HANDLE_BYTES, sizeof(h));
+        CK(cudaIpcOpenMemHandle(&c->peer_ptr[r], h, cudaIpcMemLazyEnablePeerAccess));
+    }
+    c->peers = nranks;
+    c->prank = rank;
+    c->nranks = nranks;
+    c->rank = rank;
+    return GBXCU_OK;
+}
+
+int gbxcu_peer_detach(gbxcu_ctx* c) {
+    if (!c) return fail(GBXCU_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    for (int r = 0; r < MAX_PEERS; ++r) {
+        if (c->peer_ptr[r]) cudaIpcCloseMemHandle(c->peer_ptr[r]);
+        c->peer_ptr[r] = nullptr;
+    }
+    c->peers = 1;
+    c->prank = 0;
+    c->nranks = 1;
+    c->rank = 0;
     return GBXCU_OK;
 }
 

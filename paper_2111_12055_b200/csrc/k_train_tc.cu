@@ -110,7 +110,7 @@ struct TcSmem {
     double d2[TB * SH2];
     double u[TB * SU];
     double ltgt[TB * 2];         // ln(clamp(target)) per (record, action)
-    double red[8 * 64];          // slice reduction: [CTA subset][element]
+    double red[NT + 64];         // slice reduction: [source subset][element], then totals
     uint32_t ord[2][TB];         // record indices of the next two tiles (cp.async ring)
     double stage_t[2][TB * 2];   // cp.async staging: targets
     float stage_f[2][TB * F];    // cp.async staging: raw fp32 features
@@ -140,22 +140,49 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+// Exchange accesses. Within one GPU (a single rank, or virtual ranks) they are
+// GPU-scope; a real peer set spans GPUs of the NVLink domain and needs
+// system scope (SYS), which is markedly more expensive.
+template <bool SYS>
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    if (SYS) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+template <bool SYS>
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if (SYS) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+template <bool SYS>
+__device__ __forceinline__ double ld_part(const double* p) {
+    if (SYS) {
+        double v;
+        asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+        return v;
+    }
+    return __ldcg(p);  // L2 (the coherence point of one GPU)
+}
+template <bool SYS>
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    if (SYS) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+template <bool SYS>
+__device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
+    if (SYS) asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Peer waits give up after this long (a lost rank must not hang the GPU).
+constexpr unsigned long long WATCHDOG_NS = 5000000000ull;
 
 // fp32 parameter p -> fp64 smem replica
 template <int MT>
@@ -198,9 +225,9 @@ __device__ void load_params_plain(TcSmem<MT>& S, const float* __restrict__ p) {
 }
 
 // All-gather of the LL words {tag, fp32 bits}: spin until every word this
-// thread owns carries `tag`.
-template <int MT>
-__device__ void load_params_ll(TcSmem<MT>& S, const unsigned long long* __restrict__ ll,
+// thread owns carries `tag`. False when the watchdog expired.
+template <bool SYS, int MT>
+__device__ bool load_params_ll(TcSmem<MT>& S, const unsigned long long* __restrict__ ll,
                                unsigned tag) {
     constexpr int PER = (NP + NT - 1) / NT;  // 10
     unsigned long long v[PER];
@@ -208,19 +235,26 @@ __device__ void load_params_ll(TcSmem<MT>& S, const unsigned long long* __restri
 #pragma unroll
     for (int q = 0; q < PER; ++q)
         if (threadIdx.x + q * NT < NP) pending |= 1u << q;
-    while (pending) {
+    unsigned long long t0 = 0;
+    for (unsigned it = 0; pending; ++it) {
 #pragma unroll
         for (int q = 0; q < PER; ++q)
-            if (pending & (1u << q)) v[q] = ld_relaxed_u64(ll + threadIdx.x + q * NT);
+            if (pending & (1u << q)) v[q] = ld_relaxed_u64<SYS>(ll + threadIdx.x + q * NT);
 #pragma unroll
         for (int q = 0; q < PER; ++q)
             if ((pending & (1u << q)) && (unsigned)(v[q] >> 32) == tag) pending &= ~(1u << q);
+        if (pending && (it & 255) == 255) {
+            const unsigned long long t = gtimer_ns();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > WATCHDOG_NS) return false;
+        }
     }
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
         const int p = threadIdx.x + q * NT;
         if (p < NP) put_param(S, p, (double)__uint_as_float((unsigned)v[q]));
     }
+    return true;
 }
 
 // Persistent per-thread gradient accumulators of one step.
@@ -543,14 +577,15 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
 
 // Per-step record slice of CTA `cta` (rank-major, then CTA-major; identical to
 // k_train.cu's step_slice).
-__device__ __forceinline__ void tc_slice(const TrainArgs& a, long step, int cta, int nctas,
-                                         uint32_t& lo, uint32_t& hi, uint32_t& nb) {
+__device__ __forceinline__ void tc_slice(const TrainArgs& a, int rank, int nranks, long step,
+                                         int cta, int nctas, uint32_t& lo, uint32_t& hi,
+                                         uint32_t& nb) {
     const uint32_t n = (uint32_t)a.n, batch = (uint32_t)a.batch;
     const uint32_t start = (uint32_t)step * batch;
     const uint32_t stop = min(n, start + batch);
     nb = stop - start;
-    const uint32_t per_rank = (nb + a.nranks - 1) / (uint32_t)a.nranks;
-    const uint32_t r_lo = min(stop, start + (uint32_t)a.rank * per_rank);
+    const uint32_t per_rank = (nb + nranks - 1) / (uint32_t)nranks;
+    const uint32_t r_lo = min(stop, start + (uint32_t)rank * per_rank);
     const uint32_t r_hi = min(stop, r_lo + per_rank);
     const uint32_t per_cta = (r_hi - r_lo + nctas - 1) / (uint32_t)nctas;
     lo = min(r_hi, r_lo + (uint32_t)cta * per_cta);
@@ -559,11 +594,16 @@ __device__ __forceinline__ void tc_slice(const TrainArgs& a, long step, int cta,
 
 // Next tile after (step, r0) within [step, n_steps); r0 == UINT32_MAX asks for
 // the first tile of `step`.
+struct TcWho {
+    int rank, nranks, cta, nctas;
+};
+
 template <int TB>
-__device__ bool tc_next(const TrainArgs& a, long n_steps, long& step, uint32_t& r0, int& nv) {
+__device__ bool tc_next(const TrainArgs& a, const TcWho& who, long n_steps, long& step,
+                        uint32_t& r0, int& nv) {
     uint32_t lo, hi, nb;
     if (r0 != 0xFFFFFFFFu) {
-        tc_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
+        tc_slice(a, who.rank, who.nranks, step, who.cta, who.nctas, lo, hi, nb);
         if (r0 + TB < hi) {
             r0 += TB;
             nv = (int)min((uint32_t)TB, hi - r0);
@@ -572,7 +612,7 @@ __device__ bool tc_next(const TrainArgs& a, long n_steps, long& step, uint32_t& 
         ++step;
     }
     for (; step < n_steps; ++step) {
-        tc_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
+        tc_slice(a, who.rank, who.nranks, step, who.cta, who.nctas, lo, hi, nb);
         if (hi > lo) {
             r0 = lo;
             nv = (int)min((uint32_t)TB, hi - lo);
@@ -595,18 +635,33 @@ __device__ __forceinline__ void tc_store_partial(const TcGrads& g, double* __res
 
 size_t train_tc_smem_bytes(int mt) { return mt == 4 ? sizeof(TcSmem<4>) : sizeof(TcSmem<7>); }
 
-template <int MT>
+template <int MT, bool SYS>
 __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     constexpr int TB = 8 * MT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TcSmem<MT>& S = *reinterpret_cast<TcSmem<MT>*>(smem_raw);
-    if (*a.diverged_epoch >= 0) return;
+    if (*a.diverged_epoch >= 0 || *a.status != 0) return;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int G = gridDim.x, c = blockIdx.x;
+    // peer set: R ranks x Gl CTAs; this CTA is (rank, c), global index gc
+    const int R = a.peers;
+    const int Gl = a.pvirt ? (int)gridDim.x / R : (int)gridDim.x;
+    const int rank = a.pvirt ? (int)blockIdx.x / Gl : a.prank;
+    const int c = a.pvirt ? (int)blockIdx.x % Gl : (int)blockIdx.x;
+    const int GG = R * Gl, gc = rank * Gl + c;
+    const TcWho who{rank, R, c, Gl};
     const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
-    const int chunk = (NP + G - 1) / G;
-    const int p_lo = c * chunk, p_hi = min(NP, p_lo + chunk);
-    const int n_elem = 1 + max(0, p_hi - p_lo);  // element 0 = loss, then the slice
+    // reduce-scatter slice of this CTA: element 0 = loss, then params [p_lo, p_hi)
+    const int chunk = (NP + GG - 1) / GG;
+    const int p_lo = min(NP, gc * chunk), p_hi = min(NP, p_lo + chunk);
+    const int n_elem = 1 + (p_hi - p_lo);
+    // reduction layout: EB elements x SUB source subsets (EB * SUB = NT)
+    int EB = 8;
+    while (EB < 64 && EB < n_elem) EB <<= 1;
+    const int SUB = NT / EB;
+    double* my_part = a.part[rank] + (size_t)c * PSTR;
+    unsigned long long* my_ctr = a.ctr[rank];
+    const unsigned long long* my_llp = a.llp[rank];
+    bool aborted = false;
 
     // Pipeline (tile k): rows of tile k+1 and indices of tile k+2 are fetched
     // (cp.async) at the top of tile k; tile k+1 is staged into X (P0) right
@@ -615,10 +670,10 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     long s1 = 0, s2 = 0;
     uint32_t r1 = 0xFFFFFFFFu, r2;
     int n1 = 0, n2 = 0;
-    bool h1 = tc_next<TB>(a, n_steps, s1, r1, n1);  // tile 0
+    bool h1 = tc_next<TB>(a, who, n_steps, s1, r1, n1);  // tile 0
     if (h1) tc_fetch_idx(S, 0, a, r1, n1);
     s2 = s1; r2 = r1;
-    bool h2 = h1 && tc_next<TB>(a, n_steps, s2, r2, n2);  // tile 1
+    bool h2 = h1 && tc_next<TB>(a, who, n_steps, s2, r2, n2);  // tile 1
     if (h2) tc_fetch_idx(S, 1, a, r2, n2);
     cp_async_commit();
     load_params_plain(S, a.params);
@@ -633,7 +688,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     // shift: c1 <- tile 1, c2 <- tile 2
     h1 = h2; s1 = s2; r1 = r2; n1 = n2;
     s2 = s1; r2 = r1;
-    h2 = h1 && tc_next<TB>(a, n_steps, s2, r2, n2);
+    h2 = h1 && tc_next<TB>(a, who, n_steps, s2, r2, n2);
     TcGrads g;
     tc_zero(g);
     double epoch_total = 0.0;
@@ -643,7 +698,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
 
     for (long step = 0; step < n_steps; ++step) {
         uint32_t lo, hi, nb;
-        tc_slice(a, step, c, G, lo, hi, nb);
+        tc_slice(a, rank, R, step, c, Gl, lo, hi, nb);
         const double inv_b = 1.0 / (double)nb;
         const unsigned tag = a.tag_base + (unsigned)step + 1u;
         TC_TRACE(step, 0);
@@ -655,7 +710,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
             if (h2) tc_fetch_idx(S, k & 1, a, r2, n2);        // indices of tile k+2
             cp_async_commit();
             h1 = h2; s1 = s2; r1 = r2; n1 = n2;
-            if (h2) h2 = tc_next<TB>(a, n_steps, s2, r2, n2);
+            if (h2) h2 = tc_next<TB>(a, who, n_steps, s2, r2, n2);
             TC_MARK(6);
             tc_tile<MT>(S, g, nv, inv_b);
             if (more && r0 + TB < hi) {
@@ -668,19 +723,28 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
                 stage_due = more;  // staged after this step's partial is published
             }
         }
-        // ---- 1. publish this CTA's partial; stage the next tile meanwhile
-        double* part = a.partials + (size_t)c * PSTR;
-        tc_store_partial(g, part);
+        // ---- 1. publish this CTA's partial
+        tc_store_partial(g, my_part);
         if (stage_due) cp_async_wait_all();  // this thread's copies of the next tile
         __syncthreads();                      // partial issued, gradient phase done, rows landed
-        // ---- 2. arrive, and wait for every partial (warp 0) while warps 1..15
-        //      stage the next tile
+        // ---- 2. arrive on every rank's counter; wait (warp 0) until all GG
+        //      CTAs of the set arrived while warps 1..15 stage the next tile
         if (tid == 0) {
-            red_release_add_u32(a.flags, 1u);
+            for (int r = 0; r < R; ++r) red_release_add_u64<SYS>(a.ctr[r], 1ull);
             TC_MARK(7);
             TC_TRACE(step, 1);
-            const unsigned target = tag * (unsigned)G;
-            while ((int)(ld_acquire_u32(a.flags) - target) < 0) {
+            const unsigned long long target =
+                a.ctr_base + (unsigned long long)(step + 1) * (unsigned long long)GG;
+            unsigned long long t0 = 0;
+            for (unsigned it = 0; ld_acquire_u64<SYS>(my_ctr) < target; ++it) {
+                if ((it & 255) == 255) {
+                    const unsigned long long t = gtimer_ns();
+                    if (t0 == 0) t0 = t;
+                    else if (t - t0 > WATCHDOG_NS) {
+                        S.scal[1] = 2.0;  // abort
+                        break;
+                    }
+                }
             }
         } else if (stage_due && tid >= 32) {
             tc_stage_in(S, k & 1, 32);
@@ -689,31 +753,39 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         __syncthreads();
         TC_MARK(8);
         TC_TRACE(step, 2);
+        if (S.scal[1] == 2.0) {
+            aborted = true;
+            break;
+        }
+        // ---- 3. reduce [loss | slice] over all GG partials, fixed association:
+        //      thread (e, s) folds, rank by rank, the CTAs c' = s, s + SUB, ...,
+        //      then thread e sums the SUB subset totals in order
         bool diverged = false;
-        for (int e0 = 0; e0 < n_elem; e0 += 64) {
-            // warp w: elements e0 + 32*(w&1) + lane, CTA subset s = w>>1 (c' = s + 8q)
-            const int e = e0 + 32 * (w & 1) + lane, s8 = w >> 1;
+        for (int e0 = 0; e0 < n_elem; e0 += EB) {
+            const int e = e0 + tid % EB, sb = tid / EB;
             double v = 0.0;
             if (e < n_elem) {
                 const int p = e == 0 ? NP : p_lo + e - 1;
-                const double* src = a.partials + p;
-                double buf_v[19];
+                for (int r = 0; r < R; ++r) {
+                    // all of this rank's loads in flight at once (one round trip)
+                    const double* src = a.part[r] + p;
+                    double u[20];
 #pragma unroll
-                for (int q = 0; q < 19; ++q) {
-                    const int cc = s8 + 8 * q;
-                    buf_v[q] = cc < G ? __ldcg(src + (size_t)cc * PSTR) : 0.0;
+                    for (int j = 0; j < 20; ++j) {
+                        const int q = sb + j * SUB;
+                        u[j] = q < Gl ? ld_part<SYS>(src + (size_t)q * PSTR) : 0.0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 20; ++j) v += u[j];
+                    for (int q = sb + 20 * SUB; q < Gl; q += SUB) v += ld_part<SYS>(src + (size_t)q * PSTR);
                 }
-#pragma unroll
-                for (int q = 0; q < 19; ++q) v += buf_v[q];
-                for (int cc = s8 + 8 * 19; cc < G; cc += 8) v += __ldcg(src + (size_t)cc * PSTR);
             }
-            S.red[s8 * 64 + 32 * (w & 1) + lane] = v;
+            S.red[sb * EB + tid % EB] = v;
             __syncthreads();
-            if (tid < 64) {
+            if (tid < EB) {
                 double t = 0.0;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) t += S.red[q * 64 + tid];
-                S.red[tid] = t;  // row 0 is only read by this thread
+                for (int q = 0; q < SUB; ++q) t += S.red[q * EB + tid];
+                S.red[NT + tid] = t;
                 if (e0 == 0 && tid == 0) {
                     const double loss = t / (double)nb;
                     S.scal[0] = loss;
@@ -725,14 +797,15 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
                 diverged = true;
                 break;
             }
-            // ---- 3. SGD on the slice; publish {tag, fp32} words + the plain fp32 copy
-            if (tid < 64) {
+            // ---- 4. SGD on the slice; publish {tag, fp32} words to every rank
+            if (tid < EB) {
                 const int e2 = e0 + tid;
                 if (e2 >= 1 && e2 < n_elem) {
                     const int p = p_lo + e2 - 1;
-                    const float nw = __double2float_rn(get_param(S, p) - a.lr * S.red[tid]);
-                    a.params[p] = nw;
-                    st_relaxed_u64(a.llp + p, ((unsigned long long)tag << 32) | __float_as_uint(nw));
+                    const float nw = __double2float_rn(get_param(S, p) - a.lr * S.red[NT + tid]);
+                    const unsigned long long word =
+                        ((unsigned long long)tag << 32) | __float_as_uint(nw);
+                    for (int r = 0; r < R; ++r) st_relaxed_u64<SYS>(a.llp[r] + p, word);
                 }
             }
             __syncthreads();  // S.red reuse
@@ -744,16 +817,27 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         TC_MARK(9);
         TC_TRACE(step, 3);
         if (tid == 0) epoch_total = fma(S.scal[0], (double)nb, epoch_total);
-        // ---- 4. all-gather the new parameters (the next launch reads a.params)
-        if (step + 1 < n_steps) load_params_ll(S, a.llp, tag);
+        // ---- 5. all-gather the new parameters into the fp64 replicas
+        if (!load_params_ll<SYS>(S, my_llp, tag)) S.scal[1] = 2.0;
         tc_zero(g);
+        __syncthreads();
+        if (S.scal[1] == 2.0) {
+            aborted = true;
+            break;
+        }
         TC_MARK(10);
         TC_TRACE(step, 4);
-        // (the next tile's __syncthreads orders the replicas before use)
     }
     cp_async_wait_all();
-    if (c == 0 && tid == 0 && *a.diverged_epoch < 0)
-        a.epoch_loss[a.epoch] = epoch_total / (double)a.n;
+    if (aborted) {
+        if (tid == 0) atomicExch(a.status, 1);
+        return;
+    }
+    // rank-local outputs: params (fp32 values of the replicas) and the epoch loss
+    if (c == 0 && (!a.pvirt || rank == 0) && *a.diverged_epoch < 0) {
+        for (int t = tid; t < NP; t += NT) a.params[t] = (float)get_param(S, t);
+        if (tid == 0) a.epoch_loss[a.epoch] = epoch_total / (double)a.n;
+    }
 }
 
 // Data-parallel path: one step's per-CTA partials (the reduction, NCCL
@@ -765,7 +849,7 @@ __global__ void __launch_bounds__(NT, 1) train_partial_tc_kernel(TrainArgs a, lo
     TcSmem<MT>& S = *reinterpret_cast<TcSmem<MT>*>(smem_raw);
     if (*a.diverged_epoch >= 0) return;
     uint32_t lo, hi, nb;
-    tc_slice(a, step, blockIdx.x, gridDim.x, lo, hi, nb);
+    tc_slice(a, a.rank, a.nranks, step, blockIdx.x, gridDim.x, lo, hi, nb);
     if (hi > lo) tc_prefetch<MT>(S, 0, a, lo, (int)min((uint32_t)TB, hi - lo));
     load_params_plain(S, a.params);
     tc_init_consts(S);
@@ -786,8 +870,10 @@ __global__ void __launch_bounds__(NT, 1) train_partial_tc_kernel(TrainArgs a, lo
     tc_store_partial(g, a.partials + (size_t)blockIdx.x * PSTR);
 }
 
-template __global__ void train_epoch_tc_kernel<4>(TrainArgs);
-template __global__ void train_epoch_tc_kernel<7>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<4, false>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<7, false>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<4, true>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<7, true>(TrainArgs);
 template __global__ void train_partial_tc_kernel<4>(TrainArgs, long);
 template __global__ void train_partial_tc_kernel<7>(TrainArgs, long);
 

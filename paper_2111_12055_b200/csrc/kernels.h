@@ -14,6 +14,7 @@ constexpr int SHUF_BLOCK = 256;
 constexpr int AGG_BLOCK = 256;    // aggregation: 8 warps = 8 apps per CTA
 
 constexpr int PSTR = 5028;        // per-CTA partial row: 5,026 gradient entries, loss, pad
+constexpr int MAX_PEERS = 8;      // ranks of one NVLink domain (one node)
 
 // mode bits for the inference kernels
 constexpr int FWD_PROBS = 1, FWD_ACTIONS = 2, FWD_COLLECT = 4;
@@ -32,10 +33,18 @@ struct TrainArgs {
     int epoch;
     double lr;
     int rank, nranks;
-    // multi-CTA (tensor-core) epoch kernel: data-flow step synchronisation
-    unsigned int* flags;       // [G] "partial of step tag is published"
-    unsigned long long* llp;   // [NP] {tag, fp32 bits} parameter words
-    unsigned int tag_base;     // epoch * n_steps (flags/llp zeroed once per fit)
+    // multi-CTA epoch kernel (k_train_tc.cu): data-flow step synchronisation
+    // over a peer set — one process per GPU exchanging through NVLink peer
+    // memory, or (pvirt) every rank inside one launch for single-GPU tests.
+    int peers;                               // ranks in the set (1 = this GPU alone)
+    int prank;                               // this process's rank in the set
+    int pvirt;                               // 1: rank = blockIdx.x / (gridDim.x / peers)
+    unsigned long long* ctr[MAX_PEERS];      // arrival counters (monotonic over fits)
+    unsigned long long* llp[MAX_PEERS];      // {tag, fp32 bits} parameter words [NP]
+    double* part[MAX_PEERS];                 // per-CTA partial rows [G][PSTR]
+    unsigned int tag_base;                   // steps taken on this peer set before the epoch
+    unsigned long long ctr_base;             // counter value before the epoch's first step
+    int* status;                             // watchdog: 1 = a peer wait timed out
 };
 
 struct AggArgs {
@@ -72,7 +81,7 @@ template <int TB>
 __global__ void train_epoch_kernel(TrainArgs a);
 template <int TB>
 __global__ void train_partial_kernel(TrainArgs a, long step);
-template <int MT>
+template <int MT, bool SYS>
 __global__ void train_epoch_tc_kernel(TrainArgs a);
 template <int MT>
 __global__ void train_partial_tc_kernel(TrainArgs a, long step);

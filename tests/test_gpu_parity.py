@@ -272,3 +272,38 @@ def test_fit_data_parallel_step_path(orc, batch):
     np.testing.assert_allclose(el, el_ref, rtol=1e-12)
     d.comm_destroy()
     d.close()
+
+
+# ------------------------------------------- fused peer-set (multi-GPU) path
+@pytest.mark.parametrize("vranks,batch", [(2, 4096), (4, 8192), (8, 8192), (3, 1000)])
+def test_fit_peer_set_virtual_ranks(dev, orc, vranks, batch):
+    """The multi-GPU kernel path (reduce-scatter over every rank's CTAs through
+    peer-memory partials, arrival counters on every rank, LL parameter words
+    written to every rank) run with `vranks` virtual ranks inside one launch:
+    same tolerance against the reference as the 1-GPU path, deterministic."""
+    n = 50_003
+    f, t = orc.g1(19, n)
+    p0 = orc.policy_init(13)
+    rc, p_ref, el_ref, _ = orc.fit(p0, f, t, 0.02, 2, batch, 6)
+    p, el = dev.fit(p0, f, t, 0.02, 2, batch, 6, virtual_ranks=vranks)
+    assert ulps32(p, p_ref).max() <= 2
+    np.testing.assert_allclose(el, el_ref, rtol=1e-12)
+    p2, el2 = dev.fit(p0, f, t, 0.02, 2, batch, 6, virtual_ranks=vranks)
+    np.testing.assert_array_equal(p, p2)
+    np.testing.assert_array_equal(el, el2)
+
+
+def test_fit_peer_set_divergence_agrees(dev, orc):
+    f, t = orc.g1(6, 4096)
+    f[:, 8:] *= np.float32(1e3)
+    p0 = orc.policy_init(5)
+    rc, p_ref, el_ref, ep_ref = orc.fit(p0, f, t, 1e12, 4, 512, 1)
+    assert rc == 2
+    with pytest.raises(gbx.TrainingDivergedError) as ei:
+        dev.fit(p0, f, t, 1e12, 4, 512, 1, virtual_ranks=4)
+    assert ei.value.epoch == ep_ref
+    # the context stays usable (monotonic counters / tags resynchronised)
+    f2, t2 = orc.g1(7, 20_000)
+    rc, p_ref2, _, _ = orc.fit(p0, f2, t2, 0.01, 1, 2048, 3)
+    p2, _ = dev.fit(p0, f2, t2, 0.01, 1, 2048, 3, virtual_ranks=4)
+    assert ulps32(p2, p_ref2).max() <= 2
