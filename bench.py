@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=8192,
                     help="minibatch per GPU (global = N x this; 65,536 at 8 GPUs, SURVEY C3)")
     ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--dp", default="fused", choices=["fused", "nccl"],
+                    help="N>1 gradient exchange: fused = in-kernel reduce-scatter/all-gather over "
+                         "NVLink peer memory (one launch per epoch); nccl = per-step ncclAllReduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--c5-apps", type=int, default=10_000)
@@ -233,7 +236,12 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = gbx.Device(local)
-    if world > 1:
+    if world > 1 and args.dp == "fused":
+        handles = [None] * world
+        dist.all_gather_object(handles, dev.peer_export())
+        dev.peer_attach(handles, rank)
+        dist.barrier()
+    elif world > 1:
         uid = [gbx.Device.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         dev.comm_init(uid[0], world, rank)
@@ -263,7 +271,24 @@ def main():
         kernel_ms["shuffle"] += sh
         kernel_ms["train"] += tr
 
-    for _ in range(args.warmup):
+    dp_note = None
+    try:
+        step()
+        ok = torch.tensor([1], device="cuda")
+    except gbx.CudaError as e:  # the peer exchange failed on some rank
+        ok, dp_note = torch.tensor([0], device="cuda"), str(e)
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if world > 1 and args.dp == "fused" and int(ok.item()) == 0:
+        # fall back to the per-step NCCL all-reduce path (recorded in the JSON)
+        dp_note = dp_note or "a peer rank failed"
+        dev.peer_detach()
+        uid = [gbx.Device.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        dev.comm_init(uid[0], world, rank)
+        args.dp = "nccl"
+        step()
+    for _ in range(max(0, args.warmup - 1)):
         step()
     barrier()
     kernel_ms = {"shuffle": 0.0, "train": 0.0}
@@ -355,9 +380,12 @@ def main():
         "config": {"workload": "C2: 1M-tuple experience log per GPU, default MLP 44-64-32-2, "
                                "1 fit epoch per step (fp64 parity mode)",
                    "records": n_total, "global_batch": batch, "lr": args.lr,
-                   "parallelism": f"dp{world}", "l2": "inputs (196 MB/GPU) larger than L2"},
+                   "parallelism": f"dp{world}" + (f" ({args.dp} gradient exchange)" if world > 1 else ""), "l2": "inputs (196 MB/GPU) larger than L2"},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
     }
+    if dp_note:
+        line["dp_fallback"] = "fused peer exchange failed (" + dp_note + "); measured with nccl"
+
     line.update(secondary)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
