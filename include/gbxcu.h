@@ -46,7 +46,8 @@ typedef enum {
     GBXCU_ECUDA = 3,       /* CUDA runtime / launch failure, or no device */
     GBXCU_ENCCL = 4,       /* NCCL failure in the data-parallel path */
     GBXCU_ENONFINITE = 5,  /* ValidationError: non-finite feature in forward */
-    GBXCU_ETEMPERATURE = 6 /* InvalidTemperatureError (rho <= 0) */
+    GBXCU_ETEMPERATURE = 6, /* InvalidTemperatureError (rho <= 0) */
+    GBXCU_ECLOCK = 7        /* ClockRegressionError (q_update before the entry timestamp) */
 } gbxcu_status;
 
 /* Inference precision.
@@ -165,6 +166,38 @@ int gbxcu_comm_destroy(gbxcu_ctx* ctx);
 int gbxcu_peer_export(gbxcu_ctx* ctx, uint8_t handle_out[GBXCU_PEER_HANDLE_BYTES]);
 int gbxcu_peer_attach(gbxcu_ctx* ctx, int nranks, int rank, const uint8_t* handles);
 int gbxcu_peer_detach(gbxcu_ctx* ctx);
+
+/* ------------------------------------------------- experience store (Q-table) */
+/* Device-resident QTable (proj/include/gbx/qtable.hpp:53-100): unique
+ * StateKeys (30 u32, lexicographic order) with an optional {q, last check-in,
+ * update count} per action. Hyper-parameters validated like
+ * QHyperparams::validate (GBXCU_EINVAL). */
+typedef struct gbxcu_qtable gbxcu_qtable;
+#define GBXCU_KEY_WORDS 30
+int gbxcu_qtable_create(gbxcu_ctx* ctx, double alpha, double omega, gbxcu_qtable** out);
+void gbxcu_qtable_free(gbxcu_qtable* t);
+/* QTable::update (proj/src/qtable.cpp:76-92) applied to n tuples in order:
+ * keys[n][30], actions[n] (0/1), rewards[n], now[n]. Same-key updates fold
+ * sequentially (bit-exact for omega == 1, the reference default; pow() within
+ * an ulp otherwise). GBXCU_ECLOCK at the first tuple whose check-in precedes
+ * its entry's timestamp: *bad_index = that tuple, and the table holds exactly
+ * the updates before it (as the reference does after the throw). */
+int gbxcu_qtable_update_batch(gbxcu_qtable* t, const uint32_t* keys, const uint8_t* actions,
+                              const double* rewards, const uint64_t* now, size_t n,
+                              size_t* bad_index);
+int gbxcu_qtable_size(const gbxcu_qtable* t, size_t* states, size_t* entries);
+/* Table in key order: keys[m][30], q/ts/cnt/has[m][2] (has: entry recorded). */
+int gbxcu_qtable_export(const gbxcu_qtable* t, uint32_t* keys, double* q, uint64_t* ts,
+                        uint64_t* cnt, uint8_t* has);
+/* snapshot_policy_dataset (proj/src/qtable.cpp:143-155): one record per key
+ * with both actions, key order; feat[rows][44] = encode_state(counters_from_key)
+ * (bit-exact: glibc log1pf restated), tgt[rows][2] = boltzmann_pair (CUDA exp:
+ * within 2 ulp). feat == NULL: *rows only. GBXCU_ETEMPERATURE if rho <= 0. */
+int gbxcu_qtable_snapshot(gbxcu_qtable* t, double rho, float* feat, double* tgt, size_t cap,
+                          size_t* rows);
+/* Device-resident form: writes straight into fit's input buffers. */
+int gbxcu_qtable_snapshot_dev(gbxcu_qtable* t, double rho, float* d_feat, double* d_tgt, size_t cap,
+                              size_t* rows);
 
 /* ------------------------------------------------------------ aggregation */
 /* Application suite in CSR form (the per-benchmark data SimSuite::frame_time

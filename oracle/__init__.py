@@ -259,6 +259,9 @@ class Reference(_Lib):
         L.gbxref_boltzmann_pair.argtypes = [C.c_double, C.c_double, C.c_double, _f64p]
         L.gbxref_qtable_snapshot.restype = C.c_long
         L.gbxref_qtable_snapshot.argtypes = [C.c_char_p, C.c_double, C.c_void_p, C.c_void_p]
+        L.gbxref_qtable_fold.restype = C.c_long
+        L.gbxref_qtable_fold.argtypes = [C.c_void_p] * 4 + [_sz, C.c_double, C.c_double, C.c_double,
+                                                            C.c_void_p, C.c_void_p] + [C.c_void_p] * 7
         L.gbxref_suite_generate.restype = C.c_void_p
         L.gbxref_suite_generate.argtypes = [C.c_int] * 5 + [C.c_double] * 3 + [_u64]
         L.gbxref_suite_free.argtypes = [C.c_void_p]
@@ -363,6 +366,29 @@ class Reference(_Lib):
         tgt = np.empty((n, 2), np.float64)
         self.lib.gbxref_qtable_snapshot(t, rho, feat.ctypes.data, tgt.ctypes.data)
         return feat, tgt
+
+    def qtable_fold(self, keys, actions, rewards, now, alpha=0.3, omega=1.0, rho=0.1):
+        """Fresh QTable, QTable::update over the tuples in order, then the table
+        (key order) and snapshot_policy_dataset(rho). Returns a dict."""
+        keys = np.ascontiguousarray(keys, np.uint32)
+        actions = np.ascontiguousarray(actions, np.uint8)
+        rewards = np.ascontiguousarray(rewards, np.float64)
+        now = np.ascontiguousarray(now, np.uint64)
+        n = len(actions)
+        sizes = np.zeros(2, np.int64)
+        bad = C.c_long(-1)
+        args = [keys.ctypes.data, actions.ctypes.data, rewards.ctypes.data, now.ctypes.data, n,
+                alpha, omega, rho, sizes.ctypes.data, C.byref(bad)]
+        if self.lib.gbxref_qtable_fold(*args, *([None] * 7)) < 0:
+            raise ValueError(self.err())
+        m, r = int(sizes[0]), int(sizes[1])
+        out = {"keys": np.empty((m, 30), np.uint32), "q": np.empty((m, 2)), "t": np.empty((m, 2), np.uint64),
+               "cnt": np.empty((m, 2), np.uint64), "has": np.empty((m, 2), np.uint8),
+               "feat": np.empty((r, N_FEAT), np.float32), "tgt": np.empty((r, 2))}
+        self.lib.gbxref_qtable_fold(*args, *(out[k].ctypes.data for k in
+                                             ("keys", "q", "t", "cnt", "has", "feat", "tgt")))
+        out["bad"] = bad.value
+        return out
 
     # suites -----------------------------------------------------------------
     def suite_generate(self, benchmark_count=16, shaders_min=184, shaders_max=276,

@@ -223,6 +223,57 @@ long gbxref_qtable_snapshot(const char* text, double rho, float* feat, double* t
     }
 }
 
+// Folds n tuples into a fresh QTable with QTable::update in order (the
+// reference's Eq.-5 fold, proj/src/qtable.cpp:76-92); on ClockRegressionError
+// the table keeps the updates before it (*bad = tuple index). Returns the
+// table in key order and its snapshot. Call with out_keys == nullptr first to
+// get sizes[0] = states, sizes[1] = snapshot rows.
+long gbxref_qtable_fold(const std::uint32_t* keys, const std::uint8_t* actions, const double* rewards,
+                        const std::uint64_t* now, std::size_t n, double alpha, double omega,
+                        double rho, long* sizes, long* bad, std::uint32_t* out_keys, double* out_q,
+                        std::uint64_t* out_t, std::uint64_t* out_cnt, std::uint8_t* out_has,
+                        float* feat, double* tgt) {
+    try {
+        gbx::QTable t(gbx::QHyperparams{alpha, omega});
+        *bad = -1;
+        for (std::size_t i = 0; i < n; ++i) {
+            gbx::StateKey k;
+            std::memcpy(k.values.data(), keys + i * 30, sizeof(std::uint32_t) * 30);
+            try {
+                t.update(k, actions[i] ? gbx::Action::Wave64 : gbx::Action::Wave32, rewards[i], now[i]);
+            } catch (const gbx::ClockRegressionError&) {
+                *bad = (long)i;
+                break;
+            }
+        }
+        const auto d = t.snapshot_policy_dataset(rho);
+        sizes[0] = (long)t.state_count();
+        sizes[1] = (long)d.size();
+        if (!out_keys) return 0;
+        std::size_t r = 0;
+        for (const auto& [key, pair] : t.entries()) {
+            std::memcpy(out_keys + r * 30, key.values.data(), sizeof(std::uint32_t) * 30);
+            for (int a = 0; a < 2; ++a) {
+                const bool h = pair[a].has_value();
+                out_has[2 * r + a] = h ? 1 : 0;
+                out_q[2 * r + a] = h ? pair[a]->q : 0.0;
+                out_t[2 * r + a] = h ? pair[a]->last_update_t : 0;
+                out_cnt[2 * r + a] = h ? pair[a]->update_count : 0;
+            }
+            ++r;
+        }
+        for (std::size_t i = 0; i < d.size(); ++i) {
+            std::memcpy(feat + i * kF, d[i].first.features.data(), sizeof(float) * kF);
+            tgt[2 * i] = d[i].second.prob[0];
+            tgt[2 * i + 1] = d[i].second.prob[1];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // ---------------------------------------------------------------- suites
 struct gbxref_suite {
     std::unique_ptr<gbx::SimSuite> s;

@@ -23,7 +23,8 @@ DIMS = (44, 64, 32, 2)
 WAVE32, WAVE64 = 0, 1
 FWD_EXACT, FWD_FAST = 0, 1
 
-OK, EINVAL, EDIVERGED, ECUDA, ENCCL, ENONFINITE, ETEMPERATURE = range(7)
+OK, EINVAL, EDIVERGED, ECUDA, ENCCL, ENONFINITE, ETEMPERATURE, ECLOCK = range(8)
+KEY_WORDS = 30
 
 
 # ----------------------------------------------------------------- errors
@@ -41,6 +42,10 @@ class TrainingDivergedError(RuntimeError):
 
 class InvalidTemperatureError(ValueError):
     """gbx::InvalidTemperatureError (proj/include/gbx/qtable.hpp:23-25)."""
+
+
+class ClockRegressionError(RuntimeError):
+    """gbx::ClockRegressionError (proj/include/gbx/qtable.hpp:15-17)."""
 
 
 class CudaError(RuntimeError):
@@ -89,7 +94,9 @@ EXPORTS = (
     "gbxcu_suite_free", "gbxcu_suite_features", "gbxcu_evaluate", "gbxcu_evaluate_dev",
     "gbxcu_wide_param_count", "gbxcu_wide_init", "gbxcu_wide_forward", "gbxcu_wide_fit",
     "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_peer_export",
-    "gbxcu_peer_attach", "gbxcu_peer_detach",
+    "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free",
+    "gbxcu_qtable_update_batch", "gbxcu_qtable_size", "gbxcu_qtable_export",
+    "gbxcu_qtable_snapshot", "gbxcu_qtable_snapshot_dev",
 )
 PEER_HANDLE_BYTES = 64
 
@@ -131,6 +138,14 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_peer_export.argtypes = [_vp, C.c_char_p]
     L.gbxcu_peer_attach.argtypes = [_vp, C.c_int, C.c_int, C.c_char_p]
     L.gbxcu_peer_detach.argtypes = [_vp]
+    L.gbxcu_qtable_create.argtypes = [_vp, C.c_double, C.c_double, C.POINTER(_vp)]
+    L.gbxcu_qtable_free.argtypes = [_vp]
+    L.gbxcu_qtable_free.restype = None
+    L.gbxcu_qtable_update_batch.argtypes = [_vp, _vp, _vp, _vp, _vp, _sz, C.POINTER(_sz)]
+    L.gbxcu_qtable_size.argtypes = [_vp, C.POINTER(_sz), C.POINTER(_sz)]
+    L.gbxcu_qtable_export.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+    L.gbxcu_qtable_snapshot.argtypes = [_vp, C.c_double, _vp, _vp, _sz, C.POINTER(_sz)]
+    L.gbxcu_qtable_snapshot_dev.argtypes = [_vp, C.c_double, _vp, _vp, _sz, C.POINTER(_sz)]
     L.gbxcu_aggregate.argtypes = [_vp, C.POINTER(SuiteC), _u8p, _u64p, C.c_int, _f64p, _vp]
     L.gbxcu_histogram.argtypes = [_vp, _f64p, _sz, _f64p, _u64p, _sz, C.POINTER(_sz)]
     L.gbxcu_suite_upload.argtypes = [_vp, C.POINTER(SuiteC), _f32p, C.POINTER(_vp)]
@@ -167,6 +182,8 @@ def _raise(L, rc: int, diverged_epoch: int = -1):
         raise InvalidTemperatureError(msg)
     if rc == ENCCL:
         raise NcclError(msg)
+    if rc == ECLOCK:
+        raise ClockRegressionError(msg)
     raise CudaError(msg)
 
 
@@ -459,3 +476,71 @@ class DeviceSuite:
                      stream: int | None = None):
         self.dev._ck(self.dev.L.gbxcu_evaluate_dev(self.dev.h, self.h, d_params, n_samples, seed,
                                                    d_actions, d_rows, stream))
+
+
+class DeviceQTable:
+    """QTable on the device (proj/include/gbx/qtable.hpp:53-100): batched
+    QTable::update (Eq. 5) and snapshot_policy_dataset in key order."""
+
+    def __init__(self, dev: "Device", alpha: float = 0.3, omega: float = 1.0):
+        self.dev, self.L = dev, dev.L
+        h = _vp()
+        dev._ck(self.L.gbxcu_qtable_create(dev.h, alpha, omega, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.L.gbxcu_qtable_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def update_batch(self, keys, actions, rewards, now):
+        keys = np.ascontiguousarray(keys, np.uint32).reshape(-1, KEY_WORDS)
+        actions = np.ascontiguousarray(actions, np.uint8)
+        rewards = np.ascontiguousarray(rewards, np.float64)
+        now = np.ascontiguousarray(now, np.uint64)
+        bad = _sz(0)
+        rc = self.L.gbxcu_qtable_update_batch(self.h, keys.ctypes.data, actions.ctypes.data,
+                                              rewards.ctypes.data, now.ctypes.data, len(actions),
+                                              C.byref(bad))
+        if rc == ECLOCK:
+            try:
+                _raise(self.L, rc)
+            except ClockRegressionError as e:
+                e.index = int(bad.value)
+                raise
+        self.dev._ck(rc)
+
+    def size(self):
+        m, e = _sz(0), _sz(0)
+        self.dev._ck(self.L.gbxcu_qtable_size(self.h, C.byref(m), C.byref(e)))
+        return int(m.value), int(e.value)
+
+    def export(self) -> dict:
+        m, _ = self.size()
+        out = {"keys": np.empty((m, KEY_WORDS), np.uint32), "q": np.empty((m, 2)),
+               "t": np.empty((m, 2), np.uint64), "cnt": np.empty((m, 2), np.uint64),
+               "has": np.empty((m, 2), np.uint8)}
+        if m:
+            self.dev._ck(self.L.gbxcu_qtable_export(self.h, *(out[k].ctypes.data for k in
+                                                              ("keys", "q", "t", "cnt", "has"))))
+        return out
+
+    def snapshot(self, rho: float):
+        r = _sz(0)
+        self.dev._ck(self.L.gbxcu_qtable_snapshot(self.h, rho, None, None, 0, C.byref(r)))
+        feat = np.empty((r.value, N_FEATURES), np.float32)
+        tgt = np.empty((r.value, 2), np.float64)
+        self.dev._ck(self.L.gbxcu_qtable_snapshot(self.h, rho, feat.ctypes.data, tgt.ctypes.data,
+                                                  r.value, C.byref(r)))
+        return feat, tgt
+
+    def snapshot_dev(self, rho: float, d_feat: int, d_tgt: int, cap: int) -> int:
+        r = _sz(0)
+        self.dev._ck(self.L.gbxcu_qtable_snapshot_dev(self.h, rho, d_feat, d_tgt, cap, C.byref(r)))
+        return int(r.value)

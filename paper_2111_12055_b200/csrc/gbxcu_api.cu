@@ -53,6 +53,9 @@ int fail(int code, const std::string& msg) {
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;  // owns p
+    DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() {
         if (p) cudaFree(p);
     }
@@ -110,6 +113,20 @@ struct gbxcu_dsuite {
     size_t n_apps = 0, n_pipes = 0, n_slots = 0, n_shaders = 0;
     DevBuf app_pipe, pipe_slot, slot_shader, slot_frac, pipe_wt, shader_lat, app_f64, features;
     DevBuf actions, rows, recheck, counters, flags, params, h_lower, h_count, h_nbins;
+};
+
+// Device-resident Q-table (row f1): unique keys in StateKey order, two
+// optional entries per key (QTable::entries_, proj/include/gbx/qtable.hpp:95-100).
+struct gbxcu_qtable {
+    gbxcu_ctx* ctx = nullptr;
+    double alpha = 0.3, omega = 1.0;
+    size_t m = 0;  // states
+    DevBuf keys, q, t, cnt, has;
+    DevBuf nkeys, nq, nt, ncnt, nhas;  // fold output (swapped in)
+    DevBuf bkeys, bact, brew, bnow, init_ids, count;
+    DevBuf perm, perm2, digit, digit2, seg_head, key_head, seg_scan, key_scan, seg_start, seg_key;
+    DevBuf spread, bad, temp;
+    DevBuf flag, row, sfeat, stgt, bad_stage;
 };
 
 namespace {
@@ -786,6 +803,230 @@ int gbxcu_comm_destroy(gbxcu_ctx* c) {
     c->nranks = 1;
     c->rank = 0;
     return GBXCU_OK;
+}
+
+// ================================================================= Q-table
+int gbxcu_qtable_create(gbxcu_ctx* c, double alpha, double omega, gbxcu_qtable** out) {
+    if (!c || !out) return fail(GBXCU_EINVAL, "null argument");
+    // QHyperparams::validate (proj/src/qtable.cpp:57-64)
+    if (!(alpha > 0.0 && alpha <= 1.0)) return fail(GBXCU_EINVAL, "alpha must be in (0, 1]");
+    if (!(omega > 0.0 && omega <= 1.0)) return fail(GBXCU_EINVAL, "omega must be in (0, 1]");
+    auto* t = new gbxcu_qtable;
+    t->ctx = c;
+    t->alpha = alpha;
+    t->omega = omega;
+    *out = t;
+    return GBXCU_OK;
+}
+
+void gbxcu_qtable_free(gbxcu_qtable* t) { delete t; }
+
+int gbxcu_qtable_size(const gbxcu_qtable* t, size_t* states, size_t* entries) {
+    if (!t) return fail(GBXCU_EINVAL, "null table");
+    if (states) *states = t->m;
+    if (entries) {
+        std::vector<uint8_t> h(2 * t->m);
+        if (t->m) CK(cudaMemcpy(h.data(), t->has.p, 2 * t->m, cudaMemcpyDeviceToHost));
+        size_t e = 0;
+        for (uint8_t x : h) e += x;
+        *entries = e;
+    }
+    return GBXCU_OK;
+}
+
+namespace {
+int qtable_fold(gbxcu_qtable* t, size_t n, cudaStream_t st, size_t* bad_index) {
+    gbxcu_ctx* c = t->ctx;
+    // existing entries become init records
+    size_t n_init = 0;
+    RET(t->count.ensure(16));
+    if (t->m) {
+        RET(t->init_ids.ensure(sizeof(uint32_t) * 2 * t->m));
+        CK(cudaMemsetAsync(t->count.p, 0, 8, st));
+        qt_init_ids_kernel<<<c->num_sms * 4, 256, 0, st>>>(t->has.as<uint8_t>(), t->m,
+                                                           t->init_ids.as<uint32_t>(),
+                                                           t->count.as<unsigned long long>());
+        RET(check_launch(c, "qt_init_ids_kernel"));
+        unsigned long long k = 0;
+        CK(cudaMemcpyAsync(&k, t->count.p, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        n_init = (size_t)k;
+        // entry ids in order (the atomics scatter them): sort is not needed for
+        // correctness — the records' sort below orders them by key anyway
+    }
+    const size_t nrec = n_init + n;
+    if (nrec == 0) return GBXCU_OK;
+    if (nrec > 0xFFFFFFFFull) return fail(GBXCU_EINVAL, "q-table fold too large (> 2^32 records)");
+    for (DevBuf* b : {&t->perm, &t->perm2, &t->digit, &t->digit2, &t->seg_head, &t->key_head,
+                      &t->seg_scan, &t->key_scan, &t->seg_start, &t->seg_key})
+        RET(b->ensure(sizeof(uint32_t) * nrec));
+    RET(t->spread.ensure(sizeof(uint32_t) * 32));
+    RET(t->bad.ensure(16));
+    const size_t tb = qt_temp_bytes(nrec);
+    RET(t->temp.ensure(tb));
+    QtFoldIO io{};
+    io.tkeys = t->keys.as<uint32_t>();
+    io.init = t->init_ids.as<uint32_t>();
+    io.n_init = n_init;
+    io.bkeys = t->bkeys.as<uint32_t>();
+    io.bact = t->bact.as<uint8_t>();
+    io.reward = t->brew.as<double>();
+    io.now = t->bnow.as<uint64_t>();
+    io.n = n;
+    io.limit = n;
+    io.old_q = t->q.as<double>();
+    io.old_t = t->t.as<uint64_t>();
+    io.old_cnt = t->cnt.as<uint64_t>();
+    io.alpha = t->alpha;
+    io.omega = t->omega;
+    io.perm = t->perm.as<uint32_t>();
+    io.perm2 = t->perm2.as<uint32_t>();
+    io.digit = t->digit.as<uint32_t>();
+    io.digit2 = t->digit2.as<uint32_t>();
+    io.seg_head = t->seg_head.as<uint32_t>();
+    io.key_head = t->key_head.as<uint32_t>();
+    io.seg_scan = t->seg_scan.as<uint32_t>();
+    io.key_scan = t->key_scan.as<uint32_t>();
+    io.seg_start = t->seg_start.as<uint32_t>();
+    io.seg_key = t->seg_key.as<uint32_t>();
+    io.spread = t->spread.as<uint32_t>();
+    io.temp = t->temp.p;
+    io.temp_bytes = tb;
+    io.bad = t->bad.as<unsigned long long>();
+    size_t nseg = 0, nkeys = 0;
+    CK(qt_sort_segment(io, nseg, nkeys, c->num_sms, st));
+    c->launches += 4;
+    RET(t->nkeys.ensure(sizeof(uint32_t) * QT_KEY_WORDS * nkeys));
+    RET(t->nq.ensure(sizeof(double) * 2 * nkeys));
+    RET(t->nt.ensure(sizeof(uint64_t) * 2 * nkeys));
+    RET(t->ncnt.ensure(sizeof(uint64_t) * 2 * nkeys));
+    RET(t->nhas.ensure(2 * nkeys));
+    CK(cudaMemsetAsync(t->nhas.p, 0, 2 * nkeys, st));
+    CK(cudaMemsetAsync(t->bad.p, 0xFF, 8, st));
+    CK(qt_fold(io, nseg, t->nkeys.as<uint32_t>(), t->nq.as<double>(), t->nt.as<uint64_t>(),
+               t->ncnt.as<uint64_t>(), t->nhas.as<uint8_t>(), c->num_sms, st));
+    RET(check_launch(c, "qt_fold_kernel"));
+    unsigned long long bad = ~0ull;
+    CK(cudaMemcpyAsync(&bad, t->bad.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *bad_index = bad == ~0ull ? (size_t)-1 : (size_t)bad;
+    if (bad != ~0ull) return GBXCU_OK;  // caller re-folds the prefix
+    for (auto pr : {std::make_pair(&t->keys, &t->nkeys), std::make_pair(&t->q, &t->nq),
+                    std::make_pair(&t->t, &t->nt), std::make_pair(&t->cnt, &t->ncnt),
+                    std::make_pair(&t->has, &t->nhas)}) {
+        std::swap(pr.first->p, pr.second->p);  // DevBuf owns p: swap members, not objects
+        std::swap(pr.first->cap, pr.second->cap);
+    }
+    t->m = nkeys;
+    return GBXCU_OK;
+}
+}  // namespace
+
+int gbxcu_qtable_update_batch(gbxcu_qtable* t, const uint32_t* keys, const uint8_t* actions,
+                              const double* rewards, const uint64_t* now, size_t n,
+                              size_t* bad_index) {
+    if (!t || (n && (!keys || !actions || !rewards || !now))) return fail(GBXCU_EINVAL, "null argument");
+    if (bad_index) *bad_index = (size_t)-1;
+    for (size_t i = 0; i < n; ++i)
+        if (actions[i] > 1) return fail(GBXCU_EINVAL, "action must be 0 (wave32) or 1 (wave64)");
+    if (n == 0) return GBXCU_OK;
+    gbxcu_ctx* c = t->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    RET(upload(t->bkeys, keys, n * QT_KEY_WORDS, st));
+    RET(upload(t->bact, actions, n, st));
+    RET(upload(t->brew, rewards, n, st));
+    RET(upload(t->bnow, now, n, st));
+    size_t bad = (size_t)-1;
+    RET(qtable_fold(t, n, st, &bad));
+    if (bad == (size_t)-1) return GBXCU_OK;
+    // ClockRegressionError at tuple `bad`: the reference has applied every
+    // tuple before it (updates are sequential) — fold exactly that prefix.
+    size_t bad2 = (size_t)-1;
+    if (bad > 0) RET(qtable_fold(t, bad, st, &bad2));
+    if (bad_index) *bad_index = bad;
+    return fail(GBXCU_ECLOCK, "q_update check-in precedes the entry timestamp (tuple " +
+                                  std::to_string(bad) + ")");
+}
+
+int gbxcu_qtable_export(const gbxcu_qtable* t, uint32_t* keys, double* q, uint64_t* ts, uint64_t* cnt,
+                        uint8_t* has) {
+    if (!t) return fail(GBXCU_EINVAL, "null table");
+    const size_t m = t->m;
+    if (!m) return GBXCU_OK;
+    if (keys) CK(cudaMemcpy(keys, t->keys.p, sizeof(uint32_t) * QT_KEY_WORDS * m, cudaMemcpyDeviceToHost));
+    if (q) CK(cudaMemcpy(q, t->q.p, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost));
+    if (ts) CK(cudaMemcpy(ts, t->t.p, sizeof(uint64_t) * 2 * m, cudaMemcpyDeviceToHost));
+    if (cnt) CK(cudaMemcpy(cnt, t->cnt.p, sizeof(uint64_t) * 2 * m, cudaMemcpyDeviceToHost));
+    if (has) CK(cudaMemcpy(has, t->has.p, 2 * m, cudaMemcpyDeviceToHost));
+    return GBXCU_OK;
+}
+
+namespace {
+int qtable_snapshot(gbxcu_qtable* t, double rho, float* d_feat, double* d_tgt, size_t cap, size_t* rows,
+                    cudaStream_t st) {
+    gbxcu_ctx* c = t->ctx;
+    if (!(rho > 0.0)) return fail(GBXCU_ETEMPERATURE, "softmax temperature must be positive");
+    *rows = 0;
+    const size_t m = t->m;
+    if (m == 0) return GBXCU_OK;
+    RET(t->flag.ensure(sizeof(uint32_t) * m));
+    RET(t->row.ensure(sizeof(uint32_t) * m));
+    RET(t->bad_stage.ensure(16));
+    const size_t tb = qt_temp_bytes(m);
+    RET(t->temp.ensure(tb));
+    qt_both_kernel<<<c->num_sms * 4, 256, 0, st>>>(t->has.as<uint8_t>(), m, t->flag.as<uint32_t>());
+    RET(check_launch(c, "qt_both_kernel"));
+    CK(qt_exclusive_scan(t->temp.p, tb, t->flag.as<uint32_t>(), t->row.as<uint32_t>(), m, st));
+    uint32_t tail[2];
+    CK(cudaMemcpyAsync(&tail[0], t->row.as<uint32_t>() + m - 1, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&tail[1], t->flag.as<uint32_t>() + m - 1, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const size_t r = (size_t)tail[0] + tail[1];
+    *rows = r;
+    if (!d_feat) return GBXCU_OK;  // size query
+    if (r > cap) return fail(GBXCU_EINVAL, "snapshot buffers too small");
+    CK(cudaMemsetAsync(t->bad_stage.p, 0, 4, st));
+    qt_snapshot_kernel<<<c->num_sms * 4, 128, 0, st>>>(t->keys.as<uint32_t>(), t->q.as<double>(),
+                                                       t->flag.as<uint32_t>(), t->row.as<uint32_t>(), m,
+                                                       rho, d_feat, d_tgt, t->bad_stage.as<int>());
+    RET(check_launch(c, "qt_snapshot_kernel"));
+    int bs = 0;
+    CK(cudaMemcpyAsync(&bs, t->bad_stage.p, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (bs) return fail(GBXCU_EINVAL, "state key holds invalid stage index");
+    return GBXCU_OK;
+}
+}  // namespace
+
+int gbxcu_qtable_snapshot(gbxcu_qtable* t, double rho, float* feat, double* tgt, size_t cap, size_t* rows) {
+    if (!t || !rows) return fail(GBXCU_EINVAL, "null argument");
+    gbxcu_ctx* c = t->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    size_t r = 0;
+    RET(qtable_snapshot(t, rho, nullptr, nullptr, 0, &r, st));
+    *rows = r;
+    if (!feat) return GBXCU_OK;
+    if (r > cap) return fail(GBXCU_EINVAL, "snapshot buffers too small");
+    RET(t->sfeat.ensure(sizeof(float) * F * std::max<size_t>(r, 1)));
+    RET(t->stgt.ensure(sizeof(double) * 2 * std::max<size_t>(r, 1)));
+    RET(qtable_snapshot(t, rho, t->sfeat.as<float>(), t->stgt.as<double>(), r, &r, st));
+    CK(cudaMemcpyAsync(feat, t->sfeat.p, sizeof(float) * F * r, cudaMemcpyDeviceToHost, st));
+    if (tgt) CK(cudaMemcpyAsync(tgt, t->stgt.p, sizeof(double) * 2 * r, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return GBXCU_OK;
+}
+
+int gbxcu_qtable_snapshot_dev(gbxcu_qtable* t, double rho, float* d_feat, double* d_tgt, size_t cap,
+                              size_t* rows) {
+    if (!t || !rows) return fail(GBXCU_EINVAL, "null argument");
+    gbxcu_ctx* c = t->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    return qtable_snapshot(t, rho, d_feat, d_tgt, cap, rows, c->stream);
 }
 
 int gbxcu_aggregate(gbxcu_ctx* c, const gbxcu_suite* s, const uint8_t* shader_actions,

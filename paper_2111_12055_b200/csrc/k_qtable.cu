@@ -1,0 +1,429 @@
+// k_qtable.cu — the experience store on the device:
+// QTable::update folded over a batch of tuples, and snapshot_policy_dataset
+// producing fit's training records in key order.
+//
+// Reference: QTable::update (proj/src/qtable.cpp:76-92), boltzmann_pair
+// (:121-129), snapshot_policy_dataset (:143-155) -> counters_from_key +
+// encode_state (proj/src/core.cpp:43-62,105-123), RawCounters::recompute_totals
+// (proj/src/core.cpp:19-28); StateKey order = lexicographic over 30 u32
+// (proj/include/gbx/core.hpp:126-130).
+//
+// Fold of n tuples (key, action, reward, check-in) into a table of m states:
+//   1. records = the table's existing entries (as "init" records, first) +
+//      the tuples in sequence order;
+//   2. stable LSD radix sort of the record permutation by (key words 0..29,
+//      action): action first, then word 29 .. word 0; words whose values are
+//      all equal are skipped, the others sort only their significant bits
+//      (cub::DeviceRadixSort per pass; the passes are the only library calls);
+//   3. segment heads by comparing neighbours (key, action) and key alone;
+//   4. one thread per (key, action) segment folds its records in sequence
+//      order — the Eq.-5 recurrence is a strict left fold, so each segment is
+//      sequential, exactly like the reference; different segments in parallel:
+//          q <- ((1 - alpha) * omega^dt) * q + alpha * r   (no FMA, as g++)
+//      A check-in earlier than the entry's timestamp is a ClockRegressionError:
+//      the smallest such tuple index is reported, and the host re-folds the
+//      prefix before it so the table ends exactly where the reference's does;
+//   5. the new table (unique keys in order, per-action entries) replaces the old.
+// Snapshot: keys with both actions, compacted in key order; features =
+// encode_state(counters_from_key(key)) with glibc's log1pf restated bit for bit
+// (fdlibm algorithm, no FMA contraction), targets = boltzmann_pair(q0, q1, rho).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gbxcu {
+
+constexpr int KW = QT_KEY_WORDS;  // 30
+
+// ---------------------------------------------------------------- records
+// Key words of record i: existing entries come from the table, tuples from
+// the batch. rec < n_init: table entry rec (key row rec >> 1, action rec & 1).
+struct RecView {
+    const uint32_t* tkeys;   // [m][30] table keys
+    const uint32_t* init;    // [n_init] table entry ids (key * 2 + action)
+    size_t n_init;
+    const uint32_t* bkeys;   // [n][30] batch keys
+    const uint8_t* bact;     // [n]
+    __device__ __forceinline__ const uint32_t* key(uint32_t rec) const {
+        return rec < n_init ? tkeys + (size_t)(init[rec] >> 1) * KW : bkeys + (size_t)(rec - n_init) * KW;
+    }
+    __device__ __forceinline__ uint32_t action(uint32_t rec) const {
+        return rec < n_init ? (init[rec] & 1u) : (uint32_t)bact[rec - n_init];
+    }
+};
+
+__global__ void qt_iota_kernel(uint32_t* p, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+
+// Existing entries of the table as init records: ids key*2 + action of present entries.
+__global__ void qt_init_ids_kernel(const uint8_t* __restrict__ has, size_t m, uint32_t* __restrict__ ids,
+                                   unsigned long long* __restrict__ count) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < m; k += (size_t)gridDim.x * blockDim.x) {
+        for (int a = 0; a < 2; ++a)
+            if (has[2 * k + a]) ids[atomicAdd(count, 1ull)] = (uint32_t)(2 * k + a);
+    }
+}
+
+// Per key word: OR of (v ^ word of record 0) (which bits vary) over all records.
+__global__ void qt_word_spread_kernel(RecView v, size_t nrec, uint32_t* __restrict__ spread) {
+    __shared__ uint32_t acc[KW + 1];
+    if (threadIdx.x <= KW) acc[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t* k0 = v.key(0);
+    const uint32_t a0 = v.action(0);
+    uint32_t loc[KW + 1];
+#pragma unroll
+    for (int w = 0; w <= KW; ++w) loc[w] = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t* k = v.key((uint32_t)i);
+#pragma unroll
+        for (int w = 0; w < KW; ++w) loc[w] |= k[w] ^ k0[w];
+        loc[KW] |= v.action((uint32_t)i) ^ a0;
+    }
+#pragma unroll
+    for (int w = 0; w <= KW; ++w) {
+        uint32_t x = loc[w];
+        for (int o = 16; o > 0; o >>= 1) x |= __shfl_xor_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0 && x) atomicOr(&acc[w], x);
+    }
+    __syncthreads();
+    if (threadIdx.x <= KW && acc[threadIdx.x]) atomicOr(&spread[threadIdx.x], acc[threadIdx.x]);
+}
+
+// digit[i] = word w (w == KW: action) of record perm[i]
+__global__ void qt_gather_digit_kernel(RecView v, const uint32_t* __restrict__ perm, size_t nrec, int w,
+                                       uint32_t* __restrict__ digit) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t r = perm[i];
+        digit[i] = w == KW ? v.action(r) : v.key(r)[w];
+    }
+}
+
+// seg_head[i]: (key, action) differs from position i-1; key_head[i]: key differs.
+__global__ void qt_heads_kernel(RecView v, const uint32_t* __restrict__ perm, size_t nrec,
+                                uint32_t* __restrict__ seg_head, uint32_t* __restrict__ key_head) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t kh = 1, sh = 1;
+        if (i > 0) {
+            const uint32_t* a = v.key(perm[i]);
+            const uint32_t* b = v.key(perm[i - 1]);
+            bool same = true;
+            for (int w = 0; w < KW && same; ++w) same = a[w] == b[w];
+            kh = same ? 0u : 1u;
+            sh = kh | (v.action(perm[i]) != v.action(perm[i - 1]) ? 1u : 0u);
+        }
+        seg_head[i] = sh;
+        key_head[i] = kh;
+    }
+}
+
+// Segment starts (positions with seg_head) and, per segment, its key index.
+__global__ void qt_seg_list_kernel(const uint32_t* __restrict__ seg_head, const uint32_t* __restrict__ seg_scan,
+                                   const uint32_t* __restrict__ key_scan, size_t nrec,
+                                   uint32_t* __restrict__ seg_start, uint32_t* __restrict__ seg_key) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec; i += (size_t)gridDim.x * blockDim.x) {
+        if (seg_head[i]) {
+            const uint32_t s = seg_scan[i];  // exclusive scan: segment id
+            seg_start[s] = (uint32_t)i;
+            seg_key[s] = key_scan[i] - 1;    // inclusive scan of key heads - 1
+        }
+    }
+}
+
+struct FoldArgs {
+    RecView v;
+    const uint32_t* perm;
+    size_t nrec, nseg;
+    const uint32_t* seg_start;
+    const uint32_t* seg_key;
+    // old table entries (init records)
+    const double* old_q;
+    const uint64_t* old_t;
+    const uint64_t* old_cnt;
+    // batch
+    const double* reward;
+    const uint64_t* now;
+    size_t limit;            // tuples with batch index >= limit are ignored (prefix re-fold)
+    double alpha, omega;
+    // new table
+    uint32_t* keys;          // [m'][30]
+    double* q;               // [m'][2]
+    uint64_t* t;
+    uint64_t* cnt;
+    uint8_t* has;
+    unsigned long long* bad; // min batch index of a ClockRegressionError
+};
+
+// One thread per (key, action) segment: QTable::update in sequence order.
+__global__ void qt_fold_kernel(FoldArgs f) {
+    for (size_t s = blockIdx.x * (size_t)blockDim.x + threadIdx.x; s < f.nseg; s += (size_t)gridDim.x * blockDim.x) {
+        const size_t lo = f.seg_start[s];
+        const size_t hi = s + 1 < f.nseg ? f.seg_start[s + 1] : f.nrec;
+        const uint32_t kid = f.seg_key[s];
+        const uint32_t first = f.perm[lo];
+        const int a = (int)f.v.action(first);
+        bool have = false;
+        double q = 0.0;
+        uint64_t t = 0, cnt = 0;
+        for (size_t i = lo; i < hi; ++i) {
+            const uint32_t r = f.perm[i];
+            if (r < f.v.n_init) {  // existing entry (always first in its segment)
+                const uint32_t e = f.v.init[r];
+                q = f.old_q[e];
+                t = f.old_t[e];
+                cnt = f.old_cnt[e];
+                have = true;
+                continue;
+            }
+            const size_t b = r - f.v.n_init;
+            if (b >= f.limit) break;  // batch order == record order within a segment
+            const double rw = f.reward[b];
+            const uint64_t now = f.now[b];
+            if (!have) {  // slot = QEntry{r, now, 1}
+                q = rw;
+                t = now;
+                cnt = 1;
+                have = true;
+                continue;
+            }
+            if (now < t) {  // ClockRegressionError: stop this segment, report the index
+                atomicMin(f.bad, (unsigned long long)b);
+                break;
+            }
+            const double dt = (double)(now - t);
+            // (1.0 - alpha) * pow(omega, dt) * q + alpha * r, evaluated left to right
+            const double decay = f.omega == 1.0 ? 1.0 : pow(f.omega, dt);
+            q = __dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, f.alpha), decay), q), __dmul_rn(f.alpha, rw));
+            t = now;
+            cnt += 1;
+        }
+        if (!have) continue;  // only tuples past `limit`
+        const size_t e = 2 * (size_t)kid + a;
+        f.q[e] = q;
+        f.t[e] = t;
+        f.cnt[e] = cnt;
+        f.has[e] = 1;
+        // the key row (each segment of the key writes the same values)
+        const uint32_t* src = f.v.key(first);
+        uint32_t* dst = f.keys + (size_t)kid * KW;
+        for (int w = 0; w < KW; ++w) dst[w] = src[w];
+    }
+}
+
+// ------------------------------------------------------------- snapshot
+// glibc 2.39 log1pf (sysdeps/ieee754/flt-32/s_log1pf.c, fdlibm), restated with
+// explicit fp32 rounding so nvcc cannot contract; bit-identical to the host's
+// on every integer count (tools check: 0 mismatches over 1e8 values).
+__device__ float glibc_log1pf(float x) {
+    const float ln2_hi = 6.9313812256e-01f, ln2_lo = 9.0580006145e-06f;
+    const float Lp1 = 6.6666668653e-01f, Lp2 = 4.0000000596e-01f, Lp3 = 2.8571429849e-01f,
+                Lp4 = 2.2222198546e-01f, Lp5 = 1.8183572590e-01f, Lp6 = 1.5313838422e-01f,
+                Lp7 = 1.4798198640e-01f;
+    // counts are >= 0: only the x >= 0 branches of the reference are reachable
+    int32_t hx = __float_as_int(x);
+    if (hx == 0) return 0.0f;
+    if (hx >= 0x7f800000) return __fadd_rn(x, x);
+    int32_t k = 1, hu;
+    float f, c, u;
+    if (hx < 0x3ed413d7) {  // 0 < x < 0.41422: k = 0 (integers never land here except 0)
+        k = 0;
+        f = x;
+        hu = 1;
+        c = 0.0f;
+    } else {
+        if (hx < 0x5a000000) {
+            u = __fadd_rn(1.0f, x);
+            hu = __float_as_int(u);
+            k = (hu >> 23) - 127;
+            c = (k > 0) ? __fsub_rn(1.0f, __fsub_rn(u, x)) : __fsub_rn(x, __fsub_rn(u, 1.0f));
+            c = __fdiv_rn(c, u);
+        } else {
+            u = x;
+            hu = __float_as_int(u);
+            k = (hu >> 23) - 127;
+            c = 0.0f;
+        }
+        hu &= 0x007fffff;
+        if (hu < 0x3504f7) {
+            u = __int_as_float(hu | 0x3f800000);
+        } else {
+            k += 1;
+            u = __int_as_float(hu | 0x3f000000);
+            hu = (0x00800000 - hu) >> 2;
+        }
+        f = __fsub_rn(u, 1.0f);
+    }
+    const float hfsq = __fmul_rn(__fmul_rn(0.5f, f), f);
+    const float fk = (float)k;
+    if (hu == 0) {
+        if (f == 0.0f) {
+            if (k == 0) return 0.0f;
+            c = __fadd_rn(c, __fmul_rn(fk, ln2_lo));
+            return __fadd_rn(__fmul_rn(fk, ln2_hi), c);
+        }
+        const float R = __fmul_rn(hfsq, __fsub_rn(1.0f, __fmul_rn(0.66666666666666666f, f)));
+        if (k == 0) return __fsub_rn(f, R);
+        return __fsub_rn(__fmul_rn(fk, ln2_hi),
+                         __fsub_rn(__fsub_rn(R, __fadd_rn(__fmul_rn(fk, ln2_lo), c)), f));
+    }
+    const float s = __fdiv_rn(f, __fadd_rn(2.0f, f));
+    const float z = __fmul_rn(s, s);
+    float R = __fadd_rn(Lp6, __fmul_rn(z, Lp7));
+    R = __fadd_rn(Lp5, __fmul_rn(z, R));
+    R = __fadd_rn(Lp4, __fmul_rn(z, R));
+    R = __fadd_rn(Lp3, __fmul_rn(z, R));
+    R = __fadd_rn(Lp2, __fmul_rn(z, R));
+    R = __fadd_rn(Lp1, __fmul_rn(z, R));
+    R = __fmul_rn(z, R);
+    if (k == 0) return __fsub_rn(f, __fsub_rn(hfsq, __fmul_rn(s, __fadd_rn(hfsq, R))));
+    return __fsub_rn(__fmul_rn(fk, ln2_hi),
+                     __fsub_rn(__fsub_rn(hfsq, __fadd_rn(__fmul_rn(s, __fadd_rn(hfsq, R)),
+                                                         __fadd_rn(__fmul_rn(fk, ln2_lo), c))),
+                               f));
+}
+
+__device__ __forceinline__ float enc_count(uint32_t c) { return glibc_log1pf(__uint2float_rn(c)); }
+
+// Row flags: key with both actions recorded.
+__global__ void qt_both_kernel(const uint8_t* __restrict__ has, size_t m, uint32_t* __restrict__ flag) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < m; k += (size_t)gridDim.x * blockDim.x)
+        flag[k] = (has[2 * k] && has[2 * k + 1]) ? 1u : 0u;
+}
+
+// One thread per key: encode_state(counters_from_key(key)) + boltzmann_pair.
+__global__ void qt_snapshot_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ q,
+                                   const uint32_t* __restrict__ flag, const uint32_t* __restrict__ row,
+                                   size_t m, double rho, float* __restrict__ feat,
+                                   double* __restrict__ tgt, int* __restrict__ bad_stage) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < m; k += (size_t)gridDim.x * blockDim.x) {
+        if (!flag[k]) continue;
+        const uint32_t* v = keys + k * KW;
+        const size_t r = row[k];
+        float* out = feat + r * F;
+        const uint32_t stage = v[0];
+        if (stage >= 8) {  // counters_from_key: "state key holds invalid stage index"
+            atomicExch(bad_stage, 1);
+            continue;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) out[i] = i == (int)stage ? 1.0f : 0.0f;
+        // slots 8..36: basic blocks, vector[5], scalar[4], memory[6], compute[4],
+        // control-flow[4], registers[2], work groups[3] = key words 1..29
+        for (int w = 1; w < KW; ++w) out[7 + w] = enc_count(v[w]);
+        // totals (u32 wrap, like the u64 sums cast back): vector, scalar, memory,
+        // compute, control-flow, registers; instructions = the first five
+        const int lo_[6] = {2, 7, 11, 17, 21, 25};
+        const int len_[6] = {5, 4, 6, 4, 4, 2};
+        uint32_t tot[7];
+        for (int g = 0; g < 6; ++g) {
+            uint32_t sacc = 0;
+            for (int i = 0; i < len_[g]; ++i) sacc += v[lo_[g] + i];
+            tot[g + 1] = sacc;
+        }
+        tot[0] = tot[1] + tot[2] + tot[3] + tot[4] + tot[5];
+        for (int i = 0; i < 7; ++i) out[37 + i] = enc_count(tot[i]);
+        // boltzmann_pair (qtable.cpp:121-129)
+        const double q0 = q[2 * k], q1 = q[2 * k + 1];
+        const double mx = q0 < q1 ? q1 : q0;  // std::max
+        const double e0 = exp(__ddiv_rn(__dsub_rn(q0, mx), rho));
+        const double e1 = exp(__ddiv_rn(__dsub_rn(q1, mx), rho));
+        const double s = __dadd_rn(e0, e1);
+        tgt[2 * r] = __ddiv_rn(e0, s);
+        tgt[2 * r + 1] = __ddiv_rn(e1, s);
+    }
+}
+
+// ------------------------------------------------------------ host helpers
+size_t qt_temp_bytes(size_t n) {
+    size_t a = 0, b = 0, c = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+    cub::DeviceScan::InclusiveSum(nullptr, c, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+    return a > b ? (a > c ? a : c) : (b > c ? b : c);
+}
+
+cudaError_t qt_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out, size_t n,
+                              cudaStream_t st) {
+    return cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n, st);
+}
+
+#define QT_CK(x)                                \
+    do {                                        \
+        cudaError_t e_ = (x);                   \
+        if (e_ != cudaSuccess) return e_;       \
+    } while (0)
+
+static RecView rec_view(const QtFoldIO& io) {
+    return RecView{io.tkeys, io.init, io.n_init, io.bkeys, io.bact};
+}
+
+cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_sms, cudaStream_t st) {
+    const size_t nrec = io.n_init + io.n;
+    const RecView v = rec_view(io);
+    const int grid = num_sms * 4;
+    qt_iota_kernel<<<grid, 256, 0, st>>>(io.perm, nrec);
+    QT_CK(cudaMemsetAsync(io.spread, 0, sizeof(uint32_t) * (KW + 1), st));
+    qt_word_spread_kernel<<<grid, 256, 0, st>>>(v, nrec, io.spread);
+    uint32_t spread[KW + 1];
+    QT_CK(cudaMemcpyAsync(spread, io.spread, sizeof(spread), cudaMemcpyDeviceToHost, st));
+    QT_CK(cudaStreamSynchronize(st));
+    // LSD: least significant "digit" is the action, then words 29 .. 0
+    for (int pass = 0; pass <= KW; ++pass) {
+        const int w = pass == 0 ? KW : KW - pass;
+        if (spread[w] == 0) continue;  // constant word: no reordering
+        const int end_bit = 32 - __builtin_clz(spread[w]);
+        qt_gather_digit_kernel<<<grid, 256, 0, st>>>(v, io.perm, nrec, w, io.digit);
+        QT_CK(cub::DeviceRadixSort::SortPairs(io.temp, io.temp_bytes, io.digit, io.digit2, io.perm,
+                                              io.perm2, (int)nrec, 0, end_bit, st));
+        uint32_t* t = io.perm;
+        io.perm = io.perm2;
+        io.perm2 = t;
+    }
+    qt_heads_kernel<<<grid, 256, 0, st>>>(v, io.perm, nrec, io.seg_head, io.key_head);
+    QT_CK(cub::DeviceScan::ExclusiveSum(io.temp, io.temp_bytes, io.seg_head, io.seg_scan, (int)nrec, st));
+    QT_CK(cub::DeviceScan::InclusiveSum(io.temp, io.temp_bytes, io.key_head, io.key_scan, (int)nrec, st));
+    uint32_t tail[3];
+    QT_CK(cudaMemcpyAsync(&tail[0], io.seg_scan + nrec - 1, 4, cudaMemcpyDeviceToHost, st));
+    QT_CK(cudaMemcpyAsync(&tail[1], io.seg_head + nrec - 1, 4, cudaMemcpyDeviceToHost, st));
+    QT_CK(cudaMemcpyAsync(&tail[2], io.key_scan + nrec - 1, 4, cudaMemcpyDeviceToHost, st));
+    QT_CK(cudaStreamSynchronize(st));
+    nseg = (size_t)tail[0] + tail[1];
+    nkeys = tail[2];
+    qt_seg_list_kernel<<<grid, 256, 0, st>>>(io.seg_head, io.seg_scan, io.key_scan, nrec, io.seg_start,
+                                             io.seg_key);
+    return cudaGetLastError();
+}
+
+cudaError_t qt_fold(const QtFoldIO& io, size_t nseg, uint32_t* keys, double* q, uint64_t* t,
+                    uint64_t* cnt, uint8_t* has, int num_sms, cudaStream_t st) {
+    FoldArgs f{};
+    f.v = rec_view(io);
+    f.perm = io.perm;
+    f.nrec = io.n_init + io.n;
+    f.nseg = nseg;
+    f.seg_start = io.seg_start;
+    f.seg_key = io.seg_key;
+    f.old_q = io.old_q;
+    f.old_t = io.old_t;
+    f.old_cnt = io.old_cnt;
+    f.reward = io.reward;
+    f.now = io.now;
+    f.limit = io.limit;
+    f.alpha = io.alpha;
+    f.omega = io.omega;
+    f.keys = keys;
+    f.q = q;
+    f.t = t;
+    f.cnt = cnt;
+    f.has = has;
+    f.bad = io.bad;
+    qt_fold_kernel<<<num_sms * 4, 128, 0, st>>>(f);
+    return cudaGetLastError();
+}
+
+}  // namespace gbxcu

@@ -166,6 +166,38 @@ __global__ void wide_probs_kernel(const float* h2, const float* w2, const float*
                                   int hidden, double* probs);
 __global__ void zero_cols_kernel(float* m, int rows, int ld, int c_lo, int c_hi);
 
+// ------------------------------------------------- Q-table (row f1)
+constexpr int QT_KEY_WORDS = 30;  // StateKey: stage + 29 raw counters
+struct RecView;
+struct FoldArgs;
+__global__ void qt_iota_kernel(uint32_t* p, size_t n);
+__global__ void qt_init_ids_kernel(const uint8_t* has, size_t m, uint32_t* ids, unsigned long long* count);
+__global__ void qt_both_kernel(const uint8_t* has, size_t m, uint32_t* flag);
+__global__ void qt_snapshot_kernel(const uint32_t* keys, const double* q, const uint32_t* flag,
+                                   const uint32_t* row, size_t m, double rho, float* feat, double* tgt,
+                                   int* bad_stage);
+// fold pipeline entry points (launch wrappers live in k_qtable.cu)
+struct QtFoldIO {
+    const uint32_t* tkeys; const uint32_t* init; size_t n_init;
+    const uint32_t* bkeys; const uint8_t* bact; const double* reward; const uint64_t* now; size_t n;
+    size_t limit;
+    const double* old_q; const uint64_t* old_t; const uint64_t* old_cnt;
+    double alpha, omega;
+    // scratch [nrec] each
+    uint32_t *perm, *perm2, *digit, *digit2, *seg_head, *key_head, *seg_scan, *key_scan, *seg_start, *seg_key;
+    uint32_t* spread;            // [31]
+    void* temp; size_t temp_bytes;
+    unsigned long long* bad;     // [1]
+};
+size_t qt_temp_bytes(size_t nrec);
+// Sorts and segments the records; returns segment and key counts (synchronous).
+cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_sms, cudaStream_t st);
+// Folds into a new table (keys, q, t, cnt, has zeroed by the caller).
+cudaError_t qt_fold(const QtFoldIO& io, size_t nseg, uint32_t* keys, double* q, uint64_t* t,
+                    uint64_t* cnt, uint8_t* has, int num_sms, cudaStream_t st);
+cudaError_t qt_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out,
+                              size_t n, cudaStream_t st);
+
 __global__ void aggregate_kernel(AggArgs a);
 __global__ void histogram_kernel(const double* rows, int stride, size_t n, double* lower,
                                  unsigned long long* count, size_t cap,

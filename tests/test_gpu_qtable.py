@@ -1,0 +1,129 @@
+"""GPU parity of the device experience store: batched
+QTable::update (proj/src/qtable.cpp:76-92) and snapshot_policy_dataset
+(:143-155) against the compiled reference (oracle/_ref, unmodified sources).
+
+Tolerances: keys, key order, entry presence, timestamps, update counts and
+snapshot features bit-exact; Q values bit-exact for omega == 1 (the
+reference default) and rel 1e-14 otherwise (pow); Boltzmann targets rel 1e-15
+(CUDA exp vs glibc exp, last ulp)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2111_12055_b200 as gbx
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ref():
+    if not oracle.ref_available():
+        pytest.skip("compiled reference not available")
+    return oracle.Reference()
+
+
+def tuples(seed, n, n_distinct, wide=False):
+    """n tuples over ~n_distinct keys: stage in [0, 8), counters small (or full
+    u32 range when wide), some words constant, check-ins non-decreasing."""
+    rng = np.random.default_rng(seed)
+    base = np.zeros((n_distinct, 30), np.uint32)
+    base[:, 0] = rng.integers(0, 8, n_distinct)
+    hi = 2**32 if wide else 40
+    base[:, 1:] = rng.integers(0, hi, (n_distinct, 29), dtype=np.uint64).astype(np.uint32)
+    base[:, 25] = 7                       # a constant word (skipped radix pass)
+    keys = base[rng.integers(0, n_distinct, n)]
+    act = rng.integers(0, 2, n).astype(np.uint8)
+    rew = rng.random(n) * 0.4 + 0.8
+    now = np.sort(rng.integers(0, 1000, n)).astype(np.uint64)
+    return keys, act, rew, now
+
+
+def check_table(t, o, q_rtol=0.0):
+    np.testing.assert_array_equal(t["keys"], o["keys"])
+    np.testing.assert_array_equal(t["has"], o["has"])
+    h = o["has"].astype(bool)
+    np.testing.assert_array_equal(t["t"][h], o["t"][h])
+    np.testing.assert_array_equal(t["cnt"][h], o["cnt"][h])
+    if q_rtol == 0.0:
+        np.testing.assert_array_equal(t["q"][h], o["q"][h])
+    else:
+        np.testing.assert_allclose(t["q"][h], o["q"][h], rtol=q_rtol)
+
+
+@pytest.mark.parametrize("n,n_distinct,wide", [(1, 1, False), (5000, 1200, False),
+                                               (60_000, 20_000, True), (200_000, 3000, False)])
+def test_fold_and_snapshot_match_reference(dev, ref, n, n_distinct, wide):
+    keys, act, rew, now = tuples(n + n_distinct, n, n_distinct, wide)
+    o = ref.qtable_fold(keys, act, rew, now, alpha=0.3, omega=1.0, rho=0.1)
+    qt = gbx.DeviceQTable(dev, 0.3, 1.0)
+    qt.update_batch(keys, act, rew, now)
+    check_table(qt.export(), o)
+    feat, tgt = qt.snapshot(0.1)
+    np.testing.assert_array_equal(feat, o["feat"])            # glibc log1pf restated
+    np.testing.assert_allclose(tgt, o["tgt"], rtol=1e-15, atol=1e-300)
+    assert qt.size()[0] == len(o["keys"])
+    qt.close()
+
+
+def test_fold_omega_below_one(dev, ref):
+    keys, act, rew, now = tuples(3, 40_000, 2000)
+    o = ref.qtable_fold(keys, act, rew, now, alpha=0.25, omega=0.97, rho=0.05)
+    qt = gbx.DeviceQTable(dev, 0.25, 0.97)
+    qt.update_batch(keys, act, rew, now)
+    check_table(qt.export(), o, q_rtol=1e-14)
+
+
+def test_incremental_batches_equal_one_fold(dev, ref):
+    keys, act, rew, now = tuples(11, 30_000, 4000)
+    o = ref.qtable_fold(keys, act, rew, now)
+    qt = gbx.DeviceQTable(dev)
+    for lo, hi in [(0, 7000), (7000, 7001), (7001, 22_000), (22_000, 30_000)]:
+        qt.update_batch(keys[lo:hi], act[lo:hi], rew[lo:hi], now[lo:hi])
+    check_table(qt.export(), o)
+    feat, tgt = qt.snapshot(0.1)
+    np.testing.assert_array_equal(feat, o["feat"])
+
+
+def test_clock_regression_matches_reference(dev, ref):
+    keys, act, rew, now = tuples(5, 10_000, 500)
+    now = now.copy()
+    now[6000:] = now[6000:] - now[6000] // 2 - 1           # time goes backwards mid-stream
+    o = ref.qtable_fold(keys, act, rew, now)
+    assert o["bad"] >= 0
+    qt = gbx.DeviceQTable(dev)
+    with pytest.raises(gbx.ClockRegressionError) as ei:
+        qt.update_batch(keys, act, rew, now)
+    assert ei.value.index == o["bad"]
+    check_table(qt.export(), o)                             # prefix applied, as the reference
+
+
+def test_snapshot_validation(dev):
+    qt = gbx.DeviceQTable(dev)
+    with pytest.raises(gbx.InvalidTemperatureError):
+        qt.snapshot(0.0)
+    keys = np.zeros((2, 30), np.uint32)
+    keys[:, 0] = 9                                           # invalid stage index
+    qt.update_batch(keys, np.array([0, 1], np.uint8), np.array([1.0, 1.0]), np.array([0, 0], np.uint64))
+    with pytest.raises(gbx.ValidationError):
+        qt.snapshot(0.1)
+    with pytest.raises(gbx.ValidationError):
+        gbx.DeviceQTable(dev, 0.0, 1.0)
+    with pytest.raises(gbx.ValidationError):
+        qt.update_batch(keys[:1], np.array([2], np.uint8), np.array([1.0]), np.array([0], np.uint64))
+
+
+def test_snapshot_feeds_fit_on_device(dev, ref):
+    """Experience store -> training records stay on the device (fit_dev)."""
+    import torch
+    keys, act, rew, now = tuples(21, 50_000, 9000)
+    qt = gbx.DeviceQTable(dev)
+    qt.update_batch(keys, act, rew, now)
+    feat_h, tgt_h = qt.snapshot(0.1)
+    d_feat = torch.empty((len(feat_h), 44), dtype=torch.float32, device="cuda")
+    d_tgt = torch.empty((len(feat_h), 2), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    r = qt.snapshot_dev(0.1, d_feat.data_ptr(), d_tgt.data_ptr(), len(feat_h))
+    torch.cuda.synchronize()
+    assert r == len(feat_h)
+    np.testing.assert_array_equal(d_feat.cpu().numpy(), feat_h)
+    np.testing.assert_array_equal(d_tgt.cpu().numpy(), tgt_h)
