@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--c5-apps", type=int, default=10_000)
+    ap.add_argument("--qt-tuples", type=int, default=10_000_000,
+                    help="experience-store secondary: tuples folded into a fresh device Q-table")
     ap.add_argument("--c5-shaders-per-app", type=int, default=1_000)
     return ap.parse_args()
 
@@ -470,7 +472,75 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
                        "tflops": tf, "flop_per_record": 1_669_120,
                        "tf32_peak_tflops": peaks.get("bf16_tflops", 1590.0) / 2,
                        "peak_note": "dense TF32 = half the measured bf16 cuBLAS peak"}
+
+    # row f1: experience store — fold a synthetic C3-scale tuple log into a fresh
+    # device Q-table (QTable::update x n) + snapshot_policy_dataset (device-resident)
+    out["qtable"] = run_qtable(args, dev, stream, torch, gbx, peaks)
     return out
+
+
+def qtable_tuples_torch(torch, n, seed):
+    """Synthetic experience tuples on the device: ~0.8 n distinct StateKeys
+    (stage < 8, counters < 4096), actions 0/1, rewards ~ U[0.8, 1.2),
+    non-decreasing check-ins."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    nd = max(1, int(0.8 * n))
+    base = torch.randint(0, 4096, (nd, 30), generator=g, device="cuda", dtype=torch.int64)
+    base[:, 0] %= 8
+    idx = torch.randint(0, nd, (n,), generator=g, device="cuda")
+    keys = base[idx].to(torch.int32).contiguous()
+    act = torch.randint(0, 2, (n,), generator=g, device="cuda", dtype=torch.uint8)
+    rew = torch.rand(n, generator=g, device="cuda", dtype=torch.float64) * 0.4 + 0.8
+    now = torch.sort(torch.randint(0, 1000, (n,), generator=g, device="cuda")).values.contiguous()
+    return keys, act, rew, now
+
+
+def run_qtable(args, dev, stream, torch, gbx, peaks):
+    n = args.qt_tuples
+    keys, act, rew, now = qtable_tuples_torch(torch, n, 5)
+    torch.cuda.synchronize()
+    feat = torch.empty((n, 44), dtype=torch.float32, device="cuda")
+    tgt = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+
+    qt = gbx.DeviceQTable(dev)
+
+    def once():  # fresh (cleared) table each time; device buffers reused
+        qt.clear()
+        qt.update_batch_dev(keys.data_ptr(), act.data_ptr(), rew.data_ptr(), now.data_ptr(), n)
+        rows = qt.snapshot_dev(0.1, feat.data_ptr(), tgt.data_ptr(), n)
+        return rows, qt.m_states()
+
+    once()
+    torch.cuda.synchronize()
+    reps = 3
+    ev0.record(stream)
+    for _ in range(reps):
+        rows, states = once()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    qt.close()
+    ms = ev0.elapsed_time(ev1) / reps
+    res = {"value": n / (ms * 1e-3), "unit": "tuples/s (fold + snapshot)", "ms": ms, "tuples": n,
+           "states": states, "snapshot_rows": rows,
+           "algorithmic_bytes_per_tuple": 137,
+           "hbm_gbs": n * 137 / (ms * 1e-3) / 1e9,
+           "hbm_peak_gbs": peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)}
+    if not args.no_cpu_baseline:
+        import oracle
+        if oracle.ref_available():
+            m = min(n, 200_000)
+            k = keys[:m].cpu().numpy().view(np.uint32)
+            t0 = time.perf_counter()
+            oracle.Reference().qtable_fold(k, act[:m].cpu().numpy(), rew[:m].cpu().numpy(),
+                                           now[:m].cpu().numpy().astype(np.uint64))
+            dt = time.perf_counter() - t0
+            res["cpu_baseline"] = {"value": m / dt, "unit": "tuples/s (fold + snapshot)",
+                                   "cores": 1, "kind": "reference",
+                                   "sample": f"{m} tuples of the same log, QTable::update + "
+                                             f"snapshot_policy_dataset, {dt:.1f} s on 1 host core"}
+    return res
 
 
 if __name__ == "__main__":

@@ -176,6 +176,7 @@ typedef struct gbxcu_qtable gbxcu_qtable;
 #define GBXCU_KEY_WORDS 30
 int gbxcu_qtable_create(gbxcu_ctx* ctx, double alpha, double omega, gbxcu_qtable** out);
 void gbxcu_qtable_free(gbxcu_qtable* t);
+int gbxcu_qtable_clear(gbxcu_qtable* t);  /* empty table, device buffers kept */
 /* QTable::update (proj/src/qtable.cpp:76-92) applied to n tuples in order:
  * keys[n][30], actions[n] (0/1), rewards[n], now[n]. Same-key updates fold
  * sequentially (bit-exact for omega == 1, the reference default; pow() within
@@ -185,6 +186,10 @@ void gbxcu_qtable_free(gbxcu_qtable* t);
 int gbxcu_qtable_update_batch(gbxcu_qtable* t, const uint32_t* keys, const uint8_t* actions,
                               const double* rewards, const uint64_t* now, size_t n,
                               size_t* bad_index);
+/* Device-resident tuples (actions must be 0/1; not re-validated). */
+int gbxcu_qtable_update_batch_dev(gbxcu_qtable* t, const uint32_t* d_keys, const uint8_t* d_actions,
+                                  const double* d_rewards, const uint64_t* d_now, size_t n,
+                                  size_t* bad_index);
 int gbxcu_qtable_size(const gbxcu_qtable* t, size_t* states, size_t* entries);
 /* Table in key order: keys[m][30], q/ts/cnt/has[m][2] (has: entry recorded). */
 int gbxcu_qtable_export(const gbxcu_qtable* t, uint32_t* keys, double* q, uint64_t* ts,

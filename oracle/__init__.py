@@ -98,6 +98,8 @@ class Restatement(_Lib):
         L.orc_boltzmann_pair.argtypes = [C.c_double, C.c_double, C.c_double, _f64p]
         L.orc_partial_gradient.argtypes = [_f32p, _f32p, _f64p, _u64p, _sz, C.c_double, _f64p,
                                            C.POINTER(C.c_double)]
+        L.orc_log1pf_counts.restype = C.c_float
+        L.orc_log1pf_counts.argtypes = [C.c_float]
         L.orc_fnv1a.restype = _u64
         L.orc_fnv1a.argtypes = [C.c_void_p, _sz]
 

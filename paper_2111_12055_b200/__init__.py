@@ -94,8 +94,8 @@ EXPORTS = (
     "gbxcu_suite_free", "gbxcu_suite_features", "gbxcu_evaluate", "gbxcu_evaluate_dev",
     "gbxcu_wide_param_count", "gbxcu_wide_init", "gbxcu_wide_forward", "gbxcu_wide_fit",
     "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_peer_export",
-    "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free",
-    "gbxcu_qtable_update_batch", "gbxcu_qtable_size", "gbxcu_qtable_export",
+    "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free", "gbxcu_qtable_clear",
+    "gbxcu_qtable_update_batch", "gbxcu_qtable_update_batch_dev", "gbxcu_qtable_size", "gbxcu_qtable_export",
     "gbxcu_qtable_snapshot", "gbxcu_qtable_snapshot_dev",
 )
 PEER_HANDLE_BYTES = 64
@@ -141,7 +141,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_qtable_create.argtypes = [_vp, C.c_double, C.c_double, C.POINTER(_vp)]
     L.gbxcu_qtable_free.argtypes = [_vp]
     L.gbxcu_qtable_free.restype = None
+    L.gbxcu_qtable_clear.argtypes = [_vp]
     L.gbxcu_qtable_update_batch.argtypes = [_vp, _vp, _vp, _vp, _vp, _sz, C.POINTER(_sz)]
+    L.gbxcu_qtable_update_batch_dev.argtypes = [_vp, _vp, _vp, _vp, _vp, _sz, C.POINTER(_sz)]
     L.gbxcu_qtable_size.argtypes = [_vp, C.POINTER(_sz), C.POINTER(_sz)]
     L.gbxcu_qtable_export.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
     L.gbxcu_qtable_snapshot.argtypes = [_vp, C.c_double, _vp, _vp, _sz, C.POINTER(_sz)]
@@ -515,6 +517,26 @@ class DeviceQTable:
                 e.index = int(bad.value)
                 raise
         self.dev._ck(rc)
+
+    def clear(self):
+        self.dev._ck(self.L.gbxcu_qtable_clear(self.h))
+
+    def update_batch_dev(self, d_keys: int, d_actions: int, d_rewards: int, d_now: int, n: int):
+        bad = _sz(0)
+        rc = self.L.gbxcu_qtable_update_batch_dev(self.h, d_keys, d_actions, d_rewards, d_now, n,
+                                                  C.byref(bad))
+        if rc == ECLOCK:
+            try:
+                _raise(self.L, rc)
+            except ClockRegressionError as e:
+                e.index = int(bad.value)
+                raise
+        self.dev._ck(rc)
+
+    def m_states(self) -> int:
+        m = _sz(0)
+        self.dev._ck(self.L.gbxcu_qtable_size(self.h, C.byref(m), None))
+        return int(m.value)
 
     def size(self):
         m, e = _sz(0), _sz(0)

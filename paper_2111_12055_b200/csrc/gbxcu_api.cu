@@ -821,6 +821,12 @@ int gbxcu_qtable_create(gbxcu_ctx* c, double alpha, double omega, gbxcu_qtable**
 
 void gbxcu_qtable_free(gbxcu_qtable* t) { delete t; }
 
+int gbxcu_qtable_clear(gbxcu_qtable* t) {
+    if (!t) return fail(GBXCU_EINVAL, "null table");
+    t->m = 0;  // device buffers are kept for the next fold
+    return GBXCU_OK;
+}
+
 int gbxcu_qtable_size(const gbxcu_qtable* t, size_t* states, size_t* entries) {
     if (!t) return fail(GBXCU_EINVAL, "null table");
     if (states) *states = t->m;
@@ -835,7 +841,8 @@ int gbxcu_qtable_size(const gbxcu_qtable* t, size_t* states, size_t* entries) {
 }
 
 namespace {
-int qtable_fold(gbxcu_qtable* t, size_t n, cudaStream_t st, size_t* bad_index) {
+int qtable_fold(gbxcu_qtable* t, const uint32_t* d_keys, const uint8_t* d_act, const double* d_rew,
+                const uint64_t* d_now, size_t n, cudaStream_t st, size_t* bad_index) {
     gbxcu_ctx* c = t->ctx;
     // existing entries become init records
     size_t n_init = 0;
@@ -857,9 +864,11 @@ int qtable_fold(gbxcu_qtable* t, size_t n, cudaStream_t st, size_t* bad_index) {
     const size_t nrec = n_init + n;
     if (nrec == 0) return GBXCU_OK;
     if (nrec > 0xFFFFFFFFull) return fail(GBXCU_EINVAL, "q-table fold too large (> 2^32 records)");
-    for (DevBuf* b : {&t->perm, &t->perm2, &t->digit, &t->digit2, &t->seg_head, &t->key_head,
-                      &t->seg_scan, &t->key_scan, &t->seg_start, &t->seg_key})
+    for (DevBuf* b : {&t->perm, &t->perm2, &t->seg_head, &t->key_head, &t->seg_scan, &t->key_scan,
+                      &t->seg_start, &t->seg_key})
         RET(b->ensure(sizeof(uint32_t) * nrec));
+    RET(t->digit.ensure(sizeof(unsigned long long) * nrec));   // packed 64-bit radix digits
+    RET(t->digit2.ensure(sizeof(unsigned long long) * nrec));
     RET(t->spread.ensure(sizeof(uint32_t) * 32));
     RET(t->bad.ensure(16));
     const size_t tb = qt_temp_bytes(nrec);
@@ -868,10 +877,10 @@ int qtable_fold(gbxcu_qtable* t, size_t n, cudaStream_t st, size_t* bad_index) {
     io.tkeys = t->keys.as<uint32_t>();
     io.init = t->init_ids.as<uint32_t>();
     io.n_init = n_init;
-    io.bkeys = t->bkeys.as<uint32_t>();
-    io.bact = t->bact.as<uint8_t>();
-    io.reward = t->brew.as<double>();
-    io.now = t->bnow.as<uint64_t>();
+    io.bkeys = d_keys;
+    io.bact = d_act;
+    io.reward = d_rew;
+    io.now = d_now;
     io.n = n;
     io.limit = n;
     io.old_q = t->q.as<double>();
@@ -920,6 +929,20 @@ int qtable_fold(gbxcu_qtable* t, size_t n, cudaStream_t st, size_t* bad_index) {
     t->m = nkeys;
     return GBXCU_OK;
 }
+
+int qtable_update(gbxcu_qtable* t, const uint32_t* d_keys, const uint8_t* d_act, const double* d_rew,
+                  const uint64_t* d_now, size_t n, cudaStream_t st, size_t* bad_index) {
+    size_t bad = (size_t)-1;
+    RET(qtable_fold(t, d_keys, d_act, d_rew, d_now, n, st, &bad));
+    if (bad == (size_t)-1) return GBXCU_OK;
+    // ClockRegressionError at tuple `bad`: the reference has applied every
+    // tuple before it (updates are sequential) — fold exactly that prefix.
+    size_t bad2 = (size_t)-1;
+    if (bad > 0) RET(qtable_fold(t, d_keys, d_act, d_rew, d_now, bad, st, &bad2));
+    if (bad_index) *bad_index = bad;
+    return fail(GBXCU_ECLOCK, "q_update check-in precedes the entry timestamp (tuple " +
+                                  std::to_string(bad) + ")");
+}
 }  // namespace
 
 int gbxcu_qtable_update_batch(gbxcu_qtable* t, const uint32_t* keys, const uint8_t* actions,
@@ -938,16 +961,21 @@ int gbxcu_qtable_update_batch(gbxcu_qtable* t, const uint32_t* keys, const uint8
     RET(upload(t->bact, actions, n, st));
     RET(upload(t->brew, rewards, n, st));
     RET(upload(t->bnow, now, n, st));
-    size_t bad = (size_t)-1;
-    RET(qtable_fold(t, n, st, &bad));
-    if (bad == (size_t)-1) return GBXCU_OK;
-    // ClockRegressionError at tuple `bad`: the reference has applied every
-    // tuple before it (updates are sequential) — fold exactly that prefix.
-    size_t bad2 = (size_t)-1;
-    if (bad > 0) RET(qtable_fold(t, bad, st, &bad2));
-    if (bad_index) *bad_index = bad;
-    return fail(GBXCU_ECLOCK, "q_update check-in precedes the entry timestamp (tuple " +
-                                  std::to_string(bad) + ")");
+    return qtable_update(t, t->bkeys.as<uint32_t>(), t->bact.as<uint8_t>(), t->brew.as<double>(),
+                         t->bnow.as<uint64_t>(), n, st, bad_index);
+}
+
+int gbxcu_qtable_update_batch_dev(gbxcu_qtable* t, const uint32_t* d_keys, const uint8_t* d_actions,
+                                  const double* d_rewards, const uint64_t* d_now, size_t n,
+                                  size_t* bad_index) {
+    if (!t || (n && (!d_keys || !d_actions || !d_rewards || !d_now)))
+        return fail(GBXCU_EINVAL, "null argument");
+    if (bad_index) *bad_index = (size_t)-1;
+    if (n == 0) return GBXCU_OK;
+    gbxcu_ctx* c = t->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    return qtable_update(t, d_keys, d_actions, d_rewards, d_now, n, c->stream, bad_index);
 }
 
 int gbxcu_qtable_export(const gbxcu_qtable* t, uint32_t* keys, double* q, uint64_t* ts, uint64_t* cnt,

@@ -13,8 +13,9 @@
 //      the tuples in sequence order;
 //   2. stable LSD radix sort of the record permutation by (key words 0..29,
 //      action): action first, then word 29 .. word 0; words whose values are
-//      all equal are skipped, the others sort only their significant bits
-//      (cub::DeviceRadixSort per pass; the passes are the only library calls);
+//      all equal are skipped, the others contribute only their varying low
+//      bits, packed into 64-bit digits (one gather + one cub::DeviceRadixSort
+//      per 64 bits; the sorts are the only library calls);
 //   3. segment heads by comparing neighbours (key, action) and key alone;
 //   4. one thread per (key, action) segment folds its records in sequence
 //      order — the Eq.-5 recurrence is a strict left fold, so each segment is
@@ -94,12 +95,27 @@ __global__ void qt_word_spread_kernel(RecView v, size_t nrec, uint32_t* __restri
     if (threadIdx.x <= KW && acc[threadIdx.x]) atomicOr(&spread[threadIdx.x], acc[threadIdx.x]);
 }
 
-// digit[i] = word w (w == KW: action) of record perm[i]
-__global__ void qt_gather_digit_kernel(RecView v, const uint32_t* __restrict__ perm, size_t nrec, int w,
-                                       uint32_t* __restrict__ digit) {
+// One radix pass sorts a 64-bit digit packing several key words (only their
+// varying low bits): field f = word wlist[f] (KW: the action), masked to
+// bits[f], at bit offset off[f] (least significant field first).
+struct PackSpec {
+    int nf;
+    int w[8];
+    int bits[8];
+    int off[8];
+};
+__global__ void qt_gather_digit_kernel(RecView v, const uint32_t* __restrict__ perm, size_t nrec, PackSpec ps,
+                                       unsigned long long* __restrict__ digit) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec; i += (size_t)gridDim.x * blockDim.x) {
         const uint32_t r = perm[i];
-        digit[i] = w == KW ? v.action(r) : v.key(r)[w];
+        const uint32_t* k = v.key(r);
+        unsigned long long d = 0;
+        for (int f = 0; f < ps.nf; ++f) {
+            const uint32_t x = ps.w[f] == KW ? v.action(r) : k[ps.w[f]];
+            const uint32_t m = ps.bits[f] >= 32 ? 0xFFFFFFFFu : ((1u << ps.bits[f]) - 1u);
+            d |= (unsigned long long)(x & m) << ps.off[f];
+        }
+        digit[i] = d;
     }
 }
 
@@ -340,8 +356,9 @@ __global__ void qt_snapshot_kernel(const uint32_t* __restrict__ keys, const doub
 // ------------------------------------------------------------ host helpers
 size_t qt_temp_bytes(size_t n) {
     size_t a = 0, b = 0, c = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (const unsigned long long*)nullptr,
+                                    (unsigned long long*)nullptr, (const uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)n);
     cub::DeviceScan::ExclusiveSum(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
     cub::DeviceScan::InclusiveSum(nullptr, c, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
@@ -372,14 +389,36 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
     uint32_t spread[KW + 1];
     QT_CK(cudaMemcpyAsync(spread, io.spread, sizeof(spread), cudaMemcpyDeviceToHost, st));
     QT_CK(cudaStreamSynchronize(st));
-    // LSD: least significant "digit" is the action, then words 29 .. 0
-    for (int pass = 0; pass <= KW; ++pass) {
-        const int w = pass == 0 ? KW : KW - pass;
-        if (spread[w] == 0) continue;  // constant word: no reordering
-        const int end_bit = 32 - __builtin_clz(spread[w]);
-        qt_gather_digit_kernel<<<grid, 256, 0, st>>>(v, io.perm, nrec, w, io.digit);
-        QT_CK(cub::DeviceRadixSort::SortPairs(io.temp, io.temp_bytes, io.digit, io.digit2, io.perm,
-                                              io.perm2, (int)nrec, 0, end_bit, st));
+    // LSD over the packed key: the action is the least significant field, then
+    // words 29 .. 0; each pass packs up to 64 bits of varying fields (constant
+    // words are skipped: they cannot reorder anything)
+    int w_next = KW;  // KW = action, then 29, 28, ..., 0
+    auto bits_of = [&](int w) { return spread[w] ? 32 - __builtin_clz(spread[w]) : 0; };
+    while (w_next >= 0) {
+        PackSpec ps{};
+        int used = 0;
+        while (w_next >= 0 && ps.nf < 8) {
+            const int w = w_next == KW ? KW : w_next;
+            const int b = bits_of(w);
+            if (b == 0) {  // constant field
+                w_next = w == KW ? KW - 1 : w_next - 1;
+                continue;
+            }
+            if (used + b > 64) break;
+            ps.w[ps.nf] = w;
+            ps.bits[ps.nf] = b;
+            ps.off[ps.nf] = used;
+            ps.nf++;
+            used += b;
+            w_next = w == KW ? KW - 1 : w_next - 1;
+        }
+        if (ps.nf == 0) break;
+        qt_gather_digit_kernel<<<grid, 256, 0, st>>>(v, io.perm, nrec, ps,
+                                                     reinterpret_cast<unsigned long long*>(io.digit));
+        QT_CK(cub::DeviceRadixSort::SortPairs(io.temp, io.temp_bytes,
+                                              reinterpret_cast<const unsigned long long*>(io.digit),
+                                              reinterpret_cast<unsigned long long*>(io.digit2), io.perm,
+                                              io.perm2, (int)nrec, 0, used, st));
         uint32_t* t = io.perm;
         io.perm = io.perm2;
         io.perm2 = t;

@@ -154,3 +154,23 @@ def test_qtable_snapshot_golden_shape():
     q = golden("qtable")
     # 3 keys carry both actions (stage 0, 5, 7); the one-sided key is dropped
     assert q["feat"].shape == (3, 44) and np.allclose(q["tgt"].sum(1), 1.0)
+
+
+def test_log1pf_restatement_matches_host_glibc():
+    """encode_state's log1pf (proj/src/core.cpp:50) restated (oracle C, mirrored
+    by the device kernel) equals the host glibc log1pf on integer counts."""
+    import ctypes as C
+
+    import oracle
+
+    libm = C.CDLL("libm.so.6")
+    libm.log1pf.restype = C.c_float
+    libm.log1pf.argtypes = [C.c_float]
+    r = oracle.Restatement().lib
+    rng = np.random.default_rng(0)
+    counts = np.concatenate([np.arange(0, 20000), rng.integers(0, 2**32, 20000, dtype=np.uint64)])
+    for c in counts:
+        x = float(np.float32(c))
+        a = np.float32(libm.log1pf(x))
+        b = np.float32(r.orc_log1pf_counts(x))
+        assert a.view(np.uint32) == b.view(np.uint32), c
