@@ -5,6 +5,7 @@
 // the per-epoch shuffle -> train sequence of fit, and the NCCL all-reduce of
 // the data-parallel step. All arithmetic on the path runs in the kernels; there
 // is no CPU fallback.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -20,6 +21,13 @@
 #include "kernels.h"
 
 using namespace gbxcu;
+
+namespace gbxcu {
+template <int BN>
+__global__ void tma_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
+                                const __grid_constant__ CUtensorMap map_b, GemmArgs g);
+}
+constexpr int TM_BM_HOST = 128;
 
 namespace {
 
@@ -157,6 +165,10 @@ int setup_kernel_attrs() {
         set((const void*)train_partial_tc_kernel<4>, train_tc_smem_bytes(4));
         set((const void*)train_partial_tc_kernel<7>, train_tc_smem_bytes(7));
         set((const void*)tc_gemm_kernel, gemm_smem_bytes());
+        set((const void*)wide_head_kernel, sizeof(float) * 32 * (1024 + 1));
+        set((const void*)tma_gemm_kernel<64>, tma_gemm_smem_bytes<64>());
+        set((const void*)tma_gemm_kernel<128>, tma_gemm_smem_bytes<128>());
+        set((const void*)tma_gemm_kernel<256>, tma_gemm_smem_bytes<256>());
     });
     return rc;
 }
@@ -1257,7 +1269,62 @@ constexpr int kGemmTile = 128;  // GM == GN in k_wide.cu
 
 size_t wide_param_count(int H) { return (size_t)H * F + H + (size_t)H * H + H + 2 * (size_t)H + 2; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// K-major fp32 operand [rows][ld] (K valid columns) as TMA boxes of
+// {32 fp32 = 128 B, box_rows} with the 128-byte swizzle (tma_gemm_kernel).
+bool make_operand_map(CUtensorMap* m, const float* base, int K, int rows, int ld, int box_rows) {
+    const EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+    const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+int launch_tma_gemm(gbxcu_ctx* c, const GemmArgs& g, int splits, cudaStream_t st, bool& done) {
+    CUtensorMap ma, mb;
+    done = make_operand_map(&ma, g.A, g.K, g.M, g.lda, TM_BM_HOST) &&
+           make_operand_map(&mb, g.B, g.K, g.N, g.ldb, BN);
+    if (!done) return GBXCU_OK;
+    dim3 grid((g.N + BN - 1) / BN, (g.M + TM_BM_HOST - 1) / TM_BM_HOST, splits);
+    tma_gemm_kernel<BN><<<grid, 128, tma_gemm_smem_bytes<BN>(), st>>>(ma, mb, g);
+    return check_launch(c, "tma_gemm_kernel");
+}
+
 int launch_gemm(gbxcu_ctx* c, const GemmArgs& g, int splits, cudaStream_t st) {
+    // TMA path: plain (non-gathered) operands with 16-byte row strides
+    const bool tma_ok = !g.a_rows && g.K % 4 == 0 && g.lda % 4 == 0 && g.ldb % 4 == 0 &&
+                        ((uintptr_t)g.A % 16) == 0 && ((uintptr_t)g.B % 16) == 0;
+    if (tma_ok) {
+        bool done = false;
+        int rc;
+        if (g.N <= 64) rc = launch_tma_gemm<64>(c, g, splits, st, done);
+        else if (splits > 1 || g.N < 256) rc = launch_tma_gemm<128>(c, g, splits, st, done);
+        else rc = launch_tma_gemm<256>(c, g, splits, st, done);
+        if (rc != GBXCU_OK || done) return rc;
+        // the wide path relies on TMA's zero fill past K (no tail clearing)
+        return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled unavailable or rejected the operand");
+    }
     dim3 grid((g.N + kGemmTile - 1) / kGemmTile, (g.M + kGemmTile - 1) / kGemmTile, splits);
     tc_gemm_kernel<<<grid, 128, gemm_smem_bytes(), st>>>(g);
     return check_launch(c, "tc_gemm_kernel");
@@ -1298,16 +1365,10 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
                  o_w2 = o_b1 + H;
     float* G = c->w_grad.as<float>();
     if (nbr > 0) {
-        // K tails of the transposed operands read as zeros
-        const int c_hi = (int)std::min<size_t>(ldt, ((size_t)nbr + 3) & ~(size_t)3);
-        for (DevBuf* b : {&c->w_h1t, &c->w_d2t, &c->w_d1t}) {
-            zero_cols_kernel<<<blocks((size_t)H * 4), 256, 0, st>>>(b->as<float>(), H, (int)ldt, nbr, c_hi);
-            RET(check_launch(c, "zero_cols_kernel"));
-        }
+        // (the K = batch GEMMs read exactly nbr columns through TMA, which
+        //  zero-fills past the end: no tail clearing needed)
         wide_gather_xt_kernel<<<blocks(nbr), 256, 0, st>>>(feat, rows, nbr, c->w_xt.as<float>(), (int)ldt);
         RET(check_launch(c, "wide_gather_xt_kernel"));
-        zero_cols_kernel<<<blocks(48 * 4), 256, 0, st>>>(c->w_xt.as<float>(), 48, (int)ldt, nbr, c_hi);
-        RET(check_launch(c, "zero_cols_kernel"));
 
         GemmArgs g1{};  // H1 = relu(X W0^T + b0), also H1^T
         g1.M = nbr; g1.N = H; g1.K = F;
@@ -1332,7 +1393,7 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
         h.inv_b = 1.0 / (double)nb;
         h.kl = c->w_kl.as<double>(); h.d3 = c->w_d3.as<float>();
         h.d2 = c->w_d2.as<float>(); h.d2t = c->w_d2t.as<float>();
-        wide_head_kernel<<<blocks((size_t)nbr * 32), 256, 0, st>>>(h);
+        wide_head_kernel<<<(nbr + 31) / 32, 1024, sizeof(float) * 32 * (H + 1), st>>>(h);
         RET(check_launch(c, "wide_head_kernel"));
 
         GemmArgs g3{};  // D1^T = ((D2 W1) . [H1 > 0])^T
@@ -1369,7 +1430,7 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
         RET(check_launch(c, "row_sum_kernel"));
         row_sum_kernel<<<H, 256, 0, st>>>(c->w_d2t.as<float>(), (int)ldt, nbr, G + o_b1);
         RET(check_launch(c, "row_sum_kernel"));
-        wide_w2_partial_kernel<<<dim3((H + 127) / 128, rsplit), 128, 0, st>>>(
+        wide_w2_partial_kernel<<<dim3((H + 63) / 64, rsplit), 256, 0, st>>>(
             c->w_h2.as<float>(), c->w_d3.as<float>(), c->w_kl.as<double>(), nbr, H,
             c->w_part.as<double>());
         RET(check_launch(c, "wide_w2_partial_kernel"));

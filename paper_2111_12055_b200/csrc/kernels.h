@@ -145,6 +145,8 @@ struct WideHeadArgs {
 };
 
 __global__ void tc_gemm_kernel(GemmArgs g);
+template <int BN>
+size_t tma_gemm_smem_bytes();
 size_t gemm_smem_bytes();
 __global__ void wide_gather_xt_kernel(const float* feat, const uint32_t* rows, int nb, float* xt,
                                       int ldt);

@@ -29,6 +29,20 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes
     return d;
 }
 
+// K-major operand with the 128-byte swizzle (TMA CU_TENSOR_MAP_SWIZZLE_128B):
+// rows of 128 B, 8-row groups 1024 B apart (SBO), LBO unused (K per MMA fits
+// the swizzle width), layout type SWIZZLE_128B = 2 at bits [61,64). The tile
+// base must be 1024-B aligned; K steps advance the start address.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;              // LBO (unused) = 16 B
+    d |= (uint64_t)(1024 >> 4) << 32;    // SBO = 1024 B
+    d |= (uint64_t)1 << 46;              // version = 1 (Blackwell)
+    d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+    return d;
+}
+
 // Instruction descriptor: A, B = TF32 (K-major), D = F32, dense.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4)                       // c_format = F32
