@@ -110,7 +110,7 @@ struct gbxcu_ctx {
     int fast_per_sm = 1;
     // wide MLP (C4) working set
     DevBuf w_params, w_grad, w_w1t, w_h1, w_h1t, w_h2, w_d2, w_d2t, w_d1t, w_xt, w_d3, w_kl;
-    DevBuf w_part, w_g4, w_g5, w_loss, w_feat, w_tgt, w_probs;
+    DevBuf w_part, w_g4, w_g5, w_loss, w_feat, w_tgt, w_probs, w_xg, w_w0p;
     // data parallel
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
@@ -1346,6 +1346,8 @@ int wide_alloc(gbxcu_ctx* c, int H, size_t bmax, int splits4, int splits5, int r
     RET(c->w_d2.ensure(sizeof(float) * bmax * H));
     for (DevBuf* b : {&c->w_h1t, &c->w_d2t, &c->w_d1t}) RET(b->ensure(sizeof(float) * H * ldt));
     RET(c->w_xt.ensure(sizeof(float) * 48 * ldt));
+    RET(c->w_xg.ensure(sizeof(float) * 48 * bmax));
+    RET(c->w_w0p.ensure(sizeof(float) * 48 * H));
     RET(c->w_d3.ensure(sizeof(float) * 2 * bmax));
     RET(c->w_kl.ensure(sizeof(double) * bmax));
     RET(c->w_part.ensure(sizeof(double) * rsplit * (2 * H + 3)));
@@ -1367,13 +1369,14 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
     if (nbr > 0) {
         // (the K = batch GEMMs read exactly nbr columns through TMA, which
         //  zero-fills past the end: no tail clearing needed)
-        wide_gather_xt_kernel<<<blocks(nbr), 256, 0, st>>>(feat, rows, nbr, c->w_xt.as<float>(), (int)ldt);
+        wide_gather_xt_kernel<<<blocks(nbr), 256, 0, st>>>(feat, rows, nbr, c->w_xt.as<float>(), (int)ldt,
+                                                           c->w_xg.as<float>());
         RET(check_launch(c, "wide_gather_xt_kernel"));
 
-        GemmArgs g1{};  // H1 = relu(X W0^T + b0), also H1^T
-        g1.M = nbr; g1.N = H; g1.K = F;
-        g1.A = feat; g1.lda = F; g1.a_rows = rows;
-        g1.B = P; g1.ldb = F;
+        GemmArgs g1{};  // H1 = relu(X W0^T + b0), also H1^T (X gathered, K padded to 48)
+        g1.M = nbr; g1.N = H; g1.K = 48;
+        g1.A = c->w_xg.as<float>(); g1.lda = 48;
+        g1.B = c->w_w0p.as<float>(); g1.ldb = 48;
         g1.epi = EPI_BIAS_RELU; g1.bias = P + o_b0;
         g1.out = c->w_h1.as<float>(); g1.ldo = H;
         g1.out_t = c->w_h1t.as<float>(); g1.ldt = (int)ldt;
@@ -1446,7 +1449,7 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
         CKN(ncclAllReduce(c->w_loss.p, c->w_loss.p, 1, ncclFloat64, ncclSum, c->comm, st));
     }
     wide_update_kernel<<<blocks(wide_param_count(H)), 256, 0, st>>>(
-        P, G, c->w_loss.as<double>(), nb, lr, H, c->w_w1t.as<float>(), epoch,
+        P, G, c->w_loss.as<double>(), nb, lr, H, c->w_w1t.as<float>(), c->w_w0p.as<float>(), epoch,
         c->diverged.as<int>(), c->epoch_acc.as<double>(), wide_param_count(H));
     return check_launch(c, "wide_update_kernel");
 }
@@ -1470,7 +1473,8 @@ int wide_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, c
     RET(wide_alloc(c, H, bmax, splits4, splits5, rsplit));
     RET(c->epoch_loss.ensure(sizeof(double) * cfg->epochs));
     RET(c->epoch_acc.ensure(16));
-    wide_w1t_kernel<<<blocks((size_t)H * H), 256, 0, st>>>(d_params, H, c->w_w1t.as<float>());
+    wide_w1t_kernel<<<blocks((size_t)H * std::max(H, 48)), 256, 0, st>>>(d_params, H, c->w_w1t.as<float>(),
+                                                                        c->w_w0p.as<float>());
     RET(check_launch(c, "wide_w1t_kernel"));
     const long n_steps = (long)((n + cfg->batch_size - 1) / cfg->batch_size);
     for (int e = 0; e < cfg->epochs; ++e) {

@@ -382,13 +382,18 @@ template __global__ void tma_gemm_kernel<256>(const __grid_constant__ CUtensorMa
 // XT[i][r] = feat[rows[r]][i] for i < 44, zeros for 44 <= i < 48 (K-major B
 // operand of the gW0 GEMM).
 __global__ void wide_gather_xt_kernel(const float* __restrict__ feat, const uint32_t* __restrict__ rows,
-                                      int nb, float* __restrict__ xt, int ldt) {
+                                      int nb, float* __restrict__ xt, int ldt, float* __restrict__ xg) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nb) return;
     const float4* x = reinterpret_cast<const float4*>(feat + (size_t)rows[r] * F);
     float4 v[F / 4];
 #pragma unroll
     for (int q = 0; q < F / 4; ++q) v[q] = __ldg(x + q);  // all 11 loads in flight
+    // gathered rows, K padded to 48 (TMA operand of the first GEMM)
+    float4* g4 = reinterpret_cast<float4*>(xg + (size_t)r * 48);
+#pragma unroll
+    for (int q = 0; q < F / 4; ++q) g4[q] = v[q];
+    g4[F / 4] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int q = 0; q < F / 4; ++q) {
         xt[(size_t)(4 * q) * ldt + r] = v[q].x;
@@ -574,7 +579,7 @@ __global__ void split_reduce_f64_kernel(const double* __restrict__ src, int spli
 // grad/params in serialization order: w0[H][44] b0[H] w1[H][H] b1[H] w2[2][H] b2[2].
 __global__ void wide_update_kernel(float* __restrict__ params, const float* __restrict__ grad,
                                    const double* __restrict__ loss_sum, size_t nb, double lr,
-                                   int hidden, float* __restrict__ w1t, int epoch,
+                                   int hidden, float* __restrict__ w1t, float* __restrict__ w0p, int epoch,
                                    int* __restrict__ diverged, double* __restrict__ epoch_acc,
                                    size_t np) {
     if (*diverged >= 0) return;
@@ -592,12 +597,19 @@ __global__ void wide_update_kernel(float* __restrict__ params, const float* __re
     if (p >= w1_off && p < w1_off + (size_t)hidden * hidden) {
         const size_t t = p - w1_off, k = t / hidden, j = t % hidden;
         w1t[j * hidden + k] = nw;
+    } else if (p < (size_t)hidden * F) {
+        w0p[(p / F) * 48 + p % F] = nw;  // K-padded W0 (first GEMM's B operand)
     }
 }
 
-// W1^T from the flat params (initial copy).
-__global__ void wide_w1t_kernel(const float* __restrict__ params, int hidden, float* __restrict__ w1t) {
+// W1^T and the K-padded W0 [H][48] from the flat params (initial copies).
+__global__ void wide_w1t_kernel(const float* __restrict__ params, int hidden, float* __restrict__ w1t,
+                                float* __restrict__ w0p) {
     const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < (size_t)hidden * 48) {
+        const size_t j = t / 48, i = t % 48;
+        w0p[t] = i < F ? params[j * F + i] : 0.f;
+    }
     if (t >= (size_t)hidden * hidden) return;
     const size_t w1_off = (size_t)hidden * F + hidden, k = t / hidden, j = t % hidden;
     w1t[j * hidden + k] = params[w1_off + t];

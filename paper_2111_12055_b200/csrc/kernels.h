@@ -149,7 +149,7 @@ template <int BN>
 size_t tma_gemm_smem_bytes();
 size_t gemm_smem_bytes();
 __global__ void wide_gather_xt_kernel(const float* feat, const uint32_t* rows, int nb, float* xt,
-                                      int ldt);
+                                      int ldt, float* xg);
 __global__ void wide_head_kernel(WideHeadArgs a);
 __global__ void row_sum_kernel(const float* in, int ld, int ncols, float* out);
 __global__ void wide_w2_partial_kernel(const float* h2, const float* d3, const double* kl, int nb,
@@ -159,9 +159,9 @@ __global__ void split_reduce_f32_kernel(const float* src, int splits, size_t str
 __global__ void split_reduce_f64_kernel(const double* src, int splits, int n, float* dst,
                                         double* loss_out);
 __global__ void wide_update_kernel(float* params, const float* grad, const double* loss_sum,
-                                   size_t nb, double lr, int hidden, float* w1t, int epoch,
+                                   size_t nb, double lr, int hidden, float* w1t, float* w0p, int epoch,
                                    int* diverged, double* epoch_acc, size_t np);
-__global__ void wide_w1t_kernel(const float* params, int hidden, float* w1t);
+__global__ void wide_w1t_kernel(const float* params, int hidden, float* w1t, float* w0p);
 __global__ void wide_gw0_kernel(const float* src, int splits, size_t stride, int hidden, float* dst);
 __global__ void wide_init_kernel(uint64_t seed, int hidden, float* params, size_t np);
 __global__ void wide_probs_kernel(const float* h2, const float* w2, const float* b2, int nb,
