@@ -463,9 +463,10 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
         }
         pair_sync(bar);
         TC_MARK(2);
-        // ---- F3 + B1 (both warps of the pair compute the logits / softmax;
-        //      warp h writes D2 n-tiles 2h, 2h+1, warp 0 writes U)
-        {
+        // ---- F3 + B1 on the pair's first warp (the FP64 softmax is the only
+        //      work here; the partner waits at the pair barrier instead of
+        //      duplicating it on the shared FP64 pipe)
+        if (h == 0) {
             double lg[2];
             lg[0] = tq == 0 ? S.b2[0] : 0.0;
             lg[1] = tq == 0 ? S.b2[1] : 0.0;
@@ -491,13 +492,10 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
             const double loss = a ? to + term : term + to;
             const bool valid = r < nv;
             const double d3 = (valid && tq < 2) ? pa * (lr - loss) * inv_b : 0.0;
-            if (h == 0) {
-                if (tq < 2) S.u[r * SU + tq] = d3;
-                if (tq == 0) S.u[r * SU + 2] = valid ? loss : 0.0;
-            }
+            if (tq < 2) S.u[r * SU + tq] = d3;
+            if (tq == 0) S.u[r * SU + 2] = valid ? loss : 0.0;
 #pragma unroll
-            for (int nn = 0; nn < 2; ++nn) {
-                const int nt = 2 * h + nn;
+            for (int nt = 0; nt < H2 / 8; ++nt) {
                 double dd[2] = {0.0, 0.0};
                 dmma(dd, d3, tq < A ? S.w2[tq * H2 + nt * 8 + gq] : 0.0);
                 const int k = nt * 8 + 2 * tq;
