@@ -388,6 +388,9 @@ def main():
     if dp_note:
         line["dp_fallback"] = "fused peer exchange failed (" + dp_note + "); measured with nccl"
 
+    for v in secondary.get("batch_sweep", {}).values():
+        if v.get("tflops") and fp64_peak:
+            v["roofline_frac"] = v["tflops"] / fp64_peak
     line.update(secondary)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
@@ -400,6 +403,10 @@ def main():
 def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, peaks, local):
     """Full-suite greedy inference over the 1M states + a C5-style aggregation sweep."""
     out = {}
+    # row f1: experience store — fold a synthetic C3-scale tuple log into a fresh
+    # device Q-table (QTable::update x n) + snapshot_policy_dataset (device-resident)
+    out["qtable"] = run_qtable(args, dev, stream, torch, gbx, peaks)
+    torch.cuda.empty_cache()
     n = args.n
     act_d = torch.empty(n, dtype=torch.uint8, device="cuda")
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -424,6 +431,31 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
             "hbm_gbs": rate * 177 / 1e9}
     out["inference"]["fp32_peak_tflops_measured"] = fp32_peak
     out["inference"]["hbm_peak_gbs"] = peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)
+
+    # train regimes beside the headline batch: the reference's default batch 32
+    # (bit-exact 1-CTA kernel, a serial chain of n/32 dependent steps) and a
+    # large batch (sync amortised); same 1M-record log, one epoch each
+    out["batch_sweep"] = {}
+    feat_n = feat_d.shape[0]
+    tgt_n = torch.empty((feat_n, 2), dtype=torch.float64, device="cuda")
+    tgt_n[:, 0] = 0.5
+    tgt_n[:, 1] = 0.5
+    for b in (32, 65536):
+        p_b = params_d.clone()
+        dev.fit_dev(p_b.data_ptr(), feat_d.data_ptr(), tgt_n.data_ptr(), feat_n, args.lr, 1, b, 99,
+                    stream=dev.stream)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        dev.fit_dev(p_b.data_ptr(), feat_d.data_ptr(), tgt_n.data_ptr(), feat_n, args.lr, 1, b, 99,
+                    stream=dev.stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        _, k_ms = dev.last_fit_timing()
+        out["batch_sweep"][str(b)] = {
+            "value": feat_n / (ms * 1e-3), "unit": "samples/s", "ms_per_epoch": ms,
+            "kernel": "train_epoch_kernel (fp64 exact, 1 CTA)" if b <= 32 else "train_epoch_tc_kernel",
+            "tflops": feat_n * 23936 / (k_ms * 1e-3) / 1e12 if k_ms > 0 else None}
 
     # C5-style sweep: inference + aggregation over n_apps x per_app shaders
     s, feat = synthetic_suite(args.c5_apps, args.c5_shaders_per_app)
@@ -473,9 +505,6 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
                        "tf32_peak_tflops": peaks.get("bf16_tflops", 1590.0) / 2,
                        "peak_note": "dense TF32 = half the measured bf16 cuBLAS peak"}
 
-    # row f1: experience store — fold a synthetic C3-scale tuple log into a fresh
-    # device Q-table (QTable::update x n) + snapshot_policy_dataset (device-resident)
-    out["qtable"] = run_qtable(args, dev, stream, torch, gbx, peaks)
     return out
 
 
@@ -514,14 +543,16 @@ def run_qtable(args, dev, stream, torch, gbx, peaks):
 
     once()
     torch.cuda.synchronize()
-    reps = 3
-    ev0.record(stream)
-    for _ in range(reps):
+    times = []
+    for _ in range(5):  # median of 5 (each rep: fresh fold of all n tuples + snapshot)
+        ev0.record(stream)
         rows, states = once()
-    ev1.record(stream)
-    torch.cuda.synchronize()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        times.append(ev0.elapsed_time(ev1))
     qt.close()
-    ms = ev0.elapsed_time(ev1) / reps
+    del keys, act, rew, now, feat, tgt
+    ms = statistics.median(times)
     res = {"value": n / (ms * 1e-3), "unit": "tuples/s (fold + snapshot)", "ms": ms, "tuples": n,
            "states": states, "snapshot_rows": rows,
            "algorithmic_bytes_per_tuple": 137,
