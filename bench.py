@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--c5-apps", type=int, default=10_000)
     ap.add_argument("--qt-tuples", type=int, default=10_000_000,
                     help="experience-store secondary: tuples folded into a fresh device Q-table")
-    ap.add_argument("--c5-shaders-per-app", type=int, default=1_000)
+    ap.add_argument("--c5-shaders-per-app", type=int, default=10_000)
     return ap.parse_args()
 
 
@@ -96,6 +96,43 @@ def synthetic_suite(n_apps: int, per_app: int, seed: int = 5, cap: float = np.in
              slot_shader=np.arange(n_sh, dtype=np.uint32), slot_frac=frac, pipe_wt=wt,
              shader_lat=lat, app_f64=app)
     feat, _ = synthetic_log(n_sh, seed + 1)
+    return s, feat
+
+
+def synthetic_suite_torch(torch, n_apps: int, per_app: int, seed: int = 5, cap: float = float("inf")):
+    """synthetic_suite generated on the device (C5 at its nominal 1e8 scale):
+    same distributions; G1-shaped features."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    dev = "cuda"
+    n_sh = n_apps * per_app
+    lat = torch.rand((n_sh, 3), generator=g, device=dev, dtype=torch.float64)
+    lat[:, 1] *= 1.6
+    lat[:, 2] *= 0.6
+    pipes = torch.randint(2, 5, (n_apps,), generator=g, device=dev)
+    app_pipe_off = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), torch.cumsum(pipes, 0)])
+    npipe = int(app_pipe_off[-1])
+    app_of_pipe = torch.repeat_interleave(torch.arange(n_apps, device=dev), pipes)
+    idx_in_app = torch.arange(npipe, device=dev) - app_pipe_off[app_of_pipe]
+    k = pipes[app_of_pipe]
+    sizes = per_app // k + (idx_in_app < per_app % k).to(torch.int64)
+    pipe_slot_off = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), torch.cumsum(sizes, 0)])
+    frac = torch.rand(n_sh, generator=g, device=dev, dtype=torch.float64) * 0.06 + 0.03
+    tot = torch.segment_reduce(frac, "sum", lengths=sizes)
+    scale = torch.where(tot > 0.85, 0.85 / tot, torch.ones_like(tot))
+    frac *= torch.repeat_interleave(scale, sizes)
+    wt = torch.stack([torch.rand(npipe, generator=g, device=dev, dtype=torch.float64) * 1.5 + 0.5,
+                      (torch.rand(npipe, generator=g, device=dev, dtype=torch.float64) * 6 + 2) * 1e-3], 1)
+    app = torch.stack([torch.ones(n_apps, dtype=torch.float64, device=dev),
+                       torch.full((n_apps,), cap, dtype=torch.float64, device=dev),
+                       torch.full((n_apps,), 0.005, dtype=torch.float64, device=dev),
+                       torch.ones(n_apps, dtype=torch.float64, device=dev)], 1)
+    feat = torch.rand((n_sh, 44), generator=g, device=dev, dtype=torch.float32) * 7.0
+    feat[:, :8] = 0.0
+    stage = torch.randint(0, 8, (n_sh,), generator=g, device=dev)
+    feat[torch.arange(n_sh, device=dev), stage] = 1.0
+    s = dict(app_pipe_off=app_pipe_off, pipe_slot_off=pipe_slot_off,
+             slot_shader=torch.arange(n_sh, dtype=torch.int32, device=dev), slot_frac=frac,
+             pipe_wt=wt, shader_lat=lat, app_f64=app)
     return s, feat
 
 
@@ -457,12 +494,15 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
             "kernel": "train_epoch_kernel (fp64 exact, 1 CTA)" if b <= 32 else "train_epoch_tc_kernel",
             "tflops": feat_n * 23936 / (k_ms * 1e-3) / 1e12 if k_ms > 0 else None}
 
-    # C5-style sweep: inference + aggregation over n_apps x per_app shaders
-    s, feat = synthetic_suite(args.c5_apps, args.c5_shaders_per_app)
-    ds = dev.suite_upload(s, feat)
+    # C5 sweep: inference + aggregation over n_apps x per_app shaders (generated
+    # on the device; the default is the config's 1e8 shader feature vectors)
+    s, feat = synthetic_suite_torch(torch, args.c5_apps, args.c5_shaders_per_app)
+    ds = dev.suite_upload_dev(s, feat)
+    del s, feat
+    torch.cuda.empty_cache()
     params = params_d.cpu().numpy()
     pd = torch.from_numpy(params).cuda()
-    nsh = feat.shape[0]
+    nsh = ds.n_shaders
     a_d = torch.empty(nsh, dtype=torch.uint8, device="cuda")
     rows_d = torch.empty((args.c5_apps, 5), dtype=torch.float64, device="cuda")
     for _ in range(3):
@@ -477,7 +517,8 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
     ms = ev0.elapsed_time(ev1) / reps
     out["aggregation"] = {"value": nsh / (ms * 1e-3), "unit": "shader decisions/s (infer+agg)",
                           "ms": ms, "apps": args.c5_apps, "shaders": nsh,
-                          "bytes_per_shader": 204}
+                          "bytes_per_shader": 204, "hbm_gbs": nsh * 204 / (ms * 1e-3) / 1e9,
+                          "data": "synthetic suite generated on the device (C5: 1e8 shaders)"}
     ds.close()
 
     # C4: wide MLP (44-512-512-2) fit epoch on the tcgen05 TF32 path

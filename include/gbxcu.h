@@ -236,7 +236,8 @@ int gbxcu_aggregate(gbxcu_ctx* ctx, const gbxcu_suite* suite, const uint8_t* sha
 int gbxcu_histogram(gbxcu_ctx* ctx, const double* uplift, size_t n, double* lower_out,
                     uint64_t* count_out, size_t cap, size_t* n_bins);
 
-/* Device-resident suite handle (uploaded once, reused per sweep). */
+/* Device-resident suite handle (uploaded once, reused per sweep). The suite
+ * arrays and features may live in host or device memory (unified addressing). */
 typedef struct gbxcu_dsuite gbxcu_dsuite;
 int gbxcu_suite_upload(gbxcu_ctx* ctx, const gbxcu_suite* host, const float* shader_features,
                        gbxcu_dsuite** out);

@@ -432,16 +432,31 @@ class Device:
     def suite_upload(self, suite: dict, features) -> "DeviceSuite":
         return DeviceSuite(self, suite, features)
 
+    def suite_upload_dev(self, suite: dict, features) -> "DeviceSuite":
+        """Suite whose arrays are torch CUDA tensors (keys as suite_upload)."""
+        return DeviceSuite(self, suite, features, device_arrays=True)
+
 
 class DeviceSuite:
     """A suite resident in HBM (gbxcu_suite_upload)."""
 
-    def __init__(self, dev: Device, suite: dict, features):
+    def __init__(self, dev: Device, suite: dict, features, device_arrays=False):
         self.dev = dev
-        st, keep = suite_struct(suite)
+        if device_arrays:
+            names = ("app_pipe_off", "pipe_slot_off", "slot_shader", "slot_frac", "pipe_wt",
+                     "shader_lat", "app_f64")
+            t = [suite[k].contiguous() for k in names]
+            st = SuiteC(t[0].numel() - 1, t[1].numel() - 1, t[2].numel(), t[5].shape[0],
+                        *(x.data_ptr() for x in t))
+            fptr = features.contiguous().data_ptr()
+        else:
+            st, keep = suite_struct(suite)
+            fptr = _f32(features).ctypes.data
         self.n_apps, self.n_shaders = st.n_apps, st.n_shaders
         h = _vp()
-        dev._ck(dev.L.gbxcu_suite_upload(dev.h, C.byref(st), _f32(features), C.byref(h)))
+        L = dev.L
+        L.gbxcu_suite_upload.argtypes = [_vp, C.POINTER(SuiteC), _vp, C.POINTER(_vp)]
+        dev._ck(L.gbxcu_suite_upload(dev.h, C.byref(st), fptr, C.byref(h)))
         self.h = h
 
     def close(self):

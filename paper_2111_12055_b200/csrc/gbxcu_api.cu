@@ -473,10 +473,11 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     return GBXCU_OK;
 }
 
+// Host or device source (unified addressing decides the copy direction).
 template <typename T>
-int upload(DevBuf& b, const T* host, size_t count, cudaStream_t st) {
+int upload(DevBuf& b, const T* src, size_t count, cudaStream_t st) {
     RET(b.ensure(sizeof(T) * count));
-    if (count) CK(cudaMemcpyAsync(b.p, host, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+    if (count) CK(cudaMemcpyAsync(b.p, src, sizeof(T) * count, cudaMemcpyDefault, st));
     return GBXCU_OK;
 }
 

@@ -307,3 +307,21 @@ def test_fit_peer_set_divergence_agrees(dev, orc):
     rc, p_ref2, _, _ = orc.fit(p0, f2, t2, 0.01, 1, 2048, 3)
     p2, _ = dev.fit(p0, f2, t2, 0.01, 1, 2048, 3, virtual_ranks=4)
     assert ulps32(p2, p_ref2).max() <= 2
+
+
+def test_suite_upload_from_device_memory(dev, orc):
+    """gbxcu_suite_upload accepts device-resident arrays (unified addressing):
+    same evaluate rows as the host upload of the same suite."""
+    import torch
+    s = dict(golden("suite_free"))
+    keys = ("app_pipe_off", "pipe_slot_off", "slot_shader", "slot_frac", "pipe_wt", "shader_lat",
+            "app_f64")
+    ds_h = dev.suite_upload(s, s["features"])
+    rows_h, hist_h, act_h = ds_h.evaluate(s["eval_params"], 10, int(s["eval_seed"]), want_actions=True)
+    t = {k: torch.from_numpy(np.ascontiguousarray(s[k])).cuda() for k in keys}
+    ds_d = dev.suite_upload_dev(t, torch.from_numpy(np.ascontiguousarray(s["features"], np.float32)).cuda())
+    rows_d, hist_d, act_d = ds_d.evaluate(s["eval_params"], 10, int(s["eval_seed"]), want_actions=True)
+    np.testing.assert_array_equal(rows_d, rows_h)
+    np.testing.assert_array_equal(act_d, act_h)
+    ds_h.close()
+    ds_d.close()
