@@ -467,13 +467,19 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
         //      work here; the partner waits at the pair barrier instead of
         //      duplicating it on the shared FP64 pipe)
         if (h == 0) {
-            double lg[2];
+            // two independent accumulator chains (even / odd k-steps), summed
+            double lg[2], lh[2] = {0.0, 0.0};
             lg[0] = tq == 0 ? S.b2[0] : 0.0;
             lg[1] = tq == 0 ? S.b2[1] : 0.0;
             const double* hb = S.h2 + r * SH2 + tq;
 #pragma unroll
-            for (int k0 = 0; k0 < H2; k0 += 4)
+            for (int k0 = 0; k0 < H2; k0 += 8) {
                 dmma(lg, hb[k0], gq < A ? S.w2[gq * H2 + k0 + tq] : 0.0);
+                dmma(lh, hb[k0 + 4], gq < A ? S.w2[gq * H2 + k0 + 4 + tq] : 0.0);
+            }
+            lg[0] += lh[0];
+            lg[1] += lh[1];
+            TC_MARK(11);
             const double l0 = __shfl_sync(0xffffffffu, lg[0], lane & ~3);
             const double l1 = __shfl_sync(0xffffffffu, lg[1], lane & ~3);
             const int a = tq & 1;
@@ -483,7 +489,14 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
             const double d = a ? l1 - l0 : l0 - l1;
             const double z = exp(-fabs(d));
             const double lse = log1p(z);
-            const double pa = (d >= 0.0 ? 1.0 : z) / (1.0 + z);
+            // 1 / (1 + z), 1 <= 1 + z <= 2: hardware reciprocal + Newton steps
+            const double den = 1.0 + z;
+            double rc;
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
+            rc = fma(rc, fma(-den, rc, 1.0), rc);
+            rc = fma(rc, fma(-den, rc, 1.0), rc);
+            rc = fma(rc, fma(-den, rc, 1.0), rc);
+            const double pa = d >= 0.0 ? rc : z * rc;
             const double lpc = pa < 1e-7 ? LN_PMIN : (pa > 1.0 - 1e-7 ? LN_PMAX : fmin(d, 0.0) - lse);
             const double pc = clampp(pa);
             const double lr = lpc - S.ltgt[2 * r + a];
@@ -492,6 +505,7 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
             const double loss = a ? to + term : term + to;
             const bool valid = r < nv;
             const double d3 = (valid && tq < 2) ? pa * (lr - loss) * inv_b : 0.0;
+            TC_MARK(12);
             if (tq < 2) S.u[r * SU + tq] = d3;
             if (tq == 0) S.u[r * SU + 2] = valid ? loss : 0.0;
 #pragma unroll

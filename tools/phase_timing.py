@@ -4,8 +4,8 @@ import paper_2111_12055_b200 as gbx
 lib = gbx.load_library(os.path.abspath("tools/timing/libgbxcu.so"))
 lib.gbxcu_debug_phase_cycles.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 lib.gbxcu_debug_phase_cycles_tc.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-names_tc = ["P0 convert", "F1", "F2", "F3+B1", "B2+G1+scalars", "G0", "tile top (wait+prefetch)",
-            "partial store+flag", "flag wait", "reduce+SGD+publish", "LL all-gather", "", "", "", "", ""]
+names_tc = ["P0 convert", "F1", "F2", "F3 B1 tail", "B2+G1+scalars", "G0", "tile top (wait+prefetch)",
+            "partial store+flag", "flag wait", "reduce+SGD+publish", "LL all-gather", "F3 logits", "F3 softmax", "", "", ""]
 from bench import synthetic_log
 names = ["P0 convert", "F1", "F2", "F3+B1", "B2(+gw1,extras)", "G0", "tile loop top", "wait+prefetch",
          "partials write", "grid barrier 1", "loss+param reduce", "grid barrier 2", "reload", "", "", ""]
