@@ -468,6 +468,18 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
             "hbm_gbs": rate * 177 / 1e9}
     out["inference"]["fp32_peak_tflops_measured"] = fp32_peak
     out["inference"]["hbm_peak_gbs"] = peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)
+    if not args.no_cpu_baseline:
+        import oracle
+        if oracle.ref_available():
+            m = 200_000
+            f_s = feat_d[:m].cpu().numpy()
+            p_s = params_d.cpu().numpy()
+            t0 = time.perf_counter()
+            oracle.Reference().select_greedy(p_s, f_s)
+            dt = time.perf_counter() - t0
+            out["inference"]["cpu_baseline"] = {
+                "value": m / dt, "unit": "decisions/s", "cores": 1, "kind": "reference",
+                "sample": f"select_greedy (PolicyNet::forward, fp64) over {m} states, {dt:.2f} s"}
 
     # train regimes beside the headline batch: the reference's default batch 32
     # (bit-exact 1-CTA kernel, a serial chain of n/32 dependent steps) and a
@@ -520,6 +532,24 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
                           "bytes_per_shader": 204, "hbm_gbs": nsh * 204 / (ms * 1e-3) / 1e9,
                           "data": "synthetic suite generated on the device (C5: 1e8 shaders)"}
     ds.close()
+    if not args.no_cpu_baseline:
+        import oracle
+        if oracle.ref_available():
+            R = oracle.Reference()
+            jobs = os.cpu_count() or 1
+            h = R.suite_generate(benchmark_count=1000, seed=3)
+            dims = np.empty(5, np.uint64)
+            R.lib.gbxref_suite_dims(h, dims)
+            n_slots = int(dims[3])
+            t0 = time.perf_counter()
+            R.evaluate(h, params_d.cpu().numpy(), 10, 77, jobs=jobs)
+            dt = time.perf_counter() - t0
+            R.suite_free(h)
+            out["aggregation"]["cpu_baseline"] = {
+                "value": n_slots / dt, "unit": "shader decisions/s (infer+agg)", "cores": jobs,
+                "kind": "reference",
+                "sample": f"evaluate() on a generated 1000-benchmark suite ({n_slots} slots), "
+                          f"jobs={jobs}, {dt:.2f} s"}
 
     # C4: wide MLP (44-512-512-2) fit epoch on the tcgen05 TF32 path
     H = 512
@@ -592,7 +622,7 @@ def run_qtable(args, dev, stream, torch, gbx, peaks):
         torch.cuda.synchronize()
         times.append(ev0.elapsed_time(ev1))
     qt.close()
-    del keys, act, rew, now, feat, tgt
+    del feat, tgt
     ms = statistics.median(times)
     res = {"value": n / (ms * 1e-3), "unit": "tuples/s (fold + snapshot)", "ms": ms, "tuples": n,
            "states": states, "snapshot_rows": rows,
@@ -612,6 +642,7 @@ def run_qtable(args, dev, stream, torch, gbx, peaks):
                                    "cores": 1, "kind": "reference",
                                    "sample": f"{m} tuples of the same log, QTable::update + "
                                              f"snapshot_policy_dataset, {dt:.1f} s on 1 host core"}
+    del keys, act, rew, now
     return res
 
 
