@@ -551,6 +551,11 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
                 "sample": f"evaluate() on a generated 1000-benchmark suite ({n_slots} slots), "
                           f"jobs={jobs}, {dt:.2f} s"}
 
+    # Algorithm 1 on the device (row f3 wired to A5-A11, f1): iterations of
+    # run_iteration on a generated 44-benchmark suite, reference
+    # TrainConfig defaults (batch 32, 50 epochs), against the reference's run_training
+    out["algorithm1"] = run_algorithm1(args, dev, gbx)
+
     # C4: wide MLP (44-512-512-2) fit epoch on the tcgen05 TF32 path
     H = 512
     n_w = min(n, 262_144)
@@ -577,6 +582,45 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
                        "peak_note": "dense TF32 = half the measured bf16 cuBLAS peak"}
 
     return out
+
+
+def run_algorithm1(args, dev, gbx):
+    import oracle
+    if not oracle.ref_available():
+        return {"unavailable": "compiled reference (the environment) not built"}
+    from paper_2111_12055_b200.tuner import DeviceTuner, TunerConfig
+    R = oracle.Reference()
+    iters, checkins = 3, 50
+    h = R.suite_generate(benchmark_count=44, seed=7)
+    res = {"iterations": iters, "benchmarks": 44}
+    if not args.no_cpu_baseline:
+        t0 = time.perf_counter()
+        o = R.run_training(h, iters, checkins=checkins, seed=5)
+        res["cpu_baseline"] = {"value": iters / (time.perf_counter() - t0), "unit": "iterations/s",
+                               "cores": 1, "kind": "reference",
+                               "sample": f"run_training, {iters} iterations (environment included)"}
+    tuner = DeviceTuner(dev, TunerConfig(num_iterations=iters, checkins_per_iteration=checkins, seed=5))
+    dt = 0.0
+    for i in range(iters):
+        R.suite_advance(h, checkins)
+        s = R.suite_export(h)
+        keys = R.suite_keys(h, len(s["features"]))
+        now = R.suite_checkin(h)
+        t0 = time.perf_counter()
+        log = tuner.run_iteration(i, s, keys, now)
+        dt += time.perf_counter() - t0
+    R.suite_free(h)
+    res.update({"value": iters / dt, "unit": "iterations/s",
+                "slots": int(len(s["slot_shader"])), "table_size": log["table_size"],
+                "note": "device run_iteration (collection, run_benchmark, fold, snapshot, fit, "
+                        "agreement); the environment export per iteration is not timed"})
+    if not args.no_cpu_baseline:
+        t = tuner.table.export()
+        hv = o["has"].astype(bool)
+        res["matches_reference_table"] = bool(
+            np.array_equal(t["keys"], o["keys"]) and np.array_equal(t["has"], o["has"]) and
+            np.array_equal(t["q"][hv], o["q"][hv]))
+    return res
 
 
 def qtable_tuples_torch(torch, n, seed):

@@ -264,6 +264,14 @@ class Reference(_Lib):
         L.gbxref_qtable_fold.restype = C.c_long
         L.gbxref_qtable_fold.argtypes = [C.c_void_p] * 4 + [_sz, C.c_double, C.c_double, C.c_double,
                                                             C.c_void_p, C.c_void_p] + [C.c_void_p] * 7
+        L.gbxref_suite_advance.argtypes = [C.c_void_p, _u64]
+        L.gbxref_suite_checkin.restype = _u64
+        L.gbxref_suite_checkin.argtypes = [C.c_void_p]
+        L.gbxref_suite_keys.argtypes = [C.c_void_p, C.c_void_p]
+        L.gbxref_run_training.restype = C.c_long
+        L.gbxref_run_training.argtypes = ([C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                          C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+                                          C.c_double, C.c_double, C.c_double, _u64] + [C.c_void_p] * 7)
         L.gbxref_suite_generate.restype = C.c_void_p
         L.gbxref_suite_generate.argtypes = [C.c_int] * 5 + [C.c_double] * 3 + [_u64]
         L.gbxref_suite_free.argtypes = [C.c_void_p]
@@ -402,6 +410,34 @@ class Reference(_Lib):
         if not h:
             raise ValueError(self.err())
         return h
+
+    def suite_advance(self, h, checkins: int):
+        self.lib.gbxref_suite_advance(h, checkins)
+
+    def suite_checkin(self, h) -> int:
+        return int(self.lib.gbxref_suite_checkin(h))
+
+    def suite_keys(self, h, n_shaders: int) -> np.ndarray:
+        k = np.empty((n_shaders, 30), np.uint32)
+        self.lib.gbxref_suite_keys(h, k.ctypes.data)
+        return k
+
+    def run_training(self, h, iterations, checkins=50, eps0=0.2, horizon=0, samples=10, alpha=0.3,
+                     omega=1.0, lr=0.01, epochs=50, batch=32, rho0=0.1, rho_decay=0.95,
+                     rho_min=0.01, seed=0) -> dict:
+        """The reference's run_training on a copy of the suite (jobs = 1)."""
+        a = [h, iterations, checkins, eps0, horizon, samples, alpha, omega, lr, epochs, batch, rho0,
+             rho_decay, rho_min, seed]
+        m = self.lib.gbxref_run_training(*a, *([None] * 7))
+        if m < 0:
+            raise ValueError(self.err())
+        out = {"policy": np.empty(5026, np.float32), "logs": np.empty((iterations, 4)),
+               "keys": np.empty((m, 30), np.uint32), "q": np.empty((m, 2)),
+               "t": np.empty((m, 2), np.uint64), "cnt": np.empty((m, 2), np.uint64),
+               "has": np.empty((m, 2), np.uint8)}
+        self.lib.gbxref_run_training(*a, *(out[k].ctypes.data for k in
+                                           ("policy", "logs", "keys", "q", "t", "cnt", "has")))
+        return out
 
     def suite_free(self, h):
         self.lib.gbxref_suite_free(h)

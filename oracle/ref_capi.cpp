@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <optional>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -384,6 +385,74 @@ int gbxref_run_benchmark(const gbxref_suite* h, std::uint32_t bench_id,
     } catch (const std::exception& e) {
         g_err = e.what();
         return 1;
+    }
+}
+
+void gbxref_suite_advance(gbxref_suite* h, std::uint64_t checkins) { h->s->advance_checkins(checkins); }
+std::uint64_t gbxref_suite_checkin(const gbxref_suite* h) { return h->s->checkin(); }
+
+// StateKey of every shader at the current check-in (compile(), simenv.cpp:408-412).
+void gbxref_suite_keys(const gbxref_suite* h, std::uint32_t* keys) {
+    for (std::size_t i = 0; i < h->s->shaders().size(); ++i) {
+        const auto key = h->s->compile(static_cast<std::uint32_t>(i), gbx::kDefaultAction).second;
+        std::memcpy(keys + i * 30, key.values.data(), sizeof(std::uint32_t) * 30);
+    }
+}
+
+// run_training (tuner.cpp:241-264) on a COPY of the suite: `iterations`
+// Algorithm-1 iterations (checkins_per_iteration, epsilon0 / horizon, 10
+// samples per benchmark, QHyperparams{alpha, omega}, TrainConfig{lr, epochs,
+// batch, rho0, rho_decay, rho_min}, seed, jobs = 1). Outputs: the final behavior
+// policy (flat params), logs[iterations][4] = {mean_reward, table_size,
+// distill_loss, agreement_rate}, and the table in key order (two-call
+// protocol: out_keys == nullptr returns the state count).
+long gbxref_run_training(const gbxref_suite* h, int iterations, int checkins, double eps0,
+                         int horizon, int samples, double alpha, double omega, double lr, int epochs,
+                         int batch, double rho0, double rho_decay, double rho_min, std::uint64_t seed,
+                         float* behavior_params, double* logs, std::uint32_t* out_keys,
+                         double* out_q, std::uint64_t* out_t, std::uint64_t* out_cnt,
+                         std::uint8_t* out_has) {
+    try {
+        gbx::TunerConfig cfg;
+        cfg.num_iterations = iterations;
+        cfg.checkins_per_iteration = checkins;
+        cfg.epsilon0 = eps0;
+        cfg.epsilon_horizon = horizon;
+        cfg.samples_per_benchmark = samples;
+        cfg.qtable = gbx::QHyperparams{alpha, omega};
+        cfg.train.learning_rate = lr;
+        cfg.train.epochs = epochs;
+        cfg.train.batch_size = batch;
+        cfg.train.rho0 = rho0;
+        cfg.train.rho_decay = rho_decay;
+        cfg.train.rho_min = rho_min;
+        cfg.seed = seed;
+        cfg.jobs = 1;
+        const auto res = gbx::run_training(*h->s, cfg, std::nullopt);
+        if (!out_keys) return (long)res.table.state_count();
+        net_to_flat(res.policy.net, behavior_params);
+        for (std::size_t i = 0; i < res.logs.size(); ++i) {
+            logs[4 * i] = res.logs[i].mean_reward;
+            logs[4 * i + 1] = (double)res.logs[i].table_size;
+            logs[4 * i + 2] = res.logs[i].distill_loss;
+            logs[4 * i + 3] = res.logs[i].agreement_rate;
+        }
+        std::size_t r = 0;
+        for (const auto& [key, pair] : res.table.entries()) {
+            std::memcpy(out_keys + r * 30, key.values.data(), sizeof(std::uint32_t) * 30);
+            for (int a = 0; a < 2; ++a) {
+                const bool hv = pair[a].has_value();
+                out_has[2 * r + a] = hv ? 1 : 0;
+                out_q[2 * r + a] = hv ? pair[a]->q : 0.0;
+                out_t[2 * r + a] = hv ? pair[a]->last_update_t : 0;
+                out_cnt[2 * r + a] = hv ? pair[a]->update_count : 0;
+            }
+            ++r;
+        }
+        return (long)r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
     }
 }
 
