@@ -191,6 +191,10 @@ int gbxcu_qtable_update_batch_dev(gbxcu_qtable* t, const uint32_t* d_keys, const
                                   const double* d_rewards, const uint64_t* d_now, size_t n,
                                   size_t* bad_index);
 int gbxcu_qtable_size(const gbxcu_qtable* t, size_t* states, size_t* entries);
+/* Replace the table with m states in key order (keys strictly increasing,
+ * else GBXCU_EINVAL) — e.g. a table read by QTable::load (qtable.cpp:188-231). */
+int gbxcu_qtable_import(gbxcu_qtable* t, const uint32_t* keys, const double* q, const uint64_t* ts,
+                        const uint64_t* cnt, const uint8_t* has, size_t m);
 /* Table in key order: keys[m][30], q/ts/cnt/has[m][2] (has: entry recorded). */
 int gbxcu_qtable_export(const gbxcu_qtable* t, uint32_t* keys, double* q, uint64_t* ts,
                         uint64_t* cnt, uint8_t* has);

@@ -95,7 +95,8 @@ EXPORTS = (
     "gbxcu_wide_param_count", "gbxcu_wide_init", "gbxcu_wide_forward", "gbxcu_wide_fit",
     "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_peer_export",
     "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free", "gbxcu_qtable_clear",
-    "gbxcu_qtable_update_batch", "gbxcu_qtable_update_batch_dev", "gbxcu_qtable_size", "gbxcu_qtable_export",
+    "gbxcu_qtable_update_batch", "gbxcu_qtable_update_batch_dev", "gbxcu_qtable_size",
+    "gbxcu_qtable_import", "gbxcu_qtable_export",
     "gbxcu_qtable_snapshot", "gbxcu_qtable_snapshot_dev",
 )
 PEER_HANDLE_BYTES = 64
@@ -146,6 +147,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_qtable_update_batch_dev.argtypes = [_vp, _vp, _vp, _vp, _vp, _sz, C.POINTER(_sz)]
     L.gbxcu_qtable_size.argtypes = [_vp, C.POINTER(_sz), C.POINTER(_sz)]
     L.gbxcu_qtable_export.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+    L.gbxcu_qtable_import.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _sz]
     L.gbxcu_qtable_snapshot.argtypes = [_vp, C.c_double, _vp, _vp, _sz, C.POINTER(_sz)]
     L.gbxcu_qtable_snapshot_dev.argtypes = [_vp, C.c_double, _vp, _vp, _sz, C.POINTER(_sz)]
     L.gbxcu_aggregate.argtypes = [_vp, C.POINTER(SuiteC), _u8p, _u64p, C.c_int, _f64p, _vp]
@@ -495,6 +497,19 @@ class DeviceSuite:
                                                    d_actions, d_rows, stream))
 
 
+def _parse_u64(tok: str, what: str) -> int:
+    if not tok.isdigit() or int(tok) >= 1 << 64:
+        raise ValidationError(f"bad q-table field: {what}")
+    return int(tok)
+
+
+def _parse_f64(tok: str, what: str) -> float:
+    try:
+        return float(tok)
+    except ValueError:
+        raise ValidationError(f"bad q-table field: {what}") from None
+
+
 class DeviceQTable:
     """QTable on the device (proj/include/gbx/qtable.hpp:53-100): batched
     QTable::update (Eq. 5) and snapshot_policy_dataset in key order."""
@@ -567,6 +582,60 @@ class DeviceQTable:
             self.dev._ck(self.L.gbxcu_qtable_export(self.h, *(out[k].ctypes.data for k in
                                                               ("keys", "q", "t", "cnt", "has"))))
         return out
+
+    def import_arrays(self, t: dict):
+        m = len(t["keys"])
+        arrs = [np.ascontiguousarray(t["keys"], np.uint32), np.ascontiguousarray(t["q"], np.float64),
+                np.ascontiguousarray(t["t"], np.uint64), np.ascontiguousarray(t["cnt"], np.uint64),
+                np.ascontiguousarray(t["has"], np.uint8)]
+        self.dev._ck(self.L.gbxcu_qtable_import(self.h, *(a.ctypes.data for a in arrs), m))
+
+    @classmethod
+    def load(cls, dev: "Device", text: str) -> "DeviceQTable":
+        """QTable::load (proj/src/qtable.cpp:188-231): the line-text table
+        (header `gbx-qtable 1 alpha omega`, then `key[30] action q t count`
+        records), parsed with the reference's validation, then placed on the
+        device (ready for snapshot -> fit)."""
+        lines = text.split("\n")
+        head = lines[0].split() if lines and lines[0] else []
+        if not head:
+            raise ValidationError("empty q-table file")
+        if len(head) != 4 or head[0] != "gbx-qtable":
+            raise ValidationError("not a q-table file")
+        if _parse_u64(head[1], "version") != 1:
+            raise ValidationError("unsupported q-table format version")
+        alpha, omega = _parse_f64(head[2], "alpha"), _parse_f64(head[3], "omega")
+        self = cls(dev, alpha, omega)
+        entries = {}
+        for ln, line in enumerate(lines[1:], start=2):
+            if not line:
+                continue
+            tok = line.split(" ")
+            tok = [x for x in tok if x]
+            if len(tok) != KEY_WORDS + 4:
+                raise ValidationError(f"malformed q-table record at line {ln}")
+            key = tuple(_parse_u64(x, "key") & 0xFFFFFFFF for x in tok[:KEY_WORDS])
+            a = _parse_u64(tok[KEY_WORDS], "action")
+            if a not in (0, 1):
+                raise ValidationError(f"bad action index at line {ln}")
+            q = _parse_f64(tok[KEY_WORDS + 1], "q")
+            t = _parse_u64(tok[KEY_WORDS + 2], "last_update_t")
+            n = _parse_u64(tok[KEY_WORDS + 3], "update_count")
+            if n == 0:
+                raise ValidationError("stored entry with zero update count")
+            entries.setdefault(key, [None, None])[a] = (q, t, n)
+        keys = sorted(entries)
+        m = len(keys)
+        arr = {"keys": np.array(keys, np.uint32).reshape(m, KEY_WORDS), "q": np.zeros((m, 2)),
+               "t": np.zeros((m, 2), np.uint64), "cnt": np.zeros((m, 2), np.uint64),
+               "has": np.zeros((m, 2), np.uint8)}
+        for r, k in enumerate(keys):
+            for a, e in enumerate(entries[k]):
+                if e is not None:
+                    arr["q"][r, a], arr["t"][r, a], arr["cnt"][r, a] = e
+                    arr["has"][r, a] = 1
+        self.import_arrays(arr)
+        return self
 
     def snapshot(self, rho: float):
         r = _sz(0)

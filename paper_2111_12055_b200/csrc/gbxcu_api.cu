@@ -991,6 +991,30 @@ int gbxcu_qtable_update_batch_dev(gbxcu_qtable* t, const uint32_t* d_keys, const
     return qtable_update(t, d_keys, d_actions, d_rewards, d_now, n, c->stream, bad_index);
 }
 
+int gbxcu_qtable_import(gbxcu_qtable* t, const uint32_t* keys, const double* q, const uint64_t* ts,
+                        const uint64_t* cnt, const uint8_t* has, size_t m) {
+    if (!t || (m && (!keys || !q || !ts || !cnt || !has))) return fail(GBXCU_EINVAL, "null argument");
+    // the device table is a sorted set: keys strictly increasing (lexicographic)
+    for (size_t r = 1; r < m; ++r) {
+        const uint32_t* a = keys + (r - 1) * QT_KEY_WORDS;
+        const uint32_t* b = keys + r * QT_KEY_WORDS;
+        if (!std::lexicographical_compare(a, a + QT_KEY_WORDS, b, b + QT_KEY_WORDS))
+            return fail(GBXCU_EINVAL, "imported keys must be strictly increasing");
+    }
+    gbxcu_ctx* c = t->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    RET(upload(t->keys, keys, m * QT_KEY_WORDS, st));
+    RET(upload(t->q, q, 2 * m, st));
+    RET(upload(t->t, ts, 2 * m, st));
+    RET(upload(t->cnt, cnt, 2 * m, st));
+    RET(upload(t->has, has, 2 * m, st));
+    CK(cudaStreamSynchronize(st));
+    t->m = m;
+    return GBXCU_OK;
+}
+
 int gbxcu_qtable_export(const gbxcu_qtable* t, uint32_t* keys, double* q, uint64_t* ts, uint64_t* cnt,
                         uint8_t* has) {
     if (!t) return fail(GBXCU_EINVAL, "null table");

@@ -127,3 +127,28 @@ def test_snapshot_feeds_fit_on_device(dev, ref):
     assert r == len(feat_h)
     np.testing.assert_array_equal(d_feat.cpu().numpy(), feat_h)
     np.testing.assert_array_equal(d_tgt.cpu().numpy(), tgt_h)
+
+
+def test_load_text_then_snapshot_matches_reference(dev, ref):
+    """Experience-log load (row f2): the reference's persisted Q-table text
+    (QTable::save format) -> device table -> device snapshot, against the
+    reference's QTable::load + snapshot_policy_dataset."""
+    keys, act, rew, now = tuples(17, 20_000, 3000, wide=True)
+    o = ref.qtable_fold(keys, act, rew, now)
+    h = ["gbx-qtable 1 0.3 1"]
+    for r in range(len(o["keys"])):
+        for a in (0, 1):
+            if o["has"][r, a]:
+                h.append(" ".join(str(int(v)) for v in o["keys"][r]) +
+                         f" {a} {float(o['q'][r, a])!r} {int(o['t'][r, a])} {int(o['cnt'][r, a])}")
+    text = "\n".join(h) + "\n"
+    qt = gbx.DeviceQTable.load(dev, text)
+    check_table(qt.export(), o)
+    feat, tgt = qt.snapshot(0.1)
+    f_ref, t_ref = ref.qtable_snapshot(text, 0.1)            # QTable::load in the reference
+    np.testing.assert_array_equal(feat, f_ref)
+    np.testing.assert_allclose(tgt, t_ref, rtol=1e-15, atol=1e-300)
+    with pytest.raises(gbx.ValidationError):
+        gbx.DeviceQTable.load(dev, "gbx-qtable 2 0.3 1\n")
+    with pytest.raises(gbx.ValidationError):
+        gbx.DeviceQTable.load(dev, "gbx-qtable 1 0.3 1\n1 2 3\n")
