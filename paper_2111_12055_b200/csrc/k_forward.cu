@@ -264,16 +264,21 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
 #pragma unroll 2
         for (int jp = 0; jp < H1 / 2; ++jp) {
             const float4* wr = reinterpret_cast<const float4*>(S.w0 + jp * (2 * F));
+            // two partial chains per z (even / odd inputs): twice the ILP; the
+            // guard's error bound holds for any summation order
             float2 za = make_float2(S.b0[2 * jp], S.b0[2 * jp + 1]), zb = za;
+            float2 za2 = make_float2(0.f, 0.f), zb2 = za2;
 #pragma unroll
             for (int q = 0; q < F / 2; ++q) {
                 const float4 w = wr[q];
                 const float2 w01 = make_float2(w.x, w.y), w23 = make_float2(w.z, w.w);
                 za = __ffma2_rn(w01, make_float2(xa[2 * q], xa[2 * q]), za);
                 zb = __ffma2_rn(w01, make_float2(xb[2 * q], xb[2 * q]), zb);
-                za = __ffma2_rn(w23, make_float2(xa[2 * q + 1], xa[2 * q + 1]), za);
-                zb = __ffma2_rn(w23, make_float2(xb[2 * q + 1], xb[2 * q + 1]), zb);
+                za2 = __ffma2_rn(w23, make_float2(xa[2 * q + 1], xa[2 * q + 1]), za2);
+                zb2 = __ffma2_rn(w23, make_float2(xb[2 * q + 1], xb[2 * q + 1]), zb2);
             }
+            za = make_float2(za.x + za2.x, za.y + za2.y);
+            zb = make_float2(zb.x + zb2.x, zb.y + zb2.y);
             const float hA0 = za.x > 0.f ? za.x : 0.f, hA1 = za.y > 0.f ? za.y : 0.f;
             const float hB0 = zb.x > 0.f ? zb.x : 0.f, hB1 = zb.y > 0.f ? zb.y : 0.f;
             hma = fmaxf(hma, fmaxf(hA0, hA1));
