@@ -325,3 +325,16 @@ def test_suite_upload_from_device_memory(dev, orc):
     np.testing.assert_array_equal(act_d, act_h)
     ds_h.close()
     ds_d.close()
+
+
+@pytest.mark.parametrize("vranks", [2, 5])
+def test_fit_peer_set_multi_epoch_many_tiles(dev, orc, vranks):
+    """Virtual-rank peer set with several tiles per CTA per step and several
+    epochs (tags and counters continue across epoch launches)."""
+    n = 40_003
+    f, t = orc.g1(29, n)
+    p0 = orc.policy_init(3)
+    rc, p_ref, el_ref, _ = orc.fit(p0, f, t, 0.02, 3, 20_000, 12)
+    p, el = dev.fit(p0, f, t, 0.02, 3, 20_000, 12, virtual_ranks=vranks)
+    assert ulps32(p, p_ref).max() <= 2
+    np.testing.assert_allclose(el, el_ref, rtol=1e-12)

@@ -152,3 +152,21 @@ def test_load_text_then_snapshot_matches_reference(dev, ref):
         gbx.DeviceQTable.load(dev, "gbx-qtable 2 0.3 1\n")
     with pytest.raises(gbx.ValidationError):
         gbx.DeviceQTable.load(dev, "gbx-qtable 1 0.3 1\n1 2 3\n")
+
+
+def test_hot_key_long_segment(dev, ref):
+    """One (key, action) updated 200k times in a row: a single long segment
+    folded sequentially (the Eq.-5 chain), plus a handful of cold keys."""
+    n = 200_000
+    keys = np.zeros((n, 30), np.uint32)
+    keys[:, 0] = 3
+    keys[:, 5] = 17
+    keys[::1000, 7] = np.arange(0, n, 1000, dtype=np.uint32) % 5  # a few other keys
+    act = np.zeros(n, np.uint8)
+    act[1::2] = 1
+    rew = np.random.default_rng(2).random(n) + 0.5
+    now = np.arange(n, dtype=np.uint64) // 7
+    o = ref.qtable_fold(keys, act, rew, now, alpha=0.3, omega=0.999)
+    qt = gbx.DeviceQTable(dev, 0.3, 0.999)
+    qt.update_batch(keys, act, rew, now)
+    check_table(qt.export(), o, q_rtol=1e-12)
