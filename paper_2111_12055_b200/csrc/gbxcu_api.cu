@@ -1375,7 +1375,7 @@ int wide_alloc(gbxcu_ctx* c, int H, size_t bmax, int splits4, int splits5, int r
     RET(c->w_w0p.ensure(sizeof(float) * 48 * H));
     RET(c->w_d3.ensure(sizeof(float) * 2 * bmax));
     RET(c->w_kl.ensure(sizeof(double) * bmax));
-    RET(c->w_part.ensure(sizeof(double) * rsplit * (2 * H + 3)));
+    RET(c->w_part.ensure(sizeof(double) * ((bmax + 31) / 32) * (3 * H + 3)));
     RET(c->w_g4.ensure(sizeof(float) * (size_t)splits4 * H * H));
     RET(c->w_g5.ensure(sizeof(float) * (size_t)splits5 * H * 48));
     RET(c->w_loss.ensure(64));
@@ -1421,6 +1421,7 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
         h.inv_b = 1.0 / (double)nb;
         h.kl = c->w_kl.as<double>(); h.d3 = c->w_d3.as<float>();
         h.d2 = c->w_d2.as<float>(); h.d2t = c->w_d2t.as<float>();
+        h.part = c->w_part.as<double>();
         wide_head_kernel<<<(nbr + 31) / 32, 1024, sizeof(float) * 32 * (H + 1), st>>>(h);
         RET(check_launch(c, "wide_head_kernel"));
 
@@ -1451,20 +1452,13 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
         split_reduce_f32_kernel<<<blocks((size_t)H * H), 256, 0, st>>>(
             c->w_g4.as<float>(), splits4, (size_t)H * H, H, H, H, G + o_w1, H);
         RET(check_launch(c, "split_reduce_f32_kernel"));
-        wide_gw0_kernel<<<blocks((size_t)H * F), 256, 0, st>>>(c->w_g5.as<float>(), splits5,
-                                                               (size_t)H * 48, H, G);
+        wide_gw0_kernel<<<blocks((size_t)H * (F + 1)), 256, 0, st>>>(c->w_g5.as<float>(), splits5,
+                                                                     (size_t)H * 48, H, G, G + o_b0);
         RET(check_launch(c, "wide_gw0_kernel"));
-        row_sum_kernel<<<H, 256, 0, st>>>(c->w_d1t.as<float>(), (int)ldt, nbr, G + o_b0);
-        RET(check_launch(c, "row_sum_kernel"));
-        row_sum_kernel<<<H, 256, 0, st>>>(c->w_d2t.as<float>(), (int)ldt, nbr, G + o_b1);
-        RET(check_launch(c, "row_sum_kernel"));
-        wide_w2_partial_kernel<<<dim3((H + 63) / 64, rsplit), 256, 0, st>>>(
-            c->w_h2.as<float>(), c->w_d3.as<float>(), c->w_kl.as<double>(), nbr, H,
-            c->w_part.as<double>());
-        RET(check_launch(c, "wide_w2_partial_kernel"));
-        split_reduce_f64_kernel<<<blocks(2 * H + 3), 256, 0, st>>>(
-            c->w_part.as<double>(), rsplit, 2 * H + 3, G + o_w2, c->w_loss.as<double>());
-        RET(check_launch(c, "split_reduce_f64_kernel"));
+        wide_head_reduce_kernel<<<(3 * H + 3 + 31) / 32, 256, 0, st>>>(
+            c->w_part.as<double>(), (nbr + 31) / 32, H, G + o_w2, G + o_w2 + 2 * H, G + o_b1,
+            c->w_loss.as<double>());
+        RET(check_launch(c, "wide_head_reduce_kernel"));
     } else {
         CK(cudaMemsetAsync(G, 0, sizeof(float) * wide_param_count(H), st));
         CK(cudaMemsetAsync(c->w_loss.p, 0, sizeof(double), st));

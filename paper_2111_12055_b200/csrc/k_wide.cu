@@ -401,8 +401,9 @@ __global__ void wide_gather_xt_kernel(const float* __restrict__ feat, const uint
         xt[(size_t)(4 * q + 2) * ldt + r] = v[q].z;
         xt[(size_t)(4 * q + 3) * ldt + r] = v[q].w;
     }
+    xt[(size_t)F * ldt + r] = 1.f;  // ones row: column 44 of D1^T X is gb0
 #pragma unroll
-    for (int i = F; i < 48; ++i) xt[(size_t)i * ldt + r] = 0.f;
+    for (int i = F + 1; i < 48; ++i) xt[(size_t)i * ldt + r] = 0.f;
 }
 
 // Head: one warp per record, 32 records per block (1024 threads). logits =
@@ -412,6 +413,8 @@ __global__ void wide_gather_xt_kernel(const float* __restrict__ feat, const uint
 // per-record KL and d3 kept for the reductions. Requires hidden <= 1024.
 __global__ void __launch_bounds__(1024) wide_head_kernel(WideHeadArgs a) {
     extern __shared__ float tile[];  // [32 records][hidden + 1]
+    __shared__ float sd3[32][2];
+    __shared__ double skl[32];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int r0 = blockIdx.x * 32, r = r0 + wl, Hd = a.hidden, ts = Hd + 1;
     if (r < a.nb) {
@@ -441,14 +444,47 @@ __global__ void __launch_bounds__(1024) wide_head_kernel(WideHeadArgs a) {
             a.kl[r] = loss;
             a.d3[2 * r] = (float)d30;
             a.d3[2 * r + 1] = (float)d31;
+            sd3[wl][0] = (float)d30;
+            sd3[wl][1] = (float)d31;
+            skl[wl] = loss;
         }
         for (int k = lane; k < Hd; k += 32) {
             const float d = h[k] > 0.f ? (float)(d30 * (double)a.w2[k] + d31 * (double)a.w2[Hd + k]) : 0.f;
             a.d2[(size_t)r * Hd + k] = d;
             tile[wl * ts + k] = d;
         }
+    } else if (lane == 0) {
+        sd3[wl][0] = sd3[wl][1] = 0.f;
+        skl[wl] = 0.0;
     }
     __syncthreads();
+    // block partials (fixed record order): gW2[a][k] = sum d3[r][a] H2[r][k],
+    // gb1[k] = sum D2[r][k]; gb2, KL sums by thread 0
+    const int nr = min(32, a.nb - r0);
+    double* prow = a.part + (size_t)blockIdx.x * (3 * Hd + 3);
+    for (int k = threadIdx.x; k < Hd; k += blockDim.x) {
+        double g0 = 0.0, g1 = 0.0, gb = 0.0;
+        for (int q = 0; q < nr; ++q) {
+            const double hv = a.h2[(size_t)(r0 + q) * Hd + k];
+            g0 += (double)sd3[q][0] * hv;
+            g1 += (double)sd3[q][1] * hv;
+            gb += tile[q * ts + k];
+        }
+        prow[k] = g0;
+        prow[Hd + k] = g1;
+        prow[2 * Hd + k] = gb;
+    }
+    if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0, sl = 0.0;
+        for (int q = 0; q < nr; ++q) {
+            s0 += sd3[q][0];
+            s1 += sd3[q][1];
+            sl += skl[q];
+        }
+        prow[3 * Hd] = s0;
+        prow[3 * Hd + 1] = s1;
+        prow[3 * Hd + 2] = sl;
+    }
     // transposed store: warp wl writes columns k = wl, wl + 32, ...; lane = record
     if (r0 + lane < a.nb)
         for (int k = wl; k < Hd; k += 32) a.d2t[(size_t)k * a.ldt + r0 + lane] = tile[lane * ts + k];
@@ -671,15 +707,52 @@ __global__ void zero_cols_kernel(float* __restrict__ m, int rows, int ld, int c_
     m[(size_t)(t / w) * ld + c_lo + t % w] = 0.f;
 }
 
-// gW0 [H][48] split partials -> flat grad w0 block [H][44].
+// gW0 [H][48] split partials -> flat grad w0 block [H][44]; column 44 (the
+// ones row of X^T) -> gb0.
 __global__ void wide_gw0_kernel(const float* __restrict__ src, int splits, size_t stride, int hidden,
-                                float* __restrict__ dst) {
+                                float* __restrict__ dst, float* __restrict__ gb0) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= hidden * F) return;
-    const int j = t / F, i = t % F;
+    if (t >= hidden * (F + 1)) return;
+    const int j = t / (F + 1), i = t % (F + 1);
     float s = 0.f;
     for (int q = 0; q < splits; ++q) s += src[q * stride + (size_t)j * 48 + i];
-    dst[t] = s;
+    if (i < F) dst[j * F + i] = s;
+    else gb0[j] = s;
+}
+
+// Sum the head's block partials in block order: grid ceil(W/32), block (32
+// columns x 8 block groups), 4 loads in flight per thread.
+__global__ void __launch_bounds__(256) wide_head_reduce_kernel(const double* __restrict__ part, int nblocks,
+                                                               int hidden, float* __restrict__ gw2,
+                                                               float* __restrict__ gb2, float* __restrict__ gb1,
+                                                               double* __restrict__ loss_out) {
+    __shared__ double red[8][32];
+    const int W = 3 * hidden + 3;
+    const int cx = threadIdx.x & 31, gy = threadIdx.x >> 5;
+    const int col = blockIdx.x * 32 + cx;
+    double s = 0.0;
+    if (col < W) {
+        int b = gy;
+        for (; b + 24 < nblocks; b += 32) {
+            double v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = part[(size_t)(b + 8 * j) * W + col];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s += v[j];
+        }
+        for (; b < nblocks; b += 8) s += part[(size_t)b * W + col];
+    }
+    red[gy][cx] = s;
+    __syncthreads();
+    if (gy == 0 && col < W) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t += red[q][cx];
+        if (col < 2 * hidden) gw2[col] = (float)t;
+        else if (col < 3 * hidden) gb1[col - 2 * hidden] = (float)t;
+        else if (col < 3 * hidden + 2) gb2[col - 3 * hidden] = (float)t;
+        else *loss_out = t;
+    }
 }
 
 }  // namespace gbxcu

@@ -142,7 +142,10 @@ struct WideHeadArgs {
     float* d3;              // [nb][2]
     float* d2;              // [nb][hidden]
     float* d2t;             // [hidden][ldt]
+    double* part;           // [blocks][3*hidden + 3]: gW2 rows, gb1, gb2, KL sums of the block
 };
+__global__ void wide_head_reduce_kernel(const double* part, int nblocks, int hidden, float* gw2,
+                                        float* gb2, float* gb1, double* loss_out);
 
 __global__ void tc_gemm_kernel(GemmArgs g);
 template <int BN>
@@ -162,7 +165,8 @@ __global__ void wide_update_kernel(float* params, const float* grad, const doubl
                                    size_t nb, double lr, int hidden, float* w1t, float* w0p, int epoch,
                                    int* diverged, double* epoch_acc, size_t np);
 __global__ void wide_w1t_kernel(const float* params, int hidden, float* w1t, float* w0p);
-__global__ void wide_gw0_kernel(const float* src, int splits, size_t stride, int hidden, float* dst);
+__global__ void wide_gw0_kernel(const float* src, int splits, size_t stride, int hidden, float* dst,
+                                float* gb0);
 __global__ void wide_init_kernel(uint64_t seed, int hidden, float* params, size_t np);
 __global__ void wide_probs_kernel(const float* h2, const float* w2, const float* b2, int nb,
                                   int hidden, double* probs);
