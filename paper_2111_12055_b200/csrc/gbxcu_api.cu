@@ -836,12 +836,15 @@ void gbxcu_qtable_free(gbxcu_qtable* t) { delete t; }
 
 int gbxcu_qtable_clear(gbxcu_qtable* t) {
     if (!t) return fail(GBXCU_EINVAL, "null table");
+    std::lock_guard<std::mutex> lk(t->ctx->mu);
     t->m = 0;  // device buffers are kept for the next fold
     return GBXCU_OK;
 }
 
 int gbxcu_qtable_size(const gbxcu_qtable* t, size_t* states, size_t* entries) {
     if (!t) return fail(GBXCU_EINVAL, "null table");
+    std::lock_guard<std::mutex> lk(t->ctx->mu);
+    CK(cudaSetDevice(t->ctx->device));
     if (states) *states = t->m;
     if (entries) {
         std::vector<uint8_t> h(2 * t->m);
@@ -1018,6 +1021,8 @@ int gbxcu_qtable_import(gbxcu_qtable* t, const uint32_t* keys, const double* q, 
 int gbxcu_qtable_export(const gbxcu_qtable* t, uint32_t* keys, double* q, uint64_t* ts, uint64_t* cnt,
                         uint8_t* has) {
     if (!t) return fail(GBXCU_EINVAL, "null table");
+    std::lock_guard<std::mutex> lk(t->ctx->mu);
+    CK(cudaSetDevice(t->ctx->device));
     const size_t m = t->m;
     if (!m) return GBXCU_OK;
     if (keys) CK(cudaMemcpy(keys, t->keys.p, sizeof(uint32_t) * QT_KEY_WORDS * m, cudaMemcpyDeviceToHost));
