@@ -15,6 +15,7 @@
 #include <mutex>
 #include <string>
 
+#include "gbx/device_qtable.hpp"
 #include "gbx/policy.hpp"
 #include "gbxcu.h"
 
@@ -363,6 +364,105 @@ BehaviorPolicy load_policy(const std::filesystem::path& path) {
     if (!is) throw ValidationError("cannot open policy file: " + path.string());
     std::vector<std::uint8_t> bytes((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
     return deserialize_policy(bytes);
+}
+
+// ------------------------------------------------------------ DeviceQTable
+namespace {
+void check_qt(int rc, std::size_t bad = 0) {
+    if (rc == GBXCU_ECLOCK)
+        throw ClockRegressionError("q_update check-in precedes entry timestamp (tuple " +
+                                   std::to_string(bad) + ")");
+    check(rc);
+}
+}  // namespace
+
+DeviceQTable::DeviceQTable(QHyperparams hp) : hp_(hp) {
+    hp_.validate();
+    check(gbxcu_qtable_create(ctx(), hp.alpha, hp.omega, &h_));
+}
+
+DeviceQTable::~DeviceQTable() { gbxcu_qtable_free(h_); }
+
+std::size_t DeviceQTable::state_count() const {
+    std::size_t m = 0;
+    check(gbxcu_qtable_size(h_, &m, nullptr));
+    return m;
+}
+
+void DeviceQTable::update_batch(std::span<const ExperienceTuple> tuples) {
+    const std::size_t n = tuples.size();
+    std::vector<std::uint32_t> keys(n * kStateKeySize);
+    std::vector<std::uint8_t> act(n);
+    std::vector<double> rew(n);
+    std::vector<std::uint64_t> now(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        std::memcpy(keys.data() + i * kStateKeySize, tuples[i].key.values.data(),
+                    sizeof(std::uint32_t) * kStateKeySize);
+        act[i] = static_cast<std::uint8_t>(action_index(tuples[i].action));
+        rew[i] = tuples[i].reward;
+        now[i] = tuples[i].now;
+    }
+    std::size_t bad = 0;
+    check_qt(gbxcu_qtable_update_batch(h_, keys.data(), act.data(), rew.data(), now.data(), n, &bad),
+             bad);
+}
+
+std::vector<std::pair<ShaderState, EmpiricalPolicy>> DeviceQTable::snapshot_policy_dataset(
+    double rho) const {
+    std::size_t rows = 0;
+    check(gbxcu_qtable_snapshot(h_, rho, nullptr, nullptr, 0, &rows));
+    std::vector<float> f(rows * kFeatureCount);
+    std::vector<double> t(rows * 2);
+    check(gbxcu_qtable_snapshot(h_, rho, f.data(), t.data(), rows, &rows));
+    std::vector<std::pair<ShaderState, EmpiricalPolicy>> out(rows);
+    for (std::size_t r = 0; r < rows; ++r) {
+        std::memcpy(out[r].first.features.data(), f.data() + r * kFeatureCount,
+                    sizeof(float) * kFeatureCount);
+        out[r].second.prob = {t[2 * r], t[2 * r + 1]};
+    }
+    return out;
+}
+
+QTable DeviceQTable::to_host() const {
+    std::size_t m = 0;
+    check(gbxcu_qtable_size(h_, &m, nullptr));
+    std::vector<std::uint32_t> keys(m * kStateKeySize);
+    std::vector<double> q(2 * m);
+    std::vector<std::uint64_t> ts(2 * m), cnt(2 * m);
+    std::vector<std::uint8_t> has(2 * m);
+    check(gbxcu_qtable_export(h_, keys.data(), q.data(), ts.data(), cnt.data(), has.data()));
+    QTable out(hp_);
+    for (std::size_t r = 0; r < m; ++r) {
+        StateKey k;
+        std::memcpy(k.values.data(), keys.data() + r * kStateKeySize, sizeof(std::uint32_t) * kStateKeySize);
+        auto& pair = out.entries_[k];
+        for (int a = 0; a < 2; ++a)
+            if (has[2 * r + a]) pair[a] = QEntry{q[2 * r + a], ts[2 * r + a], cnt[2 * r + a]};
+    }
+    return out;
+}
+
+DeviceQTable DeviceQTable::from_host(const QTable& table) {
+    DeviceQTable d(table.hyperparams());
+    const std::size_t m = table.state_count();
+    std::vector<std::uint32_t> keys(m * kStateKeySize);
+    std::vector<double> q(2 * m, 0.0);
+    std::vector<std::uint64_t> ts(2 * m, 0), cnt(2 * m, 0);
+    std::vector<std::uint8_t> has(2 * m, 0);
+    std::size_t r = 0;
+    for (const auto& [key, pair] : table.entries()) {  // std::map: key order
+        std::memcpy(keys.data() + r * kStateKeySize, key.values.data(), sizeof(std::uint32_t) * kStateKeySize);
+        for (int a = 0; a < 2; ++a)
+            if (pair[a]) {
+                q[2 * r + a] = pair[a]->q;
+                ts[2 * r + a] = pair[a]->last_update_t;
+                cnt[2 * r + a] = pair[a]->update_count;
+                has[2 * r + a] = 1;
+            }
+        ++r;
+    }
+    check(gbxcu_qtable_import(d.h_, keys.data(), q.data(), ts.data(), cnt.data(), has.data(), m));
+    return d;
 }
 
 }  // namespace gbx

@@ -8,6 +8,7 @@
 #include <limits>
 #include <sstream>
 
+#include "gbx/device_qtable.hpp"
 #include "gbx/policy.hpp"
 #include "gbx/qtable.hpp"
 #include "gbx/tuner.hpp"
@@ -22,6 +23,11 @@ void gbxref_batch_kl_gradient(const float* params, const float* feat, const doub
 int gbxref_fit(float* params, const float* feat, const double* tgt, std::size_t n, double lr,
                int epochs, int batch, std::uint64_t seed, double* epoch_loss, int* diverged_epoch);
 long gbxref_qtable_snapshot(const char* text, double rho, float* feat, double* tgt);
+long gbxref_qtable_fold(const std::uint32_t* keys, const std::uint8_t* actions, const double* rewards,
+                        const std::uint64_t* now, std::size_t n, double alpha, double omega,
+                        double rho, long* sizes, long* bad, std::uint32_t* out_keys, double* out_q,
+                        std::uint64_t* out_t, std::uint64_t* out_cnt, std::uint8_t* out_has,
+                        float* feat, double* tgt);
 void* gbxref_suite_generate(int, int, int, int, int, double, double, double, std::uint64_t);
 void gbxref_suite_free(void*);
 void gbxref_suite_dims(const void*, std::size_t* dims);
@@ -203,3 +209,71 @@ TEST_CASE("errors keep the reference's exception types") {
     CHECK_THROWS_AS(net.forward(bad), ValidationError);
     CHECK_THROWS_AS(boltzmann_pair(1.0, 2.0, 0.0), InvalidTemperatureError);
 }
+
+TEST_CASE("DeviceQTable fold + snapshot equal the reference QTable; host round trip") {
+    const std::size_t n = 30000;
+    std::vector<std::uint32_t> keys(n * 30);
+    std::vector<std::uint8_t> act(n);
+    std::vector<double> rew(n);
+    std::vector<std::uint64_t> now(n);
+    std::uint64_t s = 12345;
+    auto next = [&] { s = s * 6364136223846793005ull + 1442695040888963407ull; return s >> 33; };
+    std::vector<ExperienceTuple> tup(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const std::uint64_t k = next() % 4000;  // ~4000 distinct keys
+        for (int w = 0; w < 30; ++w) keys[i * 30 + w] = w == 0 ? k % 8 : (std::uint32_t)((k * (w + 7)) % 97);
+        act[i] = next() & 1;
+        rew[i] = 0.8 + (next() % 1000) / 2500.0;
+        now[i] = i / 50;
+        std::memcpy(tup[i].key.values.data(), keys.data() + i * 30, 120);
+        tup[i].action = act[i] ? Action::Wave64 : Action::Wave32;
+        tup[i].reward = rew[i];
+        tup[i].now = now[i];
+    }
+    long sizes[2], bad = -1;
+    gbxref_qtable_fold(keys.data(), act.data(), rew.data(), now.data(), n, 0.3, 1.0, 0.1, sizes, &bad,
+                       nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    std::vector<std::uint32_t> rk(sizes[0] * 30);
+    std::vector<double> rq(sizes[0] * 2), rt_f(sizes[1] * 2);
+    std::vector<std::uint64_t> rt(sizes[0] * 2), rc(sizes[0] * 2);
+    std::vector<std::uint8_t> rh(sizes[0] * 2);
+    std::vector<float> rf(sizes[1] * kFeatureCount);
+    gbxref_qtable_fold(keys.data(), act.data(), rew.data(), now.data(), n, 0.3, 1.0, 0.1, sizes, &bad,
+                       rk.data(), rq.data(), rt.data(), rc.data(), rh.data(), rf.data(), rt_f.data());
+
+    DeviceQTable dq(QHyperparams{0.3, 1.0});
+    dq.update_batch(tup);
+    CHECK(dq.state_count() == (std::size_t)sizes[0]);
+    const auto snap = dq.snapshot_policy_dataset(0.1);
+    REQUIRE(snap.size() == (std::size_t)sizes[1]);
+    bool feat_ok = true, tgt_ok = true;
+    for (std::size_t r = 0; r < snap.size(); ++r) {
+        feat_ok &= std::memcmp(snap[r].first.features.data(), rf.data() + r * kFeatureCount,
+                               4 * kFeatureCount) == 0;
+        for (int a = 0; a < 2; ++a)
+            tgt_ok &= std::abs(snap[r].second.prob[a] - rt_f[2 * r + a]) <= 1e-15 * rt_f[2 * r + a];
+    }
+    CHECK(feat_ok);
+    CHECK(tgt_ok);
+    // host round trip: to_host -> save -> load -> from_host -> same snapshot
+    const QTable host = dq.to_host();
+    std::ostringstream os;
+    host.save(os);
+    std::istringstream is(os.str());
+    const auto back = DeviceQTable::from_host(QTable::load(is));
+    const auto snap2 = back.snapshot_policy_dataset(0.1);
+    REQUIRE(snap2.size() == snap.size());
+    bool same = true;
+    for (std::size_t r = 0; r < snap.size(); ++r)
+        same &= snap[r].first == snap2[r].first && snap[r].second.prob == snap2[r].second.prob;
+    CHECK(same);
+    // ClockRegressionError: time going backwards for a repeated key
+    std::vector<ExperienceTuple> bad_t(tup.begin(), tup.begin() + 3);
+    bad_t[1] = bad_t[0];
+    bad_t[0].now = 10;
+    bad_t[1].now = 5;
+    DeviceQTable dq2;
+    CHECK_THROWS_AS(dq2.update_batch(bad_t), ClockRegressionError);
+    CHECK(dq2.state_count() == 1);
+}
+
