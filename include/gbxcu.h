@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GBXCU_ABI_VERSION 1
+#define GBXCU_ABI_VERSION 2
 
 #define GBXCU_N_FEATURES 44
 #define GBXCU_N_PARAMS 5026
@@ -123,7 +123,19 @@ typedef struct {
     int max_ctas;         /* 0 = auto (1 CTA per 32 records of the per-rank batch, <= #SMs) */
     int virtual_ranks;    /* 0/1 = off. V in 2..8: run the fused peer-set path with V ranks
                              inside one launch on this GPU (tests of the multi-GPU kernel) */
+    /* Variants the north star names and the reference lacks ("parity unpinned";
+     * restated in oracle/gbx_oracle.c:orc_fit_variant). Zero = the reference. */
+    int loss_mode;        /* GBXCU_LOSS_KL (fit's distillation) | GBXCU_LOSS_TD: regression of
+                             the taken action's output Q(x,a) on the reward, records
+                             tgt[r] = {a (0/1), r}: L = mean (Q(x,a) - r)^2 */
+    int optimizer;        /* GBXCU_OPT_SGD (fit's update) | GBXCU_OPT_ADAM (fp64 moments, owned
+                             by the reducing CTA of each parameter slice) */
+    double adam_beta1, adam_beta2, adam_eps;  /* 0 -> 0.9, 0.999, 1e-8 */
 } gbxcu_train_cfg;
+#define GBXCU_LOSS_KL 0
+#define GBXCU_LOSS_TD 1
+#define GBXCU_OPT_SGD 0
+#define GBXCU_OPT_ADAM 1
 
 /* fit (proj/src/policy.cpp:297-337): seeded in-place Fisher-Yates per epoch
  * (reproduced on the device), minibatch KL loss, analytic gradient, SGD

@@ -98,6 +98,9 @@ class Restatement(_Lib):
         L.orc_boltzmann_pair.argtypes = [C.c_double, C.c_double, C.c_double, _f64p]
         L.orc_partial_gradient.argtypes = [_f32p, _f32p, _f64p, _u64p, _sz, C.c_double, _f64p,
                                            C.POINTER(C.c_double)]
+        L.orc_fit_variant.argtypes = [_f32p, _f32p, _f64p, _sz, C.c_double, C.c_int, C.c_int, _u64,
+                                      C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _f64p,
+                                      C.POINTER(C.c_int)]
         L.orc_log1pf_counts.restype = C.c_float
         L.orc_log1pf_counts.argtypes = [C.c_float]
         L.orc_fnv1a.restype = _u64
@@ -185,6 +188,20 @@ class Restatement(_Lib):
         rc = self.lib.orc_fit_dims(p, d, len(dims) - 1, np.ascontiguousarray(feat, np.float32),
                                    np.ascontiguousarray(tgt, np.float64), feat.shape[0], lr,
                                    epochs, batch, seed, max_steps, el, C.byref(de))
+        return rc, p, el, de.value
+
+    def fit_variant(self, params, feat, tgt, lr=0.01, epochs=1, batch=32, seed=0, loss="kl",
+                    optimizer="sgd", beta1=0.9, beta2=0.999, eps=1e-8):
+        """The TD-regression / Adam variants (parity unpinned by the reference).
+        Returns (rc, params_out, epoch_loss, diverged_epoch)."""
+        p = np.array(params, np.float32, copy=True)
+        el = np.full(max(epochs, 1), np.nan, np.float64)
+        de = C.c_int(-1)
+        rc = self.lib.orc_fit_variant(p, np.ascontiguousarray(feat, np.float32),
+                                      np.ascontiguousarray(tgt, np.float64), feat.shape[0], lr, epochs,
+                                      batch, seed, 1 if loss == "td" else 0,
+                                      1 if optimizer == "adam" else 0, beta1, beta2, eps, el,
+                                      C.byref(de))
         return rc, p, el, de.value
 
     def collect(self, params, feat, seg_off, seg_seed, eps):

@@ -75,7 +75,20 @@ _u64 = C.c_uint64
 
 class TrainCfg(C.Structure):
     _fields_ = [("learning_rate", C.c_double), ("epochs", C.c_int), ("batch_size", C.c_int),
-                ("seed", C.c_uint64), ("max_ctas", C.c_int), ("virtual_ranks", C.c_int)]
+                ("seed", C.c_uint64), ("max_ctas", C.c_int), ("virtual_ranks", C.c_int),
+                ("loss_mode", C.c_int), ("optimizer", C.c_int), ("adam_beta1", C.c_double),
+                ("adam_beta2", C.c_double), ("adam_eps", C.c_double)]
+
+
+LOSSES = {"kl": 0, "td": 1}
+OPTIMIZERS = {"sgd": 0, "adam": 1}
+
+
+def _train_cfg(lr, epochs, batch, seed, max_ctas, virtual_ranks, loss, optimizer, betas, eps):
+    if loss not in LOSSES or optimizer not in OPTIMIZERS:
+        raise ValueError(f"loss in {sorted(LOSSES)}, optimizer in {sorted(OPTIMIZERS)}")
+    return TrainCfg(lr, epochs, batch, seed, max_ctas, virtual_ranks, LOSSES[loss],
+                    OPTIMIZERS[optimizer], betas[0], betas[1], eps)
 
 
 class SuiteC(C.Structure):
@@ -296,15 +309,19 @@ class Device:
         return g
 
     def fit(self, params, feat, tgt, lr=0.01, epochs=50, batch=32, seed=0, max_ctas=0,
-            raise_on_diverge=True, virtual_ranks=0):
+            raise_on_diverge=True, virtual_ranks=0, loss="kl", optimizer="sgd",
+            betas=(0.9, 0.999), eps=1e-8):
         """fit(): returns (params, epoch_loss). Raises TrainingDivergedError like the reference
         (the partially trained params are attached as .params). virtual_ranks > 1 runs the
-        multi-GPU peer-set kernel path with that many ranks inside one launch."""
+        multi-GPU peer-set kernel path with that many ranks inside one launch.
+        loss="td" (tgt rows = (action, reward); L = mean (Q(x,a) - r)^2) and
+        optimizer="adam" are the north star's variants, absent from the reference."""
         p = np.array(params, np.float32, copy=True)
         feat = _f32(feat).reshape(-1, N_FEATURES)
         el = np.full(max(epochs, 1), np.nan, np.float64)
         de = C.c_int(-1)
-        cfg = TrainCfg(lr, epochs, batch, seed, max_ctas, virtual_ranks)
+        cfg = _train_cfg(lr, epochs, batch, seed, max_ctas, virtual_ranks, loss, optimizer, betas,
+                         eps)
         rc = self.L.gbxcu_fit(self.h, p, feat, _f64(tgt), feat.shape[0], C.byref(cfg),
                               el.ctypes.data, C.byref(de))
         if rc == EDIVERGED and not raise_on_diverge:
@@ -329,10 +346,12 @@ class Device:
                                           stream))
 
     def fit_dev(self, d_params: int, d_feat: int, d_tgt: int, n: int, lr=0.01, epochs=1,
-                batch=32, seed=0, max_ctas=0, stream: int | None = None, virtual_ranks=0):
+                batch=32, seed=0, max_ctas=0, stream: int | None = None, virtual_ranks=0,
+                loss="kl", optimizer="sgd", betas=(0.9, 0.999), eps=1e-8):
         el = np.full(max(epochs, 1), np.nan, np.float64)
         de = C.c_int(-1)
-        cfg = TrainCfg(lr, epochs, batch, seed, max_ctas, virtual_ranks)
+        cfg = _train_cfg(lr, epochs, batch, seed, max_ctas, virtual_ranks, loss, optimizer, betas,
+                         eps)
         rc = self.L.gbxcu_fit_dev(self.h, d_params, d_feat, d_tgt, n, C.byref(cfg),
                                   el.ctypes.data, C.byref(de), stream)
         self._ck(rc, de.value)

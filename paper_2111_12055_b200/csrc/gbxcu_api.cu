@@ -93,6 +93,7 @@ struct gbxcu_ctx {
     // scratch
     DevBuf params, feat, tgt, probs, actions, recheck, counters, flags;
     DevBuf order, order2, partials, red, bar, diverged, epoch_loss, epoch_acc, status;
+    DevBuf adam_m, adam_v;  // Adam moments of the fused path (fp64, one per parameter)
     // multi-CTA epoch kernel: exchange regions (counter | LL words | partials)
     // of the peer set. Real peer set: xchg[0] is this rank's (exported),
     // peer_ptr[r] the opened regions of the others. Virtual ranks (single-GPU
@@ -233,6 +234,15 @@ int validate_cfg(const gbxcu_train_cfg* cfg, size_t n) {
     if (cfg->batch_size < 1) return fail(GBXCU_EINVAL, "batch size must be >= 1");
     if (n == 0) return fail(GBXCU_EINVAL, "fit requires a non-empty dataset");
     if (n > 0x7FFFFFFFull) return fail(GBXCU_EINVAL, "dataset too large (> 2^31 records)");
+    if (cfg->loss_mode != GBXCU_LOSS_KL && cfg->loss_mode != GBXCU_LOSS_TD)
+        return fail(GBXCU_EINVAL, "unknown loss mode");
+    if (cfg->optimizer != GBXCU_OPT_SGD && cfg->optimizer != GBXCU_OPT_ADAM)
+        return fail(GBXCU_EINVAL, "unknown optimizer");
+    if (cfg->optimizer == GBXCU_OPT_ADAM) {
+        const double b1 = cfg->adam_beta1, b2 = cfg->adam_beta2, ep = cfg->adam_eps;
+        if (!(b1 >= 0.0 && b1 < 1.0) || !(b2 >= 0.0 && b2 < 1.0) || !(ep >= 0.0))
+            return fail(GBXCU_EINVAL, "Adam needs 0 <= beta < 1 and eps >= 0 (0 = default)");
+    }
     return GBXCU_OK;
 }
 
@@ -337,6 +347,12 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     const size_t per_cta = ((std::min<size_t>((size_t)cfg->batch_size, n) + eff_ranks - 1) /
                                 eff_ranks + G - 1) / G;
     const int mt = per_cta <= 32 ? 4 : 7;
+    // the variants (TD loss, Adam) run on the fused tensor-core kernel at every
+    // grid size; the bit-exact 1-CTA kernel and the NCCL path are the reference's
+    const bool variant = cfg->loss_mode != GBXCU_LOSS_KL || cfg->optimizer != GBXCU_OPT_SGD;
+    if (variant && c->comm)
+        return fail(GBXCU_EINVAL, "TD loss / Adam need the fused path (no NCCL communicator)");
+    const bool fused = !c->comm && (G > 1 || variant);
     if (vranks > MAX_PEERS || vranks * G > c->num_sms)
         return fail(GBXCU_EINVAL, "virtual ranks x CTAs exceed the GPU");
     if (vranks > 1 && G == 1) return fail(GBXCU_EINVAL, "virtual ranks need multi-CTA steps");
@@ -381,6 +397,19 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     }
     const int GG = R * G;
     const long n_steps = (long)((n + cfg->batch_size - 1) / cfg->batch_size);
+    a.loss_mode = cfg->loss_mode;
+    a.optimizer = cfg->optimizer;
+    a.beta1 = cfg->adam_beta1 > 0.0 ? cfg->adam_beta1 : 0.9;
+    a.beta2 = cfg->adam_beta2 > 0.0 ? cfg->adam_beta2 : 0.999;
+    a.adam_eps = cfg->adam_eps > 0.0 ? cfg->adam_eps : 1e-8;
+    if (cfg->optimizer == GBXCU_OPT_ADAM) {  // fresh moments per fit (t counts the fit's steps)
+        RET(c->adam_m.ensure(sizeof(double) * NP));
+        RET(c->adam_v.ensure(sizeof(double) * NP));
+        CK(cudaMemsetAsync(c->adam_m.p, 0, sizeof(double) * NP, st));
+        CK(cudaMemsetAsync(c->adam_v.p, 0, sizeof(double) * NP, st));
+        a.adam_m = c->adam_m.as<double>();
+        a.adam_v = c->adam_v.as<double>();
+    }
 
     const bool timed = cfg->epochs <= 8;  // per-kernel event timing (bench / profiling)
     for (int e = 0; e < cfg->epochs; ++e) {
@@ -390,10 +419,11 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
         a.epoch = e;
         a.tag_base = c->tag_next + (unsigned int)((long)e * n_steps);
         a.ctr_base = c->ctr_base[0] + (unsigned long long)e * n_steps * GG;
+        a.step0 = (unsigned)((long)e * n_steps);
         if (!c->comm) {
             void* args[] = {&a};
             if (timed) CK(cudaEventRecord(c->ev[(2 * e + 1) % 16], st));
-            if (G == 1) {
+            if (!fused) {
                 // 1-CTA steps: the bit-exact fp64 kernel (reference summation order)
                 const void* fn = tb == 32 ? (const void*)train_epoch_kernel<32>
                                           : (const void*)train_epoch_kernel<64>;
@@ -441,7 +471,7 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     int dv = -1, wd = 0;
     CK(cudaMemcpyAsync(&dv, c->diverged.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&wd, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    const bool used_tc = !c->comm && G > 1;
+    const bool used_tc = fused;
     if (used_tc) {  // resynchronise the monotonic counters (divergence stops early)
         for (int r = 0; r < (c->peers > 1 ? 1 : vranks); ++r)
             CK(cudaMemcpyAsync(&c->ctr_base[r], c->xchg[r].p, sizeof(unsigned long long),
@@ -1483,6 +1513,8 @@ int wide_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, c
                     int* diverged_epoch, cudaStream_t st) {
     RET(check_hidden(H));
     RET(validate_cfg(cfg, n));
+    if (cfg->loss_mode != GBXCU_LOSS_KL || cfg->optimizer != GBXCU_OPT_SGD)
+        return fail(GBXCU_EINVAL, "the wide MLP trains with the reference's KL + SGD only");
     RET(setup_kernel_attrs());
     RET(prepare_order(c, n, st));
     const size_t b = std::min<size_t>((size_t)cfg->batch_size, n);

@@ -376,7 +376,7 @@ __device__ void tc_init_consts(TcSmem<MT>& S) {
 // log-targets ln(t^_a) the KL term needs. Caller: cp.async complete + barrier
 // before, barrier after.
 template <int MT>
-__device__ void tc_stage_in(TcSmem<MT>& S, int slot, int t0 = 0) {
+__device__ void tc_stage_in(TcSmem<MT>& S, int slot, int loss_mode, int t0 = 0) {
     constexpr int TB = 8 * MT;
     const int tid = threadIdx.x;
     for (int t = tid - t0; t < TB * F; t += NT - t0) {
@@ -385,7 +385,8 @@ __device__ void tc_stage_in(TcSmem<MT>& S, int slot, int t0 = 0) {
     }
     if (tid >= NT - 2 * TB) {
         const int q = tid - (NT - 2 * TB);
-        S.ltgt[q] = log(clampp(S.stage_t[slot][q]));
+        // KL: ln(clamp(target)); TD: the raw (action, reward) record
+        S.ltgt[q] = loss_mode == 1 ? S.stage_t[slot][q] : log(clampp(S.stage_t[slot][q]));
     }
 }
 
@@ -403,7 +404,7 @@ __device__ __forceinline__ void pair_sync(int id) {
 // then one CTA barrier and the gradient phase over all records (all warps):
 //   G1 (+ gb1 via H1's ones column), E, G0 (+ gb0 via X's ones column).
 template <int MT>
-__device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
+__device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b, int loss_mode) {
     constexpr int TB = 8 * MT;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int gq = lane >> 2, tq = lane & 3;
@@ -483,28 +484,37 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b) {
             const double l0 = __shfl_sync(0xffffffffu, lg[0], lane & ~3);
             const double l1 = __shfl_sync(0xffffffffu, lg[1], lane & ~3);
             const int a = tq & 1;
-            // log-softmax form: with d = l_a - l_other, z = exp(-|d|),
-            //   p_a = (d >= 0 ? 1 : z) / (1 + z),  ln p_a = min(d, 0) - log1p(z)
-            // (equal to the reference's exp / sum / log(p/t) up to fp64 rounding)
-            const double d = a ? l1 - l0 : l0 - l1;
-            const double z = exp(-fabs(d));
-            const double lse = log1p(z);
-            // 1 / (1 + z), 1 <= 1 + z <= 2: hardware reciprocal + Newton steps
-            const double den = 1.0 + z;
-            double rc;
-            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
-            rc = fma(rc, fma(-den, rc, 1.0), rc);
-            rc = fma(rc, fma(-den, rc, 1.0), rc);
-            rc = fma(rc, fma(-den, rc, 1.0), rc);
-            const double pa = d >= 0.0 ? rc : z * rc;
-            const double lpc = pa < 1e-7 ? LN_PMIN : (pa > 1.0 - 1e-7 ? LN_PMAX : fmin(d, 0.0) - lse);
-            const double pc = clampp(pa);
-            const double lr = lpc - S.ltgt[2 * r + a];
-            const double term = pc * lr;
-            const double to = __shfl_xor_sync(0xffffffffu, term, 1);
-            const double loss = a ? to + term : term + to;
             const bool valid = r < nv;
-            const double d3 = (valid && tq < 2) ? pa * (lr - loss) * inv_b : 0.0;
+            double loss, d3;
+            if (loss_mode == 1) {
+                // TD / reward regression: Q = the raw outputs, record (act, reward)
+                const int act = S.ltgt[2 * r] != 0.0 ? 1 : 0;
+                const double err = (act ? l1 : l0) - S.ltgt[2 * r + 1];
+                loss = err * err;
+                d3 = (valid && tq == act) ? 2.0 * err * inv_b : 0.0;
+            } else {
+                // log-softmax form: with d = l_a - l_other, z = exp(-|d|),
+                //   p_a = (d >= 0 ? 1 : z) / (1 + z),  ln p_a = min(d, 0) - log1p(z)
+                // (equal to the reference's exp / sum / log(p/t) up to fp64 rounding)
+                const double d = a ? l1 - l0 : l0 - l1;
+                const double z = exp(-fabs(d));
+                const double lse = log1p(z);
+                // 1 / (1 + z), 1 <= 1 + z <= 2: hardware reciprocal + Newton steps
+                const double den = 1.0 + z;
+                double rc;
+                asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
+                rc = fma(rc, fma(-den, rc, 1.0), rc);
+                rc = fma(rc, fma(-den, rc, 1.0), rc);
+                rc = fma(rc, fma(-den, rc, 1.0), rc);
+                const double pa = d >= 0.0 ? rc : z * rc;
+                const double lpc = pa < 1e-7 ? LN_PMIN : (pa > 1.0 - 1e-7 ? LN_PMAX : fmin(d, 0.0) - lse);
+                const double pc = clampp(pa);
+                const double lr = lpc - S.ltgt[2 * r + a];
+                const double term = pc * lr;
+                const double to = __shfl_xor_sync(0xffffffffu, term, 1);
+                loss = a ? to + term : term + to;
+                d3 = (valid && tq < 2) ? pa * (lr - loss) * inv_b : 0.0;
+            }
             TC_MARK(12);
             if (tq < 2) S.u[r * SU + tq] = d3;
             if (tq == 0) S.u[r * SU + 2] = valid ? loss : 0.0;
@@ -696,7 +706,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
-    if (h1) tc_stage_in(S, 0);
+    if (h1) tc_stage_in(S, 0, a.loss_mode);
     // shift: c1 <- tile 1, c2 <- tile 2
     h1 = h2; s1 = s2; r1 = r2; n1 = n2;
     s2 = s1; r2 = r1;
@@ -724,12 +734,12 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
             h1 = h2; s1 = s2; r1 = r2; n1 = n2;
             if (h2) h2 = tc_next<TB>(a, who, n_steps, s2, r2, n2);
             TC_MARK(6);
-            tc_tile<MT>(S, g, nv, inv_b);
+            tc_tile<MT>(S, g, nv, inv_b, a.loss_mode);
             if (more && r0 + TB < hi) {
                 // the next tile belongs to this step: stage it now
                 cp_async_wait_all();
                 __syncthreads();
-                tc_stage_in(S, (k + 1) & 1);
+                tc_stage_in(S, (k + 1) & 1, a.loss_mode);
                 TC_MARK(0);
             } else {
                 stage_due = more;  // staged after this step's partial is published
@@ -759,7 +769,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
                 }
             }
         } else if (stage_due && tid >= 32) {
-            tc_stage_in(S, k & 1, 32);
+            tc_stage_in(S, k & 1, a.loss_mode, 32);
         }
         stage_due = false;
         __syncthreads();
@@ -814,7 +824,21 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
                 const int e2 = e0 + tid;
                 if (e2 >= 1 && e2 < n_elem) {
                     const int p = p_lo + e2 - 1;
-                    const float nw = __double2float_rn(get_param(S, p) - a.lr * S.red[NT + tid]);
+                    const double gsum = S.red[NT + tid];
+                    double upd;
+                    if (a.optimizer == 1) {
+                        // Adam: this CTA owns the moments of its slice across steps
+                        const double m = a.beta1 * a.adam_m[p] + (1.0 - a.beta1) * gsum;
+                        const double v = a.beta2 * a.adam_v[p] + (1.0 - a.beta2) * gsum * gsum;
+                        a.adam_m[p] = m;
+                        a.adam_v[p] = v;
+                        const double t = (double)(a.step0 + (unsigned)step + 1u);
+                        const double mh = m / (1.0 - pow(a.beta1, t)), vh = v / (1.0 - pow(a.beta2, t));
+                        upd = a.lr * mh / (sqrt(vh) + a.adam_eps);
+                    } else {
+                        upd = a.lr * gsum;
+                    }
+                    const float nw = __double2float_rn(get_param(S, p) - upd);
                     const unsigned long long word =
                         ((unsigned long long)tag << 32) | __float_as_uint(nw);
                     for (int r = 0; r < R; ++r) st_relaxed_u64<SYS>(a.llp[r] + p, word);
@@ -873,11 +897,11 @@ __global__ void __launch_bounds__(NT, 1) train_partial_tc_kernel(TrainArgs a, lo
         const int nv = (int)min((uint32_t)TB, hi - r0);
         cp_async_wait_all();
         __syncthreads();
-        tc_stage_in(S, buf);
+        tc_stage_in(S, buf, a.loss_mode);
         __syncthreads();
         buf ^= 1;
         if (r0 + TB < hi) tc_prefetch<MT>(S, buf, a, r0 + TB, (int)min((uint32_t)TB, hi - r0 - TB));
-        tc_tile<MT>(S, g, nv, inv_b);
+        tc_tile<MT>(S, g, nv, inv_b, a.loss_mode);
     }
     tc_store_partial(g, a.partials + (size_t)blockIdx.x * PSTR);
 }

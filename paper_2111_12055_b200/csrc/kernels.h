@@ -44,6 +44,13 @@ struct TrainArgs {
     double* part[MAX_PEERS];                 // per-CTA partial rows [G][PSTR]
     unsigned int tag_base;                   // steps taken on this peer set before the epoch
     unsigned long long ctr_base;             // counter value before the epoch's first step
+    // variants (0 = the reference's KL + SGD)
+    int loss_mode;                           // 1: TD / reward regression of Q(x, a)
+    int optimizer;                           // 1: Adam
+    double beta1, beta2, adam_eps;
+    double* adam_m;                          // [NP] first moments (slice-owned)
+    double* adam_v;                          // [NP] second moments
+    unsigned int step0;                      // optimizer steps taken before this epoch
     int* status;                             // watchdog: 1 = a peer wait timed out
 };
 

@@ -44,7 +44,7 @@ def test_sm100a_only_cubin():
 
 
 def test_abi_version(lib):
-    assert lib.gbxcu_abi_version() == 1
+    assert lib.gbxcu_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_gpu(lib):
