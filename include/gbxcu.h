@@ -76,6 +76,10 @@ uint64_t gbxcu_launch_count(const gbxcu_ctx* ctx);
  * fit with <= 8 epochs: epoch-permutation replay and train_epoch kernel,
  * summed over epochs (0 for the data-parallel path). */
 int gbxcu_last_fit_timing(const gbxcu_ctx* ctx, double* shuffle_ms, double* train_kernel_ms);
+/* States the last FAST-mode gbxcu_forward[_dev] on this context sent to the
+ * exact fp64 re-check (guard margin inside the fp32 error bound). Synchronises
+ * the device. */
+int gbxcu_last_recheck_count(gbxcu_ctx* ctx, uint64_t* count);
 
 /* ------------------------------------------------------------------- init */
 /* PolicyNet::init (proj/src/policy.cpp:128-139) computed on the device:

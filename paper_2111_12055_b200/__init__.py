@@ -106,7 +106,7 @@ EXPORTS = (
     "gbxcu_comm_destroy", "gbxcu_aggregate", "gbxcu_histogram", "gbxcu_suite_upload",
     "gbxcu_suite_free", "gbxcu_suite_features", "gbxcu_evaluate", "gbxcu_evaluate_dev",
     "gbxcu_wide_param_count", "gbxcu_wide_init", "gbxcu_wide_forward", "gbxcu_wide_fit",
-    "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_peer_export",
+    "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_last_recheck_count", "gbxcu_peer_export",
     "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free", "gbxcu_qtable_clear",
     "gbxcu_qtable_update_batch", "gbxcu_qtable_update_batch_dev", "gbxcu_qtable_size",
     "gbxcu_qtable_import", "gbxcu_qtable_export",
@@ -183,6 +183,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                      C.POINTER(C.c_int), _vp]
     L.gbxcu_tf32_gemm.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _f32p, _f32p, _f32p]
     L.gbxcu_last_fit_timing.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.gbxcu_last_recheck_count.argtypes = [_vp, C.POINTER(C.c_uint64)]
     _LIB = L
     return L
 
@@ -266,6 +267,12 @@ class Device:
         a, b = C.c_double(), C.c_double()
         self._ck(self.L.gbxcu_last_fit_timing(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def last_recheck_count(self) -> int:
+        """States of the last FAST forward re-checked on the exact fp64 path."""
+        v = C.c_uint64()
+        self._ck(self.L.gbxcu_last_recheck_count(self.h, C.byref(v)))
+        return v.value
 
     # ------------------------------------------------------------ policy
     def policy_init(self, seed: int) -> np.ndarray:

@@ -154,6 +154,7 @@ int setup_kernel_attrs() {
         };
         set((const void*)fwd_fast_kernel, fast_smem_bytes());
         set((const void*)fwd_exact_kernel, exact_smem_bytes());
+        set((const void*)fwd_recheck_kernel, recheck_smem_bytes());
         set((const void*)train_epoch_kernel<32>, train_smem_bytes(32));
         set((const void*)train_epoch_kernel<64>, train_smem_bytes(64));
         set((const void*)train_partial_kernel<32>, train_smem_bytes(32));
@@ -203,10 +204,11 @@ int run_forward(gbxcu_ctx* c, const float* d_params, const float* d_feat, size_t
             d_params, d_feat, n, d_probs, d_actions, d_seg_off, nseg, d_seg_seed, eps,
             recheck.as<uint32_t>(), counters.as<unsigned int>(), flags.as<unsigned int>(), bits);
         RET(check_launch(c, "fwd_fast_kernel"));
-        fwd_exact_kernel<<<c->num_sms * 2, EXACT_BLOCK, exact_smem_bytes(), st>>>(
-            d_params, d_feat, n, recheck.as<uint32_t>(), counters.as<unsigned int>(), d_probs,
-            d_actions, d_seg_off, nseg, d_seg_seed, eps, flags.as<unsigned int>(), bits);
-        RET(check_launch(c, "fwd_exact_kernel(recheck)"));
+        // the list length stays on the device: a fixed grid, idle blocks exit at once
+        fwd_recheck_kernel<<<c->num_sms * 2, RECHECK_BLOCK, recheck_smem_bytes(), st>>>(
+            d_params, d_feat, recheck.as<uint32_t>(), counters.as<unsigned int>(), d_probs,
+            d_actions, d_seg_off, nseg, d_seg_seed, eps, bits);
+        RET(check_launch(c, "fwd_recheck_kernel"));
     } else {
         const size_t blocks_needed = (n + EXACT_BLOCK - 1) / EXACT_BLOCK;
         const int grid = (int)std::min<size_t>(blocks_needed, (size_t)c->num_sms * 8);
@@ -581,6 +583,19 @@ int gbxcu_last_fit_timing(const gbxcu_ctx* c, double* shuffle_ms, double* train_
     if (!c) return fail(GBXCU_EINVAL, "null context");
     if (shuffle_ms) *shuffle_ms = c->last_shuffle_ms;
     if (train_kernel_ms) *train_kernel_ms = c->last_train_ms;
+    return GBXCU_OK;
+}
+
+int gbxcu_last_recheck_count(gbxcu_ctx* c, uint64_t* count) {
+    if (!c || !count) return fail(GBXCU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    unsigned int v = 0;
+    if (c->counters.p) {
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(&v, c->counters.p, sizeof(v), cudaMemcpyDeviceToHost));
+    }
+    *count = v;
     return GBXCU_OK;
 }
 

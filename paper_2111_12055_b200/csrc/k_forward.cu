@@ -40,6 +40,25 @@ __global__ void policy_init_kernel(uint64_t seed, float* __restrict__ params) {
     params[t] = __double2float_rn(__dmul_rn(u, bound));
 }
 
+// Stage the 5,026 fp32 parameters into shared memory with ONE memory round
+// trip (16-B cp.async chunks, all in flight at once); each kernel then builds
+// its own layout from the staged copy. (A strided per-element loop costs one
+// L2 round trip per iteration: ~20 of them, ~15 us, at every launch.)
+__device__ void stage_params(float* raw, const float* __restrict__ p) {
+    if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+        for (int c = threadIdx.x; c < NP / 4; c += blockDim.x) {
+            const unsigned d = (unsigned)__cvta_generic_to_shared(raw + 4 * c);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(p + 4 * c) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        for (int t = (NP / 4) * 4 + threadIdx.x; t < NP; t += blockDim.x) raw[t] = __ldg(p + t);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+    } else {
+        for (int t = threadIdx.x; t < NP; t += blockDim.x) raw[t] = __ldg(p + t);
+    }
+    __syncthreads();
+}
+
 // --------------------------------------------------------------- fast path
 constexpr int FAST_ROWS = 64;  // states per warp per iteration (two per lane)
 // Weights are laid out for packed FFMA2 (two fp32 FMAs per instruction, each
@@ -59,43 +78,53 @@ struct FastSmem {
 };
 static_assert(offsetof(FastSmem, w0) % 16 == 0 && offsetof(FastSmem, w1t) % 16 == 0, "align");
 
-// Per-net constants of the guard: R_l = max_row ||w_row||_1, B_l = max |b|.
-// Computed in fp64 and rounded up so the fp32 bound stays an upper bound.
-__device__ void load_fast_weights(FastSmem& S, const float* __restrict__ p) {
+// Per-net constants of the guard: R_l = max_row ||w_row||_1, B_l = max |b|,
+// Rd = ||w2[1] - w2[0]||_1. Computed in fp64 and rounded up so the fp32 bound
+// stays an upper bound. `raw` = the staged parameters (S.xs, free until the
+// first feature tile is staged).
+__device__ void load_fast_weights(FastSmem& S, float* raw, const float* __restrict__ p) {
+    stage_params(raw, p);
     for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) {
-        const int j = t / F, i = t - j * F;  // coalesced read of w0[j][i]
-        S.w0[(j >> 1) * (2 * F) + 2 * i + (j & 1)] = p[OFF_W0 + t];
+        const int j = t / F, i = t - j * F;
+        S.w0[(j >> 1) * (2 * F) + 2 * i + (j & 1)] = raw[OFF_W0 + t];
     }
     for (int t = threadIdx.x; t < H1 * H2; t += blockDim.x) {
-        const int k = t / H1, j = t % H1;  // coalesced read of w1[k][j]
-        S.w1t[j * H2 + k] = p[OFF_W1 + t];
+        const int k = t / H1, j = t % H1;
+        S.w1t[j * H2 + k] = raw[OFF_W1 + t];
     }
-    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[(t % H2) * A + t / H2] = p[OFF_W2 + t];
-    for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = p[OFF_B0 + t];
-    for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = p[OFF_B1 + t];
-    if (threadIdx.x < A) S.b2[threadIdx.x] = p[OFF_B2 + threadIdx.x];
+    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[(t % H2) * A + t / H2] = raw[OFF_W2 + t];
+    for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = raw[OFF_B0 + t];
+    for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = raw[OFF_B1 + t];
+    if (threadIdx.x < A) S.b2[threadIdx.x] = raw[OFF_B2 + threadIdx.x];
+    __syncthreads();
+    // per-row / per-column norms in parallel (fp64), then one warp reduces
+    double* nrm = reinterpret_cast<double*>(raw);  // [0,64) r0 rows, [64,96) r1 cols, [96,98) r2, [128,160) rd
+    const int t = threadIdx.x;
+    if (t < H1) {
+        double s = 0;
+        for (int i = 0; i < F; ++i) s += fabs((double)S.w0[(t >> 1) * (2 * F) + 2 * i + (t & 1)]);
+        nrm[t] = s;
+    } else if (t < H1 + H2) {
+        double s = 0;
+        for (int j = 0; j < H1; ++j) s += fabs((double)S.w1t[j * H2 + (t - H1)]);
+        nrm[t] = s;
+    } else if (t < H1 + H2 + A) {
+        double s = 0;
+        for (int k = 0; k < H2; ++k) s += fabs((double)S.w2[k * A + (t - H1 - H2)]);
+        nrm[t] = s;
+    } else if (t >= 128 && t < 128 + H2) {
+        const int k = t - 128;
+        nrm[t] = fabs((double)S.w2[k * A + 1] - (double)S.w2[k * A]);
+    }
     __syncthreads();
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
-        double r0 = 0, bb0 = 0, r1 = 0, bb1 = 0, r2 = 0, bb2 = 0;
-        for (int j = lane; j < H1; j += 32) {
-            double s = 0;
-            for (int i = 0; i < F; ++i) s += fabs((double)S.w0[(j >> 1) * (2 * F) + 2 * i + (j & 1)]);
-            r0 = fmax(r0, s);
-            bb0 = fmax(bb0, fabs((double)S.b0[j]));
-        }
-        {
-            double s = 0;
-            for (int j = 0; j < H1; ++j) s += fabs((double)S.w1t[j * H2 + lane]);
-            r1 = s;
-            bb1 = fabs((double)S.b1[lane]);
-        }
-        if (lane < A) {
-            double s = 0;
-            for (int k = 0; k < H2; ++k) s += fabs((double)S.w2[k * A + lane]);
-            r2 = s;
-            bb2 = fabs((double)S.b2[lane]);
-        }
+        double r0 = fmax(nrm[lane], nrm[lane + 32]);
+        double bb0 = fmax(fabs((double)S.b0[lane]), fabs((double)S.b0[lane + 32]));
+        double r1 = nrm[H1 + lane], bb1 = fabs((double)S.b1[lane]);
+        double r2 = lane < A ? nrm[H1 + H2 + lane] : 0.0;
+        double bb2 = lane < A ? fabs((double)S.b2[lane]) : 0.0;
+        double rd = nrm[128 + lane];
         for (int o = 16; o > 0; o >>= 1) {
             r0 = fmax(r0, __shfl_xor_sync(0xffffffffu, r0, o));
             bb0 = fmax(bb0, __shfl_xor_sync(0xffffffffu, bb0, o));
@@ -103,6 +132,7 @@ __device__ void load_fast_weights(FastSmem& S, const float* __restrict__ p) {
             bb1 = fmax(bb1, __shfl_xor_sync(0xffffffffu, bb1, o));
             r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
             bb2 = fmax(bb2, __shfl_xor_sync(0xffffffffu, bb2, o));
+            rd += __shfl_xor_sync(0xffffffffu, rd, o);
         }
         if (lane == 0) {
             // 1.0001 absorbs the rounding of the fp64 row sums themselves
@@ -112,25 +142,30 @@ __device__ void load_fast_weights(FastSmem& S, const float* __restrict__ p) {
             S.stats[3] = __double2float_ru(bb1);
             S.stats[4] = __double2float_ru(r2 * 1.0001);
             S.stats[5] = __double2float_ru(bb2);
+            S.stats[6] = __double2float_ru(rd * 1.0001);
         }
     }
     __syncthreads();
 }
 
 // Forward error bound on |(l1-l0)_fp32 - (l1-l0)_exact| (Higham-style
-// recursive-summation bounds for FMA chains, u = 2^-24):
-//   D1 = g(44)(B0 + R0 X)                      X  = max_i |x_i|
-//   D2 = g(64)(B1 + R1 H1) + R1 D1             H1 = max_j h1_j  (fp32 values)
-//   D3 = g(32)(B2 + R2 H2) + R2 D2             H2 = max_k h2_k
-//   margin = 2 D3 (+1% slack; covers the fp64 reference's own rounding and
-//   the rounding of this bound's evaluation), g(n) = (n+1) u (1 + 1e-4).
+// recursive-summation bounds for FMA chains, u = 2^-24, g(n) = n u (1 + 1e-4)):
+//   D1 = g(14)(B0 + R0 X)        X  = max_i |x_i|; layer 1 runs 4 chains of
+//                                 <= 12 terms (bias in the first) + 2 levels
+//                                 of adds: 14 roundings per element at most
+//   D2 = g(65)(B1 + R1 H1) + R1 D1     H1 = max_j h1_j  (fp32 values)
+//   e3 = 2 g(33)(B2 + R2 H2) + Rd D2   H2 = max_k h2_k; Rd = ||w2[1] - w2[0]||_1
+//        (each logit's own chain rounding, plus the difference's sensitivity
+//        to the h2 errors, which relu does not amplify)
+//   margin = 1.01 e3 (+ slack for the fp64 reference's own rounding, the
+//   final fp32 subtraction and this bound's evaluation).
 __device__ __forceinline__ float guard_threshold(const float* st, float X, float Hm1, float Hm2) {
     const float u = 5.9604645e-8f;  // 2^-24
-    const float g44 = 45.f * u * 1.0001f, g64 = 65.f * u * 1.0001f, g32 = 33.f * u * 1.0001f;
-    const float D1 = g44 * (st[1] + st[0] * X);
-    const float D2 = g64 * (st[3] + st[2] * Hm1) + st[2] * D1;
-    const float D3 = g32 * (st[5] + st[4] * Hm2) + st[4] * D2;
-    return 2.02f * D3 + 1e-30f;
+    const float g14 = 14.f * u * 1.0001f, g65 = 65.f * u * 1.0001f, g33 = 33.f * u * 1.0001f;
+    const float D1 = g14 * (st[1] + st[0] * X);
+    const float D2 = g65 * (st[3] + st[2] * Hm1) + st[2] * D1;
+    const float e3 = 2.f * g33 * (st[5] + st[4] * Hm2) + st[6] * D2;
+    return 1.02f * e3 + 1e-30f;
 }
 
 // Per-state tail of the fast path: guard, fp32 softmax, action (greedy or
@@ -221,7 +256,7 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
                 unsigned int* __restrict__ flags, int mode) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FastSmem& S = *reinterpret_cast<FastSmem*>(smem_raw);
-    load_fast_weights(S, params);
+    load_fast_weights(S, &S.xs[0][0][0], params);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t n_warps_total = (size_t)gridDim.x * (FWD_BLOCK / 32);
@@ -264,21 +299,26 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
 #pragma unroll 2
         for (int jp = 0; jp < H1 / 2; ++jp) {
             const float4* wr = reinterpret_cast<const float4*>(S.w0 + jp * (2 * F));
-            // two partial chains per z (even / odd inputs): twice the ILP; the
-            // guard's error bound holds for any summation order
+            // four partial chains per z (inputs i mod 4): ILP and a 4x shorter
+            // rounding chain; the guard's bound (g(14)) holds for this order
             float2 za = make_float2(S.b0[2 * jp], S.b0[2 * jp + 1]), zb = za;
-            float2 za2 = make_float2(0.f, 0.f), zb2 = za2;
+            float2 za2 = make_float2(0.f, 0.f), zb2 = za2, za3 = za2, zb3 = za2, za4 = za2, zb4 = za2;
 #pragma unroll
-            for (int q = 0; q < F / 2; ++q) {
-                const float4 w = wr[q];
+            for (int q = 0; q < F / 2; q += 2) {
+                const float4 w = wr[q], v = wr[q + 1];
                 const float2 w01 = make_float2(w.x, w.y), w23 = make_float2(w.z, w.w);
+                const float2 v01 = make_float2(v.x, v.y), v23 = make_float2(v.z, v.w);
                 za = __ffma2_rn(w01, make_float2(xa[2 * q], xa[2 * q]), za);
                 zb = __ffma2_rn(w01, make_float2(xb[2 * q], xb[2 * q]), zb);
                 za2 = __ffma2_rn(w23, make_float2(xa[2 * q + 1], xa[2 * q + 1]), za2);
                 zb2 = __ffma2_rn(w23, make_float2(xb[2 * q + 1], xb[2 * q + 1]), zb2);
+                za3 = __ffma2_rn(v01, make_float2(xa[2 * q + 2], xa[2 * q + 2]), za3);
+                zb3 = __ffma2_rn(v01, make_float2(xb[2 * q + 2], xb[2 * q + 2]), zb3);
+                za4 = __ffma2_rn(v23, make_float2(xa[2 * q + 3], xa[2 * q + 3]), za4);
+                zb4 = __ffma2_rn(v23, make_float2(xb[2 * q + 3], xb[2 * q + 3]), zb4);
             }
-            za = make_float2(za.x + za2.x, za.y + za2.y);
-            zb = make_float2(zb.x + zb2.x, zb.y + zb2.y);
+            za = make_float2((za.x + za3.x) + (za2.x + za4.x), (za.y + za3.y) + (za2.y + za4.y));
+            zb = make_float2((zb.x + zb3.x) + (zb2.x + zb4.x), (zb.y + zb3.y) + (zb2.y + zb4.y));
             const float hA0 = za.x > 0.f ? za.x : 0.f, hA1 = za.y > 0.f ? za.y : 0.f;
             const float hB0 = zb.x > 0.f ? zb.x : 0.f, hB1 = zb.y > 0.f ? zb.y : 0.f;
             hma = fmaxf(hma, fmaxf(hA0, hA1));
@@ -329,6 +369,7 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
 
 // -------------------------------------------------------------- exact path
 struct ExactSmem {
+    __align__(16) float raw[NP + 2];  // staged parameters
     double w0[H1 * F];   // [j][i]
     double w1t[H1 * H2]; // [j][k]
     double w2[A * H2];
@@ -385,16 +426,45 @@ __device__ __forceinline__ void exact_forward(const ExactSmem& S, const float* _
 }
 
 __device__ void load_exact_weights(ExactSmem& S, const float* __restrict__ p) {
-    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) S.w0[t] = p[OFF_W0 + t];
+    stage_params(S.raw, p);
+    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) S.w0[t] = S.raw[OFF_W0 + t];
     for (int t = threadIdx.x; t < H1 * H2; t += blockDim.x) {
         const int k = t / H1, j = t % H1;
-        S.w1t[j * H2 + k] = p[OFF_W1 + t];
+        S.w1t[j * H2 + k] = S.raw[OFF_W1 + t];
     }
-    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[t] = p[OFF_W2 + t];
-    for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = p[OFF_B0 + t];
-    for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = p[OFF_B1 + t];
-    if (threadIdx.x < A) S.b2[threadIdx.x] = p[OFF_B2 + threadIdx.x];
+    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[t] = S.raw[OFF_W2 + t];
+    for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = S.raw[OFF_B0 + t];
+    for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = S.raw[OFF_B1 + t];
+    if (threadIdx.x < A) S.b2[threadIdx.x] = S.raw[OFF_B2 + threadIdx.x];
     __syncthreads();
+}
+
+// Action + outputs of one exactly evaluated state (greedy or collection draw).
+__device__ __forceinline__ void exact_finish(size_t s, double p0, double p1,
+                                             double* __restrict__ probs, uint8_t* __restrict__ actions,
+                                             const uint64_t* __restrict__ seg_off, size_t nseg,
+                                             const uint64_t* __restrict__ seg_seed, double eps,
+                                             int mode) {
+    uint8_t act;
+    if (mode & 4) {
+        size_t lo = 0, hi = nseg;
+        while (hi - lo > 1) {
+            const size_t mid = (lo + hi) >> 1;
+            if (seg_off[mid] <= s) lo = mid; else hi = mid;
+        }
+        const uint64_t j = s - seg_off[lo];
+        const uint64_t seed = seg_seed[lo];
+        const double ue = unit_of(sm_draw(seed, 2 * j + 1));
+        const double ua = unit_of(sm_draw(seed, 2 * j + 2));
+        act = ue < eps ? (ua < 0.5 ? 0 : 1) : (ua < p0 ? 0 : 1);
+    } else {
+        act = p1 >= p0 ? 1 : 0;  // ties -> Wave64 (policy.cpp:339-342)
+    }
+    if (mode & 2) actions[s] = act;
+    if (mode & 1) {
+        probs[2 * s] = p0;
+        probs[2 * s + 1] = p1;
+    }
 }
 
 // list == nullptr: all n states; else the n_list states named by list.
@@ -423,30 +493,122 @@ fwd_exact_kernel(const float* __restrict__ params, const float* __restrict__ fea
         }
         double p0, p1;
         exact_forward(S, xrow, p0, p1);
-        uint8_t act;
-        if (mode & 4) {
-            size_t lo = 0, hi = nseg;
-            while (hi - lo > 1) {
-                const size_t mid = (lo + hi) >> 1;
-                if (seg_off[mid] <= s) lo = mid; else hi = mid;
+        exact_finish(s, p0, p1, probs, actions, seg_off, nseg, seg_seed, eps, mode);
+    }
+}
+
+// Re-check of the fast path's ambiguous states: one WARP per group of RS
+// states (RS independent chains per lane hide the fp64 and shared-memory
+// latencies; each weight read feeds RS states), so the short list finishes in
+// a few group-latencies instead of one thread's full serial forward. Per
+// output the operations and their order are exact_forward's (lane j: z_j over
+// i ascending; lane k: acc2_k over j ascending; lane 2s+a: logit a of state s
+// over k ascending), so the results are bit-identical.
+constexpr int RS = 4;
+struct RecheckSmem {
+    __align__(16) float raw[NP + 2];  // staged parameters
+    double w0t[F * H1];  // [i][j]: lane j reads consecutive words
+    double w1t[H1 * H2]; // [j][k]
+    double w2[A * H2];   // [a][k]
+    double b0[H1];
+    double b1[H2];
+    double b2[A];
+    double xs[RECHECK_BLOCK / 32][RS][F];
+    double h1[RECHECK_BLOCK / 32][RS][H1];
+    double h2[RECHECK_BLOCK / 32][RS][H2];
+};
+
+__global__ void __launch_bounds__(RECHECK_BLOCK)
+fwd_recheck_kernel(const float* __restrict__ params, const float* __restrict__ feat,
+                   const uint32_t* __restrict__ list, const unsigned int* __restrict__ n_list,
+                   double* __restrict__ probs, uint8_t* __restrict__ actions,
+                   const uint64_t* __restrict__ seg_off, size_t nseg,
+                   const uint64_t* __restrict__ seg_seed, double eps, int mode) {
+    constexpr int WPB = RECHECK_BLOCK / 32;
+    const size_t count = *n_list;
+    if ((size_t)blockIdx.x * WPB * RS >= count) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RecheckSmem& S = *reinterpret_cast<RecheckSmem*>(smem_raw);
+    stage_params(S.raw, params);
+    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) {
+        const int j = t / F, i = t - j * F;
+        S.w0t[i * H1 + j] = S.raw[OFF_W0 + t];
+    }
+    for (int t = threadIdx.x; t < H1 * H2; t += blockDim.x) {
+        const int k = t / H1, j = t % H1;
+        S.w1t[j * H2 + k] = S.raw[OFF_W1 + t];
+    }
+    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[t] = S.raw[OFF_W2 + t];
+    for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = S.raw[OFF_B0 + t];
+    for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = S.raw[OFF_B1 + t];
+    if (threadIdx.x < A) S.b2[threadIdx.x] = S.raw[OFF_B2 + threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (size_t g = ((size_t)blockIdx.x * WPB + w) * RS; g < count;
+         g += (size_t)gridDim.x * WPB * RS) {
+        const int nv = (int)min((size_t)RS, count - g);
+        size_t sid[RS];
+#pragma unroll
+        for (int r = 0; r < RS; ++r) sid[r] = r < nv ? (size_t)list[g + r] : 0;
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+            const float* xrow = feat + sid[r] * F;
+            S.xs[w][r][lane] = r < nv ? (double)__ldg(xrow + lane) : 0.0;
+            if (lane + 32 < F) S.xs[w][r][lane + 32] = r < nv ? (double)__ldg(xrow + lane + 32) : 0.0;
+        }
+        __syncwarp();
+        double za[RS], zb[RS];
+#pragma unroll
+        for (int r = 0; r < RS; ++r) { za[r] = S.b0[lane]; zb[r] = S.b0[lane + 32]; }
+#pragma unroll 4
+        for (int i = 0; i < F; ++i) {
+            const double wa = S.w0t[i * H1 + lane], wb = S.w0t[i * H1 + lane + 32];
+#pragma unroll
+            for (int r = 0; r < RS; ++r) {
+                const double x = S.xs[w][r][i];
+                za[r] = fma(wa, x, za[r]);  // exact products: fma == mul-then-add
+                zb[r] = fma(wb, x, zb[r]);
             }
-            const uint64_t j = s - seg_off[lo];
-            const uint64_t seed = seg_seed[lo];
-            const double ue = unit_of(sm_draw(seed, 2 * j + 1));
-            const double ua = unit_of(sm_draw(seed, 2 * j + 2));
-            act = ue < eps ? (ua < 0.5 ? 0 : 1) : (ua < p0 ? 0 : 1);
-        } else {
-            act = p1 >= p0 ? 1 : 0;  // ties -> Wave64 (policy.cpp:339-342)
         }
-        if (mode & 2) actions[s] = act;
-        if (mode & 1) {
-            probs[2 * s] = p0;
-            probs[2 * s + 1] = p1;
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+            S.h1[w][r][lane] = za[r] > 0.0 ? za[r] : 0.0;
+            S.h1[w][r][lane + 32] = zb[r] > 0.0 ? zb[r] : 0.0;
         }
+        __syncwarp();
+        double acc[RS];
+#pragma unroll
+        for (int r = 0; r < RS; ++r) acc[r] = S.b1[lane];
+#pragma unroll 4
+        for (int j = 0; j < H1; ++j) {
+            const double wv = S.w1t[j * H2 + lane];
+#pragma unroll
+            for (int r = 0; r < RS; ++r) acc[r] = madd_rn(acc[r], wv, S.h1[w][r][j]);
+        }
+#pragma unroll
+        for (int r = 0; r < RS; ++r) S.h2[w][r][lane] = acc[r] > 0.0 ? acc[r] : 0.0;
+        __syncwarp();
+        // lane 2r + a: logit a of state r
+        const int lr = min(lane >> 1, RS - 1), la = lane & 1;
+        double l = S.b2[la];
+#pragma unroll 8
+        for (int k = 0; k < H2; ++k) l = madd_rn(l, S.w2[la * H2 + k], S.h2[w][lr][k]);
+        const double l1 = __shfl_down_sync(0xffffffffu, l, 1);
+        if (la == 0 && (lane >> 1) < nv) {
+            const double l0 = l;
+            const double m = fmax(l0, l1);
+            const double e0 = exp(__dsub_rn(l0, m));
+            const double e1 = exp(__dsub_rn(l1, m));
+            const double sum = __dadd_rn(e0, e1);
+            exact_finish((size_t)list[g + (lane >> 1)], __ddiv_rn(e0, sum),
+                         __ddiv_rn(e1, sum), probs, actions, seg_off, nseg, seg_seed, eps, mode);
+        }
+        __syncwarp();  // scratch reuse
     }
 }
 
 size_t fast_smem_bytes() { return sizeof(FastSmem); }
 size_t exact_smem_bytes() { return sizeof(ExactSmem); }
+size_t recheck_smem_bytes() { return sizeof(RecheckSmem); }
 
 }  // namespace gbxcu

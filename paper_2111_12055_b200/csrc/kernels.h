@@ -9,6 +9,7 @@ namespace gbxcu {
 
 constexpr int FWD_BLOCK = 256;    // fast inference: 8 warps, two states per thread
 constexpr int EXACT_BLOCK = 128;  // exact fp64 inference
+constexpr int RECHECK_BLOCK = 256;  // warp-per-state exact re-check
 constexpr int TRAIN_BLOCK = 512;  // train: 16 warps; tiles of 32 or 64 records
 constexpr int SHUF_BLOCK = 256;
 constexpr int AGG_BLOCK = 256;    // aggregation: 8 warps = 8 apps per CTA
@@ -81,8 +82,13 @@ __global__ void fwd_exact_kernel(const float* params, const float* feat, size_t 
                                  uint8_t* actions, const uint64_t* seg_off, size_t nseg,
                                  const uint64_t* seg_seed, double eps, unsigned int* flags,
                                  int mode);
+__global__ void fwd_recheck_kernel(const float* params, const float* feat, const uint32_t* list,
+                                   const unsigned int* n_list, double* probs, uint8_t* actions,
+                                   const uint64_t* seg_off, size_t nseg, const uint64_t* seg_seed,
+                                   double eps, int mode);
 size_t fast_smem_bytes();
 size_t exact_smem_bytes();
+size_t recheck_smem_bytes();
 
 template <int TB>
 __global__ void train_epoch_kernel(TrainArgs a);

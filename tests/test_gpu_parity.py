@@ -87,6 +87,26 @@ def test_forward_near_ties_are_exact(dev, orc):
     np.testing.assert_array_equal(act, orc.forward(p, feat)[1])
 
 
+def test_forward_recheck_path_is_bit_exact(dev, orc):
+    """A net trained on noise targets (small logit gaps): many states fall in
+    the guard band and go through the warp-per-state exact re-check, whose
+    probabilities must equal the fp64 reference bit for bit."""
+    p = golden("forward_g1")["params_trained"]
+    feat, _ = orc.g1(2024, 100_000)
+    probs_o, act_o = orc.forward(p, feat)
+    probs, act = dev.forward(p, feat, gbx.FWD_FAST)
+    n_re = dev.last_recheck_count()
+    assert 1000 < n_re < len(feat)
+    np.testing.assert_array_equal(act, act_o)
+    probs_x, _ = dev.forward(p, feat, gbx.FWD_EXACT)
+    same = (probs == probs_x).all(1)
+    assert same.sum() >= n_re          # re-checked rows carry the exact probabilities
+    seg = np.array([0, 40_000, 100_000], np.uint64)
+    seeds = np.array([11, 12], np.uint64)
+    np.testing.assert_array_equal(dev.collect(p, feat, seg, seeds, 0.1),
+                                  orc.collect(p, feat, seg, seeds, 0.1))
+
+
 def test_forward_rejects_non_finite(dev, orc):
     feat, _ = orc.g1(5, 64)
     feat[17, 10] = np.nan
