@@ -119,6 +119,22 @@ __global__ void qt_gather_digit_kernel(RecView v, const uint32_t* __restrict__ p
     }
 }
 
+// MSD fast path check: a pair of neighbours with equal top digits must have
+// equal keys (words w_from.. beyond the digit), else the order is unresolved.
+__global__ void qt_msd_check_kernel(RecView v, const uint32_t* __restrict__ perm,
+                                    const unsigned long long* __restrict__ digit, size_t nrec,
+                                    int w_from, unsigned int* __restrict__ unresolved) {
+    for (size_t i = 1 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec;
+         i += (size_t)gridDim.x * blockDim.x) {
+        if (digit[i] != digit[i - 1]) continue;
+        const uint32_t* a = v.key(perm[i]);
+        const uint32_t* b = v.key(perm[i - 1]);
+        bool same = true;
+        for (int w = w_from; w < KW && same; ++w) same = a[w] == b[w];
+        if (!same) atomicOr(unresolved, 1u);
+    }
+}
+
 // seg_head[i]: (key, action) differs from position i-1; key_head[i]: key differs.
 __global__ void qt_heads_kernel(RecView v, const uint32_t* __restrict__ perm, size_t nrec,
                                 uint32_t* __restrict__ seg_head, uint32_t* __restrict__ key_head) {
@@ -389,11 +405,74 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
     uint32_t spread[KW + 1];
     QT_CK(cudaMemcpyAsync(spread, io.spread, sizeof(spread), cudaMemcpyDeviceToHost, st));
     QT_CK(cudaStreamSynchronize(st));
+    auto bits_of = [&](int w) { return spread[w] ? 32 - __builtin_clz(spread[w]) : 0; };
+    auto sort_by = [&](const PackSpec& ps, int bits) -> cudaError_t {
+        qt_gather_digit_kernel<<<grid, 256, 0, st>>>(v, io.perm, nrec, ps,
+                                                     reinterpret_cast<unsigned long long*>(io.digit));
+        QT_CK(cub::DeviceRadixSort::SortPairs(io.temp, io.temp_bytes,
+                                              reinterpret_cast<const unsigned long long*>(io.digit),
+                                              reinterpret_cast<unsigned long long*>(io.digit2), io.perm,
+                                              io.perm2, (int)nrec, 0, bits, st));
+        std::swap(io.perm, io.perm2);
+        return cudaSuccess;
+    };
+    // MSD fast path: (1) stable partition by action, (2) stable sort by the
+    // <= 64 most significant varying key bits. If no two neighbours share
+    // those bits without sharing the whole key (checked on the device), the
+    // order is already the final (key, action, record) order; otherwise fall
+    // back to the full LSD below. Typical keys differ within their first
+    // varying words, so one 64-bit sort replaces ceil(varying bits / 64).
+    bool resolved = false;
+    {
+        if (bits_of(KW) > 0) {
+            PackSpec pa{};
+            pa.nf = 1;
+            pa.w[0] = KW;
+            pa.bits[0] = 1;
+            QT_CK(sort_by(pa, 1));
+        }
+        int ws[8], bs[8], nf = 0, used = 0, w = 0;
+        for (; w < KW && nf < 8; ++w) {
+            const int b = bits_of(w);
+            if (b == 0) continue;
+            if (used + b > 64) break;
+            ws[nf] = w;
+            bs[nf] = b;
+            ++nf;
+            used += b;
+        }
+        int w_rest = w;
+        while (w_rest < KW && bits_of(w_rest) == 0) ++w_rest;
+        if (nf > 0) {
+            PackSpec pt{};
+            int off = used;
+            for (int f = 0; f < nf; ++f) {  // most significant word in the highest bits
+                off -= bs[f];
+                pt.w[f] = ws[f];
+                pt.bits[f] = bs[f];
+                pt.off[f] = off;
+            }
+            pt.nf = nf;
+            QT_CK(sort_by(pt, used));
+        }
+        if (w_rest >= KW) {
+            resolved = true;  // the digit held every varying key bit
+        } else {
+            QT_CK(cudaMemsetAsync(io.spread + KW + 1, 0, sizeof(uint32_t), st));
+            qt_msd_check_kernel<<<grid, 256, 0, st>>>(
+                v, io.perm, reinterpret_cast<const unsigned long long*>(io.digit2), nrec, w_rest,
+                io.spread + KW + 1);
+            uint32_t unresolved = 1;
+            QT_CK(cudaMemcpyAsync(&unresolved, io.spread + KW + 1, 4, cudaMemcpyDeviceToHost, st));
+            QT_CK(cudaStreamSynchronize(st));
+            resolved = unresolved == 0;
+        }
+        if (!resolved) qt_iota_kernel<<<grid, 256, 0, st>>>(io.perm, nrec);
+    }
     // LSD over the packed key: the action is the least significant field, then
     // words 29 .. 0; each pass packs up to 64 bits of varying fields (constant
     // words are skipped: they cannot reorder anything)
-    int w_next = KW;  // KW = action, then 29, 28, ..., 0
-    auto bits_of = [&](int w) { return spread[w] ? 32 - __builtin_clz(spread[w]) : 0; };
+    int w_next = resolved ? -1 : KW;  // KW = action, then 29, 28, ..., 0
     while (w_next >= 0) {
         PackSpec ps{};
         int used = 0;

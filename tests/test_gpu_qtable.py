@@ -170,3 +170,33 @@ def test_hot_key_long_segment(dev, ref):
     qt = gbx.DeviceQTable(dev, 0.3, 0.999)
     qt.update_batch(keys, act, rew, now)
     check_table(qt.export(), o, q_rtol=1e-12)
+
+
+@pytest.mark.parametrize("case", ["shared_prefix", "few_varying_words"])
+def test_sort_paths_match_reference(dev, ref, case):
+    """The fold's MSD fast path (one sort by the top 64 varying key bits) and
+    its fallback to the full LSD sort when neighbours share those bits but
+    not the key (shared_prefix: keys differ only far down, in word 27), and
+    the case where every varying bit fits the first digit."""
+    rng = np.random.default_rng(17)
+    n_distinct, n = 3000, 40_000
+    base = np.zeros((n_distinct, 30), np.uint32)
+    if case == "shared_prefix":
+        prefix = rng.integers(0, 4096, (40, 27)).astype(np.uint32)
+        prefix[:, 0] %= 8                                   # stage < 8 (encode_state)
+        base[:, :27] = prefix[rng.integers(0, 40, n_distinct)]
+        base[:, 27] = rng.integers(0, 1 << 20, n_distinct).astype(np.uint32)
+    else:
+        base[:, 0] = rng.integers(0, 8, n_distinct)
+        base[:, 3] = rng.integers(0, 1 << 16, n_distinct).astype(np.uint32)
+    keys = base[rng.integers(0, n_distinct, n)]
+    act = rng.integers(0, 2, n).astype(np.uint8)
+    rew = rng.random(n) * 0.4 + 0.8
+    now = np.sort(rng.integers(0, 1000, n)).astype(np.uint64)
+    o = ref.qtable_fold(keys, act, rew, now, alpha=0.3, omega=1.0, rho=0.1)
+    qt = gbx.DeviceQTable(dev, 0.3, 1.0)
+    qt.update_batch(keys, act, rew, now)
+    check_table(qt.export(), o)
+    feat, tgt = qt.snapshot(0.1)
+    np.testing.assert_array_equal(feat, o["feat"])
+    np.testing.assert_allclose(tgt, o["tgt"], rtol=1e-15, atol=1e-300)
