@@ -135,7 +135,7 @@ struct gbxcu_qtable {
     DevBuf bkeys, bact, brew, bnow, init_ids, count;
     DevBuf perm, perm2, digit, digit2, seg_head, key_head, seg_scan, key_scan, seg_start, seg_key;
     DevBuf spread, bad, temp;
-    DevBuf flag, row, sfeat, stgt, bad_stage;
+    DevBuf flag, row, rowkey, sfeat, stgt, bad_stage;
 };
 
 namespace {
@@ -973,7 +973,7 @@ int qtable_fold(gbxcu_qtable* t, const uint32_t* d_keys, const uint8_t* d_act, c
     RET(t->nhas.ensure(2 * nkeys));
     CK(cudaMemsetAsync(t->nhas.p, 0, 2 * nkeys, st));
     CK(cudaMemsetAsync(t->bad.p, 0xFF, 8, st));
-    CK(qt_fold(io, nseg, t->nkeys.as<uint32_t>(), t->nq.as<double>(), t->nt.as<uint64_t>(),
+    CK(qt_fold(io, nseg, nkeys, t->nkeys.as<uint32_t>(), t->nq.as<double>(), t->nt.as<uint64_t>(),
                t->ncnt.as<uint64_t>(), t->nhas.as<uint8_t>(), c->num_sms, st));
     RET(check_launch(c, "qt_fold_kernel"));
     unsigned long long bad = ~0ull;
@@ -1103,9 +1103,15 @@ int qtable_snapshot(gbxcu_qtable* t, double rho, float* d_feat, double* d_tgt, s
     if (!d_feat) return GBXCU_OK;  // size query
     if (r > cap) return fail(GBXCU_EINVAL, "snapshot buffers too small");
     CK(cudaMemsetAsync(t->bad_stage.p, 0, 4, st));
-    qt_snapshot_kernel<<<c->num_sms * 4, 128, 0, st>>>(t->keys.as<uint32_t>(), t->q.as<double>(),
-                                                       t->flag.as<uint32_t>(), t->row.as<uint32_t>(), m,
-                                                       rho, d_feat, d_tgt, t->bad_stage.as<int>());
+    if (r == 0) return GBXCU_OK;
+    RET(t->rowkey.ensure(sizeof(uint32_t) * r));
+    qt_rowkey_kernel<<<c->num_sms * 4, 256, 0, st>>>(t->flag.as<uint32_t>(), t->row.as<uint32_t>(), m,
+                                                     t->rowkey.as<uint32_t>());
+    RET(check_launch(c, "qt_rowkey_kernel"));
+    const int sgrid = (int)std::min<size_t>((r + 127) / 128, (size_t)c->num_sms * 8);
+    qt_snapshot_kernel<<<sgrid, 128, 0, st>>>(t->keys.as<uint32_t>(), t->q.as<double>(),
+                                              t->rowkey.as<uint32_t>(), r, rho, d_feat, d_tgt,
+                                              t->bad_stage.as<int>());
     RET(check_launch(c, "qt_snapshot_kernel"));
     int bs = 0;
     CK(cudaMemcpyAsync(&bs, t->bad_stage.p, 4, cudaMemcpyDeviceToHost, st));

@@ -119,19 +119,36 @@ __global__ void qt_gather_digit_kernel(RecView v, const uint32_t* __restrict__ p
     }
 }
 
-// MSD fast path check: a pair of neighbours with equal top digits must have
-// equal keys (words w_from.. beyond the digit), else the order is unresolved.
-__global__ void qt_msd_check_kernel(RecView v, const uint32_t* __restrict__ perm,
+// MSD fast path: segment heads straight from the sorted top digits, plus the
+// check that makes them valid — neighbours with equal digits must have equal
+// keys (words w_from.. beyond the digit; none when w_from == KW), else the
+// order is unresolved and the caller falls back to the full LSD sort.
+__global__ void qt_msd_heads_kernel(RecView v, const uint32_t* __restrict__ perm,
                                     const unsigned long long* __restrict__ digit, size_t nrec,
-                                    int w_from, unsigned int* __restrict__ unresolved) {
-    for (size_t i = 1 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec;
+                                    int w_from, unsigned int* __restrict__ unresolved,
+                                    uint32_t* __restrict__ seg_head, uint32_t* __restrict__ key_head) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec;
          i += (size_t)gridDim.x * blockDim.x) {
-        if (digit[i] != digit[i - 1]) continue;
-        const uint32_t* a = v.key(perm[i]);
-        const uint32_t* b = v.key(perm[i - 1]);
-        bool same = true;
-        for (int w = w_from; w < KW && same; ++w) same = a[w] == b[w];
-        if (!same) atomicOr(unresolved, 1u);
+        uint32_t kh = 1, sh = 1;
+        if (i > 0) {
+            const uint32_t r = perm[i], r0 = perm[i - 1];
+            if (digit[i] == digit[i - 1]) {
+                kh = 0;
+                if (w_from < KW) {
+                    const uint32_t* a = v.key(r);
+                    const uint32_t* b = v.key(r0);
+                    bool same = true;
+                    for (int w = w_from; w < KW && same; ++w) same = a[w] == b[w];
+                    if (!same) {
+                        atomicOr(unresolved, 1u);
+                        kh = 1;
+                    }
+                }
+            }
+            sh = kh | (v.action(r) != v.action(r0) ? 1u : 0u);
+        }
+        seg_head[i] = sh;
+        key_head[i] = kh;
     }
 }
 
@@ -188,6 +205,7 @@ struct FoldArgs {
     uint64_t* cnt;
     uint8_t* has;
     unsigned long long* bad; // min batch index of a ClockRegressionError
+    uint32_t* src_rec;       // [m'] a record carrying each written key (0xFFFFFFFF: none)
 };
 
 // One thread per (key, action) segment: QTable::update in sequence order.
@@ -239,10 +257,23 @@ __global__ void qt_fold_kernel(FoldArgs f) {
         f.t[e] = t;
         f.cnt[e] = cnt;
         f.has[e] = 1;
-        // the key row (each segment of the key writes the same values)
-        const uint32_t* src = f.v.key(first);
-        uint32_t* dst = f.keys + (size_t)kid * KW;
-        for (int w = 0; w < KW; ++w) dst[w] = src[w];
+        // the key row is copied by qt_copy_keys_kernel (coalesced); either
+        // segment of the key names a record with the same words
+        f.src_rec[kid] = first;
+    }
+}
+
+// New key rows: thread per (key, word), so a warp reads and writes whole
+// 120-byte rows (a thread-per-key copy touches 30 sectors per instruction).
+__global__ void qt_copy_keys_kernel(RecView v, const uint32_t* __restrict__ src_rec, size_t nkeys,
+                                    uint32_t* __restrict__ keys) {
+    const size_t total = nkeys * KW;
+    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total;
+         x += (size_t)gridDim.x * blockDim.x) {
+        const size_t kid = x / KW;
+        const int w = (int)(x - kid * KW);
+        const uint32_t r = src_rec[kid];
+        if (r != 0xFFFFFFFFu) keys[x] = v.key(r)[w];
     }
 }
 
@@ -327,45 +358,78 @@ __global__ void qt_both_kernel(const uint8_t* __restrict__ has, size_t m, uint32
 }
 
 // One thread per key: encode_state(counters_from_key(key)) + boltzmann_pair.
-__global__ void qt_snapshot_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ q,
-                                   const uint32_t* __restrict__ flag, const uint32_t* __restrict__ row,
-                                   size_t m, double rho, float* __restrict__ feat,
-                                   double* __restrict__ tgt, int* __restrict__ bad_stage) {
-    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < m; k += (size_t)gridDim.x * blockDim.x) {
-        if (!flag[k]) continue;
-        const uint32_t* v = keys + k * KW;
-        const size_t r = row[k];
-        float* out = feat + r * F;
-        const uint32_t stage = v[0];
-        if (stage >= 8) {  // counters_from_key: "state key holds invalid stage index"
-            atomicExch(bad_stage, 1);
-            continue;
+// Row -> key map of the snapshot (rows = keys with both actions, key order).
+__global__ void qt_rowkey_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ row,
+                                 size_t m, uint32_t* __restrict__ rowkey) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < m; k += (size_t)gridDim.x * blockDim.x)
+        if (flag[k]) rowkey[row[k]] = (uint32_t)k;
+}
+
+// One warp per 32 consecutive output rows: the key rows are read
+// cooperatively into shared memory (whole 120-byte rows per instruction),
+// each lane encodes its row, and the 32 x 44 feature block is written back
+// as one contiguous, coalesced range.
+constexpr int SNAP_WARPS = 4;
+__global__ void __launch_bounds__(SNAP_WARPS * 32)
+qt_snapshot_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ q,
+                   const uint32_t* __restrict__ rowkey, size_t nrows, double rho,
+                   float* __restrict__ feat, double* __restrict__ tgt, int* __restrict__ bad_stage) {
+    __shared__ uint32_t kt[SNAP_WARPS][32 * (KW + 1)];
+    __shared__ float ft[SNAP_WARPS][32 * (F + 1)];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t* K = kt[w];
+    float* Fo = ft[w];
+    for (size_t r0 = ((size_t)blockIdx.x * SNAP_WARPS + w) * 32; r0 < nrows;
+         r0 += (size_t)gridDim.x * SNAP_WARPS * 32) {
+        const int nv = (int)min((size_t)32, nrows - r0);
+        const uint32_t kl = lane < nv ? rowkey[r0 + lane] : 0u;
+        for (int x0 = 0; x0 < 32 * KW; x0 += 32) {
+            const int x = x0 + lane, rr = x / KW, wd = x - rr * KW;
+            const uint32_t kk = __shfl_sync(0xffffffffu, kl, rr & 31);
+            if (rr < nv) K[rr * (KW + 1) + wd] = keys[(size_t)kk * KW + wd];
         }
+        __syncwarp();
+        if (lane < nv) {
+            const uint32_t* v = K + lane * (KW + 1);
+            float* out = Fo + lane * (F + 1);
+            const uint32_t stage = v[0];
+            if (stage >= 8) {  // counters_from_key: "state key holds invalid stage index"
+                atomicExch(bad_stage, 1);
+            } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) out[i] = i == (int)stage ? 1.0f : 0.0f;
-        // slots 8..36: basic blocks, vector[5], scalar[4], memory[6], compute[4],
-        // control-flow[4], registers[2], work groups[3] = key words 1..29
-        for (int w = 1; w < KW; ++w) out[7 + w] = enc_count(v[w]);
-        // totals (u32 wrap, like the u64 sums cast back): vector, scalar, memory,
-        // compute, control-flow, registers; instructions = the first five
-        const int lo_[6] = {2, 7, 11, 17, 21, 25};
-        const int len_[6] = {5, 4, 6, 4, 4, 2};
-        uint32_t tot[7];
-        for (int g = 0; g < 6; ++g) {
-            uint32_t sacc = 0;
-            for (int i = 0; i < len_[g]; ++i) sacc += v[lo_[g] + i];
-            tot[g + 1] = sacc;
+                for (int i = 0; i < 8; ++i) out[i] = i == (int)stage ? 1.0f : 0.0f;
+                // slots 8..36: basic blocks, vector[5], scalar[4], memory[6], compute[4],
+                // control-flow[4], registers[2], work groups[3] = key words 1..29
+                for (int wd = 1; wd < KW; ++wd) out[7 + wd] = enc_count(v[wd]);
+                // totals (u32 wrap, like the u64 sums cast back): vector, scalar, memory,
+                // compute, control-flow, registers; instructions = the first five
+                const int lo_[6] = {2, 7, 11, 17, 21, 25};
+                const int len_[6] = {5, 4, 6, 4, 4, 2};
+                uint32_t tot[7];
+                for (int g = 0; g < 6; ++g) {
+                    uint32_t sacc = 0;
+                    for (int i = 0; i < len_[g]; ++i) sacc += v[lo_[g] + i];
+                    tot[g + 1] = sacc;
+                }
+                tot[0] = tot[1] + tot[2] + tot[3] + tot[4] + tot[5];
+                for (int i = 0; i < 7; ++i) out[37 + i] = enc_count(tot[i]);
+            }
+            // boltzmann_pair (qtable.cpp:121-129)
+            const double q0 = q[2 * (size_t)kl], q1 = q[2 * (size_t)kl + 1];
+            const double mx = q0 < q1 ? q1 : q0;  // std::max
+            const double e0 = exp(__ddiv_rn(__dsub_rn(q0, mx), rho));
+            const double e1 = exp(__ddiv_rn(__dsub_rn(q1, mx), rho));
+            const double sm = __dadd_rn(e0, e1);
+            tgt[2 * (r0 + lane)] = __ddiv_rn(e0, sm);
+            tgt[2 * (r0 + lane) + 1] = __ddiv_rn(e1, sm);
         }
-        tot[0] = tot[1] + tot[2] + tot[3] + tot[4] + tot[5];
-        for (int i = 0; i < 7; ++i) out[37 + i] = enc_count(tot[i]);
-        // boltzmann_pair (qtable.cpp:121-129)
-        const double q0 = q[2 * k], q1 = q[2 * k + 1];
-        const double mx = q0 < q1 ? q1 : q0;  // std::max
-        const double e0 = exp(__ddiv_rn(__dsub_rn(q0, mx), rho));
-        const double e1 = exp(__ddiv_rn(__dsub_rn(q1, mx), rho));
-        const double s = __dadd_rn(e0, e1);
-        tgt[2 * r] = __ddiv_rn(e0, s);
-        tgt[2 * r + 1] = __ddiv_rn(e1, s);
+        __syncwarp();
+        float* dst = feat + r0 * F;
+        for (int x = lane; x < nv * F; x += 32) {
+            const int rr = x / F;
+            dst[x] = Fo[rr * (F + 1) + (x - rr * F)];
+        }
+        __syncwarp();
     }
 }
 
@@ -455,13 +519,11 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
             pt.nf = nf;
             QT_CK(sort_by(pt, used));
         }
-        if (w_rest >= KW) {
-            resolved = true;  // the digit held every varying key bit
-        } else {
+        if (nf > 0) {
             QT_CK(cudaMemsetAsync(io.spread + KW + 1, 0, sizeof(uint32_t), st));
-            qt_msd_check_kernel<<<grid, 256, 0, st>>>(
+            qt_msd_heads_kernel<<<grid, 256, 0, st>>>(
                 v, io.perm, reinterpret_cast<const unsigned long long*>(io.digit2), nrec, w_rest,
-                io.spread + KW + 1);
+                io.spread + KW + 1, io.seg_head, io.key_head);
             uint32_t unresolved = 1;
             QT_CK(cudaMemcpyAsync(&unresolved, io.spread + KW + 1, 4, cudaMemcpyDeviceToHost, st));
             QT_CK(cudaStreamSynchronize(st));
@@ -502,7 +564,7 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
         io.perm = io.perm2;
         io.perm2 = t;
     }
-    qt_heads_kernel<<<grid, 256, 0, st>>>(v, io.perm, nrec, io.seg_head, io.key_head);
+    if (!resolved) qt_heads_kernel<<<grid, 256, 0, st>>>(v, io.perm, nrec, io.seg_head, io.key_head);
     QT_CK(cub::DeviceScan::ExclusiveSum(io.temp, io.temp_bytes, io.seg_head, io.seg_scan, (int)nrec, st));
     QT_CK(cub::DeviceScan::InclusiveSum(io.temp, io.temp_bytes, io.key_head, io.key_scan, (int)nrec, st));
     uint32_t tail[3];
@@ -517,7 +579,7 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
     return cudaGetLastError();
 }
 
-cudaError_t qt_fold(const QtFoldIO& io, size_t nseg, uint32_t* keys, double* q, uint64_t* t,
+cudaError_t qt_fold(const QtFoldIO& io, size_t nseg, size_t nkeys, uint32_t* keys, double* q, uint64_t* t,
                     uint64_t* cnt, uint8_t* has, int num_sms, cudaStream_t st) {
     FoldArgs f{};
     f.v = rec_view(io);
@@ -540,7 +602,12 @@ cudaError_t qt_fold(const QtFoldIO& io, size_t nseg, uint32_t* keys, double* q, 
     f.cnt = cnt;
     f.has = has;
     f.bad = io.bad;
+    // the last sort's input digits are dead by now: a [nkeys] u32 scratch
+    f.src_rec = io.digit;
+    cudaError_t e = cudaMemsetAsync(f.src_rec, 0xFF, sizeof(uint32_t) * nkeys, st);
+    if (e != cudaSuccess) return e;
     qt_fold_kernel<<<num_sms * 4, 128, 0, st>>>(f);
+    qt_copy_keys_kernel<<<num_sms * 8, 256, 0, st>>>(f.v, f.src_rec, nkeys, keys);
     return cudaGetLastError();
 }
 

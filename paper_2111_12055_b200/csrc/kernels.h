@@ -192,9 +192,9 @@ struct FoldArgs;
 __global__ void qt_iota_kernel(uint32_t* p, size_t n);
 __global__ void qt_init_ids_kernel(const uint8_t* has, size_t m, uint32_t* ids, unsigned long long* count);
 __global__ void qt_both_kernel(const uint8_t* has, size_t m, uint32_t* flag);
-__global__ void qt_snapshot_kernel(const uint32_t* keys, const double* q, const uint32_t* flag,
-                                   const uint32_t* row, size_t m, double rho, float* feat, double* tgt,
-                                   int* bad_stage);
+__global__ void qt_rowkey_kernel(const uint32_t* flag, const uint32_t* row, size_t m, uint32_t* rowkey);
+__global__ void qt_snapshot_kernel(const uint32_t* keys, const double* q, const uint32_t* rowkey,
+                                   size_t nrows, double rho, float* feat, double* tgt, int* bad_stage);
 // fold pipeline entry points (launch wrappers live in k_qtable.cu)
 struct QtFoldIO {
     const uint32_t* tkeys; const uint32_t* init; size_t n_init;
@@ -212,7 +212,7 @@ size_t qt_temp_bytes(size_t nrec);
 // Sorts and segments the records; returns segment and key counts (synchronous).
 cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_sms, cudaStream_t st);
 // Folds into a new table (keys, q, t, cnt, has zeroed by the caller).
-cudaError_t qt_fold(const QtFoldIO& io, size_t nseg, uint32_t* keys, double* q, uint64_t* t,
+cudaError_t qt_fold(const QtFoldIO& io, size_t nseg, size_t nkeys, uint32_t* keys, double* q, uint64_t* t,
                     uint64_t* cnt, uint8_t* has, int num_sms, cudaStream_t st);
 cudaError_t qt_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out,
                               size_t n, cudaStream_t st);
