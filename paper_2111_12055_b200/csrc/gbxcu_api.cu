@@ -210,8 +210,10 @@ int run_forward(gbxcu_ctx* c, const float* d_params, const float* d_feat, size_t
             d_actions, d_seg_off, nseg, d_seg_seed, eps, bits);
         RET(check_launch(c, "fwd_recheck_kernel"));
     } else {
+        // one resident wave (2 CTAs/SM at the kernel's register count), grid-stride:
+        // each CTA builds its fp64 weight copy once
         const size_t blocks_needed = (n + EXACT_BLOCK - 1) / EXACT_BLOCK;
-        const int grid = (int)std::min<size_t>(blocks_needed, (size_t)c->num_sms * 8);
+        const int grid = (int)std::min<size_t>(blocks_needed, (size_t)c->num_sms * 2);
         fwd_exact_kernel<<<grid, EXACT_BLOCK, exact_smem_bytes(), st>>>(
             d_params, d_feat, n, nullptr, nullptr, d_probs, d_actions, d_seg_off, nseg,
             d_seg_seed, eps, flags.as<unsigned int>(), bits);

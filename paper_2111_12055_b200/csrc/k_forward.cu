@@ -369,7 +369,6 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
 
 // -------------------------------------------------------------- exact path
 struct ExactSmem {
-    __align__(16) float raw[NP + 2];  // staged parameters
     double w0[H1 * F];   // [j][i]
     double w1t[H1 * H2]; // [j][k]
     double w2[A * H2];
@@ -425,17 +424,47 @@ __device__ __forceinline__ void exact_forward(const ExactSmem& S, const float* _
     p1 = __ddiv_rn(e1, s);
 }
 
+__device__ __forceinline__ void put_exact(ExactSmem& S, int t, float v) {
+    if (t < OFF_B0) S.w0[t] = v;
+    else if (t < OFF_W1) S.b0[t - OFF_B0] = v;
+    else if (t < OFF_B1) {
+        const int k = (t - OFF_W1) / H1, j = (t - OFF_W1) % H1;
+        S.w1t[j * H2 + k] = v;
+    } else if (t < OFF_W2) S.b1[t - OFF_B1] = v;
+    else if (t < OFF_B2) S.w2[t - OFF_W2] = v;
+    else S.b2[t - OFF_B2] = v;
+}
+
+// 16-byte loads, all of a thread's in flight at once (one memory round trip;
+// the exact kernel keeps its 40 KB footprint for occupancy).
 __device__ void load_exact_weights(ExactSmem& S, const float* __restrict__ p) {
-    stage_params(S.raw, p);
-    for (int t = threadIdx.x; t < H1 * F; t += blockDim.x) S.w0[t] = S.raw[OFF_W0 + t];
-    for (int t = threadIdx.x; t < H1 * H2; t += blockDim.x) {
-        const int k = t / H1, j = t % H1;
-        S.w1t[j * H2 + k] = S.raw[OFF_W1 + t];
+    if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+        constexpr int NV = NP / 4, PER = (NV + EXACT_BLOCK - 1) / EXACT_BLOCK, CH = 4;
+        // chunks of CH loads in flight: few registers (the kernel's occupancy
+        // is set by its register count), ceil(PER / CH) round trips
+#pragma unroll 1
+        for (int u0 = 0; u0 < PER; u0 += CH) {
+            float4 v[CH];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const int c = threadIdx.x + (u0 + u) * EXACT_BLOCK;
+                if (c < NV) v[u] = __ldg(reinterpret_cast<const float4*>(p) + c);
+            }
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const int c = threadIdx.x + (u0 + u) * EXACT_BLOCK;
+                if (c < NV) {
+                    put_exact(S, 4 * c, v[u].x);
+                    put_exact(S, 4 * c + 1, v[u].y);
+                    put_exact(S, 4 * c + 2, v[u].z);
+                    put_exact(S, 4 * c + 3, v[u].w);
+                }
+            }
+        }
+        for (int t = NV * 4 + threadIdx.x; t < NP; t += blockDim.x) put_exact(S, t, __ldg(p + t));
+    } else {
+        for (int t = threadIdx.x; t < NP; t += blockDim.x) put_exact(S, t, __ldg(p + t));
     }
-    for (int t = threadIdx.x; t < A * H2; t += blockDim.x) S.w2[t] = S.raw[OFF_W2 + t];
-    for (int t = threadIdx.x; t < H1; t += blockDim.x) S.b0[t] = S.raw[OFF_B0 + t];
-    for (int t = threadIdx.x; t < H2; t += blockDim.x) S.b1[t] = S.raw[OFF_B1 + t];
-    if (threadIdx.x < A) S.b2[threadIdx.x] = S.raw[OFF_B2 + threadIdx.x];
     __syncthreads();
 }
 
