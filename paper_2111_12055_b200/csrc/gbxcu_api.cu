@@ -160,10 +160,14 @@ int setup_kernel_attrs() {
         set((const void*)train_partial_kernel<32>, train_smem_bytes(32));
         set((const void*)train_partial_kernel<64>, train_smem_bytes(64));
         set((const void*)batch_grad_kernel, train_smem_bytes(64));
-        set((const void*)train_epoch_tc_kernel<4, false>, train_tc_smem_bytes(4));
-        set((const void*)train_epoch_tc_kernel<7, false>, train_tc_smem_bytes(7));
-        set((const void*)train_epoch_tc_kernel<4, true>, train_tc_smem_bytes(4));
-        set((const void*)train_epoch_tc_kernel<7, true>, train_tc_smem_bytes(7));
+        set((const void*)train_epoch_tc_kernel<4, false, false>, train_tc_smem_bytes(4));
+        set((const void*)train_epoch_tc_kernel<7, false, false>, train_tc_smem_bytes(7));
+        set((const void*)train_epoch_tc_kernel<4, true, false>, train_tc_smem_bytes(4));
+        set((const void*)train_epoch_tc_kernel<7, true, false>, train_tc_smem_bytes(7));
+        set((const void*)train_epoch_tc_kernel<4, false, true>, train_tc_smem_bytes(4));
+        set((const void*)train_epoch_tc_kernel<7, false, true>, train_tc_smem_bytes(7));
+        set((const void*)train_epoch_tc_kernel<4, true, true>, train_tc_smem_bytes(4));
+        set((const void*)train_epoch_tc_kernel<7, true, true>, train_tc_smem_bytes(7));
         set((const void*)train_partial_tc_kernel<4>, train_tc_smem_bytes(4));
         set((const void*)train_partial_tc_kernel<7>, train_tc_smem_bytes(7));
         set((const void*)tc_gemm_kernel, gemm_smem_bytes());
@@ -435,10 +439,18 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
             } else {
                 // system-scope exchange only across GPUs (a real peer set)
                 const bool sys = c->peers > 1;
-                const void* fn = mt == 4 ? (sys ? (const void*)train_epoch_tc_kernel<4, true>
-                                                : (const void*)train_epoch_tc_kernel<4, false>)
-                                         : (sys ? (const void*)train_epoch_tc_kernel<7, true>
-                                                : (const void*)train_epoch_tc_kernel<7, false>);
+                // variants (TD loss / Adam) in their own instantiations: the
+                // reference's KL + SGD kernels carry no runtime branches for them
+                const void* fns[2][2][2] = {
+                    {{(const void*)train_epoch_tc_kernel<4, false, false>,
+                      (const void*)train_epoch_tc_kernel<4, false, true>},
+                     {(const void*)train_epoch_tc_kernel<4, true, false>,
+                      (const void*)train_epoch_tc_kernel<4, true, true>}},
+                    {{(const void*)train_epoch_tc_kernel<7, false, false>,
+                      (const void*)train_epoch_tc_kernel<7, false, true>},
+                     {(const void*)train_epoch_tc_kernel<7, true, false>,
+                      (const void*)train_epoch_tc_kernel<7, true, true>}}};
+                const void* fn = fns[mt == 4 ? 0 : 1][sys ? 1 : 0][variant ? 1 : 0];
                 CK(cudaLaunchCooperativeKernel(fn, a.pvirt ? GG : G, TRAIN_BLOCK, args,
                                                train_tc_smem_bytes(mt), st));
             }

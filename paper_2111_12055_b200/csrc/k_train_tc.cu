@@ -403,7 +403,7 @@ __device__ __forceinline__ void pair_sync(int id) {
 //   F1 (n-tiles 4h..4h+3) | F2 (n-tiles 2h, 2h+1) | F3 + B1 | B2 (n-tiles 4h..4h+3)
 // then one CTA barrier and the gradient phase over all records (all warps):
 //   G1 (+ gb1 via H1's ones column), E, G0 (+ gb0 via X's ones column).
-template <int MT>
+template <int MT, bool VAR>
 __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b, int loss_mode) {
     constexpr int TB = 8 * MT;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -486,7 +486,7 @@ __device__ void tc_tile(TcSmem<MT>& S, TcGrads& g, int nv, double inv_b, int los
             const int a = tq & 1;
             const bool valid = r < nv;
             double loss, d3;
-            if (loss_mode == 1) {
+            if (VAR && loss_mode == 1) {
                 // TD / reward regression: Q = the raw outputs, record (act, reward)
                 const int act = S.ltgt[2 * r] != 0.0 ? 1 : 0;
                 const double err = (act ? l1 : l0) - S.ltgt[2 * r + 1];
@@ -657,7 +657,7 @@ __device__ __forceinline__ void tc_store_partial(const TcGrads& g, double* __res
 
 size_t train_tc_smem_bytes(int mt) { return mt == 4 ? sizeof(TcSmem<4>) : sizeof(TcSmem<7>); }
 
-template <int MT, bool SYS>
+template <int MT, bool SYS, bool VAR>
 __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     constexpr int TB = 8 * MT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
             h1 = h2; s1 = s2; r1 = r2; n1 = n2;
             if (h2) h2 = tc_next<TB>(a, who, n_steps, s2, r2, n2);
             TC_MARK(6);
-            tc_tile<MT>(S, g, nv, inv_b, a.loss_mode);
+            tc_tile<MT, VAR>(S, g, nv, inv_b, a.loss_mode);
             if (more && r0 + TB < hi) {
                 // the next tile belongs to this step: stage it now
                 cp_async_wait_all();
@@ -826,7 +826,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
                     const int p = p_lo + e2 - 1;
                     const double gsum = S.red[NT + tid];
                     double upd;
-                    if (a.optimizer == 1) {
+                    if (VAR && a.optimizer == 1) {
                         // Adam: this CTA owns the moments of its slice across steps
                         const double m = a.beta1 * a.adam_m[p] + (1.0 - a.beta1) * gsum;
                         const double v = a.beta2 * a.adam_v[p] + (1.0 - a.beta2) * gsum * gsum;
@@ -901,15 +901,19 @@ __global__ void __launch_bounds__(NT, 1) train_partial_tc_kernel(TrainArgs a, lo
         __syncthreads();
         buf ^= 1;
         if (r0 + TB < hi) tc_prefetch<MT>(S, buf, a, r0 + TB, (int)min((uint32_t)TB, hi - r0 - TB));
-        tc_tile<MT>(S, g, nv, inv_b, a.loss_mode);
+        tc_tile<MT, false>(S, g, nv, inv_b, 0);
     }
     tc_store_partial(g, a.partials + (size_t)blockIdx.x * PSTR);
 }
 
-template __global__ void train_epoch_tc_kernel<4, false>(TrainArgs);
-template __global__ void train_epoch_tc_kernel<7, false>(TrainArgs);
-template __global__ void train_epoch_tc_kernel<4, true>(TrainArgs);
-template __global__ void train_epoch_tc_kernel<7, true>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<4, false, false>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<7, false, false>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<4, true, false>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<7, true, false>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<4, false, true>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<7, false, true>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<4, true, true>(TrainArgs);
+template __global__ void train_epoch_tc_kernel<7, true, true>(TrainArgs);
 template __global__ void train_partial_tc_kernel<4>(TrainArgs, long);
 template __global__ void train_partial_tc_kernel<7>(TrainArgs, long);
 

@@ -94,7 +94,7 @@ template <int TB>
 __global__ void train_epoch_kernel(TrainArgs a);
 template <int TB>
 __global__ void train_partial_kernel(TrainArgs a, long step);
-template <int MT, bool SYS>
+template <int MT, bool SYS, bool VAR>
 __global__ void train_epoch_tc_kernel(TrainArgs a);
 template <int MT>
 __global__ void train_partial_tc_kernel(TrainArgs a, long step);
