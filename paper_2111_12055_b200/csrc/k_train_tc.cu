@@ -614,18 +614,48 @@ __device__ __forceinline__ void tc_slice(const TrainArgs& a, int rank, int nrank
     hi = min(r_hi, lo + per_cta);
 }
 
-// Next tile after (step, r0) within [step, n_steps); r0 == UINT32_MAX asks for
-// the first tile of `step`.
+// This CTA's slice of a FULL step is the same at every step up to the offset
+// step * batch: computed once per launch (two integer divisions per call
+// otherwise, ~4 calls per step on every thread); only a final partial step
+// takes the general path.
 struct TcWho {
     int rank, nranks, cta, nctas;
+    uint32_t lo_off, hi_off;  // slice of a full step, relative to its start
 };
 
+__device__ __forceinline__ TcWho tc_who(const TrainArgs& a, int rank, int nranks, int cta,
+                                        int nctas) {
+    TcWho w{rank, nranks, cta, nctas, 0u, 0u};
+    const uint32_t batch = (uint32_t)a.batch;
+    const uint32_t per_rank = (batch + nranks - 1) / (uint32_t)nranks;
+    const uint32_t r_lo = min(batch, (uint32_t)rank * per_rank);
+    const uint32_t r_hi = min(batch, r_lo + per_rank);
+    const uint32_t per_cta = (r_hi - r_lo + nctas - 1) / (uint32_t)nctas;
+    w.lo_off = min(r_hi, r_lo + (uint32_t)cta * per_cta);
+    w.hi_off = min(r_hi, w.lo_off + per_cta);
+    return w;
+}
+
+__device__ __forceinline__ void tc_slice_w(const TrainArgs& a, const TcWho& w, long step,
+                                           uint32_t& lo, uint32_t& hi, uint32_t& nb) {
+    const uint32_t batch = (uint32_t)a.batch, start = (uint32_t)step * batch;
+    if ((size_t)start + batch <= a.n) {
+        lo = start + w.lo_off;
+        hi = start + w.hi_off;
+        nb = batch;
+    } else {
+        tc_slice(a, w.rank, w.nranks, step, w.cta, w.nctas, lo, hi, nb);
+    }
+}
+
+// Next tile after (step, r0) within [step, n_steps); r0 == UINT32_MAX asks for
+// the first tile of `step`.
 template <int TB>
 __device__ bool tc_next(const TrainArgs& a, const TcWho& who, long n_steps, long& step,
                         uint32_t& r0, int& nv) {
     uint32_t lo, hi, nb;
     if (r0 != 0xFFFFFFFFu) {
-        tc_slice(a, who.rank, who.nranks, step, who.cta, who.nctas, lo, hi, nb);
+        tc_slice_w(a, who, step, lo, hi, nb);
         if (r0 + TB < hi) {
             r0 += TB;
             nv = (int)min((uint32_t)TB, hi - r0);
@@ -634,7 +664,7 @@ __device__ bool tc_next(const TrainArgs& a, const TcWho& who, long n_steps, long
         ++step;
     }
     for (; step < n_steps; ++step) {
-        tc_slice(a, who.rank, who.nranks, step, who.cta, who.nctas, lo, hi, nb);
+        tc_slice_w(a, who, step, lo, hi, nb);
         if (hi > lo) {
             r0 = lo;
             nv = (int)min((uint32_t)TB, hi - lo);
@@ -670,7 +700,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     const int rank = a.pvirt ? (int)blockIdx.x / Gl : a.prank;
     const int c = a.pvirt ? (int)blockIdx.x % Gl : (int)blockIdx.x;
     const int GG = R * Gl, gc = rank * Gl + c;
-    const TcWho who{rank, R, c, Gl};
+    const TcWho who = tc_who(a, rank, R, c, Gl);
     const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
     // reduce-scatter slice of this CTA: element 0 = loss, then params [p_lo, p_hi)
     const int chunk = (NP + GG - 1) / GG;
@@ -720,7 +750,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
 
     for (long step = 0; step < n_steps; ++step) {
         uint32_t lo, hi, nb;
-        tc_slice(a, rank, R, step, c, Gl, lo, hi, nb);
+        tc_slice_w(a, who, step, lo, hi, nb);
         const double inv_b = 1.0 / (double)nb;
         const unsigned tag = a.tag_base + (unsigned)step + 1u;
         TC_TRACE(step, 0);
