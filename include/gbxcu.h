@@ -214,6 +214,17 @@ int gbxcu_qtable_import(gbxcu_qtable* t, const uint32_t* keys, const double* q, 
 /* Table in key order: keys[m][30], q/ts/cnt/has[m][2] (has: entry recorded). */
 int gbxcu_qtable_export(const gbxcu_qtable* t, uint32_t* keys, double* q, uint64_t* ts,
                         uint64_t* cnt, uint8_t* has);
+/* Binary columnar table file — the experience-store load path without text
+ * parsing (the text form stays QTable::save / QTable::load,
+ * proj/src/qtable.cpp:160-231). Little-endian; a 64-byte header
+ * ("GBXQTAB", version 1, key words 30, states m, alpha, omega, payload bytes,
+ * FNV-1a-64 checksum of the payload) then 64-byte-aligned columns keys[m][30]
+ * u32 | q[m][2] f64 | t[m][2] u64 | count[m][2] u64 | has[m][2] u8, keys in
+ * strictly increasing order. Load replaces the table and its alpha/omega
+ * (as QTable::load does); GBXCU_EINVAL on a bad magic/version/size/checksum,
+ * unsorted keys or an entry with zero updates. */
+int gbxcu_qtable_save_columnar(const gbxcu_qtable* t, const char* path);
+int gbxcu_qtable_load_columnar(gbxcu_qtable* t, const char* path);
 /* snapshot_policy_dataset (proj/src/qtable.cpp:143-155): one record per key
  * with both actions, key order; feat[rows][44] = encode_state(counters_from_key)
  * (bit-exact: glibc log1pf restated), tgt[rows][2] = boltzmann_pair (CUDA exp:

@@ -109,7 +109,8 @@ EXPORTS = (
     "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_last_recheck_count", "gbxcu_peer_export",
     "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free", "gbxcu_qtable_clear",
     "gbxcu_qtable_update_batch", "gbxcu_qtable_update_batch_dev", "gbxcu_qtable_size",
-    "gbxcu_qtable_import", "gbxcu_qtable_export",
+    "gbxcu_qtable_import", "gbxcu_qtable_export", "gbxcu_qtable_save_columnar",
+    "gbxcu_qtable_load_columnar",
     "gbxcu_qtable_snapshot", "gbxcu_qtable_snapshot_dev",
 )
 PEER_HANDLE_BYTES = 64
@@ -161,6 +162,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_qtable_size.argtypes = [_vp, C.POINTER(_sz), C.POINTER(_sz)]
     L.gbxcu_qtable_export.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
     L.gbxcu_qtable_import.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _sz]
+    L.gbxcu_qtable_save_columnar.argtypes = [_vp, C.c_char_p]
+    L.gbxcu_qtable_load_columnar.argtypes = [_vp, C.c_char_p]
     L.gbxcu_qtable_snapshot.argtypes = [_vp, C.c_double, _vp, _vp, _sz, C.POINTER(_sz)]
     L.gbxcu_qtable_snapshot_dev.argtypes = [_vp, C.c_double, _vp, _vp, _sz, C.POINTER(_sz)]
     L.gbxcu_aggregate.argtypes = [_vp, C.POINTER(SuiteC), _u8p, _u64p, C.c_int, _f64p, _vp]
@@ -615,6 +618,17 @@ class DeviceQTable:
                 np.ascontiguousarray(t["t"], np.uint64), np.ascontiguousarray(t["cnt"], np.uint64),
                 np.ascontiguousarray(t["has"], np.uint8)]
         self.dev._ck(self.L.gbxcu_qtable_import(self.h, *(a.ctypes.data for a in arrs), m))
+
+    def save_columnar(self, path: str):
+        """Binary columnar table file (include/gbxcu.h: gbxcu_qtable_save_columnar)."""
+        self.dev._ck(self.L.gbxcu_qtable_save_columnar(self.h, os.fsencode(path)))
+
+    @classmethod
+    def load_columnar(cls, dev: "Device", path: str) -> "DeviceQTable":
+        """The columnar file straight onto the device (table + alpha/omega)."""
+        self = cls(dev)
+        dev._ck(self.L.gbxcu_qtable_load_columnar(self.h, os.fsencode(path)))
+        return self
 
     @classmethod
     def load(cls, dev: "Device", text: str) -> "DeviceQTable":

@@ -88,6 +88,7 @@ struct gbxcu_ctx {
     cudaStream_t stream = nullptr;
     uint64_t launches = 0;
     cudaEvent_t ev[24] = {};                 // fit's per-kernel timing events
+    unsigned long long* hres = nullptr;      // pinned host scratch for fit's small results
     double last_shuffle_ms = 0, last_train_ms = 0;
     std::mutex mu;
     // scratch
@@ -484,19 +485,26 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
             RET(check_launch(c, "finish_epoch_kernel"));
         }
     }
-    int dv = -1, wd = 0;
-    CK(cudaMemcpyAsync(&dv, c->diverged.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&wd, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    // small results into pinned scratch: truly asynchronous copies, one sync
+    // (pageable destinations make each copy a blocking round trip)
+    unsigned long long local[2 + MAX_PEERS] = {};
+    unsigned long long* hr = c->hres ? c->hres : local;
+    int* hdv = reinterpret_cast<int*>(hr);  // hr[0] = {diverged, status}
+    CK(cudaMemcpyAsync(hdv, c->diverged.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hdv + 1, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     const bool used_tc = fused;
-    if (used_tc) {  // resynchronise the monotonic counters (divergence stops early)
-        for (int r = 0; r < (c->peers > 1 ? 1 : vranks); ++r)
-            CK(cudaMemcpyAsync(&c->ctr_base[r], c->xchg[r].p, sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, st));
-    }
-    if (epoch_loss_out)
-        CK(cudaMemcpyAsync(epoch_loss_out, c->epoch_loss.p, sizeof(double) * cfg->epochs,
+    const int n_ctr = used_tc ? (c->peers > 1 ? 1 : vranks) : 0;
+    for (int r = 0; r < n_ctr; ++r)  // resynchronise the monotonic counters (divergence stops early)
+        CK(cudaMemcpyAsync(hr + 1 + r, c->xchg[r].p, sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));
+    const bool loss_via_scratch = epoch_loss_out && c->hres && cfg->epochs <= 48;
+    if (epoch_loss_out)
+        CK(cudaMemcpyAsync(loss_via_scratch ? static_cast<void*>(hr + 16) : epoch_loss_out,
+                           c->epoch_loss.p, sizeof(double) * cfg->epochs, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (loss_via_scratch) std::memcpy(epoch_loss_out, hr + 16, sizeof(double) * cfg->epochs);
+    const int dv = hdv[0], wd = hdv[1];
+    for (int r = 0; r < n_ctr; ++r) c->ctr_base[r] = hr[1 + r];
     c->last_shuffle_ms = c->last_train_ms = 0.0;
     if (timed && !c->comm) {
         for (int e = 0; e < cfg->epochs; ++e) {
@@ -575,6 +583,9 @@ int gbxcu_create(int device, gbxcu_ctx** out) {
                                                   fast_smem_bytes());
     c->fast_per_sm = std::max(1, per_sm);
     for (auto& e : c->ev) cudaEventCreate(&e);
+    if (cudaHostAlloc(reinterpret_cast<void**>(&c->hres), 64 * sizeof(unsigned long long),
+                      cudaHostAllocDefault) != cudaSuccess)
+        c->hres = nullptr;  // fall back to pageable copies (slower, same results)
     *out = c;
     return GBXCU_OK;
 }
@@ -587,6 +598,7 @@ void gbxcu_destroy(gbxcu_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->hres) cudaFreeHost(c->hres);
     delete c;
 }
 
@@ -1089,6 +1101,125 @@ int gbxcu_qtable_export(const gbxcu_qtable* t, uint32_t* keys, double* q, uint64
     if (ts) CK(cudaMemcpy(ts, t->t.p, sizeof(uint64_t) * 2 * m, cudaMemcpyDeviceToHost));
     if (cnt) CK(cudaMemcpy(cnt, t->cnt.p, sizeof(uint64_t) * 2 * m, cudaMemcpyDeviceToHost));
     if (has) CK(cudaMemcpy(has, t->has.p, 2 * m, cudaMemcpyDeviceToHost));
+    return GBXCU_OK;
+}
+
+// ------------------------------------------------ columnar table file (f2)
+namespace {
+constexpr char QT_MAGIC[8] = {'G', 'B', 'X', 'Q', 'T', 'A', 'B', '\0'};
+struct QtFileHeader {  // 64 bytes, little-endian
+    char magic[8];
+    uint32_t version, key_words;
+    uint64_t m;
+    double alpha, omega;
+    uint64_t payload_bytes, checksum;
+    uint64_t reserved;
+};
+static_assert(sizeof(QtFileHeader) == 64, "header layout");
+size_t qt_align64(size_t b) { return (b + 63) & ~(size_t)63; }
+// FNV-1a over 64-bit little-endian words (the tail zero-padded)
+uint64_t qt_checksum(const unsigned char* p, size_t n) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, p + i, 8);
+        h = (h ^ w) * 0x100000001b3ull;
+    }
+    if (i < n) {
+        uint64_t w = 0;
+        std::memcpy(&w, p + i, n - i);
+        h = (h ^ w) * 0x100000001b3ull;
+    }
+    return h;
+}
+struct QtSections {
+    size_t keys, q, t, cnt, has, total;
+};
+QtSections qt_sections(size_t m) {
+    QtSections s{};
+    s.keys = 0;
+    s.q = qt_align64(s.keys + sizeof(uint32_t) * QT_KEY_WORDS * m);
+    s.t = qt_align64(s.q + sizeof(double) * 2 * m);
+    s.cnt = qt_align64(s.t + sizeof(uint64_t) * 2 * m);
+    s.has = qt_align64(s.cnt + sizeof(uint64_t) * 2 * m);
+    s.total = qt_align64(s.has + 2 * m);
+    return s;
+}
+}  // namespace
+
+int gbxcu_qtable_save_columnar(const gbxcu_qtable* t, const char* path) {
+    if (!t || !path) return fail(GBXCU_EINVAL, "null argument");
+    const size_t m = t->m;
+    const QtSections sec = qt_sections(m);
+    std::vector<unsigned char> buf(sizeof(QtFileHeader) + sec.total, 0);
+    unsigned char* pay = buf.data() + sizeof(QtFileHeader);
+    RET(gbxcu_qtable_export(t, reinterpret_cast<uint32_t*>(pay + sec.keys),
+                            reinterpret_cast<double*>(pay + sec.q), reinterpret_cast<uint64_t*>(pay + sec.t),
+                            reinterpret_cast<uint64_t*>(pay + sec.cnt), pay + sec.has));
+    QtFileHeader h{};
+    std::memcpy(h.magic, QT_MAGIC, 8);
+    h.version = 1;
+    h.key_words = QT_KEY_WORDS;
+    h.m = m;
+    h.alpha = t->alpha;
+    h.omega = t->omega;
+    h.payload_bytes = sec.total;
+    h.checksum = qt_checksum(pay, sec.total);
+    std::memcpy(buf.data(), &h, sizeof(h));
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return fail(GBXCU_EINVAL, std::string("cannot open for writing: ") + path);
+    const bool ok = std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+    if (std::fclose(f) != 0 || !ok) return fail(GBXCU_EINVAL, std::string("write failed: ") + path);
+    return GBXCU_OK;
+}
+
+int gbxcu_qtable_load_columnar(gbxcu_qtable* t, const char* path) {
+    if (!t || !path) return fail(GBXCU_EINVAL, "null argument");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return fail(GBXCU_EINVAL, std::string("cannot open: ") + path);
+    QtFileHeader h{};
+    const bool got = std::fread(&h, 1, sizeof(h), f) == sizeof(h);
+    if (!got || std::memcmp(h.magic, QT_MAGIC, 8) != 0) {
+        std::fclose(f);
+        return fail(GBXCU_EINVAL, "not a columnar q-table file");
+    }
+    if (h.version != 1 || h.key_words != QT_KEY_WORDS) {
+        std::fclose(f);
+        return fail(GBXCU_EINVAL, "unsupported columnar q-table format version");
+    }
+    // QHyperparams::validate (proj/src/qtable.cpp:57-64), as QTable::load does
+    if (!(h.alpha > 0.0 && h.alpha <= 1.0) || !(h.omega > 0.0 && h.omega <= 1.0)) {
+        std::fclose(f);
+        return fail(GBXCU_EINVAL, "columnar q-table holds invalid hyperparameters");
+    }
+    if (h.m > (size_t)1 << 32) {
+        std::fclose(f);
+        return fail(GBXCU_EINVAL, "columnar q-table too large");
+    }
+    const QtSections sec = qt_sections((size_t)h.m);
+    if (h.payload_bytes != sec.total) {
+        std::fclose(f);
+        return fail(GBXCU_EINVAL, "columnar q-table size does not match its header");
+    }
+    std::vector<unsigned char> pay(sec.total);
+    const bool full = std::fread(pay.data(), 1, sec.total, f) == sec.total;
+    const bool at_end = std::fgetc(f) == EOF;
+    std::fclose(f);
+    if (!full || !at_end) return fail(GBXCU_EINVAL, "columnar q-table truncated or has trailing bytes");
+    if (qt_checksum(pay.data(), sec.total) != h.checksum)
+        return fail(GBXCU_EINVAL, "columnar q-table checksum mismatch");
+    const uint8_t* has = pay.data() + sec.has;
+    const uint64_t* cnt = reinterpret_cast<const uint64_t*>(pay.data() + sec.cnt);
+    for (size_t e = 0; e < 2 * (size_t)h.m; ++e) {
+        if (has[e] > 1) return fail(GBXCU_EINVAL, "columnar q-table: bad presence flag");
+        if (has[e] && cnt[e] == 0) return fail(GBXCU_EINVAL, "columnar q-table: entry with zero updates");
+    }
+    RET(gbxcu_qtable_import(t, reinterpret_cast<const uint32_t*>(pay.data() + sec.keys),
+                            reinterpret_cast<const double*>(pay.data() + sec.q),
+                            reinterpret_cast<const uint64_t*>(pay.data() + sec.t), cnt, has, (size_t)h.m));
+    t->alpha = h.alpha;
+    t->omega = h.omega;
     return GBXCU_OK;
 }
 

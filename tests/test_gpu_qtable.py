@@ -200,3 +200,40 @@ def test_sort_paths_match_reference(dev, ref, case):
     feat, tgt = qt.snapshot(0.1)
     np.testing.assert_array_equal(feat, o["feat"])
     np.testing.assert_allclose(tgt, o["tgt"], rtol=1e-15, atol=1e-300)
+
+
+def test_columnar_file_round_trip(dev, ref, tmp_path):
+    """Binary columnar table file (row f2): device table -> file -> a fresh
+    device table, identical contents and hyperparameters, same snapshot as the
+    reference; corrupted / truncated / foreign files are rejected."""
+    keys, act, rew, now = tuples(23, 30_000, 4000, wide=True)
+    o = ref.qtable_fold(keys, act, rew, now, alpha=0.25, omega=0.9, rho=0.1)
+    qt = gbx.DeviceQTable(dev, 0.25, 0.9)
+    qt.update_batch(keys, act, rew, now)
+    path = str(tmp_path / "table.gbxq")
+    qt.save_columnar(path)
+    qt2 = gbx.DeviceQTable.load_columnar(dev, path)
+    a, b = qt.export(), qt2.export()
+    for k in ("keys", "q", "t", "cnt", "has"):
+        np.testing.assert_array_equal(a[k], b[k])
+    check_table(b, o, q_rtol=1e-14)
+    feat, tgt = qt2.snapshot(0.1)
+    np.testing.assert_array_equal(feat, o["feat"])
+    np.testing.assert_allclose(tgt, o["tgt"], rtol=1e-13, atol=1e-300)
+    # alpha/omega travel with the file: one more fold agrees with the original
+    k2, a2, r2, n2 = keys[:100], act[:100], rew[:100], now[:100] + 5000
+    qt.update_batch(k2, a2, r2, n2)
+    qt2.update_batch(k2, a2, r2, n2)
+    np.testing.assert_array_equal(qt.export()["q"], qt2.export()["q"])
+    raw = bytearray(open(path, "rb").read())
+    bad = str(tmp_path / "bad.gbxq")
+    for mutate in (lambda r: r.__setitem__(100, r[100] ^ 1),      # payload bit flip
+                   lambda r: r.__delitem__(slice(len(r) - 8, None)),  # truncated
+                   lambda r: r.__setitem__(0, ord("X"))):           # magic
+        r = bytearray(raw)
+        mutate(r)
+        open(bad, "wb").write(bytes(r))
+        with pytest.raises(gbx.ValidationError):
+            gbx.DeviceQTable.load_columnar(dev, bad)
+    with pytest.raises(gbx.ValidationError):
+        gbx.DeviceQTable.load_columnar(dev, str(tmp_path / "missing.gbxq"))
