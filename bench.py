@@ -409,7 +409,14 @@ def main():
     }
 
     if rank == 0 and not args.no_secondary:
-        secondary = run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak,
+        # inference / C5 use a policy of FIXED training (5 epochs of the headline
+        # fit from the same init), so their numbers do not depend on --steps:
+        # the guard's re-check share grows as a net fits the noise targets
+        p_inf = torch.from_numpy(params0).cuda()
+        dev.fit_dev(p_inf.data_ptr(), feat_d.data_ptr(), tgt_d.data_ptr(), n_total, args.lr, 5,
+                    batch, 99, stream=dev.stream)
+        torch.cuda.synchronize()
+        secondary = run_secondary(args, dev, stream, p_inf, feat_d, torch, gbx, fp32_peak,
                                   peaks, local)
 
     line = {
@@ -439,7 +446,8 @@ def main():
 
 
 def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, peaks, local):
-    """Full-suite greedy inference over the 1M states + a C5-style aggregation sweep."""
+    """Full-suite greedy inference over the 1M states + a C5-style aggregation sweep.
+    params_d: the policy after 5 epochs of the headline fit (fixed training)."""
     out = {}
     # row f1: experience store — fold a synthetic C3-scale tuple log into a fresh
     # device Q-table (QTable::update x n) + snapshot_policy_dataset (device-resident)
@@ -467,6 +475,8 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
             "value": rate, "unit": "decisions/s", "ms": ms, "states": n,
             "fp32_tflops": rate * 9856 / 1e12,
             "hbm_gbs": rate * 177 / 1e9}
+        if mode == gbx.FWD_FAST:
+            out["inference"][name]["recheck_fraction"] = dev.last_recheck_count() / n
     out["inference"]["fp32_peak_tflops_measured"] = fp32_peak
     out["inference"]["hbm_peak_gbs"] = peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)
     if not args.no_cpu_baseline:
@@ -506,6 +516,30 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
             "value": feat_n / (ms * 1e-3), "unit": "samples/s", "ms_per_epoch": ms,
             "kernel": "train_epoch_kernel (fp64 exact, 1 CTA)" if b <= 32 else "train_epoch_tc_kernel",
             "tflops": feat_n * 23936 / (k_ms * 1e-3) / 1e12 if k_ms > 0 else None}
+
+    # north-star variants on the fused kernel (absent from the reference): TD
+    # regression of Q(x, a) on the reward + Adam, same log and batch as the headline
+    tgt_td = torch.empty((feat_n, 2), dtype=torch.float64, device="cuda")
+    tgt_td[:, 0] = (feat_d[:, 8] > 3.5).to(torch.float64)   # action
+    tgt_td[:, 1] = feat_d[:, 9].to(torch.float64) / 7.0     # reward
+    out["variants"] = {}
+    for loss, opt in (("td", "sgd"), ("kl", "adam"), ("td", "adam")):
+        tg = tgt_td if loss == "td" else tgt_n
+        p_v = params_d.clone()
+        for rep in range(2):  # warm, then timed
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            dev.fit_dev(p_v.data_ptr(), feat_d.data_ptr(), tg.data_ptr(), feat_n, 1e-3, 1, args.batch,
+                        99, stream=dev.stream, loss=loss, optimizer=opt)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        _, k_ms = dev.last_fit_timing()
+        out["variants"][f"{loss}_{opt}"] = {
+            "value": feat_n / (ms * 1e-3), "unit": "samples/s", "ms_per_epoch": ms,
+            "batch": args.batch, "kernel": "train_epoch_tc_kernel (variant instantiation)",
+            "tflops": feat_n * 23936 / (k_ms * 1e-3) / 1e12 if k_ms > 0 else None}
+    del tgt_td
 
     # C5 sweep: inference + aggregation over n_apps x per_app shaders (generated
     # on the device; the default is the config's 1e8 shader feature vectors)

@@ -67,13 +67,17 @@ struct DevBuf {
     ~DevBuf() {
         if (p) cudaFree(p);
     }
+    // grows geometrically once allocated (a table or log that grows a little
+    // every call must not pay cudaFree + cudaMalloc, both device-synchronising,
+    // every time)
     int ensure(size_t bytes) {
         if (bytes <= cap) return GBXCU_OK;
+        const size_t want = std::max<size_t>({bytes, cap ? cap + cap / 2 : 0, 256});
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
-        CK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
-        cap = std::max<size_t>(bytes, 256);
+        CK(cudaMalloc(&p, want));
+        cap = want;
         return GBXCU_OK;
     }
     template <typename T>
@@ -1157,6 +1161,14 @@ int gbxcu_qtable_save_columnar(const gbxcu_qtable* t, const char* path) {
     RET(gbxcu_qtable_export(t, reinterpret_cast<uint32_t*>(pay + sec.keys),
                             reinterpret_cast<double*>(pay + sec.q), reinterpret_cast<uint64_t*>(pay + sec.t),
                             reinterpret_cast<uint64_t*>(pay + sec.cnt), pay + sec.has));
+    {  // absent entries carry no state: zero them so files are deterministic
+        uint8_t* has = pay + sec.has;
+        double* q = reinterpret_cast<double*>(pay + sec.q);
+        uint64_t* ts = reinterpret_cast<uint64_t*>(pay + sec.t);
+        uint64_t* cn = reinterpret_cast<uint64_t*>(pay + sec.cnt);
+        for (size_t e = 0; e < 2 * m; ++e)
+            if (!has[e]) q[e] = 0.0, ts[e] = 0, cn[e] = 0;
+    }
     QtFileHeader h{};
     std::memcpy(h.magic, QT_MAGIC, 8);
     h.version = 1;

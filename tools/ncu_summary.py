@@ -57,11 +57,16 @@ if __name__ == '__main__':
     shares = launch_shares('gpurun_out/launches.csv')
     for k, c, avg, sh in shares:
         lines.append(f"| {k} | {c} | {avg:.1f} | {sh:.1%} |")
-    # the timed step of the headline (one fit epoch): shuffle + train kernel
-    step = [(k, c, avg) for k, c, avg, _ in shares
-            if k.startswith(('train_epoch', 'shuffle_epoch', 'iota_kernel', 'finish_epoch'))]
+    # the timed step of the headline (one fit epoch): every kernel of a
+    # --no-secondary run (launches_step.csv) when present, else the fit kernels
+    import os
+    if os.path.exists('gpurun_out/launches_step.csv'):
+        step = [(k, c, avg) for k, c, avg, _ in launch_shares('gpurun_out/launches_step.csv')]
+    else:
+        step = [(k, c, avg) for k, c, avg, _ in shares
+                if k.startswith(('train_epoch', 'shuffle_epoch', 'iota_kernel', 'finish_epoch'))]
     tot = sum(c * avg for _, c, avg in step)
-    lines += ["", "### Share of the headline step (fit epoch: shuffle + train)", "",
+    lines += ["", "### Share of the headline step (bench.py --no-secondary: fit epochs only)", "",
               "| kernel | launches | avg us | share of step |", "|---|---|---|---|"]
     for k, c, avg in step:
         lines.append(f"| {k} | {c} | {avg:.1f} | {c * avg / tot:.1%} |")
