@@ -13,9 +13,10 @@
 //   V(q)     = A[root(q)],  root = end of the chain q -> fg(q) -> fg(fg(q)) ...
 //   final[p] = succ(p) ? V(succ(p)) : A[j_p]            (p >= 1)
 //   final[0] = fg(0)   ? V(fg(0))   : A[0]
-// Chains are O(log n) long, so pointer jumping needs ~6 rounds (measured:
-// 6 at n = 1e6 and 1e7; buckets hold <= ~21 swaps), instead of the O(log n)
-// *dependence depth* of ~50 rounds a reservation-based replay needs. The
+// Chains are O(log n) long (pointer jumping would need ~6 rounds at n = 1e6
+// and 1e7; buckets hold <= ~21 swaps), so each thread walks its own chain
+// end in one pass, instead of the O(log n) *dependence depth* of ~50 rounds a
+// reservation-based replay needs. The
 // result equals the sequential shuffle exactly (tests/test_gpu_parity.py
 // compares against the reference at 1e5 and 1e6).
 #include "common.cuh"
@@ -93,24 +94,19 @@ shuffle_epoch_kernel(ShuffleArgs s) {
     }
     grid_barrier(s.bar, target);
 
-    // 4: pointer jumping root(q) <- root(root(q)) until no change
-    uint32_t* cur = s.root;
-    uint32_t* nxt = s.root2;
-    for (int round = 0; round < 64; ++round) {
-        bool changed = false;
-        for (size_t q = tid; q < n; q += nthr) {
-            const uint32_t r = __ldcg(cur + q);
-            const uint32_t r2 = __ldcg(cur + r);
-            __stcg(nxt + q, r2);
-            changed |= r2 != r;
+    // 4: chain ends, walked directly: fg() strictly increases along a chain,
+    //    so each walk terminates; chains are O(log n) long (expected ~1-2, the
+    //    longest a few dozen), so one pass of dependent L2 loads replaces the
+    //    ~7 barrier-separated pointer-jumping rounds (half of the kernel's time)
+    for (size_t q = tid; q < n; q += nthr) {
+        uint32_t r = __ldcg(s.root + q);
+        if (r != (uint32_t)q) {
+            for (uint32_t r2 = __ldcg(s.root + r); r2 != r; r2 = __ldcg(s.root + r)) r = r2;
         }
-        if (__syncthreads_or(changed) && threadIdx.x == 0) atomicOr(s.flags + round, 1u);
-        grid_barrier(s.bar, target);
-        uint32_t* t = cur;
-        cur = nxt;
-        nxt = t;
-        if (__ldcg(s.flags + round) == 0) break;
+        __stcg(s.root2 + q, r);
     }
+    grid_barrier(s.bar, target);
+    const uint32_t* cur = s.root2;
 
     // 5: final permutation
     const uint32_t fg0 = __ldcg(s.fg0);
