@@ -96,6 +96,17 @@ int gbxcu_forward(gbxcu_ctx* ctx, const float* params, const float* feat, size_t
 int gbxcu_forward_dev(gbxcu_ctx* ctx, const float* d_params, const float* d_feat, size_t n,
                       double* d_probs, uint8_t* d_actions, int mode, void* stream);
 
+/* select_greedy over a batch (SURVEY §8b's gbxcu_forward_batch): FAST mode of
+ * gbxcu_forward — actions exact, probabilities fp32-accurate. */
+int gbxcu_forward_batch(gbxcu_ctx* ctx, const float* params, const float* feat, size_t n,
+                        double* probs, uint8_t* actions);
+/* select_sample (proj/src/policy.cpp:344-347) over a batch drawing from ONE
+ * SplitMix64 stream whose current state is rng_state: state j takes the
+ * stream's (j+1)-th next_unit(), Wave32 iff it is < p0. Exact decisions; the
+ * caller's stream advances by n draws (SplitMix64::discard(n) in gbx/rng.hpp). */
+int gbxcu_sample_batch(gbxcu_ctx* ctx, const float* params, const float* feat, size_t n,
+                       uint64_t rng_state, uint8_t* actions);
+
 /* Sampled (collection) decisions, proj/src/tuner.cpp:183-196 with
  * select_sample semantics (proj/src/policy.cpp:344-347): states are grouped
  * in segments (one per benchmark, seg_off[nseg+1]); segment b draws from

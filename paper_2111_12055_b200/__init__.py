@@ -109,6 +109,7 @@ EXPORTS = (
     "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_last_recheck_count", "gbxcu_peer_export",
     "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free", "gbxcu_qtable_clear",
     "gbxcu_qtable_update_batch", "gbxcu_qtable_update_batch_dev", "gbxcu_qtable_size",
+    "gbxcu_forward_batch", "gbxcu_sample_batch",
     "gbxcu_qtable_import", "gbxcu_qtable_export", "gbxcu_qtable_save_columnar",
     "gbxcu_qtable_load_columnar",
     "gbxcu_qtable_snapshot", "gbxcu_qtable_snapshot_dev",
@@ -162,6 +163,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_qtable_size.argtypes = [_vp, C.POINTER(_sz), C.POINTER(_sz)]
     L.gbxcu_qtable_export.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
     L.gbxcu_qtable_import.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _sz]
+    L.gbxcu_forward_batch.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
+    L.gbxcu_sample_batch.argtypes = [_vp, _vp, _vp, _sz, _u64, _vp]
     L.gbxcu_qtable_save_columnar.argtypes = [_vp, C.c_char_p]
     L.gbxcu_qtable_load_columnar.argtypes = [_vp, C.c_char_p]
     L.gbxcu_qtable_snapshot.argtypes = [_vp, C.c_double, _vp, _vp, _sz, C.POINTER(_sz)]
@@ -295,6 +298,16 @@ class Device:
 
     def select_greedy(self, params, feat, mode=FWD_FAST):
         return self.forward(params, feat, mode, want_probs=False)[1]
+
+    def sample_batch(self, params, feat, rng_state: int) -> np.ndarray:
+        """select_sample over a batch from one SplitMix64 stream (state rng_state):
+        state j uses the stream's (j+1)-th draw; the caller's stream advances n."""
+        feat = _f32(feat).reshape(-1, N_FEATURES)
+        act = np.empty(feat.shape[0], np.uint8)
+        self._ck(self.L.gbxcu_sample_batch(self.h, _f32(params).ctypes.data, feat.ctypes.data,
+                                           feat.shape[0], rng_state & ((1 << 64) - 1),
+                                           act.ctypes.data))
+        return act
 
     def collect(self, params, feat, seg_off, seg_seed, eps):
         feat = _f32(feat).reshape(-1, N_FEATURES)

@@ -218,7 +218,11 @@ FitResult fit(PolicyNet& net, const PolicyDataset& dataset, const TrainConfig& c
     std::vector<double> tgt;
     flatten_records(dataset, feat, tgt);
     auto p = net.flat();
-    gbxcu_train_cfg c{cfg.learning_rate, cfg.epochs, cfg.batch_size, cfg.seed, 0, 0};
+    gbxcu_train_cfg c{};  // zeros: the reference's KL loss + SGD, no CTA cap, no virtual ranks
+    c.learning_rate = cfg.learning_rate;
+    c.epochs = cfg.epochs;
+    c.batch_size = cfg.batch_size;
+    c.seed = cfg.seed;
     FitResult res;
     res.epoch_loss.assign(cfg.epochs, 0.0);
     int diverged = -1;
@@ -265,6 +269,20 @@ std::vector<Action> select_greedy_batch(const BehaviorPolicy& beh,
     const auto p = beh.net.flat();
     check(gbxcu_forward(ctx(), p.data(), feat.data(), states.size(), nullptr, act.data(),
                         GBXCU_FWD_FAST));
+    for (std::size_t i = 0; i < act.size(); ++i) out[i] = act[i] ? Action::Wave64 : Action::Wave32;
+    return out;
+}
+
+std::vector<Action> select_sample_batch(const BehaviorPolicy& beh,
+                                        std::span<const ShaderState> states, SplitMix64& rng) {
+    std::vector<Action> out(states.size());
+    if (states.empty()) return out;
+    std::vector<float> feat;
+    flatten_states(states, feat);
+    std::vector<std::uint8_t> act(states.size());
+    const auto p = beh.net.flat();
+    check(gbxcu_sample_batch(ctx(), p.data(), feat.data(), states.size(), rng.state(), act.data()));
+    rng.discard(states.size());
     for (std::size_t i = 0; i < act.size(); ++i) out[i] = act[i] ? Action::Wave64 : Action::Wave32;
     return out;
 }

@@ -195,11 +195,11 @@ int check_launch(gbxcu_ctx* c, const char* what) {
 int run_forward(gbxcu_ctx* c, const float* d_params, const float* d_feat, size_t n,
                 double* d_probs, uint8_t* d_actions, int mode, const uint64_t* d_seg_off,
                 size_t nseg, const uint64_t* d_seg_seed, double eps, cudaStream_t st,
-                DevBuf& recheck, DevBuf& counters, DevBuf& flags) {
+                DevBuf& recheck, DevBuf& counters, DevBuf& flags, int extra_bits = 0) {
     if (n == 0) return GBXCU_OK;
     if (n > 0xFFFFFFFFull) return fail(GBXCU_EINVAL, "batch too large (> 2^32 states)");
     const int bits = (d_probs ? FWD_PROBS : 0) | (d_actions ? FWD_ACTIONS : 0) |
-                     (d_seg_off ? FWD_COLLECT : 0);
+                     (d_seg_off ? FWD_COLLECT : 0) | extra_bits;
     RET(counters.ensure(16));
     RET(flags.ensure(16));
     CK(cudaMemsetAsync(counters.p, 0, 16, st));
@@ -692,6 +692,32 @@ int gbxcu_collect(gbxcu_ctx* c, const float* params, const float* feat, const ui
     RET(run_forward(c, c->params.as<float>(), c->feat.as<float>(), n, nullptr,
                     c->actions.as<uint8_t>(), GBXCU_FWD_FAST, c->seg_off.as<uint64_t>(), nseg,
                     c->seg_seed.as<uint64_t>(), eps, st, c->recheck, c->counters, c->flags));
+    RET(check_flags(c->flags, st));
+    CK(cudaMemcpyAsync(actions, c->actions.p, n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return GBXCU_OK;
+}
+
+int gbxcu_forward_batch(gbxcu_ctx* c, const float* params, const float* feat, size_t n,
+                        double* probs, uint8_t* actions) {
+    return gbxcu_forward(c, params, feat, n, probs, actions, GBXCU_FWD_FAST);
+}
+
+int gbxcu_sample_batch(gbxcu_ctx* c, const float* params, const float* feat, size_t n,
+                       uint64_t rng_state, uint8_t* actions) {
+    if (!c || !params || (n && !feat) || !actions) return fail(GBXCU_EINVAL, "null argument");
+    if (n == 0) return GBXCU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    RET(upload(c->params, params, NP, st));
+    RET(upload(c->feat, feat, n * F, st));
+    RET(upload(c->seg_seed, &rng_state, 1, st));
+    RET(c->actions.ensure(n));
+    RET(run_forward(c, c->params.as<float>(), c->feat.as<float>(), n, nullptr,
+                    c->actions.as<uint8_t>(), GBXCU_FWD_FAST, nullptr, 0,
+                    c->seg_seed.as<uint64_t>(), 0.0, st, c->recheck, c->counters, c->flags,
+                    FWD_SAMPLE));
     RET(check_flags(c->flags, st));
     CK(cudaMemcpyAsync(actions, c->actions.p, n, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -190,7 +190,13 @@ __device__ __forceinline__ void fast_finish(const FastSmem& S, size_t s, float l
     const float p0 = e0 / (e0 + e1);
     bool ambiguous;
     uint8_t act;
-    if (mode & 4) {
+    if (mode & 8) {
+        // select_sample over one stream: state s takes draw s + 1 of seg_seed[0]
+        const double ua = unit_of(sm_draw(seg_seed[0], (uint64_t)s + 1));
+        const double tol = 0.25 * (double)T + 16.0 * 5.9604645e-8;
+        ambiguous = fabs(ua - (double)p0) <= tol;
+        act = ua < (double)p0 ? 0 : 1;
+    } else if (mode & 4) {
         // collection: find this state's segment and its two draws
         size_t lo = 0, hi = nseg;  // seg_off[lo] <= s < seg_off[hi]
         while (hi - lo > 1) {
@@ -475,7 +481,9 @@ __device__ __forceinline__ void exact_finish(size_t s, double p0, double p1,
                                              const uint64_t* __restrict__ seg_seed, double eps,
                                              int mode) {
     uint8_t act;
-    if (mode & 4) {
+    if (mode & 8) {
+        act = unit_of(sm_draw(seg_seed[0], (uint64_t)s + 1)) < p0 ? 0 : 1;
+    } else if (mode & 4) {
         size_t lo = 0, hi = nseg;
         while (hi - lo > 1) {
             const size_t mid = (lo + hi) >> 1;

@@ -18,7 +18,7 @@ constexpr int PSTR = 5028;        // per-CTA partial row: 5,026 gradient entries
 constexpr int MAX_PEERS = 8;      // ranks of one NVLink domain (one node)
 
 // mode bits for the inference kernels
-constexpr int FWD_PROBS = 1, FWD_ACTIONS = 2, FWD_COLLECT = 4;
+constexpr int FWD_PROBS = 1, FWD_ACTIONS = 2, FWD_COLLECT = 4, FWD_SAMPLE = 8;
 
 struct TrainArgs {
     const float* feat;

@@ -134,6 +134,20 @@ TEST_CASE("greedy actions are bit-identical (per-state and batched)") {
     }
 }
 
+TEST_CASE("batched select_sample equals select_sample in order; the stream advances alike") {
+    const auto data = g1(8, 5000);
+    BehaviorPolicy beh{PolicyNet::init(4), 1, 0};
+    std::vector<ShaderState> states;
+    for (const auto& r : data) states.push_back(r.first);
+    SplitMix64 a(777), b(777);
+    const auto got = select_sample_batch(beh, states, a);
+    std::size_t diff = 0;
+    for (std::size_t i = 0; i < states.size(); ++i)
+        diff += got[i] != select_sample(beh, states[i], b);
+    CHECK(diff == 0);
+    CHECK(a.state() == b.state());
+}
+
 TEST_CASE("q-table load + snapshot equals the reference's dataset") {
     const char* text =
         "gbx-qtable 1 0.3 0.99\n"

@@ -107,6 +107,33 @@ def test_forward_recheck_path_is_bit_exact(dev, orc):
                                   orc.collect(p, feat, seg, seeds, 0.1))
 
 
+def _splitmix_units(state: int, n: int) -> np.ndarray:
+    """The first n next_unit() of SplitMix64(state) (proj/include/gbx/rng.hpp)."""
+    with np.errstate(over="ignore"):
+        k = np.arange(1, n + 1, dtype=np.uint64)
+        z = np.uint64(state) + k * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+@pytest.mark.parametrize("tag", ["init", "trained"])
+def test_sample_batch_is_sequential_select_sample(dev, orc, tag):
+    """select_sample over a batch from one stream (SURVEY §8b gbxcu_sample_batch):
+    state j uses the (j+1)-th draw; Wave32 iff u < p0 of the fp64 reference."""
+    p = golden("forward_g1")[f"params_{tag}"]
+    feat, _ = orc.g1(77, 60_000)
+    probs_o, _ = orc.forward(p, feat)
+    for state in (0, 12345, 2**64 - 3):
+        u = _splitmix_units(state, len(feat))
+        want = np.where(u < probs_o[:, 0], 0, 1).astype(np.uint8)
+        np.testing.assert_array_equal(dev.sample_batch(p, feat, state), want)
+    # near-ties: u drawn right at p0 go through the exact re-check
+    np.testing.assert_array_equal(dev.sample_batch(p, feat[:1000], 99),
+                                  np.where(_splitmix_units(99, 1000) < probs_o[:1000, 0], 0, 1))
+
+
 def test_forward_rejects_non_finite(dev, orc):
     feat, _ = orc.g1(5, 64)
     feat[17, 10] = np.nan
