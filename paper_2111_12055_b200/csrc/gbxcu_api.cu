@@ -214,7 +214,7 @@ int run_forward(gbxcu_ctx* c, const float* d_params, const float* d_feat, size_t
             recheck.as<uint32_t>(), counters.as<unsigned int>(), flags.as<unsigned int>(), bits);
         RET(check_launch(c, "fwd_fast_kernel"));
         // the list length stays on the device: a fixed grid, idle blocks exit at once
-        fwd_recheck_kernel<<<c->num_sms * 2, RECHECK_BLOCK, recheck_smem_bytes(), st>>>(
+        fwd_recheck_kernel<<<c->num_sms * 3, RECHECK_BLOCK, recheck_smem_bytes(), st>>>(
             d_params, d_feat, recheck.as<uint32_t>(), counters.as<unsigned int>(), d_probs,
             d_actions, d_seg_off, nseg, d_seg_seed, eps, bits);
         RET(check_launch(c, "fwd_recheck_kernel"));

@@ -542,17 +542,22 @@ fwd_exact_kernel(const float* __restrict__ params, const float* __restrict__ fea
 // i ascending; lane k: acc2_k over j ascending; lane 2s+a: logit a of state s
 // over k ascending), so the results are bit-identical.
 constexpr int RS = 4;
+struct RecheckScratch {
+    double xs[RECHECK_BLOCK / 32][RS][F];
+    double h1[RECHECK_BLOCK / 32][RS][H1];
+    double h2[RECHECK_BLOCK / 32][RS][H2];
+};
 struct RecheckSmem {
-    __align__(16) float raw[NP + 2];  // staged parameters
     double w0t[F * H1];  // [i][j]: lane j reads consecutive words
     double w1t[H1 * H2]; // [j][k]
     double w2[A * H2];   // [a][k]
     double b0[H1];
     double b1[H2];
     double b2[A];
-    double xs[RECHECK_BLOCK / 32][RS][F];
-    double h1[RECHECK_BLOCK / 32][RS][H1];
-    double h2[RECHECK_BLOCK / 32][RS][H2];
+    union {  // the staged parameters are dead once the fp64 copies exist
+        __align__(16) float raw[NP + 2];
+        RecheckScratch sc;
+    };
 };
 
 __global__ void __launch_bounds__(RECHECK_BLOCK)
@@ -590,8 +595,8 @@ fwd_recheck_kernel(const float* __restrict__ params, const float* __restrict__ f
 #pragma unroll
         for (int r = 0; r < RS; ++r) {
             const float* xrow = feat + sid[r] * F;
-            S.xs[w][r][lane] = r < nv ? (double)__ldg(xrow + lane) : 0.0;
-            if (lane + 32 < F) S.xs[w][r][lane + 32] = r < nv ? (double)__ldg(xrow + lane + 32) : 0.0;
+            S.sc.xs[w][r][lane] = r < nv ? (double)__ldg(xrow + lane) : 0.0;
+            if (lane + 32 < F) S.sc.xs[w][r][lane + 32] = r < nv ? (double)__ldg(xrow + lane + 32) : 0.0;
         }
         __syncwarp();
         double za[RS], zb[RS];
@@ -602,15 +607,15 @@ fwd_recheck_kernel(const float* __restrict__ params, const float* __restrict__ f
             const double wa = S.w0t[i * H1 + lane], wb = S.w0t[i * H1 + lane + 32];
 #pragma unroll
             for (int r = 0; r < RS; ++r) {
-                const double x = S.xs[w][r][i];
+                const double x = S.sc.xs[w][r][i];
                 za[r] = fma(wa, x, za[r]);  // exact products: fma == mul-then-add
                 zb[r] = fma(wb, x, zb[r]);
             }
         }
 #pragma unroll
         for (int r = 0; r < RS; ++r) {
-            S.h1[w][r][lane] = za[r] > 0.0 ? za[r] : 0.0;
-            S.h1[w][r][lane + 32] = zb[r] > 0.0 ? zb[r] : 0.0;
+            S.sc.h1[w][r][lane] = za[r] > 0.0 ? za[r] : 0.0;
+            S.sc.h1[w][r][lane + 32] = zb[r] > 0.0 ? zb[r] : 0.0;
         }
         __syncwarp();
         double acc[RS];
@@ -620,16 +625,16 @@ fwd_recheck_kernel(const float* __restrict__ params, const float* __restrict__ f
         for (int j = 0; j < H1; ++j) {
             const double wv = S.w1t[j * H2 + lane];
 #pragma unroll
-            for (int r = 0; r < RS; ++r) acc[r] = madd_rn(acc[r], wv, S.h1[w][r][j]);
+            for (int r = 0; r < RS; ++r) acc[r] = madd_rn(acc[r], wv, S.sc.h1[w][r][j]);
         }
 #pragma unroll
-        for (int r = 0; r < RS; ++r) S.h2[w][r][lane] = acc[r] > 0.0 ? acc[r] : 0.0;
+        for (int r = 0; r < RS; ++r) S.sc.h2[w][r][lane] = acc[r] > 0.0 ? acc[r] : 0.0;
         __syncwarp();
         // lane 2r + a: logit a of state r
         const int lr = min(lane >> 1, RS - 1), la = lane & 1;
         double l = S.b2[la];
 #pragma unroll 8
-        for (int k = 0; k < H2; ++k) l = madd_rn(l, S.w2[la * H2 + k], S.h2[w][lr][k]);
+        for (int k = 0; k < H2; ++k) l = madd_rn(l, S.w2[la * H2 + k], S.sc.h2[w][lr][k]);
         const double l1 = __shfl_down_sync(0xffffffffu, l, 1);
         if (la == 0 && (lane >> 1) < nv) {
             const double l0 = l;
