@@ -275,12 +275,33 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = gbx.Device(local)
+    dp_note = None
     if world > 1 and args.dp == "fused":
+        # the fused peer set needs CUDA IPC between the ranks' GPUs; if any rank
+        # cannot export/attach, every rank falls back to the NCCL path together
+        ok_attach = 1
         handles = [None] * world
-        dist.all_gather_object(handles, dev.peer_export())
-        dev.peer_attach(handles, rank)
+        try:
+            h = dev.peer_export()
+        except (gbx.CudaError, gbx.ValidationError) as e:
+            h, dp_note = None, f"peer export failed: {e}"
+        dist.all_gather_object(handles, h)
+        if any(x is None for x in handles):
+            ok_attach = 0
+        else:
+            try:
+                dev.peer_attach(handles, rank)
+            except (gbx.CudaError, gbx.ValidationError) as e:
+                ok_attach, dp_note = 0, f"peer attach failed: {e}"
+        flags = [None] * world
+        dist.all_gather_object(flags, ok_attach)
+        if not all(flags):
+            dp_note = dp_note or "a peer rank could not attach the exchange regions"
+            if ok_attach:
+                dev.peer_detach()
+            args.dp = "nccl"
         dist.barrier()
-    elif world > 1:
+    if world > 1 and args.dp == "nccl":
         uid = [gbx.Device.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         dev.comm_init(uid[0], world, rank)
@@ -310,7 +331,6 @@ def main():
         kernel_ms["shuffle"] += sh
         kernel_ms["train"] += tr
 
-    dp_note = None
     try:
         step()
         ok = torch.tensor([1], device="cuda")
