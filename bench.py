@@ -497,6 +497,9 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
             "hbm_gbs": rate * 177 / 1e9}
         if mode == gbx.FWD_FAST:
             out["inference"][name]["recheck_fraction"] = dev.last_recheck_count() / n
+        if fp32_peak:
+            # FFMA-bound path (9,856 FLOP/state): fraction of the measured FFMA peak
+            out["inference"][name]["roofline_frac_fp32"] = rate * 9856 / 1e12 / fp32_peak
     out["inference"]["fp32_peak_tflops_measured"] = fp32_peak
     out["inference"]["hbm_peak_gbs"] = peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)
     if not args.no_cpu_baseline:
@@ -520,7 +523,7 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
     tgt_n = torch.empty((feat_n, 2), dtype=torch.float64, device="cuda")
     tgt_n[:, 0] = 0.5
     tgt_n[:, 1] = 0.5
-    for b in (32, 65536):
+    for b in (32, 4096, 16384, 65536):
         p_b = params_d.clone()
         dev.fit_dev(p_b.data_ptr(), feat_d.data_ptr(), tgt_n.data_ptr(), feat_n, args.lr, 1, b, 99,
                     stream=dev.stream)
