@@ -116,7 +116,14 @@ struct gbxcu_ctx {
     int fast_per_sm = 1;
     // wide MLP (C4) working set
     DevBuf w_params, w_grad, w_w1t, w_h1, w_h1t, w_h2, w_d2, w_d2t, w_d1t, w_xt, w_d3, w_kl;
-    DevBuf w_part, w_g4, w_g5, w_loss, w_feat, w_tgt, w_probs, w_xg, w_w0p;
+    DevBuf w_part, w_g4, w_g5, w_loss, w_feat, w_tgt, w_probs, w_xg, w_w0p, w_epoch;
+    // CUDA graphs of a wide-MLP epoch's step sequence (one per epoch-permutation
+    // buffer), keyed on every pointer and size they bake in
+    struct WideGraph {
+        std::vector<const void*> key;
+        cudaGraphExec_t exec = nullptr;
+    } wg[2];
+    int wg_next = 0;
     // data parallel
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
@@ -601,6 +608,8 @@ void gbxcu_destroy(gbxcu_ctx* c) {
         if (p) cudaIpcCloseMemHandle(p);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& g : c->wg)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->hres) cudaFreeHost(c->hres);
     delete c;
@@ -1625,7 +1634,7 @@ int blocks(size_t n, int t = 256) { return (int)std::max<size_t>(1, (n + t - 1) 
 
 // One SGD step on rows[0, nbr) (this rank's slice of a global batch of nb).
 int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tgt,
-              const uint32_t* rows, int nbr, size_t nb, size_t ldt, double lr, int epoch,
+              const uint32_t* rows, int nbr, size_t nb, size_t ldt, double lr, const int* epoch,
               int splits4, int splits5, int rsplit, cudaStream_t st) {
     const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H,
                  o_w2 = o_b1 + H;
@@ -1737,17 +1746,66 @@ int wide_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, c
                                                                         c->w_w0p.as<float>());
     RET(check_launch(c, "wide_w1t_kernel"));
     const long n_steps = (long)((n + cfg->batch_size - 1) / cfg->batch_size);
-    for (int e = 0; e < cfg->epochs; ++e) {
-        RET(shuffle_epoch(c, n, cfg->seed, e, st));
-        CK(cudaMemsetAsync(c->epoch_acc.p, 0, sizeof(double), st));
-        const uint32_t* order = c->order.as<uint32_t>();
+    RET(c->w_epoch.ensure(16));
+    auto run_steps = [&](const uint32_t* order) -> int {
         for (long s = 0; s < n_steps; ++s) {
             const size_t start = (size_t)s * cfg->batch_size;
             const size_t nb = std::min(n, start + (size_t)cfg->batch_size) - start;
             const size_t per = (nb + c->nranks - 1) / c->nranks;
             const size_t lo = std::min(nb, (size_t)c->rank * per), hi = std::min(nb, lo + per);
             RET(wide_step(c, H, d_params, d_feat, d_tgt, order + start + lo, (int)(hi - lo), nb, ldt,
-                          cfg->learning_rate, e, splits4, splits5, rsplit, st));
+                          cfg->learning_rate, c->w_epoch.as<int>(), splits4, splits5, rsplit, st));
+        }
+        return GBXCU_OK;
+    };
+    // one epoch = ~12 launches per step, most of them short: replay them as a
+    // CUDA graph (single-GPU path; NCCL steps launch directly)
+    const bool use_graph = !c->comm && n_steps > 1;
+    for (int e = 0; e < cfg->epochs; ++e) {
+        RET(shuffle_epoch(c, n, cfg->seed, e, st));
+        CK(cudaMemsetAsync(c->epoch_acc.p, 0, sizeof(double), st));
+        CK(cudaMemcpyAsync(c->w_epoch.p, &e, sizeof(int), cudaMemcpyHostToDevice, st));
+        const uint32_t* order = c->order.as<uint32_t>();
+        if (!use_graph) {
+            RET(run_steps(order));
+        } else {
+            double lr = cfg->learning_rate;
+            uint64_t lr_bits;
+            std::memcpy(&lr_bits, &lr, 8);
+            const std::vector<const void*> key = {
+                order, d_params, d_feat, d_tgt, (const void*)(uintptr_t)H, (const void*)n,
+                (const void*)(uintptr_t)cfg->batch_size, (const void*)(uintptr_t)lr_bits,
+                (const void*)ldt, (const void*)(uintptr_t)splits4, (const void*)(uintptr_t)splits5,
+                c->w_grad.p, c->w_w1t.p, c->w_h1.p, c->w_h2.p, c->w_d2.p, c->w_h1t.p, c->w_d2t.p,
+                c->w_d1t.p, c->w_xt.p, c->w_xg.p, c->w_w0p.p, c->w_d3.p, c->w_kl.p, c->w_part.p,
+                c->w_g4.p, c->w_g5.p, c->w_loss.p, c->w_epoch.p, c->diverged.p, c->epoch_acc.p};
+            gbxcu_ctx::WideGraph* g = nullptr;
+            for (auto& x : c->wg)
+                if (x.exec && x.key == key) g = &x;
+            if (!g) {
+                g = &c->wg[c->wg_next];
+                c->wg_next ^= 1;
+                if (g->exec) cudaGraphExecDestroy(g->exec);
+                g->exec = nullptr;
+                g->key.clear();
+                CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                const int rc = run_steps(order);
+                cudaGraph_t graph = nullptr;
+                const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+                if (rc != GBXCU_OK) {
+                    if (graph) cudaGraphDestroy(graph);
+                    return rc;
+                }
+                if (ce != cudaSuccess) return fail(GBXCU_ECUDA, "wide-step graph capture failed");
+                const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+                cudaGraphDestroy(graph);
+                if (ie != cudaSuccess) {
+                    g->exec = nullptr;
+                    return fail(GBXCU_ECUDA, "wide-step graph instantiation failed");
+                }
+                g->key = key;
+            }
+            CK(cudaGraphLaunch(g->exec, st));
         }
         finish_epoch_kernel<<<1, 1, 0, st>>>(c->epoch_acc.as<double>(), n, e, c->diverged.as<int>(),
                                               c->epoch_loss.as<double>());

@@ -615,13 +615,13 @@ __global__ void split_reduce_f64_kernel(const double* __restrict__ src, int spli
 // grad/params in serialization order: w0[H][44] b0[H] w1[H][H] b1[H] w2[2][H] b2[2].
 __global__ void wide_update_kernel(float* __restrict__ params, const float* __restrict__ grad,
                                    const double* __restrict__ loss_sum, size_t nb, double lr,
-                                   int hidden, float* __restrict__ w1t, float* __restrict__ w0p, int epoch,
-                                   int* __restrict__ diverged, double* __restrict__ epoch_acc,
-                                   size_t np) {
+                                   int hidden, float* __restrict__ w1t, float* __restrict__ w0p,
+                                   const int* __restrict__ epoch, int* __restrict__ diverged,
+                                   double* __restrict__ epoch_acc, size_t np) {
     if (*diverged >= 0) return;
     const double loss = *loss_sum / (double)nb;
     if (!isfinite(loss)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) *diverged = epoch;
+        if (blockIdx.x == 0 && threadIdx.x == 0) *diverged = *epoch;
         return;
     }
     const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -175,8 +175,8 @@ __global__ void split_reduce_f32_kernel(const float* src, int splits, size_t str
 __global__ void split_reduce_f64_kernel(const double* src, int splits, int n, float* dst,
                                         double* loss_out);
 __global__ void wide_update_kernel(float* params, const float* grad, const double* loss_sum,
-                                   size_t nb, double lr, int hidden, float* w1t, float* w0p, int epoch,
-                                   int* diverged, double* epoch_acc, size_t np);
+                                   size_t nb, double lr, int hidden, float* w1t, float* w0p,
+                                   const int* epoch, int* diverged, double* epoch_acc, size_t np);
 __global__ void wide_w1t_kernel(const float* params, int hidden, float* w1t, float* w0p);
 __global__ void wide_gw0_kernel(const float* src, int splits, size_t stride, int hidden, float* dst,
                                 float* gb0);
