@@ -211,22 +211,58 @@ double TrainConfig::rho_at(int iteration) const {
     return std::max(rho_min, rho0 * std::pow(rho_decay, iteration));
 }
 
+namespace {
+FitResult fit_flat(PolicyNet& net, const std::vector<float>& feat, const std::vector<double>& tgt,
+                   std::size_t n, const TrainConfig& cfg, int loss_mode, const OptimizerConfig& opt);
+}  // namespace
+
 FitResult fit(PolicyNet& net, const PolicyDataset& dataset, const TrainConfig& cfg) {
+    return fit(net, dataset, cfg, OptimizerConfig{});
+}
+
+FitResult fit(PolicyNet& net, const PolicyDataset& dataset, const TrainConfig& cfg,
+              const OptimizerConfig& opt) {
     cfg.validate();
     if (dataset.empty()) throw ValidationError("fit requires a non-empty dataset");
     std::vector<float> feat;
     std::vector<double> tgt;
     flatten_records(dataset, feat, tgt);
+    return fit_flat(net, feat, tgt, dataset.size(), cfg, GBXCU_LOSS_KL, opt);
+}
+
+FitResult fit_td(PolicyNet& net, std::span<const ExperienceRecord> records, const TrainConfig& cfg,
+                 const OptimizerConfig& opt) {
+    cfg.validate();
+    if (records.empty()) throw ValidationError("fit requires a non-empty dataset");
+    std::vector<float> feat(records.size() * kFeatureCount);
+    std::vector<double> tgt(records.size() * 2);
+    for (std::size_t r = 0; r < records.size(); ++r) {
+        for (int i = 0; i < kFeatureCount; ++i) feat[r * kFeatureCount + i] = records[r].state.features[i];
+        tgt[2 * r] = records[r].action == Action::Wave64 ? 1.0 : 0.0;
+        tgt[2 * r + 1] = records[r].reward;
+    }
+    return fit_flat(net, feat, tgt, records.size(), cfg, GBXCU_LOSS_TD, opt);
+}
+
+namespace {
+FitResult fit_flat(PolicyNet& net, const std::vector<float>& feat, const std::vector<double>& tgt,
+                   std::size_t n, const TrainConfig& cfg, int loss_mode, const OptimizerConfig& opt) {
     auto p = net.flat();
     gbxcu_train_cfg c{};  // zeros: the reference's KL loss + SGD, no CTA cap, no virtual ranks
     c.learning_rate = cfg.learning_rate;
     c.epochs = cfg.epochs;
     c.batch_size = cfg.batch_size;
     c.seed = cfg.seed;
+    c.loss_mode = loss_mode;
+    c.optimizer = opt.kind == OptimizerKind::Adam ? GBXCU_OPT_ADAM : GBXCU_OPT_SGD;
+    c.adam_beta1 = opt.beta1;
+    c.adam_beta2 = opt.beta2;
+    c.adam_eps = opt.eps;
+    const std::size_t dataset_size = n;
     FitResult res;
     res.epoch_loss.assign(cfg.epochs, 0.0);
     int diverged = -1;
-    const int rc = gbxcu_fit(ctx(), p.data(), feat.data(), tgt.data(), dataset.size(), &c,
+    const int rc = gbxcu_fit(ctx(), p.data(), feat.data(), tgt.data(), dataset_size, &c,
                              res.epoch_loss.data(), &diverged);
     if (rc == GBXCU_OK || rc == GBXCU_EDIVERGED) net = PolicyNet::from_flat(p);
     if (rc == GBXCU_EDIVERGED)
@@ -235,6 +271,7 @@ FitResult fit(PolicyNet& net, const PolicyDataset& dataset, const TrainConfig& c
     check(rc);
     return res;
 }
+}  // namespace
 
 // ---------------------------------------------------------------- actions
 Action select_greedy(const BehaviorPolicy& beh, const ShaderState& s) {

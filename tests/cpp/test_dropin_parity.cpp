@@ -148,6 +148,36 @@ TEST_CASE("batched select_sample equals select_sample in order; the stream advan
     CHECK(a.state() == b.state());
 }
 
+TEST_CASE("variants (extension): TD regression and Adam through the drop-in") {
+    const auto data = g1(3, 4000);
+    std::vector<ExperienceRecord> recs;
+    SplitMix64 rng(5);
+    for (const auto& r : data) {
+        const Action a = rng.next_unit() < 0.5 ? Action::Wave32 : Action::Wave64;
+        recs.push_back({r.first, a, 0.5 + 0.1 * r.first.features[8] * (a == Action::Wave64 ? 1 : -1)});
+    }
+    TrainConfig cfg;
+    cfg.learning_rate = 1e-3;
+    cfg.epochs = 4;
+    cfg.batch_size = 64;
+    cfg.seed = 3;
+    OptimizerConfig adam;
+    adam.kind = OptimizerKind::Adam;
+    PolicyNet a = PolicyNet::init(1), b = PolicyNet::init(1);
+    const auto ra = fit_td(a, recs, cfg, adam);
+    const auto rb = fit_td(b, recs, cfg, adam);
+    CHECK(ra.epoch_loss == rb.epoch_loss);            // deterministic
+    CHECK(a.flat() == b.flat());
+    CHECK(ra.epoch_loss.back() < 0.7 * ra.epoch_loss.front());  // it learns
+    PolicyNet s = PolicyNet::init(2), m = PolicyNet::init(2);
+    fit(s, data, cfg);
+    fit(m, data, cfg, adam);
+    CHECK(s.flat() != m.flat());
+    recs[7].reward = std::numeric_limits<double>::infinity();
+    PolicyNet d = PolicyNet::init(1);
+    CHECK_THROWS_AS(fit_td(d, recs, cfg), TrainingDivergedError);
+}
+
 TEST_CASE("q-table load + snapshot equals the reference's dataset") {
     const char* text =
         "gbx-qtable 1 0.3 0.99\n"
