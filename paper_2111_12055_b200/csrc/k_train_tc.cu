@@ -818,18 +818,48 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
             double v = 0.0;
             if (e < n_elem) {
                 const int p = e == 0 ? NP : p_lo + e - 1;
-                for (int r = 0; r < R; ++r) {
-                    // all of this rank's loads in flight at once (one round trip)
-                    const double* src = a.part[r] + p;
-                    double u[20];
+                if constexpr (!SYS) {
+                    // one GPU (R = 1, or virtual ranks in tests): per rank, all
+                    // of its loads in flight at once (one L2 round trip)
+                    for (int r = 0; r < R; ++r) {
+                        const double* src = a.part[r] + p;
+                        double u[20];
 #pragma unroll
-                    for (int j = 0; j < 20; ++j) {
-                        const int q = sb + j * SUB;
-                        u[j] = q < Gl ? ld_part<SYS>(src + (size_t)q * PSTR) : 0.0;
+                        for (int j = 0; j < 20; ++j) {
+                            const int q = sb + j * SUB;
+                            u[j] = q < Gl ? ld_part<SYS>(src + (size_t)q * PSTR) : 0.0;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 20; ++j) v += u[j];
+                        for (int q = sb + 20 * SUB; q < Gl; q += SUB)
+                            v += ld_part<SYS>(src + (size_t)q * PSTR);
                     }
+                } else {
+                    // the (rank, CTA) pairs of this thread — rank by rank, CTAs
+                    // c' = s, s + SUB, ... — with up to 32 loads in flight across
+                    // ALL ranks (one round trip over NVLink, not one per rank),
+                    // summed in that fixed order afterwards
+                    const int nq = (Gl - sb + SUB - 1) / SUB;  // CTAs per rank for this thread
+                    const int total = R * nq;
+                    int t0 = 0;
+                    while (t0 < total) {
+                        double u[32];
+                        int r = t0 / max(nq, 1), qi = t0 - r * max(nq, 1);
 #pragma unroll
-                    for (int j = 0; j < 20; ++j) v += u[j];
-                    for (int q = sb + 20 * SUB; q < Gl; q += SUB) v += ld_part<SYS>(src + (size_t)q * PSTR);
+                        for (int j = 0; j < 32; ++j) {
+                            const bool ok = t0 + j < total;
+                            u[j] = ok ? ld_part<SYS>(a.part[ok ? r : 0] + p + (size_t)(sb + qi * SUB) * PSTR)
+                                      : 0.0;
+                            if (++qi == nq) {
+                                qi = 0;
+                                ++r;
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (t0 + j < total) v += u[j];
+                        t0 += 32;
+                    }
                 }
             }
             S.red[sb * EB + tid % EB] = v;
