@@ -176,6 +176,16 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsig
     if (SYS) asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
     else asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+template <bool SYS>
+__device__ __forceinline__ void red_relaxed_add_u64(unsigned long long* p, unsigned long long v) {
+    if (SYS) asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ void fence_acq_rel() {
+    if (SYS) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ unsigned long long gtimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -782,7 +792,14 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         // ---- 2. arrive on every rank's counter; wait (warp 0) until all GG
         //      CTAs of the set arrived while warps 1..15 stage the next tile
         if (tid == 0) {
-            for (int r = 0; r < R; ++r) red_release_add_u64<SYS>(a.ctr[r], 1ull);
+            if (R == 1) {
+                red_release_add_u64<SYS>(a.ctr[0], 1ull);
+            } else {
+                // one release fence for all ranks' counters (a release red per
+                // rank would fence R times), then relaxed reds
+                fence_acq_rel<SYS>();
+                for (int r = 0; r < R; ++r) red_relaxed_add_u64<SYS>(a.ctr[r], 1ull);
+            }
             TC_MARK(7);
             TC_TRACE(step, 1);
             const unsigned long long target =
