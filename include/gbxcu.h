@@ -287,6 +287,14 @@ void gbxcu_suite_free(gbxcu_dsuite* s);
 /* Raw device pointers of an uploaded suite (features [n_shaders][44] fp32). */
 const float* gbxcu_suite_features(const gbxcu_dsuite* s);
 
+/* One app-range shard of evaluate (multi-GPU: each rank evaluates
+ * [app_lo, app_hi) of the same uploaded suite, inferring only the shaders
+ * those apps reference; seeds use global app indices, so the gathered rows
+ * equal gbxcu_evaluate's bit for bit and the histogram is built once from
+ * them — SURVEY §8e). rows_out [app_hi - app_lo][5]. */
+int gbxcu_evaluate_shard(gbxcu_ctx* ctx, const gbxcu_dsuite* suite, const float* params,
+                         int n_samples, uint64_t seed, size_t app_lo, size_t app_hi,
+                         double* rows_out);
 /* Greedy evaluation sweep = evaluate() (proj/src/tuner.cpp:266-315):
  * inference over every shader, per-app aggregation with
  * run_seed = derive_seed({seed, 0x45564C, app}), uplift rows + histogram.

@@ -109,7 +109,7 @@ EXPORTS = (
     "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_last_recheck_count", "gbxcu_peer_export",
     "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free", "gbxcu_qtable_clear",
     "gbxcu_qtable_update_batch", "gbxcu_qtable_update_batch_dev", "gbxcu_qtable_size",
-    "gbxcu_forward_batch", "gbxcu_sample_batch",
+    "gbxcu_forward_batch", "gbxcu_sample_batch", "gbxcu_evaluate_shard",
     "gbxcu_qtable_import", "gbxcu_qtable_export", "gbxcu_qtable_save_columnar",
     "gbxcu_qtable_load_columnar",
     "gbxcu_qtable_snapshot", "gbxcu_qtable_snapshot_dev",
@@ -164,6 +164,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_qtable_export.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
     L.gbxcu_qtable_import.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _sz]
     L.gbxcu_forward_batch.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
+    L.gbxcu_evaluate_shard.argtypes = [_vp, _vp, _vp, C.c_int, _u64, _sz, _sz, _vp]
     L.gbxcu_sample_batch.argtypes = [_vp, _vp, _vp, _sz, _u64, _vp]
     L.gbxcu_qtable_save_columnar.argtypes = [_vp, C.c_char_p]
     L.gbxcu_qtable_load_columnar.argtypes = [_vp, C.c_char_p]
@@ -532,6 +533,32 @@ class DeviceSuite:
             C.byref(nb)))
         hist = (lo[:nb.value].copy(), cnt[:nb.value].copy())
         return (rows, hist, act) if want_actions else (rows, hist)
+
+    def evaluate_shard(self, params, n_samples: int, seed: int, app_lo: int, app_hi: int):
+        """Rows [app_hi - app_lo][5] of one app-range shard (gbxcu_evaluate_shard):
+        concatenating the shards' rows gives evaluate()'s rows bit for bit."""
+        rows = np.empty((max(0, app_hi - app_lo), 5), np.float64)
+        self.dev._ck(self.dev.L.gbxcu_evaluate_shard(self.dev.h, self.h, _f32(params).ctypes.data,
+                                                     n_samples, seed & ((1 << 64) - 1), app_lo,
+                                                     app_hi, rows.ctypes.data))
+        return rows
+
+    def evaluate_distributed(self, params, n_samples: int, seed: int, rank: int, world: int,
+                             group=None):
+        """evaluate() sharded by app range over `world` ranks (torch.distributed,
+        any backend): each rank evaluates its range, rank 0 gathers the rows in
+        app order and builds the histogram. Returns (rows, hist) on rank 0,
+        (own rows, None) elsewhere."""
+        import torch.distributed as dist
+        per = (self.n_apps + world - 1) // world
+        lo, hi = min(self.n_apps, rank * per), min(self.n_apps, (rank + 1) * per)
+        mine = self.evaluate_shard(params, n_samples, seed, lo, hi)
+        parts = [None] * world if rank == 0 else None
+        dist.gather_object(mine, parts, dst=0, group=group)
+        if rank != 0:
+            return mine, None
+        rows = np.concatenate([p for p in parts if len(p)], axis=0)
+        return rows, self.dev.histogram(rows[:, 3])
 
     def evaluate_dev(self, d_params: int, n_samples: int, seed: int, d_actions: int, d_rows: int,
                      stream: int | None = None):

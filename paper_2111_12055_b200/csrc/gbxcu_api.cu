@@ -1498,6 +1498,70 @@ static int evaluate_dev(gbxcu_ctx* c, const gbxcu_dsuite* s, const float* d_para
     return check_launch(c, "aggregate_kernel");
 }
 
+// One app-range shard of evaluate (aggregation shards by app so
+// no segment straddles GPUs): infers only the shaders the range's slots
+// reference and aggregates apps [app_lo, app_hi) with their GLOBAL indices in
+// the seeds, so gathering the shards' rows reproduces the unsharded rows bit
+// for bit (the histogram is then built from the gathered uplifts).
+int gbxcu_evaluate_shard(gbxcu_ctx* c, const gbxcu_dsuite* s, const float* params, int n_samples,
+                         uint64_t seed, size_t app_lo, size_t app_hi, double* rows_out) {
+    if (!c || !s || !params || (app_hi > app_lo && !rows_out)) return fail(GBXCU_EINVAL, "null argument");
+    if (app_lo > app_hi || app_hi > s->n_apps) return fail(GBXCU_EINVAL, "app range out of bounds");
+    if (n_samples < 1) return fail(GBXCU_EINVAL, "sample count must be >= 1");
+    if (app_hi == app_lo) return GBXCU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    gbxcu_dsuite* sm = const_cast<gbxcu_dsuite*>(s);
+    RET(upload(sm->params, params, NP, st));
+    RET(sm->actions.ensure(std::max<size_t>(1, s->n_shaders)));
+    RET(sm->rows.ensure(sizeof(double) * 5 * (app_hi - app_lo)));
+    // slot range of the apps, then the shader range those slots reference
+    uint64_t pipes[2], slots[2];
+    CK(cudaMemcpyAsync(&pipes[0], s->app_pipe.as<uint64_t>() + app_lo, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&pipes[1], s->app_pipe.as<uint64_t>() + app_hi, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpyAsync(&slots[0], s->pipe_slot.as<uint64_t>() + pipes[0], 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&slots[1], s->pipe_slot.as<uint64_t>() + pipes[1], 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    RET(sm->counters.ensure(16));
+    unsigned int range[2] = {0xFFFFFFFFu, 0u};
+    if (slots[1] > slots[0]) {
+        CK(cudaMemcpyAsync(sm->counters.p, range, 8, cudaMemcpyHostToDevice, st));
+        slot_shader_range_kernel<<<c->num_sms * 2, 256, 0, st>>>(s->slot_shader.as<uint32_t>(), slots[0],
+                                                                 slots[1], sm->counters.as<unsigned int>());
+        RET(check_launch(c, "slot_shader_range_kernel"));
+        CK(cudaMemcpyAsync(range, sm->counters.p, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (range[1] >= s->n_shaders) return fail(GBXCU_EINVAL, "slot references a missing shader");
+        RET(run_forward(c, sm->params.as<float>(), s->features.as<float>() + (size_t)range[0] * F,
+                        (size_t)range[1] - range[0] + 1, nullptr, sm->actions.as<uint8_t>() + range[0],
+                        GBXCU_FWD_FAST, nullptr, 0, nullptr, 0.0, st, sm->recheck, sm->counters,
+                        sm->flags));
+        RET(check_flags(sm->flags, st));
+    }
+    AggArgs a{};
+    a.n_apps = app_hi - app_lo;
+    a.app_pipe_off = s->app_pipe.as<uint64_t>() + app_lo;
+    a.pipe_slot_off = s->pipe_slot.as<uint64_t>();
+    a.slot_shader = s->slot_shader.as<uint32_t>();
+    a.slot_frac = s->slot_frac.as<double>();
+    a.pipe_wt = s->pipe_wt.as<double>();
+    a.shader_lat = s->shader_lat.as<double>();
+    a.app_f64 = s->app_f64.as<double>() + 4 * app_lo;
+    a.shader_action = sm->actions.as<uint8_t>();
+    a.eval_seed = seed;
+    a.n_samples = n_samples;
+    a.rows = sm->rows.as<double>();
+    a.app_base = app_lo;
+    const int grid = (int)std::min<size_t>((a.n_apps + 7) / 8, (size_t)c->num_sms * 8);
+    aggregate_kernel<<<grid, AGG_BLOCK, 0, st>>>(a);
+    RET(check_launch(c, "aggregate_kernel"));
+    CK(cudaMemcpyAsync(rows_out, sm->rows.p, sizeof(double) * 5 * a.n_apps, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return GBXCU_OK;
+}
+
 int gbxcu_evaluate(gbxcu_ctx* c, const gbxcu_dsuite* s, const float* params, int n_samples,
                    uint64_t seed, double* rows_out, uint8_t* shader_actions_out,
                    double* hist_lower, uint64_t* hist_count, size_t hist_cap, size_t* n_bins) {

@@ -86,9 +86,10 @@ __global__ void __launch_bounds__(AGG_BLOCK) aggregate_kernel(AggArgs a) {
         const double fps = __ddiv_rn(1.0, total);
 
         // noisy samples: SplitMix64(derive_seed({run_seed, 0x4E5A45, app}))
+        const uint64_t gapp = a.app_base + app;  // global app index (shards)
         const uint64_t run_seed =
-            a.run_seed ? a.run_seed[app] : derive_seed3(a.eval_seed, 0x45564Cu, (uint64_t)app);
-        const uint64_t ns = derive_seed3(run_seed, 0x4E5A45u, (uint64_t)app);
+            a.run_seed ? a.run_seed[app] : derive_seed3(a.eval_seed, 0x45564Cu, gapp);
+        const uint64_t ns = derive_seed3(run_seed, 0x4E5A45u, gapp);
         const double half = __dmul_rn(sigma, sqrt(3.0));
         double sum = 0.0;
         for (int k0 = 0; k0 < a.n_samples; k0 += 32) {
@@ -160,6 +161,27 @@ histogram_kernel(const double* __restrict__ rows, int stride, size_t n, double* 
         unsigned long long idx = __double2ull_rz(__dsub_rn(rows[k * stride + 3], lw));
         if (idx > bins - 1) idx = bins - 1;
         if (idx < cap) atomicAdd(count + idx, 1ull);
+    }
+}
+
+// [min, max] shader index referenced by slots [s_lo, s_hi) (an app-range
+// shard infers only that shader range).
+__global__ void slot_shader_range_kernel(const uint32_t* __restrict__ slot_shader, uint64_t s_lo,
+                                         uint64_t s_hi, unsigned int* __restrict__ range) {
+    unsigned int mn = 0xFFFFFFFFu, mx = 0u;
+    for (uint64_t s = s_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < s_hi;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned int v = slot_shader[s];
+        mn = min(mn, v);
+        mx = max(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(range, mn);
+        atomicMax(range + 1, mx);
     }
 }
 

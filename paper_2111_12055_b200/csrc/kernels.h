@@ -70,7 +70,10 @@ struct AggArgs {
     int n_samples;
     double* rows;              // [n_apps][5]
     double* samples;           // nullable [n_apps][n_samples]
+    size_t app_base;           // global index of app 0 (seeds of an app-range shard)
 };
+__global__ void slot_shader_range_kernel(const uint32_t* slot_shader, uint64_t s_lo, uint64_t s_hi,
+                                         unsigned int* range /* [min, max] */);
 
 __global__ void policy_init_kernel(uint64_t seed, float* params);
 __global__ void fwd_fast_kernel(const float* params, const float* feat, size_t n, double* probs,

@@ -385,3 +385,36 @@ def test_fit_peer_set_multi_epoch_many_tiles(dev, orc, vranks):
     p, el = dev.fit(p0, f, t, 0.02, 3, 20_000, 12, virtual_ranks=vranks)
     assert ulps32(p, p_ref).max() <= 2
     np.testing.assert_allclose(el, el_ref, rtol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["suite_free", "suite_contended"])
+def test_evaluate_shards_reassemble_bit_exact(dev, orc, name):
+    """aggregation sharded by app range — concatenated shard rows
+    equal evaluate()'s, and so does the histogram built from them."""
+    s = dict(golden(name))
+    ds = dev.suite_upload(s, s["features"])
+    rows, (lo, cnt) = ds.evaluate(s["eval_params"], 10, int(s["eval_seed"]))
+    na = ds.n_apps
+    for cuts in ([0, na], [0, na // 3, na], [0, 1, na // 2, na - 1, na]):
+        parts = [ds.evaluate_shard(s["eval_params"], 10, int(s["eval_seed"]), a, b)
+                 for a, b in zip(cuts[:-1], cuts[1:])]
+        got = np.concatenate(parts)
+        np.testing.assert_array_equal(got, rows)
+        lo2, cnt2 = dev.histogram(got[:, 3])
+        np.testing.assert_array_equal(lo2, lo)
+        np.testing.assert_array_equal(cnt2, cnt)
+    assert ds.evaluate_shard(s["eval_params"], 10, 1, 2, 2).shape == (0, 5)
+    with pytest.raises(gbx.ValidationError):
+        ds.evaluate_shard(s["eval_params"], 10, 1, 0, na + 1)
+    ds.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_evaluate_distributed_across_processes(world):
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "shard_eval_probe.py"),
+                        str(world)], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
