@@ -428,6 +428,9 @@ def main():
                      "peak_gbs": peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)},
     }
 
+    c5_sharded = None
+    if world > 1 and not args.no_secondary:
+        c5_sharded = run_c5_sharded(args, dev, torch, dist, rank, world)
     if rank == 0 and not args.no_secondary:
         # inference / C5 use a policy of FIXED training (5 epochs of the headline
         # fit from the same init), so their numbers do not depend on --steps:
@@ -457,6 +460,8 @@ def main():
         if v.get("tflops") and fp64_peak:
             v["roofline_frac"] = v["tflops"] / fp64_peak
     line.update(secondary)
+    if c5_sharded:
+        line["aggregation_sharded"] = c5_sharded
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
@@ -640,6 +645,43 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
                        "peak_note": "dense TF32 = half the measured bf16 cuBLAS peak"}
 
     return out
+
+
+def run_c5_sharded(args, dev, torch, dist, rank, world):
+    """C5 sharded by app range over the ranks (BASELINE configs[4]
+    "sharded 1/2/4/8 GPU"): every rank holds the same generated suite, infers
+    and aggregates its app range (gbxcu_evaluate_shard), rank 0 gathers the
+    rows; strong scaling — total shaders / max-over-ranks time."""
+    s, feat = synthetic_suite_torch(torch, args.c5_apps, args.c5_shaders_per_app)
+    ds = dev.suite_upload_dev(s, feat)
+    del s, feat
+    torch.cuda.empty_cache()
+    params = dev.policy_init(7)
+    per = (ds.n_apps + world - 1) // world
+    lo, hi = min(ds.n_apps, rank * per), min(ds.n_apps, (rank + 1) * per)
+    ds.evaluate_shard(params, 10, 77, lo, hi)  # warm
+    times = []
+    for _ in range(3):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rows = ds.evaluate_shard(params, 10, 77, lo, hi)
+        times.append(time.perf_counter() - t0)
+    # object collectives work on every backend (nccl in the bench, gloo in tests)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (statistics.median(times), rows))
+    t_max = max(g[0] for g in gathered)
+    nsh = ds.n_shaders
+    ds.close()
+    torch.cuda.empty_cache()
+    if rank != 0:
+        return None
+    n_rows = sum(len(g[1]) for g in gathered)
+    return {"value": nsh / t_max, "unit": "shader decisions/s (infer+agg)",
+            "ms": t_max * 1e3, "apps": args.c5_apps, "shaders": nsh, "ranks": world,
+            "rows_gathered": n_rows, "scaling": "strong",
+            "note": "app-range shards (gbxcu_evaluate_shard), rows gathered to rank 0; "
+                    "host wall clock around each rank's shard, max over ranks"}
 
 
 def run_algorithm1(args, dev, gbx):

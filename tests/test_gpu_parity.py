@@ -418,3 +418,15 @@ def test_evaluate_distributed_across_processes(world):
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "shard_eval_probe.py"),
                         str(world)], cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_bench_c5_sharded_collectives():
+    """bench.py's sharded-C5 secondary (run on N>1 ranks) driven by 2 processes
+    over gloo on one GPU: collectives complete and every app's row is gathered."""
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "c5_sharded_probe.py"), "2"],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
