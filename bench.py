@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1_000_000, help="records per GPU (weak scaling)")
+    ap.add_argument("--n", "--records", dest="n", type=int, default=1_000_000,
+                    help="records per GPU (weak scaling)")
     ap.add_argument("--batch", type=int, default=8192,
                     help="minibatch per GPU (global = N x this; 65,536 at 8 GPUs, SURVEY C3)")
     ap.add_argument("--lr", type=float, default=0.01)
@@ -271,9 +272,16 @@ def main():
 
     import paper_2111_12055_b200 as gbx
 
+    # one process per GPU; GBX_BENCH_BACKEND=gloo + more ranks than GPUs is a
+    # test mode only (all ranks share GPU 0: exercises the N>1 code path)
+    backend = os.environ.get("GBX_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = gbx.Device(local)
     dp_note = None
     if world > 1 and args.dp == "fused":
@@ -431,6 +439,15 @@ def main():
     c5_sharded = None
     if world > 1 and not args.no_secondary:
         c5_sharded = run_c5_sharded(args, dev, torch, dist, rank, world)
+    if world > 1:
+        # the collective fits are done: every rank leaves its peer set /
+        # communicator so rank 0's single-GPU secondaries (fits included) run
+        # locally instead of waiting on ranks that have moved on
+        dist.barrier()
+        if args.dp == "fused":
+            dev.peer_detach()
+        else:
+            dev.comm_destroy()
     if rank == 0 and not args.no_secondary:
         # inference / C5 use a policy of FIXED training (5 epochs of the headline
         # fit from the same init), so their numbers do not depend on --steps:
