@@ -74,7 +74,7 @@ struct FastSmem {
     float b0[H1];
     float b1[H2];
     float b2[A];
-    float stats[8];     // R0,B0,R1,B1,R2,B2
+    float stats[12];    // R0,B0,R1,B1,R2,B2,Rd,W0max,W1max
 };
 static_assert(offsetof(FastSmem, w0) % 16 == 0 && offsetof(FastSmem, w1t) % 16 == 0, "align");
 
@@ -115,6 +115,14 @@ __device__ void load_fast_weights(FastSmem& S, float* raw, const float* __restri
     } else if (t >= 128 && t < 128 + H2) {
         const int k = t - 128;
         nrm[t] = fabs((double)S.w2[k * A + 1] - (double)S.w2[k * A]);
+    } else if (t >= 160 && t < 160 + H1) {
+        // per-unit max |w0[j][i]| (slot 160+j) and max |w1[k][j]| over k (slot 224+j)
+        const int j = t - 160;
+        double m0 = 0, m1 = 0;
+        for (int i = 0; i < F; ++i) m0 = fmax(m0, fabs((double)S.w0[(j >> 1) * (2 * F) + 2 * i + (j & 1)]));
+        for (int k = 0; k < H2; ++k) m1 = fmax(m1, fabs((double)S.w1t[j * H2 + k]));
+        nrm[t] = m0;
+        nrm[t + H1] = m1;
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -125,6 +133,8 @@ __device__ void load_fast_weights(FastSmem& S, float* raw, const float* __restri
         double r2 = lane < A ? nrm[H1 + H2 + lane] : 0.0;
         double bb2 = lane < A ? fabs((double)S.b2[lane]) : 0.0;
         double rd = nrm[128 + lane];
+        double wm0 = fmax(nrm[160 + lane], nrm[192 + lane]);
+        double wm1 = fmax(nrm[224 + lane], nrm[256 + lane]);
         for (int o = 16; o > 0; o >>= 1) {
             r0 = fmax(r0, __shfl_xor_sync(0xffffffffu, r0, o));
             bb0 = fmax(bb0, __shfl_xor_sync(0xffffffffu, bb0, o));
@@ -133,6 +143,8 @@ __device__ void load_fast_weights(FastSmem& S, float* raw, const float* __restri
             r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
             bb2 = fmax(bb2, __shfl_xor_sync(0xffffffffu, bb2, o));
             rd += __shfl_xor_sync(0xffffffffu, rd, o);
+            wm0 = fmax(wm0, __shfl_xor_sync(0xffffffffu, wm0, o));
+            wm1 = fmax(wm1, __shfl_xor_sync(0xffffffffu, wm1, o));
         }
         if (lane == 0) {
             // 1.0001 absorbs the rounding of the fp64 row sums themselves
@@ -143,6 +155,8 @@ __device__ void load_fast_weights(FastSmem& S, float* raw, const float* __restri
             S.stats[4] = __double2float_ru(r2 * 1.0001);
             S.stats[5] = __double2float_ru(bb2);
             S.stats[6] = __double2float_ru(rd * 1.0001);
+            S.stats[7] = __double2float_ru(wm0);
+            S.stats[8] = __double2float_ru(wm1);
         }
     }
     __syncthreads();
@@ -150,20 +164,24 @@ __device__ void load_fast_weights(FastSmem& S, float* raw, const float* __restri
 
 // Forward error bound on |(l1-l0)_fp32 - (l1-l0)_exact| (Higham-style
 // recursive-summation bounds for FMA chains, u = 2^-24, g(n) = n u (1 + 1e-4)):
-//   D1 = g(14)(B0 + R0 X)        X  = max_i |x_i|; layer 1 runs 4 chains of
+//   D1 = g(14)(B0 + min(R0 X, W0 X1))  X = max_i |x_i|, X1 = sum_i |x_i|,
+//                                 W0 = max |w0| (either product bounds
+//                                 sum_i |w_ji||x_i|); layer 1 runs 4 chains of
 //                                 <= 12 terms (bias in the first) + 2 levels
 //                                 of adds: 14 roundings per element at most
-//   D2 = g(65)(B1 + R1 H1) + R1 D1     H1 = max_j h1_j  (fp32 values)
+//   D2 = g(65)(B1 + min(R1 H1, W1 H1s)) + R1 D1   H1 = max_j h1_j, H1s = sum_j h1_j
 //   e3 = 2 g(33)(B2 + R2 H2) + Rd D2   H2 = max_k h2_k; Rd = ||w2[1] - w2[0]||_1
 //        (each logit's own chain rounding, plus the difference's sensitivity
 //        to the h2 errors, which relu does not amplify)
 //   margin = 1.01 e3 (+ slack for the fp64 reference's own rounding, the
 //   final fp32 subtraction and this bound's evaluation).
-__device__ __forceinline__ float guard_threshold(const float* st, float X, float Hm1, float Hm2) {
+__device__ __forceinline__ float guard_threshold(const float* st, float X, float X1, float Hm1,
+                                                 float H1s, float Hm2) {
     const float u = 5.9604645e-8f;  // 2^-24
     const float g14 = 14.f * u * 1.0001f, g65 = 65.f * u * 1.0001f, g33 = 33.f * u * 1.0001f;
-    const float D1 = g14 * (st[1] + st[0] * X);
-    const float D2 = g65 * (st[3] + st[2] * Hm1) + st[2] * D1;
+    // sum_i |w_ji| |x_i| <= min(R0 max|x|, max|w0| sum|x|); likewise for layer 2
+    const float D1 = g14 * (st[1] + fminf(st[0] * X, st[7] * X1));
+    const float D2 = g65 * (st[3] + fminf(st[2] * Hm1, st[8] * H1s)) + st[2] * D1;
     const float e3 = 2.f * g33 * (st[5] + st[4] * Hm2) + st[6] * D2;
     return 1.02f * e3 + 1e-30f;
 }
@@ -171,7 +189,8 @@ __device__ __forceinline__ float guard_threshold(const float* st, float X, float
 // Per-state tail of the fast path: guard, fp32 softmax, action (greedy or
 // collection draw), re-check list, outputs.
 __device__ __forceinline__ void fast_finish(const FastSmem& S, size_t s, float l0, float l1,
-                                            float X, float hm1, float hm2, bool finite,
+                                            float X, float X1, float hm1, float h1s, float hm2,
+                                            bool finite,
                                             double* __restrict__ probs, uint8_t* __restrict__ actions,
                                             const uint64_t* __restrict__ seg_off, size_t nseg,
                                             const uint64_t* __restrict__ seg_seed, double eps,
@@ -182,7 +201,7 @@ __device__ __forceinline__ void fast_finish(const FastSmem& S, size_t s, float l
         atomicOr(flags, 1u);
         return;
     }
-    const float T = guard_threshold(S.stats, X, hm1, hm2);
+    const float T = guard_threshold(S.stats, X, X1, hm1, h1s, hm2);
     const float d = l1 - l0;
     // fp32 softmax (max-subtracted like the reference)
     const float m = fmaxf(l0, l1);
@@ -233,7 +252,8 @@ __device__ __forceinline__ void fast_finish(const FastSmem& S, size_t s, float l
 }
 
 // Loads one staged row into registers; returns max |x| and finiteness.
-__device__ __forceinline__ void fast_row(const float* xs, int r, float (&x)[F], float& X, bool& finite) {
+__device__ __forceinline__ void fast_row(const float* xs, int r, float (&x)[F], float& X, float& X1,
+                                         bool& finite) {
     const float4* row = reinterpret_cast<const float4*>(xs + r * F);
 #pragma unroll
     for (int q = 0; q < F / 4; ++q) {
@@ -241,11 +261,13 @@ __device__ __forceinline__ void fast_row(const float* xs, int r, float (&x)[F], 
         x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
     }
     X = 0.f;
+    X1 = 0.f;
     finite = true;
 #pragma unroll
     for (int i = 0; i < F; ++i) {
         finite &= isfinite(x[i]);
         X = fmaxf(X, fabsf(x[i]));
+        X1 += fabsf(x[i]);
     }
 }
 
@@ -291,17 +313,17 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
         const bool act0 = lane < (int)rows, act1 = lane + 32 < (int)rows;
 
         float xa[F], xb[F];
-        float Xa, Xb;
+        float Xa, Xb, X1a, X1b;
         bool fa, fb;
-        fast_row(xs, act0 ? lane : 0, xa, Xa, fa);
-        fast_row(xs, act1 ? lane + 32 : 0, xb, Xb, fb);
+        fast_row(xs, act0 ? lane : 0, xa, Xa, X1a, fa);
+        fast_row(xs, act1 ? lane + 32 : 0, xb, Xb, X1b, fb);
         __syncwarp();  // the buffer is refilled two passes later
 
         // ---- layers 1+2 interleaved: acc2[k] += w1[k][j] * relu(z1_j), packed FFMA2
         float2 ca[H2 / 2], cb[H2 / 2];
 #pragma unroll
         for (int q = 0; q < H2 / 2; ++q) ca[q] = cb[q] = make_float2(S.b1[2 * q], S.b1[2 * q + 1]);
-        float hma = 0.f, hmb = 0.f;
+        float hma = 0.f, hmb = 0.f, hsa = 0.f, hsb = 0.f;
 #pragma unroll 2
         for (int jp = 0; jp < H1 / 2; ++jp) {
             const float4* wr = reinterpret_cast<const float4*>(S.w0 + jp * (2 * F));
@@ -329,6 +351,8 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
             const float hB0 = zb.x > 0.f ? zb.x : 0.f, hB1 = zb.y > 0.f ? zb.y : 0.f;
             hma = fmaxf(hma, fmaxf(hA0, hA1));
             hmb = fmaxf(hmb, fmaxf(hB0, hB1));
+            hsa += hA0 + hA1;
+            hsb += hB0 + hB1;
             const float4* w1a = reinterpret_cast<const float4*>(S.w1t + (2 * jp) * H2);
             const float4* w1b = reinterpret_cast<const float4*>(S.w1t + (2 * jp + 1) * H2);
 #pragma unroll
@@ -365,10 +389,10 @@ fwd_fast_kernel(const float* __restrict__ params, const float* __restrict__ feat
             lb = __ffma2_rn(w2p[2 * q + 1], make_float2(b1, b1), lb);
         }
         if (act0)
-            fast_finish(S, base + lane, la.x, la.y, Xa, hma, h2a, fa, probs, actions, seg_off, nseg,
+            fast_finish(S, base + lane, la.x, la.y, Xa, X1a, hma, hsa, h2a, fa, probs, actions, seg_off, nseg,
                         seg_seed, eps, recheck, n_recheck, flags, mode);
         if (act1)
-            fast_finish(S, base + 32 + lane, lb.x, lb.y, Xb, hmb, h2b, fb, probs, actions, seg_off,
+            fast_finish(S, base + 32 + lane, lb.x, lb.y, Xb, X1b, hmb, hsb, h2b, fb, probs, actions, seg_off,
                         nseg, seg_seed, eps, recheck, n_recheck, flags, mode);
     }
 }

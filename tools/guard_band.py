@@ -38,10 +38,12 @@ def main():
         B0, B1, B2 = (np.abs(b).max() for b in (b0, b1, b2))
         Rd = np.abs(W2[1] - W2[0]).sum()
         X, H1, H2 = np.abs(x).max(1), h1.max(1), h2.max(1)
+        X1, H1s = np.abs(x).sum(1), h1.sum(1)
+        W0m, W1m = np.abs(W0).max(), np.abs(W1).max()
 
-        def band(g1, g2, g3):
-            D1 = g1 * (B0 + R0 * X)
-            D2 = g2 * (B1 + R1 * H1) + R1 * D1
+        def band(g1, g2, g3):  # k_forward.cu guard_threshold's form
+            D1 = g1 * (B0 + np.minimum(R0 * X, W0m * X1))
+            D2 = g2 * (B1 + np.minimum(R1 * H1, W1m * H1s)) + R1 * D1
             return 1.02 * (2 * g3 * (B2 + R2 * H2) + Rd * D2)
 
         rows = {"fp32 FFMA (k_forward.cu)": band(14 * u, 65 * u, 33 * u),
