@@ -785,6 +785,59 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
                 stage_due = more;  // staged after this step's partial is published
             }
         }
+        // (only the variant instantiations ever run a lone CTA: the
+        //  reference's KL + SGD uses the bit-exact 1-CTA kernel there)
+        if (VAR && GG == 1) {
+            // ---- a lone CTA (small batches, e.g. the variants at B <= 32):
+            //      its partial IS the batch gradient, so the update is applied
+            //      in place — no partial rows, counter or LL words
+            tc_for_each(g, [&](int p, double v0, double, bool) {
+                if (p == NP) {
+                    const double loss = v0 / (double)nb;
+                    S.scal[0] = loss;
+                    S.scal[1] = isfinite(loss) ? 0.0 : 1.0;
+                }
+            });
+            if (stage_due) cp_async_wait_all();
+            __syncthreads();
+            if (S.scal[1] != 0.0) {
+                if (tid == 0) *a.diverged_epoch = a.epoch;
+                break;
+            }
+            if (tid == 0) epoch_total = fma(S.scal[0], (double)nb, epoch_total);
+            const bool adam = VAR && a.optimizer == 1;
+            double c1 = 1.0, c2 = 1.0;
+            if (adam) {
+                const double t_adam = (double)(a.step0 + (unsigned)step + 1u);
+                c1 = 1.0 - pow(a.beta1, t_adam);
+                c2 = 1.0 - pow(a.beta2, t_adam);
+            }
+            auto apply = [&](int p, double gsum) {
+                double upd;
+                if (adam) {
+                    const double m = a.beta1 * a.adam_m[p] + (1.0 - a.beta1) * gsum;
+                    const double v = a.beta2 * a.adam_v[p] + (1.0 - a.beta2) * gsum * gsum;
+                    a.adam_m[p] = m;
+                    a.adam_v[p] = v;
+                    upd = a.lr * (m / c1) / (sqrt(v / c2) + a.adam_eps);
+                } else {
+                    upd = a.lr * gsum;
+                }
+                put_param(S, p, (double)__double2float_rn(get_param(S, p) - upd));
+            };
+            tc_for_each(g, [&](int p, double v0, double v1, bool pair) {
+                if (p >= NP) return;
+                apply(p, v0);
+                if (pair) apply(p + 1, v1);
+            });
+            tc_zero(g);
+            if (stage_due) {
+                __syncthreads();
+                tc_stage_in(S, k & 1, a.loss_mode);
+            }
+            stage_due = false;
+            continue;  // the loop top's barrier publishes the replicas
+        }
         // ---- 1. publish this CTA's partial
         tc_store_partial(g, my_part);
         if (stage_due) cp_async_wait_all();  // this thread's copies of the next tile
@@ -942,6 +995,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         TC_TRACE(step, 4);
     }
     cp_async_wait_all();
+    __syncthreads();  // a lone CTA's last in-place update is visible to every thread
     if (aborted) {
         if (tid == 0) atomicExch(a.status, 1);
         return;
