@@ -14,9 +14,10 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("n,batch,ranks", [(20_000, 2048, 2), (12_000, 3000, 3), (30_000, 8192, 4)])
-def test_ipc_peer_set_matches_single_process(n, batch, ranks):
+@pytest.mark.parametrize("n,batch,ranks,opt", [(20_000, 2048, 2, "sgd"), (12_000, 3000, 3, "sgd"),
+                                             (30_000, 8192, 4, "sgd"), (20_000, 4096, 2, "adam")])
+def test_ipc_peer_set_matches_single_process(n, batch, ranks, opt):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ipc_peer_probe.py"), str(n),
-                        str(batch), str(ranks)], cwd=ROOT, capture_output=True, text=True,
+                        str(batch), str(ranks), opt], cwd=ROOT, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
