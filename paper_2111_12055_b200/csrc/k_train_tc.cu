@@ -111,6 +111,7 @@ struct TcSmem {
     double u[TB * SU];
     double ltgt[TB * 2];         // ln(clamp(target)) per (record, action)
     double red[NT + 64];         // slice reduction: [source subset][element], then totals
+    double adam[2][64];          // Adam m, v of this CTA's slice (kept on chip for the epoch)
     uint32_t ord[2][TB];         // record indices of the next two tiles (cp.async ring)
     double stage_t[2][TB * 2];   // cp.async staging: targets
     float stage_f[2][TB * F];    // cp.async staging: raw fp32 features
@@ -738,6 +739,14 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     bool h2 = h1 && tc_next<TB>(a, who, n_steps, s2, r2, n2);  // tile 1
     if (h2) tc_fetch_idx(S, 1, a, r2, n2);
     cp_async_commit();
+    // Adam moments of the slice on chip for the whole epoch (written back at
+    // the end of the launch); a lone CTA or a slice wider than 64 keeps them
+    // in global memory
+    const bool adam_smem = VAR && a.optimizer == 1 && GG > 1 && p_hi - p_lo <= 64;
+    if (adam_smem && tid < p_hi - p_lo) {
+        S.adam[0][tid] = a.adam_m[p_lo + tid];
+        S.adam[1][tid] = a.adam_v[p_lo + tid];
+    }
     load_params_plain(S, a.params);
     tc_init_consts(S);
     cp_async_wait_all();
@@ -763,6 +772,14 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         tc_slice_w(a, who, step, lo, hi, nb);
         const double inv_b = 1.0 / (double)nb;
         const unsigned tag = a.tag_base + (unsigned)step + 1u;
+        // Adam's bias corrections for this step, computed up front (two pow()s
+        // off the critical path between the slice reduce and the publish)
+        double adam_c1 = 1.0, adam_c2 = 1.0;
+        if (VAR && a.optimizer == 1 && tid < 64) {
+            const double t = (double)(a.step0 + (unsigned)step + 1u);
+            adam_c1 = 1.0 - pow(a.beta1, t);
+            adam_c2 = 1.0 - pow(a.beta2, t);
+        }
         TC_TRACE(step, 0);
         for (uint32_t r0 = lo; r0 < hi; r0 += TB, ++k) {
             const int nv = (int)min((uint32_t)TB, hi - r0);
@@ -957,14 +974,16 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
                     const double gsum = S.red[NT + tid];
                     double upd;
                     if (VAR && a.optimizer == 1) {
-                        // Adam: this CTA owns the moments of its slice across steps
-                        const double m = a.beta1 * a.adam_m[p] + (1.0 - a.beta1) * gsum;
-                        const double v = a.beta2 * a.adam_v[p] + (1.0 - a.beta2) * gsum * gsum;
-                        a.adam_m[p] = m;
-                        a.adam_v[p] = v;
-                        const double t = (double)(a.step0 + (unsigned)step + 1u);
-                        const double mh = m / (1.0 - pow(a.beta1, t)), vh = v / (1.0 - pow(a.beta2, t));
-                        upd = a.lr * mh / (sqrt(vh) + a.adam_eps);
+                        // Adam: this CTA owns the moments of its slice across
+                        // steps — in shared memory for the epoch when the slice
+                        // fits (no global round trip on the step's critical path)
+                        double* pm = adam_smem ? &S.adam[0][e2 - 1] : &a.adam_m[p];
+                        double* pv = adam_smem ? &S.adam[1][e2 - 1] : &a.adam_v[p];
+                        const double m = a.beta1 * *pm + (1.0 - a.beta1) * gsum;
+                        const double v = a.beta2 * *pv + (1.0 - a.beta2) * gsum * gsum;
+                        *pm = m;
+                        *pv = v;
+                        upd = a.lr * (m / adam_c1) / (sqrt(v / adam_c2) + a.adam_eps);
                     } else {
                         upd = a.lr * gsum;
                     }
@@ -999,6 +1018,10 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     if (aborted) {
         if (tid == 0) atomicExch(a.status, 1);
         return;
+    }
+    if (adam_smem && tid < p_hi - p_lo) {  // the slice's moments for the next epoch
+        a.adam_m[p_lo + tid] = S.adam[0][tid];
+        a.adam_v[p_lo + tid] = S.adam[1][tid];
     }
     // rank-local outputs: params (fp32 values of the replicas) and the epoch loss
     if (c == 0 && (!a.pvirt || rank == 0) && *a.diverged_epoch < 0) {
