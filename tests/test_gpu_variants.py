@@ -86,3 +86,18 @@ def test_variant_validation(dev, orc):
         dev.fit(p, f, t, loss="huber")
     with pytest.raises(gbx.ValidationError):
         dev.fit(p, f, t, optimizer="adam", betas=(1.0, 0.999))
+
+
+@pytest.mark.parametrize("n,batch", [(1, 32), (7, 32), (33, 32), (100, 1000), (1500, 64)])
+def test_variant_ragged_sizes(dev, orc, n, batch):
+    """Edge sizes through the lone-CTA and multi-CTA variant paths: a single
+    record, a partial last batch, n below the batch size."""
+    for loss, opt in CASES:
+        f, t = data(orc, loss, 40 + n, n)
+        p0 = orc.policy_init(6)
+        lr = 1e-3 if opt == "adam" else 0.01
+        rc, p_ref, el_ref, _ = orc.fit_variant(p0, f, t, lr, 3, batch, 2, loss=loss, optimizer=opt)
+        assert rc == 0
+        p, el = dev.fit(p0, f, t, lr, 3, batch, 2, loss=loss, optimizer=opt)
+        assert ulps32(p, p_ref).max() <= 2, (loss, opt)
+        np.testing.assert_allclose(el, el_ref, rtol=1e-12)
