@@ -90,6 +90,8 @@ struct gbxcu_ctx {
     int device = 0;
     int num_sms = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;     // gbxcu_fit: epoch-0 shuffle overlapping the H2D
+    cudaEvent_t side_ev = nullptr;
     uint64_t launches = 0;
     cudaEvent_t ev[24] = {};                 // fit's per-kernel timing events
     unsigned long long* hres = nullptr;      // pinned host scratch for fit's small results
@@ -343,10 +345,12 @@ void bind_region(TrainArgs& a, int r, void* base) {
 
 int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double* d_tgt, size_t n,
                const gbxcu_train_cfg* cfg, double* epoch_loss_out, int* diverged_epoch,
-               cudaStream_t st) {
+               cudaStream_t st, bool pre_shuffled = false) {
     RET(validate_cfg(cfg, n));
     RET(setup_kernel_attrs());
-    RET(prepare_order(c, n, st));
+    // pre_shuffled: the caller already ran prepare_order + epoch 0's shuffle
+    // (gbxcu_fit overlaps them with the host-to-device copies)
+    if (!pre_shuffled) RET(prepare_order(c, n, st));
     RET(c->epoch_loss.ensure(sizeof(double) * cfg->epochs));
     RET(c->epoch_acc.ensure(16));
     if (c->peers < 0) return fail(GBXCU_EINVAL, "peer set timed out earlier; re-attach it");
@@ -434,7 +438,7 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
     const bool timed = cfg->epochs <= 8;  // per-kernel event timing (bench / profiling)
     for (int e = 0; e < cfg->epochs; ++e) {
         if (timed) CK(cudaEventRecord(c->ev[2 * e % 16], st));
-        RET(shuffle_epoch(c, n, cfg->seed, e, st));
+        if (!(pre_shuffled && e == 0)) RET(shuffle_epoch(c, n, cfg->seed, e, st));
         a.order = c->order.as<uint32_t>();  // the pass output (buffers ping-pong)
         a.epoch = e;
         a.tag_base = c->tag_next + (unsigned int)((long)e * n_steps);
@@ -578,7 +582,9 @@ int gbxcu_create(int device, gbxcu_ctx** out) {
     auto* c = new gbxcu_ctx;
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->side_ev, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return fail(GBXCU_ECUDA, "cudaStreamCreate failed");
     }
@@ -611,6 +617,8 @@ void gbxcu_destroy(gbxcu_ctx* c) {
     for (auto& g : c->wg)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->side_ev) cudaEventDestroy(c->side_ev);
     if (c->hres) cudaFreeHost(c->hres);
     delete c;
 }
@@ -796,11 +804,18 @@ int gbxcu_fit(gbxcu_ctx* c, float* params_inout, const float* feat, const double
     std::lock_guard<std::mutex> lk(c->mu);
     CK(cudaSetDevice(c->device));
     cudaStream_t st = c->stream;
+    // the epoch-0 permutation needs no data: replay it on the side stream while
+    // the log crosses PCIe, join before the first train launch
+    RET(setup_kernel_attrs());
+    RET(prepare_order(c, n, c->side));
+    RET(shuffle_epoch(c, n, cfg->seed, 0, c->side));
+    CK(cudaEventRecord(c->side_ev, c->side));
     RET(upload(c->params, params_inout, NP, st));
     RET(upload(c->feat, feat, n * F, st));
     RET(upload(c->tgt, tgt, n * 2, st));
+    CK(cudaStreamWaitEvent(st, c->side_ev, 0));
     int rc = fit_device(c, c->params.as<float>(), c->feat.as<float>(), c->tgt.as<double>(), n, cfg,
-                        epoch_loss_out, diverged_epoch, st);
+                        epoch_loss_out, diverged_epoch, st, /*pre_shuffled=*/true);
     if (rc != GBXCU_OK && rc != GBXCU_EDIVERGED) return rc;
     const std::string msg = g_err;
     CK(cudaMemcpyAsync(params_inout, c->params.p, sizeof(float) * NP, cudaMemcpyDeviceToHost, st));
