@@ -73,13 +73,23 @@ struct DevBuf {
     int ensure(size_t bytes) {
         if (bytes <= cap) return GBXCU_OK;
         const size_t want = std::max<size_t>({bytes, cap ? cap + cap / 2 : 0, 256});
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        CK(cudaMalloc(&p, want));
+        if (astream) {
+            // stream-ordered (pool) allocation on the one stream that uses the
+            // buffer: no device-wide synchronisation on growth
+            if (p) CK(cudaFreeAsync(p, astream));
+            p = nullptr;
+            cap = 0;
+            CK(cudaMallocAsync(&p, want, astream));
+        } else {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMalloc(&p, want));
+        }
         cap = want;
         return GBXCU_OK;
     }
+    cudaStream_t astream = nullptr;  // set: every use of the buffer is on this stream
     template <typename T>
     T* as() const { return static_cast<T*>(p); }
 };
@@ -600,6 +610,13 @@ int gbxcu_create(int device, gbxcu_ctx** out) {
                                                   fast_smem_bytes());
     c->fast_per_sm = std::max(1, per_sm);
     for (auto& e : c->ev) cudaEventCreate(&e);
+    {  // keep freed stream-ordered allocations in the pool (reused, not returned)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     if (cudaHostAlloc(reinterpret_cast<void**>(&c->hres), 64 * sizeof(unsigned long long),
                       cudaHostAllocDefault) != cudaSuccess)
         c->hres = nullptr;  // fall back to pageable copies (slower, same results)
@@ -953,6 +970,15 @@ int gbxcu_qtable_create(gbxcu_ctx* c, double alpha, double omega, gbxcu_qtable**
     t->ctx = c;
     t->alpha = alpha;
     t->omega = omega;
+    // every store operation runs on the context stream: its buffers grow
+    // through the stream-ordered pool (the table grows a little per call)
+    for (DevBuf* b : {&t->keys, &t->q, &t->t, &t->cnt, &t->has, &t->nkeys, &t->nq, &t->nt,
+                      &t->ncnt, &t->nhas, &t->bkeys, &t->bact, &t->brew, &t->bnow, &t->init_ids,
+                      &t->count, &t->perm, &t->perm2, &t->digit, &t->digit2, &t->seg_head,
+                      &t->key_head, &t->seg_scan, &t->key_scan, &t->seg_start, &t->seg_key,
+                      &t->spread, &t->bad, &t->temp, &t->flag, &t->row, &t->rowkey, &t->sfeat,
+                      &t->stgt, &t->bad_stage})
+        b->astream = c->stream;
     *out = t;
     return GBXCU_OK;
 }
