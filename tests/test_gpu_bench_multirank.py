@@ -15,11 +15,18 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def test_bench_two_ranks_one_json_line():
     env = dict(os.environ, GBX_BENCH_BACKEND="gloo")
     r = subprocess.run(
         [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-         "--master-addr", "127.0.0.1", "--master-port", str(29700 + os.getpid() % 200),
+         "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
          "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--records", "20000",
          "--c5-apps", "100", "--c5-shaders-per-app", "200", "--qt-tuples", "20000",
          "--no-cpu-baseline"],

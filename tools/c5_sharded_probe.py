@@ -27,11 +27,19 @@ def worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def free_port() -> int:
+    """A currently unused local TCP port for the rendezvous."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     world = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + os.getpid() % 1000
+    port = free_port()
     ps = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()

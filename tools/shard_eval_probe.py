@@ -33,10 +33,18 @@ def worker(rank, world, name, port, q):
     dist.destroy_process_group()
 
 
+def free_port() -> int:
+    """A currently unused local TCP port for the rendezvous."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     world = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     name = sys.argv[2] if len(sys.argv) > 2 else "suite_contended"
-    port = 29500 + (os.getpid() % 1000)
+    port = free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=worker, args=(r, world, name, port, q)) for r in range(world)]
