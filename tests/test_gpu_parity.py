@@ -265,6 +265,35 @@ def test_fit_order_full_size_is_permutation(dev, orc):
     assert orc.fnv1a(o) == orc.fnv1a(ref)
 
 
+def test_c3_size_fit_properties(dev, orc):
+    """C3 at its full size (10M records, one epoch, global batch 65,536): the
+    reference cannot be run to completion here, so size-independent
+    properties — a valid permutation (the oracle's own, by checksum),
+    determinism of the whole epoch, finite and decreasing loss on a
+    learnable target, weights changed everywhere the gradient reaches."""
+    import torch
+    n = 10_000_000
+    o = dev.fit_order(n, 5, 1)
+    assert orc.fnv1a(o) == orc.fnv1a(orc.fit_order(n, 5, 1).astype(np.uint32))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    feat = torch.rand((n, 44), generator=g, device="cuda", dtype=torch.float32) * 7.0
+    feat[:, :8] = 0.0
+    feat[torch.arange(n, device="cuda"), torch.randint(0, 8, (n,), generator=g, device="cuda")] = 1.0
+    p = torch.sigmoid(feat[:, 8].double() - 3.5)        # learnable target
+    tgt = torch.stack([p, 1.0 - p], 1).contiguous()
+    p0 = torch.from_numpy(orc.policy_init(9)).cuda()
+    outs = []
+    for _ in range(2):
+        w = p0.clone()
+        el = dev.fit_dev(w.data_ptr(), feat.data_ptr(), tgt.data_ptr(), n, 0.05, 2, 65536, 5)
+        outs.append((w.cpu().numpy(), el))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    el = outs[0][1]
+    assert np.isfinite(el).all() and el[1] < el[0]
+    assert np.mean(outs[0][0] != p0.cpu().numpy()) > 0.9
+
+
 # ------------------------------------------------------------- collection
 @pytest.mark.parametrize("eps", [0.0, 0.3, 1.0])
 def test_collect_matches_oracle(dev, orc, eps):
