@@ -294,6 +294,34 @@ def test_c3_size_fit_properties(dev, orc):
     assert np.mean(outs[0][0] != p0.cpu().numpy()) > 0.9
 
 
+def test_c5_size_evaluate_properties(dev, orc):
+    """C5 at its nominal size (1e8 shaders across 1e4 apps, generated on the
+    device): FAST actions equal the exact fp64 path on a 200k-shader sample,
+    and three app-range shards reassemble the full rows bit for bit."""
+    import torch
+    import bench
+    s, feat = bench.synthetic_suite_torch(torch, 10_000, 10_000)
+    ds = dev.suite_upload_dev(s, feat)
+    params = orc.policy_init(7)
+    pd = torch.from_numpy(params).cuda()
+    act = torch.empty(ds.n_shaders, dtype=torch.uint8, device="cuda")
+    rows = torch.empty((ds.n_apps, 5), dtype=torch.float64, device="cuda")
+    ds.evaluate_dev(pd.data_ptr(), 10, 77, act.data_ptr(), rows.data_ptr())
+    torch.cuda.synchronize()
+    rows = rows.cpu().numpy()
+    assert np.isfinite(rows).all()
+    idx = torch.randint(0, ds.n_shaders, (200_000,), device="cuda")
+    sample = feat[idx].cpu().numpy()
+    _, exact = dev.forward(params, sample, gbx.FWD_EXACT)
+    np.testing.assert_array_equal(act[idx].cpu().numpy(), exact)
+    cuts = [0, 3_333, 6_666, ds.n_apps]
+    parts = [ds.evaluate_shard(params, 10, 77, a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+    np.testing.assert_array_equal(np.concatenate(parts), rows)
+    ds.close()
+    del s, feat
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------- collection
 @pytest.mark.parametrize("eps", [0.0, 0.3, 1.0])
 def test_collect_matches_oracle(dev, orc, eps):
