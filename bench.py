@@ -139,47 +139,83 @@ def synthetic_suite_torch(torch, n_apps: int, per_app: int, seed: int = 5, cap: 
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: a background thread polls NVML every 5 ms (nvidia-smi -lms through
+    a pipe lost its block-buffered output when terminated, so a short region
+    reported no samples). Falls back to one-shot nvidia-smi queries."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.sm, self.reasons, self.max_mhz, self.source = [], set(), None, None
+
+    def _poll_nvml(self):
+        import pynvml as N
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            N.nvmlDeviceGetCurrentClocksThrottleReasons
+        masks = [(nm, getattr(N, attr, 0)) for nm, attr in self.REASONS]
+        while not self._stop.is_set():
+            self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+            r = get_r(h)
+            for nm, m in masks:
+                if m and (r & m):
+                    self.reasons.add(nm)
+            self._stop.wait(self.period)
+
+    def _poll_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout
+                f = [x.strip() for x in out.split(",")]
+                self.sm.append(float(f[0]))
+                self.max_mhz = float(f[1])
+                for nm, v in zip(names, f[2:6]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(nm)
+            except (OSError, ValueError, IndexError, subprocess.SubprocessError):
+                return
+
+    def _run(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            try:
+                self.source = "nvml"
+                self._poll_nvml()
+            finally:
+                N.nvmlShutdown()
+        except Exception:  # no NVML binding / library: nvidia-smi one-shots
+            self.source = "nvidia-smi"
+            self._poll_smi()
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
-        time.sleep(0.25)
+        import threading
+        self._stop = threading.Event()
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc:
-            time.sleep(0.15)
-            self.proc.terminate()
-            out, _ = self.proc.communicate(timeout=5)
-            self.lines = [l for l in out.splitlines() if l.strip()]
+        self._stop.set()
+        self._th.join(timeout=10)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
-            f = [x.strip() for x in l.split(",")]
-            try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
-            except (ValueError, IndexError):
-                continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": self.source}
 
 
 def measured_peaks():
@@ -204,8 +240,51 @@ def pipe_peaks(device: int):
             L.peak_fp32_tflops(device))
 
 
+def host_info():
+    """nproc and the CPU model of the host the CPU baselines run on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model,
+            "affinity_cpus": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None}
+
+
+def workload_config(args, world):
+    """The config both arms report (the driver compares them)."""
+    return {"workload": "C2: 1M-tuple experience log per GPU, default MLP 44-64-32-2, "
+                        "1 fit epoch per step (fp64 parity mode)",
+            "records": args.n * world, "global_batch": args.batch * world, "lr": args.lr,
+            "parallelism": f"dp{world}" + (f" ({args.dp} gradient exchange)" if world > 1 else ""),
+            "l2": "inputs (196 MB/GPU) larger than L2"}
+
+
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: re-run this script under
+    torch.distributed.run with one rank per GPU (rank 0 prints the line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 # ------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
+    """The reference's own CPU fit (oracle/_ref: the unmodified reference
+    library; the restatement when it is not built) on the SAME workload as
+    our arm: the same synthetic log, init, lr, seed and global batch. fit is
+    single-threaded by contract. Each step is one epoch over
+    the full log when the run fits the time budget, else over the log's
+    first `sample` records (the per-record cost of fit does not depend on n)."""
     if rank != 0:
         return
     import oracle
@@ -214,28 +293,39 @@ def run_reference(args, rank, world):
         kind, impl = "port", oracle.Restatement()
     else:
         kind, impl = "reference", oracle.Reference()
-    sample = min(args.n, 100_000)
-    feat, tgt = synthetic_log(sample)
+    n_total, batch = args.n * world, args.batch * world
+    feat, tgt = synthetic_log(n_total)
     p0 = impl.policy_init(7)
+    # rate probe on a 50k-record prefix, then size the per-step sample so the
+    # whole --warmup W --steps K run stays within ~3 minutes
+    m0 = min(n_total, 50_000)
+    t0 = time.perf_counter()
+    assert impl.fit(p0, feat[:m0], tgt[:m0], args.lr, 1, batch, 99)[0] == 0
+    rate = m0 / (time.perf_counter() - t0)
+    budget_s = float(os.environ.get("GBX_REF_BUDGET_S", "180"))
+    sample = int(min(n_total, max(m0, budget_s * rate / max(1, args.steps + args.warmup))))
+    fs, ts = (feat, tgt) if sample == n_total else (feat[:sample], tgt[:sample])
     times = []
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        rc = impl.fit(p0, feat, tgt, args.lr, 1, args.batch * world, 99)[0]
+        rc = impl.fit(p0, fs, ts, args.lr, 1, batch, 99)[0]
         dt = time.perf_counter() - t0
         assert rc == 0
         if it >= args.warmup:
             times.append(dt)
     v = sample / statistics.mean(times)
+    what = ("the full log" if sample == n_total else f"the first {sample} records of the log")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 fit epoch (reference CPU, bounded sample)",
-                   "records": sample, "batch": args.batch * world, "lr": args.lr},
+        "config": workload_config(args, world),
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": kind,
-                         "sample": f"{sample} records, 1 epoch, batch {args.batch * world}; "
-                                   "fit is single-threaded by contract (SPEC.md:301)"},
+                         "sample": f"fit, 1 epoch over {what} per step ({sample} records), "
+                                   f"batch {batch}, lr {args.lr}, seed 99, init 7; fit is "
+                                   "single-threaded by contract (SPEC.md:301)",
+                         "host": host_info()},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -246,26 +336,33 @@ def cpu_baseline(args):
 
     kind, impl = ("reference", oracle.Reference()) if oracle.ref_available() else (
         "port", oracle.Restatement())
-    sample = min(args.n, 200_000)
+    # the N=1 workload itself: one epoch over the same 1M-record log, same batch
+    sample = args.n
     feat, tgt = synthetic_log(sample)
     t0 = time.perf_counter()
     rc = impl.fit(impl.policy_init(7), feat, tgt, args.lr, 1, args.batch, 99)[0]
     dt = time.perf_counter() - t0
     assert rc == 0
     return {"value": sample / dt, "unit": "samples/s", "cores": 1, "kind": kind,
-            "sample": f"fit of {sample} synthetic records, 1 epoch, batch {args.batch}, "
+            "sample": f"fit, 1 epoch over the headline's {sample}-record log, batch {args.batch}, "
                       f"{dt:.1f} s on 1 host core (fit is single-threaded, SPEC.md:301)"}
 
 
 # ----------------------------------------------------------------- our arm
 def main():
     args = parse()
+    launched = "WORLD_SIZE" in os.environ
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if launched and args.gpus > 1 and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        # only rank 0 works; without a launcher it stands for all N ranks
+        run_reference(args, rank, world if launched else args.gpus)
         return
+    if not launched and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
 
     import torch
     import torch.distributed as dist
@@ -464,10 +561,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "C2: 1M-tuple experience log per GPU, default MLP 44-64-32-2, "
-                               "1 fit epoch per step (fp64 parity mode)",
-                   "records": n_total, "global_batch": batch, "lr": args.lr,
-                   "parallelism": f"dp{world}" + (f" ({args.dp} gradient exchange)" if world > 1 else ""), "l2": "inputs (196 MB/GPU) larger than L2"},
+        "config": workload_config(args, world),
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
     }
     if dp_note:
@@ -481,6 +575,7 @@ def main():
         line["aggregation_sharded"] = c5_sharded
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
+        line["cpu_baseline"]["host"] = host_info()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import subprocess
+import sys
 
 import numpy as np
 
@@ -212,6 +213,18 @@ def _raise(L, rc: int, diverged_epoch: int = -1):
     raise CudaError(msg)
 
 
+def _after_torch(stream) -> None:
+    """Device-pointer entry points with stream=None run on the context's
+    non-blocking stream, which does not order itself after torch's current
+    stream: wait for torch's pending work (the producer of the caller's
+    tensors) first. An explicit stream means the caller orders it."""
+    if stream is not None:
+        return
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+        torch.cuda.current_stream().synchronize()
+
+
 def _f32(a):
     return np.ascontiguousarray(a, dtype=np.float32)
 
@@ -366,6 +379,7 @@ class Device:
     # ------------------------------------------------- device-resident forms
     def forward_dev(self, d_params: int, d_feat: int, n: int, d_probs: int | None,
                     d_actions: int | None, mode=FWD_FAST, stream: int | None = None):
+        _after_torch(stream)
         self._ck(self.L.gbxcu_forward_dev(self.h, d_params, d_feat, n, d_probs, d_actions, mode,
                                           stream))
 
@@ -376,6 +390,7 @@ class Device:
         de = C.c_int(-1)
         cfg = _train_cfg(lr, epochs, batch, seed, max_ctas, virtual_ranks, loss, optimizer, betas,
                          eps)
+        _after_torch(stream)
         rc = self.L.gbxcu_fit_dev(self.h, d_params, d_feat, d_tgt, n, C.byref(cfg),
                                   el.ctypes.data, C.byref(de), stream)
         self._ck(rc, de.value)
@@ -412,6 +427,7 @@ class Device:
         el = np.full(max(epochs, 1), np.nan, np.float64)
         de = C.c_int(-1)
         cfg = TrainCfg(lr, epochs, batch, seed, 0, 0)
+        _after_torch(stream)
         self._ck(self.L.gbxcu_wide_fit_dev(self.h, hidden, d_params, d_feat, d_tgt, n, C.byref(cfg),
                                            el.ctypes.data, C.byref(de), stream), de.value)
         return el
@@ -494,6 +510,7 @@ class DeviceSuite:
             st = SuiteC(t[0].numel() - 1, t[1].numel() - 1, t[2].numel(), t[5].shape[0],
                         *(x.data_ptr() for x in t))
             fptr = features.contiguous().data_ptr()
+            _after_torch(None)  # the tensors may still be in flight on torch's stream
         else:
             st, keep = suite_struct(suite)
             fptr = _f32(features).ctypes.data
@@ -562,6 +579,7 @@ class DeviceSuite:
 
     def evaluate_dev(self, d_params: int, n_samples: int, seed: int, d_actions: int, d_rows: int,
                      stream: int | None = None):
+        _after_torch(stream)
         self.dev._ck(self.dev.L.gbxcu_evaluate_dev(self.dev.h, self.h, d_params, n_samples, seed,
                                                    d_actions, d_rows, stream))
 
@@ -622,6 +640,7 @@ class DeviceQTable:
 
     def update_batch_dev(self, d_keys: int, d_actions: int, d_rewards: int, d_now: int, n: int):
         bad = _sz(0)
+        _after_torch(None)
         rc = self.L.gbxcu_qtable_update_batch_dev(self.h, d_keys, d_actions, d_rewards, d_now, n,
                                                   C.byref(bad))
         if rc == ECLOCK:
@@ -728,5 +747,6 @@ class DeviceQTable:
 
     def snapshot_dev(self, rho: float, d_feat: int, d_tgt: int, cap: int) -> int:
         r = _sz(0)
+        _after_torch(None)
         self.dev._ck(self.L.gbxcu_qtable_snapshot_dev(self.h, rho, d_feat, d_tgt, cap, C.byref(r)))
         return int(r.value)

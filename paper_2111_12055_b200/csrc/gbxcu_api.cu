@@ -1232,7 +1232,12 @@ int gbxcu_qtable_save_columnar(const gbxcu_qtable* t, const char* path) {
     if (!t || !path) return fail(GBXCU_EINVAL, "null argument");
     const size_t m = t->m;
     const QtSections sec = qt_sections(m);
-    std::vector<unsigned char> buf(sizeof(QtFileHeader) + sec.total, 0);
+    std::vector<unsigned char> buf;
+    try {
+        buf.assign(sizeof(QtFileHeader) + sec.total, 0);
+    } catch (const std::bad_alloc&) {
+        return fail(GBXCU_EINVAL, "q-table too large for host memory");
+    }
     unsigned char* pay = buf.data() + sizeof(QtFileHeader);
     RET(gbxcu_qtable_export(t, reinterpret_cast<uint32_t*>(pay + sec.keys),
                             reinterpret_cast<double*>(pay + sec.q), reinterpret_cast<uint64_t*>(pay + sec.t),
@@ -1290,7 +1295,25 @@ int gbxcu_qtable_load_columnar(gbxcu_qtable* t, const char* path) {
         std::fclose(f);
         return fail(GBXCU_EINVAL, "columnar q-table size does not match its header");
     }
-    std::vector<unsigned char> pay(sec.total);
+    // the file must hold exactly header + payload before anything is allocated
+    // (a corrupt m must not turn into a huge allocation)
+    if (std::fseek(f, 0, SEEK_END) != 0) {
+        std::fclose(f);
+        return fail(GBXCU_EINVAL, "cannot seek in columnar q-table file");
+    }
+    const long fsize = std::ftell(f);
+    if (fsize < 0 || (unsigned long)fsize != sizeof(QtFileHeader) + sec.total ||
+        std::fseek(f, (long)sizeof(QtFileHeader), SEEK_SET) != 0) {
+        std::fclose(f);
+        return fail(GBXCU_EINVAL, "columnar q-table truncated or has trailing bytes");
+    }
+    std::vector<unsigned char> pay;
+    try {
+        pay.resize(sec.total);
+    } catch (const std::bad_alloc&) {
+        std::fclose(f);
+        return fail(GBXCU_EINVAL, "columnar q-table too large for host memory");
+    }
     const bool full = std::fread(pay.data(), 1, sec.total, f) == sec.total;
     const bool at_end = std::fgetc(f) == EOF;
     std::fclose(f);

@@ -713,9 +713,11 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     const int GG = R * Gl, gc = rank * Gl + c;
     const TcWho who = tc_who(a, rank, R, c, Gl);
     const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
-    // reduce-scatter slice of this CTA: element 0 = loss, then params [p_lo, p_hi)
-    const int chunk = (NP + GG - 1) / GG;
-    const int p_lo = min(NP, gc * chunk), p_hi = min(NP, p_lo + chunk);
+    // reduce-scatter slice of this CTA: element 0 = loss, then params [p_lo, p_hi).
+    // Balanced split: every CTA owns >= 1 parameter (GG <= 8 x 148 < NP), so
+    // every CTA publishes LL words after its reads of the step's partial rows,
+    // and no CTA can overwrite its row (next step) before all reads are done.
+    const int p_lo = (int)(((long)gc * NP) / GG), p_hi = (int)(((long)(gc + 1) * NP) / GG);
     const int n_elem = 1 + (p_hi - p_lo);
     // reduction layout: EB elements x SUB source subsets (EB * SUB = NT)
     int EB = 8;
@@ -724,7 +726,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     double* my_part = a.part[rank] + (size_t)c * PSTR;
     unsigned long long* my_ctr = a.ctr[rank];
     const unsigned long long* my_llp = a.llp[rank];
-    bool aborted = false;
+    bool aborted = false, diverged_here = false;
 
     // Pipeline (tile k): rows of tile k+1 and indices of tile k+2 are fetched
     // (cp.async) at the top of tile k; tile k+1 is staged into X (P0) right
@@ -819,6 +821,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
             __syncthreads();
             if (S.scal[1] != 0.0) {
                 if (tid == 0) *a.diverged_epoch = a.epoch;
+                diverged_here = true;
                 break;
             }
             if (tid == 0) epoch_total = fma(S.scal[0], (double)nb, epoch_total);
@@ -997,6 +1000,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         }
         if (diverged) {
             if (c == 0 && tid == 0) *a.diverged_epoch = a.epoch;
+            diverged_here = true;
             break;
         }
         TC_MARK(9);
@@ -1023,10 +1027,13 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         a.adam_m[p_lo + tid] = S.adam[0][tid];
         a.adam_v[p_lo + tid] = S.adam[1][tid];
     }
-    // rank-local outputs: params (fp32 values of the replicas) and the epoch loss
-    if (c == 0 && (!a.pvirt || rank == 0) && *a.diverged_epoch < 0) {
+    // rank-local outputs: params (fp32 values of the replicas) and the epoch loss.
+    // On divergence the replicas hold the parameters after the last finite
+    // step (the loop leaves before that step's words are gathered), which is
+    // what the reference's net holds when fit throws (policy.cpp:321-325).
+    if (c == 0 && (!a.pvirt || rank == 0)) {
         for (int t = tid; t < NP; t += NT) a.params[t] = (float)get_param(S, t);
-        if (tid == 0) a.epoch_loss[a.epoch] = epoch_total / (double)a.n;
+        if (tid == 0 && !diverged_here) a.epoch_loss[a.epoch] = epoch_total / (double)a.n;
     }
 }
 

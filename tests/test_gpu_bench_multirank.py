@@ -39,3 +39,20 @@ def test_bench_two_ranks_one_json_line():
     assert d["aggregation_sharded"]["rows_gathered"] == 100
     for k in ("inference", "qtable", "batch_sweep", "variants", "algorithm1", "wide_mlp"):
         assert k in d, k
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`python bench.py --gpus 2` with no launcher starts the two ranks itself
+    (the driver may call it that way); still one JSON line with n_gpus 2."""
+    env = dict(os.environ, GBX_BENCH_BACKEND="gloo")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    r = subprocess.run(
+        [sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+         "--records", "20000", "--no-secondary", "--no-cpu-baseline"],
+        cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["records"] == 40000

@@ -406,6 +406,14 @@ def test_fit_peer_set_divergence_agrees(dev, orc):
     with pytest.raises(gbx.TrainingDivergedError) as ei:
         dev.fit(p0, f, t, 1e12, 4, 512, 1, virtual_ranks=4)
     assert ei.value.epoch == ep_ref
+    # the net holds the weights after the last finite step, as the reference's
+    # does when fit throws (policy.cpp:321-325) — not the start of the epoch
+    pe = ei.value.params
+    both = np.isfinite(pe) & np.isfinite(p_ref)
+    same = (np.isnan(pe) & np.isnan(p_ref)) | (pe == p_ref)
+    same[both] |= ulps32(pe[both], p_ref[both]) <= 2
+    assert same.mean() > 0.99
+    assert not np.array_equal(p_ref, p0) or np.array_equal(pe, p0)
     # the context stays usable (monotonic counters / tags resynchronised)
     f2, t2 = orc.g1(7, 20_000)
     rc, p_ref2, _, _ = orc.fit(p0, f2, t2, 0.01, 1, 2048, 3)
