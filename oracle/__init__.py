@@ -93,6 +93,8 @@ class Restatement(_Lib):
         L.orc_collect.argtypes = [_f32p, _f32p, _u64p, _sz, _u64p, C.c_double, _u8p]
         L.orc_aggregate.argtypes = [_sz, _u64p, _u64p, _u32p, _f64p, _f64p, _f64p, _f64p, _u8p,
                                     _u64p, C.c_int, _f64p, C.c_void_p]
+        L.orc_aggregate_ids.argtypes = [_sz, _u64p, _u64p, _u32p, _f64p, _f64p, _f64p, _f64p, _u8p,
+                                        _u64p, C.c_void_p, C.c_int, _f64p, C.c_void_p]
         L.orc_histogram.restype = C.c_long
         L.orc_histogram.argtypes = [_f64p, _sz, _f64p, _u64p, _sz]
         L.orc_boltzmann_pair.argtypes = [C.c_double, C.c_double, C.c_double, _f64p]
@@ -212,15 +214,19 @@ class Restatement(_Lib):
                              len(seg_off) - 1, np.ascontiguousarray(seg_seed, np.uint64), eps, act)
         return act
 
-    def aggregate(self, suite: dict, shader_action, run_seed, n_samples: int, want_samples=False):
+    def aggregate(self, suite: dict, shader_action, run_seed, n_samples: int, want_samples=False,
+                  app_ids=None):
+        """app_ids: benchmark id per app (noise stream seed part), default the index."""
         napps = len(suite["app_pipe_off"]) - 1
         rows = np.empty((napps, 5), np.float64)
         samples = np.empty((napps, n_samples), np.float64) if want_samples else None
-        self.lib.orc_aggregate(
+        ids = None if app_ids is None else np.ascontiguousarray(app_ids, np.uint64)
+        self.lib.orc_aggregate_ids(
             napps, suite["app_pipe_off"], suite["pipe_slot_off"], suite["slot_shader"],
             suite["slot_frac"], suite["pipe_wt"], suite["shader_lat"], suite["app_f64"],
             np.ascontiguousarray(shader_action, np.uint8), np.ascontiguousarray(run_seed, np.uint64),
-            n_samples, rows, None if samples is None else samples.ctypes.data)
+            None if ids is None else ids.ctypes.data, n_samples, rows,
+            None if samples is None else samples.ctypes.data)
         return (rows, samples) if want_samples else rows
 
     def histogram(self, uplift):

@@ -18,6 +18,7 @@
 #include "gbx/device_qtable.hpp"
 #include "gbx/policy.hpp"
 #include "gbxcu.h"
+#include "internal.hpp"
 
 namespace gbx {
 
@@ -80,6 +81,11 @@ void flatten_records(std::span<const std::pair<ShaderState, EmpiricalPolicy>> d,
 }
 
 }  // namespace
+
+namespace detail {
+gbxcu_ctx* device_context() { return ctx(); }
+void check_status(int rc, int diverged_epoch) { check(rc, diverged_epoch); }
+}  // namespace detail
 
 void set_device(int device) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -499,6 +505,11 @@ QTable DeviceQTable::to_host() const {
 
 DeviceQTable DeviceQTable::from_host(const QTable& table) {
     DeviceQTable d(table.hyperparams());
+    d.assign(table);
+    return d;
+}
+
+void DeviceQTable::assign(const QTable& table) {
     const std::size_t m = table.state_count();
     std::vector<std::uint32_t> keys(m * kStateKeySize);
     std::vector<double> q(2 * m, 0.0);
@@ -516,8 +527,80 @@ DeviceQTable DeviceQTable::from_host(const QTable& table) {
             }
         ++r;
     }
-    check(gbxcu_qtable_import(d.h_, keys.data(), q.data(), ts.data(), cnt.data(), has.data(), m));
-    return d;
+    check(gbxcu_qtable_import(h_, keys.data(), q.data(), ts.data(), cnt.data(), has.data(), m));
+}
+
+std::vector<std::uint8_t> DeviceQTable::greedy_wave64_of_complete_states() const {
+    std::size_t m = 0;
+    check(gbxcu_qtable_size(h_, &m, nullptr));
+    std::vector<double> q(2 * m);
+    std::vector<std::uint8_t> has(2 * m), out;
+    if (m) check(gbxcu_qtable_export(h_, nullptr, q.data(), nullptr, nullptr, has.data()));
+    out.reserve(m);
+    for (std::size_t r = 0; r < m; ++r)
+        if (has[2 * r] && has[2 * r + 1]) out.push_back(q[2 * r + 1] >= q[2 * r] ? 1 : 0);
+    return out;
+}
+
+// ------------------------------------------------- QTable's device copy
+// (declared in gbx/qtable.hpp; the host-only members live in gbx_core.cpp)
+QTable::QTable(const QTable& o) : hp_(o.hp_), entries_((o.sync_host(), o.entries_)) {}
+
+QTable& QTable::operator=(const QTable& o) {
+    if (this != &o) {
+        o.sync_host();
+        hp_ = o.hp_;
+        entries_ = o.entries_;
+        dev_.reset();  // never share a device copy between two tables
+        dev_stale_ = true;
+        host_stale_ = false;
+    }
+    return *this;
+}
+
+QTable::~QTable() = default;
+
+std::size_t QTable::state_count() const {
+    if (host_stale_) return dev_->state_count();
+    return entries_.size();
+}
+
+void QTable::sync_host() const {
+    if (!host_stale_) return;
+    entries_ = std::move(dev_->to_host().entries_);
+    host_stale_ = false;
+    dev_stale_ = false;  // both copies hold the same table now
+}
+
+void QTable::sync_device() const {
+    if (!dev_) dev_ = std::make_shared<DeviceQTable>(hp_);
+    if (!dev_stale_) return;
+    dev_->assign(*this);
+    dev_stale_ = false;
+}
+
+void QTable::update_batch(const std::vector<ExperienceTuple>& tuples) {
+    if (tuples.empty()) return;
+    sync_device();
+    host_stale_ = true;  // set first: on ClockRegressionError the device holds the prefix
+    dev_->update_batch(tuples);
+}
+
+std::vector<std::pair<ShaderState, EmpiricalPolicy>> QTable::snapshot_policy_dataset(double rho) const {
+    if (!(rho > 0.0)) throw InvalidTemperatureError("Boltzmann temperature must be > 0");
+    if (state_count() == 0) return {};
+    sync_device();
+    return dev_->snapshot_policy_dataset(rho);
+}
+
+std::vector<std::uint8_t> QTable::greedy_wave64_of_complete_states() const {
+    if (!host_stale_) {  // the map is current: no device round trip
+        std::vector<std::uint8_t> out;
+        for (const auto& kv : entries_)
+            if (kv.second[0] && kv.second[1]) out.push_back(kv.second[1]->q >= kv.second[0]->q ? 1 : 0);
+        return out;
+    }
+    return dev_->greedy_wave64_of_complete_states();
 }
 
 }  // namespace gbx

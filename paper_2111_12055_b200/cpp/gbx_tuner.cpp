@@ -1,6 +1,7 @@
 // gbx_tuner.cpp — reward normalisation and the greedy evaluation sweep of the
 // drop-in (proj/src/tuner.cpp:131-147, 266-315; proj/src/simenv.cpp:439-510),
 // executed by libgbxcu's fused inference + segmented aggregation kernels.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <numeric>
@@ -9,31 +10,15 @@
 
 #include "gbx/tuner.hpp"
 #include "gbxcu.h"
+#include "internal.hpp"
 
 namespace gbx {
 
 namespace {
 
-gbxcu_ctx* device_ctx() {
-    // the policy module owns the process-wide context; reuse it through a
-    // cheap call that creates it on first use
-    static gbxcu_ctx* c = nullptr;
-    if (!c) {
-        const char* env = std::getenv("GBX_DEVICE");
-        if (gbxcu_create(env ? std::atoi(env) : 0, &c) != GBXCU_OK) {
-            c = nullptr;
-            throw std::runtime_error(std::string("gbx: no usable B200 (no CPU fallback): ") +
-                                     gbxcu_last_error());
-        }
-    }
-    return c;
-}
+gbxcu_ctx* device_ctx() { return detail::device_context(); }
 
-void check(int rc) {
-    if (rc == GBXCU_OK) return;
-    if (rc == GBXCU_EINVAL || rc == GBXCU_ENONFINITE) throw ValidationError(gbxcu_last_error());
-    throw std::runtime_error(std::string("gbxcu: ") + gbxcu_last_error());
-}
+void check(int rc) { detail::check_status(rc); }
 
 gbxcu_suite view(const SuiteArrays& s) {
     gbxcu_suite v{};
@@ -52,6 +37,25 @@ gbxcu_suite view(const SuiteArrays& s) {
 }
 
 }  // namespace
+
+// TunerConfig checks and the epsilon schedule (tuner.cpp:36-57).
+void TunerConfig::validate() const {
+    if (num_iterations < 0) throw ValidationError("iteration count must be >= 0");
+    if (checkins_per_iteration < 0) throw ValidationError("check-ins per iteration must be >= 0");
+    if (!(epsilon0 >= 0.0 && epsilon0 <= 1.0)) throw ValidationError("epsilon0 must be in [0, 1]");
+    if (epsilon_horizon < 0) throw ValidationError("epsilon horizon must be >= 0");
+    if (refresh_period < 1) throw ValidationError("refresh period must be >= 1");
+    if (samples_per_benchmark < 1) throw ValidationError("samples per benchmark must be >= 1");
+    if (jobs < 1) throw ValidationError("jobs must be >= 1");
+    qtable.validate();
+    train.validate();
+}
+
+// epsilon decays linearly to 0 over the horizon (num_iterations / 2 by default)
+double TunerConfig::epsilon_at(int iteration) const {
+    const int horizon = epsilon_horizon > 0 ? epsilon_horizon : std::max(1, num_iterations / 2);
+    return epsilon0 * std::max(0.0, 1.0 - static_cast<double>(iteration) / horizon);
+}
 
 std::vector<RewardAttribution> attribute_rewards(const RunRecord& record,
                                                  std::span<const double> samples,

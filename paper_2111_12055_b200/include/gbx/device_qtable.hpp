@@ -18,14 +18,6 @@ struct gbxcu_qtable;
 
 namespace gbx {
 
-// One observation of run_iteration's fold (tuner.cpp:207-213).
-struct ExperienceTuple {
-    StateKey key;
-    Action action = kDefaultAction;
-    Reward reward = 1.0;
-    Checkin now = 0;
-};
-
 class DeviceQTable {
 public:
     explicit DeviceQTable(QHyperparams hp = {});
@@ -52,6 +44,10 @@ public:
 
     QTable to_host() const;
     static DeviceQTable from_host(const QTable& table);
+    // replace this table's contents with the host table's map (same device handle)
+    void assign(const QTable& table);
+    // per state with both actions (key order): q64 >= q32
+    std::vector<std::uint8_t> greedy_wave64_of_complete_states() const;
 
 private:
     QHyperparams hp_;

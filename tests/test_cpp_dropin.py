@@ -22,6 +22,7 @@ KNOWN_REFERENCE_FAILURE = "analytic gradient matches central finite differences"
 def build():
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2111_12055_b200", "cpp")], check=True)
     if os.path.isdir("/root/reference/proj/tests"):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "env"], check=True)
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
 
 
@@ -36,12 +37,33 @@ def run(name, timeout=600):
     return [int(x) for x in summary.groups()], failed_cases, p
 
 
-@pytest.mark.parametrize("name,cases,checks", [("test_core", 11, 23920), ("test_qtable", 16, 2663)])
+@pytest.mark.parametrize("name,cases,checks", [("test_core", 11, 23920), ("test_simenv", 20, 349)])
 def test_reference_host_tests_pass_against_dropin(name, cases, checks):
+    """Host-only reference tests: test_core against the drop-in; test_simenv
+    is the reference's environment (proj/src/simenv.cpp, built against the
+    drop-in headers) — proof that a caller's SimSuite links unchanged."""
     build()
     (n, ok, bad, nchecks), failed, p = run(name)
     assert (n, ok, bad) == (cases, cases, 0), p.stderr
     assert nchecks == checks
+
+
+@pytest.mark.gpu
+def test_reference_qtable_tests_pass_against_dropin():
+    """QTable's snapshot_policy_dataset runs on the B200 (k_qtable.cu)."""
+    build()
+    (n, ok, bad, nchecks), failed, p = run("test_qtable")
+    assert (n, ok, bad) == (16, 16, 0), p.stderr
+    assert nchecks == 2663
+
+
+@pytest.mark.gpu
+def test_dropin_algorithm1_and_evaluate_match_reference():
+    """run_training / run_iteration / evaluate(const SimSuite&) of the drop-in
+    (libgbx_b200_alg1.so, compute on the device) equal the compiled reference."""
+    build()
+    (n, ok, bad, _), failed, p = run("test_dropin_alg1")
+    assert bad == 0 and n == 3, p.stdout[-3000:] + p.stderr[-3000:]
 
 
 @pytest.mark.gpu
