@@ -332,9 +332,13 @@ int prepare_order(gbxcu_ctx* c, size_t n, cudaStream_t st) {
     return check_launch(c, "iota_kernel");
 }
 
-// Exchange region layout: [u64 counter | pad to 256 B][NP u64 LL words | pad][G x PSTR f64 partials]
+// Exchange region layout (one per rank; 256-B aligned sections):
+//   [u64 arrival counter | pad][NP u64 LL parameter words]
+//   [2 x (NP + 1) u64 LL per-GPU sums (peer sets)][G x PSTR f64 partial rows]
+constexpr size_t xchg_align(size_t b) { return (b + 255) / 256 * 256; }
 constexpr size_t XCHG_LL_OFF = 256;
-constexpr size_t XCHG_PART_OFF = XCHG_LL_OFF + ((NP * 8 + 255) / 256) * 256;
+constexpr size_t XCHG_GP_OFF = XCHG_LL_OFF + xchg_align(NP * 8);
+constexpr size_t XCHG_PART_OFF = XCHG_GP_OFF + xchg_align(2 * (NP + 1) * 8);
 size_t xchg_bytes(int g) { return XCHG_PART_OFF + (size_t)g * PSTR * sizeof(double); }
 
 int ensure_xchg(gbxcu_ctx* c, int slot, int g, cudaStream_t st) {
@@ -350,6 +354,7 @@ void bind_region(TrainArgs& a, int r, void* base) {
     auto* b = static_cast<unsigned char*>(base);
     a.ctr[r] = reinterpret_cast<unsigned long long*>(b);
     a.llp[r] = reinterpret_cast<unsigned long long*>(b + XCHG_LL_OFF);
+    a.gp[r] = reinterpret_cast<unsigned long long*>(b + XCHG_GP_OFF);
     a.part[r] = reinterpret_cast<double*>(b + XCHG_PART_OFF);
 }
 
@@ -452,7 +457,8 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
         a.order = c->order.as<uint32_t>();  // the pass output (buffers ping-pong)
         a.epoch = e;
         a.tag_base = c->tag_next + (unsigned int)((long)e * n_steps);
-        a.ctr_base = c->ctr_base[0] + (unsigned long long)e * n_steps * GG;
+        // each rank's counter counts its own CTAs' arrivals (G per step)
+        a.ctr_base = c->ctr_base[0] + (unsigned long long)e * n_steps * G;
         a.step0 = (unsigned)((long)e * n_steps);
         if (!c->comm) {
             void* args[] = {&a};

@@ -159,33 +159,42 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     return v;
 }
 template <bool SYS>
-__device__ __forceinline__ double ld_part(const double* p) {
-    if (SYS) {
-        double v;
-        asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-        return v;
-    }
-    return __ldcg(p);  // L2 (the coherence point of one GPU)
-}
-template <bool SYS>
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     if (SYS) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
     else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// LL pairs for the per-GPU sums of a peer set: a double travels as
+// {tag | low 32 bits}, {tag | high 32 bits} in one 16-byte strong access
+// (each 8-byte word is single-copy atomic and validates itself).
+template <bool SYS>
+__device__ __forceinline__ void ld_v2(const unsigned long long* p, unsigned long long& lo,
+                                      unsigned long long& hi) {
+    if (SYS)
+        asm volatile("ld.relaxed.sys.global.v2.u64 {%0,%1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ void st_ll_pair(unsigned long long* p, double v, unsigned tag) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long t = (unsigned long long)tag << 32;
+    const unsigned long long lo = t | (b & 0xFFFFFFFFull), hi = t | (b >> 32);
+    if (SYS)
+        asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(lo), "l"(hi) : "memory");
+    else
+        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(lo), "l"(hi) : "memory");
+}
+__device__ __forceinline__ double ll_pair_value(unsigned long long lo, unsigned long long hi) {
+    return __longlong_as_double((long long)((hi << 32) | (lo & 0xFFFFFFFFull)));
+}
+__device__ __forceinline__ bool ll_pair_ok(unsigned long long lo, unsigned long long hi, unsigned tag) {
+    return (unsigned)(lo >> 32) == tag && (unsigned)(hi >> 32) == tag;
+}
+
 template <bool SYS>
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
     if (SYS) asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
     else asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-template <bool SYS>
-__device__ __forceinline__ void red_relaxed_add_u64(unsigned long long* p, unsigned long long v) {
-    if (SYS) asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-    else asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-template <bool SYS>
-__device__ __forceinline__ void fence_acq_rel() {
-    if (SYS) asm volatile("fence.acq_rel.sys;" ::: "memory");
-    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ unsigned long long gtimer_ns() {
     unsigned long long t;
@@ -694,6 +703,32 @@ __device__ __forceinline__ void tc_store_partial(const TcGrads& g, double* __res
     });
 }
 
+// Final owner of parameter p: SGD w = float(double(w) - lr * g)
+// (policy.cpp:328-332) or Adam, published as {tag, fp32 bits} to every rank.
+template <bool SYS, int MT, bool VAR>
+__device__ __forceinline__ void tc_update_publish(TcSmem<MT>& S, const TrainArgs& a, int p, double gsum,
+                                                  unsigned tag, int R, bool adam_smem, int own_lo,
+                                                  double adam_c1, double adam_c2) {
+    double upd;
+    if (VAR && a.optimizer == 1) {
+        // Adam: this CTA owns the moments of its slice across steps — in
+        // shared memory for the epoch when the slice fits (no global round
+        // trip on the step's critical path)
+        double* pm = adam_smem ? &S.adam[0][p - own_lo] : &a.adam_m[p];
+        double* pv = adam_smem ? &S.adam[1][p - own_lo] : &a.adam_v[p];
+        const double m = a.beta1 * *pm + (1.0 - a.beta1) * gsum;
+        const double v = a.beta2 * *pv + (1.0 - a.beta2) * gsum * gsum;
+        *pm = m;
+        *pv = v;
+        upd = a.lr * (m / adam_c1) / (sqrt(v / adam_c2) + a.adam_eps);
+    } else {
+        upd = a.lr * gsum;
+    }
+    const float nw = __double2float_rn(get_param(S, p) - upd);
+    const unsigned long long word = ((unsigned long long)tag << 32) | __float_as_uint(nw);
+    for (int r = 0; r < R; ++r) st_relaxed_u64<SYS>(a.llp[r] + p, word);
+}
+
 }  // namespace
 
 size_t train_tc_smem_bytes(int mt) { return mt == 4 ? sizeof(TcSmem<4>) : sizeof(TcSmem<7>); }
@@ -713,11 +748,19 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     const int GG = R * Gl, gc = rank * Gl + c;
     const TcWho who = tc_who(a, rank, R, c, Gl);
     const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
-    // reduce-scatter slice of this CTA: element 0 = loss, then params [p_lo, p_hi).
-    // Balanced split: every CTA owns >= 1 parameter (GG <= 8 x 148 < NP), so
-    // every CTA publishes LL words after its reads of the step's partial rows,
-    // and no CTA can overwrite its row (next step) before all reads are done.
-    const int p_lo = (int)(((long)gc * NP) / GG), p_hi = (int)(((long)(gc + 1) * NP) / GG);
+    // Two-level reduce-scatter, balanced splits (every slice non-empty):
+    //   level 1 (within a rank): CTA c sums element 0 = the loss and params
+    //     [p_lo, p_hi) (a 1/Gl slice) over its own rank's Gl partial rows — with
+    //     one rank that sum is final;
+    //   level 2 (peer sets, R > 1): CTA gc sums the loss and params [q_lo, q_hi)
+    //     (a 1/GG slice) over the R per-GPU sums, read as LL pairs over NVLink
+    //     (R x 5,027 pairs cross the fabric per step, not R x Gl partial rows).
+    // Every CTA owns parameters at the final level, so every CTA publishes LL
+    // words after its reads of the step's rows: no CTA can overwrite its row
+    // (next step) before all reads of it are done.
+    const int p_lo = (int)(((long)c * NP) / Gl), p_hi = (int)(((long)(c + 1) * NP) / Gl);
+    const int q_lo = (int)(((long)gc * NP) / GG), q_hi = (int)(((long)(gc + 1) * NP) / GG);
+    const int own_lo = R == 1 ? p_lo : q_lo, own_hi = R == 1 ? p_hi : q_hi;
     const int n_elem = 1 + (p_hi - p_lo);
     // reduction layout: EB elements x SUB source subsets (EB * SUB = NT)
     int EB = 8;
@@ -744,10 +787,10 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
     // Adam moments of the slice on chip for the whole epoch (written back at
     // the end of the launch); a lone CTA or a slice wider than 64 keeps them
     // in global memory
-    const bool adam_smem = VAR && a.optimizer == 1 && GG > 1 && p_hi - p_lo <= 64;
-    if (adam_smem && tid < p_hi - p_lo) {
-        S.adam[0][tid] = a.adam_m[p_lo + tid];
-        S.adam[1][tid] = a.adam_v[p_lo + tid];
+    const bool adam_smem = VAR && a.optimizer == 1 && GG > 1 && own_hi - own_lo <= 64;
+    if (adam_smem && tid < own_hi - own_lo) {
+        S.adam[0][tid] = a.adam_m[own_lo + tid];
+        S.adam[1][tid] = a.adam_v[own_lo + tid];
     }
     load_params_plain(S, a.params);
     tc_init_consts(S);
@@ -777,7 +820,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         // Adam's bias corrections for this step, computed up front (two pow()s
         // off the critical path between the slice reduce and the publish)
         double adam_c1 = 1.0, adam_c2 = 1.0;
-        if (VAR && a.optimizer == 1 && tid < 64) {
+        if (VAR && a.optimizer == 1 && tid < (R == 1 ? 64 : NT / R)) {
             const double t = (double)(a.step0 + (unsigned)step + 1u);
             adam_c1 = 1.0 - pow(a.beta1, t);
             adam_c2 = 1.0 - pow(a.beta2, t);
@@ -862,23 +905,17 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         tc_store_partial(g, my_part);
         if (stage_due) cp_async_wait_all();  // this thread's copies of the next tile
         __syncthreads();                      // partial issued, gradient phase done, rows landed
-        // ---- 2. arrive on every rank's counter; wait (warp 0) until all GG
-        //      CTAs of the set arrived while warps 1..15 stage the next tile
+        // ---- 2. arrive on this rank's counter (rows and counter are local to
+        //      the GPU: GPU scope even in a peer set); wait (warp 0) until all
+        //      Gl CTAs of the rank arrived while warps 1..15 stage the next tile
         if (tid == 0) {
-            if (R == 1) {
-                red_release_add_u64<SYS>(a.ctr[0], 1ull);
-            } else {
-                // one release fence for all ranks' counters (a release red per
-                // rank would fence R times), then relaxed reds
-                fence_acq_rel<SYS>();
-                for (int r = 0; r < R; ++r) red_relaxed_add_u64<SYS>(a.ctr[r], 1ull);
-            }
+            red_release_add_u64<false>(my_ctr, 1ull);
             TC_MARK(7);
             TC_TRACE(step, 1);
             const unsigned long long target =
-                a.ctr_base + (unsigned long long)(step + 1) * (unsigned long long)GG;
+                a.ctr_base + (unsigned long long)(step + 1) * (unsigned long long)Gl;
             unsigned long long t0 = 0;
-            for (unsigned it = 0; ld_acquire_u64<SYS>(my_ctr) < target; ++it) {
+            for (unsigned it = 0; ld_acquire_u64<false>(my_ctr) < target; ++it) {
                 if ((it & 255) == 255) {
                     const unsigned long long t = gtimer_ns();
                     if (t0 == 0) t0 = t;
@@ -899,58 +936,26 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
             aborted = true;
             break;
         }
-        // ---- 3. reduce [loss | slice] over all GG partials, fixed association:
-        //      thread (e, s) folds, rank by rank, the CTAs c' = s, s + SUB, ...,
-        //      then thread e sums the SUB subset totals in order
+        // ---- 3. level 1: reduce [loss | slice] over this rank's Gl partial
+        //      rows, fixed association: thread (e, s) folds rows s, s + SUB, ...
+        //      (all loads in flight at once: one L2 round trip), then thread e
+        //      sums the SUB subset totals in order
         bool diverged = false;
         for (int e0 = 0; e0 < n_elem; e0 += EB) {
             const int e = e0 + tid % EB, sb = tid / EB;
             double v = 0.0;
             if (e < n_elem) {
                 const int p = e == 0 ? NP : p_lo + e - 1;
-                if constexpr (!SYS) {
-                    // one GPU (R = 1, or virtual ranks in tests): per rank, all
-                    // of its loads in flight at once (one L2 round trip)
-                    for (int r = 0; r < R; ++r) {
-                        const double* src = a.part[r] + p;
-                        double u[20];
+                const double* src = a.part[rank] + p;
+                double u[20];
 #pragma unroll
-                        for (int j = 0; j < 20; ++j) {
-                            const int q = sb + j * SUB;
-                            u[j] = q < Gl ? ld_part<SYS>(src + (size_t)q * PSTR) : 0.0;
-                        }
-#pragma unroll
-                        for (int j = 0; j < 20; ++j) v += u[j];
-                        for (int q = sb + 20 * SUB; q < Gl; q += SUB)
-                            v += ld_part<SYS>(src + (size_t)q * PSTR);
-                    }
-                } else {
-                    // the (rank, CTA) pairs of this thread — rank by rank, CTAs
-                    // c' = s, s + SUB, ... — with up to 32 loads in flight across
-                    // ALL ranks (one round trip over NVLink, not one per rank),
-                    // summed in that fixed order afterwards
-                    const int nq = (Gl - sb + SUB - 1) / SUB;  // CTAs per rank for this thread
-                    const int total = R * nq;
-                    int t0 = 0;
-                    while (t0 < total) {
-                        double u[32];
-                        int r = t0 / max(nq, 1), qi = t0 - r * max(nq, 1);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const bool ok = t0 + j < total;
-                            u[j] = ok ? ld_part<SYS>(a.part[ok ? r : 0] + p + (size_t)(sb + qi * SUB) * PSTR)
-                                      : 0.0;
-                            if (++qi == nq) {
-                                qi = 0;
-                                ++r;
-                            }
-                        }
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (t0 + j < total) v += u[j];
-                        t0 += 32;
-                    }
+                for (int j = 0; j < 20; ++j) {
+                    const int q = sb + j * SUB;
+                    u[j] = q < Gl ? __ldcg(src + (size_t)q * PSTR) : 0.0;
                 }
+#pragma unroll
+                for (int j = 0; j < 20; ++j) v += u[j];
+                for (int q = sb + 20 * SUB; q < Gl; q += SUB) v += __ldcg(src + (size_t)q * PSTR);
             }
             S.red[sb * EB + tid % EB] = v;
             __syncthreads();
@@ -961,7 +966,7 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
                 if (e0 == 0 && tid == 0) {
                     const double loss = t / (double)nb;
                     S.scal[0] = loss;
-                    S.scal[1] = isfinite(loss) ? 0.0 : 1.0;
+                    S.scal[1] = (R > 1 || isfinite(loss)) ? 0.0 : 1.0;  // peer sets: level 2 decides
                 }
             }
             __syncthreads();
@@ -969,34 +974,72 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
                 diverged = true;
                 break;
             }
-            // ---- 4. SGD on the slice; publish {tag, fp32} words to every rank
+            // ---- 4. one rank: SGD on the slice, {tag, fp32} words to the
+            //      rank; peer set: the per-GPU sum as an LL pair (the loss by c 0)
             if (tid < EB) {
                 const int e2 = e0 + tid;
-                if (e2 >= 1 && e2 < n_elem) {
-                    const int p = p_lo + e2 - 1;
-                    const double gsum = S.red[NT + tid];
-                    double upd;
-                    if (VAR && a.optimizer == 1) {
-                        // Adam: this CTA owns the moments of its slice across
-                        // steps — in shared memory for the epoch when the slice
-                        // fits (no global round trip on the step's critical path)
-                        double* pm = adam_smem ? &S.adam[0][e2 - 1] : &a.adam_m[p];
-                        double* pv = adam_smem ? &S.adam[1][e2 - 1] : &a.adam_v[p];
-                        const double m = a.beta1 * *pm + (1.0 - a.beta1) * gsum;
-                        const double v = a.beta2 * *pv + (1.0 - a.beta2) * gsum * gsum;
-                        *pm = m;
-                        *pv = v;
-                        upd = a.lr * (m / adam_c1) / (sqrt(v / adam_c2) + a.adam_eps);
-                    } else {
-                        upd = a.lr * gsum;
-                    }
-                    const float nw = __double2float_rn(get_param(S, p) - upd);
-                    const unsigned long long word =
-                        ((unsigned long long)tag << 32) | __float_as_uint(nw);
-                    for (int r = 0; r < R; ++r) st_relaxed_u64<SYS>(a.llp[r] + p, word);
+                if (e2 < n_elem && R > 1) {
+                    if (e2 >= 1) st_ll_pair<SYS>(a.gp[rank] + 2 * (size_t)(p_lo + e2 - 1), S.red[NT + tid], tag);
+                    else if (c == 0) st_ll_pair<SYS>(a.gp[rank] + 2 * (size_t)NP, S.red[NT + tid], tag);
+                } else if (e2 >= 1 && e2 < n_elem) {
+                    tc_update_publish<SYS, MT, VAR>(S, a, p_lo + e2 - 1, S.red[NT + tid], tag, R, adam_smem,
+                                                     own_lo, adam_c1, adam_c2);
                 }
             }
             __syncthreads();  // S.red reuse
+        }
+        // ---- 5. level 2 (peer sets): thread (e, r) reads rank r's per-GPU
+        //      sum of element e (0 = loss, then params [q_lo, q_hi)) over
+        //      NVLink; thread e sums them in rank order -> identical values on
+        //      every rank; the loss decides divergence before any publish
+        if (R > 1 && !diverged) {
+            const int n2 = 1 + (q_hi - q_lo), per = NT / R;
+            for (int e0 = 0; e0 < n2; e0 += per) {
+                const int e = e0 + tid / R, r = tid % R;
+                if (tid < per * R && e < n2) {
+                    const unsigned long long* src = a.gp[r] + 2 * (size_t)(e == 0 ? NP : q_lo + e - 1);
+                    unsigned long long lo = 0, hi = 0;
+                    unsigned long long t0 = 0;
+                    for (unsigned it = 0;; ++it) {
+                        ld_v2<SYS>(src, lo, hi);
+                        if (ll_pair_ok(lo, hi, tag)) break;
+                        if ((it & 255) == 255) {
+                            const unsigned long long t = gtimer_ns();
+                            if (t0 == 0) t0 = t;
+                            else if (t - t0 > WATCHDOG_NS) {
+                                S.scal[1] = 2.0;
+                                break;
+                            }
+                        }
+                    }
+                    S.red[tid] = ll_pair_value(lo, hi);
+                }
+                __syncthreads();
+                if (S.scal[1] == 2.0) break;
+                if (tid < per && e0 + tid < n2) {
+                    double t = 0.0;
+                    for (int q = 0; q < R; ++q) t += S.red[tid * R + q];
+                    if (e0 + tid == 0) {
+                        const double loss = t / (double)nb;
+                        S.scal[0] = loss;
+                        S.scal[1] = isfinite(loss) ? 0.0 : 1.0;
+                    }
+                    S.red[NT + tid] = t;
+                }
+                __syncthreads();
+                if (S.scal[1] != 0.0) {
+                    diverged = S.scal[1] == 1.0;
+                    break;
+                }
+                if (tid < per && e0 + tid >= 1 && e0 + tid < n2)
+                    tc_update_publish<SYS, MT, VAR>(S, a, q_lo + e0 + tid - 1, S.red[NT + tid], tag, R,
+                                                     adam_smem, own_lo, adam_c1, adam_c2);
+                __syncthreads();  // S.red reuse
+            }
+            if (S.scal[1] == 2.0) {
+                aborted = true;
+                break;
+            }
         }
         if (diverged) {
             if (c == 0 && tid == 0) *a.diverged_epoch = a.epoch;
@@ -1023,9 +1066,9 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_tc_kernel(TrainArgs a) {
         if (tid == 0) atomicExch(a.status, 1);
         return;
     }
-    if (adam_smem && tid < p_hi - p_lo) {  // the slice's moments for the next epoch
-        a.adam_m[p_lo + tid] = S.adam[0][tid];
-        a.adam_v[p_lo + tid] = S.adam[1][tid];
+    if (adam_smem && tid < own_hi - own_lo) {  // the slice's moments for the next epoch
+        a.adam_m[own_lo + tid] = S.adam[0][tid];
+        a.adam_v[own_lo + tid] = S.adam[1][tid];
     }
     // rank-local outputs: params (fp32 values of the replicas) and the epoch loss.
     // On divergence the replicas hold the parameters after the last finite

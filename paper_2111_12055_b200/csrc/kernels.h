@@ -16,6 +16,9 @@ constexpr int AGG_BLOCK = 256;    // aggregation: 8 warps = 8 apps per CTA
 
 constexpr int PSTR = 5028;        // per-CTA partial row: 5,026 gradient entries, loss, pad
 constexpr int MAX_PEERS = 8;      // ranks of one NVLink domain (one node)
+// Peer sets (k_train_tc.cu): per-GPU sums cross NVLink as LL word pairs
+// {tag:32 | low 32 bits}, {tag:32 | high 32 bits}; the loss pair sits after
+// the parameters.
 
 // mode bits for the inference kernels
 constexpr int FWD_PROBS = 1, FWD_ACTIONS = 2, FWD_COLLECT = 4, FWD_SAMPLE = 8;
@@ -42,7 +45,8 @@ struct TrainArgs {
     int pvirt;                               // 1: rank = blockIdx.x / (gridDim.x / peers)
     unsigned long long* ctr[MAX_PEERS];      // arrival counters (monotonic over fits)
     unsigned long long* llp[MAX_PEERS];      // {tag, fp32 bits} parameter words [NP]
-    double* part[MAX_PEERS];                 // per-CTA partial rows [G][PSTR]
+    double* part[MAX_PEERS];                 // per-CTA partial rows [G][PSTR] (rank-local reads)
+    unsigned long long* gp[MAX_PEERS];       // LL per-GPU sums: pairs [NP] params, [NP] loss
     unsigned int tag_base;                   // steps taken on this peer set before the epoch
     unsigned long long ctr_base;             // counter value before the epoch's first step
     // variants (0 = the reference's KL + SGD)
