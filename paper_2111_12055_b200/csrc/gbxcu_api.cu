@@ -250,6 +250,15 @@ int run_forward(gbxcu_ctx* c, const float* d_params, const float* d_feat, size_t
     return GBXCU_OK;
 }
 
+// aggregation: one warp per app, up to 8 CTAs of AGG_BLOCK per SM
+int launch_aggregate(gbxcu_ctx* c, const AggArgs& a, cudaStream_t st) {
+    const size_t per_cta = AGG_BLOCK / 32;
+    const int grid = (int)std::max<size_t>(1, std::min<size_t>((a.n_apps + per_cta - 1) / per_cta,
+                                                               (size_t)c->num_sms * 8));
+    aggregate_kernel<<<grid, AGG_BLOCK, 0, st>>>(a);
+    return check_launch(c, "aggregate_kernel");
+}
+
 int check_flags(DevBuf& flags, cudaStream_t st) {
     unsigned int f = 0;
     CK(cudaMemcpyAsync(&f, flags.p, sizeof(f), cudaMemcpyDeviceToHost, st));
@@ -1447,9 +1456,7 @@ int gbxcu_aggregate(gbxcu_ctx* c, const gbxcu_suite* s, const uint8_t* shader_ac
     a.n_samples = n_samples;
     a.rows = c->s_rows.as<double>();
     a.samples = samples_out ? c->s_samples.as<double>() : nullptr;
-    const int grid = (int)std::min<size_t>((s->n_apps + 7) / 8, (size_t)c->num_sms * 8);
-    aggregate_kernel<<<grid, AGG_BLOCK, 0, st>>>(a);
-    RET(check_launch(c, "aggregate_kernel"));
+    RET(launch_aggregate(c, a, st));
     CK(cudaMemcpyAsync(rows_out, c->s_rows.p, sizeof(double) * 5 * s->n_apps,
                        cudaMemcpyDeviceToHost, st));
     if (samples_out)
@@ -1563,9 +1570,7 @@ static int evaluate_dev(gbxcu_ctx* c, const gbxcu_dsuite* s, const float* d_para
     a.n_samples = n_samples;
     a.rows = d_rows;
     a.samples = nullptr;
-    const int grid = (int)std::min<size_t>((s->n_apps + 7) / 8, (size_t)c->num_sms * 8);
-    aggregate_kernel<<<grid, AGG_BLOCK, 0, st>>>(a);
-    return check_launch(c, "aggregate_kernel");
+    return launch_aggregate(c, a, st);
 }
 
 // One app-range shard of evaluate (aggregation shards by app so
@@ -1624,9 +1629,7 @@ int gbxcu_evaluate_shard(gbxcu_ctx* c, const gbxcu_dsuite* s, const float* param
     a.n_samples = n_samples;
     a.rows = sm->rows.as<double>();
     a.app_base = app_lo;
-    const int grid = (int)std::min<size_t>((a.n_apps + 7) / 8, (size_t)c->num_sms * 8);
-    aggregate_kernel<<<grid, AGG_BLOCK, 0, st>>>(a);
-    RET(check_launch(c, "aggregate_kernel"));
+    RET(launch_aggregate(c, a, st));
     CK(cudaMemcpyAsync(rows_out, sm->rows.p, sizeof(double) * 5 * a.n_apps, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return GBXCU_OK;

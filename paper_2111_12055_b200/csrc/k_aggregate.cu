@@ -10,19 +10,95 @@
 // (coalesced slot arrays, gathered shader latents/actions), forms the 32
 // per-slot terms in parallel, and folds them in slot order with register
 // shuffles — the serial part is one DADD per slot, everything else (gathers,
-// products, divisions) is lane-parallel. Results are bit-identical to the
-// reference.
+// products, divisions) is lane-parallel, and the loads run two chunks ahead
+// of the fold (see SlotRaw). Results are bit-identical to the reference.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace gbxcu {
 
+// acc (+|-)= term of lanes 0..count-1, in lane order. A full chunk is
+// unrolled so every shuffle issues ahead of the serial DADD chain.
 __device__ __forceinline__ double warp_fold(double acc, double term, int count, bool sub) {
+    if (count == 32) {
+#pragma unroll
+        for (int k0 = 0; k0 < 32; k0 += 8) {
+            double t[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, term, k0 + k);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc = sub ? __dsub_rn(acc, t[k]) : __dadd_rn(acc, t[k]);
+        }
+        return acc;
+    }
     for (int k = 0; k < count; ++k) {
         const double t = __shfl_sync(0xffffffffu, term, k);
         acc = sub ? __dsub_rn(acc, t) : __dadd_rn(acc, t);
     }
     return acc;
+}
+
+// Slot stream of a warp: 32 slots per chunk, loads software-pipelined two
+// chunks deep so the memory round trips overlap the (serial) fold of the
+// current chunk: at chunk c the slot arrays of chunk c+2 and the gathers of
+// chunk c+1 are in flight.
+struct SlotRaw {
+    uint32_t sh;
+    double frac;
+};
+
+__device__ __forceinline__ SlotRaw slot_raw(const AggArgs& a, uint64_t s, uint64_t s_hi) {
+    SlotRaw r{0xFFFFFFFFu, 0.0};
+    if (s < s_hi) {
+        r.sh = a.slot_shader[s];
+        r.frac = a.slot_frac[s];
+    }
+    return r;
+}
+
+// pass-1 term of a slot: p * demand(a)
+struct Term1In {
+    double frac, bw;
+    uint8_t act;
+    bool ok;
+};
+__device__ __forceinline__ Term1In term1_gather(const AggArgs& a, const SlotRaw& r) {
+    Term1In t{r.frac, 0.0, 0, r.sh != 0xFFFFFFFFu};
+    if (t.ok) {
+        t.bw = a.shader_lat[3 * (size_t)r.sh + 1];
+        t.act = a.shader_action[r.sh];
+    }
+    return t;
+}
+__device__ __forceinline__ double term1(const Term1In& t) {
+    if (!t.ok) return 0.0;
+    const double demand = t.act == 1 ? __dmul_rn(2.0, t.bw) : t.bw;
+    return __dmul_rn(t.frac, demand);
+}
+
+// pass-2 term of a slot: p / s_eff
+struct Term2In {
+    double frac, d, bw, kap;
+    uint8_t act;
+    bool ok;
+};
+__device__ __forceinline__ Term2In term2_gather(const AggArgs& a, const SlotRaw& r) {
+    Term2In t{r.frac, 0.0, 0.0, 0.0, 0, r.sh != 0xFFFFFFFFu};
+    if (t.ok) {
+        const double* lat = a.shader_lat + 3 * (size_t)r.sh;
+        t.d = lat[0];
+        t.bw = lat[1];
+        t.kap = lat[2];
+        t.act = a.shader_action[r.sh];
+    }
+    return t;
+}
+__device__ __forceinline__ double term2(const Term2In& t, double thr, double throttle) {
+    if (!t.ok) return 0.0;
+    // wave64_speedup = (1 + kappa)(1 - 0.5 d)  (simenv.hpp:65-67)
+    double sp = t.act == 1 ? __dmul_rn(__dadd_rn(1.0, t.kap), __dsub_rn(1.0, __dmul_rn(0.5, t.d))) : 1.0;
+    if (t.bw > thr) sp = __dmul_rn(sp, throttle);
+    return __ddiv_rn(t.frac, sp);
 }
 
 __global__ void __launch_bounds__(AGG_BLOCK) aggregate_kernel(AggArgs a) {
@@ -34,19 +110,17 @@ __global__ void __launch_bounds__(AGG_BLOCK) aggregate_kernel(AggArgs a) {
         const double sigma = a.app_f64[4 * app + 2], thr = a.app_f64[4 * app + 3];
         const uint64_t p_lo = a.app_pipe_off[app], p_hi = a.app_pipe_off[app + 1];
 
-        // pass 1: bandwidth load = sum over all slots of p * demand(a)
+        // pass 1: bandwidth load = sum over all slots of p * demand(a) — the
+        // app's slots are contiguous (pipelines in order), one stream
         double load = 0.0;
-        for (uint64_t p = p_lo; p < p_hi; ++p) {
-            const uint64_t s_lo = a.pipe_slot_off[p], s_hi = a.pipe_slot_off[p + 1];
+        {
+            const uint64_t s_lo = a.pipe_slot_off[p_lo], s_hi = a.pipe_slot_off[p_hi];
+            SlotRaw raw2 = slot_raw(a, s_lo + 32 + lane, s_hi);
+            Term1In in1 = term1_gather(a, slot_raw(a, s_lo + lane, s_hi));
             for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
-                const uint64_t s = s0 + lane;
-                double term = 0.0;
-                if (s < s_hi) {
-                    const uint32_t sh = a.slot_shader[s];
-                    const double bw = a.shader_lat[3 * (size_t)sh + 1];
-                    const double demand = a.shader_action[sh] == 1 ? __dmul_rn(2.0, bw) : bw;
-                    term = __dmul_rn(a.slot_frac[s], demand);
-                }
+                const double term = term1(in1);
+                in1 = term1_gather(a, raw2);               // chunk c+1's gathers
+                raw2 = slot_raw(a, s0 + 64 + lane, s_hi);  // chunk c+2's slot arrays
                 load = warp_fold(load, term, (int)min((uint64_t)32, s_hi - s0), false);
             }
         }
@@ -58,27 +132,23 @@ __global__ void __launch_bounds__(AGG_BLOCK) aggregate_kernel(AggArgs a) {
         for (uint64_t p = p_lo; p < p_hi; ++p) {
             const uint64_t s_lo = a.pipe_slot_off[p], s_hi = a.pipe_slot_off[p + 1];
             double inner = 1.0;
-            for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
-                const uint64_t s = s0 + lane;
-                const double term = s < s_hi ? a.slot_frac[s] : 0.0;
-                inner = warp_fold(inner, term, (int)min((uint64_t)32, s_hi - s0), true);
-            }
-            for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
-                const uint64_t s = s0 + lane;
-                double term = 0.0;
-                if (s < s_hi) {
-                    const uint32_t sh = a.slot_shader[s];
-                    const double d = a.shader_lat[3 * (size_t)sh];
-                    const double bw = a.shader_lat[3 * (size_t)sh + 1];
-                    const double kap = a.shader_lat[3 * (size_t)sh + 2];
-                    // wave64_speedup = (1 + kappa)(1 - 0.5 d)  (simenv.hpp:65-67)
-                    double sp = a.shader_action[sh] == 1
-                                    ? __dmul_rn(__dadd_rn(1.0, kap), __dsub_rn(1.0, __dmul_rn(0.5, d)))
-                                    : 1.0;
-                    if (bw > thr) sp = __dmul_rn(sp, throttle);
-                    term = __ddiv_rn(a.slot_frac[s], sp);
+            {
+                double fnext = s_lo + lane < s_hi ? a.slot_frac[s_lo + lane] : 0.0;
+                for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+                    const double term = fnext;
+                    fnext = s0 + 32 + lane < s_hi ? a.slot_frac[s0 + 32 + lane] : 0.0;
+                    inner = warp_fold(inner, term, (int)min((uint64_t)32, s_hi - s0), true);
                 }
-                inner = warp_fold(inner, term, (int)min((uint64_t)32, s_hi - s0), false);
+            }
+            {
+                SlotRaw raw2 = slot_raw(a, s_lo + 32 + lane, s_hi);
+                Term2In in2 = term2_gather(a, slot_raw(a, s_lo + lane, s_hi));
+                for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+                    const double term = term2(in2, thr, throttle);
+                    in2 = term2_gather(a, raw2);
+                    raw2 = slot_raw(a, s0 + 64 + lane, s_hi);
+                    inner = warp_fold(inner, term, (int)min((uint64_t)32, s_hi - s0), false);
+                }
             }
             const double wt = __dmul_rn(a.pipe_wt[2 * p], a.pipe_wt[2 * p + 1]);
             total = __dadd_rn(total, __dmul_rn(wt, inner));
