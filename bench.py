@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--qt-tuples", type=int, default=10_000_000,
                     help="experience-store secondary: tuples folded into a fresh device Q-table")
     ap.add_argument("--c5-shaders-per-app", type=int, default=10_000)
+    ap.add_argument("--wide-records", type=int, default=10_000_000,
+                    help="C4 secondary: records of the wide-MLP (hidden 512) epoch")
     return ap.parse_args()
 
 
@@ -474,22 +476,36 @@ def main():
     ms_step = ms_max / args.steps
     value = n_total * args.steps / (ms_max * 1e-3)
 
-    # ---- e2e: public host API, host buffers, H2D + D2H inside the region
-    pinned_feat = torch.from_numpy(feat_h).pin_memory().numpy()
-    pinned_tgt = torch.from_numpy(tgt_h).pin_memory().numpy()
-    dev.fit(params0, pinned_feat, pinned_tgt, args.lr, 1, batch, 99)  # warm
+    # ---- e2e: public host API, host buffers, H2D + D2H inside the region.
+    #      N = 1: gbxcu_fit (uploads the whole log). N > 1: fit_sharded — each
+    #      rank uploads only its 1/N of the log from pinned memory and the
+    #      shards are all-gathered over NVLink before the fused fit.
+    lo, hi = rank * args.n, (rank + 1) * args.n
+    pinned_feat = torch.from_numpy(feat_h[lo:hi] if world > 1 else feat_h).pin_memory().numpy()
+    pinned_tgt = torch.from_numpy(tgt_h[lo:hi] if world > 1 else tgt_h).pin_memory().numpy()
+
+    def e2e_step():
+        if world > 1:
+            dev.fit_sharded(params0, pinned_feat, pinned_tgt, args.lr, 1, batch, 99)
+        else:
+            dev.fit(params0, pinned_feat, pinned_tgt, args.lr, 1, batch, 99)
+
+    e2e_step()  # warm
     barrier()
     e2e_times = []
     for _ in range(max(1, min(args.steps, 5))):
+        barrier()
         t0 = time.perf_counter()
-        dev.fit(params0, pinned_feat, pinned_tgt, args.lr, 1, batch, 99)
+        e2e_step()
         e2e_times.append(time.perf_counter() - t0)
     tt = torch.tensor([statistics.median(e2e_times)], device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e = {"value": n_total / float(tt.item()), "unit": "samples/s",
-           "h2d_bytes_per_step": int(feat_h.nbytes + tgt_h.nbytes + 4 * 5026),
-           "d2h_bytes_per_step": int(4 * 5026 + 8)}
+           "h2d_bytes_per_step": int(pinned_feat.nbytes + pinned_tgt.nbytes + 4 * 5026),
+           "d2h_bytes_per_step": int(4 * 5026 + 8),
+           "path": "gbxcu_fit (whole log H2D)" if world == 1 else
+                   "fit_sharded: 1/N of the log H2D per rank + NCCL all-gather on the device"}
 
     # ---- roofline of the dominant kernel (train_epoch_kernel)
     peaks = measured_peaks()
@@ -731,30 +747,41 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
     # TrainConfig defaults (batch 32, 50 epochs), against the reference's run_training
     out["algorithm1"] = run_algorithm1(args, dev, gbx)
 
-    # C4: wide MLP (44-512-512-2) fit epoch on the tcgen05 TF32 path
+    # C4 (BASELINE configs[3]): wide MLP 44-512-512-2 on a synthetic 10M-tuple
+    # log (G1-shaped, generated on the device), one fit epoch on the tcgen05
+    # TF32 path, B = 8192 per GPU (C4's 8-GPU global batch is 65,536)
     H = 512
-    n_w = min(n, 262_144)
+    n_w = args.wide_records
+    g = torch.Generator(device="cuda").manual_seed(11)
+    fw = torch.rand((n_w, 44), generator=g, device="cuda", dtype=torch.float32) * 7.0
+    fw[:, :8] = 0.0
+    fw[torch.arange(n_w, device="cuda"), torch.randint(0, 8, (n_w,), generator=g, device="cuda")] = 1.0
+    pt = torch.rand(n_w, generator=g, device="cuda", dtype=torch.float64) * 0.96 + 0.02
+    tw = torch.stack([pt, 1.0 - pt], 1).contiguous()
+    del pt
     pw = torch.from_numpy(dev.wide_init(H, 7)).cuda()
-    tw = torch.empty((n_w, 2), dtype=torch.float64, device="cuda")
-    tw[:, 0] = 0.5
-    tw[:, 1] = 0.5
-    dev.wide_fit_dev(H, pw.data_ptr(), feat_d.data_ptr(), tw.data_ptr(), n_w, 0.01, 1, args.batch, 1,
+    torch.cuda.synchronize()
+    dev.wide_fit_dev(H, pw.data_ptr(), fw.data_ptr(), tw.data_ptr(), n_w, 0.01, 1, args.batch, 1,
                      stream=dev.stream)
     torch.cuda.synchronize()
     ev0.record(stream)
-    reps = 3
+    reps = 2
     for _ in range(reps):
-        dev.wide_fit_dev(H, pw.data_ptr(), feat_d.data_ptr(), tw.data_ptr(), n_w, 0.01, 1, args.batch,
-                         1, stream=dev.stream)
+        el_w = dev.wide_fit_dev(H, pw.data_ptr(), fw.data_ptr(), tw.data_ptr(), n_w, 0.01, 1,
+                                args.batch, 1, stream=dev.stream)
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / reps
     tf = n_w * 1_669_120 / (ms * 1e-3) / 1e12
     out["wide_mlp"] = {"value": n_w / (ms * 1e-3), "unit": "samples/s", "ms_per_epoch": ms,
                        "records": n_w, "hidden": H, "batch": args.batch, "dtype": "tf32",
-                       "tflops": tf, "flop_per_record": 1_669_120,
+                       "epoch_loss": float(el_w[0]), "tflops": tf, "flop_per_record": 1_669_120,
                        "tf32_peak_tflops": peaks.get("bf16_tflops", 1590.0) / 2,
+                       "roofline_frac": tf / (peaks.get("bf16_tflops", 1590.0) / 2),
+                       "data": "synthetic G1-shaped 10M-tuple log generated on the device",
                        "peak_note": "dense TF32 = half the measured bf16 cuBLAS peak"}
+    del fw, tw
+    torch.cuda.empty_cache()
 
     return out
 

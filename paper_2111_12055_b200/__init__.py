@@ -371,6 +371,48 @@ class Device:
                 raise
         return (p, el, -1) if not raise_on_diverge else (p, el)
 
+    def fit_sharded(self, params, feat_local, tgt_local, lr=0.01, epochs=1, batch=32, seed=0,
+                    group=None):
+        """Data-parallel fit with the log SHARDED over the ranks of a
+        torch.distributed group (one process per GPU): rank r passes records
+        [r * n_local, (r + 1) * n_local) of the global log (host arrays,
+        pinned for full PCIe rate). Each rank uploads only its shard; the
+        shards are all-gathered on the device (NCCL over NVLink), then every
+        rank trains its slice of each global batch (peer set or communicator
+        attached beforehand; `batch` is the GLOBAL batch). Returns
+        (params, epoch_loss) — identical on every rank."""
+        import torch
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        fl = np.ascontiguousarray(feat_local, np.float32).reshape(-1, N_FEATURES)
+        tl = np.ascontiguousarray(tgt_local, np.float64).reshape(-1, 2)
+        nl = fl.shape[0]
+        n = nl * world
+        buf = getattr(self, "_shard_bufs", None)
+        if buf is None or buf[0].shape[0] != n:
+            buf = (torch.empty((n, N_FEATURES), dtype=torch.float32, device="cuda"),
+                   torch.empty((n, 2), dtype=torch.float64, device="cuda"),
+                   torch.empty(N_PARAMS, dtype=torch.float32, device="cuda"))
+            self._shard_bufs = buf
+        fa, ta, pd = buf
+        lo, hi = rank * nl, (rank + 1) * nl
+        fa[lo:hi].copy_(torch.from_numpy(fl), non_blocking=True)
+        ta[lo:hi].copy_(torch.from_numpy(tl), non_blocking=True)
+        pd.copy_(torch.from_numpy(np.ascontiguousarray(params, np.float32)), non_blocking=True)
+        if world > 1 and dist.get_backend(group) == "nccl":
+            # in place: each rank's input is its own slice of the output
+            dist.all_gather_into_tensor(fa, fa[lo:hi], group=group)
+            dist.all_gather_into_tensor(ta, ta[lo:hi], group=group)
+        elif world > 1:  # gloo (CPU test mode): gather through host tensors
+            for dst, src in ((fa, fl), (ta, tl)):
+                parts = [torch.empty_like(torch.from_numpy(src)) for _ in range(world)]
+                dist.all_gather(parts, torch.from_numpy(src), group=group)
+                dst.copy_(torch.cat(parts).to("cuda"))
+        el = self.fit_dev(pd.data_ptr(), fa.data_ptr(), ta.data_ptr(), n, lr, epochs, batch, seed)
+        return pd.cpu().numpy(), el
+
     def fit_order(self, n: int, seed: int, epochs: int) -> np.ndarray:
         o = np.empty(n, np.uint32)
         self._ck(self.L.gbxcu_fit_order(self.h, n, seed, epochs, o))

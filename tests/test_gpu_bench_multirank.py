@@ -29,6 +29,7 @@ def test_bench_two_ranks_one_json_line():
          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
          "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--records", "20000",
          "--c5-apps", "100", "--c5-shaders-per-app", "200", "--qt-tuples", "20000",
+         "--wide-records", "65536",
          "--no-cpu-baseline"],
         cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
