@@ -701,7 +701,8 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
     # on the device; the default is the config's 1e8 shader feature vectors)
     s, feat = synthetic_suite_torch(torch, args.c5_apps, args.c5_shaders_per_app)
     ds = dev.suite_upload_dev(s, feat)
-    del s, feat
+    n_slots_c5 = int(s["pipe_slot_off"][-1])
+    del s
     torch.cuda.empty_cache()
     params = params_d.cpu().numpy()
     pd = torch.from_numpy(params).cuda()
@@ -718,9 +719,28 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / reps
+    # split: the greedy inference alone over the same features (K2), the rest is K3
+    ev0.record(stream)
+    for _ in range(reps):
+        dev.forward_dev(pd.data_ptr(), feat.data_ptr(), nsh, None, a_d.data_ptr(), gbx.FWD_FAST,
+                        dev.stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms_fwd = ev0.elapsed_time(ev1) / reps
+    del feat
+    ms_agg = max(ms - ms_fwd, 1e-6)
+    # K3 algorithmic bytes: per slot the shader index, fraction, latents (3 f64)
+    # and action (37 B), per app its 5-double row (the 8-B fraction re-read of
+    # each pipeline's A segment is not counted)
+    agg_bytes = 37.0 * n_slots_c5 + 40.0 * args.c5_apps
+    hbm_peak = measured_peaks().get("hbm_gbs", HBM_PEAK_FALLBACK)
     out["aggregation"] = {"value": nsh / (ms * 1e-3), "unit": "shader decisions/s (infer+agg)",
                           "ms": ms, "apps": args.c5_apps, "shaders": nsh,
                           "bytes_per_shader": 204, "hbm_gbs": nsh * 204 / (ms * 1e-3) / 1e9,
+                          "inference_ms": ms_fwd, "aggregate_ms": ms_agg,
+                          "aggregate_hbm_gbs": agg_bytes / (ms_agg * 1e-3) / 1e9,
+                          "aggregate_roofline_frac": agg_bytes / (ms_agg * 1e-3) / 1e9 / hbm_peak,
+                          "inference_fp32_tflops": nsh * 9856 / (ms_fwd * 1e-3) / 1e12,
                           "data": "synthetic suite generated on the device (C5: 1e8 shaders)"}
     ds.close()
     if not args.no_cpu_baseline:

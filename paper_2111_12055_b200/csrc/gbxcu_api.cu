@@ -250,12 +250,12 @@ int run_forward(gbxcu_ctx* c, const float* d_params, const float* d_feat, size_t
     return GBXCU_OK;
 }
 
-// aggregation: one warp per app, up to 8 CTAs of AGG_BLOCK per SM
+// aggregation: AGG_APPS apps per warp, one resident wave, grid-stride beyond it
 int launch_aggregate(gbxcu_ctx* c, const AggArgs& a, cudaStream_t st) {
-    const size_t per_cta = AGG_BLOCK / 32;
+    const size_t per_cta = (size_t)(AGG_BLOCK / 32) * AGG_APPS;
     const int grid = (int)std::max<size_t>(1, std::min<size_t>((a.n_apps + per_cta - 1) / per_cta,
-                                                               (size_t)c->num_sms * 8));
-    aggregate_kernel<<<grid, AGG_BLOCK, 0, st>>>(a);
+                                                               (size_t)c->num_sms * AGG_MINB));
+    aggregate_kernel<AGG_APPS, AGG_MINB><<<grid, AGG_BLOCK, 0, st>>>(a);
     return check_launch(c, "aggregate_kernel");
 }
 

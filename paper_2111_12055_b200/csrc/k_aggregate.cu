@@ -5,13 +5,9 @@
 // (proj/src/tuner.cpp:131-147, proj/src/core.cpp:125-133), and evaluate's
 // uplift and 1%-bin histogram (proj/src/tuner.cpp:282-313).
 //
-// One warp per application (segment). The reference's per-app sums are strict
-// left folds in pipeline -> slot order, so each warp loads 32 slots at a time
-// (coalesced slot arrays, gathered shader latents/actions), forms the 32
-// per-slot terms in parallel, and folds them in slot order with register
-// shuffles — the serial part is one DADD per slot, everything else (gathers,
-// products, divisions) is lane-parallel, and the loads run two chunks ahead
-// of the fold (see SlotRaw). Results are bit-identical to the reference.
+// A warp folds AGG_APPS applications at once (lane j = app j) over terms the
+// whole warp forms lane-parallel; see aggregate_kernel below. Results are
+// bit-identical to the reference.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -38,152 +34,217 @@ __device__ __forceinline__ double warp_fold(double acc, double term, int count, 
     return acc;
 }
 
-// Slot stream of a warp: 32 slots per chunk, loads software-pipelined two
-// chunks deep so the memory round trips overlap the (serial) fold of the
-// current chunk: at chunk c the slot arrays of chunk c+2 and the gathers of
-// chunk c+1 are in flight.
-struct SlotRaw {
-    uint32_t sh;
-    double frac;
+// ---------------------------------------------------------------- K3 kernel
+// K applications per warp. The reference's sums are strict left folds,
+// so an app's folds are serial; what a warp can share is the fold
+// *instruction*: lane j (< K) folds app j while the whole warp loads
+// and forms the per-slot terms of every app's next 32-slot chunk
+// lane-parallel (coalesced slot arrays, gathered shader latents / actions)
+// and stages them in shared memory. One fold instruction thus advances
+// K apps by one slot; the warp-per-app form spent one DADD and one
+// SHFL per slot and pass on a single app and was issue-bound (ncu: 58% issue
+// active, MIO throttle the top stall).
+//
+// One streaming read per pipeline: run_benchmark's bandwidth load (pass 1,
+// over all the app's slots) and each pipeline's inner sum (pass 2: 1 - sum p,
+// then + sum p / s_eff) are folded in the reference's order, with the pass-2
+// terms formed under the speculation that the app is not throttled
+// (throttle == 1, so s_eff is the wave64 speedup exactly). Per pipeline that
+// is an "A" segment (its fractions: inner -= p) then a "B" segment (load +=
+// p * demand, inner += p / s_eff): 45 B read per slot instead of the 82 B of
+// three separate passes (the A read is mostly an L2 hit for B). An app whose
+// final load exceeds its cap (throttle != 1) runs pass 2 again with the true
+// throttle ("redo" segments, which leave the load unchanged). Bit-identical to
+// the reference either way.
+struct AggLane {  // lanes < K: app `lane`'s fold cursor
+    uint64_t pos, end;  // slots still to fold in the current segment
+    uint64_t p, p_lo, p_hi;
+    double load, inner, total, throttle, cap;
+    int seg;   // 0 = A (fractions), 1 = B (terms), 2 = done
+    int redo;  // pass 2 again with the app's true throttle
 };
 
-__device__ __forceinline__ SlotRaw slot_raw(const AggArgs& a, uint64_t s, uint64_t s_hi) {
-    SlotRaw r{0xFFFFFFFFu, 0.0};
-    if (s < s_hi) {
-        r.sh = a.slot_shader[s];
-        r.frac = a.slot_frac[s];
-    }
-    return r;
+__device__ __forceinline__ void agg_start_pipeline(const AggArgs& a, AggLane& L) {
+    L.seg = 0;
+    L.inner = 1.0;
+    L.pos = a.pipe_slot_off[L.p];
+    L.end = a.pipe_slot_off[L.p + 1];
 }
 
-// pass-1 term of a slot: p * demand(a)
-struct Term1In {
-    double frac, bw;
-    uint8_t act;
-    bool ok;
-};
-__device__ __forceinline__ Term1In term1_gather(const AggArgs& a, const SlotRaw& r) {
-    Term1In t{r.frac, 0.0, 0, r.sh != 0xFFFFFFFFu};
-    if (t.ok) {
-        t.bw = a.shader_lat[3 * (size_t)r.sh + 1];
-        t.act = a.shader_action[r.sh];
+// past the end of the current segment: on to the next non-empty one (or done)
+__device__ void agg_advance(const AggArgs& a, AggLane& L) {
+    while (L.seg != 2 && L.pos >= L.end) {
+        if (L.seg == 0) {  // A -> B over the same pipeline
+            L.seg = 1;
+            L.pos = a.pipe_slot_off[L.p];
+            L.end = a.pipe_slot_off[L.p + 1];
+            continue;
+        }
+        // B done: the pipeline's weighted inner sum (frame_time, simenv.cpp:439-474)
+        const double wt = __dmul_rn(a.pipe_wt[2 * L.p], a.pipe_wt[2 * L.p + 1]);
+        L.total = __dadd_rn(L.total, __dmul_rn(wt, L.inner));
+        if (++L.p < L.p_hi) {
+            agg_start_pipeline(a, L);
+            continue;
+        }
+        if (!L.redo) {  // end of the app's load: its throttle
+            double thr = 1.0;
+            if (isfinite(L.cap) && L.load > L.cap) thr = __ddiv_rn(L.cap, L.load);
+            L.throttle = thr;
+            if (thr != 1.0) {
+                L.redo = 1;
+                L.total = 0.0;
+                L.p = L.p_lo;
+                agg_start_pipeline(a, L);
+                continue;
+            }
+        }
+        L.seg = 2;
     }
-    return t;
-}
-__device__ __forceinline__ double term1(const Term1In& t) {
-    if (!t.ok) return 0.0;
-    const double demand = t.act == 1 ? __dmul_rn(2.0, t.bw) : t.bw;
-    return __dmul_rn(t.frac, demand);
 }
 
-// pass-2 term of a slot: p / s_eff
-struct Term2In {
-    double frac, d, bw, kap;
-    uint8_t act;
-    bool ok;
-};
-__device__ __forceinline__ Term2In term2_gather(const AggArgs& a, const SlotRaw& r) {
-    Term2In t{r.frac, 0.0, 0.0, 0.0, 0, r.sh != 0xFFFFFFFFu};
-    if (t.ok) {
-        const double* lat = a.shader_lat + 3 * (size_t)r.sh;
-        t.d = lat[0];
-        t.bw = lat[1];
-        t.kap = lat[2];
-        t.act = a.shader_action[r.sh];
-    }
-    return t;
-}
-__device__ __forceinline__ double term2(const Term2In& t, double thr, double throttle) {
-    if (!t.ok) return 0.0;
-    // wave64_speedup = (1 + kappa)(1 - 0.5 d)  (simenv.hpp:65-67)
-    double sp = t.act == 1 ? __dmul_rn(__dadd_rn(1.0, t.kap), __dsub_rn(1.0, __dmul_rn(0.5, t.d))) : 1.0;
-    if (t.bw > thr) sp = __dmul_rn(sp, throttle);
-    return __ddiv_rn(t.frac, sp);
-}
-
-__global__ void __launch_bounds__(AGG_BLOCK) aggregate_kernel(AggArgs a) {
-    const int lane = threadIdx.x & 31;
+template <int K, int MINB>
+__global__ void __launch_bounds__(AGG_BLOCK, MINB) aggregate_kernel(AggArgs a) {
+    __shared__ double2 buf[AGG_BLOCK / 32][K][33];  // staged (load term, inner term)
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const size_t warps = (size_t)gridDim.x * (AGG_BLOCK / 32);
-    for (size_t app = (size_t)blockIdx.x * (AGG_BLOCK / 32) + (threadIdx.x >> 5); app < a.n_apps;
-         app += warps) {
-        const double baseline = a.app_f64[4 * app], cap = a.app_f64[4 * app + 1];
-        const double sigma = a.app_f64[4 * app + 2], thr = a.app_f64[4 * app + 3];
-        const uint64_t p_lo = a.app_pipe_off[app], p_hi = a.app_pipe_off[app + 1];
-
-        // pass 1: bandwidth load = sum over all slots of p * demand(a) — the
-        // app's slots are contiguous (pipelines in order), one stream
-        double load = 0.0;
-        {
-            const uint64_t s_lo = a.pipe_slot_off[p_lo], s_hi = a.pipe_slot_off[p_hi];
-            SlotRaw raw2 = slot_raw(a, s_lo + 32 + lane, s_hi);
-            Term1In in1 = term1_gather(a, slot_raw(a, s_lo + lane, s_hi));
-            for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
-                const double term = term1(in1);
-                in1 = term1_gather(a, raw2);               // chunk c+1's gathers
-                raw2 = slot_raw(a, s0 + 64 + lane, s_hi);  // chunk c+2's slot arrays
-                load = warp_fold(load, term, (int)min((uint64_t)32, s_hi - s0), false);
+    const size_t n_groups = (a.n_apps + K - 1) / K;
+    for (size_t grp = (size_t)blockIdx.x * (AGG_BLOCK / 32) + wib; grp < n_groups; grp += warps) {
+        const size_t app0 = grp * K;
+        AggLane L{};
+        L.seg = 2;
+        L.throttle = 1.0;
+        double thr_me = 0.0;
+        if (lane < K && app0 + lane < a.n_apps) {
+            const size_t app = app0 + lane;
+            L.cap = a.app_f64[4 * app + 1];
+            thr_me = a.app_f64[4 * app + 3];
+            L.p_lo = L.p = a.app_pipe_off[app];
+            L.p_hi = a.app_pipe_off[app + 1];
+            if (L.p < L.p_hi) {
+                agg_start_pipeline(a, L);
+                agg_advance(a, L);  // (empty leading segments)
             }
         }
-        double throttle = 1.0;
-        if (isfinite(cap) && load > cap) throttle = __ddiv_rn(cap, load);
-
-        // pass 2: per pipeline inner = 1 - sum p + sum p / s_eff
-        double total = 0.0;
-        for (uint64_t p = p_lo; p < p_hi; ++p) {
-            const uint64_t s_lo = a.pipe_slot_off[p], s_hi = a.pipe_slot_off[p + 1];
-            double inner = 1.0;
-            {
-                double fnext = s_lo + lane < s_hi ? a.slot_frac[s_lo + lane] : 0.0;
-                for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
-                    const double term = fnext;
-                    fnext = s0 + 32 + lane < s_hi ? a.slot_frac[s0 + 32 + lane] : 0.0;
-                    inner = warp_fold(inner, term, (int)min((uint64_t)32, s_hi - s0), true);
+        for (;;) {
+            // this round's chunk of every app: (segment | redo | count), start, threshold, throttle
+            const int cnt_me = L.seg == 2 ? 0 : (int)min((uint64_t)32, L.end - L.pos);
+            const int info_me = cnt_me | (L.seg << 8) | (L.redo << 10);
+            int info[K];
+            uint64_t pos[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                info[j] = __shfl_sync(0xffffffffu, info_me, j);
+                pos[j] = __shfl_sync(0xffffffffu, L.pos, j);
+            }
+            bool any = false;
+#pragma unroll
+            for (int j = 0; j < K; ++j) any |= (info[j] & 0xFF) != 0;
+            if (!any) break;
+            // loads: slot arrays of every app's chunk, then the shader gathers
+            double fr[K];
+            uint32_t sh[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const bool ok = lane < (info[j] & 0xFF);
+                fr[j] = ok ? a.slot_frac[pos[j] + lane] : 0.0;
+                sh[j] = ok && (info[j] >> 8 & 3) == 1 ? a.slot_shader[pos[j] + lane] : 0xFFFFFFFFu;
+            }
+            double ld[K], lb[K], lk[K];
+            uint8_t ac[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                ld[j] = lb[j] = lk[j] = 0.0;
+                ac[j] = 0;
+                if (sh[j] != 0xFFFFFFFFu) {
+                    const double* lat = a.shader_lat + 3 * (size_t)sh[j];
+                    ld[j] = lat[0];
+                    lb[j] = lat[1];
+                    lk[j] = lat[2];
+                    ac[j] = a.shader_action[sh[j]];
                 }
             }
-            {
-                SlotRaw raw2 = slot_raw(a, s_lo + 32 + lane, s_hi);
-                Term2In in2 = term2_gather(a, slot_raw(a, s_lo + lane, s_hi));
-                for (uint64_t s0 = s_lo; s0 < s_hi; s0 += 32) {
-                    const double term = term2(in2, thr, throttle);
-                    in2 = term2_gather(a, raw2);
-                    raw2 = slot_raw(a, s0 + 64 + lane, s_hi);
-                    inner = warp_fold(inner, term, (int)min((uint64_t)32, s_hi - s0), false);
+            // terms
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const double thr = __shfl_sync(0xffffffffu, thr_me, j);
+                const double throttle = __shfl_sync(0xffffffffu, L.throttle, j);
+                double x = 0.0, y = 0.0;
+                if (lane < (info[j] & 0xFF)) {
+                    if ((info[j] >> 8 & 3) == 0) {
+                        y = -fr[j];  // inner - p == inner + (-p) exactly
+                    } else {
+                        // pass 1: p * demand(a) (simenv.cpp:481-510)
+                        if (!(info[j] >> 10 & 1))
+                            x = __dmul_rn(fr[j], ac[j] == 1 ? __dmul_rn(2.0, lb[j]) : lb[j]);
+                        // pass 2: p / s_eff, wave64_speedup = (1 + kappa)(1 - 0.5 d)
+                        double sp = ac[j] == 1 ? __dmul_rn(__dadd_rn(1.0, lk[j]),
+                                                           __dsub_rn(1.0, __dmul_rn(0.5, ld[j])))
+                                               : 1.0;
+                        if (lb[j] > thr) sp = __dmul_rn(sp, throttle);
+                        y = __ddiv_rn(fr[j], sp);
+                    }
                 }
+                buf[wib][j][lane] = make_double2(x, y);
             }
-            const double wt = __dmul_rn(a.pipe_wt[2 * p], a.pipe_wt[2 * p + 1]);
-            total = __dadd_rn(total, __dmul_rn(wt, inner));
+            __syncwarp();
+            // folds: lane j folds app j's chunk in slot order
+            if (lane < K) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    if (k < cnt_me) {
+                        const double2 t = buf[wib][lane][k];
+                        L.load = __dadd_rn(L.load, t.x);
+                        L.inner = __dadd_rn(L.inner, t.y);
+                    }
+                }
+                L.pos += cnt_me;
+                agg_advance(a, L);
+            }
+            __syncwarp();
         }
-        const double fps = __ddiv_rn(1.0, total);
 
-        // noisy samples: SplitMix64(derive_seed({run_seed, 0x4E5A45, app}))
-        const uint64_t gapp = a.app_base + app;  // global app index (shards)
-        const uint64_t run_seed =
-            a.run_seed ? a.run_seed[app] : derive_seed3(a.eval_seed, 0x45564Cu, gapp);
-        const uint64_t ns = derive_seed3(run_seed, 0x4E5A45u, gapp);
-        const double half = __dmul_rn(sigma, sqrt(3.0));
-        double sum = 0.0;
-        for (int k0 = 0; k0 < a.n_samples; k0 += 32) {
-            const int k = k0 + lane;
-            double smp = 0.0;
-            if (k < a.n_samples) {
-                const double su = signed_unit_of(sm_draw(ns, (uint64_t)k + 1));
-                smp = __dmul_rn(fps, __dadd_rn(1.0, __dmul_rn(su, half)));
-                if (a.samples) a.samples[app * (size_t)a.n_samples + k] = smp;
+        // per app: noisy samples SplitMix64(derive_seed({run_seed, 0x4E5A45, app})),
+        // tuned fps, uplift and reward ratio (tuner.cpp:276-291, core.cpp:125-133)
+        for (int j = 0; j < K && app0 + j < a.n_apps; ++j) {
+            const size_t app = app0 + j;
+            const double total = __shfl_sync(0xffffffffu, L.total, j);
+            const double fps = __ddiv_rn(1.0, total);
+            const double baseline = a.app_f64[4 * app], sigma = a.app_f64[4 * app + 2];
+            const uint64_t gapp = a.app_base + app;  // global app index (shards)
+            const uint64_t run_seed =
+                a.run_seed ? a.run_seed[app] : derive_seed3(a.eval_seed, 0x45564Cu, gapp);
+            const uint64_t ns = derive_seed3(run_seed, 0x4E5A45u, gapp);
+            const double half = __dmul_rn(sigma, sqrt(3.0));
+            double sum = 0.0;
+            for (int k0 = 0; k0 < a.n_samples; k0 += 32) {
+                const int k = k0 + lane;
+                double smp = 0.0;
+                if (k < a.n_samples) {
+                    const double su = signed_unit_of(sm_draw(ns, (uint64_t)k + 1));
+                    smp = __dmul_rn(fps, __dadd_rn(1.0, __dmul_rn(su, half)));
+                    if (a.samples) a.samples[app * (size_t)a.n_samples + k] = smp;
+                }
+                sum = warp_fold(sum, smp, min(32, a.n_samples - k0), false);
             }
-            sum = warp_fold(sum, smp, min(32, a.n_samples - k0), false);
-        }
-        if (lane == 0) {
-            const double tuned = __ddiv_rn(sum, (double)a.n_samples);
-            const double ratio = __ddiv_rn(tuned, baseline);
-            double* row = a.rows + 5 * app;
-            row[0] = total;
-            row[1] = fps;
-            row[2] = tuned;
-            row[3] = __dmul_rn(100.0, __dsub_rn(ratio, 1.0));
-            row[4] = ratio;
+            if (lane == 0) {
+                const double tuned = __ddiv_rn(sum, (double)a.n_samples);
+                const double ratio = __ddiv_rn(tuned, baseline);
+                double* row = a.rows + 5 * app;
+                row[0] = total;
+                row[1] = fps;
+                row[2] = tuned;
+                row[3] = __dmul_rn(100.0, __dsub_rn(ratio, 1.0));
+                row[4] = ratio;
+            }
         }
     }
 }
+
+// AGG_APPS apps per warp, 3 CTAs per SM (register cap 80): measured at C5
+// (1e8 slots, 1e4 apps) against 1/2/8 apps per warp and 2-4 CTAs per SM
+// (profiles/r02/k3_variants.md)
+template __global__ void aggregate_kernel<AGG_APPS, AGG_MINB>(AggArgs);
 
 // evaluate's histogram (proj/src/tuner.cpp:293-313), one CTA.
 __global__ void __launch_bounds__(1024)

@@ -12,7 +12,9 @@ constexpr int EXACT_BLOCK = 128;  // exact fp64 inference
 constexpr int RECHECK_BLOCK = 256;  // warp-per-state exact re-check
 constexpr int TRAIN_BLOCK = 512;  // train: 16 warps; tiles of 32 or 64 records
 constexpr int SHUF_BLOCK = 256;
-constexpr int AGG_BLOCK = 256;    // aggregation: 8 warps = 8 apps per CTA
+constexpr int AGG_BLOCK = 256;    // aggregation: 8 warps per CTA
+constexpr int AGG_APPS = 4;       // aggregation: apps folded together by one warp (lane j = app j)
+constexpr int AGG_MINB = 3;       // aggregation: resident CTAs per SM the register budget targets
 
 constexpr int PSTR = 5028;        // per-CTA partial row: 5,026 gradient entries, loss, pad
 constexpr int MAX_PEERS = 8;      // ranks of one NVLink domain (one node)
@@ -224,6 +226,7 @@ cudaError_t qt_fold(const QtFoldIO& io, size_t nseg, size_t nkeys, uint32_t* key
 cudaError_t qt_exclusive_scan(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out,
                               size_t n, cudaStream_t st);
 
+template <int K, int MINB>
 __global__ void aggregate_kernel(AggArgs a);
 __global__ void histogram_kernel(const double* rows, int stride, size_t n, double* lower,
                                  unsigned long long* count, size_t cap,

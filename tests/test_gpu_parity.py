@@ -353,6 +353,51 @@ def test_aggregate_and_evaluate_match_golden(dev, orc, name):
     ds.close()
 
 
+def _ragged_suite(seed, n_apps):
+    """Random CSR suite with the shapes the reference never guarantees away:
+    apps without pipelines, pipelines without slots, long and 1-slot
+    pipelines, shared shaders, and caps that throttle about half the apps."""
+    rng = np.random.default_rng(seed)
+    pipes = rng.integers(1, 5, n_apps)
+    pipes[rng.random(n_apps) < 0.05] = 0
+    npipe = int(pipes.sum())
+    sizes = rng.integers(0, 120, npipe)
+    sizes[rng.random(npipe) < 0.1] = 0
+    sizes[rng.random(npipe) < 0.05] = 1
+    sizes[rng.random(npipe) < 0.05] = 700
+    n_slots = int(sizes.sum())
+    n_sh = max(1, n_slots // 2)
+    lat = rng.random((n_sh, 3))
+    lat[:, 1] *= 1.6
+    lat[:, 2] *= 0.6
+    frac = rng.random(n_slots) * 0.06 + 0.01
+    app_f64 = np.stack([rng.random(n_apps) + 0.5,                         # baseline fps
+                        np.where(rng.random(n_apps) < 0.6, rng.random(n_apps) * 8.0, np.inf),  # cap
+                        rng.random(n_apps) * 0.01,                       # sigma
+                        rng.random(n_apps) * 1.2], 1)                    # throttle threshold
+    return dict(app_pipe_off=np.concatenate([[0], np.cumsum(pipes)]).astype(np.uint64),
+                pipe_slot_off=np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint64),
+                slot_shader=rng.integers(0, n_sh, n_slots).astype(np.uint32),
+                slot_frac=frac,
+                pipe_wt=np.stack([rng.random(npipe) * 1.5 + 0.5, (rng.random(npipe) * 6 + 2) * 1e-3], 1),
+                shader_lat=lat, app_f64=app_f64), rng.integers(0, 2, n_sh).astype(np.uint8)
+
+
+@pytest.mark.parametrize("seed,n_apps", [(1, 1), (2, 3), (3, 97), (4, 1030)])
+def test_aggregate_ragged_suites_match_oracle(dev, orc, seed, n_apps):
+    """K3 (several apps folded per warp, speculative single pass per pipeline,
+    re-run for throttled apps) against the oracle's frame_time / run_benchmark
+    / evaluate rows (simenv.cpp:439-510, tuner.cpp:276-291), bit for bit."""
+    s, act = _ragged_suite(seed, n_apps)
+    run_seed = np.array([orc.derive_seed(seed, 0x45564C, b) for b in range(n_apps)], np.uint64)
+    rows_o, smp_o = orc.aggregate(s, act, run_seed, 10, want_samples=True)
+    rows, smp = dev.aggregate(s, act, run_seed, 10, want_samples=True)
+    throttled = np.isfinite(s["app_f64"][:, 1])
+    assert n_apps < 50 or throttled.any()
+    np.testing.assert_array_equal(rows, rows_o)
+    np.testing.assert_array_equal(smp, smp_o)
+
+
 @pytest.mark.parametrize("uplift", [[3.0], [-2.5, -2.5], [0.0, 1.0, 2.0], [-7.3, 0.2, 12.9, 12.0]])
 def test_histogram_edges(dev, orc, uplift):
     lo, cnt = dev.histogram(uplift)
