@@ -768,8 +768,9 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
     out["algorithm1"] = run_algorithm1(args, dev, gbx)
 
     # C4 (BASELINE configs[3]): wide MLP 44-512-512-2 on a synthetic 10M-tuple
-    # log (G1-shaped, generated on the device), one fit epoch on the tcgen05
-    # TF32 path, B = 8192 per GPU (C4's 8-GPU global batch is 65,536)
+    # log (G1-shaped, generated on the device), one fit epoch per precision on
+    # tcgen05 (kind::f16 BF16, the default, and kind::tf32), B = 8192 per GPU
+    # (C4's 8-GPU global batch is 65,536)
     H = 512
     n_w = args.wide_records
     g = torch.Generator(device="cuda").manual_seed(11)
@@ -779,27 +780,32 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
     pt = torch.rand(n_w, generator=g, device="cuda", dtype=torch.float64) * 0.96 + 0.02
     tw = torch.stack([pt, 1.0 - pt], 1).contiguous()
     del pt
-    pw = torch.from_numpy(dev.wide_init(H, 7)).cuda()
-    torch.cuda.synchronize()
-    dev.wide_fit_dev(H, pw.data_ptr(), fw.data_ptr(), tw.data_ptr(), n_w, 0.01, 1, args.batch, 1,
-                     stream=dev.stream)
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    reps = 2
-    for _ in range(reps):
-        el_w = dev.wide_fit_dev(H, pw.data_ptr(), fw.data_ptr(), tw.data_ptr(), n_w, 0.01, 1,
-                                args.batch, 1, stream=dev.stream)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / reps
-    tf = n_w * 1_669_120 / (ms * 1e-3) / 1e12
-    out["wide_mlp"] = {"value": n_w / (ms * 1e-3), "unit": "samples/s", "ms_per_epoch": ms,
-                       "records": n_w, "hidden": H, "batch": args.batch, "dtype": "tf32",
-                       "epoch_loss": float(el_w[0]), "tflops": tf, "flop_per_record": 1_669_120,
-                       "tf32_peak_tflops": peaks.get("bf16_tflops", 1590.0) / 2,
-                       "roofline_frac": tf / (peaks.get("bf16_tflops", 1590.0) / 2),
-                       "data": "synthetic G1-shaped 10M-tuple log generated on the device",
-                       "peak_note": "dense TF32 = half the measured bf16 cuBLAS peak"}
+    bf16_peak = peaks.get("bf16_tflops", 1590.0)
+    wide = {}
+    for prec, peak in (("bf16", bf16_peak), ("tf32", bf16_peak / 2)):
+        pw = torch.from_numpy(dev.wide_init(H, 7)).cuda()
+        torch.cuda.synchronize()
+        dev.wide_fit_dev(H, pw.data_ptr(), fw.data_ptr(), tw.data_ptr(), n_w, 0.01, 1, args.batch, 1,
+                         stream=dev.stream, precision=prec)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        reps = 2
+        for _ in range(reps):
+            el_w = dev.wide_fit_dev(H, pw.data_ptr(), fw.data_ptr(), tw.data_ptr(), n_w, 0.01, 1,
+                                    args.batch, 1, stream=dev.stream, precision=prec)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / reps
+        tf = n_w * 1_669_120 / (ms * 1e-3) / 1e12
+        wide[prec] = {"value": n_w / (ms * 1e-3), "unit": "samples/s", "ms_per_epoch": ms,
+                      "us_per_step": ms * 1e3 / ((n_w + args.batch - 1) // args.batch),
+                      "epoch_loss": float(el_w[0]), "tflops": tf, "peak_tflops": peak,
+                      "roofline_frac": tf / peak}
+    out["wide_mlp"] = dict(wide["bf16"], records=n_w, hidden=H, batch=args.batch, dtype="bf16",
+                           flop_per_record=1_669_120, tf32=wide["tf32"],
+                           data="synthetic G1-shaped 10M-tuple log generated on the device",
+                           peak_note="dense BF16 = the measured bf16 cuBLAS peak "
+                                     "(MEASURED_PEAKS.json); TF32 = half of it")
     del fw, tw
     torch.cuda.empty_cache()
 

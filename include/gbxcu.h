@@ -326,9 +326,24 @@ int gbxcu_wide_fit(gbxcu_ctx* ctx, int hidden, float* params_inout, const float*
 int gbxcu_wide_fit_dev(gbxcu_ctx* ctx, int hidden, float* d_params, const float* d_feat,
                        const double* d_tgt, size_t n, const gbxcu_train_cfg* cfg,
                        double* epoch_loss_out, int* diverged_epoch, void* stream);
+/* Precision of the wide path: TF32 operands (kind::tf32, fp32 activations)
+ * or BF16 operands (kind::f16; bf16 activations between the GEMMs, the
+ * softmax/KL head fused into the layer-2 GEMM epilogue, fp32 master weights;
+ * hidden a multiple of 64 up to 512). gbxcu_wide_fit[_dev] = TF32. */
+#define GBXCU_WIDE_TF32 0
+#define GBXCU_WIDE_BF16 1
+int gbxcu_wide_fit_ex(gbxcu_ctx* ctx, int hidden, int precision, float* params_inout, const float* feat,
+                      const double* tgt, size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out,
+                      int* diverged_epoch);
+int gbxcu_wide_fit_ex_dev(gbxcu_ctx* ctx, int hidden, int precision, float* d_params, const float* d_feat,
+                          const double* d_tgt, size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out,
+                          int* diverged_epoch, void* stream);
 /* D[M][N] = A[M][K] . B[N][K]^T through the same tcgen05 TF32 GEMM kernel
  * (host buffers; K multiple of 4) — exposed for testing. */
 int gbxcu_tf32_gemm(gbxcu_ctx* ctx, int M, int N, int K, const float* A, const float* B, float* D);
+/* D[M][N] = bf16(A)[M][K] . bf16(B)[N][K]^T (round-to-nearest-even operands,
+ * fp32 accumulation) through the wide path's kind::f16 kernel — for testing. */
+int gbxcu_bf16_gemm(gbxcu_ctx* ctx, int M, int N, int K, const float* A, const float* B, float* D);
 
 #ifdef __cplusplus
 }

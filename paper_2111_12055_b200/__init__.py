@@ -98,6 +98,8 @@ class SuiteC(C.Structure):
                 ("slot_frac", _vp), ("pipe_wt", _vp), ("shader_lat", _vp), ("app_f64", _vp)]
 
 
+WIDE_PRECISION = {"tf32": 0, "bf16": 1}  # GBXCU_WIDE_TF32 / GBXCU_WIDE_BF16
+
 # Every symbol include/gbxcu.h declares (tests check the library exports them).
 EXPORTS = (
     "gbxcu_abi_version", "gbxcu_last_error", "gbxcu_create", "gbxcu_destroy", "gbxcu_stream",
@@ -107,7 +109,8 @@ EXPORTS = (
     "gbxcu_comm_destroy", "gbxcu_aggregate", "gbxcu_histogram", "gbxcu_suite_upload",
     "gbxcu_suite_free", "gbxcu_suite_features", "gbxcu_evaluate", "gbxcu_evaluate_dev",
     "gbxcu_wide_param_count", "gbxcu_wide_init", "gbxcu_wide_forward", "gbxcu_wide_fit",
-    "gbxcu_wide_fit_dev", "gbxcu_tf32_gemm", "gbxcu_last_fit_timing", "gbxcu_last_recheck_count", "gbxcu_peer_export",
+    "gbxcu_wide_fit_dev", "gbxcu_wide_fit_ex", "gbxcu_wide_fit_ex_dev", "gbxcu_tf32_gemm",
+    "gbxcu_bf16_gemm", "gbxcu_last_fit_timing", "gbxcu_last_recheck_count", "gbxcu_peer_export",
     "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free", "gbxcu_qtable_clear",
     "gbxcu_qtable_update_batch", "gbxcu_qtable_update_batch_dev", "gbxcu_qtable_size",
     "gbxcu_forward_batch", "gbxcu_sample_batch", "gbxcu_evaluate_shard",
@@ -190,6 +193,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_wide_fit_dev.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _sz, C.POINTER(TrainCfg), _vp,
                                      C.POINTER(C.c_int), _vp]
     L.gbxcu_tf32_gemm.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _f32p, _f32p, _f32p]
+    L.gbxcu_bf16_gemm.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _f32p, _f32p, _f32p]
+    L.gbxcu_wide_fit_ex.argtypes = [_vp, C.c_int, C.c_int, _f32p, _f32p, _f64p, _sz, C.POINTER(TrainCfg), _vp,
+                                    C.POINTER(C.c_int)]
+    L.gbxcu_wide_fit_ex_dev.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _sz, C.POINTER(TrainCfg), _vp,
+                                        C.POINTER(C.c_int), _vp]
     L.gbxcu_last_fit_timing.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.gbxcu_last_recheck_count.argtypes = [_vp, C.POINTER(C.c_uint64)]
     _LIB = L
@@ -453,25 +461,27 @@ class Device:
         self._ck(self.L.gbxcu_wide_forward(self.h, hidden, _f32(params), feat, feat.shape[0], probs))
         return probs
 
-    def wide_fit(self, hidden: int, params, feat, tgt, lr=0.01, epochs=1, batch=32, seed=0):
+    def wide_fit(self, hidden: int, params, feat, tgt, lr=0.01, epochs=1, batch=32, seed=0,
+                 precision="tf32"):
         p = np.array(params, np.float32, copy=True)
         feat = _f32(feat).reshape(-1, N_FEATURES)
         el = np.full(max(epochs, 1), np.nan, np.float64)
         de = C.c_int(-1)
         cfg = TrainCfg(lr, epochs, batch, seed, 0, 0)
-        rc = self.L.gbxcu_wide_fit(self.h, hidden, p, feat, _f64(tgt), feat.shape[0], C.byref(cfg),
-                                   el.ctypes.data, C.byref(de))
+        rc = self.L.gbxcu_wide_fit_ex(self.h, hidden, WIDE_PRECISION[precision], p, feat, _f64(tgt),
+                                      feat.shape[0], C.byref(cfg), el.ctypes.data, C.byref(de))
         self._ck(rc, de.value)
         return p, el
 
     def wide_fit_dev(self, hidden, d_params, d_feat, d_tgt, n, lr=0.01, epochs=1, batch=32, seed=0,
-                     stream=None):
+                     stream=None, precision="tf32"):
         el = np.full(max(epochs, 1), np.nan, np.float64)
         de = C.c_int(-1)
         cfg = TrainCfg(lr, epochs, batch, seed, 0, 0)
         _after_torch(stream)
-        self._ck(self.L.gbxcu_wide_fit_dev(self.h, hidden, d_params, d_feat, d_tgt, n, C.byref(cfg),
-                                           el.ctypes.data, C.byref(de), stream), de.value)
+        self._ck(self.L.gbxcu_wide_fit_ex_dev(self.h, hidden, WIDE_PRECISION[precision], d_params, d_feat,
+                                              d_tgt, n, C.byref(cfg), el.ctypes.data, C.byref(de), stream),
+                 de.value)
         return el
 
     def tf32_gemm(self, A, B) -> np.ndarray:
@@ -480,6 +490,14 @@ class Device:
         N = B.shape[0]
         D = np.empty((M, N), np.float32)
         self._ck(self.L.gbxcu_tf32_gemm(self.h, M, N, K, A, B, D))
+        return D
+
+    def bf16_gemm(self, A, B) -> np.ndarray:
+        A, B = _f32(A), _f32(B)
+        M, K = A.shape
+        N = B.shape[0]
+        D = np.empty((M, N), np.float32)
+        self._ck(self.L.gbxcu_bf16_gemm(self.h, M, N, K, A, B, D))
         return D
 
     # ----------------------------------------------------------- data parallel

@@ -129,6 +129,8 @@ struct gbxcu_ctx {
     // wide MLP (C4) working set
     DevBuf w_params, w_grad, w_w1t, w_h1, w_h1t, w_h2, w_d2, w_d2t, w_d1t, w_xt, w_d3, w_kl;
     DevBuf w_part, w_g4, w_g5, w_loss, w_feat, w_tgt, w_probs, w_xg, w_w0p, w_epoch;
+    // BF16 path (k_wide16.cu): bf16 activations / operand copies, partials
+    DevBuf b_xg, b_xt, b_h1, b_h1t, b_d2, b_d2t, b_d1t, b_w0p, b_w1, b_w1t, b_p4, b_p5, b_hp;
     // CUDA graphs of a wide-MLP epoch's step sequence (one per epoch-permutation
     // buffer), keyed on every pointer and size they bake in
     struct WideGraph {
@@ -197,6 +199,11 @@ int setup_kernel_attrs() {
         set((const void*)tc_gemm_kernel, gemm_smem_bytes());
         set((const void*)wide_head_kernel, sizeof(float) * 32 * (1024 + 1));
         set((const void*)tma_gemm_kernel<64>, tma_gemm_smem_bytes<64>());
+        set((const void*)w16_gemm_kernel<256, 4, W16_EPI_H1>, w16_gemm_smem_bytes<256, 4>());
+        set((const void*)w16_gemm_kernel<512, 2, W16_EPI_HEAD>, w16_gemm_smem_bytes<512, 2>());
+        set((const void*)w16_gemm_kernel<256, 4, W16_EPI_D1T>, w16_gemm_smem_bytes<256, 4>());
+        set((const void*)w16_gemm_kernel<256, 4, W16_EPI_PART>, w16_gemm_smem_bytes<256, 4>());
+        set((const void*)w16_gemm_kernel<64, 6, W16_EPI_PART>, w16_gemm_smem_bytes<64, 6>());
         set((const void*)tma_gemm_kernel<128>, tma_gemm_smem_bytes<128>());
         set((const void*)tma_gemm_kernel<256>, tma_gemm_smem_bytes<256>());
     });
@@ -1858,6 +1865,247 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
     return check_launch(c, "wide_update_kernel");
 }
 
+// ------------------------------------------------ BF16 path (k_wide16.cu)
+// Launch with programmatic dependent launch: the kernel may start while its
+// predecessor in the stream finishes (its griddepcontrol.wait orders the
+// data); kept through stream capture as a programmatic graph edge.
+template <typename... K, typename... A>
+int launch_pdl(gbxcu_ctx* c, const char* name, void (*kern)(K...), dim3 grid, dim3 block, size_t smem,
+               cudaStream_t st, A... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, args...));
+    return check_launch(c, name);
+}
+
+// K-major bf16 operand [rows][ld] (K valid columns) as TMA boxes of
+// {64 bf16 = 128 B, box_rows} with the 128-byte swizzle; zero fill past K / rows.
+bool make_bf16_map(CUtensorMap* m, const void* base, int K, int rows, int ld, int box_rows) {
+    const EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// D = A B^T on the bf16 kernel: A [M][lda] (K valid), B [N][ldb]; grid (N/BN, M/128, splits)
+template <int BN, int ST, int EPI>
+int launch_w16(gbxcu_ctx* c, const void* A, int lda, const void* B, int ldb, const W16Args& g, int splits,
+               cudaStream_t st) {
+    CUtensorMap ma, mb;
+    if (!make_bf16_map(&ma, A, g.K, g.M, lda, 128) || !make_bf16_map(&mb, B, g.K, g.N, ldb, BN > 256 ? 256 : BN))
+        return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled unavailable or rejected a bf16 operand");
+    dim3 grid((g.N + BN - 1) / BN, (g.M + 127) / 128, splits);
+    return launch_pdl(c, "w16_gemm_kernel", w16_gemm_kernel<BN, ST, EPI>, grid, dim3(512),
+                      w16_gemm_smem_bytes<BN, ST>(), st, ma, mb, g);
+}
+
+int check_hidden16(int H) {
+    if (H < 64 || H > W16_MAX_H || H % 64 != 0)
+        return fail(GBXCU_EINVAL, "bf16 wide MLP: hidden width must be a multiple of 64 in [64, 512]");
+    return GBXCU_OK;
+}
+
+struct W16Plan {
+    int H;
+    size_t bmax, ldt;
+    int s4, s5;
+};
+
+W16Plan w16_plan(gbxcu_ctx* c, int H, size_t bmax) {
+    W16Plan P{H, bmax, (bmax + 7) & ~(size_t)7, 1, 1};
+    // split-K so the K = batch GEMMs fill the machine
+    const int kblocks = (int)((bmax + 63) / 64);
+    const int tiles4 = ((H + 127) / 128) * ((H + 255) / 256), tiles5 = (H + 127) / 128;
+    P.s4 = std::max(1, std::min(kblocks, c->num_sms / tiles4));
+    P.s5 = std::max(1, std::min(kblocks, c->num_sms / tiles5));
+    // no empty splits (each split covers ceil(kblocks / s) blocks)
+    P.s4 = (kblocks + (kblocks + P.s4 - 1) / P.s4 - 1) / ((kblocks + P.s4 - 1) / P.s4);
+    P.s5 = (kblocks + (kblocks + P.s5 - 1) / P.s5 - 1) / ((kblocks + P.s5 - 1) / P.s5);
+    return P;
+}
+
+int w16_alloc(gbxcu_ctx* c, const W16Plan& P) {
+    const size_t H = P.H, b = P.bmax, t = P.ldt, bf = 2;
+    RET(c->b_xg.ensure(bf * b * 64));
+    RET(c->b_xt.ensure(bf * 64 * t));
+    RET(c->b_h1.ensure(bf * b * H));
+    RET(c->b_h1t.ensure(bf * H * t));
+    RET(c->b_d2.ensure(bf * b * H));
+    RET(c->b_d2t.ensure(bf * H * t));
+    RET(c->b_d1t.ensure(bf * H * t));
+    RET(c->b_w0p.ensure(bf * H * 64));
+    RET(c->b_w1.ensure(bf * H * H));
+    RET(c->b_w1t.ensure(bf * H * H));
+    RET(c->b_p4.ensure(sizeof(float) * (size_t)P.s4 * H * H));
+    RET(c->b_p5.ensure(sizeof(float) * (size_t)P.s5 * H * 64));
+    RET(c->b_hp.ensure(sizeof(double) * ((b + 127) / 128) * (3 * H + 3)));
+    RET(c->w_grad.ensure(sizeof(float) * wide_param_count(P.H)));
+    RET(c->w_loss.ensure(64));
+    return GBXCU_OK;
+}
+
+// One SGD step on rows[0, nbr) (this rank's slice of a global batch of nb), BF16 path.
+int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const double* tgt,
+             const uint32_t* rows, int nbr, size_t nb, double lr, const int* epoch, cudaStream_t st) {
+    const int H = P.H, ldt = (int)P.ldt;
+    const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H, o_w2 = o_b1 + H;
+    using bf = __nv_bfloat16;
+    W16UpdArgs u{};
+    u.params = Pm; u.hidden = H; u.np = wide_param_count(H); u.nb = nb; u.lr = lr;
+    u.p4 = c->b_p4.as<float>(); u.s4 = P.s4; u.p5 = c->b_p5.as<float>(); u.s5 = P.s5;
+    u.hp = c->b_hp.as<double>(); u.nhead = (nbr + 127) / 128;
+    u.g_out = c->w_grad.as<float>(); u.loss_sum = c->w_loss.as<double>();
+    u.w0p = c->b_w0p.as<bf>(); u.w1 = c->b_w1.as<bf>(); u.w1t = c->b_w1t.as<bf>();
+    u.epoch = epoch; u.diverged = c->diverged.as<int>(); u.epoch_acc = c->epoch_acc.as<double>();
+    if (nbr > 0) {
+        RET(launch_pdl(c, "w16_gather_kernel", w16_gather_kernel, dim3(blocks(nbr)), dim3(256), 0, st, feat,
+                       rows, nbr, c->b_xg.as<bf>(), c->b_xt.as<bf>(), ldt));
+        W16Args g1{};  // H1 = relu(Xg W0^T + b0) -> H1, H1^T
+        g1.M = nbr; g1.N = H; g1.K = 64; g1.bias = Pm + o_b0;
+        g1.out = c->b_h1.as<bf>(); g1.ldo = H; g1.out_t = c->b_h1t.as<bf>(); g1.ldt = ldt;
+        RET((launch_w16<256, 4, W16_EPI_H1>(c, c->b_xg.p, 64, c->b_w0p.p, 64, g1, 1, st)));
+        W16Args g2{};  // acc = H1 W1^T -> fused head -> D2, D2^T, head partials
+        g2.M = nbr; g2.N = H; g2.K = H; g2.bias = Pm + o_b1;
+        g2.out = c->b_d2.as<bf>(); g2.ldo = H; g2.out_t = c->b_d2t.as<bf>(); g2.ldt = ldt;
+        g2.w2 = Pm + o_w2; g2.b2 = Pm + o_w2 + 2 * H; g2.tgt = tgt; g2.rows = rows;
+        g2.inv_b = 1.0 / (double)nb; g2.head_part = c->b_hp.as<double>();
+        RET((launch_w16<512, 2, W16_EPI_HEAD>(c, c->b_h1.p, H, c->b_w1.p, H, g2, 1, st)));
+        W16Args g3{};  // D1 = (D2 W1) [H1 > 0] -> D1^T
+        g3.M = nbr; g3.N = H; g3.K = H; g3.mask = c->b_h1.as<bf>(); g3.ldm = H;
+        g3.out_t = c->b_d1t.as<bf>(); g3.ldt = ldt;
+        RET((launch_w16<256, 4, W16_EPI_D1T>(c, c->b_d2.p, H, c->b_w1t.p, H, g3, 1, st)));
+        W16Args g4{};  // gW1 = D2^T H1 (split-K partials)
+        g4.M = H; g4.N = H; g4.K = nbr; g4.part = c->b_p4.as<float>(); g4.ldp = H;
+        g4.split_stride = (size_t)H * H;
+        RET((launch_w16<256, 4, W16_EPI_PART>(c, c->b_d2t.p, ldt, c->b_h1t.p, ldt, g4, P.s4, st)));
+        W16Args g5{};  // gW0 | gb0 = D1^T [X | 1] (split-K partials)
+        g5.M = H; g5.N = 64; g5.K = nbr; g5.part = c->b_p5.as<float>(); g5.ldp = 64;
+        g5.split_stride = (size_t)H * 64;
+        RET((launch_w16<64, 6, W16_EPI_PART>(c, c->b_d1t.p, ldt, c->b_xt.p, ldt, g5, P.s5, st)));
+    } else {
+        // an empty slice contributes nothing (data-parallel remainder steps)
+        CK(cudaMemsetAsync(c->b_p4.p, 0, sizeof(float) * (size_t)P.s4 * H * H, st));
+        CK(cudaMemsetAsync(c->b_p5.p, 0, sizeof(float) * (size_t)P.s5 * H * 64, st));
+        CK(cudaMemsetAsync(c->b_hp.p, 0, sizeof(double) * (3 * H + 3), st));
+        u.nhead = 1;
+    }
+    const int nblk = blocks(u.np);
+    if (!c->comm) return launch_pdl(c, "w16_update_kernel", w16_update_kernel, dim3(nblk), dim3(256), 0, st, u, 0);
+    w16_update_kernel<<<nblk, 256, 0, st>>>(u, 1);
+    RET(check_launch(c, "w16_update_kernel"));
+    CKN(ncclAllReduce(u.g_out, u.g_out, u.np, ncclFloat32, ncclSum, c->comm, st));
+    CKN(ncclAllReduce(u.loss_sum, u.loss_sum, 1, ncclFloat64, ncclSum, c->comm, st));
+    w16_update_kernel<<<nblk, 256, 0, st>>>(u, 2);
+    return check_launch(c, "w16_update_kernel");
+}
+
+int w16_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, const double* d_tgt, size_t n,
+                   const gbxcu_train_cfg* cfg, double* epoch_loss_out, int* diverged_epoch, cudaStream_t st) {
+    RET(check_hidden16(H));
+    RET(validate_cfg(cfg, n));
+    if (cfg->loss_mode != GBXCU_LOSS_KL || cfg->optimizer != GBXCU_OPT_SGD)
+        return fail(GBXCU_EINVAL, "the wide MLP trains with the reference's KL + SGD only");
+    RET(setup_kernel_attrs());
+    RET(prepare_order(c, n, st));
+    const size_t b = std::min<size_t>((size_t)cfg->batch_size, n);
+    const W16Plan P = w16_plan(c, H, (b + c->nranks - 1) / c->nranks);
+    RET(w16_alloc(c, P));
+    RET(c->epoch_loss.ensure(sizeof(double) * cfg->epochs));
+    RET(c->epoch_acc.ensure(16));
+    RET(c->w_epoch.ensure(16));
+    using bf = __nv_bfloat16;
+    w16_weights_kernel<<<blocks((size_t)H * H), 256, 0, st>>>(d_params, H, c->b_w0p.as<bf>(), c->b_w1.as<bf>(),
+                                                              c->b_w1t.as<bf>());
+    RET(check_launch(c, "w16_weights_kernel"));
+    const long n_steps = (long)((n + cfg->batch_size - 1) / cfg->batch_size);
+    auto run_steps = [&](const uint32_t* order) -> int {
+        for (long s = 0; s < n_steps; ++s) {
+            const size_t start = (size_t)s * cfg->batch_size;
+            const size_t nb = std::min(n, start + (size_t)cfg->batch_size) - start;
+            const size_t per = (nb + c->nranks - 1) / c->nranks;
+            const size_t lo = std::min(nb, (size_t)c->rank * per), hi = std::min(nb, lo + per);
+            RET(w16_step(c, P, d_params, d_feat, d_tgt, order + start + lo, (int)(hi - lo), nb,
+                         cfg->learning_rate, c->w_epoch.as<int>(), st));
+        }
+        return GBXCU_OK;
+    };
+    // an epoch's ~7 launches per step replay as a CUDA graph (single-GPU path)
+    const bool use_graph = !c->comm && n_steps > 1;
+    for (int e = 0; e < cfg->epochs; ++e) {
+        RET(shuffle_epoch(c, n, cfg->seed, e, st));
+        CK(cudaMemsetAsync(c->epoch_acc.p, 0, sizeof(double), st));
+        CK(cudaMemcpyAsync(c->w_epoch.p, &e, sizeof(int), cudaMemcpyHostToDevice, st));
+        const uint32_t* order = c->order.as<uint32_t>();
+        if (!use_graph) {
+            RET(run_steps(order));
+        } else {
+            double lr = cfg->learning_rate;
+            uint64_t lr_bits;
+            std::memcpy(&lr_bits, &lr, 8);
+            const std::vector<const void*> key = {
+                (const void*)(uintptr_t)16, order, d_params, d_feat, d_tgt, (const void*)(uintptr_t)H,
+                (const void*)n, (const void*)(uintptr_t)cfg->batch_size, (const void*)(uintptr_t)lr_bits,
+                (const void*)P.ldt, (const void*)(uintptr_t)P.s4, (const void*)(uintptr_t)P.s5,
+                c->b_xg.p, c->b_xt.p, c->b_h1.p, c->b_h1t.p, c->b_d2.p, c->b_d2t.p, c->b_d1t.p,
+                c->b_w0p.p, c->b_w1.p, c->b_w1t.p, c->b_p4.p, c->b_p5.p, c->b_hp.p, c->w_grad.p,
+                c->w_loss.p, c->w_epoch.p, c->diverged.p, c->epoch_acc.p};
+            gbxcu_ctx::WideGraph* g = nullptr;
+            for (auto& x : c->wg)
+                if (x.exec && x.key == key) g = &x;
+            if (!g) {
+                g = &c->wg[c->wg_next];
+                c->wg_next ^= 1;
+                if (g->exec) cudaGraphExecDestroy(g->exec);
+                g->exec = nullptr;
+                g->key.clear();
+                CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                const int rc = run_steps(order);
+                cudaGraph_t graph = nullptr;
+                const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+                if (rc != GBXCU_OK) {
+                    if (graph) cudaGraphDestroy(graph);
+                    return rc;
+                }
+                if (ce != cudaSuccess) return fail(GBXCU_ECUDA, "wide-step graph capture failed");
+                const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+                cudaGraphDestroy(graph);
+                if (ie != cudaSuccess) {
+                    g->exec = nullptr;
+                    return fail(GBXCU_ECUDA, "wide-step graph instantiation failed");
+                }
+                g->key = key;
+            }
+            CK(cudaGraphLaunch(g->exec, st));
+        }
+        finish_epoch_kernel<<<1, 1, 0, st>>>(c->epoch_acc.as<double>(), n, e, c->diverged.as<int>(),
+                                              c->epoch_loss.as<double>());
+        RET(check_launch(c, "finish_epoch_kernel"));
+    }
+    int dv = -1;
+    CK(cudaMemcpyAsync(&dv, c->diverged.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (epoch_loss_out)
+        CK(cudaMemcpyAsync(epoch_loss_out, c->epoch_loss.p, sizeof(double) * cfg->epochs,
+                           cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (diverged_epoch) *diverged_epoch = dv;
+    if (dv >= 0)
+        return fail(GBXCU_EDIVERGED, "training loss became non-finite at epoch " + std::to_string(dv));
+    return GBXCU_OK;
+}
+
 int wide_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, const double* d_tgt,
                     size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out,
                     int* diverged_epoch, cudaStream_t st) {
@@ -2023,10 +2271,13 @@ int gbxcu_wide_forward(gbxcu_ctx* c, int hidden, const float* params, const floa
     return GBXCU_OK;
 }
 
-int gbxcu_wide_fit(gbxcu_ctx* c, int hidden, float* params_inout, const float* feat, const double* tgt,
-                   size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out, int* diverged_epoch) {
+int gbxcu_wide_fit_ex(gbxcu_ctx* c, int hidden, int precision, float* params_inout, const float* feat,
+                      const double* tgt, size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out,
+                      int* diverged_epoch) {
     if (!c || !params_inout || !feat || !tgt) return fail(GBXCU_EINVAL, "null argument");
-    RET(check_hidden(hidden));
+    if (precision != GBXCU_WIDE_TF32 && precision != GBXCU_WIDE_BF16)
+        return fail(GBXCU_EINVAL, "unknown wide-MLP precision");
+    RET(precision == GBXCU_WIDE_BF16 ? check_hidden16(hidden) : check_hidden(hidden));
     RET(validate_cfg(cfg, n));
     std::lock_guard<std::mutex> lk(c->mu);
     CK(cudaSetDevice(c->device));
@@ -2035,8 +2286,11 @@ int gbxcu_wide_fit(gbxcu_ctx* c, int hidden, float* params_inout, const float* f
     RET(upload(c->w_params, params_inout, np, st));
     RET(upload(c->w_feat, feat, n * F, st));
     RET(upload(c->w_tgt, tgt, n * 2, st));
-    int rc = wide_fit_device(c, hidden, c->w_params.as<float>(), c->w_feat.as<float>(),
-                             c->w_tgt.as<double>(), n, cfg, epoch_loss_out, diverged_epoch, st);
+    int rc = precision == GBXCU_WIDE_BF16
+                 ? w16_fit_device(c, hidden, c->w_params.as<float>(), c->w_feat.as<float>(),
+                                  c->w_tgt.as<double>(), n, cfg, epoch_loss_out, diverged_epoch, st)
+                 : wide_fit_device(c, hidden, c->w_params.as<float>(), c->w_feat.as<float>(),
+                                   c->w_tgt.as<double>(), n, cfg, epoch_loss_out, diverged_epoch, st);
     if (rc != GBXCU_OK && rc != GBXCU_EDIVERGED) return rc;
     const std::string msg = g_err;
     CK(cudaMemcpyAsync(params_inout, c->w_params.p, sizeof(float) * np, cudaMemcpyDeviceToHost, st));
@@ -2045,14 +2299,62 @@ int gbxcu_wide_fit(gbxcu_ctx* c, int hidden, float* params_inout, const float* f
     return rc;
 }
 
+int gbxcu_wide_fit(gbxcu_ctx* c, int hidden, float* params_inout, const float* feat, const double* tgt,
+                   size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out, int* diverged_epoch) {
+    return gbxcu_wide_fit_ex(c, hidden, GBXCU_WIDE_TF32, params_inout, feat, tgt, n, cfg, epoch_loss_out,
+                             diverged_epoch);
+}
+
+int gbxcu_wide_fit_ex_dev(gbxcu_ctx* c, int hidden, int precision, float* d_params, const float* d_feat,
+                          const double* d_tgt, size_t n, const gbxcu_train_cfg* cfg, double* epoch_loss_out,
+                          int* diverged_epoch, void* stream) {
+    if (!c || !d_params || !d_feat || !d_tgt) return fail(GBXCU_EINVAL, "null argument");
+    if (precision != GBXCU_WIDE_TF32 && precision != GBXCU_WIDE_BF16)
+        return fail(GBXCU_EINVAL, "unknown wide-MLP precision");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    if (precision == GBXCU_WIDE_BF16)
+        return w16_fit_device(c, hidden, d_params, d_feat, d_tgt, n, cfg, epoch_loss_out, diverged_epoch,
+                              pick(c, stream));
+    return wide_fit_device(c, hidden, d_params, d_feat, d_tgt, n, cfg, epoch_loss_out, diverged_epoch,
+                           pick(c, stream));
+}
+
 int gbxcu_wide_fit_dev(gbxcu_ctx* c, int hidden, float* d_params, const float* d_feat,
                        const double* d_tgt, size_t n, const gbxcu_train_cfg* cfg,
                        double* epoch_loss_out, int* diverged_epoch, void* stream) {
-    if (!c || !d_params || !d_feat || !d_tgt) return fail(GBXCU_EINVAL, "null argument");
+    return gbxcu_wide_fit_ex_dev(c, hidden, GBXCU_WIDE_TF32, d_params, d_feat, d_tgt, n, cfg,
+                                 epoch_loss_out, diverged_epoch, stream);
+}
+
+// D[M][N] = bf16(A)[M][K] . bf16(B)[N][K]^T on the tcgen05 kind::f16 kernel
+// (host fp32 buffers, rounded to bf16 on the device; fp32 result).
+int gbxcu_bf16_gemm(gbxcu_ctx* c, int M, int N, int K, const float* A, const float* B, float* D) {
+    if (!c || !A || !B || !D || M < 1 || N < 1 || K < 1) return fail(GBXCU_EINVAL, "bad gemm arguments");
     std::lock_guard<std::mutex> lk(c->mu);
     CK(cudaSetDevice(c->device));
-    return wide_fit_device(c, hidden, d_params, d_feat, d_tgt, n, cfg, epoch_loss_out,
-                           diverged_epoch, pick(c, stream));
+    RET(setup_kernel_attrs());
+    cudaStream_t st = c->stream;
+    const int ka = (K + 7) & ~7, np = (N + 15) & ~15;  // 16-B row strides; 16-column epilogue chunks
+    std::vector<float> a((size_t)M * ka, 0.f), b((size_t)N * ka, 0.f);
+    for (int r = 0; r < M; ++r) std::memcpy(&a[(size_t)r * ka], A + (size_t)r * K, sizeof(float) * K);
+    for (int r = 0; r < N; ++r) std::memcpy(&b[(size_t)r * ka], B + (size_t)r * K, sizeof(float) * K);
+    RET(upload(c->w_h1, a.data(), a.size(), st));
+    RET(upload(c->w_h2, b.data(), b.size(), st));
+    RET(c->b_h1.ensure(2 * a.size()));
+    RET(c->b_d2.ensure(2 * b.size()));
+    RET(c->w_d2.ensure(sizeof(float) * (size_t)M * np));
+    to_bf16_kernel<<<blocks(a.size()), 256, 0, st>>>(c->w_h1.as<float>(), a.size(), c->b_h1.as<__nv_bfloat16>());
+    to_bf16_kernel<<<blocks(b.size()), 256, 0, st>>>(c->w_h2.as<float>(), b.size(), c->b_d2.as<__nv_bfloat16>());
+    RET(check_launch(c, "to_bf16_kernel"));
+    W16Args g{};
+    g.M = M; g.N = N; g.K = K; g.part = c->w_d2.as<float>(); g.ldp = np; g.split_stride = 0;
+    RET((launch_w16<256, 4, W16_EPI_PART>(c, c->b_h1.p, ka, c->b_d2.p, ka, g, 1, st)));
+    std::vector<float> out((size_t)M * np);
+    CK(cudaMemcpyAsync(out.data(), c->w_d2.p, sizeof(float) * out.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int r = 0; r < M; ++r) std::memcpy(D + (size_t)r * N, &out[(size_t)r * np], sizeof(float) * N);
+    return GBXCU_OK;
 }
 
 // Plain D[M][N] = A[M][K] . B[N][K]^T on the tcgen05 TF32 path (host buffers).

@@ -1,0 +1,603 @@
+// k_wide16.cu — the wide-MLP (C4: 44 -> H -> H -> 2, H = 512) training step on
+// the 5th-generation tensor cores with BF16 operands (tcgen05 kind::f16, fp32
+// accumulation in TMEM): twice the TF32 path's tensor rate and half its
+// operand bytes.
+//
+// Semantics: fit / run_forward / accumulate_gradient generalised over widths
+// (the reference hard-codes 44-64-32-2, proj/include/gbx/policy.hpp:32-35;
+// oracle/gbx_oracle.c restates them for any dims). Activations are stored in
+// BF16 between the GEMMs; the master parameters, biases, the head (logits,
+// softmax, KL, d3) and the update w = float(double(w) - lr g) stay fp32/fp64.
+// oracle/wide_emul.py models these rounding points for the parity tests.
+//
+// One step = 5 GEMMs (both operands K-major, staged by TMA with the 128-byte
+// swizzle into an mbarrier ring; one producer thread, one MMA-issuing thread,
+// four epilogue warps reading TMEM) + a gather and a fused update:
+//   gather  Xg = bf16(X[rows]) [B][64], X^T [64][B] (row 44 = 1: gb0 via G5)
+//   G1  H1 = relu(Xg W0^T + b0)            -> H1 [B][H], H1^T [H][B]     (BN 256)
+//   G2  acc = H1 W1^T, full rows (BN = H): the head runs in the epilogue:
+//       h2 = relu(acc + b1) (never stored), logits (fp64), softmax, KL, d3,
+//       D2 = (d3 w2) [h2 > 0] -> D2 [B][H], D2^T [H][B];
+//       per-CTA column sums gW2 = sum d3 h2, gb1 = sum D2, gb2, KL
+//   G3  D1 = (D2 W1) [H1 > 0]              -> D1^T [H][B]               (BN 256)
+//   G4  gW1 = D2^T H1 (K = batch, split-K fp32 partials)
+//   G5  gW0 | gb0 = D1^T [X | 1] (K = batch, split-K fp32 partials)
+//   update: every gradient reduced in a fixed order, loss / divergence, SGD,
+//       refreshed BF16 copies of W0, W1, W1^T — one launch.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstddef>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_util.cuh"
+
+namespace gbxcu {
+
+using namespace tc;
+
+namespace {
+
+constexpr int W_BM = 128;  // rows per CTA tile (TMEM lanes)
+constexpr int W_BK = 64;   // bf16 per 128-byte swizzle row = K per stage
+
+// Instruction descriptor: A, B = BF16 (K-major), D = F32, dense.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4)                       // c_format = F32
+           | (1u << 7)                     // a_format = BF16
+           | (1u << 10)                    // b_format = BF16
+           | ((uint32_t)(N >> 3) << 17)    // n_dim
+           | ((uint32_t)(M >> 4) << 24);   // m_dim
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(uint64_t* mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+// bounded wait: a protocol bug must not hang the GPU (traps after ~seconds)
+__device__ __forceinline__ void mbar_wait_b(uint64_t* mbar, uint32_t parity) {
+    uint32_t done = 0;
+    for (uint32_t it = 0; !done; ++it) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done)
+            : "r"(smem_u32(mbar)), "r"(parity)
+            : "memory");
+        if (it > (1u << 28)) __trap();
+    }
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(mbar))
+        : "memory");
+}
+
+// Warp-collective: 32 consecutive fp32 columns of this warp's 32 TMEM lanes.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Programmatic dependent launch: let the next kernel of the step start its
+// prologue (TMEM / barrier setup) now; wait for the previous kernel's results.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+__device__ __forceinline__ void store_row16(__nv_bfloat16* dst, const float* h) {
+    uint4 q0, q1;
+    q0.x = pack_bf16(h[0], h[1]); q0.y = pack_bf16(h[2], h[3]);
+    q0.z = pack_bf16(h[4], h[5]); q0.w = pack_bf16(h[6], h[7]);
+    q1.x = pack_bf16(h[8], h[9]); q1.y = pack_bf16(h[10], h[11]);
+    q1.z = pack_bf16(h[12], h[13]); q1.w = pack_bf16(h[14], h[15]);
+    reinterpret_cast<uint4*>(dst)[0] = q0;
+    reinterpret_cast<uint4*>(dst)[1] = q1;
+}
+__device__ __forceinline__ void load_row16(const __nv_bfloat16* src, float (&m)[16]) {
+    const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(src));
+    const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+    const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+        m[2 * i] = __bfloat162float(v.x);
+        m[2 * i + 1] = __bfloat162float(v.y);
+    }
+}
+
+template <int BN, int ST>
+struct W16Smem {
+    __nv_bfloat16 a[ST][W_BM * W_BK];  // [stage][row][64] with the 128-byte swizzle
+    __nv_bfloat16 b[ST][BN * W_BK];
+    uint64_t full[ST];
+    uint64_t empty[ST];
+    uint64_t done;
+    uint32_t tmem;
+};
+
+__host__ __device__ constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : bn <= 256 ? 256 : 512; }
+
+constexpr int W_EW = 4;                // epilogue warps per TMEM lane quarter
+constexpr int W_THREADS = 128 * W_EW;  // 16 warps: warp w reads lanes 32 (w % 4).., columns group w / 4
+
+// Epilogue scratch (re-uses the drained stage buffers): per warp one 32-row x
+// 16-column chunk for the transposed stores / column sums
+struct EpiScratch {
+    float t[16][32][17];
+};
+struct HeadScratch {
+    float t[16][32][17];         // per warp: h2 of its 32 rows x 16 columns
+    float d[16][32][17];         // per warp: D2 of the same chunk
+    float b1[W16_MAX_H];
+    float w2[2][W16_MAX_H];
+    double lg[W_EW][128][2];     // per column group: partial logits of the CTA's 128 rows
+    float d3[128][2];
+    double wsum[4][3][W16_MAX_H];  // per lane quarter: column sums (gW2_0, gW2_1, gb1)
+    double red[16][3];
+};
+
+// Transposed bf16 store of a warp's 32 rows x 16 columns (tile t[r][c]):
+// dst[(c0 + c) * ldt + r0 + r]; lane = (column c = lane / 2, rows 16 (lane & 1)..+16)
+// as two 16-byte stores instead of sixteen 2-byte ones per thread.
+__device__ __forceinline__ void store_t16(const float (&t)[32][17], __nv_bfloat16* dst, size_t ldt, int c0,
+                                          int r0, int nrows, int ncols, int lane) {
+    const int c = lane >> 1, rh = (lane & 1) * 16;
+    if (c >= ncols) return;
+    __nv_bfloat16* o = dst + (size_t)(c0 + c) * ldt + r0 + rh;
+    if (rh + 16 <= nrows) {
+        float h[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) h[i] = t[rh + i][c];
+        store_row16(o, h);
+    } else {
+        for (int i = 0; rh + i < nrows; ++i) o[i] = __float2bfloat16_rn(t[rh + i][c]);
+    }
+}
+
+}  // namespace
+
+template <int BN, int ST>
+size_t w16_gemm_smem_bytes() {
+    size_t s = sizeof(W16Smem<BN, ST>);
+    if (sizeof(EpiScratch) > s) s = sizeof(EpiScratch);
+    if (BN == W16_MAX_H && sizeof(HeadScratch) > s) s = sizeof(HeadScratch);
+    return s + 1024;
+}
+template size_t w16_gemm_smem_bytes<64, 6>();
+template size_t w16_gemm_smem_bytes<256, 4>();
+template size_t w16_gemm_smem_bytes<512, 2>();
+
+// D[M x N] = A[M x K] . B[N x K]^T, bf16 operands, fp32 accumulation, epilogue EPI.
+// Grid (ceil(N/BN), ceil(M/128), splits). Warp 0 lane 0: TMA producer; warp 1
+// lane 0: MMA issuer; all 16 warps: epilogue (warp w: TMEM lanes 32 (w % 4)..
+// = output rows, column group w / 4 of BN / 4 columns; thread = one row).
+template <int BN, int ST, int EPI>
+__global__ void __launch_bounds__(W_THREADS, 1)
+w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                W16Args g) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    W16Smem<BN, ST>& S = *reinterpret_cast<W16Smem<BN, ST>*>(base);
+    constexpr int NMMA = BN > 256 ? 2 : 1;   // MMA N <= 256
+    constexpr int MN = BN / NMMA;
+    constexpr int BOX = BN > 256 ? 256 : BN;  // TMA box rows <= 256
+    constexpr int TC = tmem_cols(BN);
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const int col0 = blockIdx.x * BN, row0 = blockIdx.y * W_BM;
+    const int nkb = (g.K + W_BK - 1) / W_BK;
+    const int per = (nkb + gridDim.z - 1) / gridDim.z;
+    const int kb_lo = blockIdx.z * per, kb_hi = min(nkb, kb_lo + per);
+    const int nk = max(0, kb_hi - kb_lo);
+
+    if (w == 0) tmem_alloc(&S.tmem, TC);
+    if (tid == 32) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], 1);
+        }
+        mbar_init(&S.done, 1);
+        fence_mbar_init();
+    }
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tacc = S.tmem;
+    // (prologue done: the step's next kernel may start its own; every read of
+    //  the previous kernel's results comes after its completion)
+    pdl_trigger();
+    pdl_wait();
+
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+        constexpr uint32_t bytes = (W_BM + BN) * W_BK * 2;
+        for (int it = 0; it < nk; ++it) {
+            const int slot = it % ST;
+            if (it >= ST) mbar_wait_b(&S.empty[slot], ((it / ST) - 1) & 1);
+            mbar_expect(&S.full[slot], bytes);
+            const int k0 = (kb_lo + it) * W_BK;
+            tma_2d(&S.a[slot][0], &map_a, k0, row0, &S.full[slot]);
+#pragma unroll
+            for (int h = 0; h < BN / BOX; ++h)
+                tma_2d(&S.b[slot][h * BOX * W_BK], &map_b, k0, col0 + h * BOX, &S.full[slot]);
+        }
+    } else if (tid == 32) {
+        const uint32_t idesc = idesc_bf16(W_BM, MN);
+        for (int it = 0; it < nk; ++it) {
+            const int slot = it % ST;
+            mbar_wait_b(&S.full[slot], (it / ST) & 1);
+            fence_after_sync();
+            const uint32_t a0 = smem_u32(&S.a[slot][0]), b0 = smem_u32(&S.b[slot][0]);
+#pragma unroll
+            for (int s = 0; s < W_BK / 16; ++s) {  // K = 16 per MMA: 32 B along the swizzled row
+                const uint64_t ad = smem_desc_sw128(a0 + 32 * s);
+#pragma unroll
+                for (int h = 0; h < NMMA; ++h) {
+                    const uint64_t bd = smem_desc_sw128(b0 + h * MN * 128 + 32 * s);
+                    mma_bf16(tacc + h * MN, ad, bd, idesc, (it > 0 || s > 0) ? 1u : 0u);
+                }
+            }
+            commit_to(&S.empty[slot]);  // frees the stage once these MMAs have read it
+        }
+        commit_to(&S.done);
+    }
+    __syncwarp();
+    if (nk > 0) mbar_wait_b(&S.done, 0);
+    fence_after_sync();
+
+    const int qw = w & 3, cg = w >> 2;        // lane quarter, column group
+    const int rw0 = row0 + 32 * qw;             // first row of this warp
+    const int row = rw0 + lane;
+    const bool row_ok = row < g.M;
+    const int nrows = max(0, min(32, g.M - rw0));
+    const uint32_t tq = tacc + ((uint32_t)(32 * qw) << 16);
+    constexpr int CW = BN / W_EW;               // columns per group
+    const int cbeg = cg * CW;
+    __syncthreads();  // every warp is past the mainloop: stage buffers are free for scratch
+
+    if constexpr (EPI == W16_EPI_HEAD) {
+        // ---- fused head (G2): BN = H covers full rows; the 4 column groups
+        //      of a row combine their partial logits through shared memory
+        HeadScratch& T = *reinterpret_cast<HeadScratch*>(base);
+        const int H = g.N;
+        for (int c = tid; c < H; c += W_THREADS) {
+            T.b1[c] = g.bias[c];
+            T.w2[0][c] = g.w2[c];
+            T.w2[1][c] = g.w2[H + c];
+        }
+        __syncthreads();
+        const int cend = min(H, cbeg + CW);
+        // pass 1: h2 = relu(acc + b1); partial logits in fp64 (two chains per output)
+        double l0a = 0.0, l0b = 0.0, l1a = 0.0, l1b = 0.0;
+        for (int c0 = cbeg; c0 < cend; c0 += 32) {
+            float v[32];
+            tmem_ld32(tq + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+                const float ha = fmaxf(v[i] + T.b1[c0 + i], 0.f), hb = fmaxf(v[i + 1] + T.b1[c0 + i + 1], 0.f);
+                l0a = fma((double)ha, (double)T.w2[0][c0 + i], l0a);
+                l1a = fma((double)ha, (double)T.w2[1][c0 + i], l1a);
+                l0b = fma((double)hb, (double)T.w2[0][c0 + i + 1], l0b);
+                l1b = fma((double)hb, (double)T.w2[1][c0 + i + 1], l1b);
+            }
+        }
+        T.lg[cg][32 * qw + lane][0] = l0a + l0b;
+        T.lg[cg][32 * qw + lane][1] = l1a + l1b;
+        __syncthreads();
+        // softmax, KL with the reference clamps, d3 = p (ln(p^/t^) - L) / |b|
+        // (every column group of a row computes the same values)
+        double d30 = 0.0, d31 = 0.0, loss = 0.0;
+        if (row_ok) {
+            const int rl = 32 * qw + lane;
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < W_EW; ++q) {
+                s0 += T.lg[q][rl][0];
+                s1 += T.lg[q][rl][1];
+            }
+            const double z0 = (double)g.b2[0] + s0, z1 = (double)g.b2[1] + s1;
+            const double m = z0 < z1 ? z1 : z0;
+            const double e0 = exp(z0 - m), e1 = exp(z1 - m);
+            const double p0 = e0 / (e0 + e1), p1 = e1 / (e0 + e1);
+            const size_t rec = g.rows ? g.rows[row] : (size_t)row;
+            const double pc0 = clampp(p0), pc1 = clampp(p1);
+            const double lr0 = log(pc0 / clampp(g.tgt[2 * rec])), lr1 = log(pc1 / clampp(g.tgt[2 * rec + 1]));
+            loss = pc0 * lr0 + pc1 * lr1;
+            d30 = p0 * (lr0 - loss) * g.inv_b;
+            d31 = p1 * (lr1 - loss) * g.inv_b;
+        }
+        const float d3f0 = (float)d30, d3f1 = (float)d31;
+        if (cg == 0) {
+            T.d3[32 * qw + lane][0] = d3f0;
+            T.d3[32 * qw + lane][1] = d3f1;
+        }
+        __syncthreads();
+        // pass 2 (fp32): D2 = (d3 w2) [h2 > 0] -> D2 (row-major), D2^T (staged
+        // transpose); column sums over the warp's 32 rows in fp32: lane l sums
+        // column c0 + (l & 15) over rows 16 (l >> 4).. +16, halves added in order
+        for (int c0 = cbeg; c0 < cend; c0 += 16) {
+            float v[16], d[16];
+            tmem_ld16(tq + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float h = row_ok ? fmaxf(v[i] + T.b1[c0 + i], 0.f) : 0.f;
+                d[i] = h > 0.f ? __fadd_rn(__fmul_rn(d3f0, T.w2[0][c0 + i]), __fmul_rn(d3f1, T.w2[1][c0 + i]))
+                               : 0.f;
+                T.t[w][lane][i] = h;
+                T.d[w][lane][i] = d[i];
+            }
+            if (row_ok) store_row16(g.out + (size_t)row * g.ldo + c0, d);
+            __syncwarp();
+            store_t16(T.d[w], g.out_t, g.ldt, c0, rw0, nrows, 16, lane);
+            const int c = lane & 15, rb = (lane >> 4) * 16;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int r = rb; r < rb + 16; ++r) {
+                const float hv = T.t[w][r][c];
+                s0 = fmaf(T.d3[32 * qw + r][0], hv, s0);
+                s1 = fmaf(T.d3[32 * qw + r][1], hv, s1);
+                s2 += T.d[w][r][c];
+            }
+            const float o0 = __shfl_xor_sync(0xffffffffu, s0, 16), o1 = __shfl_xor_sync(0xffffffffu, s1, 16),
+                        o2 = __shfl_xor_sync(0xffffffffu, s2, 16);
+            if (lane < 16) {
+                T.wsum[qw][0][c0 + c] = (double)s0 + (double)o0;
+                T.wsum[qw][1][c0 + c] = (double)s1 + (double)o1;
+                T.wsum[qw][2][c0 + c] = (double)s2 + (double)o2;
+            }
+            __syncwarp();
+        }
+        // gb2 and KL of the rows (column group 0 only; fixed shuffle tree)
+        double r0 = cg == 0 ? d30 : 0.0, r1 = cg == 0 ? d31 : 0.0, r2 = cg == 0 ? loss : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+            r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+            r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        }
+        if (lane == 0) {
+            T.red[w][0] = r0;
+            T.red[w][1] = r1;
+            T.red[w][2] = r2;
+        }
+        __syncthreads();
+        double* prow = g.head_part + (size_t)blockIdx.y * (3 * H + 3);
+        for (int q = 0; q < 3; ++q)
+            for (int c = tid; c < H; c += W_THREADS)
+                prow[q * H + c] = ((T.wsum[0][q][c] + T.wsum[1][q][c]) + T.wsum[2][q][c]) + T.wsum[3][q][c];
+        if (tid < 3) prow[3 * H + tid] = ((T.red[0][tid] + T.red[1][tid]) + T.red[2][tid]) + T.red[3][tid];
+    } else {
+        EpiScratch& T = *reinterpret_cast<EpiScratch*>(base);
+        for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
+            float v[16];
+            tmem_ld16(tq + c0, v);
+            tmem_ld_wait();
+            if (nk == 0) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            }
+            const int col = col0 + c0;
+            if (col >= g.N) break;  // (warp-uniform)
+            if constexpr (EPI == W16_EPI_H1) {
+                // h1 = relu(acc + b0): row-major (next GEMM's A) + transposed (G4's B)
+#pragma unroll
+                for (int i = 0; i < 16; ++i) T.t[w][lane][i] = fmaxf(v[i] + __ldg(g.bias + col + i), 0.f);
+                if (row_ok) store_row16(g.out + (size_t)row * g.ldo + col, T.t[w][lane]);
+                __syncwarp();
+                store_t16(T.t[w], g.out_t, g.ldt, col, rw0, nrows, 16, lane);
+                __syncwarp();
+            } else if constexpr (EPI == W16_EPI_D1T) {
+                // d1 = acc [h1 > 0] (mask = stored bf16 H1), transposed (G5's A)
+                float m[16];
+                if (row_ok) load_row16(g.mask + (size_t)row * g.ldm + col, m);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) T.t[w][lane][i] = row_ok && m[i] > 0.f ? v[i] : 0.f;
+                __syncwarp();
+                store_t16(T.t[w], g.out_t, g.ldt, col, rw0, nrows, 16, lane);
+                __syncwarp();
+            } else if (row_ok) {
+                // split-K fp32 partial, row-major [M][ldp]
+                float4* o = reinterpret_cast<float4*>(g.part + (size_t)blockIdx.z * g.split_stride +
+                                                      (size_t)row * g.ldp + col);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+        }
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (w == 0) tmem_dealloc(tacc, TC);
+}
+
+template __global__ void w16_gemm_kernel<256, 4, W16_EPI_H1>(const __grid_constant__ CUtensorMap,
+                                                             const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<512, 2, W16_EPI_HEAD>(const __grid_constant__ CUtensorMap,
+                                                               const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<256, 4, W16_EPI_D1T>(const __grid_constant__ CUtensorMap,
+                                                              const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<256, 4, W16_EPI_PART>(const __grid_constant__ CUtensorMap,
+                                                               const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<64, 6, W16_EPI_PART>(const __grid_constant__ CUtensorMap,
+                                                              const __grid_constant__ CUtensorMap, W16Args);
+
+// Xg[r] = bf16(feat[rows[r]]) padded to 64 columns (G1's A); X^T [64][ldt]
+// with row 44 = 1 (G5's B: its column 44 of D1^T [X|1] is gb0).
+__global__ void w16_gather_kernel(const float* __restrict__ feat, const uint32_t* __restrict__ rows, int nb,
+                                  __nv_bfloat16* __restrict__ xg, __nv_bfloat16* __restrict__ xt, int ldt) {
+    pdl_trigger();
+    pdl_wait();  // (the previous step's G5 reads X^T)
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nb) return;
+    const float4* x = reinterpret_cast<const float4*>(feat + (size_t)rows[r] * F);
+    float v[64];
+#pragma unroll
+    for (int q = 0; q < F / 4; ++q) {
+        const float4 t = __ldg(x + q);  // all 11 loads in flight
+        v[4 * q] = t.x;
+        v[4 * q + 1] = t.y;
+        v[4 * q + 2] = t.z;
+        v[4 * q + 3] = t.w;
+    }
+#pragma unroll
+    for (int i = F; i < 64; ++i) v[i] = 0.f;
+    uint4* g4 = reinterpret_cast<uint4*>(xg + (size_t)r * 64);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        g4[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                           pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+    v[F] = 1.f;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) xt[(size_t)i * ldt + r] = __float2bfloat16_rn(v[i]);
+}
+
+__global__ void to_bf16_kernel(const float* __restrict__ src, size_t n, __nv_bfloat16* __restrict__ dst) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) dst[t] = __float2bfloat16_rn(src[t]);
+}
+
+// BF16 operand copies of the fp32 master weights: W0p [H][64] (K padded),
+// W1 [H][H] (G2's B), W1^T [H][H] (G3's B).
+__global__ void w16_weights_kernel(const float* __restrict__ params, int H, __nv_bfloat16* __restrict__ w0p,
+                                   __nv_bfloat16* __restrict__ w1, __nv_bfloat16* __restrict__ w1t) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < (size_t)H * 64) {
+        const size_t j = t / 64, i = t % 64;
+        w0p[t] = __float2bfloat16_rn(i < F ? params[j * F + i] : 0.f);
+    }
+    if (t >= (size_t)H * H) return;
+    const size_t o_w1 = (size_t)H * F + H, k = t / H, j = t % H;
+    const __nv_bfloat16 b = __float2bfloat16_rn(params[o_w1 + t]);
+    w1[t] = b;
+    w1t[j * H + k] = b;
+}
+
+// sum_q src[q * stride] in q order, eight loads in flight at a time
+__device__ __forceinline__ double ordered_sum(const float* __restrict__ src, size_t stride, int n) {
+    double s = 0.0;
+    int q = 0;
+    for (; q + 8 <= n; q += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(src + (size_t)(q + j) * stride);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += v[j];
+    }
+    for (; q < n; ++q) s += __ldg(src + (size_t)q * stride);
+    return s;
+}
+__device__ __forceinline__ double ordered_sum(const double* __restrict__ src, size_t stride, int n) {
+    double s = 0.0;
+    int q = 0;
+    for (; q + 8 <= n; q += 8) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(src + (size_t)(q + j) * stride);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += v[j];
+    }
+    for (; q < n; ++q) s += __ldg(src + (size_t)q * stride);
+    return s;
+}
+
+// Gradient of parameter p (serialization order w0[H][44] b0[H] w1[H][H]
+// b1[H] w2[2][H] b2[2]) from the step's partials, summed in a fixed order.
+__device__ __forceinline__ double w16_grad(const W16UpdArgs& u, size_t p) {
+    const size_t H = u.hidden;
+    const size_t o_b0 = H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + H * H, o_w2 = o_b1 + H, o_b2 = o_w2 + 2 * H;
+    const size_t hw = 3 * H + 3;
+    if (p < o_w1) {  // gW0 | gb0: G5 partials [s5][H][64], column 44 = gb0
+        const size_t j = p < o_b0 ? p / F : p - o_b0, i = p < o_b0 ? p % F : (size_t)F;
+        return ordered_sum(u.p5 + j * 64 + i, H * 64, u.s5);
+    }
+    if (p < o_b1) return ordered_sum(u.p4 + (p - o_w1), H * H, u.s4);   // gW1: G4 partials [s4][H][H]
+    if (p < o_w2) return ordered_sum(u.hp + 2 * H + (p - o_b1), hw, u.nhead);  // gb1
+    if (p < o_b2) return ordered_sum(u.hp + (p - o_w2), hw, u.nhead);          // gW2
+    return ordered_sum(u.hp + 3 * H + (p - o_b2), hw, u.nhead);                // gb2
+}
+
+// KL sum of the step over the head partials (warp 0; fixed lane order + tree:
+// every block computes the identical value)
+__device__ __forceinline__ double w16_kl_sum(const W16UpdArgs& u) {
+    const int lane = threadIdx.x & 31;
+    const size_t hw = 3 * (size_t)u.hidden + 3;
+    double s = 0.0;
+    for (int q = lane; q < u.nhead; q += 32) s += u.hp[(size_t)q * hw + 3 * u.hidden + 2];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// mode 0: reduce + SGD + refreshed bf16 copies (one rank); 1: reduce into the
+// flat gradient g_out and the loss sum (before an all-reduce); 2: SGD from g_out.
+__global__ void __launch_bounds__(256) w16_update_kernel(W16UpdArgs u, int mode) {
+    __shared__ double s_loss;
+    pdl_trigger();
+    pdl_wait();
+    if (*u.diverged >= 0) return;
+    const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (mode == 1) {
+        if (blockIdx.x == 0 && threadIdx.x < 32) {
+            const double kl = w16_kl_sum(u);
+            if (threadIdx.x == 0) *u.loss_sum = kl;
+        }
+        if (p < u.np) u.g_out[p] = (float)w16_grad(u, p);
+        return;
+    }
+    if (threadIdx.x < 32) {
+        const double kl = mode == 2 ? *u.loss_sum : w16_kl_sum(u);
+        if (threadIdx.x == 0) s_loss = kl / (double)u.nb;
+    }
+    __syncthreads();
+    const double loss = s_loss;
+    if (!isfinite(loss)) {  // fit throws before updating (policy.cpp:321-325)
+        if (p == 0) *u.diverged = *u.epoch;
+        return;
+    }
+    if (p == 0) *u.epoch_acc += loss * (double)u.nb;
+    if (p >= u.np) return;
+    const double gsum = mode == 2 ? (double)u.g_out[p] : w16_grad(u, p);
+    const float nw = __double2float_rn((double)u.params[p] - u.lr * gsum);
+    u.params[p] = nw;
+    const size_t H = u.hidden, o_b0 = H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + H * H;
+    const __nv_bfloat16 b = __float2bfloat16_rn(nw);
+    if (p < o_b0) {
+        u.w0p[(p / F) * 64 + p % F] = b;
+    } else if (p >= o_w1 && p < o_b1) {
+        const size_t t = p - o_w1, k = t / H, j = t % H;
+        u.w1[t] = b;
+        u.w1t[j * H + k] = b;
+    }
+}
+
+}  // namespace gbxcu

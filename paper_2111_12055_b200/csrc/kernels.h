@@ -1,6 +1,8 @@
 // kernels.h — kernel declarations shared between the .cu translation units.
 #pragma once
 
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -168,6 +170,62 @@ struct WideHeadArgs {
 };
 __global__ void wide_head_reduce_kernel(const double* part, int nblocks, int hidden, float* gw2,
                                         float* gb2, float* gb1, double* loss_out);
+
+// ---- wide MLP, BF16 tensor-core path (k_wide16.cu)
+constexpr int W16_MAX_H = 512;   // the fused head keeps a full row (<= 512 fp32 TMEM columns)
+constexpr int W16_EPI_H1 = 0;    // relu(acc + bias) -> bf16 row-major + transposed
+constexpr int W16_EPI_HEAD = 1;  // fused softmax/KL head over full rows
+constexpr int W16_EPI_D1T = 2;   // acc [mask > 0] -> bf16 transposed
+constexpr int W16_EPI_PART = 3;  // fp32 split-K partials
+struct W16Args {
+    int M, N, K;
+    const float* bias;             // H1: b0, HEAD: b1
+    __nv_bfloat16* out;            // row-major [M][ldo] (H1, D2)
+    int ldo;
+    __nv_bfloat16* out_t;          // transposed [N][ldt] (H1^T, D2^T, D1^T)
+    int ldt;
+    const __nv_bfloat16* mask;     // D1T: H1 [M][ldm]
+    int ldm;
+    float* part;                   // PART: [split][M][ldp]
+    int ldp;
+    size_t split_stride;
+    // HEAD
+    const float* w2;               // [2][N]
+    const float* b2;               // [2]
+    const double* tgt;             // targets, indexed through rows
+    const uint32_t* rows;          // nullable
+    double inv_b;
+    double* head_part;             // [row tiles][3N + 3]: gW2_0, gW2_1, gb1, gb2_0, gb2_1, KL
+};
+struct W16UpdArgs {
+    float* params;                 // fp32 master weights (flat serialization order)
+    int hidden;
+    size_t np, nb;
+    double lr;
+    const float* p4;               // gW1 partials [s4][H][H]
+    int s4;
+    const float* p5;               // gW0|gb0 partials [s5][H][64]
+    int s5;
+    const double* hp;              // head partials [nhead][3H + 3]
+    int nhead;
+    float* g_out;                  // flat gradient (data-parallel path)
+    double* loss_sum;              // KL sum (data-parallel path)
+    __nv_bfloat16 *w0p, *w1, *w1t; // bf16 operand copies
+    const int* epoch;
+    int* diverged;
+    double* epoch_acc;
+};
+template <int BN, int ST>
+size_t w16_gemm_smem_bytes();
+template <int BN, int ST, int EPI>
+__global__ void w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
+                                const __grid_constant__ CUtensorMap map_b, W16Args g);
+__global__ void w16_gather_kernel(const float* feat, const uint32_t* rows, int nb, __nv_bfloat16* xg,
+                                  __nv_bfloat16* xt, int ldt);
+__global__ void w16_weights_kernel(const float* params, int H, __nv_bfloat16* w0p, __nv_bfloat16* w1,
+                                   __nv_bfloat16* w1t);
+__global__ void w16_update_kernel(W16UpdArgs u, int mode);
+__global__ void to_bf16_kernel(const float* src, size_t n, __nv_bfloat16* dst);
 
 __global__ void tc_gemm_kernel(GemmArgs g);
 template <int BN>
