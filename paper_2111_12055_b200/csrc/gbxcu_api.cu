@@ -200,10 +200,11 @@ int setup_kernel_attrs() {
         set((const void*)wide_head_kernel, sizeof(float) * 32 * (1024 + 1));
         set((const void*)tma_gemm_kernel<64>, tma_gemm_smem_bytes<64>());
         set((const void*)w16_gemm_kernel<256, 4, W16_EPI_H1>, w16_gemm_smem_bytes<256, 4>());
-        set((const void*)w16_gemm_kernel<512, 2, W16_EPI_HEAD>, w16_gemm_smem_bytes<512, 2>());
+        set((const void*)w16_gemm_kernel<256, 4, W16_EPI_HEAD>, w16_gemm_smem_bytes<256, 4>());
         set((const void*)w16_gemm_kernel<256, 4, W16_EPI_D1T>, w16_gemm_smem_bytes<256, 4>());
         set((const void*)w16_gemm_kernel<256, 4, W16_EPI_PART>, w16_gemm_smem_bytes<256, 4>());
         set((const void*)w16_gemm_kernel<64, 6, W16_EPI_PART>, w16_gemm_smem_bytes<64, 6>());
+        set((const void*)w16_gemm_kernel<128, 6, W16_EPI_PART>, w16_gemm_smem_bytes<128, 6>());
         set((const void*)tma_gemm_kernel<128>, tma_gemm_smem_bytes<128>());
         set((const void*)tma_gemm_kernel<256>, tma_gemm_smem_bytes<256>());
     });
@@ -1870,20 +1871,29 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
 // predecessor in the stream finishes (its griddepcontrol.wait orders the
 // data); kept through stream capture as a programmatic graph edge.
 template <typename... K, typename... A>
-int launch_pdl(gbxcu_ctx* c, const char* name, void (*kern)(K...), dim3 grid, dim3 block, size_t smem,
-               cudaStream_t st, A... args) {
+int launch_pdl_cl(gbxcu_ctx* c, const char* name, void (*kern)(K...), dim3 grid, dim3 block, size_t smem,
+                  cudaStream_t st, int cluster_x, A... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = (unsigned)cluster_x;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = cluster_x > 1 ? 2 : 1;
     CK(cudaLaunchKernelEx(&cfg, kern, args...));
     return check_launch(c, name);
+}
+template <typename... K, typename... A>
+int launch_pdl(gbxcu_ctx* c, const char* name, void (*kern)(K...), dim3 grid, dim3 block, size_t smem,
+               cudaStream_t st, A... args) {
+    return launch_pdl_cl(c, name, kern, grid, block, smem, st, 1, args...);
 }
 
 // K-major bf16 operand [rows][ld] (K valid columns) as TMA boxes of
@@ -1903,13 +1913,13 @@ bool make_bf16_map(CUtensorMap* m, const void* base, int K, int rows, int ld, in
 // D = A B^T on the bf16 kernel: A [M][lda] (K valid), B [N][ldb]; grid (N/BN, M/128, splits)
 template <int BN, int ST, int EPI>
 int launch_w16(gbxcu_ctx* c, const void* A, int lda, const void* B, int ldb, const W16Args& g, int splits,
-               cudaStream_t st) {
+               cudaStream_t st, int cluster_x = 1) {
     CUtensorMap ma, mb;
     if (!make_bf16_map(&ma, A, g.K, g.M, lda, 128) || !make_bf16_map(&mb, B, g.K, g.N, ldb, BN > 256 ? 256 : BN))
         return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled unavailable or rejected a bf16 operand");
     dim3 grid((g.N + BN - 1) / BN, (g.M + 127) / 128, splits);
-    return launch_pdl(c, "w16_gemm_kernel", w16_gemm_kernel<BN, ST, EPI>, grid, dim3(512),
-                      w16_gemm_smem_bytes<BN, ST>(), st, ma, mb, g);
+    return launch_pdl_cl(c, "w16_gemm_kernel", w16_gemm_kernel<BN, ST, EPI>, grid, dim3(512),
+                         w16_gemm_smem_bytes<BN, ST>(), st, cluster_x, ma, mb, g);
 }
 
 int check_hidden16(int H) {
@@ -1928,7 +1938,7 @@ W16Plan w16_plan(gbxcu_ctx* c, int H, size_t bmax) {
     W16Plan P{H, bmax, (bmax + 7) & ~(size_t)7, 1, 1};
     // split-K so the K = batch GEMMs fill the machine
     const int kblocks = (int)((bmax + 63) / 64);
-    const int tiles4 = ((H + 127) / 128) * ((H + 255) / 256), tiles5 = (H + 127) / 128;
+    const int tiles4 = ((H + 127) / 128) * ((H + 127) / 128), tiles5 = (H + 127) / 128;
     P.s4 = std::max(1, std::min(kblocks, c->num_sms / tiles4));
     P.s5 = std::max(1, std::min(kblocks, c->num_sms / tiles5));
     // no empty splits (each split covers ceil(kblocks / s) blocks)
@@ -1982,7 +1992,8 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
         g2.out = c->b_d2.as<bf>(); g2.ldo = H; g2.out_t = c->b_d2t.as<bf>(); g2.ldt = ldt;
         g2.w2 = Pm + o_w2; g2.b2 = Pm + o_w2 + 2 * H; g2.tgt = tgt; g2.rows = rows;
         g2.inv_b = 1.0 / (double)nb; g2.head_part = c->b_hp.as<double>();
-        RET((launch_w16<512, 2, W16_EPI_HEAD>(c, c->b_h1.p, H, c->b_w1.p, H, g2, 1, st)));
+        // a CTA pair (cluster along x) per 128-row tile covers the full rows
+        RET((launch_w16<256, 4, W16_EPI_HEAD>(c, c->b_h1.p, H, c->b_w1.p, H, g2, 1, st, (H + 255) / 256)));
         W16Args g3{};  // D1 = (D2 W1) [H1 > 0] -> D1^T
         g3.M = nbr; g3.N = H; g3.K = H; g3.mask = c->b_h1.as<bf>(); g3.ldm = H;
         g3.out_t = c->b_d1t.as<bf>(); g3.ldt = ldt;
@@ -1990,7 +2001,7 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
         W16Args g4{};  // gW1 = D2^T H1 (split-K partials)
         g4.M = H; g4.N = H; g4.K = nbr; g4.part = c->b_p4.as<float>(); g4.ldp = H;
         g4.split_stride = (size_t)H * H;
-        RET((launch_w16<256, 4, W16_EPI_PART>(c, c->b_d2t.p, ldt, c->b_h1t.p, ldt, g4, P.s4, st)));
+        RET((launch_w16<128, 6, W16_EPI_PART>(c, c->b_d2t.p, ldt, c->b_h1t.p, ldt, g4, P.s4, st)));
         W16Args g5{};  // gW0 | gb0 = D1^T [X | 1] (split-K partials)
         g5.M = H; g5.N = 64; g5.K = nbr; g5.part = c->b_p5.as<float>(); g5.ldp = 64;
         g5.split_stride = (size_t)H * 64;
@@ -2002,7 +2013,9 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
         CK(cudaMemsetAsync(c->b_hp.p, 0, sizeof(double) * (3 * H + 3), st));
         u.nhead = 1;
     }
-    const int nblk = blocks(u.np);
+    int nb0, nw1, nb2;
+    w16_update_layout(H, u.np, nb0, nw1, nb2);
+    const int nblk = nb0 + nw1 + nb2;
     if (!c->comm) return launch_pdl(c, "w16_update_kernel", w16_update_kernel, dim3(nblk), dim3(256), 0, st, u, 0);
     w16_update_kernel<<<nblk, 256, 0, st>>>(u, 1);
     RET(check_launch(c, "w16_update_kernel"));

@@ -108,6 +108,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Thread-block cluster (the fused head's CTA pair): barrier and a read of
+// the peer CTA's shared memory (distributed shared memory).
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ double ld_peer_f64(const double* local, uint32_t peer) {
+    uint32_t a = smem_u32(local), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(peer));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&v);
@@ -159,6 +177,7 @@ struct HeadScratch {
     float b1[W16_MAX_H];
     float w2[2][W16_MAX_H];
     double lg[W_EW][128][2];     // per column group: partial logits of the CTA's 128 rows
+    double own[128][2];          // the CTA's partial logits (its columns), read by the pair peer
     float d3[128][2];
     double wsum[4][3][W16_MAX_H];  // per lane quarter: column sums (gW2_0, gW2_1, gb1)
     double red[16][3];
@@ -188,12 +207,12 @@ template <int BN, int ST>
 size_t w16_gemm_smem_bytes() {
     size_t s = sizeof(W16Smem<BN, ST>);
     if (sizeof(EpiScratch) > s) s = sizeof(EpiScratch);
-    if (BN == W16_MAX_H && sizeof(HeadScratch) > s) s = sizeof(HeadScratch);
+    if (sizeof(HeadScratch) > s) s = sizeof(HeadScratch);
     return s + 1024;
 }
 template size_t w16_gemm_smem_bytes<64, 6>();
+template size_t w16_gemm_smem_bytes<128, 6>();
 template size_t w16_gemm_smem_bytes<256, 4>();
-template size_t w16_gemm_smem_bytes<512, 2>();
 
 // D[M x N] = A[M x K] . B[N x K]^T, bf16 operands, fp32 accumulation, epilogue EPI.
 // Grid (ceil(N/BN), ceil(M/128), splits). Warp 0 lane 0: TMA producer; warp 1
@@ -285,22 +304,24 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     __syncthreads();  // every warp is past the mainloop: stage buffers are free for scratch
 
     if constexpr (EPI == W16_EPI_HEAD) {
-        // ---- fused head (G2): BN = H covers full rows; the 4 column groups
-        //      of a row combine their partial logits through shared memory
+        // ---- fused head (G2). A CTA pair (thread-block cluster along x)
+        //      covers full rows: each CTA its BN columns; the partial logits
+        //      of its 4 column groups and of the pair combine in a fixed
+        //      order (column group, then CTA) through (distributed) shared memory
         HeadScratch& T = *reinterpret_cast<HeadScratch*>(base);
         const int H = g.N;
-        for (int c = tid; c < H; c += W_THREADS) {
+        for (int c = col0 + tid; c < min(H, col0 + BN); c += W_THREADS) {
             T.b1[c] = g.bias[c];
             T.w2[0][c] = g.w2[c];
             T.w2[1][c] = g.w2[H + c];
         }
         __syncthreads();
-        const int cend = min(H, cbeg + CW);
+        const int cb = col0 + cbeg, cend = min(H, cb + CW);
         // pass 1: h2 = relu(acc + b1); partial logits in fp64 (two chains per output)
         double l0a = 0.0, l0b = 0.0, l1a = 0.0, l1b = 0.0;
-        for (int c0 = cbeg; c0 < cend; c0 += 32) {
+        for (int c0 = cb; c0 < cend; c0 += 32) {
             float v[32];
-            tmem_ld32(tq + c0, v);
+            tmem_ld32(tq + (c0 - col0), v);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
@@ -314,17 +335,36 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         T.lg[cg][32 * qw + lane][0] = l0a + l0b;
         T.lg[cg][32 * qw + lane][1] = l1a + l1b;
         __syncthreads();
-        // softmax, KL with the reference clamps, d3 = p (ln(p^/t^) - L) / |b|
-        // (every column group of a row computes the same values)
-        double d30 = 0.0, d31 = 0.0, loss = 0.0;
-        if (row_ok) {
-            const int rl = 32 * qw + lane;
+        const int rl = 32 * qw + lane;
+        if (cg == 0) {
             double s0 = 0.0, s1 = 0.0;
 #pragma unroll
             for (int q = 0; q < W_EW; ++q) {
                 s0 += T.lg[q][rl][0];
                 s1 += T.lg[q][rl][1];
             }
+            T.own[rl][0] = s0;
+            T.own[rl][1] = s1;
+        }
+        const uint32_t crank = cluster_rank(), npair = (uint32_t)gridDim.x;  // 1 or 2 CTAs per row tile
+        if (npair > 1) cluster_sync();  // the peer's partial logits are written
+        else __syncthreads();
+        // softmax, KL with the reference clamps, d3 = p (ln(p^/t^) - L) / |b|
+        // (every column group of a row computes the same values)
+        double d30 = 0.0, d31 = 0.0, loss = 0.0;
+        {
+            double s0 = T.own[rl][0], s1 = T.own[rl][1];
+            if (npair > 1) {  // CTA 0's columns first
+                const double p0 = ld_peer_f64(&T.own[rl][0], crank ^ 1u), p1 = ld_peer_f64(&T.own[rl][1], crank ^ 1u);
+                if (crank == 0) {
+                    s0 += p0;
+                    s1 += p1;
+                } else {
+                    s0 = p0 + s0;
+                    s1 = p1 + s1;
+                }
+            }
+            if (row_ok) {
             const double z0 = (double)g.b2[0] + s0, z1 = (double)g.b2[1] + s1;
             const double m = z0 < z1 ? z1 : z0;
             const double e0 = exp(z0 - m), e1 = exp(z1 - m);
@@ -335,6 +375,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             loss = pc0 * lr0 + pc1 * lr1;
             d30 = p0 * (lr0 - loss) * g.inv_b;
             d31 = p1 * (lr1 - loss) * g.inv_b;
+            }
         }
         const float d3f0 = (float)d30, d3f1 = (float)d31;
         if (cg == 0) {
@@ -345,9 +386,9 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         // pass 2 (fp32): D2 = (d3 w2) [h2 > 0] -> D2 (row-major), D2^T (staged
         // transpose); column sums over the warp's 32 rows in fp32: lane l sums
         // column c0 + (l & 15) over rows 16 (l >> 4).. +16, halves added in order
-        for (int c0 = cbeg; c0 < cend; c0 += 16) {
+        for (int c0 = cb; c0 < cend; c0 += 16) {
             float v[16], d[16];
-            tmem_ld16(tq + c0, v);
+            tmem_ld16(tq + (c0 - col0), v);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -379,7 +420,8 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             __syncwarp();
         }
         // gb2 and KL of the rows (column group 0 only; fixed shuffle tree)
-        double r0 = cg == 0 ? d30 : 0.0, r1 = cg == 0 ? d31 : 0.0, r2 = cg == 0 ? loss : 0.0;
+        const bool first = cg == 0 && crank == 0;
+        double r0 = first ? d30 : 0.0, r1 = first ? d31 : 0.0, r2 = first ? loss : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             r0 += __shfl_xor_sync(0xffffffffu, r0, o);
@@ -394,9 +436,11 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         __syncthreads();
         double* prow = g.head_part + (size_t)blockIdx.y * (3 * H + 3);
         for (int q = 0; q < 3; ++q)
-            for (int c = tid; c < H; c += W_THREADS)
+            for (int c = col0 + tid; c < min(H, col0 + BN); c += W_THREADS)
                 prow[q * H + c] = ((T.wsum[0][q][c] + T.wsum[1][q][c]) + T.wsum[2][q][c]) + T.wsum[3][q][c];
-        if (tid < 3) prow[3 * H + tid] = ((T.red[0][tid] + T.red[1][tid]) + T.red[2][tid]) + T.red[3][tid];
+        if (tid < 3 && crank == 0)
+            prow[3 * H + tid] = ((T.red[0][tid] + T.red[1][tid]) + T.red[2][tid]) + T.red[3][tid];
+        if (npair > 1) cluster_sync();  // the peer has read this CTA's partial logits
     } else {
         EpiScratch& T = *reinterpret_cast<EpiScratch*>(base);
         for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
@@ -442,7 +486,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 
 template __global__ void w16_gemm_kernel<256, 4, W16_EPI_H1>(const __grid_constant__ CUtensorMap,
                                                              const __grid_constant__ CUtensorMap, W16Args);
-template __global__ void w16_gemm_kernel<512, 2, W16_EPI_HEAD>(const __grid_constant__ CUtensorMap,
+template __global__ void w16_gemm_kernel<256, 4, W16_EPI_HEAD>(const __grid_constant__ CUtensorMap,
                                                                const __grid_constant__ CUtensorMap, W16Args);
 template __global__ void w16_gemm_kernel<256, 4, W16_EPI_D1T>(const __grid_constant__ CUtensorMap,
                                                               const __grid_constant__ CUtensorMap, W16Args);
@@ -450,6 +494,8 @@ template __global__ void w16_gemm_kernel<256, 4, W16_EPI_PART>(const __grid_cons
                                                                const __grid_constant__ CUtensorMap, W16Args);
 template __global__ void w16_gemm_kernel<64, 6, W16_EPI_PART>(const __grid_constant__ CUtensorMap,
                                                               const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<128, 6, W16_EPI_PART>(const __grid_constant__ CUtensorMap,
+                                                               const __grid_constant__ CUtensorMap, W16Args);
 
 // Xg[r] = bf16(feat[rows[r]]) padded to 64 columns (G1's A); X^T [64][ldt]
 // with row 44 = 1 (G5's B: its column 44 of D1^T [X|1] is gb0).
@@ -560,43 +606,76 @@ __device__ __forceinline__ double w16_kl_sum(const W16UpdArgs& u) {
 
 // mode 0: reduce + SGD + refreshed bf16 copies (one rank); 1: reduce into the
 // flat gradient g_out and the loss sum (before an all-reduce); 2: SGD from g_out.
+// Block layout of the update grid: [0, nb0) 1-D over params [0, o_w1) (W0,
+// b0); then (H/16)^2 blocks of 16 x 16 W1 tiles (coalesced W1 and W1^T
+// writes through a shared-memory transpose); then 1-D over [o_b1, np).
+__host__ __device__ void w16_update_layout(int H, size_t np, int& nb0, int& nw1, int& nb2) {
+    const size_t o_w1 = (size_t)H * F + H, o_b1 = o_w1 + (size_t)H * H;
+    nb0 = (int)((o_w1 + 255) / 256);
+    nw1 = (H / 16) * (H / 16);
+    nb2 = (int)((np - o_b1 + 255) / 256);
+}
+
 __global__ void __launch_bounds__(256) w16_update_kernel(W16UpdArgs u, int mode) {
     __shared__ double s_loss;
+    __shared__ __nv_bfloat16 s_t[16][17];
     pdl_trigger();
     pdl_wait();
     if (*u.diverged >= 0) return;
-    const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int H = u.hidden;
+    const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H;
+    int nb0, nw1, nb2;
+    w16_update_layout(H, u.np, nb0, nw1, nb2);
+    const int bx = blockIdx.x, tid = threadIdx.x;
+    const bool tile = bx >= nb0 && bx < nb0 + nw1;
+    size_t p;
+    int tk = 0, tj = 0;
+    if (bx < nb0) {
+        p = (size_t)bx * 256 + tid;
+        if (p >= o_w1) p = u.np;  // (past W0 / b0: idle)
+    } else if (tile) {
+        const int t = bx - nb0, nt = H / 16;
+        tk = t / nt;
+        tj = t % nt;
+        p = o_w1 + (size_t)(tk * 16 + (tid >> 4)) * H + tj * 16 + (tid & 15);
+    } else {
+        p = o_b1 + (size_t)(bx - nb0 - nw1) * 256 + tid;
+    }
     if (mode == 1) {
-        if (blockIdx.x == 0 && threadIdx.x < 32) {
+        if (bx == 0 && tid < 32) {
             const double kl = w16_kl_sum(u);
-            if (threadIdx.x == 0) *u.loss_sum = kl;
+            if (tid == 0) *u.loss_sum = kl;
         }
         if (p < u.np) u.g_out[p] = (float)w16_grad(u, p);
         return;
     }
-    if (threadIdx.x < 32) {
+    if (tid < 32) {
         const double kl = mode == 2 ? *u.loss_sum : w16_kl_sum(u);
-        if (threadIdx.x == 0) s_loss = kl / (double)u.nb;
+        if (tid == 0) s_loss = kl / (double)u.nb;
     }
     __syncthreads();
     const double loss = s_loss;
     if (!isfinite(loss)) {  // fit throws before updating (policy.cpp:321-325)
-        if (p == 0) *u.diverged = *u.epoch;
+        if (bx == 0 && tid == 0) *u.diverged = *u.epoch;
         return;
     }
-    if (p == 0) *u.epoch_acc += loss * (double)u.nb;
-    if (p >= u.np) return;
-    const double gsum = mode == 2 ? (double)u.g_out[p] : w16_grad(u, p);
-    const float nw = __double2float_rn((double)u.params[p] - u.lr * gsum);
-    u.params[p] = nw;
-    const size_t H = u.hidden, o_b0 = H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + H * H;
-    const __nv_bfloat16 b = __float2bfloat16_rn(nw);
-    if (p < o_b0) {
-        u.w0p[(p / F) * 64 + p % F] = b;
-    } else if (p >= o_w1 && p < o_b1) {
-        const size_t t = p - o_w1, k = t / H, j = t % H;
-        u.w1[t] = b;
-        u.w1t[j * H + k] = b;
+    if (bx == 0 && tid == 0) *u.epoch_acc += loss * (double)u.nb;
+    if (p < u.np) {
+        const double gsum = mode == 2 ? (double)u.g_out[p] : w16_grad(u, p);
+        const float nw = __double2float_rn((double)u.params[p] - u.lr * gsum);
+        u.params[p] = nw;
+        const __nv_bfloat16 b = __float2bfloat16_rn(nw);
+        if (p < o_b0) {
+            u.w0p[(p / F) * 64 + p % F] = b;
+        } else if (tile) {
+            u.w1[p - o_w1] = b;
+            s_t[tid >> 4][tid & 15] = b;
+        }
+    }
+    if (tile) {  // W1^T[j][k]: 16 consecutive k per row of the tile
+        __syncthreads();
+        const int j = tid >> 4, k = tid & 15;
+        u.w1t[(size_t)(tj * 16 + j) * H + tk * 16 + k] = s_t[k][j];
     }
 }
 

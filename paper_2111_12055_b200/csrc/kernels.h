@@ -172,7 +172,7 @@ __global__ void wide_head_reduce_kernel(const double* part, int nblocks, int hid
                                         float* gb2, float* gb1, double* loss_out);
 
 // ---- wide MLP, BF16 tensor-core path (k_wide16.cu)
-constexpr int W16_MAX_H = 512;   // the fused head keeps a full row (<= 512 fp32 TMEM columns)
+constexpr int W16_MAX_H = 512;   // the fused head: a CTA pair (2 x 256 TMEM columns) covers a full row
 constexpr int W16_EPI_H1 = 0;    // relu(acc + bias) -> bf16 row-major + transposed
 constexpr int W16_EPI_HEAD = 1;  // fused softmax/KL head over full rows
 constexpr int W16_EPI_D1T = 2;   // acc [mask > 0] -> bf16 transposed
@@ -225,6 +225,7 @@ __global__ void w16_gather_kernel(const float* feat, const uint32_t* rows, int n
 __global__ void w16_weights_kernel(const float* params, int H, __nv_bfloat16* w0p, __nv_bfloat16* w1,
                                    __nv_bfloat16* w1t);
 __global__ void w16_update_kernel(W16UpdArgs u, int mode);
+__host__ __device__ void w16_update_layout(int H, size_t np, int& nb0, int& nw1, int& nb2);
 __global__ void to_bf16_kernel(const float* src, size_t n, __nv_bfloat16* dst);
 
 __global__ void tc_gemm_kernel(GemmArgs g);
