@@ -570,7 +570,7 @@ def main():
                     batch, 99, stream=dev.stream)
         torch.cuda.synchronize()
         secondary = run_secondary(args, dev, stream, p_inf, feat_d, torch, gbx, fp32_peak,
-                                  peaks, local)
+                                  dict(peaks, dfma_tflops=dfma_peak), local)
 
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
@@ -668,10 +668,21 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1)
         _, k_ms = dev.last_fit_timing()
-        out["batch_sweep"][str(b)] = {
+        row = {
             "value": feat_n / (ms * 1e-3), "unit": "samples/s", "ms_per_epoch": ms,
             "kernel": "train_epoch_kernel (fp64 exact, 1 CTA)" if b <= 32 else "train_epoch_tc_kernel",
             "tflops": feat_n * 23936 / (k_ms * 1e-3) / 1e12 if k_ms > 0 else None}
+        if b <= 32 and k_ms > 0:
+            # latency regime: a serial chain of n/32 dependent steps
+            # on ONE SM, so the roofline is per SM, not chip-wide: 11,968 MAC per
+            # record x 32 records at the SM's fp64 FMA rate (measured DFMA peak / 148)
+            steps = (feat_n + b - 1) // b
+            us = k_ms * 1e3 / steps
+            dfma = (peaks.get("dfma_tflops") or 34.1) * 1e12 / 2 / 148  # FMA/s per SM
+            bound_us = 11968 * b / dfma * 1e6
+            row.update({"us_per_step": us, "per_sm_bound_us": bound_us, "per_sm_frac": bound_us / us,
+                        "bound_note": "one SM; 11,968 fp64 MAC/record at the measured DFMA rate / 148 SMs"})
+        out["batch_sweep"][str(b)] = row
 
     # north-star variants on the fused kernel (absent from the reference): TD
     # regression of Q(x, a) on the reward + Adam, same log and batch as the headline
