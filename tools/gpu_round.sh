@@ -10,5 +10,5 @@ B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_step.csv $B --no-secondary > gpurun_out/ncu_launch_step.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:train_epoch -s 1 -c 1 -o gpurun_out/prof_train -f $B --no-secondary > gpurun_out/ncu_train.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fwd_fast|aggregate_kernel|tma_gemm|shuffle|qt_" -s 2 -c 8 -o gpurun_out/prof_other -f $B > gpurun_out/ncu_other.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fwd_fast|aggregate_kernel|w16_gemm|w16_update|qt_fold|qt_snapshot" -s 1 -c 10 -o gpurun_out/prof_other -f $B > gpurun_out/ncu_other.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; tail -c 600 gpurun_out/bench.log
