@@ -163,12 +163,15 @@ class ClockSampler:
         get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             N.nvmlDeviceGetCurrentClocksThrottleReasons
         masks = [(nm, getattr(N, attr, 0)) for nm, attr in self.REASONS]
-        while not self._stop.is_set():
+        while True:  # at least one sample, and one after the region ends
             self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
             r = get_r(h)
             for nm, m in masks:
                 if m and (r & m):
                     self.reasons.add(nm)
+            self._ready.set()
+            if self._stop.is_set():
+                break
             self._stop.wait(self.period)
 
     def _poll_smi(self):
@@ -187,7 +190,9 @@ class ClockSampler:
                 for nm, v in zip(names, f[2:6]):
                     if v.lower().startswith("active"):
                         self.reasons.add(nm)
+                self._ready.set()
             except (OSError, ValueError, IndexError, subprocess.SubprocessError):
+                self._ready.set()
                 return
 
     def _run(self):
@@ -202,12 +207,17 @@ class ClockSampler:
         except Exception:  # no NVML binding / library: nvidia-smi one-shots
             self.source = "nvidia-smi"
             self._poll_smi()
+        self._ready.set()
 
     def __enter__(self):
         import threading
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._th = threading.Thread(target=self._run, daemon=True)
         self._th.start()
+        # NVML start-up can outlast a short timed region: the region begins
+        # only once the sampler is polling (first sample taken)
+        self._ready.wait(timeout=10)
         return self
 
     def __exit__(self, *exc):
@@ -730,16 +740,10 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / reps
-    # split: the greedy inference alone over the same features (K2), the rest is K3
-    ev0.record(stream)
-    for _ in range(reps):
-        dev.forward_dev(pd.data_ptr(), feat.data_ptr(), nsh, None, a_d.data_ptr(), gbx.FWD_FAST,
-                        dev.stream)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms_fwd = ev0.elapsed_time(ev1) / reps
+    # split of the last evaluate into its inference (K2) and aggregation (K3)
+    # launches, CUDA events recorded inside gbxcu_evaluate_dev on its stream
+    ms_fwd, ms_agg = dev.last_eval_timing()
     del feat
-    ms_agg = max(ms - ms_fwd, 1e-6)
     # K3 algorithmic bytes: per slot the shader index, fraction, latents (3 f64)
     # and action (37 B), per app its 5-double row (the 8-B fraction re-read of
     # each pipeline's A segment is not counted)

@@ -76,6 +76,10 @@ uint64_t gbxcu_launch_count(const gbxcu_ctx* ctx);
  * fit with <= 8 epochs: epoch-permutation replay and train_epoch kernel,
  * summed over epochs (0 for the data-parallel path). */
 int gbxcu_last_fit_timing(const gbxcu_ctx* ctx, double* shuffle_ms, double* train_kernel_ms);
+/* Device time (CUDA events on the call's stream) of the last gbxcu_evaluate[_dev]
+ * on this context: the inference (fast forward + exact re-check) and the
+ * per-app aggregation (frame_time / run_benchmark rows). Waits for that call. */
+int gbxcu_last_eval_timing(gbxcu_ctx* ctx, double* infer_ms, double* aggregate_ms);
 /* States the last FAST-mode gbxcu_forward[_dev] on this context sent to the
  * exact fp64 re-check (guard margin inside the fp32 error bound). Synchronises
  * the device. */

@@ -110,7 +110,7 @@ EXPORTS = (
     "gbxcu_suite_free", "gbxcu_suite_features", "gbxcu_evaluate", "gbxcu_evaluate_dev",
     "gbxcu_wide_param_count", "gbxcu_wide_init", "gbxcu_wide_forward", "gbxcu_wide_fit",
     "gbxcu_wide_fit_dev", "gbxcu_wide_fit_ex", "gbxcu_wide_fit_ex_dev", "gbxcu_tf32_gemm",
-    "gbxcu_bf16_gemm", "gbxcu_last_fit_timing", "gbxcu_last_recheck_count", "gbxcu_peer_export",
+    "gbxcu_bf16_gemm", "gbxcu_last_fit_timing", "gbxcu_last_eval_timing", "gbxcu_last_recheck_count", "gbxcu_peer_export",
     "gbxcu_peer_attach", "gbxcu_peer_detach", "gbxcu_qtable_create", "gbxcu_qtable_free", "gbxcu_qtable_clear",
     "gbxcu_qtable_update_batch", "gbxcu_qtable_update_batch_dev", "gbxcu_qtable_size",
     "gbxcu_forward_batch", "gbxcu_sample_batch", "gbxcu_evaluate_shard",
@@ -199,6 +199,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.gbxcu_wide_fit_ex_dev.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _sz, C.POINTER(TrainCfg), _vp,
                                         C.POINTER(C.c_int), _vp]
     L.gbxcu_last_fit_timing.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.gbxcu_last_eval_timing.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.gbxcu_last_recheck_count.argtypes = [_vp, C.POINTER(C.c_uint64)]
     _LIB = L
     return L
@@ -294,6 +295,12 @@ class Device:
         """(shuffle_ms, train_kernel_ms) of the last single-GPU fit (CUDA events)."""
         a, b = C.c_double(), C.c_double()
         self._ck(self.L.gbxcu_last_fit_timing(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def last_eval_timing(self):
+        """(inference_ms, aggregate_ms) of the last evaluate on this context (CUDA events)."""
+        a, b = C.c_double(), C.c_double()
+        self._ck(self.L.gbxcu_last_eval_timing(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
     def last_recheck_count(self) -> int:

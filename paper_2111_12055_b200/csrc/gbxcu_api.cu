@@ -104,6 +104,7 @@ struct gbxcu_ctx {
     cudaEvent_t side_ev = nullptr;
     uint64_t launches = 0;
     cudaEvent_t ev[24] = {};                 // fit's per-kernel timing events
+    cudaEvent_t eval_ev[3] = {};             // evaluate: before inference | before aggregation | after
     unsigned long long* hres = nullptr;      // pinned host scratch for fit's small results
     double last_shuffle_ms = 0, last_train_ms = 0;
     std::mutex mu;
@@ -633,6 +634,7 @@ int gbxcu_create(int device, gbxcu_ctx** out) {
                                                   fast_smem_bytes());
     c->fast_per_sm = std::max(1, per_sm);
     for (auto& e : c->ev) cudaEventCreate(&e);
+    for (auto& e : c->eval_ev) cudaEventCreate(&e);
     {  // keep freed stream-ordered allocations in the pool (reused, not returned)
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -652,6 +654,8 @@ void gbxcu_destroy(gbxcu_ctx* c) {
     if (c->comm) ncclCommDestroy(c->comm);
     for (auto& p : c->peer_ptr)
         if (p) cudaIpcCloseMemHandle(p);
+    for (auto& e : c->eval_ev)
+        if (e) cudaEventDestroy(e);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& g : c->wg)
@@ -670,6 +674,19 @@ int gbxcu_last_fit_timing(const gbxcu_ctx* c, double* shuffle_ms, double* train_
     if (!c) return fail(GBXCU_EINVAL, "null context");
     if (shuffle_ms) *shuffle_ms = c->last_shuffle_ms;
     if (train_kernel_ms) *train_kernel_ms = c->last_train_ms;
+    return GBXCU_OK;
+}
+
+int gbxcu_last_eval_timing(gbxcu_ctx* c, double* infer_ms, double* aggregate_ms) {
+    if (!c) return fail(GBXCU_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    CK(cudaEventSynchronize(c->eval_ev[2]));
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, c->eval_ev[0], c->eval_ev[1]));
+    CK(cudaEventElapsedTime(&b, c->eval_ev[1], c->eval_ev[2]));
+    if (infer_ms) *infer_ms = a;
+    if (aggregate_ms) *aggregate_ms = b;
     return GBXCU_OK;
 }
 
@@ -1560,9 +1577,14 @@ static int evaluate_dev(gbxcu_ctx* c, const gbxcu_dsuite* s, const float* d_para
                         int n_samples, uint64_t seed, uint8_t* d_actions, double* d_rows,
                         cudaStream_t st, DevBuf& recheck, DevBuf& counters, DevBuf& flags) {
     if (n_samples < 1) return fail(GBXCU_EINVAL, "sample count must be >= 1");
+    CK(cudaEventRecord(c->eval_ev[0], st));
     RET(run_forward(c, d_params, s->features.as<float>(), s->n_shaders, nullptr, d_actions,
                     GBXCU_FWD_FAST, nullptr, 0, nullptr, 0.0, st, recheck, counters, flags));
-    if (s->n_apps == 0) return GBXCU_OK;
+    CK(cudaEventRecord(c->eval_ev[1], st));
+    if (s->n_apps == 0) {
+        CK(cudaEventRecord(c->eval_ev[2], st));
+        return GBXCU_OK;
+    }
     AggArgs a{};
     a.n_apps = s->n_apps;
     a.app_pipe_off = s->app_pipe.as<uint64_t>();
@@ -1578,7 +1600,9 @@ static int evaluate_dev(gbxcu_ctx* c, const gbxcu_dsuite* s, const float* d_para
     a.n_samples = n_samples;
     a.rows = d_rows;
     a.samples = nullptr;
-    return launch_aggregate(c, a, st);
+    RET(launch_aggregate(c, a, st));
+    CK(cudaEventRecord(c->eval_ev[2], st));
+    return GBXCU_OK;
 }
 
 // One app-range shard of evaluate (aggregation shards by app so
