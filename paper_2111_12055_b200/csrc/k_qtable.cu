@@ -119,6 +119,28 @@ __global__ void qt_gather_digit_kernel(RecView v, const uint32_t* __restrict__ p
     }
 }
 
+// Words [w_from, KW) of two keys equal? Both 120-byte rows are read with all
+// fifteen 8-byte loads in flight at once (an early-exit word loop issues one
+// dependent round trip per word).
+__device__ __forceinline__ bool key_tail_equal(const uint32_t* a, const uint32_t* b, int w_from) {
+    const uint2* a2 = reinterpret_cast<const uint2*>(a);
+    const uint2* b2 = reinterpret_cast<const uint2*>(b);
+    uint2 x[KW / 2], y[KW / 2];
+#pragma unroll
+    for (int q = 0; q < KW / 2; ++q) {
+        x[q] = __ldg(a2 + q);
+        y[q] = __ldg(b2 + q);
+    }
+    bool same = true;
+#pragma unroll
+    for (int q = 0; q < KW / 2; ++q) {
+        if (2 * q >= w_from) same &= x[q].x == y[q].x;
+        if (2 * q + 1 >= w_from) same &= x[q].y == y[q].y;
+    }
+    return same;
+}
+static_assert(KW % 2 == 0, "keys are read as 8-byte pairs");
+
 // MSD fast path: segment heads straight from the sorted top digits, plus the
 // check that makes them valid — neighbours with equal digits must have equal
 // keys (words w_from.. beyond the digit; none when w_from == KW), else the
@@ -135,11 +157,7 @@ __global__ void qt_msd_heads_kernel(RecView v, const uint32_t* __restrict__ perm
             if (digit[i] == digit[i - 1]) {
                 kh = 0;
                 if (w_from < KW) {
-                    const uint32_t* a = v.key(r);
-                    const uint32_t* b = v.key(r0);
-                    bool same = true;
-                    for (int w = w_from; w < KW && same; ++w) same = a[w] == b[w];
-                    if (!same) {
+                    if (!key_tail_equal(v.key(r), v.key(r0), w_from)) {
                         atomicOr(unresolved, 1u);
                         kh = 1;
                     }
@@ -158,11 +176,7 @@ __global__ void qt_heads_kernel(RecView v, const uint32_t* __restrict__ perm, si
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec; i += (size_t)gridDim.x * blockDim.x) {
         uint32_t kh = 1, sh = 1;
         if (i > 0) {
-            const uint32_t* a = v.key(perm[i]);
-            const uint32_t* b = v.key(perm[i - 1]);
-            bool same = true;
-            for (int w = 0; w < KW && same; ++w) same = a[w] == b[w];
-            kh = same ? 0u : 1u;
+            kh = key_tail_equal(v.key(perm[i]), v.key(perm[i - 1]), 0) ? 0u : 1u;
             sh = kh | (v.action(perm[i]) != v.action(perm[i - 1]) ? 1u : 0u);
         }
         seg_head[i] = sh;
