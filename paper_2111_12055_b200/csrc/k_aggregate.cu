@@ -169,8 +169,11 @@ __global__ void __launch_bounds__(AGG_BLOCK, MINB) aggregate_kernel(AggArgs a) {
             for (int j = 0; j < K; ++j) {
                 const double thr = __shfl_sync(0xffffffffu, thr_me, j);
                 const double throttle = __shfl_sync(0xffffffffu, L.throttle, j);
-                double x = 0.0, y = 0.0;
+                // (-0.0 pads the chunk: x + (-0.0) == x for every x, so the
+                //  folds below need no per-slot predicate)
+                double x = -0.0, y = -0.0;
                 if (lane < (info[j] & 0xFF)) {
+                    x = 0.0;
                     if ((info[j] >> 8 & 3) == 0) {
                         y = -fr[j];  // inner - p == inner + (-p) exactly
                     } else {
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(AGG_BLOCK, MINB) aggregate_kernel(AggArgs a) {
                                                            __dsub_rn(1.0, __dmul_rn(0.5, ld[j])))
                                                : 1.0;
                         if (lb[j] > thr) sp = __dmul_rn(sp, throttle);
-                        y = __ddiv_rn(fr[j], sp);
+                        y = sp == 1.0 ? fr[j] : __ddiv_rn(fr[j], sp);  // (p / 1 == p exactly)
                     }
                 }
                 buf[wib][j][lane] = make_double2(x, y);
@@ -192,11 +195,9 @@ __global__ void __launch_bounds__(AGG_BLOCK, MINB) aggregate_kernel(AggArgs a) {
             if (lane < K) {
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    if (k < cnt_me) {
-                        const double2 t = buf[wib][lane][k];
-                        L.load = __dadd_rn(L.load, t.x);
-                        L.inner = __dadd_rn(L.inner, t.y);
-                    }
+                    const double2 t = buf[wib][lane][k];
+                    L.load = __dadd_rn(L.load, t.x);
+                    L.inner = __dadd_rn(L.inner, t.y);
                 }
                 L.pos += cnt_me;
                 agg_advance(a, L);
