@@ -289,6 +289,17 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         }
         commit_to(&S.done);
     }
+    // (the head's targets: a gather through the record indices, issued while
+    //  the MMAs run)
+    double tg0 = 0.0, tg1 = 0.0;
+    if constexpr (EPI == W16_EPI_HEAD) {
+        const int rr = row0 + 32 * (w & 3) + (tid & 31);
+        if (rr < g.M) {
+            const size_t rec = g.rows ? g.rows[rr] : (size_t)rr;
+            tg0 = g.tgt[2 * rec];
+            tg1 = g.tgt[2 * rec + 1];
+        }
+    }
     __syncwarp();
     if (nk > 0) mbar_wait_b(&S.done, 0);
     fence_after_sync();
@@ -369,9 +380,8 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             const double m = z0 < z1 ? z1 : z0;
             const double e0 = exp(z0 - m), e1 = exp(z1 - m);
             const double p0 = e0 / (e0 + e1), p1 = e1 / (e0 + e1);
-            const size_t rec = g.rows ? g.rows[row] : (size_t)row;
             const double pc0 = clampp(p0), pc1 = clampp(p1);
-            const double lr0 = log(pc0 / clampp(g.tgt[2 * rec])), lr1 = log(pc1 / clampp(g.tgt[2 * rec + 1]));
+            const double lr0 = log(pc0 / clampp(tg0)), lr1 = log(pc1 / clampp(tg1));
             loss = pc0 * lr0 + pc1 * lr1;
             d30 = p0 * (lr0 - loss) * g.inv_b;
             d31 = p1 * (lr1 - loss) * g.inv_b;
