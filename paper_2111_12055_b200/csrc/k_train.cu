@@ -82,6 +82,7 @@ struct TrainSmem {
     double d3[TB * 2];
     double tgt[TB * 2];
     double kl[TB];
+    uint32_t ord[2][TB];        // record indices of the next two tiles (cp.async ring)
     double stage_t[2][TB * 2];  // cp.async staging: targets
     float stage_f[2][TB * F];   // cp.async staging: raw fp32 features
     double scal[4];             // [1] batch loss, [2] diverged flag
@@ -303,6 +304,33 @@ __device__ void prefetch_tile(TrainSmem<TB>& S, int buf, const TrainArgs& a, siz
     cp_async_commit();
 }
 
+// Epoch kernel ring: record indices of a tile two ahead, then its rows one
+// ahead through the indices already in shared memory (the row gather issues
+// without a dependent global load on the step's critical path).
+template <int TB>
+__device__ __forceinline__ void fetch_idx(TrainSmem<TB>& S, int slot, const TrainArgs& a, size_t r0, int nv) {
+    if ((int)threadIdx.x < nv) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(&S.ord[slot][threadIdx.x]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(a.order + r0 + threadIdx.x)
+                     : "memory");
+    }
+}
+template <int TB>
+__device__ __forceinline__ void fetch_rows(TrainSmem<TB>& S, int slot, const TrainArgs& a, int nv) {
+    for (int t = threadIdx.x; t < TB * (F / 4); t += NT) {
+        const int r = t / (F / 4), q = t - r * (F / 4);
+        const float* src = a.feat;
+        if (r < nv) src = a.feat + (size_t)S.ord[slot][r] * F + 4 * q;
+        cp_async16(&S.stage_f[slot][r * F + 4 * q], src, r < nv ? 16 : 0);
+    }
+    if (threadIdx.x < TB) {
+        const int r = threadIdx.x;
+        const double* src = a.tgt;
+        if (r < nv) src = a.tgt + 2 * (size_t)S.ord[slot][r];
+        cp_async16(&S.stage_t[slot][2 * r], src, r < nv ? 16 : 0);
+    }
+}
+
 // One tile: rows [0, nv) of the staged buffer `buf`; accumulates into g.
 template <int TB>
 __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, double inv_b) {
@@ -461,6 +489,9 @@ __device__ void train_tile(TrainSmem<TB>& S, GradRegs& g, int buf, int nv, doubl
             for (int r = 0; r < nv; ++r) g.gx = __dadd_rn(g.gx, S.d3[2 * r + a]);
         } else if (tid == NT - 1) {
             for (int r = 0; r < nv; ++r) g.loss = __dadd_rn(g.loss, S.kl[r]);
+            // divergence flag of the step so far (loss = sum / |b| is finite iff
+            // the sum is): read after the tile's closing barrier
+            S.scal[2] = isfinite(g.loss) ? 0.0 : 1.0;
         }
     }
     __syncthreads();
@@ -518,55 +549,63 @@ __global__ void __launch_bounds__(NT, 1) train_epoch_kernel(TrainArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
 
-    // first tile's records in flight while the weights load
-    long pf_step = 0;
-    size_t pf_r0 = (size_t)-1;
-    int pf_nv = 0;
-    bool have_next = next_tile<TB>(a, n_steps, pf_step, pf_r0, pf_nv);
-    int buf = 0;
-    if (have_next) prefetch_tile<TB>(S, buf, a, pf_r0, pf_nv);
+    // Ring (tile k): rows of tile k in stage[k & 1] (fetched during tile
+    // k - 1), indices of tile k + 1 in ord[(k + 1) & 1]. Cursors: c1 = tile
+    // k + 1, c2 = tile k + 2.
+    long s1 = 0, s2 = 0;
+    size_t r1 = (size_t)-1, r2 = 0;
+    int n1 = 0, n2 = 0;
+    bool h1 = next_tile<TB>(a, n_steps, s1, r1, n1);  // tile 0
+    if (h1) fetch_idx(S, 0, a, r1, n1);
+    s2 = s1;
+    r2 = r1;
+    bool h2 = h1 && next_tile<TB>(a, n_steps, s2, r2, n2);  // tile 1
+    if (h2) fetch_idx(S, 1, a, r2, n2);
+    cp_async_commit();
     load_train_weights(S, a.params, false);
+    cp_async_wait_all();
+    __syncthreads();
+    if (h1) fetch_rows(S, 0, a, n1);
+    cp_async_commit();
+    h1 = h2; s1 = s2; r1 = r2; n1 = n2;  // c1 <- tile 1, c2 <- tile 2
+    s2 = s1; r2 = r1;
+    h2 = h1 && next_tile<TB>(a, n_steps, s2, r2, n2);
     GradRegs g;
     zero_grads(g);
-    double epoch_total = 0.0;
-    __syncthreads();
+    double epoch_total = 0.0;  // thread NT - 1 (it holds the loss sums)
+    int k = 0;
 
     for (long step = 0; step < n_steps; ++step) {
         size_t lo, hi, nb;
         step_slice(a, step, 0, 1, lo, hi, nb);
         const double inv_b = 1.0 / (double)nb;  // batch_kl_gradient's 1/|b| (global batch)
-        for (size_t r0 = lo; r0 < hi; r0 += TB) {
+        for (size_t r0 = lo; r0 < hi; r0 += TB, ++k) {
             const int nv = (int)min((size_t)TB, hi - r0);
             PHASE_MARK(6);
-            cp_async_wait_all();
+            cp_async_wait_all();  // this thread's copies: tile k's rows, tile k+1's indices
             __syncthreads();
-            const int cur = buf;
-            buf ^= 1;
-            // queue the following tile (this step or a later one)
-            have_next = next_tile<TB>(a, n_steps, pf_step, pf_r0, pf_nv);
-            if (have_next) prefetch_tile<TB>(S, buf, a, pf_r0, pf_nv);
+            if (h1) fetch_rows(S, (k + 1) & 1, a, n1);  // rows of tile k+1
+            if (h2) fetch_idx(S, k & 1, a, r2, n2);     // indices of tile k+2
+            cp_async_commit();
+            h1 = h2; s1 = s2; r1 = r2; n1 = n2;
+            if (h2) h2 = next_tile<TB>(a, n_steps, s2, r2, n2);
             PHASE_MARK(7);
-            train_tile<TB>(S, g, cur, nv, inv_b);
+            train_tile<TB>(S, g, k & 1, nv, inv_b);
         }
-        // loss = (sum of per-record KL, batch order) / |b|  (policy.cpp:194-201)
-        if (tid == NT - 1) {
-            const double loss = __ddiv_rn(g.loss, (double)nb);
-            S.scal[1] = loss;
-            S.scal[2] = isfinite(loss) ? 0.0 : 1.0;
-        }
-        __syncthreads();
+        // loss = (sum of per-record KL, batch order) / |b|  (policy.cpp:194-201);
+        // its finiteness was flagged in B2, before the tile's closing barrier
         if (S.scal[2] != 0.0) {
             if (tid == 0) *a.diverged_epoch = a.epoch;
             break;
         }
-        if (tid == 0) epoch_total = madd_rn(epoch_total, S.scal[1], (double)nb);
+        if (tid == NT - 1) epoch_total = madd_rn(epoch_total, __ddiv_rn(g.loss, (double)nb), (double)nb);
         sgd_update_owned(S, g, a.lr);
         zero_grads(g);
         __syncthreads();
     }
     cp_async_wait_all();
     // epoch loss = total / n (policy.cpp:334); params back to global
-    if (tid == 0 && *a.diverged_epoch < 0)
+    if (tid == NT - 1 && *a.diverged_epoch < 0)
         a.epoch_loss[a.epoch] = __ddiv_rn(epoch_total, (double)a.n);
     __syncthreads();
     for (int t = tid; t < NP; t += NT) a.params[t] = (float)get_smem_param(S, t);
