@@ -184,6 +184,7 @@ int setup_kernel_attrs() {
         set((const void*)fwd_recheck_kernel, recheck_smem_bytes());
         set((const void*)train_epoch_kernel<32>, train_smem_bytes(32));
         set((const void*)train_epoch_kernel<64>, train_smem_bytes(64));
+        set((const void*)train_epoch_cluster_kernel, train_cl_smem_bytes());
         set((const void*)train_partial_kernel<32>, train_smem_bytes(32));
         set((const void*)train_partial_kernel<64>, train_smem_bytes(64));
         set((const void*)batch_grad_kernel, train_smem_bytes(64));
@@ -482,10 +483,18 @@ int fit_device(gbxcu_ctx* c, float* d_params, const float* d_feat, const double*
             void* args[] = {&a};
             if (timed) CK(cudaEventRecord(c->ev[(2 * e + 1) % 16], st));
             if (!fused) {
-                // 1-CTA steps: the bit-exact fp64 kernel (reference summation order)
-                const void* fn = tb == 32 ? (const void*)train_epoch_kernel<32>
-                                          : (const void*)train_epoch_kernel<64>;
-                CK(cudaLaunchKernel(fn, 1, TRAIN_BLOCK, args, train_smem_bytes(tb), st));
+                // 1-CTA steps: the bit-exact fp64 kernel (reference summation
+                // order); batches <= 32 on one rank spread each step over a
+                // cluster of CTAs (same chains, same order)
+                static const bool one_cta = getenv("GBX_TRAIN32_1CTA") != nullptr;  // (A/B timing)
+                if (tb == 32 && c->nranks == 1 && !one_cta) {
+                    CK(cudaLaunchKernel((const void*)train_epoch_cluster_kernel, TRAIN_CLUSTER, TRAIN_BLOCK,
+                                        args, train_cl_smem_bytes(), st));
+                } else {
+                    const void* fn = tb == 32 ? (const void*)train_epoch_kernel<32>
+                                              : (const void*)train_epoch_kernel<64>;
+                    CK(cudaLaunchKernel(fn, 1, TRAIN_BLOCK, args, train_smem_bytes(tb), st));
+                }
             } else {
                 // system-scope exchange only across GPUs (a real peer set)
                 const bool sys = c->peers > 1;

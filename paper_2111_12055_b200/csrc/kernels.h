@@ -103,6 +103,10 @@ size_t recheck_smem_bytes();
 
 template <int TB>
 __global__ void train_epoch_kernel(TrainArgs a);
+// batch <= 32 on one rank: the same bit-exact step on a TRAIN_CLUSTER-CTA cluster (k_train_cl.cu)
+constexpr int TRAIN_CLUSTER = 4;
+__global__ void train_epoch_cluster_kernel(TrainArgs a);
+size_t train_cl_smem_bytes();
 template <int TB>
 __global__ void train_partial_kernel(TrainArgs a, long step);
 template <int MT, bool SYS, bool VAR>
