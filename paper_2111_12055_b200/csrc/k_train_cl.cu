@@ -19,12 +19,12 @@
 //   F2  h2[:, K_c]                       -> cluster barrier, gather h2 (24 cols)
 //   F3  logits / softmax / KL / d3 (all records, redundantly in every CTA)
 //   B1  d2[:, K_c]                       -> cluster barrier, gather d2 (24 cols)
-//   B2  d1[:, J_c]                       -> cluster barrier (W1 copies free)
+//   B2  d1[:, J_c]
 //   G   the gradient chains of the parameters CTA c owns (W0/b0 rows J_c,
 //       W1/b1 rows K_c, W2 columns K_c, b2 on CTA 0, the loss everywhere)
 //   SGD on the owned parameters; updated W1 / W2 / b2 entries pushed into the
-//       other CTAs' copies (ordered before their use by the next step's
-//       first cluster barrier).
+//       other buffer of every CTA's (double-buffered) copies, ordered before
+//       their use by the next step's first cluster barrier.
 // Every CTA computes the identical loss, so all agree on divergence.
 #include <cstddef>
 
@@ -32,6 +32,22 @@
 #include "kernels.h"
 
 namespace gbxcu {
+
+#ifdef GBX_PHASE_TIMING
+// Debug build only (tools/phase_timing.sh): per-phase cycle totals of CTA 0, thread 0.
+__device__ unsigned long long g_cl_phase[16];
+__device__ unsigned long long g_cl_t;
+#define CL_MARK(i)                                                                             \
+    do {                                                                                       \
+        if (threadIdx.x == 0 && blockIdx.x == 0) {                                             \
+            const unsigned long long t_ = clock64();                                           \
+            if ((i) >= 0) g_cl_phase[(i) < 0 ? 0 : (i)] += t_ - g_cl_t;                        \
+            g_cl_t = t_;                                                                       \
+        }                                                                                      \
+    } while (0)
+#else
+#define CL_MARK(i) ((void)0)
+#endif
 
 namespace {
 
@@ -57,10 +73,10 @@ struct ClSmem {
     double w0[J1 * W0S];   // own rows of W0: [jj][i]
     double b0[J1];
     double w1r[K2 * W1S];  // own rows of W1: [kk][j] (F2)
-    double w1c[H2 * WCS];  // columns J_c of W1: [k][jj] (B2)
+    double w1c[2][H2 * WCS];  // columns J_c of W1: [k][jj] (B2), double-buffered by step
     double b1[K2];
-    double w2[A * H2];     // all of W2 (F3, B1)
-    double b2[A];
+    double w2[2][A * H2];  // all of W2 (F3, B1), double-buffered by step
+    double b2[2][A];
     double x[TBR * XS];
     double h1[TBR * HS1];  // all 64 columns (own computed, the rest gathered)
     double h2[TBR * HS2];  // all 32
@@ -70,6 +86,7 @@ struct ClSmem {
     double tgt[TBR * 2];
     double kl[TBR];
     double flag;           // 1: the step's loss sum is not finite
+    double zero, one;      // operands of the G phase's dummy / bias chains
     uint32_t ord[2][TBR];  // record indices of the next two tiles (cp.async ring)
     alignas(16) double stage_t[2][TBR * 2];  // (16-byte cp.async destinations)
     alignas(16) float stage_f[2][TBR * F];
@@ -91,6 +108,8 @@ __device__ __forceinline__ uint32_t cl_addr(const void* local, uint32_t rank) {
                  : "r"((uint32_t)__cvta_generic_to_shared(local)), "r"(rank));
     return ra;
 }
+// (volatile + memory clobber: never moved across the cluster barriers; a
+//  gather issues all its loads before their first use, so they overlap)
 __device__ __forceinline__ double cl_ld(const double* local, uint32_t rank) {
     double v;
     asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(cl_addr(local, rank)) : "memory");
@@ -188,11 +207,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
     }
     for (int t = tid; t < H2 * J1; t += NTC) {
         const int k = t / J1, jj = t - k * J1;
-        S.w1c[k * WCS + jj] = (double)a.params[OFF_W1 + k * H1 + c * J1 + jj];
+        S.w1c[0][k * WCS + jj] = (double)a.params[OFF_W1 + k * H1 + c * J1 + jj];
     }
     if (tid < K2) S.b1[tid] = (double)a.params[OFF_B1 + c * K2 + tid];
-    if (tid < A * H2) S.w2[tid] = (double)a.params[OFF_W2 + tid];
-    if (tid < A) S.b2[tid] = (double)a.params[OFF_B2 + tid];
+    if (tid < A * H2) S.w2[0][tid] = (double)a.params[OFF_W2 + tid];
+    if (tid < A) S.b2[0][tid] = (double)a.params[OFF_B2 + tid];
+    if (tid == 0) {
+        S.zero = 0.0;
+        S.one = 1.0;
+    }
     cp_wait();
     __syncthreads();
     if (h1) cl_fetch_rows(S, 0, a, n1);
@@ -205,7 +228,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
 #pragma unroll
     for (int m = 0; m < QPT; ++m) g[m] = 0.0;
     double epoch_total = 0.0;  // CTA 0, the thread holding the loss chain
+    int wb = 0;                // buffer of the W1-column / W2 / b2 copies the next step reads
     cl_sync();                 // every CTA of the cluster is running before any DSMEM access
+    CL_MARK(-1);
 
     for (long step = 0; step < n_steps; ++step) {
         const int k = (int)(step & 1);
@@ -221,6 +246,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
         h1 = h2; s1 = s2; r1 = r2; n1 = n2;
         if (h2) h2 = cl_next(a, n_steps, s2, r2, n2);
 
+        CL_MARK(0);  // step top (wait, prefetch issue)
         // ---- P0: staged fp32 -> fp64
         for (int t = tid; t < TBR * F; t += NTC) {
             const int r = t / F;
@@ -229,49 +255,73 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
         if (tid < 2 * TBR) S.tgt[tid] = S.stage_t[k][tid];
         __syncthreads();
 
+        CL_MARK(1);  // P0
         // ---- F1: h1[r][16c + jj] = relu(b0 + sum_i w0[j][i] x[r][i]), DFMA chain over i
         {
             const int r = tid >> 4, jj = tid & 15;
             double acc = S.b0[jj];
             const double* wr = S.w0 + jj * W0S;
             const double* xr = S.x + r * XS;
-#pragma unroll 4
+#pragma unroll
             for (int i = 0; i < F; ++i) acc = fma(wr[i], xr[i], acc);  // fp32 x fp32 exact in fp64
             S.h1[r * HS1 + c * J1 + jj] = acc > 0.0 ? acc : 0.0;
         }
+        CL_MARK(2);  // F1
         cl_sync();
+        CL_MARK(3);  // barrier 1
         // gather the other CTAs' h1 columns (32 records x 48 units)
-        for (int t = tid; t < TBR * (H1 - J1); t += NTC) {
-            const int r = t / (H1 - J1), q = t - r * (H1 - J1);
-            const int j = q < c * J1 ? q : q + J1;  // skip the own block
-            S.h1[r * HS1 + j] = cl_ld(&S.h1[r * HS1 + j], (uint32_t)(j / J1));
+        {
+            constexpr int NG = TBR * (H1 - J1) / NTC;  // 3 per thread, all in flight
+            double v[NG];
+            int at[NG];
+#pragma unroll
+            for (int u = 0; u < NG; ++u) {
+                const int t = tid + u * NTC, r = t / (H1 - J1), q = t - r * (H1 - J1);
+                const int j = q < c * J1 ? q : q + J1;  // skip the own block
+                at[u] = r * HS1 + j;
+                v[u] = cl_ld(&S.h1[at[u]], (uint32_t)(j / J1));
+            }
+#pragma unroll
+            for (int u = 0; u < NG; ++u) S.h1[at[u]] = v[u];
         }
         __syncthreads();
 
+        CL_MARK(4);  // gather h1
         // ---- F2: h2[r][8c + kk] = relu(b1 + sum_j w1[k][j] h1[r][j]), mul-then-add
         if (tid < TBR * K2) {
             const int r = tid >> 3, kk = tid & 7;
             double acc = S.b1[kk];
             const double* wr = S.w1r + kk * W1S;
             const double* hr = S.h1 + r * HS1;
-#pragma unroll 4
+#pragma unroll 16
             for (int j = 0; j < H1; ++j) acc = madd_rn(acc, wr[j], hr[j]);
             S.h2[r * HS2 + c * K2 + kk] = acc > 0.0 ? acc : 0.0;
         }
         cl_sync();
-        for (int t = tid; t < TBR * (H2 - K2); t += NTC) {
-            const int r = t / (H2 - K2), q = t - r * (H2 - K2);
-            const int kx = q < c * K2 ? q : q + K2;
-            S.h2[r * HS2 + kx] = cl_ld(&S.h2[r * HS2 + kx], (uint32_t)(kx / K2));
+        {
+            constexpr int NG = (TBR * (H2 - K2) + NTC - 1) / NTC;  // 2 per thread
+            double v[NG];
+            int at[NG];
+#pragma unroll
+            for (int u = 0; u < NG; ++u) {
+                const int t = tid + u * NTC, r = t / (H2 - K2), q = t - r * (H2 - K2);
+                const int kx = q < c * K2 ? q : q + K2;
+                at[u] = t < TBR * (H2 - K2) ? r * HS2 + kx : -1;
+                if (at[u] >= 0) v[u] = cl_ld(&S.h2[at[u]], (uint32_t)(kx / K2));
+            }
+#pragma unroll
+            for (int u = 0; u < NG; ++u)
+                if (at[u] >= 0) S.h2[at[u]] = v[u];
         }
         __syncthreads();
 
+        CL_MARK(5);  // F2 + barrier 2 + gather h2
         // ---- F3 (all records, identical in every CTA) + B1 (own columns)
         if (tid < 2 * TBR) {
             const int r = tid >> 1, a2 = tid & 1;
-            double l = S.b2[a2];
+            double l = S.b2[wb][a2];
             const double* h = S.h2 + r * HS2;
-            const double* wr = S.w2 + a2 * H2;
+            const double* wr = S.w2[wb] + a2 * H2;
 #pragma unroll 8
             for (int kx = 0; kx < H2; ++kx) l = madd_rn(l, wr[kx], h[kx]);
             const double lo = __shfl_xor_sync(0xffffffffu, l, 1);
@@ -298,66 +348,97 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
 #pragma unroll
             for (int q = 0; q < K2 / 2; ++q) {
                 const int kx = c * K2 + (K2 / 2) * a2 + q;
-                double d = madd_rn(0.0, d30, S.w2[kx]);
-                d = madd_rn(d, d31, S.w2[H2 + kx]);
+                double d = madd_rn(0.0, d30, S.w2[wb][kx]);
+                d = madd_rn(d, d31, S.w2[wb][H2 + kx]);
                 S.d2[r * HS2 + kx] = h[kx] <= 0.0 ? 0.0 : d;
             }
         }
         cl_sync();
-        for (int t = tid; t < TBR * (H2 - K2); t += NTC) {
-            const int r = t / (H2 - K2), q = t - r * (H2 - K2);
-            const int kx = q < c * K2 ? q : q + K2;
-            S.d2[r * HS2 + kx] = cl_ld(&S.d2[r * HS2 + kx], (uint32_t)(kx / K2));
+        {
+            constexpr int NG = (TBR * (H2 - K2) + NTC - 1) / NTC;
+            double v[NG];
+            int at[NG];
+#pragma unroll
+            for (int u = 0; u < NG; ++u) {
+                const int t = tid + u * NTC, r = t / (H2 - K2), q = t - r * (H2 - K2);
+                const int kx = q < c * K2 ? q : q + K2;
+                at[u] = t < TBR * (H2 - K2) ? r * HS2 + kx : -1;
+                if (at[u] >= 0) v[u] = cl_ld(&S.d2[at[u]], (uint32_t)(kx / K2));
+            }
+#pragma unroll
+            for (int u = 0; u < NG; ++u)
+                if (at[u] >= 0) S.d2[at[u]] = v[u];
         }
         __syncthreads();
 
+        CL_MARK(6);  // F3 + B1 + barrier 3 + gather d2
         // ---- B2: d1[r][jj] = sum_k d2[r][k] w1[k][16c + jj], masked by h1 > 0
         {
             const int r = tid >> 4, jj = tid & 15;
             double acc = 0.0;
             const double* dr = S.d2 + r * HS2;
-#pragma unroll 4
-            for (int kx = 0; kx < H2; ++kx) acc = madd_rn(acc, dr[kx], S.w1c[kx * WCS + jj]);
+#pragma unroll
+            for (int kx = 0; kx < H2; ++kx) acc = madd_rn(acc, dr[kx], S.w1c[wb][kx * WCS + jj]);
             S.d1[r * DS1 + jj] = S.h1[r * HS1 + c * J1 + jj] <= 0.0 ? 0.0 : acc;
         }
-        cl_sync();  // every CTA is done reading its W1 / W2 copies: the pushes below may land
-        // (d1 above is CTA-local: the cluster barrier also orders it for this CTA)
+        __syncthreads();
+        // (no cluster barrier: the SGD below writes the OTHER copy buffer, which
+        //  every CTA last read a step ago — before this step's first barrier)
 
-        // ---- G: the owned parameters' gradient chains, records in batch order
+        CL_MARK(7);  // B2
+        // ---- G: the owned parameters' gradient chains, records in batch order,
+        //      the thread's (up to 3) chains interleaved. Every chain is
+        //      acc = acc + (A[r] * B[r]) with B = 1.0 for the bias / loss sums
+        //      (a * 1.0 == a exactly, so this IS acc + a). All 32 rows: a padding
+        //      row's d1 / d2 / d3 / kl are +0, which leave every accumulator
+        //      unchanged (they start at +0 and can never become -0).
+        {
+            const double* pa[QPT];
+            const double* pb[QPT];
+            int sa[QPT], sb[QPT];
 #pragma unroll
-        for (int m = 0; m < QPT; ++m) {
-            const int q = tid + m * NTC;
-            if (q >= NQ) continue;
-            double acc = g[m];
-            if (q < Q_B0) {
-                const int jj = q / F, i = q - jj * F;
-                for (int r = 0; r < nv; ++r) acc = madd_rn(acc, S.d1[r * DS1 + jj], S.x[r * XS + i]);
-            } else if (q < Q_W1) {
-                const int jj = q - Q_B0;
-                for (int r = 0; r < nv; ++r) acc = __dadd_rn(acc, S.d1[r * DS1 + jj]);
-            } else if (q < Q_B1) {
-                const int kk = (q - Q_W1) / H1, j = (q - Q_W1) % H1;
-                for (int r = 0; r < nv; ++r) acc = madd_rn(acc, S.d2[r * HS2 + c * K2 + kk], S.h1[r * HS1 + j]);
-            } else if (q < Q_W2) {
-                const int kk = q - Q_B1;
-                for (int r = 0; r < nv; ++r) acc = __dadd_rn(acc, S.d2[r * HS2 + c * K2 + kk]);
-            } else if (q < Q_B2) {
-                const int a2 = (q - Q_W2) / K2, kk = (q - Q_W2) % K2;
-                for (int r = 0; r < nv; ++r) acc = madd_rn(acc, S.d3[2 * r + a2], S.h2[r * HS2 + c * K2 + kk]);
-            } else if (q < Q_LOSS) {
-                if (c == 0)
-                    for (int r = 0; r < nv; ++r) acc = __dadd_rn(acc, S.d3[2 * r + (q - Q_B2)]);
-            } else {
-                for (int r = 0; r < nv; ++r) acc = __dadd_rn(acc, S.kl[r]);
-                S.flag = isfinite(acc) ? 0.0 : 1.0;  // loss = sum / |b| is finite iff the sum is
+            for (int m = 0; m < QPT; ++m) {
+                const int q = tid + m * NTC;
+                pa[m] = &S.zero;  // (not owned here: a dummy chain of zeros)
+                pb[m] = &S.one;
+                sa[m] = sb[m] = 0;
+                if (q < Q_B0) {
+                    const int jj = q / F, i = q - jj * F;
+                    pa[m] = S.d1 + jj; sa[m] = DS1;
+                    pb[m] = S.x + i; sb[m] = XS;
+                } else if (q < Q_W1) {
+                    pa[m] = S.d1 + (q - Q_B0); sa[m] = DS1;
+                } else if (q < Q_B1) {
+                    const int kk = (q - Q_W1) / H1, j = (q - Q_W1) % H1;
+                    pa[m] = S.d2 + c * K2 + kk; sa[m] = HS2;
+                    pb[m] = S.h1 + j; sb[m] = HS1;
+                } else if (q < Q_W2) {
+                    pa[m] = S.d2 + c * K2 + (q - Q_B1); sa[m] = HS2;
+                } else if (q < Q_B2) {
+                    const int a2 = (q - Q_W2) / K2, kk = (q - Q_W2) % K2;
+                    pa[m] = S.d3 + a2; sa[m] = 2;
+                    pb[m] = S.h2 + c * K2 + kk; sb[m] = HS2;
+                } else if (q < Q_LOSS) {
+                    if (c == 0) { pa[m] = S.d3 + (q - Q_B2); sa[m] = 2; }
+                } else if (q == Q_LOSS) {
+                    pa[m] = S.kl; sa[m] = 1;
+                }
             }
-            g[m] = acc;
+#pragma unroll
+            for (int r = 0; r < TBR; ++r) {
+#pragma unroll
+                for (int m = 0; m < QPT; ++m) g[m] = madd_rn(g[m], pa[m][r * sa[m]], pb[m][r * sb[m]]);
+            }
+#pragma unroll
+            for (int m = 0; m < QPT; ++m)
+                if (tid + m * NTC == Q_LOSS) S.flag = isfinite(g[m]) ? 0.0 : 1.0;  // loss finite iff the sum is
         }
         __syncthreads();
         if (S.flag != 0.0) {  // identical on every CTA: all leave at the same step
             if (c == 0 && tid == 0) *a.diverged_epoch = a.epoch;
             break;
         }
+        CL_MARK(8);  // G + flag
         // ---- SGD on the owned parameters, new W1 / W2 / b2 entries into every copy
 #pragma unroll
         for (int m = 0; m < QPT; ++m) {
@@ -374,9 +455,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
                 const int kk = (q - Q_W1) / H1, j = (q - Q_W1) % H1;
                 const double w = cl_sgd(S.w1r[kk * W1S + j], a.lr, g[m]);
                 S.w1r[kk * W1S + j] = w;
-                // column copy of the CTA owning unit j (B2 there)
+                // next step's column copy of the CTA owning unit j (B2 there)
                 const uint32_t oc = (uint32_t)(j / J1);
-                double* dst = &S.w1c[(c * K2 + kk) * WCS + (j - (int)oc * J1)];
+                double* dst = &S.w1c[wb ^ 1][(c * K2 + kk) * WCS + (j - (int)oc * J1)];
                 if ((int)oc == c) *dst = w;
                 else cl_st(dst, oc, w);
             } else if (q < Q_W2) {
@@ -384,17 +465,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
             } else if (q < Q_B2) {
                 const int a2 = (q - Q_W2) / K2, kk = (q - Q_W2) % K2;
                 const int idx = a2 * H2 + c * K2 + kk;
-                const double w = cl_sgd(S.w2[idx], a.lr, g[m]);
-                S.w2[idx] = w;
-                for (int o = 1; o < CL; ++o) cl_st(&S.w2[idx], (uint32_t)((c + o) % CL), w);
+                const double w = cl_sgd(S.w2[wb][idx], a.lr, g[m]);
+                S.w2[wb ^ 1][idx] = w;
+                for (int o = 1; o < CL; ++o) cl_st(&S.w2[wb ^ 1][idx], (uint32_t)((c + o) % CL), w);
             } else if (c == 0) {
                 const int a2 = q - Q_B2;
-                const double w = cl_sgd(S.b2[a2], a.lr, g[m]);
-                S.b2[a2] = w;
-                for (int o = 1; o < CL; ++o) cl_st(&S.b2[a2], (uint32_t)o, w);
+                const double w = cl_sgd(S.b2[wb][a2], a.lr, g[m]);
+                S.b2[wb ^ 1][a2] = w;
+                for (int o = 1; o < CL; ++o) cl_st(&S.b2[wb ^ 1][a2], (uint32_t)o, w);
             }
             g[m] = 0.0;
         }
+        wb ^= 1;
+        CL_MARK(9);  // SGD + pushes
         // (the next step's first cluster barrier orders the pushes before
         //  F3 / B2 read them; this CTA's own updates before its next F1 / F2
         //  by the step-top barrier)
@@ -412,10 +495,21 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
         else if (q < Q_W1) v = S.b0[q - Q_B0];
         else if (q < Q_B1) v = S.w1r[((q - Q_W1) / H1) * W1S + (q - Q_W1) % H1];
         else if (q < Q_W2) v = S.b1[q - Q_B1];
-        else if (q < Q_B2) v = S.w2[((q - Q_W2) / K2) * H2 + c * K2 + (q - Q_W2) % K2];
-        else v = S.b2[q - Q_B2];
+        else if (q < Q_B2) v = S.w2[wb][((q - Q_W2) / K2) * H2 + c * K2 + (q - Q_W2) % K2];
+        else v = S.b2[wb][q - Q_B2];
         a.params[p] = (float)v;
     }
 }
 
 }  // namespace gbxcu
+
+#ifdef GBX_PHASE_TIMING
+extern "C" int gbxcu_debug_phase_cycles_cl(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, gbxcu::g_cl_phase, sizeof(unsigned long long) * 16) != cudaSuccess) return 3;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(gbxcu::g_cl_phase, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
