@@ -680,7 +680,7 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
         _, k_ms = dev.last_fit_timing()
         row = {
             "value": feat_n / (ms * 1e-3), "unit": "samples/s", "ms_per_epoch": ms,
-            "kernel": "train_epoch_kernel (fp64 exact, 1 CTA)" if b <= 32 else "train_epoch_tc_kernel",
+            "kernel": "train_epoch_cluster_kernel (fp64 exact, 4-CTA cluster)" if b <= 32 else "train_epoch_tc_kernel",
             "tflops": feat_n * 23936 / (k_ms * 1e-3) / 1e12 if k_ms > 0 else None}
         if b <= 32 and k_ms > 0:
             # latency regime: a serial chain of n/32 dependent steps
@@ -691,7 +691,9 @@ def run_secondary(args, dev, stream, params_d, feat_d, torch, gbx, fp32_peak, pe
             dfma = (peaks.get("dfma_tflops") or 34.1) * 1e12 / 2 / 148  # FMA/s per SM
             bound_us = 11968 * b / dfma * 1e6
             row.update({"us_per_step": us, "per_sm_bound_us": bound_us, "per_sm_frac": bound_us / us,
-                        "bound_note": "one SM; 11,968 fp64 MAC/record at the measured DFMA rate / 148 SMs"})
+                        "bound_note": "one SM's throughput: 11,968 fp64 MAC/record at the measured DFMA "
+                                      "rate / 148 SMs (the step now runs on a 4-CTA cluster, latency-bound: "
+                                      "a ~270-deep dependent fp64 chain + 3 cluster barriers per step)"})
         out["batch_sweep"][str(b)] = row
 
     # north-star variants on the fused kernel (absent from the reference): TD
