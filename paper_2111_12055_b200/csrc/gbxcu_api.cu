@@ -1943,16 +1943,36 @@ bool make_bf16_map(CUtensorMap* m, const void* base, int K, int rows, int ld, in
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// D = A B^T on the bf16 kernel: A [M][lda] (K valid), B [N][ldb]; grid (N/BN, M/128, splits)
+// bf16 epilogue output [rows][ld] (cols valid) as TMA store boxes of
+// {box_cols, box_rows}, no swizzle; stores past cols / rows are clipped.
+bool make_bf16_store_map(CUtensorMap* m, const void* base, int cols, int rows, int ld, int box_cols,
+                         int box_rows) {
+    const EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// D = A B^T on the bf16 kernel: A [M][lda] (K valid), B [N][ldb]; grid (N/BN, M/128, splits).
+// Epilogue outputs through TMA stores: g.out [M][g.ldo] row-major and g.out_t
+// [N][g.ldt] transposed (each when non-null), in 32-row x 16-column chunks.
 template <int BN, int ST, int EPI>
 int launch_w16(gbxcu_ctx* c, const void* A, int lda, const void* B, int ldb, const W16Args& g, int splits,
                cudaStream_t st, int cluster_x = 1) {
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mo{}, mot{};
     if (!make_bf16_map(&ma, A, g.K, g.M, lda, 128) || !make_bf16_map(&mb, B, g.K, g.N, ldb, BN > 256 ? 256 : BN))
         return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled unavailable or rejected a bf16 operand");
+    if ((g.out && !make_bf16_store_map(&mo, g.out, g.N, g.M, g.ldo, 16, 32)) ||
+        (g.out_t && !make_bf16_store_map(&mot, g.out_t, g.M, g.N, g.ldt, 32, 16)))
+        return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled rejected a bf16 epilogue output");
     dim3 grid((g.N + BN - 1) / BN, (g.M + 127) / 128, splits);
     return launch_pdl_cl(c, "w16_gemm_kernel", w16_gemm_kernel<BN, ST, EPI>, grid, dim3(512),
-                         w16_gemm_smem_bytes<BN, ST>(), st, cluster_x, ma, mb, g);
+                         w16_gemm_smem_bytes<BN, ST>(), st, cluster_x, ma, mb, mo, mot, g);
 }
 
 int check_hidden16(int H) {
@@ -2001,8 +2021,17 @@ int w16_alloc(gbxcu_ctx* c, const W16Plan& P) {
 }
 
 // One SGD step on rows[0, nbr) (this rank's slice of a global batch of nb), BF16 path.
+// timeline slot base of the step being enqueued (GBX_PHASE_TIMING builds)
+int g_w16_dbg_step = -1;
+
 int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const double* tgt,
              const uint32_t* rows, int nbr, size_t nb, double lr, const int* epoch, cudaStream_t st) {
+#ifdef GBX_PHASE_TIMING
+    const int dbg = g_w16_dbg_step >= 0 && g_w16_dbg_step < 8 ? 8 * g_w16_dbg_step : -100;
+#else
+    const int dbg = -100;
+#endif
+    auto slot = [&](int k) { return dbg >= 0 ? dbg + k : -1; };
     const int H = P.H, ldt = (int)P.ldt;
     const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H, o_w2 = o_b1 + H;
     using bf = __nv_bfloat16;
@@ -2013,29 +2042,35 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
     u.g_out = c->w_grad.as<float>(); u.loss_sum = c->w_loss.as<double>();
     u.w0p = c->b_w0p.as<bf>(); u.w1 = c->b_w1.as<bf>(); u.w1t = c->b_w1t.as<bf>();
     u.epoch = epoch; u.diverged = c->diverged.as<int>(); u.epoch_acc = c->epoch_acc.as<double>();
+    u.dbg = slot(6);
     if (nbr > 0) {
-        RET(launch_pdl(c, "w16_gather_kernel", w16_gather_kernel, dim3(blocks(nbr)), dim3(256), 0, st, feat,
-                       rows, nbr, c->b_xg.as<bf>(), c->b_xt.as<bf>(), ldt));
-        W16Args g1{};  // H1 = relu(Xg W0^T + b0) -> H1, H1^T
+        RET(launch_pdl(c, "w16_gather_kernel", w16_gather_kernel, dim3((nbr + 63) / 64), dim3(256), 0, st, feat,
+                       rows, nbr, slot(0), c->b_xg.as<bf>(), c->b_xt.as<bf>(), ldt));
+        W16Args g1{};
+        g1.dbg = slot(1);  // H1 = relu(Xg W0^T + b0) -> H1, H1^T
         g1.M = nbr; g1.N = H; g1.K = 64; g1.bias = Pm + o_b0;
         g1.out = c->b_h1.as<bf>(); g1.ldo = H; g1.out_t = c->b_h1t.as<bf>(); g1.ldt = ldt;
         RET((launch_w16<256, 4, W16_EPI_H1>(c, c->b_xg.p, 64, c->b_w0p.p, 64, g1, 1, st)));
-        W16Args g2{};  // acc = H1 W1^T -> fused head -> D2, D2^T, head partials
+        W16Args g2{};
+        g2.dbg = slot(2);  // acc = H1 W1^T -> fused head -> D2, D2^T, head partials
         g2.M = nbr; g2.N = H; g2.K = H; g2.bias = Pm + o_b1;
         g2.out = c->b_d2.as<bf>(); g2.ldo = H; g2.out_t = c->b_d2t.as<bf>(); g2.ldt = ldt;
         g2.w2 = Pm + o_w2; g2.b2 = Pm + o_w2 + 2 * H; g2.tgt = tgt; g2.rows = rows;
         g2.inv_b = 1.0 / (double)nb; g2.head_part = c->b_hp.as<double>();
         // a CTA pair (cluster along x) per 128-row tile covers the full rows
         RET((launch_w16<256, 4, W16_EPI_HEAD>(c, c->b_h1.p, H, c->b_w1.p, H, g2, 1, st, (H + 255) / 256)));
-        W16Args g3{};  // D1 = (D2 W1) [H1 > 0] -> D1^T
+        W16Args g3{};
+        g3.dbg = slot(3);  // D1 = (D2 W1) [H1 > 0] -> D1^T
         g3.M = nbr; g3.N = H; g3.K = H; g3.mask = c->b_h1.as<bf>(); g3.ldm = H;
         g3.out_t = c->b_d1t.as<bf>(); g3.ldt = ldt;
         RET((launch_w16<256, 4, W16_EPI_D1T>(c, c->b_d2.p, H, c->b_w1t.p, H, g3, 1, st)));
-        W16Args g4{};  // gW1 = D2^T H1 (split-K partials)
+        W16Args g4{};
+        g4.dbg = slot(4);  // gW1 = D2^T H1 (split-K partials)
         g4.M = H; g4.N = H; g4.K = nbr; g4.part = c->b_p4.as<float>(); g4.ldp = H;
         g4.split_stride = (size_t)H * H;
         RET((launch_w16<128, 6, W16_EPI_PART>(c, c->b_d2t.p, ldt, c->b_h1t.p, ldt, g4, P.s4, st)));
-        W16Args g5{};  // gW0 | gb0 = D1^T [X | 1] (split-K partials)
+        W16Args g5{};
+        g5.dbg = slot(5);  // gW0 | gb0 = D1^T [X | 1] (split-K partials)
         g5.M = H; g5.N = 64; g5.K = nbr; g5.part = c->b_p5.as<float>(); g5.ldp = 64;
         g5.split_stride = (size_t)H * 64;
         RET((launch_w16<64, 6, W16_EPI_PART>(c, c->b_d1t.p, ldt, c->b_xt.p, ldt, g5, P.s5, st)));
@@ -2083,6 +2118,7 @@ int w16_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, co
             const size_t nb = std::min(n, start + (size_t)cfg->batch_size) - start;
             const size_t per = (nb + c->nranks - 1) / c->nranks;
             const size_t lo = std::min(nb, (size_t)c->rank * per), hi = std::min(nb, lo + per);
+            g_w16_dbg_step = (int)s;
             RET(w16_step(c, P, d_params, d_feat, d_tgt, order + start + lo, (int)(hi - lo), nb,
                          cfg->learning_rate, c->w_epoch.as<int>(), st));
         }
@@ -2394,6 +2430,7 @@ int gbxcu_bf16_gemm(gbxcu_ctx* c, int M, int N, int K, const float* A, const flo
     to_bf16_kernel<<<blocks(b.size()), 256, 0, st>>>(c->w_h2.as<float>(), b.size(), c->b_d2.as<__nv_bfloat16>());
     RET(check_launch(c, "to_bf16_kernel"));
     W16Args g{};
+    g.dbg = -1;
     g.M = M; g.N = N; g.K = K; g.part = c->w_d2.as<float>(); g.ldp = np; g.split_stride = 0;
     RET((launch_w16<256, 4, W16_EPI_PART>(c, c->b_h1.p, ka, c->b_d2.p, ka, g, 1, st)));
     std::vector<float> out((size_t)M * np);

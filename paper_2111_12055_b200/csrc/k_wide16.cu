@@ -37,6 +37,27 @@ namespace gbxcu {
 
 using namespace tc;
 
+#ifdef GBX_PHASE_TIMING
+// Debug build only (tools/phase_timing.sh): per-launch timeline of the first
+// eight steps of a fit — slot = step * 8 + launch (0 gather, 1..5 G1..G5,
+// 6 update); points 0 entry, 1 inputs ready (after griddepcontrol.wait),
+// 2 main loop done, 3 exit; {min, max} over the CTAs (globaltimer ns).
+__device__ unsigned long long g_w16_tr[64][4][2];
+#define W16_TR(slot, pt)                                                          \
+    do {                                                                          \
+        if ((slot) >= 0 && threadIdx.x == 0) {                                    \
+            unsigned long long t_;                                                \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                \
+            atomicMin(&g_w16_tr[slot][pt][0], t_);                                \
+            atomicMax(&g_w16_tr[slot][pt][1], t_);                                \
+        }                                                                         \
+    } while (0)
+#else
+#define W16_TR(slot, pt) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace {
 
 constexpr int W_BM = 128;  // rows per CTA tile (TMEM lanes)
@@ -87,6 +108,20 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
         : "memory");
 }
 
+// TMA tensor store shared -> global (bulk-group completion), issued by one thread.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(c0),
+                 "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most one committed group still reading its shared-memory source
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+// every committed group complete (writes performed)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the TMA (async proxy)
+__device__ __forceinline__ void fence_proxy_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // Warp-collective: 32 consecutive fp32 columns of this warp's 32 TMEM lanes.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
@@ -130,15 +165,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&v);
 }
-__device__ __forceinline__ void store_row16(__nv_bfloat16* dst, const float* h) {
-    uint4 q0, q1;
-    q0.x = pack_bf16(h[0], h[1]); q0.y = pack_bf16(h[2], h[3]);
-    q0.z = pack_bf16(h[4], h[5]); q0.w = pack_bf16(h[6], h[7]);
-    q1.x = pack_bf16(h[8], h[9]); q1.y = pack_bf16(h[10], h[11]);
-    q1.z = pack_bf16(h[12], h[13]); q1.w = pack_bf16(h[14], h[15]);
-    reinterpret_cast<uint4*>(dst)[0] = q0;
-    reinterpret_cast<uint4*>(dst)[1] = q1;
-}
 __device__ __forceinline__ void load_row16(const __nv_bfloat16* src, float (&m)[16]) {
     const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(src));
     const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
@@ -166,48 +192,84 @@ __host__ __device__ constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn 
 constexpr int W_EW = 4;                // epilogue warps per TMEM lane quarter
 constexpr int W_THREADS = 128 * W_EW;  // 16 warps: warp w reads lanes 32 (w % 4).., columns group w / 4
 
-// Epilogue scratch (re-uses the drained stage buffers): per warp one 32-row x
-// 16-column chunk for the transposed stores / column sums
-struct EpiScratch {
-    float t[16][32][17];
+// Epilogue output staging (per warp, double-buffered over its 16-column
+// chunks): the chunk's 32 rows x 16 columns in bf16, row-major ([32][16], one
+// 32-byte row per lane) and transposed ([16][32], a 64-byte row per column),
+// written to global memory by two TMA tensor stores (full 32-byte sectors,
+// no per-lane address streams).
+struct OutStage {
+    __nv_bfloat16 rm[2][32 * 16];
+    __nv_bfloat16 tr[2][16 * 32];
 };
+constexpr size_t OUT_STAGE_BYTES = 16 * sizeof(OutStage);
 struct HeadScratch {
-    float t[16][32][17];         // per warp: h2 of its 32 rows x 16 columns
-    float d[16][32][17];         // per warp: D2 of the same chunk
     float b1[W16_MAX_H];
     float w2[2][W16_MAX_H];
+    double w2d[2][W16_MAX_H];    // w2 widened once (the logits accumulate in fp64)
     double lg[W_EW][128][2];     // per column group: partial logits of the CTA's 128 rows
     double own[128][2];          // the CTA's partial logits (its columns), read by the pair peer
-    float d3[128][2];
     double wsum[4][3][W16_MAX_H];  // per lane quarter: column sums (gW2_0, gW2_1, gb1)
     double red[16][3];
 };
 
-// Transposed bf16 store of a warp's 32 rows x 16 columns (tile t[r][c]):
-// dst[(c0 + c) * ldt + r0 + r]; lane = (column c = lane / 2, rows 16 (lane & 1)..+16)
-// as two 16-byte stores instead of sixteen 2-byte ones per thread.
-__device__ __forceinline__ void store_t16(const float (&t)[32][17], __nv_bfloat16* dst, size_t ldt, int c0,
-                                          int r0, int nrows, int ncols, int lane) {
-    const int c = lane >> 1, rh = (lane & 1) * 16;
-    if (c >= ncols) return;
-    __nv_bfloat16* o = dst + (size_t)(c0 + c) * ldt + r0 + rh;
-    if (rh + 16 <= nrows) {
-        float h[16];
+// Column sums of a warp's 32 rows: v[16] = this lane's (row's) values of 16
+// columns; returns, in lanes l and l ^ 16, the sum over the 32 lanes of
+// column l & 15 (recursive halving over lane bits 3..0, then bit 4: a fixed
+// tree, 16 shuffles instead of a shared-memory round trip per row).
+__device__ __forceinline__ float col_reduce16(float (&v)[16], int lane) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) h[i] = t[rh + i][c];
-        store_row16(o, h);
-    } else {
-        for (int i = 0; rh + i < nrows; ++i) o[i] = __float2bfloat16_rn(t[rh + i][c]);
+    for (int b = 3, n = 8; b >= 0; --b, n >>= 1) {
+        const bool hi = (lane >> b) & 1;
+#pragma unroll
+        for (int j = 0; j < n; ++j) {
+            const float send = hi ? v[j] : v[j + n], keep = hi ? v[j + n] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << b);
+        }
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+// One 16-column chunk of a warp's output (lane = row): stage it in bf16 and
+// issue its TMA stores (row-major at (col, row0), transposed at (row0, col);
+// RM / TR select which). Buffer k & 1 is reused two chunks later, after its
+// previous stores have read it. Rows past M are clipped by the tensor maps.
+template <bool RM, bool TR>
+__device__ __forceinline__ void stage_chunk(OutStage& o, int k, const float (&h)[16], const CUtensorMap* map_o,
+                                            const CUtensorMap* map_ot, int col, int row0, int lane) {
+    const int b = k & 1;
+    if (k >= 2) {
+        if (lane == 0) bulk_wait_read1();
+        __syncwarp();
+    }
+    if constexpr (RM) {
+        uint4* q = reinterpret_cast<uint4*>(o.rm[b] + lane * 16);
+        q[0] = make_uint4(pack_bf16(h[0], h[1]), pack_bf16(h[2], h[3]), pack_bf16(h[4], h[5]), pack_bf16(h[6], h[7]));
+        q[1] = make_uint4(pack_bf16(h[8], h[9]), pack_bf16(h[10], h[11]), pack_bf16(h[12], h[13]),
+                          pack_bf16(h[14], h[15]));
+    }
+    if constexpr (TR) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o.tr[b][i * 32 + lane] = __float2bfloat16_rn(h[i]);
+    }
+    fence_proxy_smem();
+    __syncwarp();
+    if (lane == 0) {
+        if constexpr (RM) tma_store_2d(map_o, o.rm[b], col, row0);
+        if constexpr (TR) tma_store_2d(map_ot, o.tr[b], row0, col);
+        bulk_commit();
     }
 }
 
 }  // namespace
 
+// the head keeps its scratch; its output staging follows it
+__host__ __device__ constexpr size_t head_stage_off() { return (sizeof(HeadScratch) + 1023) & ~(size_t)1023; }
+
 template <int BN, int ST>
 size_t w16_gemm_smem_bytes() {
     size_t s = sizeof(W16Smem<BN, ST>);
-    if (sizeof(EpiScratch) > s) s = sizeof(EpiScratch);
-    if (sizeof(HeadScratch) > s) s = sizeof(HeadScratch);
+    if (OUT_STAGE_BYTES > s) s = OUT_STAGE_BYTES;
+    if (head_stage_off() + OUT_STAGE_BYTES > s) s = head_stage_off() + OUT_STAGE_BYTES;
     return s + 1024;
 }
 template size_t w16_gemm_smem_bytes<64, 6>();
@@ -221,7 +283,7 @@ template size_t w16_gemm_smem_bytes<256, 4>();
 template <int BN, int ST, int EPI>
 __global__ void __launch_bounds__(W_THREADS, 1)
 w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                W16Args g) {
+                const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_ot, W16Args g) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -237,6 +299,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const int kb_lo = blockIdx.z * per, kb_hi = min(nkb, kb_lo + per);
     const int nk = max(0, kb_hi - kb_lo);
 
+    W16_TR(g.dbg, 0);
     if (w == 0) tmem_alloc(&S.tmem, TC);
     if (tid == 32) {
         for (int s = 0; s < ST; ++s) {
@@ -254,10 +317,15 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     //  the previous kernel's results comes after its completion)
     pdl_trigger();
     pdl_wait();
+    W16_TR(g.dbg, 1);
 
     if (tid == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+        if constexpr (EPI != W16_EPI_PART) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_o) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_ot) : "memory");
+        }
         constexpr uint32_t bytes = (W_BM + BN) * W_BK * 2;
         for (int it = 0; it < nk; ++it) {
             const int slot = it % ST;
@@ -303,12 +371,12 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     __syncwarp();
     if (nk > 0) mbar_wait_b(&S.done, 0);
     fence_after_sync();
+    W16_TR(g.dbg, 2);
 
     const int qw = w & 3, cg = w >> 2;        // lane quarter, column group
     const int rw0 = row0 + 32 * qw;             // first row of this warp
     const int row = rw0 + lane;
     const bool row_ok = row < g.M;
-    const int nrows = max(0, min(32, g.M - rw0));
     const uint32_t tq = tacc + ((uint32_t)(32 * qw) << 16);
     constexpr int CW = BN / W_EW;               // columns per group
     const int cbeg = cg * CW;
@@ -320,11 +388,14 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         //      of its 4 column groups and of the pair combine in a fixed
         //      order (column group, then CTA) through (distributed) shared memory
         HeadScratch& T = *reinterpret_cast<HeadScratch*>(base);
+        OutStage& O = reinterpret_cast<OutStage*>(base + head_stage_off())[w];
         const int H = g.N;
         for (int c = col0 + tid; c < min(H, col0 + BN); c += W_THREADS) {
             T.b1[c] = g.bias[c];
             T.w2[0][c] = g.w2[c];
             T.w2[1][c] = g.w2[H + c];
+            T.w2d[0][c] = (double)g.w2[c];
+            T.w2d[1][c] = (double)g.w2[H + c];
         }
         __syncthreads();
         const int cb = col0 + cbeg, cend = min(H, cb + CW);
@@ -335,12 +406,22 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             tmem_ld32(tq + (c0 - col0), v);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-                const float ha = fmaxf(v[i] + T.b1[c0 + i], 0.f), hb = fmaxf(v[i + 1] + T.b1[c0 + i + 1], 0.f);
-                l0a = fma((double)ha, (double)T.w2[0][c0 + i], l0a);
-                l1a = fma((double)ha, (double)T.w2[1][c0 + i], l1a);
-                l0b = fma((double)hb, (double)T.w2[0][c0 + i + 1], l0b);
-                l1b = fma((double)hb, (double)T.w2[1][c0 + i + 1], l1b);
+            for (int i = 0; i < 32; i += 4) {
+                const float4 bb = *reinterpret_cast<const float4*>(&T.b1[c0 + i]);
+                const double2 w0a = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i]);
+                const double2 w0b = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i + 2]);
+                const double2 w1a = *reinterpret_cast<const double2*>(&T.w2d[1][c0 + i]);
+                const double2 w1b = *reinterpret_cast<const double2*>(&T.w2d[1][c0 + i + 2]);
+                const float h0 = fmaxf(v[i] + bb.x, 0.f), h1 = fmaxf(v[i + 1] + bb.y, 0.f);
+                const float h2 = fmaxf(v[i + 2] + bb.z, 0.f), h3 = fmaxf(v[i + 3] + bb.w, 0.f);
+                l0a = fma((double)h0, w0a.x, l0a);
+                l1a = fma((double)h0, w1a.x, l1a);
+                l0b = fma((double)h1, w0a.y, l0b);
+                l1b = fma((double)h1, w1a.y, l1b);
+                l0a = fma((double)h2, w0b.x, l0a);
+                l1a = fma((double)h2, w1b.x, l1a);
+                l0b = fma((double)h3, w0b.y, l0b);
+                l1b = fma((double)h3, w1b.y, l1b);
             }
         }
         T.lg[cg][32 * qw + lane][0] = l0a + l0b;
@@ -388,46 +469,39 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             }
         }
         const float d3f0 = (float)d30, d3f1 = (float)d31;
-        if (cg == 0) {
-            T.d3[32 * qw + lane][0] = d3f0;
-            T.d3[32 * qw + lane][1] = d3f1;
-        }
-        __syncthreads();
-        // pass 2 (fp32): D2 = (d3 w2) [h2 > 0] -> D2 (row-major), D2^T (staged
-        // transpose); column sums over the warp's 32 rows in fp32: lane l sums
-        // column c0 + (l & 15) over rows 16 (l >> 4).. +16, halves added in order
+        // pass 2 (fp32): D2 = (d3 w2) [h2 > 0] -> D2 (row-major), D2^T (TMA
+        // stores); column sums gW2 = sum d3 h2, gb1 = sum D2 over the warp's 32
+        // rows (fp32 shuffle trees), per lane quarter in shared memory
         for (int c0 = cb; c0 < cend; c0 += 16) {
-            float v[16], d[16];
+            float v[16], h[16], d[16];
             tmem_ld16(tq + (c0 - col0), v);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float h = row_ok ? fmaxf(v[i] + T.b1[c0 + i], 0.f) : 0.f;
-                d[i] = h > 0.f ? __fadd_rn(__fmul_rn(d3f0, T.w2[0][c0 + i]), __fmul_rn(d3f1, T.w2[1][c0 + i]))
-                               : 0.f;
-                T.t[w][lane][i] = h;
-                T.d[w][lane][i] = d[i];
-            }
-            if (row_ok) store_row16(g.out + (size_t)row * g.ldo + c0, d);
-            __syncwarp();
-            store_t16(T.d[w], g.out_t, g.ldt, c0, rw0, nrows, 16, lane);
-            const int c = lane & 15, rb = (lane >> 4) * 16;
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+            for (int i = 0; i < 16; i += 4) {
+                const float4 bb = *reinterpret_cast<const float4*>(&T.b1[c0 + i]);
+                const float4 wa = *reinterpret_cast<const float4*>(&T.w2[0][c0 + i]);
+                const float4 wb = *reinterpret_cast<const float4*>(&T.w2[1][c0 + i]);
+                const float b4[4] = {bb.x, bb.y, bb.z, bb.w}, a4[4] = {wa.x, wa.y, wa.z, wa.w},
+                            c4[4] = {wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
-            for (int r = rb; r < rb + 16; ++r) {
-                const float hv = T.t[w][r][c];
-                s0 = fmaf(T.d3[32 * qw + r][0], hv, s0);
-                s1 = fmaf(T.d3[32 * qw + r][1], hv, s1);
-                s2 += T.d[w][r][c];
+                for (int j = 0; j < 4; ++j) {
+                    h[i + j] = row_ok ? fmaxf(v[i + j] + b4[j], 0.f) : 0.f;
+                    d[i + j] = h[i + j] > 0.f ? __fadd_rn(__fmul_rn(d3f0, a4[j]), __fmul_rn(d3f1, c4[j])) : 0.f;
+                }
             }
-            const float o0 = __shfl_xor_sync(0xffffffffu, s0, 16), o1 = __shfl_xor_sync(0xffffffffu, s1, 16),
-                        o2 = __shfl_xor_sync(0xffffffffu, s2, 16);
+            stage_chunk<true, true>(O, (c0 - cb) >> 4, d, &map_o, &map_ot, c0, rw0, lane);
+            float p0[16], p1[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                p0[i] = d3f0 * h[i];
+                p1[i] = d3f1 * h[i];
+            }
+            const float s0 = col_reduce16(p0, lane), s1 = col_reduce16(p1, lane), s2 = col_reduce16(d, lane);
             if (lane < 16) {
-                T.wsum[qw][0][c0 + c] = (double)s0 + (double)o0;
-                T.wsum[qw][1][c0 + c] = (double)s1 + (double)o1;
-                T.wsum[qw][2][c0 + c] = (double)s2 + (double)o2;
+                T.wsum[qw][0][c0 + lane] = (double)s0;
+                T.wsum[qw][1][c0 + lane] = (double)s1;
+                T.wsum[qw][2][c0 + lane] = (double)s2;
             }
-            __syncwarp();
         }
         // gb2 and KL of the rows (column group 0 only; fixed shuffle tree)
         const bool first = cg == 0 && crank == 0;
@@ -450,9 +524,10 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 prow[q * H + c] = ((T.wsum[0][q][c] + T.wsum[1][q][c]) + T.wsum[2][q][c]) + T.wsum[3][q][c];
         if (tid < 3 && crank == 0)
             prow[3 * H + tid] = ((T.red[0][tid] + T.red[1][tid]) + T.red[2][tid]) + T.red[3][tid];
+        if (lane == 0) bulk_wait_all();
         if (npair > 1) cluster_sync();  // the peer has read this CTA's partial logits
     } else {
-        EpiScratch& T = *reinterpret_cast<EpiScratch*>(base);
+        OutStage& O = reinterpret_cast<OutStage*>(base)[w];
         for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
             float v[16];
             tmem_ld16(tq + c0, v);
@@ -465,21 +540,23 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             if (col >= g.N) break;  // (warp-uniform)
             if constexpr (EPI == W16_EPI_H1) {
                 // h1 = relu(acc + b0): row-major (next GEMM's A) + transposed (G4's B)
+                float h[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) T.t[w][lane][i] = fmaxf(v[i] + __ldg(g.bias + col + i), 0.f);
-                if (row_ok) store_row16(g.out + (size_t)row * g.ldo + col, T.t[w][lane]);
-                __syncwarp();
-                store_t16(T.t[w], g.out_t, g.ldt, col, rw0, nrows, 16, lane);
-                __syncwarp();
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 bb = __ldg(reinterpret_cast<const float4*>(g.bias + col + i));
+                    h[i] = fmaxf(v[i] + bb.x, 0.f);
+                    h[i + 1] = fmaxf(v[i + 1] + bb.y, 0.f);
+                    h[i + 2] = fmaxf(v[i + 2] + bb.z, 0.f);
+                    h[i + 3] = fmaxf(v[i + 3] + bb.w, 0.f);
+                }
+                stage_chunk<true, true>(O, (c0 - cbeg) >> 4, h, &map_o, &map_ot, col, rw0, lane);
             } else if constexpr (EPI == W16_EPI_D1T) {
                 // d1 = acc [h1 > 0] (mask = stored bf16 H1), transposed (G5's A)
-                float m[16];
+                float m[16], h[16];
                 if (row_ok) load_row16(g.mask + (size_t)row * g.ldm + col, m);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) T.t[w][lane][i] = row_ok && m[i] > 0.f ? v[i] : 0.f;
-                __syncwarp();
-                store_t16(T.t[w], g.out_t, g.ldt, col, rw0, nrows, 16, lane);
-                __syncwarp();
+                for (int i = 0; i < 16; ++i) h[i] = row_ok && m[i] > 0.f ? v[i] : 0.f;
+                stage_chunk<false, true>(O, (c0 - cbeg) >> 4, h, &map_o, &map_ot, col, rw0, lane);
             } else if (row_ok) {
                 // split-K fp32 partial, row-major [M][ldp]
                 float4* o = reinterpret_cast<float4*>(g.part + (size_t)blockIdx.z * g.split_stride +
@@ -488,53 +565,84 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 for (int q = 0; q < 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             }
         }
+        if constexpr (EPI != W16_EPI_PART)
+            if (lane == 0) bulk_wait_all();
     }
     fence_before_sync();
     __syncthreads();
     if (w == 0) tmem_dealloc(tacc, TC);
+    W16_TR(g.dbg, 3);
 }
 
-template __global__ void w16_gemm_kernel<256, 4, W16_EPI_H1>(const __grid_constant__ CUtensorMap,
-                                                             const __grid_constant__ CUtensorMap, W16Args);
-template __global__ void w16_gemm_kernel<256, 4, W16_EPI_HEAD>(const __grid_constant__ CUtensorMap,
-                                                               const __grid_constant__ CUtensorMap, W16Args);
-template __global__ void w16_gemm_kernel<256, 4, W16_EPI_D1T>(const __grid_constant__ CUtensorMap,
-                                                              const __grid_constant__ CUtensorMap, W16Args);
-template __global__ void w16_gemm_kernel<256, 4, W16_EPI_PART>(const __grid_constant__ CUtensorMap,
-                                                               const __grid_constant__ CUtensorMap, W16Args);
-template __global__ void w16_gemm_kernel<64, 6, W16_EPI_PART>(const __grid_constant__ CUtensorMap,
-                                                              const __grid_constant__ CUtensorMap, W16Args);
-template __global__ void w16_gemm_kernel<128, 6, W16_EPI_PART>(const __grid_constant__ CUtensorMap,
-                                                               const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<256, 4, W16_EPI_H1>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<256, 4, W16_EPI_HEAD>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<256, 4, W16_EPI_D1T>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<256, 4, W16_EPI_PART>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<64, 6, W16_EPI_PART>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<128, 6, W16_EPI_PART>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
 
 // Xg[r] = bf16(feat[rows[r]]) padded to 64 columns (G1's A); X^T [64][ldt]
-// with row 44 = 1 (G5's B: its column 44 of D1^T [X|1] is gb0).
-__global__ void w16_gather_kernel(const float* __restrict__ feat, const uint32_t* __restrict__ rows, int nb,
-                                  __nv_bfloat16* __restrict__ xg, __nv_bfloat16* __restrict__ xt, int ldt) {
+// with row 44 = 1 (G5's B: its column 44 of D1^T [X|1] is gb0). A block
+// stages 64 rows in shared memory (the gathered 176-byte rows as float4
+// loads, all in flight) and writes both layouts with coalesced 16-byte stores.
+constexpr int GATHER_ROWS = 64;
+__global__ void __launch_bounds__(256) w16_gather_kernel(const float* __restrict__ feat,
+                                                         const uint32_t* __restrict__ rows, int nb, int dbg,
+                                                         __nv_bfloat16* __restrict__ xg,
+                                                         __nv_bfloat16* __restrict__ xt, int ldt) {
+    __shared__ __align__(16) __nv_bfloat16 t[GATHER_ROWS][64 + 8];
+    W16_TR(dbg, 0);
     pdl_trigger();
     pdl_wait();  // (the previous step's G5 reads X^T)
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= nb) return;
-    const float4* x = reinterpret_cast<const float4*>(feat + (size_t)rows[r] * F);
-    float v[64];
+    W16_TR(dbg, 1);
+    const int tid = threadIdx.x, r0 = blockIdx.x * GATHER_ROWS;
+    const int nr = min(GATHER_ROWS, nb - r0);
+    constexpr int NQ = F / 4;  // 11 float4 per row
+    float4 v[3];
 #pragma unroll
-    for (int q = 0; q < F / 4; ++q) {
-        const float4 t = __ldg(x + q);  // all 11 loads in flight
-        v[4 * q] = t.x;
-        v[4 * q + 1] = t.y;
-        v[4 * q + 2] = t.z;
-        v[4 * q + 3] = t.w;
+    for (int k = 0; k < 3; ++k) {
+        const int it = tid + k * 256, r = it / NQ, q = it % NQ;
+        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (it < GATHER_ROWS * NQ && r < nr)
+            v[k] = __ldg(reinterpret_cast<const float4*>(feat + (size_t)rows[r0 + r] * F) + q);
     }
 #pragma unroll
-    for (int i = F; i < 64; ++i) v[i] = 0.f;
-    uint4* g4 = reinterpret_cast<uint4*>(xg + (size_t)r * 64);
+    for (int k = 0; k < 3; ++k) {
+        const int it = tid + k * 256, r = it / NQ, q = it % NQ;
+        if (it < GATHER_ROWS * NQ)
+            *reinterpret_cast<uint2*>(&t[r][4 * q]) = make_uint2(pack_bf16(v[k].x, v[k].y), pack_bf16(v[k].z, v[k].w));
+    }
+    // columns 44..63: zero in Xg; X^T row 44 = 1
+    for (int it = tid; it < GATHER_ROWS * 20; it += 256) t[it / 20][F + it % 20] = __float2bfloat16_rn(0.f);
+    __syncthreads();
+    // Xg: 64 rows x 128 B
+    for (int it = tid; it < GATHER_ROWS * 8; it += 256) {
+        const int r = it >> 3, q = it & 7;
+        if (r < nr)
+            reinterpret_cast<uint4*>(xg + (size_t)(r0 + r) * 64)[q] = *reinterpret_cast<const uint4*>(&t[r][8 * q]);
+    }
+    // X^T: 64 columns x 64 rows (128 B per column), 8 rows per 16-byte store
+    for (int it = tid; it < 64 * 8; it += 256) {
+        const int c = it >> 3, rq = (it & 7) * 8;
+        if (rq >= nr) continue;
+        __nv_bfloat16 e[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-        g4[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                           pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
-    v[F] = 1.f;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) xt[(size_t)i * ldt + r] = __float2bfloat16_rn(v[i]);
+        for (int j = 0; j < 8; ++j)
+            e[j] = c == F ? (rq + j < nr ? __float2bfloat16_rn(1.f) : __float2bfloat16_rn(0.f)) : t[rq + j][c];
+        __nv_bfloat16* dst = xt + (size_t)c * ldt + r0 + rq;
+        if (rq + 8 <= nr && ((r0 + rq) & 7) == 0) {
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(e);
+        } else {
+            for (int j = 0; j < 8 && rq + j < nr; ++j) dst[j] = e[j];
+        }
+    }
+    W16_TR(dbg, 3);
 }
 
 __global__ void to_bf16_kernel(const float* __restrict__ src, size_t n, __nv_bfloat16* __restrict__ dst) {
@@ -558,31 +666,18 @@ __global__ void w16_weights_kernel(const float* __restrict__ params, int H, __nv
     w1t[j * H + k] = b;
 }
 
-// sum_q src[q * stride] in q order, eight loads in flight at a time
-__device__ __forceinline__ double ordered_sum(const float* __restrict__ src, size_t stride, int n) {
+// sum_q src[q * stride] in q order, sixteen loads in flight at a time
+template <typename T>
+__device__ __forceinline__ double ordered_sum(const T* __restrict__ src, size_t stride, int n) {
     double s = 0.0;
-    int q = 0;
-    for (; q + 8 <= n; q += 8) {
-        float v[8];
+    for (int q = 0; q < n; q += 16) {
+        T v[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = __ldg(src + (size_t)(q + j) * stride);
+        for (int j = 0; j < 16; ++j) v[j] = q + j < n ? __ldg(src + (size_t)(q + j) * stride) : T(0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s += v[j];
+        for (int j = 0; j < 16; ++j)
+            if (q + j < n) s += v[j];
     }
-    for (; q < n; ++q) s += __ldg(src + (size_t)q * stride);
-    return s;
-}
-__device__ __forceinline__ double ordered_sum(const double* __restrict__ src, size_t stride, int n) {
-    double s = 0.0;
-    int q = 0;
-    for (; q + 8 <= n; q += 8) {
-        double v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = __ldg(src + (size_t)(q + j) * stride);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) s += v[j];
-    }
-    for (; q < n; ++q) s += __ldg(src + (size_t)q * stride);
     return s;
 }
 
@@ -616,77 +711,118 @@ __device__ __forceinline__ double w16_kl_sum(const W16UpdArgs& u) {
 
 // mode 0: reduce + SGD + refreshed bf16 copies (one rank); 1: reduce into the
 // flat gradient g_out and the loss sum (before an all-reduce); 2: SGD from g_out.
-// Block layout of the update grid: [0, nb0) 1-D over params [0, o_w1) (W0,
-// b0); then (H/16)^2 blocks of 16 x 16 W1 tiles (coalesced W1 and W1^T
-// writes through a shared-memory transpose); then 1-D over [o_b1, np).
+// Block layout of the update grid: [0, nb2) 1-D over [o_b1, np) (b1, W2, b2:
+// the longest sums, over every row tile's head partials, so they start
+// first); then [nb2, nb2 + nb0) 1-D over [0, o_w1) (W0, b0); then 32 x 16 W1
+// tiles, two parameters per thread (coalesced W1 and W1^T writes through a
+// shared-memory transpose). One wave on 148 SMs at H = 512.
 __host__ __device__ void w16_update_layout(int H, size_t np, int& nb0, int& nw1, int& nb2) {
     const size_t o_w1 = (size_t)H * F + H, o_b1 = o_w1 + (size_t)H * H;
-    nb0 = (int)((o_w1 + 255) / 256);
-    nw1 = (H / 16) * (H / 16);
     nb2 = (int)((np - o_b1 + 255) / 256);
+    nb0 = (int)((o_w1 + 255) / 256);
+    nw1 = (H / 32) * (H / 16);
 }
 
 __global__ void __launch_bounds__(256) w16_update_kernel(W16UpdArgs u, int mode) {
     __shared__ double s_loss;
-    __shared__ __nv_bfloat16 s_t[16][17];
+    __shared__ __nv_bfloat16 s_t[32][17];
+    W16_TR(u.dbg, 0);
     pdl_trigger();
     pdl_wait();
-    if (*u.diverged >= 0) return;
+    W16_TR(u.dbg, 1);
+    const int diverged = *u.diverged;  // (checked after the barrier: its load overlaps the others)
     const int H = u.hidden;
     const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H;
     int nb0, nw1, nb2;
     w16_update_layout(H, u.np, nb0, nw1, nb2);
     const int bx = blockIdx.x, tid = threadIdx.x;
-    const bool tile = bx >= nb0 && bx < nb0 + nw1;
-    size_t p;
+    const bool tile = bx >= nb2 + nb0;
+    size_t p[2] = {u.np, u.np};
     int tk = 0, tj = 0;
-    if (bx < nb0) {
-        p = (size_t)bx * 256 + tid;
-        if (p >= o_w1) p = u.np;  // (past W0 / b0: idle)
-    } else if (tile) {
-        const int t = bx - nb0, nt = H / 16;
+    if (bx < nb2) {
+        p[0] = o_b1 + (size_t)bx * 256 + tid;
+    } else if (!tile) {
+        p[0] = (size_t)(bx - nb2) * 256 + tid;
+        if (p[0] >= o_w1) p[0] = u.np;  // (past W0 / b0: idle)
+    } else {
+        const int t = bx - nb2 - nb0, nt = H / 16;
         tk = t / nt;
         tj = t % nt;
-        p = o_w1 + (size_t)(tk * 16 + (tid >> 4)) * H + tj * 16 + (tid & 15);
-    } else {
-        p = o_b1 + (size_t)(bx - nb0 - nw1) * 256 + tid;
+        p[0] = o_w1 + (size_t)(tk * 32 + (tid >> 4)) * H + tj * 16 + (tid & 15);
+        p[1] = p[0] + (size_t)16 * H;
     }
     if (mode == 1) {
+        if (diverged >= 0) return;
         if (bx == 0 && tid < 32) {
             const double kl = w16_kl_sum(u);
             if (tid == 0) *u.loss_sum = kl;
         }
-        if (p < u.np) u.g_out[p] = (float)w16_grad(u, p);
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (p[q] < u.np) u.g_out[p[q]] = (float)w16_grad(u, p[q]);
         return;
     }
+    // the gradient sums and the old weights are loaded before the loss is
+    // known (one round trip for all of them); nothing is written before it is
+    double gsum[2] = {0.0, 0.0};
+    float wold[2] = {0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+        if (p[q] < u.np) {
+            gsum[q] = mode == 2 ? (double)u.g_out[p[q]] : w16_grad(u, p[q]);
+            wold[q] = u.params[p[q]];
+        }
     if (tid < 32) {
         const double kl = mode == 2 ? *u.loss_sum : w16_kl_sum(u);
         if (tid == 0) s_loss = kl / (double)u.nb;
     }
     __syncthreads();
+    if (diverged >= 0) return;
+    W16_TR(u.dbg, 2);
     const double loss = s_loss;
     if (!isfinite(loss)) {  // fit throws before updating (policy.cpp:321-325)
         if (bx == 0 && tid == 0) *u.diverged = *u.epoch;
         return;
     }
     if (bx == 0 && tid == 0) *u.epoch_acc += loss * (double)u.nb;
-    if (p < u.np) {
-        const double gsum = mode == 2 ? (double)u.g_out[p] : w16_grad(u, p);
-        const float nw = __double2float_rn((double)u.params[p] - u.lr * gsum);
-        u.params[p] = nw;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        if (p[q] >= u.np) continue;
+        const float nw = __double2float_rn((double)wold[q] - u.lr * gsum[q]);
+        u.params[p[q]] = nw;
         const __nv_bfloat16 b = __float2bfloat16_rn(nw);
-        if (p < o_b0) {
-            u.w0p[(p / F) * 64 + p % F] = b;
+        if (p[q] < o_b0) {
+            u.w0p[(p[q] / F) * 64 + p[q] % F] = b;
         } else if (tile) {
-            u.w1[p - o_w1] = b;
-            s_t[tid >> 4][tid & 15] = b;
+            u.w1[p[q] - o_w1] = b;
+            s_t[(tid >> 4) + 16 * q][tid & 15] = b;
         }
     }
-    if (tile) {  // W1^T[j][k]: 16 consecutive k per row of the tile
+    if (tile) {  // W1^T[j][k]: 32 consecutive k per row of the tile
         __syncthreads();
-        const int j = tid >> 4, k = tid & 15;
-        u.w1t[(size_t)(tj * 16 + j) * H + tk * 16 + k] = s_t[k][j];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int idx = tid + 256 * q, j = idx >> 5, k = idx & 31;
+            u.w1t[(size_t)(tj * 16 + j) * H + tk * 32 + k] = s_t[k][j];
+        }
     }
+    W16_TR(u.dbg, 3);
 }
 
 }  // namespace gbxcu
+
+#ifdef GBX_PHASE_TIMING
+extern "C" int gbxcu_debug_w16_trace(unsigned long long* out, int reset) {
+    if (out && cudaMemcpyFromSymbol(out, gbxcu::g_w16_tr, sizeof(gbxcu::g_w16_tr)) != cudaSuccess) return 3;
+    if (reset) {
+        static unsigned long long z[64][4][2];
+        for (int i = 0; i < 64; ++i)
+            for (int j = 0; j < 4; ++j) {
+                z[i][j][0] = ~0ull;
+                z[i][j][1] = 0;
+            }
+        if (cudaMemcpyToSymbol(gbxcu::g_w16_tr, z, sizeof(z)) != cudaSuccess) return 3;
+    }
+    return 0;
+}
+#endif

@@ -200,6 +200,7 @@ struct W16Args {
     const uint32_t* rows;          // nullable
     double inv_b;
     double* head_part;             // [row tiles][3N + 3]: gW2_0, gW2_1, gb1, gb2_0, gb2_1, KL
+    int dbg;                       // timeline slot (GBX_PHASE_TIMING builds), -1 = none
 };
 struct W16UpdArgs {
     float* params;                 // fp32 master weights (flat serialization order)
@@ -218,13 +219,16 @@ struct W16UpdArgs {
     const int* epoch;
     int* diverged;
     double* epoch_acc;
+    int dbg;                       // timeline slot (GBX_PHASE_TIMING builds), -1 = none
 };
 template <int BN, int ST>
 size_t w16_gemm_smem_bytes();
 template <int BN, int ST, int EPI>
 __global__ void w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                                const __grid_constant__ CUtensorMap map_b, W16Args g);
-__global__ void w16_gather_kernel(const float* feat, const uint32_t* rows, int nb, __nv_bfloat16* xg,
+                                const __grid_constant__ CUtensorMap map_b,
+                                const __grid_constant__ CUtensorMap map_o,
+                                const __grid_constant__ CUtensorMap map_ot, W16Args g);
+__global__ void w16_gather_kernel(const float* feat, const uint32_t* rows, int nb, int dbg, __nv_bfloat16* xg,
                                   __nv_bfloat16* xt, int ldt);
 __global__ void w16_weights_kernel(const float* params, int H, __nv_bfloat16* w0p, __nv_bfloat16* w1,
                                    __nv_bfloat16* w1t);
