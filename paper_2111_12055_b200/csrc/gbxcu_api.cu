@@ -343,6 +343,12 @@ int prepare_order(gbxcu_ctx* c, size_t n, cudaStream_t st) {
                       &c->sh_root, &c->sh_root2})
         RET(b->ensure(n * 4));
     RET(c->sh_flags.ensure(80 * sizeof(uint32_t)));
+    // epoch e of every call reads the same buffer (shuffle_epoch ping-pongs
+    // order / order2): graphs captured over an epoch's steps stay valid
+    if (c->order.p > c->order2.p) {
+        std::swap(c->order.p, c->order2.p);
+        std::swap(c->order.cap, c->order2.cap);
+    }
     RET(c->bar.ensure(16));
     RET(c->diverged.ensure(16));
     CK(cudaMemsetAsync(c->diverged.p, 0xFF, 16, st));
@@ -2045,7 +2051,7 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
     u.dbg = slot(6);
     if (nbr > 0) {
         RET(launch_pdl(c, "w16_gather_kernel", w16_gather_kernel, dim3((nbr + 63) / 64), dim3(256), 0, st, feat,
-                       rows, nbr, slot(0), c->b_xg.as<bf>(), c->b_xt.as<bf>(), ldt));
+                       rows, nbr, dbg >= 0 ? slot(0) : -(g_w16_dbg_step + 2), c->b_xg.as<bf>(), c->b_xt.as<bf>(), ldt));
         W16Args g1{};
         g1.dbg = slot(1);  // H1 = relu(Xg W0^T + b0) -> H1, H1^T
         g1.M = nbr; g1.N = H; g1.K = 64; g1.bias = Pm + o_b0;
@@ -2125,7 +2131,8 @@ int w16_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, co
         return GBXCU_OK;
     };
     // an epoch's ~7 launches per step replay as a CUDA graph (single-GPU path)
-    const bool use_graph = !c->comm && n_steps > 1;
+    const char* ge = getenv("GBX_WIDE_GRAPH");
+    const bool use_graph = !c->comm && n_steps > 1 && !(ge && ge[0] == '0');
     for (int e = 0; e < cfg->epochs; ++e) {
         RET(shuffle_epoch(c, n, cfg->seed, e, st));
         CK(cudaMemsetAsync(c->epoch_acc.p, 0, sizeof(double), st));
@@ -2153,6 +2160,7 @@ int w16_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, co
                 if (g->exec) cudaGraphExecDestroy(g->exec);
                 g->exec = nullptr;
                 g->key.clear();
+                if (getenv("GBX_DEBUG_GRAPH")) fprintf(stderr, "[gbxcu] capturing the wide-step graph\n");
                 CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
                 const int rc = run_steps(order);
                 cudaGraph_t graph = nullptr;
@@ -2227,7 +2235,8 @@ int wide_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, c
     };
     // one epoch = ~12 launches per step, most of them short: replay them as a
     // CUDA graph (single-GPU path; NCCL steps launch directly)
-    const bool use_graph = !c->comm && n_steps > 1;
+    const char* ge = getenv("GBX_WIDE_GRAPH");
+    const bool use_graph = !c->comm && n_steps > 1 && !(ge && ge[0] == '0');
     for (int e = 0; e < cfg->epochs; ++e) {
         RET(shuffle_epoch(c, n, cfg->seed, e, st));
         CK(cudaMemsetAsync(c->epoch_acc.p, 0, sizeof(double), st));
@@ -2255,6 +2264,7 @@ int wide_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, c
                 if (g->exec) cudaGraphExecDestroy(g->exec);
                 g->exec = nullptr;
                 g->key.clear();
+                if (getenv("GBX_DEBUG_GRAPH")) fprintf(stderr, "[gbxcu] capturing the wide-step graph\n");
                 CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
                 const int rc = run_steps(order);
                 cudaGraph_t graph = nullptr;

@@ -43,6 +43,7 @@ using namespace tc;
 // 6 update); points 0 entry, 1 inputs ready (after griddepcontrol.wait),
 // 2 main loop done, 3 exit; {min, max} over the CTAs (globaltimer ns).
 __device__ unsigned long long g_w16_tr[64][4][2];
+__device__ unsigned long long g_w16_steps[4096];  // every step: first gather CTA entry
 #define W16_TR(slot, pt)                                                          \
     do {                                                                          \
         if ((slot) >= 0 && threadIdx.x == 0) {                                    \
@@ -598,6 +599,16 @@ __global__ void __launch_bounds__(256) w16_gather_kernel(const float* __restrict
                                                          __nv_bfloat16* __restrict__ xt, int ldt) {
     __shared__ __align__(16) __nv_bfloat16 t[GATHER_ROWS][64 + 8];
     W16_TR(dbg, 0);
+#ifdef GBX_PHASE_TIMING
+    {  // dbg < 0 encodes an untraced step as -(step + 2)
+        const int stp = dbg >= 0 ? dbg / 8 : -dbg - 2;
+        if (threadIdx.x == 0 && stp >= 0 && stp < 4096) {
+            unsigned long long t_;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+            atomicMin(&g_w16_steps[stp], t_);
+        }
+    }
+#endif
     pdl_trigger();
     pdl_wait();  // (the previous step's G5 reads X^T)
     W16_TR(dbg, 1);
@@ -822,6 +833,15 @@ extern "C" int gbxcu_debug_w16_trace(unsigned long long* out, int reset) {
                 z[i][j][1] = 0;
             }
         if (cudaMemcpyToSymbol(gbxcu::g_w16_tr, z, sizeof(z)) != cudaSuccess) return 3;
+    }
+    return 0;
+}
+extern "C" int gbxcu_debug_w16_steps(unsigned long long* out, int reset) {
+    if (out && cudaMemcpyFromSymbol(out, gbxcu::g_w16_steps, sizeof(gbxcu::g_w16_steps)) != cudaSuccess) return 3;
+    if (reset) {
+        static unsigned long long z[4096];
+        for (auto& x : z) x = ~0ull;
+        if (cudaMemcpyToSymbol(gbxcu::g_w16_steps, z, sizeof(z)) != cudaSuccess) return 3;
     }
     return 0;
 }

@@ -8,11 +8,12 @@ sys.path.insert(0, ".")
 import paper_2111_12055_b200 as gbx
 lib = gbx.load_library(os.path.abspath("tools/timing/libgbxcu.so"))
 lib.gbxcu_debug_w16_trace.argtypes = [C.c_void_p, C.c_int]
+lib.gbxcu_debug_w16_steps.argtypes = [C.c_void_p, C.c_int]
 import torch
 H = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 b = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 dev = gbx.Device(0)
-n = 8 * b
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 8 * b  # records (steps past the 8th are not traced)
 feat = torch.rand((n, 44), device="cuda") * 7
 tgt = torch.rand((n, 2), device="cuda", dtype=torch.float64)
 tgt = tgt / tgt.sum(1, keepdim=True)
@@ -20,8 +21,25 @@ p = torch.from_numpy(dev.wide_init(H, 7)).cuda()
 torch.cuda.synchronize()
 run = lambda: dev.wide_fit_dev(H, p.data_ptr(), feat.data_ptr(), tgt.data_ptr(), n, 1e-3, 1, b, 5, dev.stream,
                                precision="bf16")
-run()  # graph capture + warm-up
+import time
+t0 = time.perf_counter(); run(); torch.cuda.synchronize()  # graph capture + warm-up
+print(f"first call (capture + instantiate + run): {(time.perf_counter() - t0) * 1e3:.1f} ms host")
+t0 = time.perf_counter(); run(); torch.cuda.synchronize()
+print(f"second call: {(time.perf_counter() - t0) * 1e3:.1f} ms host")
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+lib.gbxcu_debug_w16_steps(None, 1)
+e0.record(torch.cuda.ExternalStream(dev.stream))
+run()
+e1.record(torch.cuda.ExternalStream(dev.stream))
+torch.cuda.synchronize()
+st = np.zeros(4096, np.uint64)
+lib.gbxcu_debug_w16_steps(st.ctypes.data, 0)
+ns = min(4096, (n + b - 1) // b)
+d = np.diff(st[:ns].astype(np.float64)) / 1e3
+print("per-step us (gather entry to next): first 12", np.round(d[:12], 1), "median", np.median(d),
+      "p90", np.percentile(d, 90), "max", d.max(), "sum", d.sum())
+print(f"epoch of {n} records: {e0.elapsed_time(e1):.3f} ms = {e0.elapsed_time(e1) * 1e3 / ((n + b - 1) // b):.1f} us/step")
 res = []
 for rep in range(5):
     lib.gbxcu_debug_w16_trace(None, 1)
