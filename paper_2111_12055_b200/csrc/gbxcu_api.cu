@@ -1977,7 +1977,8 @@ int launch_w16(gbxcu_ctx* c, const void* A, int lda, const void* B, int ldb, con
         (g.out_t && !make_bf16_store_map(&mot, g.out_t, g.M, g.N, g.ldt, 32, 16)))
         return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled rejected a bf16 epilogue output");
     dim3 grid((g.N + BN - 1) / BN, (g.M + 127) / 128, splits);
-    return launch_pdl_cl(c, "w16_gemm_kernel", w16_gemm_kernel<BN, ST, EPI>, grid, dim3(512),
+    return launch_pdl_cl(c, "w16_gemm_kernel", w16_gemm_kernel<BN, ST, EPI>, grid,
+                         dim3(128 * w_ew<EPI>()),
                          w16_gemm_smem_bytes<BN, ST>(), st, cluster_x, ma, mb, mo, mot, g);
 }
 

@@ -190,8 +190,11 @@ struct W16Smem {
 
 __host__ __device__ constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : bn <= 256 ? 256 : 512; }
 
-constexpr int W_EW = 4;                // epilogue warps per TMEM lane quarter
-constexpr int W_THREADS = 128 * W_EW;  // 16 warps: warp w reads lanes 32 (w % 4).., columns group w / 4
+// Epilogue warps per TMEM lane quarter (w_ew<EPI>(), kernels.h): warp w reads
+// lanes 32 (w % 4).., column group w / 4. (32 warps for the head measured
+// slower: 64 registers per thread spill, and the larger shared-memory
+// footprint slowed the launches that follow the GEMMs.)
+constexpr int W_EW_MAX = 4;
 
 // Epilogue output staging (per warp, double-buffered over its 16-column
 // chunks): the chunk's 32 rows x 16 columns in bf16, row-major ([32][16], one
@@ -202,15 +205,15 @@ struct OutStage {
     __nv_bfloat16 rm[2][32 * 16];
     __nv_bfloat16 tr[2][16 * 32];
 };
-constexpr size_t OUT_STAGE_BYTES = 16 * sizeof(OutStage);
+constexpr size_t OUT_STAGE_BYTES = 4 * W_EW_MAX * sizeof(OutStage);
 struct HeadScratch {
     float b1[W16_MAX_H];
     float w2[2][W16_MAX_H];
     double w2d[2][W16_MAX_H];    // w2 widened once (the logits accumulate in fp64)
-    double lg[W_EW][128][2];     // per column group: partial logits of the CTA's 128 rows
+    double lg[W_EW_MAX][128][2];  // per column group: partial logits of the CTA's 128 rows
     double own[128][2];          // the CTA's partial logits (its columns), read by the pair peer
     double wsum[4][3][W16_MAX_H];  // per lane quarter: column sums (gW2_0, gW2_1, gb1)
-    double red[16][3];
+    double red[4 * W_EW_MAX][3];
 };
 
 // Column sums of a warp's 32 rows: v[16] = this lane's (row's) values of 16
@@ -282,7 +285,7 @@ template size_t w16_gemm_smem_bytes<256, 4>();
 // lane 0: MMA issuer; all 16 warps: epilogue (warp w: TMEM lanes 32 (w % 4)..
 // = output rows, column group w / 4 of BN / 4 columns; thread = one row).
 template <int BN, int ST, int EPI>
-__global__ void __launch_bounds__(W_THREADS, 1)
+__global__ void __launch_bounds__(128 * w_ew<EPI>(), 1)
 w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_ot, W16Args g) {
     extern __shared__ unsigned char smem_raw[];
@@ -293,6 +296,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     constexpr int MN = BN / NMMA;
     constexpr int BOX = BN > 256 ? 256 : BN;  // TMA box rows <= 256
     constexpr int TC = tmem_cols(BN);
+    constexpr int EW = w_ew<EPI>(), NTH = 128 * EW;
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     const int col0 = blockIdx.x * BN, row0 = blockIdx.y * W_BM;
     const int nkb = (g.K + W_BK - 1) / W_BK;
@@ -379,7 +383,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const int row = rw0 + lane;
     const bool row_ok = row < g.M;
     const uint32_t tq = tacc + ((uint32_t)(32 * qw) << 16);
-    constexpr int CW = BN / W_EW;               // columns per group
+    constexpr int CW = BN / EW;                 // columns per group
     const int cbeg = cg * CW;
     __syncthreads();  // every warp is past the mainloop: stage buffers are free for scratch
 
@@ -391,7 +395,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         HeadScratch& T = *reinterpret_cast<HeadScratch*>(base);
         OutStage& O = reinterpret_cast<OutStage*>(base + head_stage_off())[w];
         const int H = g.N;
-        for (int c = col0 + tid; c < min(H, col0 + BN); c += W_THREADS) {
+        for (int c = col0 + tid; c < min(H, col0 + BN); c += NTH) {
             T.b1[c] = g.bias[c];
             T.w2[0][c] = g.w2[c];
             T.w2[1][c] = g.w2[H + c];
@@ -402,12 +406,12 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         const int cb = col0 + cbeg, cend = min(H, cb + CW);
         // pass 1: h2 = relu(acc + b1); partial logits in fp64 (two chains per output)
         double l0a = 0.0, l0b = 0.0, l1a = 0.0, l1b = 0.0;
-        for (int c0 = cb; c0 < cend; c0 += 32) {
-            float v[32];
-            tmem_ld32(tq + (c0 - col0), v);
+        for (int c0 = cb; c0 < cend; c0 += 16) {
+            float v[16];
+            tmem_ld16(tq + (c0 - col0), v);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
+            for (int i = 0; i < 16; i += 4) {
                 const float4 bb = *reinterpret_cast<const float4*>(&T.b1[c0 + i]);
                 const double2 w0a = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i]);
                 const double2 w0b = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i + 2]);
@@ -432,7 +436,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         if (cg == 0) {
             double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-            for (int q = 0; q < W_EW; ++q) {
+            for (int q = 0; q < EW; ++q) {
                 s0 += T.lg[q][rl][0];
                 s1 += T.lg[q][rl][1];
             }
@@ -491,13 +495,14 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 }
             }
             stage_chunk<true, true>(O, (c0 - cb) >> 4, d, &map_o, &map_ot, c0, rw0, lane);
-            float p0[16], p1[16];
+            float p[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                p0[i] = d3f0 * h[i];
-                p1[i] = d3f1 * h[i];
-            }
-            const float s0 = col_reduce16(p0, lane), s1 = col_reduce16(p1, lane), s2 = col_reduce16(d, lane);
+            for (int i = 0; i < 16; ++i) p[i] = d3f0 * h[i];
+            const float s0 = col_reduce16(p, lane);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) p[i] = d3f1 * h[i];
+            const float s1 = col_reduce16(p, lane);
+            const float s2 = col_reduce16(d, lane);
             if (lane < 16) {
                 T.wsum[qw][0][c0 + lane] = (double)s0;
                 T.wsum[qw][1][c0 + lane] = (double)s1;
@@ -521,7 +526,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         __syncthreads();
         double* prow = g.head_part + (size_t)blockIdx.y * (3 * H + 3);
         for (int q = 0; q < 3; ++q)
-            for (int c = col0 + tid; c < min(H, col0 + BN); c += W_THREADS)
+            for (int c = col0 + tid; c < min(H, col0 + BN); c += NTH)
                 prow[q * H + c] = ((T.wsum[0][q][c] + T.wsum[1][q][c]) + T.wsum[2][q][c]) + T.wsum[3][q][c];
         if (tid < 3 && crank == 0)
             prow[3 * H + tid] = ((T.red[0][tid] + T.red[1][tid]) + T.red[2][tid]) + T.red[3][tid];
@@ -609,7 +614,6 @@ __global__ void __launch_bounds__(256) w16_gather_kernel(const float* __restrict
         }
     }
 #endif
-    pdl_trigger();
     pdl_wait();  // (the previous step's G5 reads X^T)
     W16_TR(dbg, 1);
     const int tid = threadIdx.x, r0 = blockIdx.x * GATHER_ROWS;
@@ -653,6 +657,9 @@ __global__ void __launch_bounds__(256) w16_gather_kernel(const float* __restrict
             for (int j = 0; j < 8 && rq + j < nr; ++j) dst[j] = e[j];
         }
     }
+    // (G1 launches after the gather's work: early G1 CTAs would hold whole
+    //  SMs while the previous step's update still needs them)
+    pdl_trigger();
     W16_TR(dbg, 3);
 }
 

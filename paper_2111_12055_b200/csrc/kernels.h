@@ -221,6 +221,9 @@ struct W16UpdArgs {
     double* epoch_acc;
     int dbg;                       // timeline slot (GBX_PHASE_TIMING builds), -1 = none
 };
+// epilogue warps per TMEM lane quarter of w16_gemm_kernel<.., EPI> (128 x this threads)
+template <int EPI>
+__host__ __device__ constexpr int w_ew() { return EPI == W16_EPI_HEAD ? 4 : 4; }
 template <int BN, int ST>
 size_t w16_gemm_smem_bytes();
 template <int BN, int ST, int EPI>
