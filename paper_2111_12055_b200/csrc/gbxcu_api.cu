@@ -207,6 +207,7 @@ int setup_kernel_attrs() {
         set((const void*)w16_gemm_kernel<256, 4, W16_EPI_PART>, w16_gemm_smem_bytes<256, 4>());
         set((const void*)w16_gemm_kernel<64, 6, W16_EPI_PART>, w16_gemm_smem_bytes<64, 6>());
         set((const void*)w16_gemm_kernel<128, 6, W16_EPI_PART>, w16_gemm_smem_bytes<128, 6>());
+        set((const void*)w16_gemm_kernel<128, 6, W16_EPI_SGD>, w16_gemm_smem_bytes<128, 6>());
         set((const void*)tma_gemm_kernel<128>, tma_gemm_smem_bytes<128>());
         set((const void*)tma_gemm_kernel<256>, tma_gemm_smem_bytes<256>());
     });
@@ -1911,7 +1912,7 @@ int wide_step(gbxcu_ctx* c, int H, float* P, const float* feat, const double* tg
 // data); kept through stream capture as a programmatic graph edge.
 template <typename... K, typename... A>
 int launch_pdl_cl(gbxcu_ctx* c, const char* name, void (*kern)(K...), dim3 grid, dim3 block, size_t smem,
-                  cudaStream_t st, int cluster_x, A... args) {
+                  cudaStream_t st, dim3 cluster, A... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -1921,18 +1922,18 @@ int launch_pdl_cl(gbxcu_ctx* c, const char* name, void (*kern)(K...), dim3 grid,
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = (unsigned)cluster_x;
-    at[1].val.clusterDim.y = 1;
-    at[1].val.clusterDim.z = 1;
+    at[1].val.clusterDim.x = cluster.x;
+    at[1].val.clusterDim.y = cluster.y;
+    at[1].val.clusterDim.z = cluster.z;
     cfg.attrs = at;
-    cfg.numAttrs = cluster_x > 1 ? 2 : 1;
+    cfg.numAttrs = cluster.x * cluster.y * cluster.z > 1 ? 2 : 1;
     CK(cudaLaunchKernelEx(&cfg, kern, args...));
     return check_launch(c, name);
 }
 template <typename... K, typename... A>
 int launch_pdl(gbxcu_ctx* c, const char* name, void (*kern)(K...), dim3 grid, dim3 block, size_t smem,
                cudaStream_t st, A... args) {
-    return launch_pdl_cl(c, name, kern, grid, block, smem, st, 1, args...);
+    return launch_pdl_cl(c, name, kern, grid, block, smem, st, dim3(1, 1, 1), args...);
 }
 
 // K-major bf16 operand [rows][ld] (K valid columns) as TMA boxes of
@@ -1969,7 +1970,7 @@ bool make_bf16_store_map(CUtensorMap* m, const void* base, int cols, int rows, i
 // [N][g.ldt] transposed (each when non-null), in 32-row x 16-column chunks.
 template <int BN, int ST, int EPI>
 int launch_w16(gbxcu_ctx* c, const void* A, int lda, const void* B, int ldb, const W16Args& g, int splits,
-               cudaStream_t st, int cluster_x = 1) {
+               cudaStream_t st, int cluster_x = 1, int cluster_z = 1) {
     CUtensorMap ma, mb, mo{}, mot{};
     if (!make_bf16_map(&ma, A, g.K, g.M, lda, 128) || !make_bf16_map(&mb, B, g.K, g.N, ldb, BN > 256 ? 256 : BN))
         return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled unavailable or rejected a bf16 operand");
@@ -1979,7 +1980,22 @@ int launch_w16(gbxcu_ctx* c, const void* A, int lda, const void* B, int ldb, con
     dim3 grid((g.N + BN - 1) / BN, (g.M + 127) / 128, splits);
     return launch_pdl_cl(c, "w16_gemm_kernel", w16_gemm_kernel<BN, ST, EPI>, grid,
                          dim3(128 * w_ew<EPI>()),
-                         w16_gemm_smem_bytes<BN, ST>(), st, cluster_x, ma, mb, mo, mot, g);
+                         w16_gemm_smem_bytes<BN, ST>(), st, dim3(cluster_x, 1, cluster_z), ma, mb, mo, mot, g);
+}
+
+// The fused G4 + G5 + SGD launch: grid (1, T1 + T0, W16_SPLITS), clusters of
+// W16_SPLITS along z; tiles y < T1 = (H/128)^2 are gW1 = D2^T H1 tiles, the
+// T0 = H/128 others [gW0 | gb0] = D1^T [X | 1] tiles (maps in the o / ot slots).
+int launch_w16_sgd(gbxcu_ctx* c, const W16Args& g, int ldt, cudaStream_t st) {
+    const int H = g.M;
+    CUtensorMap ma, mb, m5a, m5b;
+    if (!make_bf16_map(&ma, c->b_d2t.p, g.K, H, ldt, 128) || !make_bf16_map(&mb, c->b_h1t.p, g.K, H, ldt, 128) ||
+        !make_bf16_map(&m5a, c->b_d1t.p, g.K, H, ldt, 128) || !make_bf16_map(&m5b, c->b_xt.p, g.K, 64, ldt, 128))
+        return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled unavailable or rejected a bf16 operand");
+    const int nt = (H + 127) / 128;
+    dim3 grid(1, nt * nt + nt, W16_SPLITS);
+    return launch_pdl_cl(c, "w16_gemm_kernel", w16_gemm_kernel<128, 6, W16_EPI_SGD>, grid, dim3(512),
+                         w16_gemm_smem_bytes<128, 6>(), st, dim3(1, 1, W16_SPLITS), ma, mb, m5a, m5b, g);
 }
 
 int check_hidden16(int H) {
@@ -2075,11 +2091,18 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
         g4.dbg = slot(4);  // gW1 = D2^T H1 (split-K partials)
         g4.M = H; g4.N = H; g4.K = nbr; g4.part = c->b_p4.as<float>(); g4.ldp = H;
         g4.split_stride = (size_t)H * H;
-        RET((launch_w16<128, 6, W16_EPI_PART>(c, c->b_d2t.p, ldt, c->b_h1t.p, ldt, g4, P.s4, st)));
         W16Args g5{};
         g5.dbg = slot(5);  // gW0 | gb0 = D1^T [X | 1] (split-K partials)
         g5.M = H; g5.N = 64; g5.K = nbr; g5.part = c->b_p5.as<float>(); g5.ldp = 64;
         g5.split_stride = (size_t)H * 64;
+        if (!c->comm) {
+            // one rank: G4 and G5 share one launch whose epilogue reduces the
+            // K splits across a cluster and applies SGD (no update launch)
+            g4.u = u;
+            g4.dbg = slot(4);
+            return launch_w16_sgd(c, g4, ldt, st);
+        }
+        RET((launch_w16<128, 6, W16_EPI_PART>(c, c->b_d2t.p, ldt, c->b_h1t.p, ldt, g4, P.s4, st)));
         RET((launch_w16<64, 6, W16_EPI_PART>(c, c->b_d1t.p, ldt, c->b_xt.p, ldt, g5, P.s5, st)));
     } else {
         // an empty slice contributes nothing (data-parallel remainder steps)

@@ -280,6 +280,49 @@ template size_t w16_gemm_smem_bytes<64, 6>();
 template size_t w16_gemm_smem_bytes<128, 6>();
 template size_t w16_gemm_smem_bytes<256, 4>();
 
+// sum_q src[q * stride] in q order, sixteen loads in flight at a time
+template <typename T>
+__device__ __forceinline__ double ordered_sum(const T* __restrict__ src, size_t stride, int n) {
+    double s = 0.0;
+    for (int q = 0; q < n; q += 16) {
+        T v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = q + j < n ? __ldg(src + (size_t)(q + j) * stride) : T(0);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (q + j < n) s += v[j];
+    }
+    return s;
+}
+
+// Gradient of parameter p (serialization order w0[H][44] b0[H] w1[H][H]
+// b1[H] w2[2][H] b2[2]) from the step's partials, summed in a fixed order.
+__device__ __forceinline__ double w16_grad(const W16UpdArgs& u, size_t p) {
+    const size_t H = u.hidden;
+    const size_t o_b0 = H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + H * H, o_w2 = o_b1 + H, o_b2 = o_w2 + 2 * H;
+    const size_t hw = 3 * H + 3;
+    if (p < o_w1) {  // gW0 | gb0: G5 partials [s5][H][64], column 44 = gb0
+        const size_t j = p < o_b0 ? p / F : p - o_b0, i = p < o_b0 ? p % F : (size_t)F;
+        return ordered_sum(u.p5 + j * 64 + i, H * 64, u.s5);
+    }
+    if (p < o_b1) return ordered_sum(u.p4 + (p - o_w1), H * H, u.s4);   // gW1: G4 partials [s4][H][H]
+    if (p < o_w2) return ordered_sum(u.hp + 2 * H + (p - o_b1), hw, u.nhead);  // gb1
+    if (p < o_b2) return ordered_sum(u.hp + (p - o_w2), hw, u.nhead);          // gW2
+    return ordered_sum(u.hp + 3 * H + (p - o_b2), hw, u.nhead);                // gb2
+}
+
+// KL sum of the step over the head partials (warp 0; fixed lane order + tree:
+// every block computes the identical value)
+__device__ __forceinline__ double w16_kl_sum(const W16UpdArgs& u) {
+    const int lane = threadIdx.x & 31;
+    const size_t hw = 3 * (size_t)u.hidden + 3;
+    double s = 0.0;
+    for (int q = lane; q < u.nhead; q += 32) s += u.hp[(size_t)q * hw + 3 * u.hidden + 2];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
 // D[M x N] = A[M x K] . B[N x K]^T, bf16 operands, fp32 accumulation, epilogue EPI.
 // Grid (ceil(N/BN), ceil(M/128), splits). Warp 0 lane 0: TMA producer; warp 1
 // lane 0: MMA issuer; all 16 warps: epilogue (warp w: TMEM lanes 32 (w % 4)..
@@ -298,7 +341,25 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     constexpr int TC = tmem_cols(BN);
     constexpr int EW = w_ew<EPI>(), NTH = 128 * EW;
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-    const int col0 = blockIdx.x * BN, row0 = blockIdx.y * W_BM;
+    int col0 = blockIdx.x * BN, row0 = blockIdx.y * W_BM;
+    // the fused SGD launch: tiles y < T1 are gW1 tiles (A = map_a, B = map_b),
+    // the rest [gW0 | gb0] tiles (A = map_o, B = map_ot, 64 columns)
+    const CUtensorMap* pma = &map_a;
+    const CUtensorMap* pmb = &map_b;
+    bool w0tile = false;
+    if constexpr (EPI == W16_EPI_SGD) {
+        const int nN = (g.N + BN - 1) / BN, T1 = ((g.M + W_BM - 1) / W_BM) * nN, t = blockIdx.y;
+        if (t < T1) {
+            row0 = (t / nN) * W_BM;
+            col0 = (t % nN) * BN;
+        } else {
+            w0tile = true;
+            row0 = (t - T1) * W_BM;
+            col0 = 0;
+            pma = &map_o;
+            pmb = &map_ot;
+        }
+    }
     const int nkb = (g.K + W_BK - 1) / W_BK;
     const int per = (nkb + gridDim.z - 1) / gridDim.z;
     const int kb_lo = blockIdx.z * per, kb_hi = min(nkb, kb_lo + per);
@@ -325,9 +386,9 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     W16_TR(g.dbg, 1);
 
     if (tid == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
-        if constexpr (EPI != W16_EPI_PART) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(pma) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(pmb) : "memory");
+        if constexpr (EPI <= W16_EPI_D1T) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_o) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_ot) : "memory");
         }
@@ -337,10 +398,10 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             if (it >= ST) mbar_wait_b(&S.empty[slot], ((it / ST) - 1) & 1);
             mbar_expect(&S.full[slot], bytes);
             const int k0 = (kb_lo + it) * W_BK;
-            tma_2d(&S.a[slot][0], &map_a, k0, row0, &S.full[slot]);
+            tma_2d(&S.a[slot][0], pma, k0, row0, &S.full[slot]);
 #pragma unroll
             for (int h = 0; h < BN / BOX; ++h)
-                tma_2d(&S.b[slot][h * BOX * W_BK], &map_b, k0, col0 + h * BOX, &S.full[slot]);
+                tma_2d(&S.b[slot][h * BOX * W_BK], pmb, k0, col0 + h * BOX, &S.full[slot]);
         }
     } else if (tid == 32) {
         const uint32_t idesc = idesc_bf16(W_BM, MN);
@@ -532,6 +593,141 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             prow[3 * H + tid] = ((T.red[0][tid] + T.red[1][tid]) + T.red[2][tid]) + T.red[3][tid];
         if (lane == 0) bulk_wait_all();
         if (npair > 1) cluster_sync();  // the peer has read this CTA's partial logits
+    } else if constexpr (EPI == W16_EPI_SGD) {
+        // ---- fused split-K reduction + SGD (single-rank path). The S CTAs of
+        //      a cluster (along z) hold the S K-split partials of one output
+        //      tile; CTA cr sums its 128 / S rows of all S partials in split
+        //      order (fp32 partials, fp64 sum: the update kernel's order) through
+        //      distributed shared memory and applies SGD to them
+        //      (policy.cpp:328-332), refreshing the bf16 operand copies. The
+        //      gW1 and [gW0 | gb0] tiles share the launch; every thread of the
+        //      grid also helps sum the head parameters' gradients (b1, W2, b2).
+        const W16UpdArgs& u = g.u;
+        constexpr int RS = BN + 4;  // padded fp32 row stride: conflict-free 16-byte stores
+        constexpr int S = W16_SPLITS, B4 = BN / 4;
+        constexpr int MAXG = (128 / S + 1) * B4 / NTH + 1;  // float4 groups per thread (upper bound)
+        float* R = reinterpret_cast<float*>(base);
+        double* sc = reinterpret_cast<double*>(R + 128 * RS);
+        __nv_bfloat16* TT = reinterpret_cast<__nv_bfloat16*>(sc + 4);  // [BN][24] W1^T staging (<= 24 rows)
+        const int H = u.hidden;
+        const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H;
+        const int ncol = w0tile ? F + 1 : g.N;  // valid output columns
+        if (w == 0) {  // the step's loss (every CTA sums the head partials identically)
+            const double kl = w16_kl_sum(u);
+            if (lane == 0) {
+                sc[0] = kl / (double)u.nb;
+                sc[1] = (double)*u.diverged;
+            }
+        }
+        for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
+            float v[16];
+            tmem_ld16(tq + c0, v);
+            tmem_ld_wait();
+            if (nk == 0) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            }
+            float4* d = reinterpret_cast<float4*>(R + (32 * qw + lane) * RS + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+        // this CTA's rows of the tile: [r_lo, r_hi) (128 rows over S CTAs)
+        const int cr = (int)cluster_rank();
+        const int r_lo = cr * 128 / S, r_hi = (cr + 1) * 128 / S;
+        const int n4 = (r_hi - r_lo) * B4;  // float4 groups of the slice
+        // the old weights of the slice, loaded before the exchange
+        float wold[MAXG][4];
+#pragma unroll
+        for (int t = 0; t < MAXG; ++t) {
+            const int idx = tid + t * NTH, j = row0 + r_lo + idx / B4;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int kl = 4 * (idx % B4) + e;
+                wold[t][e] = 0.f;
+                if (idx >= n4 || j >= g.M || col0 + kl >= ncol) continue;
+                wold[t][e] = w0tile ? u.params[kl < F ? (size_t)j * F + kl : o_b0 + j]
+                                    : u.params[o_w1 + (size_t)j * H + col0 + kl];
+            }
+        }
+        // head parameter gradients: four threads per parameter, each summing a
+        // quarter of the row tiles' head partials, combined in a fixed tree
+        const size_t nh = u.np - o_b1;
+        const size_t gt = (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * NTH + tid;
+        const size_t ph = o_b1 + gt / 4;
+        double gh = 0.0;
+        if (gt / 4 < nh) {
+            const size_t hw = 3 * (size_t)H + 3, o_w2 = o_b1 + H, o_b2 = o_w2 + 2 * (size_t)H;
+            const double* col = ph < o_w2 ? u.hp + 2 * H + (ph - o_b1)
+                                : ph < o_b2 ? u.hp + (ph - o_w2) : u.hp + 3 * H + (ph - o_b2);
+            const int qn = (u.nhead + 3) / 4, q0 = (int)(gt % 4) * qn, q1 = min(u.nhead, q0 + qn);
+            if (q1 > q0) gh = ordered_sum(col + (size_t)q0 * hw, hw, q1 - q0);
+        }
+        gh += __shfl_xor_sync(0xffffffffu, gh, 1);
+        gh += __shfl_xor_sync(0xffffffffu, gh, 2);
+        float wh = 0.f;
+        if (gt % 4 == 0 && gt / 4 < nh) wh = u.params[ph];
+        cluster_sync();  // all S partials are in shared memory
+        double gs[MAXG][4];
+#pragma unroll
+        for (int t = 0; t < MAXG; ++t) {
+            const int idx = tid + t * NTH;
+            gs[t][0] = gs[t][1] = gs[t][2] = gs[t][3] = 0.0;
+            if (idx >= n4) continue;
+            const uint32_t la = smem_u32(R + (r_lo + idx / B4) * RS + 4 * (idx % B4));
+            float pv[S][4];
+#pragma unroll
+            for (int q = 0; q < S; ++q) {
+                uint32_t ra;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(q));
+                asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(pv[q][0]), "=f"(pv[q][1]), "=f"(pv[q][2]), "=f"(pv[q][3])
+                             : "r"(ra)
+                             : "memory");
+            }
+#pragma unroll
+            for (int q = 0; q < S; ++q)  // split order (the update kernel's order)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) gs[t][e] += (double)pv[q][e];
+        }
+        cluster_sync();  // every CTA has read the others' partials
+        const double loss = sc[0];
+        const bool apply = sc[1] < 0.0 && isfinite(loss);  // fit throws before updating (policy.cpp:321-325)
+#pragma unroll
+        for (int t = 0; t < MAXG; ++t) {
+            const int idx = tid + t * NTH;
+            const int rl = idx / B4, j = row0 + r_lo + rl;  // output row = parameter row
+            if (!apply || idx >= n4 || j >= g.M) continue;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int kl = 4 * (idx % B4) + e, k = col0 + kl;
+                if (k >= ncol) continue;
+                const float nw = __double2float_rn((double)wold[t][e] - u.lr * gs[t][e]);
+                const __nv_bfloat16 b = __float2bfloat16_rn(nw);
+                if (w0tile) {  // [X | 1] column: W0 (k < 44), b0 (k == 44)
+                    u.params[k < F ? (size_t)j * F + k : o_b0 + j] = nw;
+                    if (k < F) u.w0p[(size_t)j * 64 + k] = b;
+                } else {
+                    u.params[o_w1 + (size_t)j * H + k] = nw;
+                    u.w1[(size_t)j * H + k] = b;
+                    TT[kl * 24 + rl] = b;
+                }
+            }
+        }
+        if (!w0tile) {
+            __syncthreads();
+            // W1^T [k][j]: the CTA's rows j of column k are contiguous
+            const int j0 = row0 + r_lo, nj = min(r_hi - r_lo, g.M - j0);
+            if (apply && nj > 0)
+                for (int t = tid; t < BN * nj; t += NTH) {
+                    const int kk = t / nj, jj = t % nj;
+                    if (col0 + kk < ncol) u.w1t[(size_t)(col0 + kk) * H + j0 + jj] = TT[kk * 24 + jj];
+                }
+        }
+        if (apply && gt % 4 == 0 && gt / 4 < nh) u.params[ph] = __double2float_rn((double)wh - u.lr * gh);
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && sc[1] < 0.0) {
+            if (isfinite(loss)) *u.epoch_acc += loss * (double)u.nb;
+            else *u.diverged = *u.epoch;
+        }
     } else {
         OutStage& O = reinterpret_cast<OutStage*>(base)[w];
         for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
@@ -589,6 +785,8 @@ template __global__ void w16_gemm_kernel<256, 4, W16_EPI_D1T>(const __grid_const
 template __global__ void w16_gemm_kernel<256, 4, W16_EPI_PART>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
                                                    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
 template __global__ void w16_gemm_kernel<64, 6, W16_EPI_PART>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
+template __global__ void w16_gemm_kernel<128, 6, W16_EPI_SGD>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
                                                    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
 template __global__ void w16_gemm_kernel<128, 6, W16_EPI_PART>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
                                                    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, W16Args);
@@ -682,49 +880,6 @@ __global__ void w16_weights_kernel(const float* __restrict__ params, int H, __nv
     const __nv_bfloat16 b = __float2bfloat16_rn(params[o_w1 + t]);
     w1[t] = b;
     w1t[j * H + k] = b;
-}
-
-// sum_q src[q * stride] in q order, sixteen loads in flight at a time
-template <typename T>
-__device__ __forceinline__ double ordered_sum(const T* __restrict__ src, size_t stride, int n) {
-    double s = 0.0;
-    for (int q = 0; q < n; q += 16) {
-        T v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = q + j < n ? __ldg(src + (size_t)(q + j) * stride) : T(0);
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (q + j < n) s += v[j];
-    }
-    return s;
-}
-
-// Gradient of parameter p (serialization order w0[H][44] b0[H] w1[H][H]
-// b1[H] w2[2][H] b2[2]) from the step's partials, summed in a fixed order.
-__device__ __forceinline__ double w16_grad(const W16UpdArgs& u, size_t p) {
-    const size_t H = u.hidden;
-    const size_t o_b0 = H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + H * H, o_w2 = o_b1 + H, o_b2 = o_w2 + 2 * H;
-    const size_t hw = 3 * H + 3;
-    if (p < o_w1) {  // gW0 | gb0: G5 partials [s5][H][64], column 44 = gb0
-        const size_t j = p < o_b0 ? p / F : p - o_b0, i = p < o_b0 ? p % F : (size_t)F;
-        return ordered_sum(u.p5 + j * 64 + i, H * 64, u.s5);
-    }
-    if (p < o_b1) return ordered_sum(u.p4 + (p - o_w1), H * H, u.s4);   // gW1: G4 partials [s4][H][H]
-    if (p < o_w2) return ordered_sum(u.hp + 2 * H + (p - o_b1), hw, u.nhead);  // gb1
-    if (p < o_b2) return ordered_sum(u.hp + (p - o_w2), hw, u.nhead);          // gW2
-    return ordered_sum(u.hp + 3 * H + (p - o_b2), hw, u.nhead);                // gb2
-}
-
-// KL sum of the step over the head partials (warp 0; fixed lane order + tree:
-// every block computes the identical value)
-__device__ __forceinline__ double w16_kl_sum(const W16UpdArgs& u) {
-    const int lane = threadIdx.x & 31;
-    const size_t hw = 3 * (size_t)u.hidden + 3;
-    double s = 0.0;
-    for (int q = lane; q < u.nhead; q += 32) s += u.hp[(size_t)q * hw + 3 * u.hidden + 2];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    return s;
 }
 
 // mode 0: reduce + SGD + refreshed bf16 copies (one rank); 1: reduce into the

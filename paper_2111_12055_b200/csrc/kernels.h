@@ -181,6 +181,29 @@ constexpr int W16_EPI_H1 = 0;    // relu(acc + bias) -> bf16 row-major + transpo
 constexpr int W16_EPI_HEAD = 1;  // fused softmax/KL head over full rows
 constexpr int W16_EPI_D1T = 2;   // acc [mask > 0] -> bf16 transposed
 constexpr int W16_EPI_PART = 3;  // fp32 split-K partials
+constexpr int W16_EPI_SGD = 4;   // gW1 and [gW0|gb0] tiles, split-K over W16_SPLITS-CTA clusters -> SGD
+                                 // of every parameter + bf16 copies (one launch, no update kernel)
+constexpr int W16_SPLITS = 6;    // K splits (= cluster size along z) of the fused SGD epilogues:
+                                 // 22 clusters of 6 fit on 148 SMs at once (of 7 or 8: 15 < 16 tiles)
+struct W16UpdArgs {
+    float* params;                 // fp32 master weights (flat serialization order)
+    int hidden;
+    size_t np, nb;
+    double lr;
+    const float* p4;               // gW1 partials [s4][H][H]
+    int s4;
+    const float* p5;               // gW0|gb0 partials [s5][H][64]
+    int s5;
+    const double* hp;              // head partials [nhead][3H + 3]
+    int nhead;
+    float* g_out;                  // flat gradient (data-parallel path)
+    double* loss_sum;              // KL sum (data-parallel path)
+    __nv_bfloat16 *w0p, *w1, *w1t; // bf16 operand copies
+    const int* epoch;
+    int* diverged;
+    double* epoch_acc;
+    int dbg;                       // timeline slot (GBX_PHASE_TIMING builds), -1 = none
+};
 struct W16Args {
     int M, N, K;
     const float* bias;             // H1: b0, HEAD: b1
@@ -201,25 +224,7 @@ struct W16Args {
     double inv_b;
     double* head_part;             // [row tiles][3N + 3]: gW2_0, gW2_1, gb1, gb2_0, gb2_1, KL
     int dbg;                       // timeline slot (GBX_PHASE_TIMING builds), -1 = none
-};
-struct W16UpdArgs {
-    float* params;                 // fp32 master weights (flat serialization order)
-    int hidden;
-    size_t np, nb;
-    double lr;
-    const float* p4;               // gW1 partials [s4][H][H]
-    int s4;
-    const float* p5;               // gW0|gb0 partials [s5][H][64]
-    int s5;
-    const double* hp;              // head partials [nhead][3H + 3]
-    int nhead;
-    float* g_out;                  // flat gradient (data-parallel path)
-    double* loss_sum;              // KL sum (data-parallel path)
-    __nv_bfloat16 *w0p, *w1, *w1t; // bf16 operand copies
-    const int* epoch;
-    int* diverged;
-    double* epoch_acc;
-    int dbg;                       // timeline slot (GBX_PHASE_TIMING builds), -1 = none
+    W16UpdArgs u;                  // SGD1 / SGD0: the step's update
 };
 // epilogue warps per TMEM lane quarter of w16_gemm_kernel<.., EPI> (128 x this threads)
 template <int EPI>

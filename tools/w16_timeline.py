@@ -56,10 +56,12 @@ for buf in res:
         t0 = buf[8 * s, 0, 0]
         nxt = buf[8 * (s + 1), 0, 0] if s < 7 else np.nan
         rows.append([[buf[8 * s + k, 0, 0] - t0, buf[8 * s + k, 1, 0] - t0, buf[8 * s + k, 2, 1] - t0,
-                      buf[8 * s + k, 3, 1] - t0] for k in range(7)] + [[nxt - t0] * 4])
+                      buf[8 * s + k, 3, 1] - t0, buf[8 * s + k, 1, 1] - t0, buf[8 * s + k, 2, 0] - t0,
+                      buf[8 * s + k, 3, 0] - t0] for k in range(7)] + [[nxt - t0] * 7])
 a = np.nanmedian(np.array(rows), axis=0)
 print(f"H={H} B={b}: step (gather entry to next gather entry) {a[7][0] / 1e3:.2f} us  (median of steps 1-6)")
-print(f"{'launch':24s} {'1st entry':>10s} {'ready':>8s} {'mainloop':>9s} {'last exit':>10s}   (us from step start)")
+print(f"{'launch':24s} {'1st entry':>10s} {'ready':>13s} {'main loop':>13s} {'exit':>13s}   (us from step start;"
+      " min-max over CTAs)")
 for k in range(7):
-    e, r, m, x = a[k] / 1e3
-    print(f"{names[k]:24s} {e:10.2f} {r:8.2f} {m:9.2f} {x:10.2f}")
+    e, r, m, x, r1, m0, x0 = a[k] / 1e3
+    print(f"{names[k]:24s} {e:10.2f} {r:6.2f}-{r1:6.2f} {m0:6.2f}-{m:6.2f} {x0:6.2f}-{x:6.2f}")
