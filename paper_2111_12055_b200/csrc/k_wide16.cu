@@ -42,7 +42,7 @@ using namespace tc;
 // eight steps of a fit — slot = step * 8 + launch (0 gather, 1..5 G1..G5,
 // 6 update); points 0 entry, 1 inputs ready (after griddepcontrol.wait),
 // 2 main loop done, 3 exit; {min, max} over the CTAs (globaltimer ns).
-__device__ unsigned long long g_w16_tr[64][4][2];
+__device__ unsigned long long g_w16_tr[64][8][2];  // points 4..7: epilogue phases (head / SGD)
 __device__ unsigned long long g_w16_steps[4096];  // every step: first gather CTA entry
 #define W16_TR(slot, pt)                                                          \
     do {                                                                          \
@@ -492,6 +492,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         }
         T.lg[cg][32 * qw + lane][0] = l0a + l0b;
         T.lg[cg][32 * qw + lane][1] = l1a + l1b;
+        W16_TR(g.dbg, 4);
         __syncthreads();
         const int rl = 32 * qw + lane;
         if (cg == 0) {
@@ -535,6 +536,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             }
         }
         const float d3f0 = (float)d30, d3f1 = (float)d31;
+        W16_TR(g.dbg, 5);
         // pass 2 (fp32): D2 = (d3 w2) [h2 > 0] -> D2 (row-major), D2^T (TMA
         // stores); column sums gW2 = sum d3 h2, gb1 = sum D2 over the warp's 32
         // rows (fp32 shuffle trees), per lane quarter in shared memory
@@ -570,6 +572,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 T.wsum[qw][2][c0 + lane] = (double)s2;
             }
         }
+        W16_TR(g.dbg, 6);
         // gb2 and KL of the rows (column group 0 only; fixed shuffle tree)
         const bool first = cg == 0 && crank == 0;
         double r0 = first ? d30 : 0.0, r1 = first ? d31 : 0.0, r2 = first ? loss : 0.0;
@@ -666,7 +669,9 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         gh += __shfl_xor_sync(0xffffffffu, gh, 2);
         float wh = 0.f;
         if (gt % 4 == 0 && gt / 4 < nh) wh = u.params[ph];
+        W16_TR(g.dbg, 4);
         cluster_sync();  // all S partials are in shared memory
+        W16_TR(g.dbg, 5);
         double gs[MAXG][4];
 #pragma unroll
         for (int t = 0; t < MAXG; ++t) {
@@ -689,7 +694,9 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
                 for (int e = 0; e < 4; ++e) gs[t][e] += (double)pv[q][e];
         }
+        W16_TR(g.dbg, 6);
         cluster_sync();  // every CTA has read the others' partials
+        W16_TR(g.dbg, 7);
         const double loss = sc[0];
         const bool apply = sc[1] < 0.0 && isfinite(loss);  // fit throws before updating (policy.cpp:321-325)
 #pragma unroll
@@ -988,9 +995,9 @@ __global__ void __launch_bounds__(256) w16_update_kernel(W16UpdArgs u, int mode)
 extern "C" int gbxcu_debug_w16_trace(unsigned long long* out, int reset) {
     if (out && cudaMemcpyFromSymbol(out, gbxcu::g_w16_tr, sizeof(gbxcu::g_w16_tr)) != cudaSuccess) return 3;
     if (reset) {
-        static unsigned long long z[64][4][2];
+        static unsigned long long z[64][8][2];
         for (int i = 0; i < 64; ++i)
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < 8; ++j) {
                 z[i][j][0] = ~0ull;
                 z[i][j][1] = 0;
             }

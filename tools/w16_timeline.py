@@ -45,7 +45,7 @@ for rep in range(5):
     lib.gbxcu_debug_w16_trace(None, 1)
     run()
     torch.cuda.synchronize()
-    buf = np.zeros((64, 4, 2), np.uint64)
+    buf = np.zeros((64, 8, 2), np.uint64)
     lib.gbxcu_debug_w16_trace(buf.ctypes.data, 0)
     res.append(buf.astype(np.float64))
 names = ["gather", "G1 (X W0^T)", "G2 (H1 W1^T + head)", "G3 (D2 W1)", "G4 (gW1 split-K)", "G5 (gW0 split-K)",
@@ -59,9 +59,19 @@ for buf in res:
                       buf[8 * s + k, 3, 1] - t0, buf[8 * s + k, 1, 1] - t0, buf[8 * s + k, 2, 0] - t0,
                       buf[8 * s + k, 3, 0] - t0] for k in range(7)] + [[nxt - t0] * 7])
 a = np.nanmedian(np.array(rows), axis=0)
+ph = []
+for buf in res:
+    for s in range(1, 7):
+        t0 = buf[8 * s, 0, 0]
+        ph.append([[buf[8 * s + k, q, 0] - t0, buf[8 * s + k, q, 1] - t0] for k in (2, 4) for q in range(4, 8)])
+ph = np.nanmedian(np.array(ph), axis=0) / 1e3
 print(f"H={H} B={b}: step (gather entry to next gather entry) {a[7][0] / 1e3:.2f} us  (median of steps 1-6)")
 print(f"{'launch':24s} {'1st entry':>10s} {'ready':>13s} {'main loop':>13s} {'exit':>13s}   (us from step start;"
       " min-max over CTAs)")
 for k in range(7):
     e, r, m, x, r1, m0, x0 = a[k] / 1e3
     print(f"{names[k]:24s} {e:10.2f} {r:6.2f}-{r1:6.2f} {m0:6.2f}-{m:6.2f} {x0:6.2f}-{x:6.2f}")
+print("G2 head phases (min-max over CTAs): logits done, softmax done, pass 2 done, sums written:")
+print("   " + "  ".join(f"{x:6.2f}-{y:6.2f}" for x, y in ph[0:4]))
+print("G4/G5 SGD phases: partial dumped, barrier 1 passed, reduce done, barrier 2 passed:")
+print("   " + "  ".join(f"{x:6.2f}-{y:6.2f}" for x, y in ph[4:8]))
