@@ -216,6 +216,7 @@ struct HeadScratch {
     double red[4 * W_EW_MAX][3];
 };
 
+
 // Column sums of a warp's 32 rows: v[16] = this lane's (row's) values of 16
 // columns; returns, in lanes l and l ^ 16, the sum over the 32 lanes of
 // column l & 15 (recursive halving over lane bits 3..0, then bit 4: a fixed
@@ -426,12 +427,18 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     // (the head's targets: a gather through the record indices, issued while
     //  the MMAs run)
     double tg0 = 0.0, tg1 = 0.0;
+    float hb1 = 0.f, hw20 = 0.f, hw21 = 0.f;  // (the head's b1 / w2 of column col0 + tid)
     if constexpr (EPI == W16_EPI_HEAD) {
         const int rr = row0 + 32 * (w & 3) + (tid & 31);
         if (rr < g.M) {
             const size_t rec = g.rows ? g.rows[rr] : (size_t)rr;
             tg0 = g.tgt[2 * rec];
             tg1 = g.tgt[2 * rec + 1];
+        }
+        if (tid < BN && col0 + tid < g.N) {
+            hb1 = g.bias[col0 + tid];
+            hw20 = g.w2[col0 + tid];
+            hw21 = g.w2[g.N + col0 + tid];
         }
     }
     __syncwarp();
@@ -456,23 +463,25 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         HeadScratch& T = *reinterpret_cast<HeadScratch*>(base);
         OutStage& O = reinterpret_cast<OutStage*>(base + head_stage_off())[w];
         const int H = g.N;
-        for (int c = col0 + tid; c < min(H, col0 + BN); c += NTH) {
-            T.b1[c] = g.bias[c];
-            T.w2[0][c] = g.w2[c];
-            T.w2[1][c] = g.w2[H + c];
-            T.w2d[0][c] = (double)g.w2[c];
-            T.w2d[1][c] = (double)g.w2[H + c];
+        static_assert(BN <= NTH, "one head column per thread");
+        if (tid < BN && col0 + tid < H) {
+            const int c = col0 + tid;
+            T.b1[c] = hb1;
+            T.w2[0][c] = hw20;
+            T.w2[1][c] = hw21;
+            T.w2d[0][c] = (double)hw20;
+            T.w2d[1][c] = (double)hw21;
         }
         __syncthreads();
         const int cb = col0 + cbeg, cend = min(H, cb + CW);
         // pass 1: h2 = relu(acc + b1); partial logits in fp64 (two chains per output)
         double l0a = 0.0, l0b = 0.0, l1a = 0.0, l1b = 0.0;
-        for (int c0 = cb; c0 < cend; c0 += 16) {
-            float v[16];
-            tmem_ld16(tq + (c0 - col0), v);
+        for (int c0 = cb; c0 < cend; c0 += 32) {
+            float v[32];
+            tmem_ld32(tq + (c0 - col0), v);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 16; i += 4) {
+            for (int i = 0; i < 32; i += 4) {
                 const float4 bb = *reinterpret_cast<const float4*>(&T.b1[c0 + i]);
                 const double2 w0a = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i]);
                 const double2 w0b = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i + 2]);
@@ -540,10 +549,14 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         // pass 2 (fp32): D2 = (d3 w2) [h2 > 0] -> D2 (row-major), D2^T (TMA
         // stores); column sums gW2 = sum d3 h2, gb1 = sum D2 over the warp's 32
         // rows (fp32 shuffle trees), per lane quarter in shared memory
+        float vn[16];  // the next chunk's accumulators, loaded one chunk ahead
+        tmem_ld16(tq + (cb - col0), vn);
         for (int c0 = cb; c0 < cend; c0 += 16) {
             float v[16], h[16], d[16];
-            tmem_ld16(tq + (c0 - col0), v);
             tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = vn[i];
+            if (c0 + 16 < cend) tmem_ld16(tq + (c0 + 16 - col0), vn);
 #pragma unroll
             for (int i = 0; i < 16; i += 4) {
                 const float4 bb = *reinterpret_cast<const float4*>(&T.b1[c0 + i]);
@@ -551,19 +564,34 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 const float4 wb = *reinterpret_cast<const float4*>(&T.w2[1][c0 + i]);
                 const float b4[4] = {bb.x, bb.y, bb.z, bb.w}, a4[4] = {wa.x, wa.y, wa.z, wa.w},
                             c4[4] = {wb.x, wb.y, wb.z, wb.w};
+                // (packed fp32 pairs: each half rounds exactly like the scalar op)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    h[i + j] = row_ok ? fmaxf(v[i + j] + b4[j], 0.f) : 0.f;
-                    d[i + j] = h[i + j] > 0.f ? __fadd_rn(__fmul_rn(d3f0, a4[j]), __fmul_rn(d3f1, c4[j])) : 0.f;
+                for (int j = 0; j < 4; j += 2) {
+                    const float2 s2v = __fadd2_rn(make_float2(v[i + j], v[i + j + 1]), make_float2(b4[j], b4[j + 1]));
+                    const float2 da = __fmul2_rn(make_float2(d3f0, d3f0), make_float2(a4[j], a4[j + 1]));
+                    const float2 dc = __fmul2_rn(make_float2(d3f1, d3f1), make_float2(c4[j], c4[j + 1]));
+                    const float2 dd = __fadd2_rn(da, dc);
+                    h[i + j] = row_ok ? fmaxf(s2v.x, 0.f) : 0.f;
+                    h[i + j + 1] = row_ok ? fmaxf(s2v.y, 0.f) : 0.f;
+                    d[i + j] = h[i + j] > 0.f ? dd.x : 0.f;
+                    d[i + j + 1] = h[i + j + 1] > 0.f ? dd.y : 0.f;
                 }
             }
             stage_chunk<true, true>(O, (c0 - cb) >> 4, d, &map_o, &map_ot, c0, rw0, lane);
             float p[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) p[i] = d3f0 * h[i];
+            for (int i = 0; i < 16; i += 2) {
+                const float2 q = __fmul2_rn(make_float2(d3f0, d3f0), make_float2(h[i], h[i + 1]));
+                p[i] = q.x;
+                p[i + 1] = q.y;
+            }
             const float s0 = col_reduce16(p, lane);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) p[i] = d3f1 * h[i];
+            for (int i = 0; i < 16; i += 2) {
+                const float2 q = __fmul2_rn(make_float2(d3f1, d3f1), make_float2(h[i], h[i + 1]));
+                p[i] = q.x;
+                p[i + 1] = q.y;
+            }
             const float s1 = col_reduce16(p, lane);
             const float s2 = col_reduce16(d, lane);
             if (lane < 16) {
