@@ -56,7 +56,6 @@ constexpr int NTC = 512;           // threads per CTA
 constexpr int TBR = 32;            // records per step
 constexpr int J1 = H1 / CL;        // layer-1 units per CTA (16)
 constexpr int K2 = H2 / CL;        // layer-2 units per CTA (8)
-constexpr int XS = F + 1;          // odd strides: column reads across rows are conflict-free
 constexpr int W0S = F + 1;
 constexpr int W1S = H1 + 1;
 constexpr int WCS = J1 + 1;
@@ -68,6 +67,7 @@ constexpr int DS1 = J1 + 1;
 constexpr int Q_W0 = 0, Q_B0 = Q_W0 + J1 * F, Q_W1 = Q_B0 + J1, Q_B1 = Q_W1 + K2 * H1,
               Q_W2 = Q_B1 + K2, Q_B2 = Q_W2 + A * K2, Q_LOSS = Q_B2 + A, NQ = Q_LOSS + 1;
 constexpr int QPT = (NQ + NTC - 1) / NTC;  // chains per thread (3)
+static_assert(QPT == 3, "the G phase is written for three chains per thread");
 
 struct ClSmem {
     double w0[J1 * W0S];   // own rows of W0: [jj][i]
@@ -77,7 +77,6 @@ struct ClSmem {
     double b1[K2];
     double w2[2][A * H2];  // all of W2 (F3, B1), double-buffered by step
     double b2[2][A];
-    double x[TBR * XS];
     double h1[TBR * HS1];  // all 64 columns (own computed, the rest gathered)
     double h2[TBR * HS2];  // all 32
     double d2[TBR * HS2];  // all 32
@@ -247,11 +246,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
         if (h2) h2 = cl_next(a, n_steps, s2, r2, n2);
 
         CL_MARK(0);  // step top (wait, prefetch issue)
-        // ---- P0: staged fp32 -> fp64
-        for (int t = tid; t < TBR * F; t += NTC) {
-            const int r = t / F;
-            S.x[r * XS + (t - r * F)] = (double)S.stage_f[k][t];
-        }
+        // ---- P0: the step's targets (its fp32 features are read in place from
+        //      the staging slot: widened per use, exactly)
+        const float* xs = S.stage_f[k];
         if (tid < 2 * TBR) S.tgt[tid] = S.stage_t[k][tid];
         __syncthreads();
 
@@ -261,9 +258,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
             const int r = tid >> 4, jj = tid & 15;
             double acc = S.b0[jj];
             const double* wr = S.w0 + jj * W0S;
-            const double* xr = S.x + r * XS;
+            const float* xr = xs + r * F;
 #pragma unroll
-            for (int i = 0; i < F; ++i) acc = fma(wr[i], xr[i], acc);  // fp32 x fp32 exact in fp64
+            for (int i = 0; i < F; ++i) acc = fma(wr[i], (double)xr[i], acc);  // fp32 x fp32 exact in fp64
             S.h1[r * HS1 + c * J1 + jj] = acc > 0.0 ? acc : 0.0;
         }
         CL_MARK(2);  // F1
@@ -395,17 +392,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
         {
             const double* pa[QPT];
             const double* pb[QPT];
+            const float* px[QPT];  // W0 chains: B = the fp32 features (widened exactly)
             int sa[QPT], sb[QPT];
 #pragma unroll
             for (int m = 0; m < QPT; ++m) {
                 const int q = tid + m * NTC;
                 pa[m] = &S.zero;  // (not owned here: a dummy chain of zeros)
                 pb[m] = &S.one;
+                px[m] = nullptr;
                 sa[m] = sb[m] = 0;
                 if (q < Q_B0) {
                     const int jj = q / F, i = q - jj * F;
                     pa[m] = S.d1 + jj; sa[m] = DS1;
-                    pb[m] = S.x + i; sb[m] = XS;
+                    px[m] = xs + i; sb[m] = F;
                 } else if (q < Q_W1) {
                     pa[m] = S.d1 + (q - Q_B0); sa[m] = DS1;
                 } else if (q < Q_B1) {
@@ -424,10 +423,24 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
                     pa[m] = S.kl; sa[m] = 1;
                 }
             }
+            // chain 0 is a W0 chain on every thread (Q_B0 > NTC), chain 1 on
+            // threads < Q_B0 - NTC (whole warps), chain 2 never
+            static_assert(Q_B0 >= NTC && Q_B0 - NTC <= NTC && (Q_B0 - NTC) % 32 == 0 && 2 * NTC >= Q_B0,
+                          "W0 chain layout");
+            if (tid < Q_B0 - NTC) {
 #pragma unroll
-            for (int r = 0; r < TBR; ++r) {
+                for (int r = 0; r < TBR; ++r) {
+                    g[0] = madd_rn(g[0], pa[0][r * sa[0]], (double)px[0][r * F]);
+                    g[1] = madd_rn(g[1], pa[1][r * sa[1]], (double)px[1][r * F]);
+                    g[2] = madd_rn(g[2], pa[2][r * sa[2]], pb[2][r * sb[2]]);
+                }
+            } else {
 #pragma unroll
-                for (int m = 0; m < QPT; ++m) g[m] = madd_rn(g[m], pa[m][r * sa[m]], pb[m][r * sb[m]]);
+                for (int r = 0; r < TBR; ++r) {
+                    g[0] = madd_rn(g[0], pa[0][r * sa[0]], (double)px[0][r * F]);
+                    g[1] = madd_rn(g[1], pa[1][r * sa[1]], pb[1][r * sb[1]]);
+                    g[2] = madd_rn(g[2], pa[2][r * sa[2]], pb[2][r * sb[2]]);
+                }
             }
 #pragma unroll
             for (int m = 0; m < QPT; ++m)
