@@ -15,10 +15,10 @@
 // and layer-2 units K_c = [8c, 8c+8) — and the activations the next phase
 // needs in full move through distributed shared memory:
 //   P0  x (all 32 records, every CTA)
-//   F1  h1[:, J_c]                       -> cluster barrier, gather h1 (48 cols)
-//   F2  h2[:, K_c]                       -> cluster barrier, gather h2 (24 cols)
+//   F1  h1[:, J_c]  pushed to every CTA  -> cluster barrier
+//   F2  h2[:, K_c]  pushed               -> cluster barrier
 //   F3  logits / softmax / KL / d3 (all records, redundantly in every CTA)
-//   B1  d2[:, K_c]                       -> cluster barrier, gather d2 (24 cols)
+//   B1  d2[:, K_c]  pushed               -> cluster barrier
 //   B2  d1[:, J_c]
 //   G   the gradient chains of the parameters CTA c owns (W0/b0 rows J_c,
 //       W1/b1 rows K_c, W2 columns K_c, b2 on CTA 0, the loss everywhere)
@@ -77,9 +77,13 @@ struct ClSmem {
     double b1[K2];
     double w2[2][A * H2];  // all of W2 (F3, B1), double-buffered by step
     double b2[2][A];
-    double h1[TBR * HS1];  // all 64 columns (own computed, the rest gathered)
-    double h2[TBR * HS2];  // all 32
-    double d2[TBR * HS2];  // all 32
+    // activations, double-buffered by step parity: every CTA pushes its own
+    // columns into all four copies (distributed shared memory stores) before
+    // the cluster barrier; a push of step s + 2 cannot reach a CTA still
+    // reading step s's copy (three cluster barriers lie between them)
+    double h1[2][TBR * HS1];  // all 64 columns
+    double h2[2][TBR * HS2];  // all 32
+    double d2[2][TBR * HS2];  // all 32
     double d1[TBR * DS1];  // own columns
     double d3[TBR * 2];
     double tgt[TBR * 2];
@@ -107,13 +111,7 @@ __device__ __forceinline__ uint32_t cl_addr(const void* local, uint32_t rank) {
                  : "r"((uint32_t)__cvta_generic_to_shared(local)), "r"(rank));
     return ra;
 }
-// (volatile + memory clobber: never moved across the cluster barriers; a
-//  gather issues all its loads before their first use, so they overlap)
-__device__ __forceinline__ double cl_ld(const double* local, uint32_t rank) {
-    double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(cl_addr(local, rank)) : "memory");
-    return v;
-}
+// (volatile + memory clobber: never moved across the cluster barriers)
 __device__ __forceinline__ void cl_st(double* local, uint32_t rank, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(cl_addr(local, rank)), "d"(v) : "memory");
 }
@@ -179,7 +177,7 @@ size_t train_cl_smem_bytes() { return sizeof(ClSmem); }
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch_cluster_kernel(TrainArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ClSmem& S = *reinterpret_cast<ClSmem*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const int c = (int)cl_rank();
     if (*a.diverged_epoch >= 0) return;  // (uniform over the cluster)
     const long n_steps = (long)((a.n + a.batch - 1) / a.batch);
@@ -261,63 +259,38 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
             const float* xr = xs + r * F;
 #pragma unroll
             for (int i = 0; i < F; ++i) acc = fma(wr[i], (double)xr[i], acc);  // fp32 x fp32 exact in fp64
-            S.h1[r * HS1 + c * J1 + jj] = acc > 0.0 ? acc : 0.0;
+            const double h = acc > 0.0 ? acc : 0.0;
+            double* dst = &S.h1[k][r * HS1 + c * J1 + jj];
+            *dst = h;
+#pragma unroll
+            for (int o = 1; o < CL; ++o) cl_st(dst, (uint32_t)((c + o) % CL), h);
         }
         CL_MARK(2);  // F1
         cl_sync();
         CL_MARK(3);  // barrier 1
-        // gather the other CTAs' h1 columns (32 records x 48 units)
-        {
-            constexpr int NG = TBR * (H1 - J1) / NTC;  // 3 per thread, all in flight
-            double v[NG];
-            int at[NG];
-#pragma unroll
-            for (int u = 0; u < NG; ++u) {
-                const int t = tid + u * NTC, r = t / (H1 - J1), q = t - r * (H1 - J1);
-                const int j = q < c * J1 ? q : q + J1;  // skip the own block
-                at[u] = r * HS1 + j;
-                v[u] = cl_ld(&S.h1[at[u]], (uint32_t)(j / J1));
-            }
-#pragma unroll
-            for (int u = 0; u < NG; ++u) S.h1[at[u]] = v[u];
-        }
-        __syncthreads();
-
         CL_MARK(4);  // gather h1
         // ---- F2: h2[r][8c + kk] = relu(b1 + sum_j w1[k][j] h1[r][j]), mul-then-add
         if (tid < TBR * K2) {
             const int r = tid >> 3, kk = tid & 7;
             double acc = S.b1[kk];
             const double* wr = S.w1r + kk * W1S;
-            const double* hr = S.h1 + r * HS1;
+            const double* hr = S.h1[k] + r * HS1;
 #pragma unroll 16
             for (int j = 0; j < H1; ++j) acc = madd_rn(acc, wr[j], hr[j]);
-            S.h2[r * HS2 + c * K2 + kk] = acc > 0.0 ? acc : 0.0;
+            const double h = acc > 0.0 ? acc : 0.0;
+            double* dst = &S.h2[k][r * HS2 + c * K2 + kk];
+            *dst = h;
+#pragma unroll
+            for (int o = 1; o < CL; ++o) cl_st(dst, (uint32_t)((c + o) % CL), h);
         }
         cl_sync();
-        {
-            constexpr int NG = (TBR * (H2 - K2) + NTC - 1) / NTC;  // 2 per thread
-            double v[NG];
-            int at[NG];
-#pragma unroll
-            for (int u = 0; u < NG; ++u) {
-                const int t = tid + u * NTC, r = t / (H2 - K2), q = t - r * (H2 - K2);
-                const int kx = q < c * K2 ? q : q + K2;
-                at[u] = t < TBR * (H2 - K2) ? r * HS2 + kx : -1;
-                if (at[u] >= 0) v[u] = cl_ld(&S.h2[at[u]], (uint32_t)(kx / K2));
-            }
-#pragma unroll
-            for (int u = 0; u < NG; ++u)
-                if (at[u] >= 0) S.h2[at[u]] = v[u];
-        }
-        __syncthreads();
 
         CL_MARK(5);  // F2 + barrier 2 + gather h2
         // ---- F3 (all records, identical in every CTA) + B1 (own columns)
         if (tid < 2 * TBR) {
             const int r = tid >> 1, a2 = tid & 1;
             double l = S.b2[wb][a2];
-            const double* h = S.h2 + r * HS2;
+            const double* h = S.h2[k] + r * HS2;
             const double* wr = S.w2[wb] + a2 * H2;
 #pragma unroll 8
             for (int kx = 0; kx < H2; ++kx) l = madd_rn(l, wr[kx], h[kx]);
@@ -347,36 +320,24 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
                 const int kx = c * K2 + (K2 / 2) * a2 + q;
                 double d = madd_rn(0.0, d30, S.w2[wb][kx]);
                 d = madd_rn(d, d31, S.w2[wb][H2 + kx]);
-                S.d2[r * HS2 + kx] = h[kx] <= 0.0 ? 0.0 : d;
+                const double dv = h[kx] <= 0.0 ? 0.0 : d;
+                double* dst = &S.d2[k][r * HS2 + kx];
+                *dst = dv;
+#pragma unroll
+                for (int o = 1; o < CL; ++o) cl_st(dst, (uint32_t)((c + o) % CL), dv);
             }
         }
         cl_sync();
-        {
-            constexpr int NG = (TBR * (H2 - K2) + NTC - 1) / NTC;
-            double v[NG];
-            int at[NG];
-#pragma unroll
-            for (int u = 0; u < NG; ++u) {
-                const int t = tid + u * NTC, r = t / (H2 - K2), q = t - r * (H2 - K2);
-                const int kx = q < c * K2 ? q : q + K2;
-                at[u] = t < TBR * (H2 - K2) ? r * HS2 + kx : -1;
-                if (at[u] >= 0) v[u] = cl_ld(&S.d2[at[u]], (uint32_t)(kx / K2));
-            }
-#pragma unroll
-            for (int u = 0; u < NG; ++u)
-                if (at[u] >= 0) S.d2[at[u]] = v[u];
-        }
-        __syncthreads();
 
         CL_MARK(6);  // F3 + B1 + barrier 3 + gather d2
         // ---- B2: d1[r][jj] = sum_k d2[r][k] w1[k][16c + jj], masked by h1 > 0
         {
             const int r = tid >> 4, jj = tid & 15;
             double acc = 0.0;
-            const double* dr = S.d2 + r * HS2;
+            const double* dr = S.d2[k] + r * HS2;
 #pragma unroll
             for (int kx = 0; kx < H2; ++kx) acc = madd_rn(acc, dr[kx], S.w1c[wb][kx * WCS + jj]);
-            S.d1[r * DS1 + jj] = S.h1[r * HS1 + c * J1 + jj] <= 0.0 ? 0.0 : acc;
+            S.d1[r * DS1 + jj] = S.h1[k][r * HS1 + c * J1 + jj] <= 0.0 ? 0.0 : acc;
         }
         __syncthreads();
         // (no cluster barrier: the SGD below writes the OTHER copy buffer, which
@@ -409,14 +370,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
                     pa[m] = S.d1 + (q - Q_B0); sa[m] = DS1;
                 } else if (q < Q_B1) {
                     const int kk = (q - Q_W1) / H1, j = (q - Q_W1) % H1;
-                    pa[m] = S.d2 + c * K2 + kk; sa[m] = HS2;
-                    pb[m] = S.h1 + j; sb[m] = HS1;
+                    pa[m] = S.d2[k] + c * K2 + kk; sa[m] = HS2;
+                    pb[m] = S.h1[k] + j; sb[m] = HS1;
                 } else if (q < Q_W2) {
-                    pa[m] = S.d2 + c * K2 + (q - Q_B1); sa[m] = HS2;
+                    pa[m] = S.d2[k] + c * K2 + (q - Q_B1); sa[m] = HS2;
                 } else if (q < Q_B2) {
                     const int a2 = (q - Q_W2) / K2, kk = (q - Q_W2) % K2;
                     pa[m] = S.d3 + a2; sa[m] = 2;
-                    pb[m] = S.h2 + c * K2 + kk; sb[m] = HS2;
+                    pb[m] = S.h2[k] + c * K2 + kk; sb[m] = HS2;
                 } else if (q < Q_LOSS) {
                     if (c == 0) { pa[m] = S.d3 + (q - Q_B2); sa[m] = 2; }
                 } else if (q == Q_LOSS) {
