@@ -643,30 +643,22 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         const int H = u.hidden;
         const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H;
         const int ncol = w0tile ? F + 1 : g.N;  // valid output columns
-        if (w == 0) {  // the step's loss (every CTA sums the head partials identically)
-            const double kl = w16_kl_sum(u);
-            if (lane == 0) {
-                sc[0] = kl / (double)u.nb;
-                sc[1] = (double)*u.diverged;
-            }
-        }
-        for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
-            float v[16];
-            tmem_ld16(tq + c0, v);
-            tmem_ld_wait();
-            if (nk == 0) {
+        // every global load of the epilogue is issued first (the step's KL
+        // partials, the slice's old weights, the head partials) and consumed
+        // after the TMEM dump: one round trip, overlapped with it
+        const size_t hwd = 3 * (size_t)H + 3;
+        double klv[2] = {0.0, 0.0};
+        int dv = -1;
+        if (w == 0) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = 0.f;
-            }
-            float4* d = reinterpret_cast<float4*>(R + (32 * qw + lane) * RS + c0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            for (int t = 0; t < 2; ++t)
+                if (lane + 32 * t < u.nhead) klv[t] = u.hp[(size_t)(lane + 32 * t) * hwd + 3 * H + 2];
+            dv = *u.diverged;
         }
         // this CTA's rows of the tile: [r_lo, r_hi) (128 rows over S CTAs)
         const int cr = (int)cluster_rank();
         const int r_lo = cr * 128 / S, r_hi = (cr + 1) * 128 / S;
         const int n4 = (r_hi - r_lo) * B4;  // float4 groups of the slice
-        // the old weights of the slice, loaded before the exchange
         float wold[MAXG][4];
 #pragma unroll
         for (int t = 0; t < MAXG; ++t) {
@@ -685,18 +677,48 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         const size_t nh = u.np - o_b1;
         const size_t gt = (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * NTH + tid;
         const size_t ph = o_b1 + gt / 4;
-        double gh = 0.0;
+        constexpr int HQ = 16;  // head partial rows per thread (nhead <= 64 in one batch)
+        double hv[HQ];
+        int q0 = 0, q1 = 0;
+        const double* hcol = u.hp;
         if (gt / 4 < nh) {
-            const size_t hw = 3 * (size_t)H + 3, o_w2 = o_b1 + H, o_b2 = o_w2 + 2 * (size_t)H;
-            const double* col = ph < o_w2 ? u.hp + 2 * H + (ph - o_b1)
-                                : ph < o_b2 ? u.hp + (ph - o_w2) : u.hp + 3 * H + (ph - o_b2);
-            const int qn = (u.nhead + 3) / 4, q0 = (int)(gt % 4) * qn, q1 = min(u.nhead, q0 + qn);
-            if (q1 > q0) gh = ordered_sum(col + (size_t)q0 * hw, hw, q1 - q0);
+            const size_t o_w2 = o_b1 + H, o_b2 = o_w2 + 2 * (size_t)H;
+            hcol = ph < o_w2 ? u.hp + 2 * H + (ph - o_b1) : ph < o_b2 ? u.hp + (ph - o_w2) : u.hp + 3 * H + (ph - o_b2);
+            const int qn = (u.nhead + 3) / 4;
+            q0 = (int)(gt % 4) * qn;
+            q1 = min(u.nhead, q0 + qn);
         }
-        gh += __shfl_xor_sync(0xffffffffu, gh, 1);
-        gh += __shfl_xor_sync(0xffffffffu, gh, 2);
+#pragma unroll
+        for (int t = 0; t < HQ; ++t) hv[t] = q0 + t < q1 ? __ldg(hcol + (size_t)(q0 + t) * hwd) : 0.0;
         float wh = 0.f;
         if (gt % 4 == 0 && gt / 4 < nh) wh = u.params[ph];
+        for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
+            float v[16];
+            tmem_ld16(tq + c0, v);
+            tmem_ld_wait();
+            if (nk == 0) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            }
+            float4* d = reinterpret_cast<float4*>(R + (32 * qw + lane) * RS + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+        if (w == 0) {  // the step's loss: the KL partials in lane order + a fixed tree (w16_kl_sum)
+            double kl = klv[0] + klv[1];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) kl += __shfl_xor_sync(0xffffffffu, kl, o);
+            if (lane == 0) {
+                sc[0] = kl / (double)u.nb;
+                sc[1] = (double)dv;
+            }
+        }
+        double gh = 0.0;
+#pragma unroll
+        for (int t = 0; t < HQ; ++t) gh += hv[t];  // (+0.0 past q1: a no-op, gh is never -0)
+        for (int q = q0 + HQ; q < q1; ++q) gh += __ldg(hcol + (size_t)q * hwd);  // (nhead > 64)
+        gh += __shfl_xor_sync(0xffffffffu, gh, 1);
+        gh += __shfl_xor_sync(0xffffffffu, gh, 2);
         W16_TR(g.dbg, 4);
         cluster_sync();  // all S partials are in shared memory
         W16_TR(g.dbg, 5);
