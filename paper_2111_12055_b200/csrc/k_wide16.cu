@@ -706,6 +706,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         }
         if (w == 0) {  // the step's loss: the KL partials in lane order + a fixed tree (w16_kl_sum)
             double kl = klv[0] + klv[1];
+            for (int q = lane + 64; q < u.nhead; q += 32) kl += u.hp[(size_t)q * hwd + 3 * H + 2];  // (nhead > 64)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) kl += __shfl_xor_sync(0xffffffffu, kl, o);
             if (lane == 0) {

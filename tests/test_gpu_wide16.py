@@ -54,7 +54,11 @@ def test_wide_bf16_one_step_matches_model(dev, orc):
     np.testing.assert_allclose(lg, le, rtol=1e-5)
 
 
-@pytest.mark.parametrize("h,n,batch,epochs", [(512, 4096, 1024, 2), (128, 777, 100, 1), (256, 3000, 512, 2)])
+# (64, 20000, 16384, 1): one gW1 tile, one W0 tile, 128 row tiles of head
+# partials (more than one batch of head-partial loads per thread in the fused
+# SGD launch), a ragged final step
+@pytest.mark.parametrize("h,n,batch,epochs", [(512, 4096, 1024, 2), (128, 777, 100, 1), (256, 3000, 512, 2),
+                                               (64, 20000, 16384, 1)])
 def test_wide_bf16_fit_tracks_model(dev, orc, h, n, batch, epochs):
     p0, pe, le, pg, lg, (feat, tgt) = _fit_pair(dev, orc, h, n, batch, epochs)
     change = np.abs(pe.astype(np.float64) - p0).max()
