@@ -106,3 +106,19 @@ def test_wide_bf16_data_parallel_path(orc):
     change = np.abs(p_one.astype(np.float64) - p0).max()
     assert np.abs(p.astype(np.float64) - p_one).max() <= 1e-3 * change
     np.testing.assert_allclose(el, el_one, rtol=1e-6)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+def test_wide_fit_divergence_raises(dev, orc, precision):
+    """fit throws TrainingDivergedError{epoch} once the batch loss is not
+    finite, before updating (policy.cpp:321-325): a huge learning rate blows
+    the weights up within the first epoch, on the fused-SGD BF16 path and the
+    TF32 path alike; a sane rate does not."""
+    import paper_2111_12055_b200 as gbx
+    feat, tgt = orc.g1(42, 4096)
+    p0 = orc.policy_init(7, (44, 128, 128, 2))
+    with pytest.raises(gbx.TrainingDivergedError) as ei:
+        dev.wide_fit(128, p0, feat, tgt, 1e30, 2, 512, 5, precision=precision)
+    assert ei.value.epoch == 0
+    p, el = dev.wide_fit(128, p0, feat, tgt, 0.01, 2, 512, 5, precision=precision)
+    assert np.all(np.isfinite(p)) and np.all(np.isfinite(el))
