@@ -1986,11 +1986,11 @@ int launch_w16(gbxcu_ctx* c, const void* A, int lda, const void* B, int ldb, con
 // The fused G4 + G5 + SGD launch: grid (1, T1 + T0, W16_SPLITS), clusters of
 // W16_SPLITS along z; tiles y < T1 = (H/128)^2 are gW1 = D2^T H1 tiles, the
 // T0 = H/128 others [gW0 | gb0] = D1^T [X | 1] tiles (maps in the o / ot slots).
-int launch_w16_sgd(gbxcu_ctx* c, const W16Args& g, int ldt, cudaStream_t st) {
+int launch_w16_sgd(gbxcu_ctx* c, const W16Args& g, int ldt, const void* xt, cudaStream_t st) {
     const int H = g.M;
     CUtensorMap ma, mb, m5a, m5b;
     if (!make_bf16_map(&ma, c->b_d2t.p, g.K, H, ldt, 128) || !make_bf16_map(&mb, c->b_h1t.p, g.K, H, ldt, 128) ||
-        !make_bf16_map(&m5a, c->b_d1t.p, g.K, H, ldt, 128) || !make_bf16_map(&m5b, c->b_xt.p, g.K, 64, ldt, 128))
+        !make_bf16_map(&m5a, c->b_d1t.p, g.K, H, ldt, 128) || !make_bf16_map(&m5b, xt, g.K, 64, ldt, 128))
         return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled unavailable or rejected a bf16 operand");
     const int nt = (H + 127) / 128;
     dim3 grid(1, nt * nt + nt, W16_SPLITS);
@@ -2025,8 +2025,8 @@ W16Plan w16_plan(gbxcu_ctx* c, int H, size_t bmax) {
 
 int w16_alloc(gbxcu_ctx* c, const W16Plan& P) {
     const size_t H = P.H, b = P.bmax, t = P.ldt, bf = 2;
-    RET(c->b_xg.ensure(bf * b * 64));
-    RET(c->b_xt.ensure(bf * 64 * t));
+    RET(c->b_xg.ensure(2 * bf * b * 64));  // (two copies: by step parity)
+    RET(c->b_xt.ensure(2 * bf * 64 * t));
     RET(c->b_h1.ensure(bf * b * H));
     RET(c->b_h1t.ensure(bf * H * t));
     RET(c->b_d2.ensure(bf * b * H));
@@ -2047,8 +2047,11 @@ int w16_alloc(gbxcu_ctx* c, const W16Plan& P) {
 // timeline slot base of the step being enqueued (GBX_PHASE_TIMING builds)
 int g_w16_dbg_step = -1;
 
+// Xg / X^T live in two copies selected by the step's parity `par`: the next
+// step's gather overwrites the other copy while this step's G4+G5 still
+// reads X^T, so the gather runs beside it and waits for it only at its end.
 int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const double* tgt,
-             const uint32_t* rows, int nbr, size_t nb, double lr, const int* epoch, cudaStream_t st) {
+             const uint32_t* rows, int nbr, size_t nb, double lr, const int* epoch, cudaStream_t st, int par) {
 #ifdef GBX_PHASE_TIMING
     const int dbg = g_w16_dbg_step >= 0 && g_w16_dbg_step < 8 ? 8 * g_w16_dbg_step : -100;
 #else
@@ -2058,6 +2061,8 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
     const int H = P.H, ldt = (int)P.ldt;
     const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H, o_w2 = o_b1 + H;
     using bf = __nv_bfloat16;
+    bf* xg = c->b_xg.as<bf>() + (size_t)par * P.bmax * 64;
+    bf* xt = c->b_xt.as<bf>() + (size_t)par * 64 * P.ldt;
     W16UpdArgs u{};
     u.params = Pm; u.hidden = H; u.np = wide_param_count(H); u.nb = nb; u.lr = lr;
     u.p4 = c->b_p4.as<float>(); u.s4 = P.s4; u.p5 = c->b_p5.as<float>(); u.s5 = P.s5;
@@ -2068,12 +2073,12 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
     u.dbg = slot(6);
     if (nbr > 0) {
         RET(launch_pdl(c, "w16_gather_kernel", w16_gather_kernel, dim3((nbr + 63) / 64), dim3(256), 0, st, feat,
-                       rows, nbr, dbg >= 0 ? slot(0) : -(g_w16_dbg_step + 2), c->b_xg.as<bf>(), c->b_xt.as<bf>(), ldt));
+                       rows, nbr, dbg >= 0 ? slot(0) : -(g_w16_dbg_step + 2), xg, xt, ldt));
         W16Args g1{};
         g1.dbg = slot(1);  // H1 = relu(Xg W0^T + b0) -> H1, H1^T
         g1.M = nbr; g1.N = H; g1.K = 64; g1.bias = Pm + o_b0;
         g1.out = c->b_h1.as<bf>(); g1.ldo = H; g1.out_t = c->b_h1t.as<bf>(); g1.ldt = ldt;
-        RET((launch_w16<256, 4, W16_EPI_H1>(c, c->b_xg.p, 64, c->b_w0p.p, 64, g1, 1, st)));
+        RET((launch_w16<256, 4, W16_EPI_H1>(c, xg, 64, c->b_w0p.p, 64, g1, 1, st)));
         W16Args g2{};
         g2.dbg = slot(2);  // acc = H1 W1^T -> fused head -> D2, D2^T, head partials
         g2.M = nbr; g2.N = H; g2.K = H; g2.bias = Pm + o_b1;
@@ -2100,10 +2105,10 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
             // K splits across a cluster and applies SGD (no update launch)
             g4.u = u;
             g4.dbg = slot(4);
-            return launch_w16_sgd(c, g4, ldt, st);
+            return launch_w16_sgd(c, g4, ldt, xt, st);
         }
         RET((launch_w16<128, 6, W16_EPI_PART>(c, c->b_d2t.p, ldt, c->b_h1t.p, ldt, g4, P.s4, st)));
-        RET((launch_w16<64, 6, W16_EPI_PART>(c, c->b_d1t.p, ldt, c->b_xt.p, ldt, g5, P.s5, st)));
+        RET((launch_w16<64, 6, W16_EPI_PART>(c, c->b_d1t.p, ldt, xt, ldt, g5, P.s5, st)));
     } else {
         // an empty slice contributes nothing (data-parallel remainder steps)
         CK(cudaMemsetAsync(c->b_p4.p, 0, sizeof(float) * (size_t)P.s4 * H * H, st));
@@ -2150,7 +2155,7 @@ int w16_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, co
             const size_t lo = std::min(nb, (size_t)c->rank * per), hi = std::min(nb, lo + per);
             g_w16_dbg_step = (int)s;
             RET(w16_step(c, P, d_params, d_feat, d_tgt, order + start + lo, (int)(hi - lo), nb,
-                         cfg->learning_rate, c->w_epoch.as<int>(), st));
+                         cfg->learning_rate, c->w_epoch.as<int>(), st, (int)(s & 1)));
         }
         return GBXCU_OK;
     };

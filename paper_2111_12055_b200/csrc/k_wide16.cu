@@ -381,9 +381,18 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     fence_after_sync();
     const uint32_t tacc = S.tmem;
     // (prologue done: the step's next kernel may start its own; every read of
-    //  the previous kernel's results comes after its completion)
-    pdl_trigger();
-    pdl_wait();
+    //  the previous kernel's results comes after its completion). G1 lets its
+    //  successor launch only after its wait: the gather before it writes its
+    //  Xg / X^T copy without waiting, so the chain of early launches must not
+    //  run ahead to the gather two steps on (same copy) while this step's
+    //  G4+G5 may still read it
+    if constexpr (EPI == W16_EPI_H1) {
+        pdl_wait();
+        pdl_trigger();
+    } else {
+        pdl_trigger();
+        pdl_wait();
+    }
     W16_TR(g.dbg, 1);
 
     if (tid == 0) {
@@ -870,7 +879,10 @@ __global__ void __launch_bounds__(256) w16_gather_kernel(const float* __restrict
         }
     }
 #endif
-    pdl_wait();  // (the previous step's G5 reads X^T)
+    // (no wait here: this step's copy of Xg / X^T is not the one the previous
+    //  step's G4+G5 reads, so the gather runs beside it; G1 may launch now —
+    //  its own wait covers the gather, which completes only after G4+G5)
+    pdl_trigger();
     W16_TR(dbg, 1);
     const int tid = threadIdx.x, r0 = blockIdx.x * GATHER_ROWS;
     const int nr = min(GATHER_ROWS, nb - r0);
@@ -913,9 +925,9 @@ __global__ void __launch_bounds__(256) w16_gather_kernel(const float* __restrict
             for (int j = 0; j < 8 && rq + j < nr; ++j) dst[j] = e[j];
         }
     }
-    // (G1 launches after the gather's work: early G1 CTAs would hold whole
-    //  SMs while the previous step's update still needs them)
-    pdl_trigger();
+    // G1 needs the previous step's update (G4+G5) complete: the gather
+    // completes only after it
+    pdl_wait();
     W16_TR(dbg, 3);
 }
 
