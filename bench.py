@@ -491,8 +491,9 @@ def main():
     #      rank uploads only its 1/N of the log from pinned memory and the
     #      shards are all-gathered over NVLink before the fused fit.
     lo, hi = rank * args.n, (rank + 1) * args.n
-    pinned_feat = torch.from_numpy(feat_h[lo:hi] if world > 1 else feat_h).pin_memory().numpy()
-    pinned_tgt = torch.from_numpy(tgt_h[lo:hi] if world > 1 else tgt_h).pin_memory().numpy()
+    pinned_feat_t = torch.from_numpy(feat_h[lo:hi] if world > 1 else feat_h).pin_memory()
+    pinned_tgt_t = torch.from_numpy(tgt_h[lo:hi] if world > 1 else tgt_h).pin_memory()
+    pinned_feat, pinned_tgt = pinned_feat_t.numpy(), pinned_tgt_t.numpy()
 
     def e2e_step():
         if world > 1:
@@ -516,6 +517,25 @@ def main():
            "d2h_bytes_per_step": int(4 * 5026 + 8),
            "path": "gbxcu_fit (whole log H2D)" if world == 1 else
                    "fit_sharded: 1/N of the log H2D per rank + NCCL all-gather on the device"}
+    # its floor: the same bytes over the host link alone (pinned -> device, CUDA
+    # events) plus the device-resident step; e2e is host-link bound when close
+    df = torch.empty_like(pinned_feat_t, device="cuda")
+    dtg = torch.empty_like(pinned_tgt_t, device="cuda")
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h2d = []
+    for _ in range(3):
+        h0.record()
+        df.copy_(pinned_feat_t, non_blocking=True)
+        dtg.copy_(pinned_tgt_t, non_blocking=True)
+        h1.record()
+        torch.cuda.synchronize()
+        h2d.append(h0.elapsed_time(h1))
+    h2d_ms = min(h2d)
+    del df, dtg
+    e2e.update({"ms_per_step": 1e3 * float(tt.item()), "h2d_ms": h2d_ms,
+                "h2d_gbs": (pinned_feat.nbytes + pinned_tgt.nbytes) / (h2d_ms * 1e-3) / 1e9,
+                "floor_ms": h2d_ms + ms_step,
+                "note": "floor = the log's host-to-device copy alone + the device-resident step"})
 
     # ---- roofline of the dominant kernel (train_epoch_kernel)
     peaks = measured_peaks()
