@@ -649,6 +649,8 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         float* R = reinterpret_cast<float*>(base);
         double* sc = reinterpret_cast<double*>(R + 128 * RS);
         __nv_bfloat16* TT = reinterpret_cast<__nv_bfloat16*>(sc + 4);  // [BN][24] W1^T staging (<= 24 rows)
+        static_assert((128 + W16_SPLITS - 1) / W16_SPLITS <= 24, "W1^T staging rows");
+        static_assert(128 * RS * 4 + 32 + BN * 24 * 2 <= (int)sizeof(W16Smem<BN, ST>), "SGD scratch fits the ring");
         const int H = u.hidden;
         const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H;
         const int ncol = w0tile ? F + 1 : g.N;  // valid output columns
