@@ -1986,11 +1986,14 @@ int launch_w16(gbxcu_ctx* c, const void* A, int lda, const void* B, int ldb, con
 // The fused G4 + G5 + SGD launch: grid (1, T1 + T0, W16_SPLITS), clusters of
 // W16_SPLITS along z; tiles y < T1 = (H/128)^2 are gW1 = D2^T H1 tiles, the
 // T0 = H/128 others [gW0 | gb0] = D1^T [X | 1] tiles (maps in the o / ot slots).
-int launch_w16_sgd(gbxcu_ctx* c, const W16Args& g, int ldt, const void* xt, cudaStream_t st) {
-    const int H = g.M;
+// Operands are MN-major — the row-major D2 / H1 (gW1 tiles) and D1 / Xg (W0
+// tiles), K = the records along their rows — as {64 M/N, 64 K} boxes, so no
+// transposed copy of any activation is written on this path.
+int launch_w16_sgd(gbxcu_ctx* c, const W16Args& g, const void* d1, const void* xg, cudaStream_t st) {
+    const int H = g.M, K = g.K;
     CUtensorMap ma, mb, m5a, m5b;
-    if (!make_bf16_map(&ma, c->b_d2t.p, g.K, H, ldt, 128) || !make_bf16_map(&mb, c->b_h1t.p, g.K, H, ldt, 128) ||
-        !make_bf16_map(&m5a, c->b_d1t.p, g.K, H, ldt, 128) || !make_bf16_map(&m5b, xt, g.K, 64, ldt, 128))
+    if (!make_bf16_map(&ma, c->b_d2.p, H, K, H, 64) || !make_bf16_map(&mb, c->b_h1.p, H, K, H, 64) ||
+        !make_bf16_map(&m5a, d1, H, K, H, 64) || !make_bf16_map(&m5b, xg, 64, K, 64, 64))
         return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled unavailable or rejected a bf16 operand");
     const int nt = (H + 127) / 128;
     dim3 grid(1, nt * nt + nt, W16_SPLITS);
@@ -2073,16 +2076,16 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
     u.dbg = slot(6);
     if (nbr > 0) {
         RET(launch_pdl(c, "w16_gather_kernel", w16_gather_kernel, dim3((nbr + 63) / 64), dim3(256), 0, st, feat,
-                       rows, nbr, dbg >= 0 ? slot(0) : -(g_w16_dbg_step + 2), xg, xt, ldt));
+                       rows, nbr, dbg >= 0 ? slot(0) : -(g_w16_dbg_step + 2), xg, c->comm ? xt : nullptr, ldt));
         W16Args g1{};
         g1.dbg = slot(1);  // H1 = relu(Xg W0^T + b0) -> H1, H1^T
         g1.M = nbr; g1.N = H; g1.K = 64; g1.bias = Pm + o_b0;
-        g1.out = c->b_h1.as<bf>(); g1.ldo = H; g1.out_t = c->b_h1t.as<bf>(); g1.ldt = ldt;
+        g1.out = c->b_h1.as<bf>(); g1.ldo = H; g1.out_t = c->comm ? c->b_h1t.as<bf>() : nullptr; g1.ldt = ldt;
         RET((launch_w16<256, 4, W16_EPI_H1>(c, xg, 64, c->b_w0p.p, 64, g1, 1, st)));
         W16Args g2{};
         g2.dbg = slot(2);  // acc = H1 W1^T -> fused head -> D2, D2^T, head partials
         g2.M = nbr; g2.N = H; g2.K = H; g2.bias = Pm + o_b1;
-        g2.out = c->b_d2.as<bf>(); g2.ldo = H; g2.out_t = c->b_d2t.as<bf>(); g2.ldt = ldt;
+        g2.out = c->b_d2.as<bf>(); g2.ldo = H; g2.out_t = c->comm ? c->b_d2t.as<bf>() : nullptr; g2.ldt = ldt;
         g2.w2 = Pm + o_w2; g2.b2 = Pm + o_w2 + 2 * H; g2.tgt = tgt; g2.rows = rows;
         g2.inv_b = 1.0 / (double)nb; g2.head_part = c->b_hp.as<double>();
         // a CTA pair (cluster along x) per 128-row tile covers the full rows
@@ -2090,7 +2093,11 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
         W16Args g3{};
         g3.dbg = slot(3);  // D1 = (D2 W1) [H1 > 0] -> D1^T
         g3.M = nbr; g3.N = H; g3.K = H; g3.mask = c->b_h1.as<bf>(); g3.ldm = H;
-        g3.out_t = c->b_d1t.as<bf>(); g3.ldt = ldt;
+        if (c->comm) {  // D1^T for the split-K G5
+            g3.out_t = c->b_d1t.as<bf>(); g3.ldt = ldt;
+        } else {        // D1 row-major (same buffer) for the fused SGD launch
+            g3.out = c->b_d1t.as<bf>(); g3.ldo = H;
+        }
         RET((launch_w16<256, 4, W16_EPI_D1T>(c, c->b_d2.p, H, c->b_w1t.p, H, g3, 1, st)));
         W16Args g4{};
         g4.dbg = slot(4);  // gW1 = D2^T H1 (split-K partials)
@@ -2105,7 +2112,7 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
             // K splits across a cluster and applies SGD (no update launch)
             g4.u = u;
             g4.dbg = slot(4);
-            return launch_w16_sgd(c, g4, ldt, xt, st);
+            return launch_w16_sgd(c, g4, c->b_d1t.p, xg, st);
         }
         RET((launch_w16<128, 6, W16_EPI_PART>(c, c->b_d2t.p, ldt, c->b_h1t.p, ldt, g4, P.s4, st)));
         RET((launch_w16<64, 6, W16_EPI_PART>(c, c->b_d1t.p, ldt, xt, ldt, g5, P.s5, st)));

@@ -73,6 +73,21 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
            | ((uint32_t)(M >> 4) << 24);   // m_dim
 }
 
+// MN-major operand with the 128-byte swizzle: TMA boxes of {64 elements along
+// M/N (128 B), 64 K rows}, so a K row of 64 M/N elements is one 128-byte row,
+// 8 K rows form a 1024-byte swizzle atom (SBO), and the next 64 M/N elements
+// are the next box, 8 KB on (LBO). K steps of 16 advance the start 2 KB.
+__device__ __forceinline__ uint64_t smem_desc_mn128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)(8192 >> 4) << 16;    // LBO: next 64-element M/N chunk
+    d |= (uint64_t)(1024 >> 4) << 32;    // SBO: next 8 K rows
+    d |= (uint64_t)1 << 46;              // version = 1 (Blackwell)
+    d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+    return d;
+}
+constexpr uint32_t IDESC_A_MN = 1u << 15, IDESC_B_MN = 1u << 16;
+
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
     asm volatile(
@@ -238,29 +253,29 @@ __device__ __forceinline__ float col_reduce16(float (&v)[16], int lane) {
 // issue its TMA stores (row-major at (col, row0), transposed at (row0, col);
 // RM / TR select which). Buffer k & 1 is reused two chunks later, after its
 // previous stores have read it. Rows past M are clipped by the tensor maps.
-template <bool RM, bool TR>
 __device__ __forceinline__ void stage_chunk(OutStage& o, int k, const float (&h)[16], const CUtensorMap* map_o,
-                                            const CUtensorMap* map_ot, int col, int row0, int lane) {
+                                            const CUtensorMap* map_ot, int col, int row0, int lane, bool RM,
+                                            bool TR) {
     const int b = k & 1;
     if (k >= 2) {
         if (lane == 0) bulk_wait_read1();
         __syncwarp();
     }
-    if constexpr (RM) {
+    if (RM) {
         uint4* q = reinterpret_cast<uint4*>(o.rm[b] + lane * 16);
         q[0] = make_uint4(pack_bf16(h[0], h[1]), pack_bf16(h[2], h[3]), pack_bf16(h[4], h[5]), pack_bf16(h[6], h[7]));
         q[1] = make_uint4(pack_bf16(h[8], h[9]), pack_bf16(h[10], h[11]), pack_bf16(h[12], h[13]),
                           pack_bf16(h[14], h[15]));
     }
-    if constexpr (TR) {
+    if (TR) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) o.tr[b][i * 32 + lane] = __float2bfloat16_rn(h[i]);
     }
     fence_proxy_smem();
     __syncwarp();
     if (lane == 0) {
-        if constexpr (RM) tma_store_2d(map_o, o.rm[b], col, row0);
-        if constexpr (TR) tma_store_2d(map_ot, o.tr[b], row0, col);
+        if (RM) tma_store_2d(map_o, o.rm[b], col, row0);
+        if (TR) tma_store_2d(map_ot, o.tr[b], row0, col);
         bulk_commit();
     }
 }
@@ -408,25 +423,41 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             if (it >= ST) mbar_wait_b(&S.empty[slot], ((it / ST) - 1) & 1);
             mbar_expect(&S.full[slot], bytes);
             const int k0 = (kb_lo + it) * W_BK;
-            tma_2d(&S.a[slot][0], pma, k0, row0, &S.full[slot]);
+            if constexpr (EPI == W16_EPI_SGD) {
+                // MN-major operands (row-major D2 / H1 / D1 / Xg: K = records
+                // are their rows): boxes of {64 M/N, 64 K}
 #pragma unroll
-            for (int h = 0; h < BN / BOX; ++h)
-                tma_2d(&S.b[slot][h * BOX * W_BK], pmb, k0, col0 + h * BOX, &S.full[slot]);
+                for (int h = 0; h < W_BM / 64; ++h) tma_2d(&S.a[slot][h * 64 * W_BK], pma, row0 + 64 * h, k0, &S.full[slot]);
+#pragma unroll
+                for (int h = 0; h < BN / 64; ++h) tma_2d(&S.b[slot][h * 64 * W_BK], pmb, col0 + 64 * h, k0, &S.full[slot]);
+            } else {
+                tma_2d(&S.a[slot][0], pma, k0, row0, &S.full[slot]);
+#pragma unroll
+                for (int h = 0; h < BN / BOX; ++h)
+                    tma_2d(&S.b[slot][h * BOX * W_BK], pmb, k0, col0 + h * BOX, &S.full[slot]);
+            }
         }
     } else if (tid == 32) {
-        const uint32_t idesc = idesc_bf16(W_BM, MN);
+        constexpr bool MNM = EPI == W16_EPI_SGD;  // MN-major A and B
+        const uint32_t idesc = idesc_bf16(W_BM, MN) | (MNM ? IDESC_A_MN | IDESC_B_MN : 0u);
         for (int it = 0; it < nk; ++it) {
             const int slot = it % ST;
             mbar_wait_b(&S.full[slot], (it / ST) & 1);
             fence_after_sync();
             const uint32_t a0 = smem_u32(&S.a[slot][0]), b0 = smem_u32(&S.b[slot][0]);
 #pragma unroll
-            for (int s = 0; s < W_BK / 16; ++s) {  // K = 16 per MMA: 32 B along the swizzled row
-                const uint64_t ad = smem_desc_sw128(a0 + 32 * s);
+            for (int s = 0; s < W_BK / 16; ++s) {  // K = 16 per MMA
+                if constexpr (MNM) {  // 16 K rows of 128 B further
+                    static_assert(NMMA == 1, "MN-major path: one MMA per K step");
+                    mma_bf16(tacc, smem_desc_mn128(a0 + 2048 * s), smem_desc_mn128(b0 + 2048 * s), idesc,
+                             (it > 0 || s > 0) ? 1u : 0u);
+                } else {  // 32 B along the swizzled K-major row
+                    const uint64_t ad = smem_desc_sw128(a0 + 32 * s);
 #pragma unroll
-                for (int h = 0; h < NMMA; ++h) {
-                    const uint64_t bd = smem_desc_sw128(b0 + h * MN * 128 + 32 * s);
-                    mma_bf16(tacc + h * MN, ad, bd, idesc, (it > 0 || s > 0) ? 1u : 0u);
+                    for (int h = 0; h < NMMA; ++h) {
+                        const uint64_t bd = smem_desc_sw128(b0 + h * MN * 128 + 32 * s);
+                        mma_bf16(tacc + h * MN, ad, bd, idesc, (it > 0 || s > 0) ? 1u : 0u);
+                    }
                 }
             }
             commit_to(&S.empty[slot]);  // frees the stage once these MMAs have read it
@@ -586,7 +617,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                     d[i + j + 1] = h[i + j + 1] > 0.f ? dd.y : 0.f;
                 }
             }
-            stage_chunk<true, true>(O, (c0 - cb) >> 4, d, &map_o, &map_ot, c0, rw0, lane);
+            stage_chunk(O, (c0 - cb) >> 4, d, &map_o, &map_ot, c0, rw0, lane, true, g.out_t != nullptr);
             float p[16];
 #pragma unroll
             for (int i = 0; i < 16; i += 2) {
@@ -820,14 +851,17 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                     h[i + 2] = fmaxf(v[i + 2] + bb.z, 0.f);
                     h[i + 3] = fmaxf(v[i + 3] + bb.w, 0.f);
                 }
-                stage_chunk<true, true>(O, (c0 - cbeg) >> 4, h, &map_o, &map_ot, col, rw0, lane);
+                stage_chunk(O, (c0 - cbeg) >> 4, h, &map_o, &map_ot, col, rw0, lane, true, g.out_t != nullptr);
             } else if constexpr (EPI == W16_EPI_D1T) {
                 // d1 = acc [h1 > 0] (mask = stored bf16 H1), transposed (G5's A)
                 float m[16], h[16];
                 if (row_ok) load_row16(g.mask + (size_t)row * g.ldm + col, m);
 #pragma unroll
                 for (int i = 0; i < 16; ++i) h[i] = row_ok && m[i] > 0.f ? v[i] : 0.f;
-                stage_chunk<false, true>(O, (c0 - cbeg) >> 4, h, &map_o, &map_ot, col, rw0, lane);
+                // (one rank: D1 row-major, the fused SGD launch's MN-major A;
+                //  data-parallel: D1^T, the split-K G5's K-major A)
+                stage_chunk(O, (c0 - cbeg) >> 4, h, &map_o, &map_ot, col, rw0, lane, g.out != nullptr,
+                            g.out_t != nullptr);
             } else if (row_ok) {
                 // split-K fp32 partial, row-major [M][ldp]
                 float4* o = reinterpret_cast<float4*>(g.part + (size_t)blockIdx.z * g.split_stride +
@@ -903,8 +937,10 @@ __global__ void __launch_bounds__(256) w16_gather_kernel(const float* __restrict
         if (it < GATHER_ROWS * NQ)
             *reinterpret_cast<uint2*>(&t[r][4 * q]) = make_uint2(pack_bf16(v[k].x, v[k].y), pack_bf16(v[k].z, v[k].w));
     }
-    // columns 44..63: zero in Xg; X^T row 44 = 1
-    for (int it = tid; it < GATHER_ROWS * 20; it += 256) t[it / 20][F + it % 20] = __float2bfloat16_rn(0.f);
+    // columns 44..63: column 44 = 1 (the ones column of [X | 1]: gb0 in the
+    // fused SGD launch; W0p's column 44 is 0, so G1 ignores it), the rest 0
+    for (int it = tid; it < GATHER_ROWS * 20; it += 256)
+        t[it / 20][F + it % 20] = __float2bfloat16_rn(it % 20 == 0 && it / 20 < nr ? 1.f : 0.f);
     __syncthreads();
     // Xg: 64 rows x 128 B
     for (int it = tid; it < GATHER_ROWS * 8; it += 256) {
@@ -912,8 +948,8 @@ __global__ void __launch_bounds__(256) w16_gather_kernel(const float* __restrict
         if (r < nr)
             reinterpret_cast<uint4*>(xg + (size_t)(r0 + r) * 64)[q] = *reinterpret_cast<const uint4*>(&t[r][8 * q]);
     }
-    // X^T: 64 columns x 64 rows (128 B per column), 8 rows per 16-byte store
-    for (int it = tid; it < 64 * 8; it += 256) {
+    // X^T (data-parallel path only): 64 columns x 64 rows (128 B per column), 8 rows per 16-byte store
+    for (int it = tid; xt && it < 64 * 8; it += 256) {
         const int c = it >> 3, rq = (it & 7) * 8;
         if (rq >= nr) continue;
         __nv_bfloat16 e[8];
