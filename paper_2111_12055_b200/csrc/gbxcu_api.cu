@@ -1972,7 +1972,10 @@ template <int BN, int ST, int EPI>
 int launch_w16(gbxcu_ctx* c, const void* A, int lda, const void* B, int ldb, const W16Args& g, int splits,
                cudaStream_t st, int cluster_x = 1, int cluster_z = 1) {
     CUtensorMap ma, mb, mo{}, mot{};
-    if (!make_bf16_map(&ma, A, g.K, g.M, lda, 128) || !make_bf16_map(&mb, B, g.K, g.N, ldb, BN > 256 ? 256 : BN))
+    // (G3, EPI_D1T: B is MN-major — [K rows][N] — as {64 N, 64 K} boxes)
+    const bool b_ok = EPI == W16_EPI_D1T ? make_bf16_map(&mb, B, g.N, g.K, ldb, 64)
+                                         : make_bf16_map(&mb, B, g.K, g.N, ldb, BN > 256 ? 256 : BN);
+    if (!make_bf16_map(&ma, A, g.K, g.M, lda, 128) || !b_ok)
         return fail(GBXCU_ECUDA, "cuTensorMapEncodeTiled unavailable or rejected a bf16 operand");
     if ((g.out && !make_bf16_store_map(&mo, g.out, g.N, g.M, g.ldo, 16, 32)) ||
         (g.out_t && !make_bf16_store_map(&mot, g.out_t, g.M, g.N, g.ldt, 32, 16)))
@@ -2098,7 +2101,7 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
         } else {        // D1 row-major (same buffer) for the fused SGD launch
             g3.out = c->b_d1t.as<bf>(); g3.ldo = H;
         }
-        RET((launch_w16<256, 4, W16_EPI_D1T>(c, c->b_d2.p, H, c->b_w1t.p, H, g3, 1, st)));
+        RET((launch_w16<256, 4, W16_EPI_D1T>(c, c->b_d2.p, H, c->b_w1.p, H, g3, 1, st)));  // B = W1, MN-major
         W16Args g4{};
         g4.dbg = slot(4);  // gW1 = D2^T H1 (split-K partials)
         g4.M = H; g4.N = H; g4.K = nbr; g4.part = c->b_p4.as<float>(); g4.ldp = H;

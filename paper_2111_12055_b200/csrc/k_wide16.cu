@@ -430,6 +430,12 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 for (int h = 0; h < W_BM / 64; ++h) tma_2d(&S.a[slot][h * 64 * W_BK], pma, row0 + 64 * h, k0, &S.full[slot]);
 #pragma unroll
                 for (int h = 0; h < BN / 64; ++h) tma_2d(&S.b[slot][h * 64 * W_BK], pmb, col0 + 64 * h, k0, &S.full[slot]);
+            } else if constexpr (EPI == W16_EPI_D1T) {
+                // A = D2 K-major; B = W1 itself, MN-major ([j][k]: K = j its
+                // rows), so no transposed copy of W1 is kept
+                tma_2d(&S.a[slot][0], pma, k0, row0, &S.full[slot]);
+#pragma unroll
+                for (int h = 0; h < BN / 64; ++h) tma_2d(&S.b[slot][h * 64 * W_BK], pmb, col0 + 64 * h, k0, &S.full[slot]);
             } else {
                 tma_2d(&S.a[slot][0], pma, k0, row0, &S.full[slot]);
 #pragma unroll
@@ -439,7 +445,9 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         }
     } else if (tid == 32) {
         constexpr bool MNM = EPI == W16_EPI_SGD;  // MN-major A and B
-        const uint32_t idesc = idesc_bf16(W_BM, MN) | (MNM ? IDESC_A_MN | IDESC_B_MN : 0u);
+        constexpr bool BMN = EPI == W16_EPI_D1T;  // K-major A, MN-major B
+        const uint32_t idesc =
+            idesc_bf16(W_BM, MN) | (MNM ? IDESC_A_MN | IDESC_B_MN : 0u) | (BMN ? IDESC_B_MN : 0u);
         for (int it = 0; it < nk; ++it) {
             const int slot = it % ST;
             mbar_wait_b(&S.full[slot], (it / ST) & 1);
@@ -450,6 +458,10 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 if constexpr (MNM) {  // 16 K rows of 128 B further
                     static_assert(NMMA == 1, "MN-major path: one MMA per K step");
                     mma_bf16(tacc, smem_desc_mn128(a0 + 2048 * s), smem_desc_mn128(b0 + 2048 * s), idesc,
+                             (it > 0 || s > 0) ? 1u : 0u);
+                } else if constexpr (BMN) {
+                    static_assert(NMMA == 1, "MN-major B: one MMA per K step");
+                    mma_bf16(tacc, smem_desc_sw128(a0 + 32 * s), smem_desc_mn128(b0 + 2048 * s), idesc,
                              (it > 0 || s > 0) ? 1u : 0u);
                 } else {  // 32 B along the swizzled K-major row
                     const uint64_t ad = smem_desc_sw128(a0 + 32 * s);
@@ -670,7 +682,8 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         //      tile; CTA cr sums its 128 / S rows of all S partials in split
         //      order (fp32 partials, fp64 sum: the update kernel's order) through
         //      distributed shared memory and applies SGD to them
-        //      (policy.cpp:328-332), refreshing the bf16 operand copies. The
+        //      (policy.cpp:328-332), refreshing the bf16 operand copies (W1
+        //      only: G3 reads it MN-major, no transposed copy). The
         //      gW1 and [gW0 | gb0] tiles share the launch; every thread of the
         //      grid also helps sum the head parameters' gradients (b1, W2, b2).
         const W16UpdArgs& u = g.u;
@@ -679,9 +692,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         constexpr int MAXG = (128 / S + 1) * B4 / NTH + 1;  // float4 groups per thread (upper bound)
         float* R = reinterpret_cast<float*>(base);
         double* sc = reinterpret_cast<double*>(R + 128 * RS);
-        __nv_bfloat16* TT = reinterpret_cast<__nv_bfloat16*>(sc + 4);  // [BN][24] W1^T staging (<= 24 rows)
-        static_assert((128 + W16_SPLITS - 1) / W16_SPLITS <= 24, "W1^T staging rows");
-        static_assert(128 * RS * 4 + 32 + BN * 24 * 2 <= (int)sizeof(W16Smem<BN, ST>), "SGD scratch fits the ring");
+        static_assert(128 * RS * 4 + 32 <= (int)sizeof(W16Smem<BN, ST>), "SGD scratch fits the ring");
         const int H = u.hidden;
         const size_t o_b0 = (size_t)H * F, o_w1 = o_b0 + H, o_b1 = o_w1 + (size_t)H * H;
         const int ncol = w0tile ? F + 1 : g.N;  // valid output columns
@@ -809,19 +820,8 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 } else {
                     u.params[o_w1 + (size_t)j * H + k] = nw;
                     u.w1[(size_t)j * H + k] = b;
-                    TT[kl * 24 + rl] = b;
                 }
             }
-        }
-        if (!w0tile) {
-            __syncthreads();
-            // W1^T [k][j]: the CTA's rows j of column k are contiguous
-            const int j0 = row0 + r_lo, nj = min(r_hi - r_lo, g.M - j0);
-            if (apply && nj > 0)
-                for (int t = tid; t < BN * nj; t += NTH) {
-                    const int kk = t / nj, jj = t % nj;
-                    if (col0 + kk < ncol) u.w1t[(size_t)(col0 + kk) * H + j0 + jj] = TT[kk * 24 + jj];
-                }
         }
         if (apply && gt % 4 == 0 && gt / 4 < nh) u.params[ph] = __double2float_rn((double)wh - u.lr * gh);
         if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && sc[1] < 0.0) {
