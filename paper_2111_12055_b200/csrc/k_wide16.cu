@@ -493,6 +493,22 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             hw21 = g.w2[g.N + col0 + tid];
         }
     }
+    // (G3's mask — the stored bf16 H1 of this thread's row and 64 columns,
+    //  written by G1, complete before this kernel's wait — loaded while the
+    //  MMAs run)
+    uint4 mk[EPI == W16_EPI_D1T ? 8 : 1];
+    if constexpr (EPI == W16_EPI_D1T) {
+        constexpr int CWm = BN / w_ew<EPI>();
+        static_assert(CWm == 64, "mask prefetch: 64 columns per thread");
+        const int rr = row0 + 32 * (w & 3) + (tid & 31), cb0 = col0 + (w >> 2) * CWm;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mk[q] = make_uint4(0u, 0u, 0u, 0u);
+        if (rr < g.M && cb0 < g.N) {
+            const uint4* src = reinterpret_cast<const uint4*>(g.mask + (size_t)rr * g.ldm + cb0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) mk[q] = __ldg(src + q);
+        }
+    }
     __syncwarp();
     if (nk > 0) mbar_wait_b(&S.done, 0);
     fence_after_sync();
@@ -854,10 +870,20 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 stage_chunk(O, (c0 - cbeg) >> 4, h, &map_o, &map_ot, col, rw0, lane, true, g.out_t != nullptr);
             } else if constexpr (EPI == W16_EPI_D1T) {
                 // d1 = acc [h1 > 0] (mask = stored bf16 H1), transposed (G5's A)
-                float m[16], h[16];
-                if (row_ok) load_row16(g.mask + (size_t)row * g.ldm + col, m);
+                float h[16];
+                const int kq = (c0 - cbeg) >> 4;  // this chunk's two mask words
 #pragma unroll
-                for (int i = 0; i < 16; ++i) h[i] = row_ok && m[i] > 0.f ? v[i] : 0.f;
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const uint4 mq = kq == 0 ? mk[q2] : kq == 1 ? mk[2 + q2] : kq == 2 ? mk[4 + q2] : mk[6 + q2];
+                    const uint32_t wv[4] = {mq.x, mq.y, mq.z, mq.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&wv[e]);
+                        const int i = 8 * q2 + 2 * e;
+                        h[i] = row_ok && __bfloat162float(b2.x) > 0.f ? v[i] : 0.f;
+                        h[i + 1] = row_ok && __bfloat162float(b2.y) > 0.f ? v[i + 1] : 0.f;
+                    }
+                }
                 // (one rank: D1 row-major, the fused SGD launch's MN-major A;
                 //  data-parallel: D1^T, the split-K G5's K-major A)
                 stage_chunk(O, (c0 - cbeg) >> 4, h, &map_o, &map_ot, col, rw0, lane, g.out != nullptr,
