@@ -164,6 +164,9 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+// split form: loads issued between the two are not held up by the release
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -496,6 +499,20 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     // (G3's mask — the stored bf16 H1 of this thread's row and 64 columns,
     //  written by G1, complete before this kernel's wait — loaded while the
     //  MMAs run)
+    // (the fused SGD launch: the step's KL partials and the divergence flag,
+    //  read by warp 2 while the MMAs run)
+    double klv[2] = {0.0, 0.0};
+    int dv = -1;
+    if constexpr (EPI == W16_EPI_SGD) {
+        if (w == 2) {
+            const size_t hwd = 3 * (size_t)g.u.hidden + 3;
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+                if (lane + 32 * t < g.u.nhead)
+                    klv[t] = g.u.hp[(size_t)(lane + 32 * t) * hwd + 3 * g.u.hidden + 2];
+            dv = *g.u.diverged;
+        }
+    }
     uint4 mk[EPI == W16_EPI_D1T ? 8 : 1];
     if constexpr (EPI == W16_EPI_D1T) {
         constexpr int CWm = BN / w_ew<EPI>();
@@ -702,6 +719,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         //      only: G3 reads it MN-major, no transposed copy). The
         //      gW1 and [gW0 | gb0] tiles share the launch; every thread of the
         //      grid also helps sum the head parameters' gradients (b1, W2, b2).
+        W16_TR(g.dbg, 6);  // (probe: epilogue entry)
         const W16UpdArgs& u = g.u;
         constexpr int RS = BN + 4;  // padded fp32 row stride: conflict-free 16-byte stores
         constexpr int S = W16_SPLITS, B4 = BN / 4;
@@ -716,18 +734,39 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         // partials, the slice's old weights, the head partials) and consumed
         // after the TMEM dump: one round trip, overlapped with it
         const size_t hwd = 3 * (size_t)H + 3;
-        double klv[2] = {0.0, 0.0};
-        int dv = -1;
-        if (w == 0) {
-#pragma unroll
-            for (int t = 0; t < 2; ++t)
-                if (lane + 32 * t < u.nhead) klv[t] = u.hp[(size_t)(lane + 32 * t) * hwd + 3 * H + 2];
-            dv = *u.diverged;
-        }
         // this CTA's rows of the tile: [r_lo, r_hi) (128 rows over S CTAs)
         const int cr = (int)cluster_rank();
         const int r_lo = cr * 128 / S, r_hi = (cr + 1) * 128 / S;
         const int n4 = (r_hi - r_lo) * B4;  // float4 groups of the slice
+        for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
+            float v[16];
+            tmem_ld16(tq + c0, v);
+            tmem_ld_wait();
+            if (nk == 0) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            }
+            float4* d = reinterpret_cast<float4*>(R + (32 * qw + lane) * RS + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+        W16_TR(g.dbg, 7);  // (probe: TMEM dumped)
+        if (w == 2) {  // the step's loss: the KL partials in lane order + a fixed tree (w16_kl_sum)
+            double kl = klv[0] + klv[1];
+            for (int q = lane + 64; q < u.nhead; q += 32) kl += u.hp[(size_t)q * hwd + 3 * H + 2];  // (nhead > 64)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) kl += __shfl_xor_sync(0xffffffffu, kl, o);
+            if (lane == 0) {
+                sc[0] = kl / (double)u.nb;
+                sc[1] = (double)dv;
+            }
+        }
+        W16_TR(g.dbg, 4);
+        // all S partials are in shared memory after this barrier; the
+        // epilogue's global loads (old weights, head partials — used after the
+        // exchange) go out between its arrive (whose release would otherwise
+        // wait for them) and its wait
+        cluster_arrive();
         float wold[MAXG][4];
 #pragma unroll
         for (int t = 0; t < MAXG; ++t) {
@@ -744,7 +783,12 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         // head parameter gradients: four threads per parameter, each summing a
         // quarter of the row tiles' head partials, combined in a fixed tree
         const size_t nh = u.np - o_b1;
-        const size_t gt = (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * NTH + tid;
+        // (spread over every CTA — the first 64 threads of each — so no cluster
+        //  waits on a CTA carrying many of these loads)
+        const size_t ncta = (size_t)gridDim.x * gridDim.y * gridDim.z;
+        const size_t HT = ((4 * nh + ncta - 1) / ncta + 3) & ~(size_t)3;  // head threads per CTA (<= 4 * 386 / 12)
+        const size_t cta = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        const size_t gt = (size_t)tid < HT ? cta * HT + tid : ~(size_t)0 >> 2;
         const size_t ph = o_b1 + gt / 4;
         constexpr int HQ = 16;  // head partial rows per thread (nhead <= 64 in one batch)
         double hv[HQ];
@@ -761,36 +805,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         for (int t = 0; t < HQ; ++t) hv[t] = q0 + t < q1 ? __ldg(hcol + (size_t)(q0 + t) * hwd) : 0.0;
         float wh = 0.f;
         if (gt % 4 == 0 && gt / 4 < nh) wh = u.params[ph];
-        for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
-            float v[16];
-            tmem_ld16(tq + c0, v);
-            tmem_ld_wait();
-            if (nk == 0) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = 0.f;
-            }
-            float4* d = reinterpret_cast<float4*>(R + (32 * qw + lane) * RS + c0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
-        if (w == 0) {  // the step's loss: the KL partials in lane order + a fixed tree (w16_kl_sum)
-            double kl = klv[0] + klv[1];
-            for (int q = lane + 64; q < u.nhead; q += 32) kl += u.hp[(size_t)q * hwd + 3 * H + 2];  // (nhead > 64)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) kl += __shfl_xor_sync(0xffffffffu, kl, o);
-            if (lane == 0) {
-                sc[0] = kl / (double)u.nb;
-                sc[1] = (double)dv;
-            }
-        }
-        double gh = 0.0;
-#pragma unroll
-        for (int t = 0; t < HQ; ++t) gh += hv[t];  // (+0.0 past q1: a no-op, gh is never -0)
-        for (int q = q0 + HQ; q < q1; ++q) gh += __ldg(hcol + (size_t)q * hwd);  // (nhead > 64)
-        gh += __shfl_xor_sync(0xffffffffu, gh, 1);
-        gh += __shfl_xor_sync(0xffffffffu, gh, 2);
-        W16_TR(g.dbg, 4);
-        cluster_sync();  // all S partials are in shared memory
+        cluster_wait();
         W16_TR(g.dbg, 5);
         double gs[MAXG][4];
 #pragma unroll
@@ -814,9 +829,14 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
                 for (int e = 0; e < 4; ++e) gs[t][e] += (double)pv[q][e];
         }
-        W16_TR(g.dbg, 6);
+        // the head parameters' sums (their loads were issued before the dump)
+        double gh = 0.0;
+#pragma unroll
+        for (int t = 0; t < HQ; ++t) gh += hv[t];  // (+0.0 past q1: a no-op, gh is never -0)
+        for (int q = q0 + HQ; q < q1; ++q) gh += __ldg(hcol + (size_t)q * hwd);  // (nhead > 64)
+        gh += __shfl_xor_sync(0xffffffffu, gh, 1);
+        gh += __shfl_xor_sync(0xffffffffu, gh, 2);
         cluster_sync();  // every CTA has read the others' partials
-        W16_TR(g.dbg, 7);
         const double loss = sc[0];
         const bool apply = sc[1] < 0.0 && isfinite(loss);  // fit throws before updating (policy.cpp:321-325)
 #pragma unroll

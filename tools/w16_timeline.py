@@ -73,5 +73,5 @@ for k in range(7):
     print(f"{names[k]:24s} {e:10.2f} {r:6.2f}-{r1:6.2f} {m0:6.2f}-{m:6.2f} {x0:6.2f}-{x:6.2f}")
 print("G2 head phases (min-max over CTAs): logits done, softmax done, pass 2 done, sums written:")
 print("   " + "  ".join(f"{x:6.2f}-{y:6.2f}" for x, y in ph[0:4]))
-print("G4/G5 SGD phases: partial dumped, barrier 1 passed, reduce done, barrier 2 passed:")
+print("G4/G5 SGD phases: partial dumped, barrier 1 passed, epilogue entry, TMEM dumped:")
 print("   " + "  ".join(f"{x:6.2f}-{y:6.2f}" for x, y in ph[4:8]))
