@@ -131,7 +131,7 @@ struct gbxcu_ctx {
     DevBuf w_params, w_grad, w_w1t, w_h1, w_h1t, w_h2, w_d2, w_d2t, w_d1t, w_xt, w_d3, w_kl;
     DevBuf w_part, w_g4, w_g5, w_loss, w_feat, w_tgt, w_probs, w_xg, w_w0p, w_epoch;
     // BF16 path (k_wide16.cu): bf16 activations / operand copies, partials
-    DevBuf b_xg, b_xt, b_h1, b_h1t, b_d2, b_d2t, b_d1t, b_w0p, b_w1, b_w1t, b_p4, b_p5, b_hp;
+    DevBuf b_xg, b_xt, b_h1, b_h1t, b_d2, b_d2t, b_d1t, b_w0p, b_w1, b_p4, b_p5, b_hp;
     // CUDA graphs of a wide-MLP epoch's step sequence (one per epoch-permutation
     // buffer), keyed on every pointer and size they bake in
     struct WideGraph {
@@ -2040,7 +2040,6 @@ int w16_alloc(gbxcu_ctx* c, const W16Plan& P) {
     RET(c->b_d1t.ensure(bf * H * t));
     RET(c->b_w0p.ensure(bf * H * 64));
     RET(c->b_w1.ensure(bf * H * H));
-    RET(c->b_w1t.ensure(bf * H * H));
     RET(c->b_p4.ensure(sizeof(float) * (size_t)P.s4 * H * H));
     RET(c->b_p5.ensure(sizeof(float) * (size_t)P.s5 * H * 64));
     RET(c->b_hp.ensure(sizeof(double) * ((b + 127) / 128) * (3 * H + 3)));
@@ -2074,7 +2073,7 @@ int w16_step(gbxcu_ctx* c, const W16Plan& P, float* Pm, const float* feat, const
     u.p4 = c->b_p4.as<float>(); u.s4 = P.s4; u.p5 = c->b_p5.as<float>(); u.s5 = P.s5;
     u.hp = c->b_hp.as<double>(); u.nhead = (nbr + 127) / 128;
     u.g_out = c->w_grad.as<float>(); u.loss_sum = c->w_loss.as<double>();
-    u.w0p = c->b_w0p.as<bf>(); u.w1 = c->b_w1.as<bf>(); u.w1t = c->b_w1t.as<bf>();
+    u.w0p = c->b_w0p.as<bf>(); u.w1 = c->b_w1.as<bf>(); u.w1t = nullptr;  // (G3 reads W1 MN-major)
     u.epoch = epoch; u.diverged = c->diverged.as<int>(); u.epoch_acc = c->epoch_acc.as<double>();
     u.dbg = slot(6);
     if (nbr > 0) {
@@ -2154,7 +2153,7 @@ int w16_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, co
     RET(c->w_epoch.ensure(16));
     using bf = __nv_bfloat16;
     w16_weights_kernel<<<blocks((size_t)H * H), 256, 0, st>>>(d_params, H, c->b_w0p.as<bf>(), c->b_w1.as<bf>(),
-                                                              c->b_w1t.as<bf>());
+                                                              nullptr);
     RET(check_launch(c, "w16_weights_kernel"));
     const long n_steps = (long)((n + cfg->batch_size - 1) / cfg->batch_size);
     auto run_steps = [&](const uint32_t* order) -> int {
@@ -2188,7 +2187,7 @@ int w16_fit_device(gbxcu_ctx* c, int H, float* d_params, const float* d_feat, co
                 (const void*)n, (const void*)(uintptr_t)cfg->batch_size, (const void*)(uintptr_t)lr_bits,
                 (const void*)P.ldt, (const void*)(uintptr_t)P.s4, (const void*)(uintptr_t)P.s5,
                 c->b_xg.p, c->b_xt.p, c->b_h1.p, c->b_h1t.p, c->b_d2.p, c->b_d2t.p, c->b_d1t.p,
-                c->b_w0p.p, c->b_w1.p, c->b_w1t.p, c->b_p4.p, c->b_p5.p, c->b_hp.p, c->w_grad.p,
+                c->b_w0p.p, c->b_w1.p, c->b_p4.p, c->b_p5.p, c->b_hp.p, c->w_grad.p,
                 c->w_loss.p, c->w_epoch.p, c->diverged.p, c->epoch_acc.p};
             gbxcu_ctx::WideGraph* g = nullptr;
             for (auto& x : c->wg)

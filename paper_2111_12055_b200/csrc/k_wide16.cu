@@ -1033,7 +1033,7 @@ __global__ void w16_weights_kernel(const float* __restrict__ params, int H, __nv
     const size_t o_w1 = (size_t)H * F + H, k = t / H, j = t % H;
     const __nv_bfloat16 b = __float2bfloat16_rn(params[o_w1 + t]);
     w1[t] = b;
-    w1t[j * H + k] = b;
+    if (w1t) w1t[j * H + k] = b;
 }
 
 // mode 0: reduce + SGD + refreshed bf16 copies (one rank); 1: reduce into the
@@ -1125,7 +1125,7 @@ __global__ void __launch_bounds__(256) w16_update_kernel(W16UpdArgs u, int mode)
             s_t[(tid >> 4) + 16 * q][tid & 15] = b;
         }
     }
-    if (tile) {  // W1^T[j][k]: 32 consecutive k per row of the tile
+    if (tile && u.w1t) {  // W1^T[j][k] (when a caller keeps one): 32 consecutive k per row of the tile
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
