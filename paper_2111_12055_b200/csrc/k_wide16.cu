@@ -342,6 +342,191 @@ __device__ __forceinline__ double w16_kl_sum(const W16UpdArgs& u) {
     return s;
 }
 
+// The fused softmax/KL head of G2 (see the kernel below), one CTA of a pair:
+// TMEM accumulators at `tq` (this warp's lane quarter), the CTA's output
+// columns [col0, col0 + BN). Also the tail of the fused G1+G2 launch.
+template <int BN, int EW>
+__device__ __forceinline__ void w16_head_epilogue(unsigned char* base, const W16Args& g, const CUtensorMap& map_o,
+                                                  const CUtensorMap& map_ot, uint32_t tq, int col0, int row0,
+                                                  double tg0, double tg1, float hb1, float hw20, float hw21) {
+    constexpr int NTH = 128 * EW, CW = BN / EW;
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const int qw = w & 3, cg = w >> 2;
+    const int rw0 = row0 + 32 * qw, row = rw0 + lane;
+    const bool row_ok = row < g.M;
+    const int cbeg = cg * CW;
+    const uint32_t col0u = (uint32_t)col0;
+    (void)col0u;
+    // ---- fused head (G2). A CTA pair (thread-block cluster along x)
+    //      covers full rows: each CTA its BN columns; the partial logits
+    //      of its 4 column groups and of the pair combine in a fixed
+    //      order (column group, then CTA) through (distributed) shared memory
+    HeadScratch& T = *reinterpret_cast<HeadScratch*>(base);
+    OutStage& O = reinterpret_cast<OutStage*>(base + head_stage_off())[w];
+    const int H = g.N;
+    static_assert(BN <= NTH, "one head column per thread");
+    if (tid < BN && col0 + tid < H) {
+        const int c = col0 + tid;
+        T.b1[c] = hb1;
+        T.w2[0][c] = hw20;
+        T.w2[1][c] = hw21;
+        T.w2d[0][c] = (double)hw20;
+        T.w2d[1][c] = (double)hw21;
+    }
+    __syncthreads();
+    const int cb = col0 + cbeg, cend = min(H, cb + CW);
+    // pass 1: h2 = relu(acc + b1); partial logits in fp64 (two chains per output)
+    double l0a = 0.0, l0b = 0.0, l1a = 0.0, l1b = 0.0;
+    for (int c0 = cb; c0 < cend; c0 += 32) {
+        float v[32];
+        tmem_ld32(tq + (c0 - col0), v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(&T.b1[c0 + i]);
+            const double2 w0a = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i]);
+            const double2 w0b = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i + 2]);
+            const double2 w1a = *reinterpret_cast<const double2*>(&T.w2d[1][c0 + i]);
+            const double2 w1b = *reinterpret_cast<const double2*>(&T.w2d[1][c0 + i + 2]);
+            const float h0 = fmaxf(v[i] + bb.x, 0.f), h1 = fmaxf(v[i + 1] + bb.y, 0.f);
+            const float h2 = fmaxf(v[i + 2] + bb.z, 0.f), h3 = fmaxf(v[i + 3] + bb.w, 0.f);
+            l0a = fma((double)h0, w0a.x, l0a);
+            l1a = fma((double)h0, w1a.x, l1a);
+            l0b = fma((double)h1, w0a.y, l0b);
+            l1b = fma((double)h1, w1a.y, l1b);
+            l0a = fma((double)h2, w0b.x, l0a);
+            l1a = fma((double)h2, w1b.x, l1a);
+            l0b = fma((double)h3, w0b.y, l0b);
+            l1b = fma((double)h3, w1b.y, l1b);
+        }
+    }
+    T.lg[cg][32 * qw + lane][0] = l0a + l0b;
+    T.lg[cg][32 * qw + lane][1] = l1a + l1b;
+    W16_TR(g.dbg, 4);
+    __syncthreads();
+    const int rl = 32 * qw + lane;
+    if (cg == 0) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < EW; ++q) {
+            s0 += T.lg[q][rl][0];
+            s1 += T.lg[q][rl][1];
+        }
+        T.own[rl][0] = s0;
+        T.own[rl][1] = s1;
+    }
+    const uint32_t crank = cluster_rank(), npair = (uint32_t)gridDim.x;  // 1 or 2 CTAs per row tile
+    if (npair > 1) cluster_sync();  // the peer's partial logits are written
+    else __syncthreads();
+    // softmax, KL with the reference clamps, d3 = p (ln(p^/t^) - L) / |b|
+    // (every column group of a row computes the same values)
+    double d30 = 0.0, d31 = 0.0, loss = 0.0;
+    {
+        double s0 = T.own[rl][0], s1 = T.own[rl][1];
+        if (npair > 1) {  // CTA 0's columns first
+            const double p0 = ld_peer_f64(&T.own[rl][0], crank ^ 1u), p1 = ld_peer_f64(&T.own[rl][1], crank ^ 1u);
+            if (crank == 0) {
+                s0 += p0;
+                s1 += p1;
+            } else {
+                s0 = p0 + s0;
+                s1 = p1 + s1;
+            }
+        }
+        if (row_ok) {
+        const double z0 = (double)g.b2[0] + s0, z1 = (double)g.b2[1] + s1;
+        const double m = z0 < z1 ? z1 : z0;
+        const double e0 = exp(z0 - m), e1 = exp(z1 - m);
+        const double p0 = e0 / (e0 + e1), p1 = e1 / (e0 + e1);
+        const double pc0 = clampp(p0), pc1 = clampp(p1);
+        const double lr0 = log(pc0 / clampp(tg0)), lr1 = log(pc1 / clampp(tg1));
+        loss = pc0 * lr0 + pc1 * lr1;
+        d30 = p0 * (lr0 - loss) * g.inv_b;
+        d31 = p1 * (lr1 - loss) * g.inv_b;
+        }
+    }
+    const float d3f0 = (float)d30, d3f1 = (float)d31;
+    W16_TR(g.dbg, 5);
+    // pass 2 (fp32): D2 = (d3 w2) [h2 > 0] -> D2 (row-major), D2^T (TMA
+    // stores); column sums gW2 = sum d3 h2, gb1 = sum D2 over the warp's 32
+    // rows (fp32 shuffle trees), per lane quarter in shared memory
+    float vn[16];  // the next chunk's accumulators, loaded one chunk ahead
+    tmem_ld16(tq + (cb - col0), vn);
+    for (int c0 = cb; c0 < cend; c0 += 16) {
+        float v[16], h[16], d[16];
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = vn[i];
+        if (c0 + 16 < cend) tmem_ld16(tq + (c0 + 16 - col0), vn);
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(&T.b1[c0 + i]);
+            const float4 wa = *reinterpret_cast<const float4*>(&T.w2[0][c0 + i]);
+            const float4 wb = *reinterpret_cast<const float4*>(&T.w2[1][c0 + i]);
+            const float b4[4] = {bb.x, bb.y, bb.z, bb.w}, a4[4] = {wa.x, wa.y, wa.z, wa.w},
+                        c4[4] = {wb.x, wb.y, wb.z, wb.w};
+            // (packed fp32 pairs: each half rounds exactly like the scalar op)
+#pragma unroll
+            for (int j = 0; j < 4; j += 2) {
+                const float2 s2v = __fadd2_rn(make_float2(v[i + j], v[i + j + 1]), make_float2(b4[j], b4[j + 1]));
+                const float2 da = __fmul2_rn(make_float2(d3f0, d3f0), make_float2(a4[j], a4[j + 1]));
+                const float2 dc = __fmul2_rn(make_float2(d3f1, d3f1), make_float2(c4[j], c4[j + 1]));
+                const float2 dd = __fadd2_rn(da, dc);
+                h[i + j] = row_ok ? fmaxf(s2v.x, 0.f) : 0.f;
+                h[i + j + 1] = row_ok ? fmaxf(s2v.y, 0.f) : 0.f;
+                d[i + j] = h[i + j] > 0.f ? dd.x : 0.f;
+                d[i + j + 1] = h[i + j + 1] > 0.f ? dd.y : 0.f;
+            }
+        }
+        stage_chunk(O, (c0 - cb) >> 4, d, &map_o, &map_ot, c0, rw0, lane, true, g.out_t != nullptr);
+        float p[16];
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+            const float2 q = __fmul2_rn(make_float2(d3f0, d3f0), make_float2(h[i], h[i + 1]));
+            p[i] = q.x;
+            p[i + 1] = q.y;
+        }
+        const float s0 = col_reduce16(p, lane);
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+            const float2 q = __fmul2_rn(make_float2(d3f1, d3f1), make_float2(h[i], h[i + 1]));
+            p[i] = q.x;
+            p[i + 1] = q.y;
+        }
+        const float s1 = col_reduce16(p, lane);
+        const float s2 = col_reduce16(d, lane);
+        if (lane < 16) {
+            T.wsum[qw][0][c0 + lane] = (double)s0;
+            T.wsum[qw][1][c0 + lane] = (double)s1;
+            T.wsum[qw][2][c0 + lane] = (double)s2;
+        }
+    }
+    W16_TR(g.dbg, 6);
+    // gb2 and KL of the rows (column group 0 only; fixed shuffle tree)
+    const bool first = cg == 0 && crank == 0;
+    double r0 = first ? d30 : 0.0, r1 = first ? d31 : 0.0, r2 = first ? loss : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+        r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    }
+    if (lane == 0) {
+        T.red[w][0] = r0;
+        T.red[w][1] = r1;
+        T.red[w][2] = r2;
+    }
+    __syncthreads();
+    double* prow = g.head_part + (size_t)blockIdx.y * (3 * H + 3);
+    for (int q = 0; q < 3; ++q)
+        for (int c = col0 + tid; c < min(H, col0 + BN); c += NTH)
+            prow[q * H + c] = ((T.wsum[0][q][c] + T.wsum[1][q][c]) + T.wsum[2][q][c]) + T.wsum[3][q][c];
+    if (tid < 3 && crank == 0)
+        prow[3 * H + tid] = ((T.red[0][tid] + T.red[1][tid]) + T.red[2][tid]) + T.red[3][tid];
+    if (lane == 0) bulk_wait_all();
+    if (npair > 1) cluster_sync();  // the peer has read this CTA's partial logits
+}
+
 // D[M x N] = A[M x K] . B[N x K]^T, bf16 operands, fp32 accumulation, epilogue EPI.
 // Grid (ceil(N/BN), ceil(M/128), splits). Warp 0 lane 0: TMA producer; warp 1
 // lane 0: MMA issuer; all 16 warps: epilogue (warp w: TMEM lanes 32 (w % 4)..
@@ -541,174 +726,7 @@ w16_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     __syncthreads();  // every warp is past the mainloop: stage buffers are free for scratch
 
     if constexpr (EPI == W16_EPI_HEAD) {
-        // ---- fused head (G2). A CTA pair (thread-block cluster along x)
-        //      covers full rows: each CTA its BN columns; the partial logits
-        //      of its 4 column groups and of the pair combine in a fixed
-        //      order (column group, then CTA) through (distributed) shared memory
-        HeadScratch& T = *reinterpret_cast<HeadScratch*>(base);
-        OutStage& O = reinterpret_cast<OutStage*>(base + head_stage_off())[w];
-        const int H = g.N;
-        static_assert(BN <= NTH, "one head column per thread");
-        if (tid < BN && col0 + tid < H) {
-            const int c = col0 + tid;
-            T.b1[c] = hb1;
-            T.w2[0][c] = hw20;
-            T.w2[1][c] = hw21;
-            T.w2d[0][c] = (double)hw20;
-            T.w2d[1][c] = (double)hw21;
-        }
-        __syncthreads();
-        const int cb = col0 + cbeg, cend = min(H, cb + CW);
-        // pass 1: h2 = relu(acc + b1); partial logits in fp64 (two chains per output)
-        double l0a = 0.0, l0b = 0.0, l1a = 0.0, l1b = 0.0;
-        for (int c0 = cb; c0 < cend; c0 += 32) {
-            float v[32];
-            tmem_ld32(tq + (c0 - col0), v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                const float4 bb = *reinterpret_cast<const float4*>(&T.b1[c0 + i]);
-                const double2 w0a = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i]);
-                const double2 w0b = *reinterpret_cast<const double2*>(&T.w2d[0][c0 + i + 2]);
-                const double2 w1a = *reinterpret_cast<const double2*>(&T.w2d[1][c0 + i]);
-                const double2 w1b = *reinterpret_cast<const double2*>(&T.w2d[1][c0 + i + 2]);
-                const float h0 = fmaxf(v[i] + bb.x, 0.f), h1 = fmaxf(v[i + 1] + bb.y, 0.f);
-                const float h2 = fmaxf(v[i + 2] + bb.z, 0.f), h3 = fmaxf(v[i + 3] + bb.w, 0.f);
-                l0a = fma((double)h0, w0a.x, l0a);
-                l1a = fma((double)h0, w1a.x, l1a);
-                l0b = fma((double)h1, w0a.y, l0b);
-                l1b = fma((double)h1, w1a.y, l1b);
-                l0a = fma((double)h2, w0b.x, l0a);
-                l1a = fma((double)h2, w1b.x, l1a);
-                l0b = fma((double)h3, w0b.y, l0b);
-                l1b = fma((double)h3, w1b.y, l1b);
-            }
-        }
-        T.lg[cg][32 * qw + lane][0] = l0a + l0b;
-        T.lg[cg][32 * qw + lane][1] = l1a + l1b;
-        W16_TR(g.dbg, 4);
-        __syncthreads();
-        const int rl = 32 * qw + lane;
-        if (cg == 0) {
-            double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-            for (int q = 0; q < EW; ++q) {
-                s0 += T.lg[q][rl][0];
-                s1 += T.lg[q][rl][1];
-            }
-            T.own[rl][0] = s0;
-            T.own[rl][1] = s1;
-        }
-        const uint32_t crank = cluster_rank(), npair = (uint32_t)gridDim.x;  // 1 or 2 CTAs per row tile
-        if (npair > 1) cluster_sync();  // the peer's partial logits are written
-        else __syncthreads();
-        // softmax, KL with the reference clamps, d3 = p (ln(p^/t^) - L) / |b|
-        // (every column group of a row computes the same values)
-        double d30 = 0.0, d31 = 0.0, loss = 0.0;
-        {
-            double s0 = T.own[rl][0], s1 = T.own[rl][1];
-            if (npair > 1) {  // CTA 0's columns first
-                const double p0 = ld_peer_f64(&T.own[rl][0], crank ^ 1u), p1 = ld_peer_f64(&T.own[rl][1], crank ^ 1u);
-                if (crank == 0) {
-                    s0 += p0;
-                    s1 += p1;
-                } else {
-                    s0 = p0 + s0;
-                    s1 = p1 + s1;
-                }
-            }
-            if (row_ok) {
-            const double z0 = (double)g.b2[0] + s0, z1 = (double)g.b2[1] + s1;
-            const double m = z0 < z1 ? z1 : z0;
-            const double e0 = exp(z0 - m), e1 = exp(z1 - m);
-            const double p0 = e0 / (e0 + e1), p1 = e1 / (e0 + e1);
-            const double pc0 = clampp(p0), pc1 = clampp(p1);
-            const double lr0 = log(pc0 / clampp(tg0)), lr1 = log(pc1 / clampp(tg1));
-            loss = pc0 * lr0 + pc1 * lr1;
-            d30 = p0 * (lr0 - loss) * g.inv_b;
-            d31 = p1 * (lr1 - loss) * g.inv_b;
-            }
-        }
-        const float d3f0 = (float)d30, d3f1 = (float)d31;
-        W16_TR(g.dbg, 5);
-        // pass 2 (fp32): D2 = (d3 w2) [h2 > 0] -> D2 (row-major), D2^T (TMA
-        // stores); column sums gW2 = sum d3 h2, gb1 = sum D2 over the warp's 32
-        // rows (fp32 shuffle trees), per lane quarter in shared memory
-        float vn[16];  // the next chunk's accumulators, loaded one chunk ahead
-        tmem_ld16(tq + (cb - col0), vn);
-        for (int c0 = cb; c0 < cend; c0 += 16) {
-            float v[16], h[16], d[16];
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = vn[i];
-            if (c0 + 16 < cend) tmem_ld16(tq + (c0 + 16 - col0), vn);
-#pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-                const float4 bb = *reinterpret_cast<const float4*>(&T.b1[c0 + i]);
-                const float4 wa = *reinterpret_cast<const float4*>(&T.w2[0][c0 + i]);
-                const float4 wb = *reinterpret_cast<const float4*>(&T.w2[1][c0 + i]);
-                const float b4[4] = {bb.x, bb.y, bb.z, bb.w}, a4[4] = {wa.x, wa.y, wa.z, wa.w},
-                            c4[4] = {wb.x, wb.y, wb.z, wb.w};
-                // (packed fp32 pairs: each half rounds exactly like the scalar op)
-#pragma unroll
-                for (int j = 0; j < 4; j += 2) {
-                    const float2 s2v = __fadd2_rn(make_float2(v[i + j], v[i + j + 1]), make_float2(b4[j], b4[j + 1]));
-                    const float2 da = __fmul2_rn(make_float2(d3f0, d3f0), make_float2(a4[j], a4[j + 1]));
-                    const float2 dc = __fmul2_rn(make_float2(d3f1, d3f1), make_float2(c4[j], c4[j + 1]));
-                    const float2 dd = __fadd2_rn(da, dc);
-                    h[i + j] = row_ok ? fmaxf(s2v.x, 0.f) : 0.f;
-                    h[i + j + 1] = row_ok ? fmaxf(s2v.y, 0.f) : 0.f;
-                    d[i + j] = h[i + j] > 0.f ? dd.x : 0.f;
-                    d[i + j + 1] = h[i + j + 1] > 0.f ? dd.y : 0.f;
-                }
-            }
-            stage_chunk(O, (c0 - cb) >> 4, d, &map_o, &map_ot, c0, rw0, lane, true, g.out_t != nullptr);
-            float p[16];
-#pragma unroll
-            for (int i = 0; i < 16; i += 2) {
-                const float2 q = __fmul2_rn(make_float2(d3f0, d3f0), make_float2(h[i], h[i + 1]));
-                p[i] = q.x;
-                p[i + 1] = q.y;
-            }
-            const float s0 = col_reduce16(p, lane);
-#pragma unroll
-            for (int i = 0; i < 16; i += 2) {
-                const float2 q = __fmul2_rn(make_float2(d3f1, d3f1), make_float2(h[i], h[i + 1]));
-                p[i] = q.x;
-                p[i + 1] = q.y;
-            }
-            const float s1 = col_reduce16(p, lane);
-            const float s2 = col_reduce16(d, lane);
-            if (lane < 16) {
-                T.wsum[qw][0][c0 + lane] = (double)s0;
-                T.wsum[qw][1][c0 + lane] = (double)s1;
-                T.wsum[qw][2][c0 + lane] = (double)s2;
-            }
-        }
-        W16_TR(g.dbg, 6);
-        // gb2 and KL of the rows (column group 0 only; fixed shuffle tree)
-        const bool first = cg == 0 && crank == 0;
-        double r0 = first ? d30 : 0.0, r1 = first ? d31 : 0.0, r2 = first ? loss : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            r0 += __shfl_xor_sync(0xffffffffu, r0, o);
-            r1 += __shfl_xor_sync(0xffffffffu, r1, o);
-            r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-        }
-        if (lane == 0) {
-            T.red[w][0] = r0;
-            T.red[w][1] = r1;
-            T.red[w][2] = r2;
-        }
-        __syncthreads();
-        double* prow = g.head_part + (size_t)blockIdx.y * (3 * H + 3);
-        for (int q = 0; q < 3; ++q)
-            for (int c = col0 + tid; c < min(H, col0 + BN); c += NTH)
-                prow[q * H + c] = ((T.wsum[0][q][c] + T.wsum[1][q][c]) + T.wsum[2][q][c]) + T.wsum[3][q][c];
-        if (tid < 3 && crank == 0)
-            prow[3 * H + tid] = ((T.red[0][tid] + T.red[1][tid]) + T.red[2][tid]) + T.red[3][tid];
-        if (lane == 0) bulk_wait_all();
-        if (npair > 1) cluster_sync();  // the peer has read this CTA's partial logits
+        w16_head_epilogue<BN, EW>(base, g, map_o, map_ot, tq, col0, row0, tg0, tg1, hb1, hw20, hw21);
     } else if constexpr (EPI == W16_EPI_SGD) {
         // ---- fused split-K reduction + SGD (single-rank path). The S CTAs of
         //      a cluster (along z) hold the S K-split partials of one output
