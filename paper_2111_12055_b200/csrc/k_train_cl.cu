@@ -86,7 +86,6 @@ struct ClSmem {
     double d2[2][TBR * HS2];  // all 32
     double d1[TBR * DS1];  // own columns
     double d3[TBR * 2];
-    double tgt[TBR * 2];
     double kl[TBR];
     double flag;           // 1: the step's loss sum is not finite
     double zero, one;      // operands of the G phase's dummy / bias chains
@@ -244,11 +243,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
         if (h2) h2 = cl_next(a, n_steps, s2, r2, n2);
 
         CL_MARK(0);  // step top (wait, prefetch issue)
-        // ---- P0: the step's targets (its fp32 features are read in place from
-        //      the staging slot: widened per use, exactly)
+        // ---- P0: the step's features and targets are read in place from the
+        //      staging slot (features widened per use, exactly); the step-top
+        //      barrier made them visible
         const float* xs = S.stage_f[k];
-        if (tid < 2 * TBR) S.tgt[tid] = S.stage_t[k][tid];
-        __syncthreads();
+        const double* tg = S.stage_t[k];
 
         CL_MARK(1);  // P0
         // ---- F1: h1[r][16c + jj] = relu(b0 + sum_i w0[j][i] x[r][i]), DFMA chain over i
@@ -302,7 +301,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTC, 1) train_epoch
             const double s = a2 ? __dadd_rn(eo, e) : __dadd_rn(e, eo);  // e0 + e1
             const double p = __ddiv_rn(e, s);
             const double pc = clampp(p);
-            const double tc = clampp(S.tgt[2 * r + a2]);
+            const double tc = clampp(tg[2 * r + a2]);
             const double lr = log(__ddiv_rn(pc, tc));
             const double term = __dmul_rn(pc, lr);
             const double to = __shfl_xor_sync(0xffffffffu, term, 1);
