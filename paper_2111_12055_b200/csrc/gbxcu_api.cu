@@ -163,6 +163,8 @@ struct gbxcu_qtable {
     DevBuf perm, perm2, digit, digit2, seg_head, key_head, seg_scan, key_scan, seg_start, seg_key;
     DevBuf spread, bad, temp;
     DevBuf flag, row, rowkey, sfeat, stgt, bad_stage;
+    DevBuf enc_tab;  // qt_enc_table_kernel output, filled on the first snapshot
+    bool enc_ready = false;
 };
 
 namespace {
@@ -1033,7 +1035,7 @@ int gbxcu_qtable_create(gbxcu_ctx* c, double alpha, double omega, gbxcu_qtable**
                       &t->count, &t->perm, &t->perm2, &t->digit, &t->digit2, &t->seg_head,
                       &t->key_head, &t->seg_scan, &t->key_scan, &t->seg_start, &t->seg_key,
                       &t->spread, &t->bad, &t->temp, &t->flag, &t->row, &t->rowkey, &t->sfeat,
-                      &t->stgt, &t->bad_stage})
+                      &t->stgt, &t->bad_stage, &t->enc_tab})
         b->astream = c->stream;
     *out = t;
     return GBXCU_OK;
@@ -1420,10 +1422,16 @@ int qtable_snapshot(gbxcu_qtable* t, double rho, float* d_feat, double* d_tgt, s
     qt_rowkey_kernel<<<c->num_sms * 4, 256, 0, st>>>(t->flag.as<uint32_t>(), t->row.as<uint32_t>(), m,
                                                      t->rowkey.as<uint32_t>());
     RET(check_launch(c, "qt_rowkey_kernel"));
-    const int sgrid = (int)std::min<size_t>((r + 127) / 128, (size_t)c->num_sms * 8);
+    if (!t->enc_ready) {
+        RET(t->enc_tab.ensure(sizeof(float) * QT_ENC_TAB));
+        qt_enc_table_kernel<<<QT_ENC_TAB / 256, 256, 0, st>>>(t->enc_tab.as<float>());
+        RET(check_launch(c, "qt_enc_table_kernel"));
+        t->enc_ready = true;
+    }
+    const int sgrid = (int)std::min<size_t>((r + 127) / 128, (size_t)c->num_sms * 5);  // 5 CTAs/SM (smem)
     qt_snapshot_kernel<<<sgrid, 128, 0, st>>>(t->keys.as<uint32_t>(), t->q.as<double>(),
-                                              t->rowkey.as<uint32_t>(), r, rho, d_feat, d_tgt,
-                                              t->bad_stage.as<int>());
+                                              t->rowkey.as<uint32_t>(), r, rho, t->enc_tab.as<float>(),
+                                              d_feat, d_tgt, t->bad_stage.as<int>());
     RET(check_launch(c, "qt_snapshot_kernel"));
     int bs = 0;
     CK(cudaMemcpyAsync(&bs, t->bad_stage.p, 4, cudaMemcpyDeviceToHost, st));

@@ -141,29 +141,31 @@ __device__ __forceinline__ bool key_tail_equal(const uint32_t* a, const uint32_t
 }
 static_assert(KW % 2 == 0, "keys are read as 8-byte pairs");
 
-// MSD fast path: segment heads straight from the sorted top digits, plus the
-// check that makes them valid — neighbours with equal digits must have equal
-// keys (words w_from.. beyond the digit; none when w_from == KW), else the
-// order is unresolved and the caller falls back to the full LSD sort.
+// MSD fast path: segment heads straight from the sorted digits (key bits
+// above `abits` action bits), plus the check that makes them valid —
+// neighbours with equal key bits must have equal keys (words w_from.. beyond
+// the digit; none when w_from == KW), else the order is unresolved and the
+// caller falls back to the full LSD sort. With abits == 0 every record has
+// the same action.
 __global__ void qt_msd_heads_kernel(RecView v, const uint32_t* __restrict__ perm,
                                     const unsigned long long* __restrict__ digit, size_t nrec,
-                                    int w_from, unsigned int* __restrict__ unresolved,
+                                    int w_from, int abits, unsigned int* __restrict__ unresolved,
                                     uint32_t* __restrict__ seg_head, uint32_t* __restrict__ key_head) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec;
          i += (size_t)gridDim.x * blockDim.x) {
         uint32_t kh = 1, sh = 1;
         if (i > 0) {
-            const uint32_t r = perm[i], r0 = perm[i - 1];
-            if (digit[i] == digit[i - 1]) {
+            const unsigned long long d = digit[i], d0 = digit[i - 1];
+            if ((d >> abits) == (d0 >> abits)) {
                 kh = 0;
                 if (w_from < KW) {
-                    if (!key_tail_equal(v.key(r), v.key(r0), w_from)) {
+                    if (!key_tail_equal(v.key(perm[i]), v.key(perm[i - 1]), w_from)) {
                         atomicOr(unresolved, 1u);
                         kh = 1;
                     }
                 }
             }
-            sh = kh | (v.action(r) != v.action(r0) ? 1u : 0u);
+            sh = kh | (uint32_t)((d ^ d0) & (unsigned long long)abits);
         }
         seg_head[i] = sh;
         key_head[i] = kh;
@@ -365,6 +367,15 @@ __device__ float glibc_log1pf(float x) {
 
 __device__ __forceinline__ float enc_count(uint32_t c) { return glibc_log1pf(__uint2float_rn(c)); }
 
+// enc_count of every count below QT_ENC_TAB, computed by the same function
+// (so a lookup is bit-identical): the snapshot encodes 36 counts per row and
+// real counts are mostly small, so most of its ~150-instruction log1pf calls
+// become one L1/L2-resident load.
+__global__ void qt_enc_table_kernel(float* __restrict__ tab) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < QT_ENC_TAB) tab[c] = enc_count(c);
+}
+
 // Row flags: key with both actions recorded.
 __global__ void qt_both_kernel(const uint8_t* __restrict__ has, size_t m, uint32_t* __restrict__ flag) {
     for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < m; k += (size_t)gridDim.x * blockDim.x)
@@ -384,10 +395,11 @@ __global__ void qt_rowkey_kernel(const uint32_t* __restrict__ flag, const uint32
 // each lane encodes its row, and the 32 x 44 feature block is written back
 // as one contiguous, coalesced range.
 constexpr int SNAP_WARPS = 4;
-__global__ void __launch_bounds__(SNAP_WARPS * 32)
+__global__ void __launch_bounds__(SNAP_WARPS * 32, 5)
 qt_snapshot_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ q,
                    const uint32_t* __restrict__ rowkey, size_t nrows, double rho,
-                   float* __restrict__ feat, double* __restrict__ tgt, int* __restrict__ bad_stage) {
+                   const float* __restrict__ enc_tab, float* __restrict__ feat, double* __restrict__ tgt,
+                   int* __restrict__ bad_stage) {
     __shared__ uint32_t kt[SNAP_WARPS][32 * (KW + 1)];
     __shared__ float ft[SNAP_WARPS][32 * (F + 1)];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -397,10 +409,18 @@ qt_snapshot_kernel(const uint32_t* __restrict__ keys, const double* __restrict__
          r0 += (size_t)gridDim.x * SNAP_WARPS * 32) {
         const int nv = (int)min((size_t)32, nrows - r0);
         const uint32_t kl = lane < nv ? rowkey[r0 + lane] : 0u;
-        for (int x0 = 0; x0 < 32 * KW; x0 += 32) {
-            const int x = x0 + lane, rr = x / KW, wd = x - rr * KW;
+        // all 30 loads of the warp's rows in flight before the first store
+        uint32_t kv[KW];
+#pragma unroll
+        for (int j = 0; j < KW; ++j) {
+            const int x = 32 * j + lane, rr = x / KW, wd = x - rr * KW;
             const uint32_t kk = __shfl_sync(0xffffffffu, kl, rr & 31);
-            if (rr < nv) K[rr * (KW + 1) + wd] = keys[(size_t)kk * KW + wd];
+            kv[j] = rr < nv ? __ldg(keys + (size_t)kk * KW + wd) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < KW; ++j) {
+            const int x = 32 * j + lane, rr = x / KW, wd = x - rr * KW;
+            K[rr * (KW + 1) + wd] = kv[j];
         }
         __syncwarp();
         if (lane < nv) {
@@ -414,7 +434,13 @@ qt_snapshot_kernel(const uint32_t* __restrict__ keys, const double* __restrict__
                 for (int i = 0; i < 8; ++i) out[i] = i == (int)stage ? 1.0f : 0.0f;
                 // slots 8..36: basic blocks, vector[5], scalar[4], memory[6], compute[4],
                 // control-flow[4], registers[2], work groups[3] = key words 1..29
-                for (int wd = 1; wd < KW; ++wd) out[7 + wd] = enc_count(v[wd]);
+                // table loads issued together (clamped); counts past the table
+                // are recomputed below
+#pragma unroll
+                for (int wd = 1; wd < KW; ++wd) out[7 + wd] = __ldg(enc_tab + min(v[wd], QT_ENC_TAB - 1));
+#pragma unroll 1
+                for (int wd = 1; wd < KW; ++wd)
+                    if (v[wd] >= QT_ENC_TAB) out[7 + wd] = enc_count(v[wd]);
                 // totals (u32 wrap, like the u64 sums cast back): vector, scalar, memory,
                 // compute, control-flow, registers; instructions = the first five
                 const int lo_[6] = {2, 7, 11, 17, 21, 25};
@@ -426,7 +452,11 @@ qt_snapshot_kernel(const uint32_t* __restrict__ keys, const double* __restrict__
                     tot[g + 1] = sacc;
                 }
                 tot[0] = tot[1] + tot[2] + tot[3] + tot[4] + tot[5];
-                for (int i = 0; i < 7; ++i) out[37 + i] = enc_count(tot[i]);
+#pragma unroll
+                for (int i = 0; i < 7; ++i) out[37 + i] = __ldg(enc_tab + min(tot[i], QT_ENC_TAB - 1));
+#pragma unroll
+                for (int i = 0; i < 7; ++i)
+                    if (tot[i] >= QT_ENC_TAB) out[37 + i] = enc_count(tot[i]);
             }
             // boltzmann_pair (qtable.cpp:121-129)
             const double q0 = q[2 * (size_t)kl], q1 = q[2 * (size_t)kl + 1];
@@ -494,23 +524,20 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
         std::swap(io.perm, io.perm2);
         return cudaSuccess;
     };
-    // MSD fast path: (1) stable partition by action, (2) stable sort by the
-    // <= 64 most significant varying key bits. If no two neighbours share
-    // those bits without sharing the whole key (checked on the device), the
-    // order is already the final (key, action, record) order; otherwise fall
-    // back to the full LSD below. Typical keys differ within their first
-    // varying words, so one 64-bit sort replaces ceil(varying bits / 64).
+    // MSD fast path: one stable sort (records start in record order) by a
+    // 64-bit digit packing the most significant varying key bits above the
+    // action bit, i.e. by (top key bits, action, record). If no two
+    // neighbours share those key bits without sharing the whole key (checked
+    // on the device), the order is already the final (key, action, record)
+    // order; otherwise fall back to the full LSD below. Typical keys differ
+    // within their first varying words, so one sort replaces the action pass
+    // plus ceil(varying bits / 64) key passes, and the action travels in the
+    // sorted digit instead of being gathered per record afterwards.
     bool resolved = false;
     {
-        if (bits_of(KW) > 0) {
-            PackSpec pa{};
-            pa.nf = 1;
-            pa.w[0] = KW;
-            pa.bits[0] = 1;
-            QT_CK(sort_by(pa, 1));
-        }
-        int ws[8], bs[8], nf = 0, used = 0, w = 0;
-        for (; w < KW && nf < 8; ++w) {
+        const int abits = bits_of(KW) > 0 ? 1 : 0;
+        int ws[8], bs[8], nf = 0, used = abits, w = 0;
+        for (; w < KW && nf + abits < 8; ++w) {
             const int b = bits_of(w);
             if (b == 0) continue;
             if (used + b > 64) break;
@@ -530,13 +557,16 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
                 pt.bits[f] = bs[f];
                 pt.off[f] = off;
             }
-            pt.nf = nf;
+            if (abits) {  // the action: least significant field
+                pt.w[nf] = KW;
+                pt.bits[nf] = 1;
+                pt.off[nf] = 0;
+            }
+            pt.nf = nf + abits;
             QT_CK(sort_by(pt, used));
-        }
-        if (nf > 0) {
             QT_CK(cudaMemsetAsync(io.spread + KW + 1, 0, sizeof(uint32_t), st));
             qt_msd_heads_kernel<<<grid, 256, 0, st>>>(
-                v, io.perm, reinterpret_cast<const unsigned long long*>(io.digit2), nrec, w_rest,
+                v, io.perm, reinterpret_cast<const unsigned long long*>(io.digit2), nrec, w_rest, abits,
                 io.spread + KW + 1, io.seg_head, io.key_head);
             uint32_t unresolved = 1;
             QT_CK(cudaMemcpyAsync(&unresolved, io.spread + KW + 1, 4, cudaMemcpyDeviceToHost, st));

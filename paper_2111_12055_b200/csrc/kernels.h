@@ -277,8 +277,11 @@ __global__ void qt_iota_kernel(uint32_t* p, size_t n);
 __global__ void qt_init_ids_kernel(const uint8_t* has, size_t m, uint32_t* ids, unsigned long long* count);
 __global__ void qt_both_kernel(const uint8_t* has, size_t m, uint32_t* flag);
 __global__ void qt_rowkey_kernel(const uint32_t* flag, const uint32_t* row, size_t m, uint32_t* rowkey);
+constexpr uint32_t QT_ENC_TAB = 1u << 16;  // log1pf(count) table: counts below this
+__global__ void qt_enc_table_kernel(float* tab);
 __global__ void qt_snapshot_kernel(const uint32_t* keys, const double* q, const uint32_t* rowkey,
-                                   size_t nrows, double rho, float* feat, double* tgt, int* bad_stage);
+                                   size_t nrows, double rho, const float* enc_tab, float* feat, double* tgt,
+                                   int* bad_stage);
 // fold pipeline entry points (launch wrappers live in k_qtable.cu)
 struct QtFoldIO {
     const uint32_t* tkeys; const uint32_t* init; size_t n_init;

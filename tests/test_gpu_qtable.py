@@ -172,12 +172,17 @@ def test_hot_key_long_segment(dev, ref):
     check_table(qt.export(), o, q_rtol=1e-12)
 
 
-@pytest.mark.parametrize("case", ["shared_prefix", "few_varying_words"])
+@pytest.mark.parametrize("case", ["shared_prefix", "few_varying_words", "bench_shape", "digit_edge",
+                                  "one_action"])
 def test_sort_paths_match_reference(dev, ref, case):
-    """The fold's MSD fast path (one sort by the top 64 varying key bits) and
-    its fallback to the full LSD sort when neighbours share those bits but
-    not the key (shared_prefix: keys differ only far down, in word 27), and
-    the case where every varying bit fits the first digit."""
+    """The fold's MSD fast path (one sort by the top varying key bits above
+    the action bit) and its fallback to the full LSD sort when neighbours
+    share those bits but not the key (shared_prefix: keys differ only far
+    down, in word 27); few_varying_words: every varying bit fits the digit;
+    bench_shape: the benchmark's keys (3 + 5 x 12 key bits + the action fill
+    the 64-bit digit exactly, words 6.. checked on the device); digit_edge:
+    two 32-bit words, only the first fits beside the action bit; one_action:
+    every tuple has action 1 (no action bit in the digit)."""
     rng = np.random.default_rng(17)
     n_distinct, n = 3000, 40_000
     base = np.zeros((n_distinct, 30), np.uint32)
@@ -186,11 +191,25 @@ def test_sort_paths_match_reference(dev, ref, case):
         prefix[:, 0] %= 8                                   # stage < 8 (encode_state)
         base[:, :27] = prefix[rng.integers(0, 40, n_distinct)]
         base[:, 27] = rng.integers(0, 1 << 20, n_distinct).astype(np.uint32)
-    else:
+    elif case == "few_varying_words":
         base[:, 0] = rng.integers(0, 8, n_distinct)
         base[:, 3] = rng.integers(0, 1 << 16, n_distinct).astype(np.uint32)
+    elif case == "bench_shape":
+        base[:] = rng.integers(0, 4096, (n_distinct, 30)).astype(np.uint32)
+        base[:, 0] %= 8
+        base[:, 0] |= 4                                     # word 0 spans exactly 3 bits
+        base[:, 1:6] |= 2048                                # words 1..5 exactly 12 bits
+    elif case == "digit_edge":
+        base[:, 0] = 5
+        base[:, 2] = rng.integers(0, 2**32, n_distinct, dtype=np.uint64).astype(np.uint32) | 2**31
+        base[:, 4] = rng.integers(0, 2**32, n_distinct, dtype=np.uint64).astype(np.uint32) | 2**31
+    else:  # one_action
+        base[:, 0] = rng.integers(0, 8, n_distinct)
+        base[:, 1:5] = rng.integers(0, 1 << 20, (n_distinct, 4)).astype(np.uint32)
     keys = base[rng.integers(0, n_distinct, n)]
     act = rng.integers(0, 2, n).astype(np.uint8)
+    if case == "one_action":
+        act[:] = 1
     rew = rng.random(n) * 0.4 + 0.8
     now = np.sort(rng.integers(0, 1000, n)).astype(np.uint64)
     o = ref.qtable_fold(keys, act, rew, now, alpha=0.3, omega=1.0, rho=0.1)
