@@ -161,7 +161,7 @@ struct gbxcu_qtable {
     DevBuf nkeys, nq, nt, ncnt, nhas;  // fold output (swapped in)
     DevBuf bkeys, bact, brew, bnow, init_ids, count;
     DevBuf perm, perm2, digit, digit2, seg_head, key_head, seg_scan, key_scan, seg_start, seg_key;
-    DevBuf spread, bad, temp;
+    DevBuf spread, bad, temp, rn;
     DevBuf flag, row, rowkey, sfeat, stgt, bad_stage;
     DevBuf enc_tab;  // qt_enc_table_kernel output, filled on the first snapshot
     bool enc_ready = false;
@@ -1035,7 +1035,7 @@ int gbxcu_qtable_create(gbxcu_ctx* c, double alpha, double omega, gbxcu_qtable**
                       &t->count, &t->perm, &t->perm2, &t->digit, &t->digit2, &t->seg_head,
                       &t->key_head, &t->seg_scan, &t->key_scan, &t->seg_start, &t->seg_key,
                       &t->spread, &t->bad, &t->temp, &t->flag, &t->row, &t->rowkey, &t->sfeat,
-                      &t->stgt, &t->bad_stage, &t->enc_tab})
+                      &t->stgt, &t->bad_stage, &t->enc_tab, &t->rn})
         b->astream = c->stream;
     *out = t;
     return GBXCU_OK;
@@ -1094,7 +1094,8 @@ int qtable_fold(gbxcu_qtable* t, const uint32_t* d_keys, const uint8_t* d_act, c
         RET(b->ensure(sizeof(uint32_t) * nrec));
     RET(t->digit.ensure(sizeof(unsigned long long) * nrec));   // packed 64-bit radix digits
     RET(t->digit2.ensure(sizeof(unsigned long long) * nrec));
-    RET(t->spread.ensure(sizeof(uint32_t) * 32));
+    RET(t->spread.ensure(sizeof(uint32_t) * 64));
+    RET(t->rn.ensure(16 * std::max<size_t>(n, 1)));
     RET(t->bad.ensure(16));
     const size_t tb = qt_temp_bytes(nrec);
     RET(t->temp.ensure(tb));
@@ -1124,6 +1125,7 @@ int qtable_fold(gbxcu_qtable* t, const uint32_t* d_keys, const uint8_t* d_act, c
     io.seg_start = t->seg_start.as<uint32_t>();
     io.seg_key = t->seg_key.as<uint32_t>();
     io.spread = t->spread.as<uint32_t>();
+    io.rn = t->rn.p;
     io.temp = t->temp.p;
     io.temp_bytes = tb;
     io.bad = t->bad.as<unsigned long long>();

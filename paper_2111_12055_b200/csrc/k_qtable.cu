@@ -69,8 +69,9 @@ __global__ void qt_init_ids_kernel(const uint8_t* __restrict__ has, size_t m, ui
     }
 }
 
-// Per key word: OR of (v ^ word of record 0) (which bits vary) over all records.
-__global__ void qt_word_spread_kernel(RecView v, size_t nrec, uint32_t* __restrict__ spread) {
+// Per key word: OR of (v ^ word of record 0) (which bits vary) over the
+// records 0, stride, 2 stride, ... (stride 1: all records).
+__global__ void qt_word_spread_kernel(RecView v, size_t nrec, size_t stride, uint32_t* __restrict__ spread) {
     __shared__ uint32_t acc[KW + 1];
     if (threadIdx.x <= KW) acc[threadIdx.x] = 0;
     __syncthreads();
@@ -79,11 +80,81 @@ __global__ void qt_word_spread_kernel(RecView v, size_t nrec, uint32_t* __restri
     uint32_t loc[KW + 1];
 #pragma unroll
     for (int w = 0; w <= KW; ++w) loc[w] = 0;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec; i += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t* k = v.key((uint32_t)i);
+    const size_t ns = (nrec + stride - 1) / stride;
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < ns; j += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)(j * stride);
+        const uint32_t* k = v.key(i);
 #pragma unroll
         for (int w = 0; w < KW; ++w) loc[w] |= k[w] ^ k0[w];
-        loc[KW] |= v.action((uint32_t)i) ^ a0;
+        loc[KW] |= v.action(i) ^ a0;
+    }
+#pragma unroll
+    for (int w = 0; w <= KW; ++w) {
+        uint32_t x = loc[w];
+        for (int o = 16; o > 0; o >>= 1) x |= __shfl_xor_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0 && x) atomicOr(&acc[w], x);
+    }
+    __syncthreads();
+    if (threadIdx.x <= KW && acc[threadIdx.x]) atomicOr(&spread[threadIdx.x], acc[threadIdx.x]);
+}
+
+// The fold's one sequential pass over the records (in record order): the MSD
+// digit under a packing chosen from a sample of the records (per word: mask
+// of its field, bit offset; index KW = the action), the exact word spread
+// (checked by the host against that packing — a bit the sample missed means
+// a re-run with the exact one), and the tuples' (reward, check-in) packed
+// into one 16-byte record so the fold's per-record gather is one load.
+struct WordPack {
+    uint32_t mask[KW + 1];
+    uint32_t off[KW + 1];
+};
+template <bool V2>
+__global__ void __launch_bounds__(256) qt_first_pass_kernel(RecView v, size_t nrec, WordPack wp,
+                                                            unsigned long long* __restrict__ digit,
+                                                            uint32_t* __restrict__ spread,
+                                                            const double* __restrict__ reward,
+                                                            const uint64_t* __restrict__ now,
+                                                            ulonglong2* __restrict__ rn) {
+    __shared__ uint32_t acc[KW + 1];
+    if (threadIdx.x <= KW) acc[threadIdx.x] = 0;
+    __syncthreads();
+    uint32_t k0[KW], loc[KW + 1];
+    {
+        const uint32_t* r0 = v.key(0);
+#pragma unroll
+        for (int w = 0; w < KW; ++w) k0[w] = __ldg(r0 + w);
+    }
+    const uint32_t a0 = v.action(0);
+#pragma unroll
+    for (int w = 0; w <= KW; ++w) loc[w] = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t* k = v.key((uint32_t)i);
+        uint32_t x[KW];
+        if (V2) {  // rows are 120 bytes: 8-byte aligned when the base is
+            const uint2* k2 = reinterpret_cast<const uint2*>(k);
+#pragma unroll
+            for (int q = 0; q < KW / 2; ++q) {
+                const uint2 t = __ldg(k2 + q);
+                x[2 * q] = t.x;
+                x[2 * q + 1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int w = 0; w < KW; ++w) x[w] = __ldg(k + w);
+        }
+        const uint32_t a = v.action((uint32_t)i);
+        unsigned long long d = (unsigned long long)(a & wp.mask[KW]) << wp.off[KW];
+#pragma unroll
+        for (int w = 0; w < KW; ++w) {
+            loc[w] |= x[w] ^ k0[w];
+            d |= (unsigned long long)(x[w] & wp.mask[w]) << wp.off[w];
+        }
+        loc[KW] |= a ^ a0;
+        digit[i] = d;
+        if (i >= v.n_init) {
+            const size_t b = i - v.n_init;
+            rn[b] = make_ulonglong2((unsigned long long)__double_as_longlong(reward[b]), now[b]);
+        }
     }
 #pragma unroll
     for (int w = 0; w <= KW; ++w) {
@@ -209,9 +280,8 @@ struct FoldArgs {
     const double* old_q;
     const uint64_t* old_t;
     const uint64_t* old_cnt;
-    // batch
-    const double* reward;
-    const uint64_t* now;
+    // batch: (reward bits, check-in) per tuple, packed by the first pass
+    const ulonglong2* rn;
     size_t limit;            // tuples with batch index >= limit are ignored (prefix re-fold)
     double alpha, omega;
     // new table
@@ -247,8 +317,9 @@ __global__ void qt_fold_kernel(FoldArgs f) {
             }
             const size_t b = r - f.v.n_init;
             if (b >= f.limit) break;  // batch order == record order within a segment
-            const double rw = f.reward[b];
-            const uint64_t now = f.now[b];
+            const ulonglong2 p = f.rn[b];
+            const double rw = __longlong_as_double((long long)p.x);
+            const uint64_t now = p.y;
             if (!have) {  // slot = QEntry{r, now, 1}
                 q = rw;
                 t = now;
@@ -508,22 +579,17 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
     const RecView v = rec_view(io);
     const int grid = num_sms * 4;
     qt_iota_kernel<<<grid, 256, 0, st>>>(io.perm, nrec);
-    QT_CK(cudaMemsetAsync(io.spread, 0, sizeof(uint32_t) * (KW + 1), st));
-    qt_word_spread_kernel<<<grid, 256, 0, st>>>(v, nrec, io.spread);
+    // spread[0..KW]: a sample's word spread; [KW + 1]: the unresolved flag;
+    // [KW + 2 .. 2 KW + 2]: the exact spread from the first pass
+    uint32_t* exact = io.spread + KW + 2;
+    QT_CK(cudaMemsetAsync(io.spread, 0, sizeof(uint32_t) * (2 * KW + 3), st));
+    const size_t stride = std::max<size_t>(1, nrec / 65536);
+    qt_word_spread_kernel<<<grid, 256, 0, st>>>(v, nrec, stride, io.spread);
     uint32_t spread[KW + 1];
     QT_CK(cudaMemcpyAsync(spread, io.spread, sizeof(spread), cudaMemcpyDeviceToHost, st));
     QT_CK(cudaStreamSynchronize(st));
     auto bits_of = [&](int w) { return spread[w] ? 32 - __builtin_clz(spread[w]) : 0; };
-    auto sort_by = [&](const PackSpec& ps, int bits) -> cudaError_t {
-        qt_gather_digit_kernel<<<grid, 256, 0, st>>>(v, io.perm, nrec, ps,
-                                                     reinterpret_cast<unsigned long long*>(io.digit));
-        QT_CK(cub::DeviceRadixSort::SortPairs(io.temp, io.temp_bytes,
-                                              reinterpret_cast<const unsigned long long*>(io.digit),
-                                              reinterpret_cast<unsigned long long*>(io.digit2), io.perm,
-                                              io.perm2, (int)nrec, 0, bits, st));
-        std::swap(io.perm, io.perm2);
-        return cudaSuccess;
-    };
+    const bool v2 = (reinterpret_cast<uintptr_t>(io.bkeys) & 7) == 0;
     // MSD fast path: one stable sort (records start in record order) by a
     // 64-bit digit packing the most significant varying key bits above the
     // action bit, i.e. by (top key bits, action, record). If no two
@@ -532,9 +598,12 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
     // order; otherwise fall back to the full LSD below. Typical keys differ
     // within their first varying words, so one sort replaces the action pass
     // plus ceil(varying bits / 64) key passes, and the action travels in the
-    // sorted digit instead of being gathered per record afterwards.
+    // sorted digit instead of being gathered per record afterwards. The
+    // packing comes from the sample; the first pass reports the exact spread,
+    // and a packing that missed a varying bit (of a packed word, of a word
+    // before the last packed one, or of the action) is re-run with it.
     bool resolved = false;
-    {
+    for (int attempt = 0; attempt < 2; ++attempt) {
         const int abits = bits_of(KW) > 0 ? 1 : 0;
         int ws[8], bs[8], nf = 0, used = abits, w = 0;
         for (; w < KW && nf + abits < 8; ++w) {
@@ -548,33 +617,49 @@ cudaError_t qt_sort_segment(QtFoldIO& io, size_t& nseg, size_t& nkeys, int num_s
         }
         int w_rest = w;
         while (w_rest < KW && bits_of(w_rest) == 0) ++w_rest;
-        if (nf > 0) {
-            PackSpec pt{};
+        WordPack wp{};
+        {
             int off = used;
             for (int f = 0; f < nf; ++f) {  // most significant word in the highest bits
                 off -= bs[f];
-                pt.w[f] = ws[f];
-                pt.bits[f] = bs[f];
-                pt.off[f] = off;
+                wp.mask[ws[f]] = bs[f] >= 32 ? 0xFFFFFFFFu : ((1u << bs[f]) - 1u);
+                wp.off[ws[f]] = (uint32_t)off;
             }
-            if (abits) {  // the action: least significant field
-                pt.w[nf] = KW;
-                pt.bits[nf] = 1;
-                pt.off[nf] = 0;
-            }
-            pt.nf = nf + abits;
-            QT_CK(sort_by(pt, used));
+            wp.mask[KW] = abits ? 1u : 0u;  // the action: least significant field
+        }
+        QT_CK(cudaMemsetAsync(exact, 0, sizeof(uint32_t) * (KW + 1), st));
+        if (v2)
+            qt_first_pass_kernel<true><<<grid, 256, 0, st>>>(v, nrec, wp, reinterpret_cast<unsigned long long*>(io.digit),
+                                                             exact, io.reward, io.now, static_cast<ulonglong2*>(io.rn));
+        else
+            qt_first_pass_kernel<false><<<grid, 256, 0, st>>>(v, nrec, wp, reinterpret_cast<unsigned long long*>(io.digit),
+                                                              exact, io.reward, io.now, static_cast<ulonglong2*>(io.rn));
+        if (nf > 0) {
+            QT_CK(cub::DeviceRadixSort::SortPairs(io.temp, io.temp_bytes,
+                                                  reinterpret_cast<const unsigned long long*>(io.digit),
+                                                  reinterpret_cast<unsigned long long*>(io.digit2), io.perm,
+                                                  io.perm2, (int)nrec, 0, used, st));
+            std::swap(io.perm, io.perm2);
             QT_CK(cudaMemsetAsync(io.spread + KW + 1, 0, sizeof(uint32_t), st));
             qt_msd_heads_kernel<<<grid, 256, 0, st>>>(
                 v, io.perm, reinterpret_cast<const unsigned long long*>(io.digit2), nrec, w_rest, abits,
                 io.spread + KW + 1, io.seg_head, io.key_head);
-            uint32_t unresolved = 1;
-            QT_CK(cudaMemcpyAsync(&unresolved, io.spread + KW + 1, 4, cudaMemcpyDeviceToHost, st));
-            QT_CK(cudaStreamSynchronize(st));
-            resolved = unresolved == 0;
         }
-        if (!resolved) qt_iota_kernel<<<grid, 256, 0, st>>>(io.perm, nrec);
+        uint32_t back[KW + 2];  // unresolved flag, exact spread
+        QT_CK(cudaMemcpyAsync(back, io.spread + KW + 1, sizeof(back), cudaMemcpyDeviceToHost, st));
+        QT_CK(cudaStreamSynchronize(st));
+        bool packing_ok = true;
+        for (int x = 0; x < KW; ++x)
+            if (x < w_rest && (back[1 + x] & ~wp.mask[x])) packing_ok = false;
+        if (back[1 + KW] && !abits) packing_ok = false;
+        for (int x = 0; x <= KW; ++x) spread[x] = back[1 + x];  // exact from here on
+        if (packing_ok) {
+            resolved = nf > 0 && back[0] == 0;
+            break;
+        }
+        qt_iota_kernel<<<grid, 256, 0, st>>>(io.perm, nrec);
     }
+    if (!resolved) qt_iota_kernel<<<grid, 256, 0, st>>>(io.perm, nrec);
     // LSD over the packed key: the action is the least significant field, then
     // words 29 .. 0; each pass packs up to 64 bits of varying fields (constant
     // words are skipped: they cannot reorder anything)
@@ -635,8 +720,7 @@ cudaError_t qt_fold(const QtFoldIO& io, size_t nseg, size_t nkeys, uint32_t* key
     f.old_q = io.old_q;
     f.old_t = io.old_t;
     f.old_cnt = io.old_cnt;
-    f.reward = io.reward;
-    f.now = io.now;
+    f.rn = reinterpret_cast<const ulonglong2*>(io.rn);
     f.limit = io.limit;
     f.alpha = io.alpha;
     f.omega = io.omega;

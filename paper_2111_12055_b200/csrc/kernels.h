@@ -291,7 +291,8 @@ struct QtFoldIO {
     double alpha, omega;
     // scratch [nrec] each
     uint32_t *perm, *perm2, *digit, *digit2, *seg_head, *key_head, *seg_scan, *key_scan, *seg_start, *seg_key;
-    uint32_t* spread;            // [31]
+    uint32_t* spread;            // [64]: sample spread, unresolved flag, exact spread
+    void* rn;                    // [n] 16-byte (reward bits, check-in) per tuple
     void* temp; size_t temp_bytes;
     unsigned long long* bad;     // [1]
 };

@@ -173,7 +173,7 @@ def test_hot_key_long_segment(dev, ref):
 
 
 @pytest.mark.parametrize("case", ["shared_prefix", "few_varying_words", "bench_shape", "digit_edge",
-                                  "one_action"])
+                                  "one_action", "rare_word", "rare_action"])
 def test_sort_paths_match_reference(dev, ref, case):
     """The fold's MSD fast path (one sort by the top varying key bits above
     the action bit) and its fallback to the full LSD sort when neighbours
@@ -182,9 +182,12 @@ def test_sort_paths_match_reference(dev, ref, case):
     bench_shape: the benchmark's keys (3 + 5 x 12 key bits + the action fill
     the 64-bit digit exactly, words 6.. checked on the device); digit_edge:
     two 32-bit words, only the first fits beside the action bit; one_action:
-    every tuple has action 1 (no action bit in the digit)."""
+    every tuple has action 1 (no action bit in the digit); rare_word /
+    rare_action: a bit that varies in one tuple only, off the sample the
+    packing is chosen from (200k tuples: every 3rd is sampled) — the first
+    pass's exact spread must trigger the re-run."""
     rng = np.random.default_rng(17)
-    n_distinct, n = 3000, 40_000
+    n_distinct, n = 3000, (200_000 if case.startswith("rare") else 40_000)
     base = np.zeros((n_distinct, 30), np.uint32)
     if case == "shared_prefix":
         prefix = rng.integers(0, 4096, (40, 27)).astype(np.uint32)
@@ -203,6 +206,9 @@ def test_sort_paths_match_reference(dev, ref, case):
         base[:, 0] = 5
         base[:, 2] = rng.integers(0, 2**32, n_distinct, dtype=np.uint64).astype(np.uint32) | 2**31
         base[:, 4] = rng.integers(0, 2**32, n_distinct, dtype=np.uint64).astype(np.uint32) | 2**31
+    elif case.startswith("rare"):
+        base[:, 0] = rng.integers(0, 8, n_distinct)
+        base[:, 4] = rng.integers(0, 1 << 12, n_distinct).astype(np.uint32)
     else:  # one_action
         base[:, 0] = rng.integers(0, 8, n_distinct)
         base[:, 1:5] = rng.integers(0, 1 << 20, (n_distinct, 4)).astype(np.uint32)
@@ -210,6 +216,12 @@ def test_sort_paths_match_reference(dev, ref, case):
     act = rng.integers(0, 2, n).astype(np.uint8)
     if case == "one_action":
         act[:] = 1
+    if case == "rare_word":
+        keys = keys.copy()
+        keys[100_000, 2] = 5                                # word 2 constant elsewhere; 100000 % 3 == 1
+    if case == "rare_action":
+        act[:] = 0
+        act[100_001] = 1
     rew = rng.random(n) * 0.4 + 0.8
     now = np.sort(rng.integers(0, 1000, n)).astype(np.uint64)
     o = ref.qtable_fold(keys, act, rew, now, alpha=0.3, omega=1.0, rho=0.1)
