@@ -217,29 +217,52 @@ static_assert(KW % 2 == 0, "keys are read as 8-byte pairs");
 // neighbours with equal key bits must have equal keys (words w_from.. beyond
 // the digit; none when w_from == KW), else the order is unresolved and the
 // caller falls back to the full LSD sort. With abits == 0 every record has
-// the same action.
+// the same action. Warp-wide over 32 consecutive positions: a row needed by
+// a tie is loaded once, by its own lane, and handed to the next lane by
+// shuffles (lane 0 loads its predecessor itself).
 __global__ void qt_msd_heads_kernel(RecView v, const uint32_t* __restrict__ perm,
                                     const unsigned long long* __restrict__ digit, size_t nrec,
                                     int w_from, int abits, unsigned int* __restrict__ unresolved,
                                     uint32_t* __restrict__ seg_head, uint32_t* __restrict__ key_head) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nrec;
-         i += (size_t)gridDim.x * blockDim.x) {
-        uint32_t kh = 1, sh = 1;
-        if (i > 0) {
-            const unsigned long long d = digit[i], d0 = digit[i - 1];
-            if ((d >> abits) == (d0 >> abits)) {
-                kh = 0;
-                if (w_from < KW) {
-                    if (!key_tail_equal(v.key(perm[i]), v.key(perm[i - 1]), w_from)) {
-                        atomicOr(unresolved, 1u);
-                        kh = 1;
-                    }
+    const int lane = threadIdx.x & 31;
+    const size_t step = (size_t)gridDim.x * blockDim.x;
+    for (size_t base = blockIdx.x * (size_t)blockDim.x + threadIdx.x - lane; base < nrec; base += step) {
+        const size_t i = base + lane;
+        const bool act = i < nrec;
+        const unsigned long long d = act ? digit[i] : 0ull;
+        const unsigned long long dp = (act && i > 0) ? digit[i - 1] : 0ull;
+        const bool tie = act && i > 0 && (d >> abits) == (dp >> abits);
+        uint32_t kh = tie ? 0u : 1u;
+        if (w_from < KW && __any_sync(0xffffffffu, tie)) {
+            bool tie_next = __shfl_down_sync(0xffffffffu, tie, 1);
+            if (lane == 31) tie_next = i + 1 < nrec && (digit[i + 1] >> abits) == (d >> abits);
+            const uint2* own = act ? reinterpret_cast<const uint2*>(v.key(perm[i])) : nullptr;
+            const bool need = tie || tie_next;
+            bool same = true;
+            if (lane == 0 && tie) same = key_tail_equal(v.key(perm[i]), v.key(perm[i - 1]), w_from);
+            uint2 xs[KW / 2];  // all loads in flight before the first shuffle
+#pragma unroll
+            for (int q = 0; q < KW / 2; ++q)
+                xs[q] = need && 2 * q + 1 >= w_from ? __ldg(own + q) : make_uint2(0u, 0u);
+#pragma unroll
+            for (int q = 0; q < KW / 2; ++q) {
+                const uint2 x = xs[q];
+                const uint32_t yx = __shfl_up_sync(0xffffffffu, x.x, 1);
+                const uint32_t yy = __shfl_up_sync(0xffffffffu, x.y, 1);
+                if (lane > 0) {
+                    if (2 * q >= w_from) same &= x.x == yx;
+                    if (2 * q + 1 >= w_from) same &= x.y == yy;
                 }
             }
-            sh = kh | (uint32_t)((d ^ d0) & (unsigned long long)abits);
+            if (tie && !same) {
+                atomicOr(unresolved, 1u);
+                kh = 1;
+            }
         }
-        seg_head[i] = sh;
-        key_head[i] = kh;
+        if (act) {
+            seg_head[i] = kh | (uint32_t)((d ^ dp) & (unsigned long long)abits);
+            key_head[i] = kh;
+        }
     }
 }
 
