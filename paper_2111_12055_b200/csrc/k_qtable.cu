@@ -374,16 +374,29 @@ __global__ void qt_fold_kernel(FoldArgs f) {
 }
 
 // New key rows: thread per (key, word), so a warp reads and writes whole
-// 120-byte rows (a thread-per-key copy touches 30 sectors per instruction).
+// 120-byte rows (a thread-per-key copy touches 30 sectors per instruction);
+// four independent items per thread per iteration keep enough random row
+// reads in flight.
 __global__ void qt_copy_keys_kernel(RecView v, const uint32_t* __restrict__ src_rec, size_t nkeys,
                                     uint32_t* __restrict__ keys) {
+    constexpr int U = 4;
     const size_t total = nkeys * KW;
-    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < total;
-         x += (size_t)gridDim.x * blockDim.x) {
-        const size_t kid = x / KW;
-        const int w = (int)(x - kid * KW);
-        const uint32_t r = src_rec[kid];
-        if (r != 0xFFFFFFFFu) keys[x] = v.key(r)[w];
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t x0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x0 < total; x0 += U * stride) {
+        uint32_t r[U], val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const size_t x = x0 + u * stride;
+            r[u] = x < total ? __ldg(src_rec + x / KW) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const size_t x = x0 + u * stride;
+            if (r[u] != 0xFFFFFFFFu) val[u] = __ldg(v.key(r[u]) + (x - (x / KW) * KW));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (r[u] != 0xFFFFFFFFu) keys[x0 + u * stride] = val[u];
     }
 }
 
